@@ -1,0 +1,123 @@
+"""Pins for the oracle's s-step CG outer iteration (restart form)."""
+import math
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle as orc
+
+
+def diag_csr(vals):
+    n = len(vals)
+    return orc.csr(np.arange(n + 1), np.arange(n), np.asarray(vals, float))
+
+
+def test_worked_example_one_outer(golden):
+    g = golden["restart_sstep_diag13"]
+    A = diag_csr(g["A_diag"])
+    b = np.array(g["b"])
+    x1, tr = orc.sstep_cg(A, 1.0, 3.0, 2, 1, b, rtol=0.0, max_outer=1, D=np.ones(2))
+    assert np.array_equal(x1, g["x1_nu1"])
+    assert np.array_equal(b - A.n * 0 - orc.apply(A, x1), g["r1_nu1"])
+    assert np.array_equal(tr.ghat[0], [[4, 2], [2, 4]]) and np.array_equal(tr.c[0], [2, 0])
+    assert np.array_equal(tr.alpha_t[0], [1.0, -0.5]) and np.array_equal(tr.alpha[0], [0.5, -0.25])
+    x2, _ = orc.sstep_cg(A, 1.0, 3.0, 2, 2, b, rtol=0.0, max_outer=1, D=np.ones(2))
+    assert np.array_equal(x2, g["x1_nu2"])
+
+
+@pytest.mark.parametrize("nu,k", [(1, 1), (1, 3), (2, 2), (3, 4)])
+def test_worked_example_closed_form(golden, nu, k):
+    """r_k = 4^{-nu k} [1,1],  x_k = (1 - 4^{-nu k}) [1, 1/3]."""
+    g = golden["restart_sstep_diag13"]
+    A = diag_csr(g["A_diag"])
+    b = np.array(g["b"])
+    x, tr = orc.sstep_cg(A, 1.0, 3.0, 2, nu, b, rtol=0.0, max_outer=k, D=np.ones(2))
+    f = 4.0 ** (-nu * k)
+    assert np.allclose(x, (1 - f) * np.array(g["x_limit"]), rtol=1e-15, atol=1e-16)
+    assert np.allclose(b - orc.apply(A, x), f * np.ones(2), rtol=1e-12, atol=1e-17)
+    assert tr.relres[k] == pytest.approx(f, rel=1e-12)
+
+
+def test_exact_in_one_outer_with_s_modes():
+    """If r has exactly s eigen-modes, an (effectively) exact Gram solve gives
+    x_1 = A^{-1} b in one outer iteration (Krylov space contains A^{-1} b)."""
+    dims = (9, 8, 7)
+    A = orc.stencil(orc.KIND_7PT, *dims)
+    s = 4
+    modes = [(1, 1, 1), (2, 3, 1), (5, 2, 4), (8, 7, 6)]
+    coef = [1.0, -0.5, 0.25, 0.8]
+    b = sum(c * inputs.sine_mode(*dims, *m) for c, m in zip(coef, modes))
+    xstar = sum(c / inputs.sine_mode_eig("7pt", dims, m) * inputs.sine_mode(*dims, *m) for c, m in zip(coef, modes))
+    lmin, lmax = inputs.analytic_bounds("7pt", *dims)
+    x, tr = orc.sstep_cg(A, lmin, lmax, s, 4000, b, rtol=0.0, max_outer=1)
+    assert np.linalg.norm(x - xstar) <= 1e-8 * np.linalg.norm(xstar)
+
+
+@pytest.mark.parametrize("nu", [1, 3, 20])
+def test_energy_identity(nu):
+    """||e_k||_A^2 - ||e_{k+1}||_A^2 = 2 a~^T c~ - a~^T G a~ > 0 (each unit-
+    diagonal GS coordinate step is an exact line minimisation of the energy)."""
+    dims = (10, 9, 1)
+    A = orc.stencil(orc.KIND_5PT2D, *dims)
+    b = inputs.rhs_uniform(10, 9, 1, seed=3)
+    lmin, lmax = inputs.analytic_bounds("5pt", 10, 9)
+    K = 6
+    xs = [np.zeros(A.n)]
+    for k in range(1, K + 1):
+        x, tr = orc.sstep_cg(A, lmin, lmax, 4, nu, b, rtol=0.0, max_outer=k)
+        xs.append(x)
+    f = [-0.5 * x @ (b + (b - orc.apply(A, x))) for x in xs]     # f(x) = 1/2 x'Ax - b'x
+    for k in range(K):
+        drop = 2 * (f[k] - f[k + 1])
+        assert drop > 0
+        assert abs(drop - tr.energy[k]) <= 1e-12 * max(1.0, abs(drop)) + 1e-13 * abs(f[0])
+
+
+def test_cfg1_matches_dense_direct_solve():
+    """BASELINE cfg 1 (2D 5-pt 64x64, s=8, nu=20, rtol 1e-8) vs a dense direct
+    solve: ||x - x*|| / ||x*|| <= kappa(M^-1 A) * rtol and the true residual
+    ||b - Ax|| <= rtol ||b|| (1 + 1e-6)."""
+    nx = ny = 64
+    A = orc.stencil(orc.KIND_5PT2D, nx, ny, 1)
+    b = inputs.rhs_uniform(nx, ny, 1, seed=42)
+    lmin, lmax = inputs.analytic_bounds("5pt", nx, ny)
+    x, tr = orc.sstep_cg(A, lmin, lmax, 8, 20, b, rtol=1e-8, max_outer=1000)
+    assert tr.converged and not tr.breakdown
+    T = 2 * np.eye(nx) - np.eye(nx, k=1) - np.eye(nx, k=-1)
+    M = np.kron(np.eye(ny), T) + np.kron(T, np.eye(nx))
+    xstar = np.linalg.solve(M, b)
+    kappa = lmax / lmin
+    assert np.linalg.norm(x - xstar) <= kappa * 1e-8 * np.linalg.norm(xstar)
+    assert np.linalg.norm(b - M @ x) <= 1e-8 * np.linalg.norm(b) * (1 + 1e-6)
+    # recurrence residual vs true residual
+    assert abs(tr.relres[tr.outer] - np.linalg.norm(b - M @ x) / np.linalg.norm(b)) < 1e-12
+    assert 40 <= tr.outer <= 300
+
+
+def test_zero_rhs_converges_immediately():
+    A = orc.stencil(orc.KIND_7PT, 4, 4, 4)
+    x, tr = orc.sstep_cg(A, 0.1, 1.9, 4, 5, np.zeros(64), rtol=1e-8, max_outer=10)
+    assert tr.converged and tr.outer == 0 and np.all(x == 0)
+
+
+def test_nonzero_x0_restart_equivalence():
+    """Resuming from x_k reproduces the uninterrupted run (restart form is
+    memoryless except for x), up to recomputing r = b - A x_k."""
+    dims = (8, 8, 8)
+    A = orc.stencil(orc.KIND_7PT, *dims)
+    b = inputs.rhs_uniform(*dims, seed=9)
+    lmin, lmax = inputs.analytic_bounds("7pt", *dims)
+    x6, _ = orc.sstep_cg(A, lmin, lmax, 5, 10, b, rtol=0.0, max_outer=6)
+    x3, _ = orc.sstep_cg(A, lmin, lmax, 5, 10, b, rtol=0.0, max_outer=3)
+    x6b, _ = orc.sstep_cg(A, lmin, lmax, 5, 10, b, x0=x3, rtol=0.0, max_outer=3)
+    assert np.linalg.norm(x6b - x6) <= 1e-10 * np.linalg.norm(x6)
+
+
+def test_classical_pcg_reference():
+    dims = (16, 16, 1)
+    A = orc.stencil(orc.KIND_5PT2D, *dims)
+    b = inputs.rhs_uniform(*dims, seed=1)
+    x, it = orc.pcg(A, b, rtol=1e-10)
+    assert np.linalg.norm(b - orc.apply(A, x)) <= 1e-10 * np.linalg.norm(b) * 1.0001
+    assert it <= 16 * 16
