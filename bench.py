@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark: Chebyshev s-step PCG outer iterations with nu-sweep FGS Gram
+solves on B200 (BASELINE.json metric: time per outer iteration and GDOF/s at
+1/2/4/8 GPUs; fraction of the HBM roofline).
+
+Workload (BASELINE.json configs[4], "cfg5"): 3D 7-point Poisson, 448^3
+unknowns per GPU stacked in z (weak scaling, ~90M unknowns per GPU), FP64,
+Jacobi, b ~ U[-1,1] (SplitMix64 on the global index, seed 42), x0 = 0,
+analytic global spectral bounds, s = 16, nu = 30.  One "step" = one outer
+iteration: s basis SpMVs (+halo exchange), the fused Gram pass + the single
+allreduce, the FGS solve and the update.  The working set (P and W: 23 GB per
+GPU) is ~180x the 126 MB L2, so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "s-step CG time/outer-iter & GDOF/s at 1/2/4/8 B200; % of HBM peak"
+UNIT = "GDOF/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=448, help="grid edge per GPU (cfg5: 448)")
+    ap.add_argument("--s", type=int, default=16)
+    ap.add_argument("--nu", type=int, default=30)
+    ap.add_argument("--cpu-planes", type=int, default=16, help="z-planes of the oracle's CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(a, nranks):
+    n = a.n
+    return {"workload": f"cfg5: 3D 7-point Poisson {n}^3 per GPU (z-slab weak scaling), FP64, Jacobi, "
+                        f"analytic bounds, s={a.s}, nu={a.nu}, x0=0, b~U[-1,1] seed 42",
+            "nx": n, "ny": n, "nz_per_gpu": n, "nz_global": n * nranks, "s": a.s, "nu": a.nu,
+            "n_global": n * n * n * nranks, "parallelism": f"z-slab x{nranks}",
+            "l2": "no flush: per-GPU working set 2*s vectors (%.1f GB) >> 126 MB L2" % (2 * a.s * n ** 3 * 8 / 1e9)}
+
+
+# --------------------------------------------------------------------------
+# CPU oracle (the reported baseline / --impl reference arm)
+def oracle_sample(a, steps, warmup):
+    """Time `steps` outer iterations of the CPU oracle on a bounded sample:
+    the first `cpu_planes` z-planes of the same n x n grid (Dirichlet box of
+    n x n x cpu_planes, same s, nu, seed; bounds of that box).  Returns
+    (GDOF/s, seconds per step, description)."""
+    import inputs
+    import oracle as orc
+    n, zs = a.n, a.cpu_planes
+    A = orc.stencil(orc.KIND_7PT, n, n, zs)
+    b = inputs.rhs_uniform(n, n, zs, seed=42)
+    lmin, lmax = inputs.analytic_bounds("7pt", n, n, zs)
+    t0 = time.perf_counter()
+    orc.sstep_cg(A, lmin, lmax, a.s, a.nu, b, rtol=0.0, max_outer=warmup)
+    t1 = time.perf_counter()
+    orc.sstep_cg(A, lmin, lmax, a.s, a.nu, b, rtol=0.0, max_outer=warmup + steps)
+    t2 = time.perf_counter()
+    per = ((t2 - t1) - (t1 - t0)) / steps
+    npts = n * n * zs
+    desc = (f"oracle/sscg_oracle.c (gcc -O2 -fopenmp, FP64) on a {n}x{n}x{zs} sample "
+            f"({npts} unknowns), {steps} outer iterations timed as t(max_outer={warmup + steps}) - "
+            f"t(max_outer={warmup})")
+    return npts / per / 1e9, per, desc
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    value, per, desc = oracle_sample(a, a.steps, a.warmup)
+    cfg = workload(a, a.gpus)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfgkey):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    capture of this workload (profiles/*ncu_summary.json), else None."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_summary.json"))):
+        try:
+            d = json.load(open(f))
+            if d.get("config") == cfgkey and "k1_dram_bytes_per_launch" in d:
+                best = d
+        except Exception:
+            pass
+    return None if best is None else best["k1_dram_bytes_per_launch"]
+
+
+def run_ours(a):
+    import numpy as np
+    import torch
+
+    import inputs
+    import paper_2512_09642_b200 as sscg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, s, nu = a.n, a.s, a.nu
+    nz = n * world
+    z0, nzl = sscg.partition(nz, world, 1, rank)
+    lmin, lmax = inputs.analytic_bounds("7pt", n, n, nz)
+    b_host = torch.from_numpy(inputs.rhs_uniform(n, n, nz, seed=42, z0=z0, nzl=nzl)).pin_memory()
+    b = b_host.cuda()
+    nid = None
+    if world > 1:
+        obj = [sscg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    S = sscg.Solver(sscg.Stencil("7pt", n, n, nz), lmin, lmax, s, nu, rank=rank, nranks=world, nccl_id=nid)
+    n_local, n_global = S.n_local, n * n * nz
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # r_0 = b and the first basis/Gram (untimed), then W warm-up steps
+    x = S.solve(b, rtol=0.0, max_outer=0)
+    S.iterate(x, a.warmup)
+    # timed region: exactly K outer iterations, device-timed inside the library
+    barrier()
+    S.set_profiling(True)
+    with Clocks(local) as clk:
+        S.iterate(x, a.steps)
+        barrier()
+    st = S.stats()
+    prof = S.profile()
+    S.set_profiling(False)
+    ms = max_over_ranks(st.ms_total)
+    value = n_global * a.steps / (ms / 1e3) / 1e9
+    launches = st.kernel_launches
+
+    # roofline of the dominant kernel (K1: basis step) and the others
+    peak, peak_src = peaks()
+    vec = 8.0 * n_local
+    bytes_per_outer = {"basis": (4 * s - 3) * vec, "gram": 2 * s * vec, "update": (2 * s + 3) * vec}
+    kern = {}
+    for k, byt in bytes_per_outer.items():
+        t_ms, cnt = prof[k]
+        per_launch = byt * a.steps / max(cnt, 1)
+        gbs = per_launch / (t_ms / max(cnt, 1) / 1e3) / 1e9 if t_ms > 0 else None
+        kern[k] = {"launches": cnt, "ms_per_launch": t_ms / max(cnt, 1), "bytes_per_launch": per_launch,
+                   "achieved_gbs": gbs, "frac": (gbs / peak) if gbs else None,
+                   "share_of_step": t_ms / (st.ms_total) if st.ms_total else None}
+    for k in ("fgs", "allreduce", "halo"):
+        t_ms, cnt = prof[k]
+        kern[k] = {"launches": cnt, "us_per_launch": 1e3 * t_ms / max(cnt, 1),
+                   "share_of_step": t_ms / st.ms_total if st.ms_total else None}
+    k1 = kern["basis"]
+    cfg = workload(a, world)
+    roof = {"bound": "hbm", "kernel": "K1 k1_stencil<7pt> (SpMV + Jacobi + Chebyshev recurrence)",
+            "achieved": k1["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": k1["frac"],
+            "traffic": ncu_traffic("cfg5-%d-s%d" % (n, s)), "peak_source": peak_src,
+            "bytes_rule": "(4s-3) FP64 vectors per outer / s launches (SURVEY 8(d))",
+            "path_bytes_per_step": 64.0 * s * n_local,
+            "path_achieved_gbs": 64.0 * s * n_local / (st.ms_total / a.steps / 1e3) / 1e9,
+            "path_frac": 64.0 * s * n_local / (st.ms_total / a.steps / 1e3) / 1e9 / peak}
+    # end-to-end: host b in, host x out, through the C ABI (sscg_solve_host)
+    e2e = None
+    if not a.no_e2e:
+        xh = torch.empty(n_local, dtype=torch.float64).pin_memory()
+        bh = b_host.numpy()
+        barrier()
+        t0 = time.perf_counter()
+        S.solve_host(bh, xh.numpy(), rtol=0.0, max_outer=a.steps)
+        t1 = time.perf_counter()
+        te = max_over_ranks(t1 - t0)
+        e2e = {"value": n_global * a.steps / te / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 8.0 * n_local / a.steps, "d2h_bytes_per_step": 8.0 * n_local / a.steps,
+               "note": f"one sscg_solve_host call: b H2D, {a.steps} outer iterations (+ final stopping-test "
+                       "basis/Gram), x D2H; host wall clock, max over ranks"}
+    S.close()
+    if dist:
+        dist.barrier()
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        v, per, desc = oracle_sample(a, 1, 1)
+        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg, "roofline": roof,
+            "kernels": kern, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "impl": "ours"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

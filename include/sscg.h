@@ -1,0 +1,223 @@
+/*
+ * sscg.h -- C ABI of the B200-native Chebyshev-basis s-step PCG with
+ * nu-sweep Forward Gauss-Seidel (FGS) Gram solves.
+ *
+ * Method: Thomas & D'Ambra, "Inexact Gauss-Seidel Coarse Solvers for AMG and
+ * s-step CG", arxiv 2512.09642.  One outer iteration k computes
+ *   1. the Chebyshev basis P = [p_0..p_{s-1}] of K_s(M^{-1}A, r_k)
+ *        p_0 = r_k, p_1 = theta (M^{-1}A - sigma I) p_0,
+ *        p_{j+1} = 2 theta (M^{-1}A - sigma I) p_j - p_{j-1}
+ *      with theta = 2/(lmax-lmin), sigma = (lmax+lmin)/2,
+ *      together with W = A P;
+ *   2. Ghat = P^T A P and c = P^T r_k in one pass, summed over all ranks with
+ *      exactly one allreduce of the s x (s+1) block;
+ *   3. the Ruhe scaling d_i = Ghat_ii^{-1/2}, G = S Ghat S = I + L + L^T,
+ *      c~ = S c, and nu FGS sweeps (I + L) a^(l+1) = c~ - L^T a^(l), a^(0) = 0
+ *                                                          (PAPER.md:47-55);
+ *   4. alpha = S a~;  x += P alpha;  r -= W alpha.
+ * Restart form, recurrence residual, stopping test ||r_k|| <= rtol ||r_0|| with
+ * ||r_k||^2 = c_0 taken from the Gram block (readings R3-R5).
+ *
+ * Data decomposition: the nx*ny*nz grid is split in z into
+ * nranks*slabs_per_rank slabs (sscg_partition); each process owns a
+ * contiguous run of slabs_per_rank slabs.  Halo planes move by NCCL
+ * send/recv between processes and by device copies between the slabs of one
+ * process; the Gram block is reduced over local slabs in a fixed order and
+ * then by one ncclAllReduce.
+ *
+ * Conventions
+ *  - All double* / int* arguments documented "device" are CUDA device
+ *    pointers valid on the calling process's current device; "host" pointers
+ *    are ordinary host memory.
+ *  - Grid functions (b, x, diag_M, face coefficients) are process-local,
+ *    dense, x fastest: index (x, y, zl) -> x + nx*(y + ny*zl), zl in
+ *    [0, nz_proc).  CSR vectors are indexed by row.
+ *  - Ownership: the caller owns b, x, diag_M and all operator arrays and keeps
+ *    them valid for the lifetime of the context; the library never frees
+ *    them.  The library owns its workspace (basis, Gram buffers, history,
+ *    NCCL communicator) and releases it in sscg_destroy.
+ *  - Every call returns an sscg_status; on failure sscg_last_error() returns
+ *    a thread-local message.  No exception or abort crosses the ABI.
+ *  - A context is not re-entrant; use one per process and device.
+ */
+#ifndef SSCG_H
+#define SSCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SSCG_API __attribute__((visibility("default")))
+#else
+#define SSCG_API
+#endif
+
+typedef struct sscg_ctx sscg_ctx;
+
+typedef enum {
+    SSCG_OK = 0,
+    SSCG_ERR_INVALID = 1,      /* argument out of range / inconsistent sizes        */
+    SSCG_ERR_CUDA = 2,         /* a CUDA runtime call failed (incl. no device)      */
+    SSCG_ERR_NCCL = 3,         /* an NCCL call failed                               */
+    SSCG_ERR_OOM = 4,          /* device allocation failed                          */
+    SSCG_ERR_BREAKDOWN = 5,    /* some Ghat_ii <= 0 or non-finite (R19); x = best so far */
+    SSCG_ERR_NONFINITE = 6,    /* ||r_k|| became NaN/Inf                            */
+    SSCG_ERR_UNSUPPORTED = 7   /* valid request this build does not implement       */
+} sscg_status;
+
+typedef enum {
+    SSCG_OP_STENCIL5_2D = 0,   /* 2D 5-point: 4 / -1, nz must be 1 (BASELINE cfg 1) */
+    SSCG_OP_STENCIL7 = 1,      /* 3D 7-point: 6 / -1 (cfg 2, 5)                     */
+    SSCG_OP_STENCIL27 = 2,     /* 3D 27-point: 26 / -1 for all 26 neighbours (cfg 3) */
+    SSCG_OP_VARCOEF7 = 3,      /* 3D variable-coefficient 7-point FV (cfg 4; R12)   */
+    SSCG_OP_CSR = 4            /* general symmetric CSR, single slab only           */
+} sscg_op_kind;
+
+/* Operator A ("sparse SPD A"; stencils of PAPER.md:308 and the
+ * BASELINE configs).  Homogeneous Dirichlet: values outside the global grid
+ * are zero.  For VARCOEF7, the face arrays cover this process's planes
+ * [z0, z0+nz_proc) (device, row-major):
+ *   kx[(zl*ny + y)*(nx+1) + f]   face between x=f-1 and x=f, f in [0, nx]
+ *   ky[(zl*(ny+1) + f)*nx + x]   face between y=f-1 and y=f, f in [0, ny]
+ *   kz[(fl*ny + y)*nx + x]       face between global planes z0+fl-1 and z0+fl,
+ *                                fl in [0, nz_proc]
+ * A_ii = sum of the six faces of cell i, A_i,nbr = -k_face.
+ * For CSR: n rows, int64 rowptr[n+1], int32 colind[nnz], double val[nnz]
+ * (device), both triangles stored. */
+typedef struct {
+    int32_t kind;              /* sscg_op_kind                                      */
+    int64_t nx, ny, nz;        /* GLOBAL interior grid; nz = 1 for STENCIL5_2D      */
+    const double *kx, *ky, *kz;/* VARCOEF7 faces (device), else NULL                */
+    int64_t n;                 /* CSR rows, else 0                                  */
+    const int64_t *rowptr;     /* CSR (device)                                      */
+    const int32_t *colind;     /* CSR (device)                                      */
+    const double *val;         /* CSR (device)                                      */
+} sscg_operator;
+
+/* Process group.  nranks == 1 needs no NCCL.  For nranks > 1, every rank
+ * passes the same 128-byte ncclUniqueId (host) obtained by rank 0 with
+ * sscg_nccl_unique_id and broadcast by the caller (e.g. torch.distributed).
+ * slabs_per_rank > 1 splits this process's planes further into that many
+ * slabs on the same GPU (in-process halo copies; used to test the
+ * decomposition on one device). */
+typedef struct {
+    int32_t rank, nranks;
+    int32_t slabs_per_rank;    /* >= 1                                              */
+    const void *nccl_id;       /* host, 128 bytes; ignored when nranks == 1         */
+} sscg_comm;
+
+/* Planes [z0, z0+nzl) owned by process `rank` when nz planes are split into
+ * nranks*slabs_per_rank slabs, slab g = [floor(g nz/S), floor((g+1) nz/S)).
+ * Pure host arithmetic; needs no GPU.  Returns SSCG_ERR_INVALID if some slab
+ * would be empty. */
+SSCG_API sscg_status sscg_partition(int64_t nz, int32_t nranks, int32_t slabs_per_rank, int32_t rank,
+                           int64_t *z0, int64_t *nzl);
+
+/* Fill `out` (host, 128 bytes) with a fresh ncclUniqueId.  Needs no GPU. */
+SSCG_API sscg_status sscg_nccl_unique_id(void *out);
+
+/* Create a solver context (PAPER.md:33-55 fixes theta, sigma, s, nu).
+ *   A          operator (arrays device, see sscg_operator)
+ *   diag_M     device, process-local grid function: the Jacobi diagonal M;
+ *              NULL => M = diag(A) (BASELINE configs).  Copied at setup.
+ *   lambda_min, lambda_max  bounds of the spectrum of M^{-1}A, 0 < lmin < lmax
+ *              (PAPER.md:34); theta = 2/(lmax-lmin), sigma = (lmax+lmin)/2.
+ *   s          basis size, 1 <= s <= 64;   nu  FGS sweeps, nu >= 1.
+ *   comm       NULL => single process, one slab.
+ *   stream     cudaStream_t to run on (NULL => the library creates one).
+ * Allocates the basis P and W = AP (2 s vectors with one halo plane each
+ * side), Gram partials and history; zeroes the global-boundary halos.
+ * Errors: SSCG_ERR_INVALID for out-of-range arguments (incl. a slab with no
+ * planes, STENCIL5_2D with nz != 1, CSR with more than one slab),
+ * SSCG_ERR_OOM, SSCG_ERR_CUDA, SSCG_ERR_NCCL.  *out is NULL on failure. */
+SSCG_API sscg_status sscg_setup(const sscg_operator *A, const double *diag_M, double lambda_min,
+                       double lambda_max, int32_t s, int32_t nu, const sscg_comm *comm,
+                       void *stream, sscg_ctx **out);
+
+#define SSCG_SOLVE_X0_ZERO 1u  /* flag: treat x as 0 on entry (r_0 = b, no SpMV)   */
+
+/* Solve A x = b by restart s-step CG until
+ * ||r_k|| <= rtol ||r_0|| or max_outer updates.  b, x: device, process-local.
+ * x holds x_0 on entry (ignored with SSCG_SOLVE_X0_ZERO) and x_k on return.
+ * Synchronous on return.  rtol = 0 runs exactly max_outer outer iterations.
+ * Non-convergence is not an error (SSCG_OK, stats.converged = 0).
+ * Breakdown returns SSCG_ERR_BREAKDOWN with the last good x. */
+SSCG_API sscg_status sscg_solve(sscg_ctx *ctx, const double *b, double *x, double rtol, int32_t max_outer,
+                       uint32_t flags);
+
+/* Same as sscg_solve with HOST b and x (process-local, pageable or pinned):
+ * b is copied to the device, x is copied in (unless X0_ZERO) and back out.
+ * The copies are part of the call (end-to-end path). */
+SSCG_API sscg_status sscg_solve_host(sscg_ctx *ctx, const double *b_host, double *x_host, double rtol,
+                            int32_t max_outer, uint32_t flags);
+
+/* Run exactly `nsteps` further outer iterations (basis, Gram + allreduce,
+ * FGS, update: every step of PAPER.md:31/33-55) from the state the last
+ * sscg_solve left (r_k inside the context, x_k in `x`), with the stopping
+ * test disabled and no host round trip between iterations.  x: device, the
+ * vector the last sscg_solve returned.  Used to time a fixed number of outer
+ * iterations (BASELINE cfg 3-5).  SSCG_ERR_INVALID if no solve preceded. */
+SSCG_API sscg_status sscg_iterate(sscg_ctx *ctx, double *x, int32_t nsteps);
+
+/* Per-kernel device time: with profiling on, every launch group is bracketed
+ * by CUDA events on the solver stream and accumulated per category. */
+enum { SSCG_PROF_BASIS = 0, SSCG_PROF_GRAM = 1, SSCG_PROF_ALLREDUCE = 2, SSCG_PROF_FGS = 3,
+       SSCG_PROF_UPDATE = 4, SSCG_PROF_HALO = 5, SSCG_PROF_N = 6 };
+typedef struct {
+    double ms[SSCG_PROF_N];          /* accumulated device milliseconds           */
+    int64_t launches[SSCG_PROF_N];   /* events pairs (= launches, or NCCL groups)  */
+} sscg_profile_t;
+SSCG_API sscg_status sscg_set_profiling(sscg_ctx *ctx, int32_t on);   /* also resets */
+SSCG_API sscg_status sscg_profile(sscg_ctx *ctx, sscg_profile_t *out); /* synchronises */
+
+typedef struct {
+    int32_t outer_iterations;  /* updates applied                                   */
+    int32_t converged;         /* ||r_k|| <= rtol ||r_0|| reached                    */
+    int32_t breakdown;         /* Ghat_ii <= 0 or non-finite                         */
+    int32_t nonfinite;         /* ||r_k|| not finite                                 */
+    double r0_norm;            /* ||r_0||_2                                          */
+    double relres_final;       /* ||r_k|| / ||r_0|| at exit (recurrence residual)    */
+    int32_t history_len;       /* entries in relres_history (outer_iterations + 1)  */
+    const double *relres_history; /* host, owned by ctx, valid until next solve     */
+    const double *delta_history;  /* host: ||c~ - G a~||/||c~|| per update */
+    double ms_total;           /* device time of the last solve (CUDA events)        */
+    int64_t kernel_launches;   /* library kernels launched by the last solve        */
+    int64_t allreduces;        /* NCCL allreduces issued by the last solve          */
+} sscg_stats_t;
+
+SSCG_API sscg_status sscg_stats(const sscg_ctx *ctx, sscg_stats_t *out);
+
+/* Parity hooks: copy internal state of the LAST solve to host memory.
+ *   SSCG_INSPECT_P, _W     column `index` of P / W = AP of the last basis built
+ *                          (process-local grid layout, nx*ny*nz_proc doubles)
+ *   SSCG_INSPECT_GRAM      outer `index`: [Ghat (s*s, row-major, mirrored) | c (s)]
+ *                          after the allreduce
+ *   SSCG_INSPECT_D, _ALPHA_T, _ALPHA   outer `index`: s doubles
+ *   SSCG_INSPECT_DELTA     outer `index`: 1 double
+ * `capacity` is the byte size of host_out; too small => SSCG_ERR_INVALID.
+ * History entries exist for outer indices 0..max_outer of the last solve. */
+enum {
+    SSCG_INSPECT_P = 0, SSCG_INSPECT_W = 1, SSCG_INSPECT_GRAM = 2, SSCG_INSPECT_D = 3,
+    SSCG_INSPECT_ALPHA_T = 4, SSCG_INSPECT_ALPHA = 5, SSCG_INSPECT_DELTA = 6
+};
+SSCG_API sscg_status sscg_inspect(const sscg_ctx *ctx, int32_t what, int32_t index, void *host_out,
+                         int64_t capacity);
+
+/* Process-local sizes: planes [z0, z0+nz_proc) (CSR: n rows, z0 = 0). */
+SSCG_API sscg_status sscg_local_shape(const sscg_ctx *ctx, int64_t *z0, int64_t *nz_proc, int64_t *n_local);
+
+SSCG_API void sscg_destroy(sscg_ctx *ctx);
+
+/* Thread-local description of the last error ("" if none). */
+SSCG_API const char *sscg_last_error(void);
+
+/* Library version string. */
+SSCG_API const char *sscg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSCG_H */

@@ -1,0 +1,270 @@
+"""B200-native Chebyshev-basis s-step PCG with nu-sweep Forward Gauss-Seidel
+Gram solves (Thomas & D'Ambra, arxiv 2512.09642).
+
+Thin Python binding of ``libsscg.so`` (C ABI in ``include/sscg.h``): this
+module only marshals arguments (torch tensors / numpy arrays -> pointers);
+every step of the solve runs in the library's sm_100a kernels.  There is no
+CPU fallback: if the library cannot be loaded, every call raises.
+
+    import paper_2512_09642_b200 as sscg
+    op = sscg.Stencil("7pt", nx, ny, nz)
+    with sscg.Solver(op, lmin, lmax, s=16, nu=25) as S:
+        x = S.solve(b, rtol=1e-8, max_outer=1000)      # b: cuda float64 tensor
+        print(S.stats())
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsscg.so")
+
+OK, ERR_INVALID, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_BREAKDOWN, ERR_NONFINITE, ERR_UNSUPPORTED = range(8)
+OP_STENCIL5_2D, OP_STENCIL7, OP_STENCIL27, OP_VARCOEF7, OP_CSR = range(5)
+INSPECT_P, INSPECT_W, INSPECT_GRAM, INSPECT_D, INSPECT_ALPHA_T, INSPECT_ALPHA, INSPECT_DELTA = range(7)
+SOLVE_X0_ZERO = 1
+
+EXPORTS = ["sscg_partition", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host", "sscg_iterate",
+           "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect", "sscg_local_shape", "sscg_destroy",
+           "sscg_last_error", "sscg_version"]
+PROF_NAMES = ["basis", "gram", "allreduce", "fgs", "update", "halo"]
+
+
+class SSCGError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"sscg error {code}: {msg}")
+        self.code = code
+
+
+class _Operator(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
+                ("kx", C.c_void_p), ("ky", C.c_void_p), ("kz", C.c_void_p), ("n", C.c_int64),
+                ("rowptr", C.c_void_p), ("colind", C.c_void_p), ("val", C.c_void_p)]
+
+
+class _Comm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("slabs_per_rank", C.c_int32),
+                ("nccl_id", C.c_void_p)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("outer_iterations", C.c_int32), ("converged", C.c_int32), ("breakdown", C.c_int32),
+                ("nonfinite", C.c_int32), ("r0_norm", C.c_double), ("relres_final", C.c_double),
+                ("history_len", C.c_int32), ("relres_history", C.POINTER(C.c_double)),
+                ("delta_history", C.POINTER(C.c_double)), ("ms_total", C.c_double),
+                ("kernel_launches", C.c_int64), ("allreduces", C.c_int64)]
+
+
+class _Profile(C.Structure):
+    _fields_ = [("ms", C.c_double * 6), ("launches", C.c_int64 * 6)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libsscg.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run `python -m paper_2512_09642_b200.build`")
+    L = C.CDLL(path)
+    vp, i32, i64, d, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_uint32
+    L.sscg_partition.argtypes = [i64, i32, i32, i32, C.POINTER(i64), C.POINTER(i64)]
+    L.sscg_nccl_unique_id.argtypes = [vp]
+    L.sscg_setup.argtypes = [C.POINTER(_Operator), vp, d, d, i32, i32, C.POINTER(_Comm), vp, C.POINTER(vp)]
+    L.sscg_solve.argtypes = [vp, vp, vp, d, i32, u32]
+    L.sscg_solve_host.argtypes = [vp, vp, vp, d, i32, u32]
+    L.sscg_iterate.argtypes = [vp, vp, i32]
+    L.sscg_set_profiling.argtypes = [vp, i32]
+    L.sscg_profile.argtypes = [vp, C.POINTER(_Profile)]
+    L.sscg_stats.argtypes = [vp, C.POINTER(_Stats)]
+    L.sscg_inspect.argtypes = [vp, i32, i32, vp, i64]
+    L.sscg_local_shape.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+    L.sscg_destroy.argtypes = [vp]
+    L.sscg_destroy.restype = None
+    L.sscg_last_error.restype = C.c_char_p
+    L.sscg_version.restype = C.c_char_p
+    for name in ("sscg_partition", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host",
+                 "sscg_iterate", "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect",
+                 "sscg_local_shape"):
+        getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(code):
+    if code != OK:
+        raise SSCGError(code, load().sscg_last_error().decode())
+
+
+def partition(nz: int, nranks: int, slabs_per_rank: int, rank: int) -> tuple[int, int]:
+    """Planes (z0, nzl) of process `rank` (sscg_partition; host only)."""
+    z0, nzl = C.c_int64(), C.c_int64()
+    _check(load().sscg_partition(nz, nranks, slabs_per_rank, rank, C.byref(z0), C.byref(nzl)))
+    return z0.value, nzl.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load().sscg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _ptr(t):
+    """Device/host pointer of a torch tensor or numpy array (no copies)."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+@dataclass
+class Stencil:
+    """Constant/variable-coefficient stencil on the GLOBAL nx*ny*nz grid.
+    kind: '5pt' (2D), '7pt', '27pt', 'varcoef7' (faces kx, ky, kz: device
+    float64 tensors covering this process's planes, see include/sscg.h)."""
+    kind: str
+    nx: int
+    ny: int
+    nz: int = 1
+    kx: object = None
+    ky: object = None
+    kz: object = None
+
+    def _struct(self):
+        k = {"5pt": OP_STENCIL5_2D, "7pt": OP_STENCIL7, "27pt": OP_STENCIL27, "varcoef7": OP_VARCOEF7}[self.kind]
+        return _Operator(k, self.nx, self.ny, self.nz, _ptr(self.kx), _ptr(self.ky), _ptr(self.kz), 0, None, None, None)
+
+
+@dataclass
+class CSR:
+    """General symmetric CSR (device tensors: int64 rowptr, int32 colind,
+    float64 val), single process."""
+    rowptr: object
+    colind: object
+    val: object
+
+    def _struct(self):
+        n = int(self.rowptr.shape[0]) - 1
+        return _Operator(OP_CSR, 0, 0, 0, None, None, None, n, _ptr(self.rowptr), _ptr(self.colind), _ptr(self.val))
+
+
+@dataclass
+class Stats:
+    outer_iterations: int
+    converged: bool
+    breakdown: bool
+    nonfinite: bool
+    r0_norm: float
+    relres_final: float
+    relres_history: np.ndarray
+    delta_history: np.ndarray
+    ms_total: float
+    kernel_launches: int
+    allreduces: int
+
+
+class Solver:
+    """One sscg context (sscg_setup ... sscg_destroy)."""
+
+    def __init__(self, op, lmin: float, lmax: float, s: int, nu: int, diag_M=None, rank: int = 0,
+                 nranks: int = 1, slabs_per_rank: int = 1, nccl_id: bytes | None = None, stream=None):
+        L = load()
+        self._op = op
+        self._opst = op._struct()
+        self.s, self.nu = s, nu
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        comm = _Comm(rank, nranks, slabs_per_rank, C.cast(idbuf, C.c_void_p) if idbuf is not None else None)
+        h = C.c_void_p()
+        strm = None if stream is None else (stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        _check(L.sscg_setup(C.byref(self._opst), _ptr(diag_M), lmin, lmax, s, nu, C.byref(comm), strm,
+                            C.byref(h)))
+        self._h = h
+        z0, nzp, nloc = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(L.sscg_local_shape(h, C.byref(z0), C.byref(nzp), C.byref(nloc)))
+        self.z0, self.nz_local, self.n_local = z0.value, nzp.value, nloc.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().sscg_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def solve(self, b, x=None, rtol: float = 1e-8, max_outer: int = 1000, raise_on_breakdown: bool = True):
+        """b, x: float64 CUDA tensors (process-local).  x=None => x_0 = 0 and a
+        new tensor is returned; otherwise x is updated in place."""
+        import torch
+        assert b.is_cuda and b.dtype == torch.float64 and b.is_contiguous() and b.numel() == self.n_local
+        flags = 0
+        if x is None:
+            x = torch.empty_like(b)
+            flags = SOLVE_X0_ZERO
+        assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous() and x.numel() == self.n_local
+        code = load().sscg_solve(self._h, _ptr(b), _ptr(x), rtol, max_outer, flags)
+        if code in (ERR_BREAKDOWN, ERR_NONFINITE) and not raise_on_breakdown:
+            return x
+        _check(code)
+        return x
+
+    def solve_host(self, b: np.ndarray, x: np.ndarray | None = None, rtol: float = 1e-8, max_outer: int = 1000):
+        """End-to-end call with host buffers (copies are inside the call)."""
+        assert b.dtype == np.float64 and b.flags.c_contiguous and b.size == self.n_local
+        flags = 0
+        if x is None:
+            x = np.empty_like(b)
+            flags = SOLVE_X0_ZERO
+        _check(load().sscg_solve_host(self._h, _ptr(b), _ptr(x), rtol, max_outer, flags))
+        return x
+
+    def iterate(self, x, nsteps: int):
+        """Exactly nsteps more outer iterations from the last solve's state."""
+        _check(load().sscg_iterate(self._h, _ptr(x), nsteps))
+        return x
+
+    def set_profiling(self, on: bool = True):
+        _check(load().sscg_set_profiling(self._h, 1 if on else 0))
+
+    def profile(self) -> dict:
+        """{category: (ms, launches)} accumulated since set_profiling."""
+        p = _Profile()
+        _check(load().sscg_profile(self._h, C.byref(p)))
+        return {n: (p.ms[i], int(p.launches[i])) for i, n in enumerate(PROF_NAMES)}
+
+    def stats(self) -> Stats:
+        st = _Stats()
+        _check(load().sscg_stats(self._h, C.byref(st)))
+        rh = (np.ctypeslib.as_array(st.relres_history, (st.history_len,)).copy()
+              if st.history_len and bool(st.relres_history) else np.zeros(0))
+        nd = max(st.history_len - 1, 0)
+        dh = np.ctypeslib.as_array(st.delta_history, (nd,)).copy() if nd and bool(st.delta_history) else np.zeros(0)
+        return Stats(st.outer_iterations, bool(st.converged), bool(st.breakdown), bool(st.nonfinite), st.r0_norm,
+                     st.relres_final, rh, dh, st.ms_total, st.kernel_launches, st.allreduces)
+
+    def inspect(self, what: int, index: int) -> np.ndarray:
+        n = {INSPECT_P: self.n_local, INSPECT_W: self.n_local, INSPECT_GRAM: self.s * self.s + self.s,
+             INSPECT_D: self.s, INSPECT_ALPHA_T: self.s, INSPECT_ALPHA: self.s, INSPECT_DELTA: 1}[what]
+        out = np.empty(n, dtype=np.float64)
+        _check(load().sscg_inspect(self._h, what, index, out.ctypes.data, out.nbytes))
+        return out
+
+    def basis(self, j: int):
+        return self.inspect(INSPECT_P, j), self.inspect(INSPECT_W, j)
+
+    def gram(self, k: int):
+        g = self.inspect(INSPECT_GRAM, k)
+        s = self.s
+        return g[: s * s].reshape(s, s), g[s * s:]

@@ -1,0 +1,705 @@
+// Host driver and C ABI of libsscg (include/sscg.h).
+//
+// Per outer iteration k (restart form, R3):
+//   for j = 0..s-1:  halo(p_j) ; K1(j)            basis + W = AP
+//   K2 per slab -> [slab sum] -> one ncclAllReduce  Gram block [Ghat | c]
+//   K4                                              stop test, scaling, FGS
+//   K5 per slab                                     x += P alpha, r -= W alpha
+// The stopping decision is taken on the device (K4 sets DevState::done and
+// every later kernel exits at once), so the host enqueues several outer
+// iterations before it reads the flag back.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sscg.h"
+#include "sscg_internal.cuh"
+
+using namespace sscg;
+
+static thread_local std::string g_err;
+
+static sscg_status fail(sscg_status st, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(e_ == cudaErrorMemoryAllocation ? SSCG_ERR_OOM : SSCG_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                        \
+    } while (0)
+
+#define NC(call)                                                                                   \
+    do {                                                                                           \
+        ncclResult_t r_ = (call);                                                                  \
+        if (r_ != ncclSuccess)                                                                     \
+            return fail(SSCG_ERR_NCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__); \
+    } while (0)
+
+struct sscg_ctx {
+    Geo g{};
+    int s = 0, nu = 0;
+    double lmin = 0, lmax = 0, theta = 0, sigma = 0;
+    int rank = 0, nranks = 1, spr = 1;
+    int64_t nz_global = 1, z0_proc = 0, nzl_proc = 1, n_local = 0;
+    std::vector<Slab> slabs;
+    std::vector<void *> allocs;
+    double *blk = nullptr;            // final [Ghat | c]
+    double **blkptrs = nullptr;       // device array of slab block pointers
+    double *alpha = nullptr;
+    DevState *st = nullptr;
+    DevState *st_host = nullptr;      // pinned
+    // history (device) and host copies
+    int hist_cap = 0;
+    double *h_gram = nullptr, *h_d = nullptr, *h_at = nullptr, *h_al = nullptr, *h_delta = nullptr,
+           *h_relres = nullptr;
+    std::vector<double> relres_host, delta_host;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double *bbuf = nullptr, *xbuf = nullptr;   // device buffers of sscg_solve_host
+    double *scratch = nullptr;                 // process-layout scratch for inspect
+    sscg_stats_t stats{};
+    int64_t launches = 0, allreduces = 0;
+    int last_max_outer = -1;
+    bool solved = false;
+    // profiling
+    bool prof_on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    std::vector<int> prof_cat;
+    size_t prof_used = 0;
+    sscg_profile_t prof{};
+};
+
+static const char *kVersion = "sscg-b200 0.1 (sm_100a)";
+
+extern "C" const char *sscg_version(void) { return kVersion; }
+extern "C" const char *sscg_last_error(void) { return g_err.c_str(); }
+
+extern "C" sscg_status sscg_partition(int64_t nz, int32_t nranks, int32_t spr, int32_t rank, int64_t *z0,
+                                      int64_t *nzl)
+{
+    if (nz < 1 || nranks < 1 || spr < 1 || rank < 0 || rank >= nranks || !z0 || !nzl)
+        return fail(SSCG_ERR_INVALID, "sscg_partition: bad arguments");
+    const int64_t S = (int64_t)nranks * spr;
+    if (nz < S) return fail(SSCG_ERR_INVALID, "sscg_partition: %lld planes < %lld slabs", (long long)nz, (long long)S);
+    const int64_t g0 = (int64_t)rank * spr, g1 = g0 + spr;
+    *z0 = g0 * nz / S;
+    *nzl = g1 * nz / S - *z0;
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_nccl_unique_id(void *out)
+{
+    if (!out) return fail(SSCG_ERR_INVALID, "null output");
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    memcpy(out, &id, sizeof id);
+    return SSCG_OK;
+}
+
+template <class T>
+static sscg_status dalloc(sscg_ctx *c, T **p, size_t count)
+{
+    void *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, count * sizeof(T) + 16);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return fail(SSCG_ERR_OOM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+    }
+    c->allocs.push_back(q);
+    *p = static_cast<T *>(q);
+    return SSCG_OK;
+}
+
+#define TRY(x)                           \
+    do {                                 \
+        sscg_status t_ = (x);            \
+        if (t_ != SSCG_OK) return t_;    \
+    } while (0)
+
+__global__ void k_recip_pack(Geo g, const double *diag, double *dinv, int nzl)
+{
+    // dinv (padded vector layout) = 1 / diag (process layout)
+    const int64_t nxy = (int64_t)g.nx * g.ny, tot = nxy * nzl;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t zl = e / nxy, rem = e - zl * nxy;
+        const int64_t y = rem / g.nx, x = rem - y * g.nx;
+        dinv[(zl + 1) * g.plane + y * g.pitch + x] = 1.0 / diag[e];
+    }
+}
+
+__global__ void k_csr_dinv(Geo g, double *dinv)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= g.n) return;
+    double d = 0.0;
+    for (int64_t q = g.rowptr[r]; q < g.rowptr[r + 1]; ++q)
+        if (g.colind[q] == r) d += g.val[q];
+    dinv[g.plane + r] = 1.0 / d;
+}
+
+static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, double lmin, double lmax, int s,
+                              int nu, const sscg_comm *cm, void *stream, sscg_ctx *c)
+{
+    if (!A) return fail(SSCG_ERR_INVALID, "null operator");
+    if (s < 1 || s > 64) return fail(SSCG_ERR_INVALID, "s = %d outside [1, 64]", s);
+    if (nu < 1) return fail(SSCG_ERR_INVALID, "nu = %d < 1", nu);
+    if (!(lmin > 0.0) || !(lmax > lmin) || !std::isfinite(lmax))
+        return fail(SSCG_ERR_INVALID, "need 0 < lambda_min < lambda_max (got %g, %g)", lmin, lmax);
+    if (A->kind < 0 || A->kind > 4) return fail(SSCG_ERR_INVALID, "unknown operator kind %d", A->kind);
+    c->s = s;
+    c->nu = nu;
+    c->lmin = lmin;
+    c->lmax = lmax;
+    c->theta = 2.0 / (lmax - lmin);
+    c->sigma = (lmax + lmin) / 2.0;
+    if (cm) {
+        c->rank = cm->rank;
+        c->nranks = cm->nranks;
+        c->spr = cm->slabs_per_rank;
+    }
+    if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks || c->spr < 1)
+        return fail(SSCG_ERR_INVALID, "bad comm (rank %d of %d, %d slabs per rank)", c->rank, c->nranks, c->spr);
+
+    Geo &g = c->g;
+    g.kind = A->kind;
+    if (A->kind == SSCG_OP_CSR) {
+        if (c->nranks * c->spr != 1) return fail(SSCG_ERR_INVALID, "CSR operator supports a single slab only");
+        if (A->n < 1 || !A->rowptr || !A->colind || !A->val) return fail(SSCG_ERR_INVALID, "CSR arrays missing");
+        g.n = A->n;
+        g.rowptr = A->rowptr;
+        g.colind = A->colind;
+        g.val = A->val;
+        g.nx = (int)A->n;   // one "row" of n doubles per plane
+        g.ny = 1;
+        g.pitch = (int)A->n + (int)(A->n & 1);
+        c->nz_global = 1;
+    } else {
+        if (A->nx < 1 || A->ny < 1 || A->nz < 1 || A->nx > (1 << 30) || A->ny > (1 << 30))
+            return fail(SSCG_ERR_INVALID, "bad grid %lld x %lld x %lld", (long long)A->nx, (long long)A->ny,
+                        (long long)A->nz);
+        if (A->kind == SSCG_OP_STENCIL5_2D && A->nz != 1) return fail(SSCG_ERR_INVALID, "5-point stencil needs nz = 1");
+        if (A->kind == SSCG_OP_VARCOEF7 && (!A->kx || !A->ky || !A->kz))
+            return fail(SSCG_ERR_INVALID, "VARCOEF7 needs kx, ky, kz");
+        g.nx = (int)A->nx;
+        g.ny = (int)A->ny;
+        g.pitch = g.nx + (g.nx & 1);
+        c->nz_global = A->nz;
+    }
+    g.plane = (int64_t)g.ny * g.pitch;
+    g.center = (A->kind == 0) ? 4.0 : (A->kind == 1) ? 6.0 : (A->kind == 2) ? 26.0 : 0.0;
+    g.dinv_c = (g.center > 0) ? 1.0 / g.center : 0.0;
+
+    TRY(sscg_partition(c->nz_global, c->nranks, c->spr, c->rank, &c->z0_proc, &c->nzl_proc));
+    c->n_local = (A->kind == SSCG_OP_CSR) ? A->n : (int64_t)g.nx * g.ny * c->nzl_proc;
+
+    if (stream) {
+        c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    CU(cudaEventCreate(&c->ev0));
+    CU(cudaEventCreate(&c->ev1));
+    CU(cudaMallocHost(&c->st_host, sizeof(DevState)));
+    TRY(dalloc(c, &c->st, 1));
+
+    // slabs of this process
+    const int S = c->nranks * c->spr;
+    int max_nzl = 0;
+    for (int l = 0; l < c->spr; ++l) {
+        const int gidx = c->rank * c->spr + l;
+        Slab sl{};
+        sl.z0 = (int64_t)gidx * c->nz_global / S;
+        sl.nzl = (int)((int64_t)(gidx + 1) * c->nz_global / S - sl.z0);
+        sl.zoff = sl.z0 - c->z0_proc;
+        max_nzl = std::max(max_nzl, sl.nzl);
+        c->slabs.push_back(sl);
+    }
+    g.vstride = ((int64_t)(max_nzl + 2) * g.plane + 31) / 32 * 32;   // 256-B aligned vectors
+    const int nent = s * s + s;
+    const int64_t npart = (int64_t)k2_grid() * 8 * nent;
+    for (auto &sl : c->slabs) {
+        TRY(dalloc(c, &sl.P, (size_t)g.vstride * s));
+        TRY(dalloc(c, &sl.W, (size_t)g.vstride * s));
+        CU(cudaMemsetAsync(sl.P, 0, (size_t)g.vstride * s * sizeof(double), c->stream));
+        CU(cudaMemsetAsync(sl.W, 0, (size_t)g.vstride * s * sizeof(double), c->stream));
+        TRY(dalloc(c, &sl.part, (size_t)npart));
+        TRY(dalloc(c, &sl.blk, (size_t)nent));
+        TRY(dalloc(c, &sl.ticket, 1));
+        CU(cudaMemsetAsync(sl.ticket, 0, sizeof(unsigned), c->stream));
+        if (A->kind == SSCG_OP_VARCOEF7) {
+            sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
+            sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;
+            sl.kz = A->kz + sl.zoff * g.ny * g.nx;
+        }
+        if (diag_M || A->kind == SSCG_OP_CSR) {
+            double *dv = nullptr;
+            TRY(dalloc(c, &dv, (size_t)g.vstride));
+            CU(cudaMemsetAsync(dv, 0, (size_t)g.vstride * sizeof(double), c->stream));
+            if (diag_M) {
+                const int nzl = (A->kind == SSCG_OP_CSR) ? 1 : sl.nzl;
+                const int64_t tot = (int64_t)g.nx * g.ny * nzl;
+                k_recip_pack<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, c->stream>>>(
+                    g, diag_M + sl.zoff * (int64_t)g.nx * g.ny, dv, nzl);
+            } else {
+                k_csr_dinv<<<(unsigned)((g.n + 255) / 256), 256, 0, c->stream>>>(g, dv);
+            }
+            CU(cudaGetLastError());
+            sl.dinv = dv;
+        }
+    }
+    TRY(dalloc(c, &c->blk, (size_t)nent));
+    TRY(dalloc(c, &c->alpha, 64));
+    {
+        std::vector<double *> ptrs;
+        for (auto &sl : c->slabs) ptrs.push_back(sl.blk);
+        TRY(dalloc(c, &c->blkptrs, ptrs.size()));
+        CU(cudaMemcpyAsync(c->blkptrs, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice,
+                           c->stream));
+    }
+    TRY(dalloc(c, &c->scratch, (size_t)c->n_local));
+    if (c->nranks > 1) {
+        if (!cm->nccl_id) return fail(SSCG_ERR_INVALID, "nranks > 1 needs nccl_id");
+        ncclUniqueId id;
+        memcpy(&id, cm->nccl_id, sizeof id);
+        NC(ncclCommInitRank(&c->comm, c->nranks, id, c->rank));
+    }
+    CU(cudaStreamSynchronize(c->stream));
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_setup(const sscg_operator *A, const double *diag_M, double lambda_min,
+                                  double lambda_max, int32_t s, int32_t nu, const sscg_comm *comm, void *stream,
+                                  sscg_ctx **out)
+{
+    if (!out) return fail(SSCG_ERR_INVALID, "null out");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(SSCG_ERR_CUDA, "no CUDA device");
+    sscg_ctx *c = new sscg_ctx();
+    sscg_status st = setup_impl(A, diag_M, lambda_min, lambda_max, s, nu, comm, stream, c);
+    if (st != SSCG_OK) {
+        std::string keep = g_err;
+        sscg_destroy(c);
+        g_err = keep;
+        return st;
+    }
+    *out = c;
+    return SSCG_OK;
+}
+
+extern "C" void sscg_destroy(sscg_ctx *c)
+{
+    if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->st_host) cudaFreeHost(c->st_host);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    for (auto &e : c->prof_events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+// ---------------------------------------------------------------------------
+// halo exchange of basis vector j (one plane per side)
+static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab)
+{
+    const Geo &g = c->g;
+    if (g.kind == SSCG_OP_CSR) return SSCG_OK;
+    const size_t pb = (size_t)g.plane * sizeof(double);
+    const int L = (int)c->slabs.size();
+    // in-process neighbours
+    for (int l = 0; l + 1 < L; ++l) {
+        double *lo = vec_of_slab[l], *hi = vec_of_slab[l + 1];
+        const int nzl = c->slabs[l].nzl;
+        CU(cudaMemcpyAsync(hi, lo + (int64_t)nzl * g.plane, pb, cudaMemcpyDeviceToDevice, c->stream));
+        CU(cudaMemcpyAsync(lo + (int64_t)(nzl + 1) * g.plane, hi + g.plane, pb, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    if (c->nranks > 1) {
+        NC(ncclGroupStart());
+        if (c->rank > 0) {
+            double *v = vec_of_slab[0];
+            NC(ncclSend(v + g.plane, (size_t)g.plane, ncclDouble, c->rank - 1, c->comm, c->stream));
+            NC(ncclRecv(v, (size_t)g.plane, ncclDouble, c->rank - 1, c->comm, c->stream));
+        }
+        if (c->rank < c->nranks - 1) {
+            double *v = vec_of_slab[L - 1];
+            const int nzl = c->slabs[L - 1].nzl;
+            NC(ncclSend(v + (int64_t)nzl * g.plane, (size_t)g.plane, ncclDouble, c->rank + 1, c->comm, c->stream));
+            NC(ncclRecv(v + (int64_t)(nzl + 1) * g.plane, (size_t)g.plane, ncclDouble, c->rank + 1, c->comm,
+                        c->stream));
+        }
+        NC(ncclGroupEnd());
+    }
+    return SSCG_OK;
+}
+
+// profiling: CUDA event pairs around launch groups, resolved on demand
+static sscg_status prof_mark(sscg_ctx *c, int cat, bool begin)
+{
+    if (!c->prof_on) return SSCG_OK;
+    if (begin) {
+        if (c->prof_used == c->prof_events.size()) {
+            cudaEvent_t e0, e1;
+            CU(cudaEventCreate(&e0));
+            CU(cudaEventCreate(&e1));
+            c->prof_events.push_back({e0, e1});
+            c->prof_cat.push_back(cat);
+        }
+        c->prof_cat[c->prof_used] = cat;
+        CU(cudaEventRecord(c->prof_events[c->prof_used].first, c->stream));
+    } else {
+        CU(cudaEventRecord(c->prof_events[c->prof_used].second, c->stream));
+        ++c->prof_used;
+    }
+    return SSCG_OK;
+}
+
+static sscg_status prof_resolve(sscg_ctx *c)
+{
+    if (!c->prof_used) return SSCG_OK;
+    CU(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < c->prof_used; ++i) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, c->prof_events[i].first, c->prof_events[i].second));
+        c->prof.ms[c->prof_cat[i]] += ms;
+        c->prof.launches[c->prof_cat[i]] += 1;
+    }
+    c->prof_used = 0;
+    return SSCG_OK;
+}
+
+static sscg_status enqueue_outer(sscg_ctx *c, double *x)
+{
+    const Geo &g = c->g;
+    const int s = c->s;
+    const int L = (int)c->slabs.size();
+    std::vector<double *> vj(L);
+    const bool halo = (L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR;
+    for (int j = 0; j < s; ++j) {
+        for (int l = 0; l < L; ++l) vj[l] = c->slabs[l].P + (int64_t)j * g.vstride;
+        if (halo) {
+            TRY(prof_mark(c, SSCG_PROF_HALO, true));
+            TRY(exchange(c, vj.data()));
+            TRY(prof_mark(c, SSCG_PROF_HALO, false));
+        }
+        for (auto &sl : c->slabs) {
+            K1Args a{};
+            a.p = sl.P + (int64_t)j * g.vstride;
+            a.pm = (j > 0) ? sl.P + (int64_t)(j - 1) * g.vstride : nullptr;
+            a.w = sl.W + (int64_t)j * g.vstride;
+            a.pn = (j < s - 1) ? sl.P + (int64_t)(j + 1) * g.vstride : nullptr;
+            a.kx = sl.kx; a.ky = sl.ky; a.kz = sl.kz;
+            a.dinv = sl.dinv;
+            a.dinv_c = g.dinv_c;
+            a.sigma = c->sigma;
+            a.coef = (j == 0) ? c->theta : 2.0 * c->theta;
+            a.mode = (j == s - 1) ? 0 : (j == 0 ? 1 : 2);
+            a.zb = 1;
+            a.ze = sl.nzl + 1;
+            a.nzl = sl.nzl;
+            TRY(prof_mark(c, SSCG_PROF_BASIS, true));
+            launch_k1(g, a, c->st, c->stream);
+            TRY(prof_mark(c, SSCG_PROF_BASIS, false));
+            ++c->launches;
+        }
+    }
+    for (auto &sl : c->slabs) {
+        TRY(prof_mark(c, SSCG_PROF_GRAM, true));
+        launch_k2(g, sl, s, c->st, L == 1 ? c->blk : sl.blk, c->stream);
+        TRY(prof_mark(c, SSCG_PROF_GRAM, false));
+        ++c->launches;
+    }
+    if (L > 1) {
+        TRY(prof_mark(c, SSCG_PROF_GRAM, true));
+        launch_slab_sum(c->blkptrs, L, s * s + s, c->blk, c->st, c->stream);
+        TRY(prof_mark(c, SSCG_PROF_GRAM, false));
+        ++c->launches;
+    }
+    if (c->nranks > 1) {
+        TRY(prof_mark(c, SSCG_PROF_ALLREDUCE, true));
+        NC(ncclAllReduce(c->blk, c->blk, (size_t)(s * s + s), ncclDouble, ncclSum, c->comm, c->stream));
+        TRY(prof_mark(c, SSCG_PROF_ALLREDUCE, false));
+        ++c->allreduces;
+    }
+    K4Args a4{};
+    a4.blk = c->blk;
+    a4.alpha = c->alpha;
+    a4.s = s;
+    a4.nu = c->nu;
+    a4.h_gram = c->h_gram; a4.h_d = c->h_d; a4.h_at = c->h_at; a4.h_al = c->h_al;
+    a4.h_delta = c->h_delta; a4.h_relres = c->h_relres;
+    TRY(prof_mark(c, SSCG_PROF_FGS, true));
+    launch_k4(a4, c->st, c->stream);
+    TRY(prof_mark(c, SSCG_PROF_FGS, false));
+    ++c->launches;
+    for (auto &sl : c->slabs) {
+        TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
+        launch_k5(g, sl, s, c->alpha, x + sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream);
+        TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
+        ++c->launches;
+    }
+    CU(cudaGetLastError());
+    return SSCG_OK;
+}
+
+static sscg_status ensure_history(sscg_ctx *c, int cap)
+{
+    if (cap <= c->hist_cap) return SSCG_OK;
+    const int s = c->s, nent = s * s + s;
+    TRY(dalloc(c, &c->h_gram, (size_t)cap * nent));
+    TRY(dalloc(c, &c->h_d, (size_t)cap * s));
+    TRY(dalloc(c, &c->h_at, (size_t)cap * s));
+    TRY(dalloc(c, &c->h_al, (size_t)cap * s));
+    TRY(dalloc(c, &c->h_delta, (size_t)cap));
+    TRY(dalloc(c, &c->h_relres, (size_t)cap));
+    c->hist_cap = cap;
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, double rtol, int32_t max_outer,
+                                  uint32_t flags)
+{
+    if (!c || !b || !x) return fail(SSCG_ERR_INVALID, "null argument");
+    if (max_outer < 0 || !(rtol >= 0.0)) return fail(SSCG_ERR_INVALID, "bad rtol/max_outer");
+    const Geo &g = c->g;
+    const int cap = std::min(max_outer + 1, 1 << 20);
+    TRY(ensure_history(c, cap));
+    c->launches = 0;
+    c->allreduces = 0;
+    c->last_max_outer = max_outer;
+    DevState h{};
+    h.hist_cap = c->hist_cap;
+    h.rtol = rtol;
+    h.max_outer = max_outer;
+    *c->st_host = h;
+    CU(cudaEventRecord(c->ev0, c->stream));
+    CU(cudaMemcpyAsync(c->st, c->st_host, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+    const int L = (int)c->slabs.size();
+    // r_0 = b - A x_0 into p_0
+    if (flags & SSCG_SOLVE_X0_ZERO) {
+        CU(cudaMemsetAsync(x, 0, (size_t)c->n_local * sizeof(double), c->stream));
+        for (auto &sl : c->slabs) {
+            launch_pack(g, b + sl.zoff * (int64_t)g.nx * g.ny, sl.P, sl.nzl, nullptr, c->stream);
+            ++c->launches;
+        }
+    } else {
+        std::vector<double *> w0(L);
+        for (int l = 0; l < L; ++l) {
+            auto &sl = c->slabs[l];
+            launch_pack(g, x + sl.zoff * (int64_t)g.nx * g.ny, sl.W, sl.nzl, nullptr, c->stream);
+            ++c->launches;
+            w0[l] = sl.W;
+        }
+        TRY(exchange(c, w0.data()));
+        for (auto &sl : c->slabs) {
+            K1Args a{};
+            a.p = sl.W;
+            a.w = sl.P;
+            a.b = b + sl.zoff * (int64_t)g.nx * g.ny;
+            a.kx = sl.kx; a.ky = sl.ky; a.kz = sl.kz;
+            a.dinv = sl.dinv;
+            a.dinv_c = g.dinv_c;
+            a.mode = 3;
+            a.zb = 1;
+            a.ze = sl.nzl + 1;
+            a.nzl = sl.nzl;
+            launch_k1(g, a, nullptr, c->stream);
+            ++c->launches;
+        }
+    }
+    // outer iterations in chunks; the device decides when to stop
+    int issued = 0;
+    int chunk = 2;
+    while (issued < max_outer + 1) {
+        const int n = std::min(chunk, max_outer + 1 - issued);
+        for (int i = 0; i < n; ++i) TRY(enqueue_outer(c, x));
+        issued += n;
+        CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        if (c->st_host->done) break;
+        chunk = std::min(chunk * 2, 16);
+    }
+    CU(cudaEventRecord(c->ev1, c->stream));
+    CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    const DevState &f = *c->st_host;
+    const int outer = f.outer;
+    c->relres_host.assign((size_t)std::min(outer + 1, c->hist_cap), 0.0);
+    c->delta_host.assign((size_t)std::min(outer, c->hist_cap), 0.0);
+    if (!c->relres_host.empty())
+        CU(cudaMemcpy(c->relres_host.data(), c->h_relres, c->relres_host.size() * sizeof(double),
+                      cudaMemcpyDeviceToHost));
+    if (!c->delta_host.empty())
+        CU(cudaMemcpy(c->delta_host.data(), c->h_delta, c->delta_host.size() * sizeof(double),
+                      cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    sscg_stats_t &S = c->stats;
+    S = sscg_stats_t{};
+    S.outer_iterations = outer;
+    S.converged = f.converged;
+    S.breakdown = f.breakdown;
+    S.nonfinite = f.nonfinite;
+    S.r0_norm = f.r0norm;
+    S.history_len = (int32_t)c->relres_host.size();
+    S.relres_final = c->relres_host.empty() ? 0.0 : c->relres_host.back();
+    S.relres_history = c->relres_host.data();
+    S.delta_history = c->delta_host.data();
+    S.ms_total = ms;
+    S.kernel_launches = c->launches;
+    S.allreduces = c->allreduces;
+    c->solved = true;
+    TRY(prof_resolve(c));
+    if (f.breakdown) return fail(SSCG_ERR_BREAKDOWN, "Gram breakdown at outer %d (Ghat_ii <= 0 or non-finite)", outer);
+    if (f.nonfinite) return fail(SSCG_ERR_NONFINITE, "non-finite residual at outer %d", outer);
+    g_err.clear();
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_solve_host(sscg_ctx *c, const double *b_host, double *x_host, double rtol,
+                                       int32_t max_outer, uint32_t flags)
+{
+    if (!c || !b_host || !x_host) return fail(SSCG_ERR_INVALID, "null argument");
+    const size_t bytes = (size_t)c->n_local * sizeof(double);
+    if (!c->bbuf) TRY(dalloc(c, &c->bbuf, (size_t)c->n_local));
+    if (!c->xbuf) TRY(dalloc(c, &c->xbuf, (size_t)c->n_local));
+    CU(cudaMemcpyAsync(c->bbuf, b_host, bytes, cudaMemcpyHostToDevice, c->stream));
+    if (!(flags & SSCG_SOLVE_X0_ZERO)) CU(cudaMemcpyAsync(c->xbuf, x_host, bytes, cudaMemcpyHostToDevice, c->stream));
+    sscg_status st = sscg_solve(c, c->bbuf, c->xbuf, rtol, max_outer, flags);
+    if (st != SSCG_OK && st != SSCG_ERR_BREAKDOWN && st != SSCG_ERR_NONFINITE) return st;
+    std::string keep = g_err;
+    CU(cudaMemcpyAsync(x_host, c->xbuf, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    g_err = keep;
+    return st;
+}
+
+extern "C" sscg_status sscg_stats(const sscg_ctx *c, sscg_stats_t *out)
+{
+    if (!c || !out) return fail(SSCG_ERR_INVALID, "null argument");
+    *out = c->stats;
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_local_shape(const sscg_ctx *c, int64_t *z0, int64_t *nz_proc, int64_t *n_local)
+{
+    if (!c) return fail(SSCG_ERR_INVALID, "null ctx");
+    if (z0) *z0 = c->z0_proc;
+    if (nz_proc) *nz_proc = c->nzl_proc;
+    if (n_local) *n_local = c->n_local;
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_inspect(const sscg_ctx *cc, int32_t what, int32_t index, void *host_out,
+                                    int64_t capacity)
+{
+    sscg_ctx *c = const_cast<sscg_ctx *>(cc);
+    if (!c || !host_out) return fail(SSCG_ERR_INVALID, "null argument");
+    const Geo &g = c->g;
+    const int s = c->s, nent = s * s + s;
+    CU(cudaStreamSynchronize(c->stream));
+    auto need = [&](int64_t bytes) { return capacity >= bytes; };
+    if (what == SSCG_INSPECT_P || what == SSCG_INSPECT_W) {
+        if (index < 0 || index >= s) return fail(SSCG_ERR_INVALID, "column %d out of range", index);
+        if (!need(c->n_local * 8)) return fail(SSCG_ERR_INVALID, "buffer too small");
+        for (auto &sl : c->slabs) {
+            const double *v = (what == SSCG_INSPECT_P ? sl.P : sl.W) + (int64_t)index * g.vstride;
+            launch_unpack(g, v, c->scratch + sl.zoff * (int64_t)g.nx * g.ny, sl.nzl, c->stream);
+        }
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(host_out, c->scratch, (size_t)c->n_local * 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        return SSCG_OK;
+    }
+    if (index < 0 || index >= c->hist_cap || index > c->last_max_outer)
+        return fail(SSCG_ERR_INVALID, "history index %d out of range", index);
+    const double *src = nullptr;
+    int64_t cnt = 0;
+    switch (what) {
+    case SSCG_INSPECT_GRAM: src = c->h_gram + (int64_t)index * nent; cnt = nent; break;
+    case SSCG_INSPECT_D: src = c->h_d + (int64_t)index * s; cnt = s; break;
+    case SSCG_INSPECT_ALPHA_T: src = c->h_at + (int64_t)index * s; cnt = s; break;
+    case SSCG_INSPECT_ALPHA: src = c->h_al + (int64_t)index * s; cnt = s; break;
+    case SSCG_INSPECT_DELTA: src = c->h_delta + index; cnt = 1; break;
+    default: return fail(SSCG_ERR_INVALID, "unknown inspect target %d", what);
+    }
+    if (!need(cnt * 8)) return fail(SSCG_ERR_INVALID, "buffer too small");
+    CU(cudaMemcpy(host_out, src, (size_t)cnt * 8, cudaMemcpyDeviceToHost));
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_iterate(sscg_ctx *c, double *x, int32_t nsteps)
+{
+    if (!c || !x || nsteps < 0) return fail(SSCG_ERR_INVALID, "bad argument");
+    if (!c->solved) return fail(SSCG_ERR_INVALID, "sscg_iterate needs a preceding sscg_solve");
+    if (c->st_host->breakdown || c->st_host->nonfinite) return fail(SSCG_ERR_INVALID, "last solve broke down");
+    c->launches = 0;
+    c->allreduces = 0;
+    DevState h = *c->st_host;
+    h.done = 0;
+    h.converged = 0;
+    h.rtol = 0.0;
+    h.max_outer = 0x3fffffff;
+    *c->st_host = h;
+    CU(cudaEventRecord(c->ev0, c->stream));
+    CU(cudaMemcpyAsync(c->st, c->st_host, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+    for (int i = 0; i < nsteps; ++i) TRY(enqueue_outer(c, x));
+    CU(cudaEventRecord(c->ev1, c->stream));
+    CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->stats.ms_total = ms;
+    c->stats.kernel_launches = c->launches;
+    c->stats.allreduces = c->allreduces;
+    c->stats.outer_iterations = c->st_host->outer;
+    c->stats.history_len = 0;
+    c->stats.relres_history = nullptr;
+    c->stats.delta_history = nullptr;
+    TRY(prof_resolve(c));
+    if (c->st_host->breakdown) return fail(SSCG_ERR_BREAKDOWN, "Gram breakdown during sscg_iterate");
+    if (c->st_host->nonfinite) return fail(SSCG_ERR_NONFINITE, "non-finite residual during sscg_iterate");
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_set_profiling(sscg_ctx *c, int32_t on)
+{
+    if (!c) return fail(SSCG_ERR_INVALID, "null ctx");
+    TRY(prof_resolve(c));
+    c->prof_on = on != 0;
+    c->prof = sscg_profile_t{};
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_profile(sscg_ctx *c, sscg_profile_t *out)
+{
+    if (!c || !out) return fail(SSCG_ERR_INVALID, "null argument");
+    TRY(prof_resolve(c));
+    *out = c->prof;
+    return SSCG_OK;
+}

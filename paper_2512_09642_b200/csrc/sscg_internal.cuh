@@ -1,0 +1,111 @@
+// Internal declarations shared by the sm_100a kernels and the host driver of
+// libsscg.  Nothing here is visible through the C ABI (include/sscg.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sscg {
+
+// Device-resident solver state.  K4 (FGS) is the only writer of the control
+// fields; every hot kernel reads `done` first and exits if it is set, so the
+// host can enqueue several outer iterations without a round trip
+// (device-side stopping test).
+struct DevState {
+    int k;            // current outer index (basis/Gram being built)
+    int done;         // 1 => stop: kernels of later outer iterations are no-ops
+    int converged;
+    int breakdown;
+    int nonfinite;
+    int outer;        // updates applied
+    int hist_cap;     // history slots available
+    int pad_;
+    double r0norm;    // ||r_0||
+    double rtol;
+    int max_outer;
+    int pad2_;
+};
+
+// One z-slab of the decomposition in the workspace layout.
+//   plane  = ny * pitch doubles; pitch = nx rounded up to even (16-B rows)
+//   vector = (nzl + 2) planes: plane 0 = lower halo, 1..nzl interior,
+//            nzl+1 = upper halo (zero at global boundaries).
+struct Slab {
+    int64_t z0;        // first global plane
+    int nzl;           // interior planes
+    int64_t zoff;      // first plane relative to the process-local range
+    double *P;         // s vectors, stride vstride
+    double *W;         // s vectors, stride vstride
+    double *part;      // Gram partials [grid][nent]
+    double *blk;       // this slab's reduced block (s*s + s)
+    unsigned *ticket;  // last-CTA counter for K2
+    const double *kx, *ky, *kz;   // VARCOEF7 faces of this slab
+    const double *dinv;           // Jacobi 1/diag(M) interior layout (or nullptr)
+};
+
+struct Geo {
+    int kind;          // sscg_op_kind
+    int nx, ny;        // grid in x, y
+    int pitch;         // row pitch (doubles)
+    int64_t plane;     // ny * pitch
+    int64_t vstride;   // doubles between consecutive basis vectors
+    double center;     // 4, 6, 26 for constant stencils
+    double dinv_c;     // 1/center
+    // CSR
+    int64_t n;
+    const int64_t *rowptr;
+    const int32_t *colind;
+    const double *val;
+};
+
+// K1: fused SpMV + Jacobi + Chebyshev recurrence over planes [zb, ze)
+//   mode 0: w = A p                                   (j = s-1)
+//   mode 1: w = A p; pn = coef * (dinv w - sigma p)   (j = 0, coef = theta)
+//   mode 2: w = A p; pn = coef * (dinv w - sigma p) - pm   (coef = 2 theta)
+//   mode 3: w = b - A p (residual r_0 = b - A x_0; b in process layout)
+struct K1Args {
+    const double *p;
+    const double *pm;
+    double *w;
+    double *pn;
+    const double *b;       // mode 3 only (process layout, slab offset applied)
+    const double *kx, *ky, *kz;
+    const double *dinv;    // interior layout with pitch, or nullptr => dinv_c
+    double dinv_c;
+    double coef, sigma;
+    int zb, ze;            // padded plane indices (1..nzl)
+    int mode;
+    int nzl;
+};
+
+void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s);
+
+// copy a process-layout grid function into the padded interior of `dst`
+void launch_pack(const Geo &g, const double *src, double *dst, int nzl, const DevState *st,
+                 cudaStream_t s);
+// copy the padded interior of `src` back to process layout
+void launch_unpack(const Geo &g, const double *src, double *dst, int nzl, cudaStream_t s);
+
+// K2: fused Gram Ghat = P^T W (upper incl. diagonal) and c = P^T p_0
+void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk,
+               cudaStream_t stream);
+int k2_grid();
+int k2_num_entries(int s);
+
+// fixed-order sum of per-slab blocks into `blk`
+void launch_slab_sum(const double *const *blks_dev, int nslab, int len, double *blk,
+                     const DevState *st, cudaStream_t s);
+
+// K4: Ruhe scaling + nu FGS sweeps (single CTA) + stopping test + history
+struct K4Args {
+    const double *blk;     // [Ghat (s*s) | c (s)] after allreduce
+    double *alpha;         // out: alpha = d o a~ (s)
+    int s, nu;
+    double *h_gram, *h_d, *h_at, *h_al, *h_delta, *h_relres;  // history [cap][...]
+};
+void launch_k4(const K4Args &a, DevState *st, cudaStream_t s);
+
+// K5: x += P alpha;  p_0 -= W alpha
+void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *x_slab,
+               const DevState *st, cudaStream_t stream);
+
+}  // namespace sscg

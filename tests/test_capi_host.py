@@ -1,0 +1,79 @@
+"""CPU-side checks of the C-ABI library: it builds for sm_100a, loads, exports
+every symbol include/sscg.h declares, and its host-only entry points
+(partition, NCCL id) behave -- no compute call is made without a GPU."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_2512_09642_b200 as sscg
+from paper_2512_09642_b200 import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return sscg.load()
+
+
+def declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "sscg.h")).read()
+    return sorted(set(re.findall(r"SSCG_API\s+[\w\s\*]+?\b(sscg_\w+)\s*\(", hdr)))
+
+
+def test_header_declares_boundary():
+    syms = declared_symbols()
+    for name in ("sscg_setup", "sscg_solve", "sscg_stats", "sscg_inspect", "sscg_destroy"):
+        assert name in syms
+    assert set(syms) == set(sscg.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    # exported dynamic symbols are exactly the C ABI (-fvisibility=hidden)
+    out = os.popen(f"nm -D --defined-only {sscg.LIB_PATH}").read()
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    assert set(declared_symbols()) <= exported
+    assert not [s for s in exported if s.startswith("_ZN4sscg")]
+
+
+def test_sass_targets_sm100a(lib):
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump -lelf {sscg.LIB_PATH}").read()
+    assert "sm_100a" in out
+    sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {sscg.LIB_PATH}").read()
+    assert "UBLKCP" in sass           # K2 streams P and W with bulk TMA copies
+    assert "DFMA" in sass
+
+
+def test_version_and_error(lib):
+    assert b"sm_100a" in lib.sscg_version()
+    assert isinstance(lib.sscg_last_error(), bytes)
+
+
+def test_partition_host_logic(lib):
+    for nz, P, spr in ((448 * 8, 8, 1), (384, 8, 1), (33, 2, 3), (7, 7, 1), (100, 3, 2)):
+        planes = []
+        for r in range(P):
+            z0, nzl = sscg.partition(nz, P, spr, r)
+            assert nzl >= spr
+            planes.append((z0, nzl))
+        assert planes[0][0] == 0
+        for (a0, an), (b0, _) in zip(planes, planes[1:]):
+            assert a0 + an == b0
+        assert planes[-1][0] + planes[-1][1] == nz
+    with pytest.raises(sscg.SSCGError) as e:
+        sscg.partition(3, 4, 1, 0)
+    assert e.value.code == sscg.ERR_INVALID
+
+
+def test_setup_without_gpu_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(sscg.SSCGError) as e:
+        sscg.Solver(sscg.Stencil("7pt", 8, 8, 8), 0.1, 1.9, 4, 4)
+    assert e.value.code == sscg.ERR_CUDA

@@ -1,0 +1,222 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs, at sizes the oracle finishes in seconds, with the
+north_star tolerances (BASELINE.json; R15)."""
+import numpy as np
+import pytest
+
+import inputs
+import oracle as orc
+from gpu_cases import (TOL_ALPHA_DRIFT, TOL_BASIS_DRIFT, TOL_GRAM, TOL_GRAM_DRIFT, TOL_X10, Problem, assert_alpha,
+                       assert_basis, assert_gram, rel_inf)
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # kind, nx, ny, nz, s, nu
+    ("5pt", 64, 64, 1, 8, 20),          # BASELINE cfg 1 (full size)
+    ("7pt", 40, 36, 33, 16, 25),        # cfg 2 shape, reduced
+    ("27pt", 30, 28, 26, 16, 30),       # cfg 3 shape, reduced (Lanczos bounds)
+    ("varcoef7", 24, 22, 20, 8, 20),    # cfg 4 shape, reduced (Lanczos bounds)
+    ("7pt", 33, 17, 19, 5, 10),         # odd nx: padded row pitch, ragged tiles
+]
+
+
+def _ids(c):
+    return "-".join(map(str, c))
+
+
+@pytest.fixture(scope="module", params=CASES, ids=_ids)
+def case(request):
+    kind, nx, ny, nz, s, nu = request.param
+    return Problem(kind, nx, ny, nz, s, nu, lanczos=(kind == "27pt"))
+
+
+def test_basis_and_gram_iteration0(case):
+    x_or, tr = case.oracle(max_outer=0, dump_iter=0)
+    with case.gpu_solver() as S:
+        S.solve(case.b_gpu(), rtol=0.0, max_outer=0)
+        st = S.stats()
+        assert st.outer_iterations == 0
+        assert_basis(S, tr, case.s)
+        assert_gram(S, tr, 0)
+
+
+def test_ten_outer_iterations(case):
+    """Identical inputs at k = 0 (strict north_star tolerances); for k >= 1 the
+    two sides iterate on their own r_k, which differ by propagated rounding,
+    so Gram/alpha get the drift budget of DESIGN.md R15; x after 10 outer
+    iterations is held to the north_star 1e-8."""
+    x_or, tr = case.oracle(max_outer=10, dump_iter=10)
+    with case.gpu_solver() as S:
+        x = S.solve(case.b_gpu(), rtol=0.0, max_outer=10).cpu().numpy()
+        st = S.stats()
+        assert st.outer_iterations == 10
+        assert_gram(S, tr, 0)
+        assert_alpha(S, tr, 0)
+        for k in range(1, 11):
+            assert_gram(S, tr, k, tol=TOL_GRAM_DRIFT)
+        for k in range(1, 10):
+            assert_alpha(S, tr, k, tol=TOL_ALPHA_DRIFT)
+        assert_basis(S, tr, case.s, tol=TOL_BASIS_DRIFT)    # basis of r_10 (after 10 updates)
+        ex = np.linalg.norm(x - x_or) / np.linalg.norm(x_or)
+        assert ex <= TOL_X10, ex
+        assert np.allclose(st.relres_history, tr.relres[:11], rtol=1e-8, atol=0)
+        assert np.allclose(st.delta_history, tr.delta[:10], rtol=1e-5, atol=1e-14)
+
+
+@pytest.mark.parametrize("k", [3, 7])
+def test_restart_identical_inputs(case, k):
+    """Strict parity deep into the iteration: both sides restart from the
+    ORACLE's x_k (r = b - A x_k), so their inputs are identical again."""
+    import torch
+    xk, _ = case.oracle(max_outer=k)
+    x1_or, tr = orc.sstep_cg(case.A, case.lmin, case.lmax, case.s, case.nu, case.b, x0=xk, rtol=0.0,
+                             max_outer=1, dump_iter=0)
+    with case.gpu_solver() as S:
+        x = torch.from_numpy(xk.copy()).cuda()
+        S.solve(case.b_gpu(), x, rtol=0.0, max_outer=0)
+        assert_basis(S, tr, case.s)
+        assert_gram(S, tr, 0)
+        x = torch.from_numpy(xk.copy()).cuda()
+        S.solve(case.b_gpu(), x, rtol=0.0, max_outer=1)
+        assert_gram(S, tr, 0)
+        assert_alpha(S, tr, 0)
+        x1 = x.cpu().numpy()
+    assert np.linalg.norm(x1 - x1_or) <= 1e-12 * np.linalg.norm(x1_or)
+
+
+FULL = [("5pt", 64, 64, 1, 8, 20), ("7pt", 32, 32, 32, 16, 25), ("27pt", 24, 24, 24, 16, 30),
+        ("varcoef7", 16, 16, 16, 8, 20)]
+
+
+@pytest.mark.parametrize("cfg", FULL, ids=_ids)
+def test_full_solve_outer_count(cfg):
+    kind, nx, ny, nz, s, nu = cfg
+    P = Problem(kind, nx, ny, nz, s, nu, lanczos=(kind == "27pt"))
+    x_or, tr = P.oracle(max_outer=3000, rtol=1e-8)
+    assert tr.converged
+    with P.gpu_solver() as S:
+        x = S.solve(P.b_gpu(), rtol=1e-8, max_outer=3000).cpu().numpy()
+        st = S.stats()
+    assert st.converged
+    assert abs(st.outer_iterations - tr.outer) <= 1, (st.outer_iterations, tr.outer)
+    # true residual of the GPU solution, computed by the oracle operator
+    res = np.linalg.norm(P.b - orc.apply(P.A, x)) / np.linalg.norm(P.b)
+    assert res <= 1e-8 * (1 + 1e-6), res
+
+
+@pytest.mark.parametrize("cfg,slabs", [(("7pt", 40, 36, 33, 10, 20), 3), (("27pt", 24, 20, 30, 8, 20), 4),
+                                       (("varcoef7", 20, 18, 21, 6, 15), 3), (("7pt", 33, 17, 19, 5, 10), 2)],
+                         ids=lambda v: _ids(v) if isinstance(v, tuple) else str(v))
+def test_slab_decomposition(cfg, slabs):
+    """P in-process slabs (halo copies + fixed-order Gram sum, the N>1
+    decomposition on one device) equal the one-slab solve to 1e-12 and the
+    oracle within the parity tolerances (P6)."""
+    kind, nx, ny, nz, s, nu = cfg
+    P = Problem(kind, nx, ny, nz, s, nu, lanczos=(kind == "27pt"))
+    x_or, tr = P.oracle(max_outer=6, dump_iter=6)
+    with P.gpu_solver(slabs=1) as S1:
+        x1 = S1.solve(P.b_gpu(), rtol=0.0, max_outer=6).cpu().numpy()
+        G1 = [S1.gram(k)[0] for k in range(7)]
+    with P.gpu_solver(slabs=slabs) as S:
+        x = S.solve(P.b_gpu(), rtol=0.0, max_outer=6).cpu().numpy()
+        for k in range(7):
+            assert np.max(np.abs(S.gram(k)[0] - G1[k])) <= 1e-12 * np.max(np.abs(G1[k]))
+            assert_gram(S, tr, k, tol=TOL_GRAM if k == 0 else TOL_GRAM_DRIFT)
+        assert_basis(S, tr, s, tol=TOL_BASIS_DRIFT)
+    assert np.linalg.norm(x - x1) <= 1e-12 * np.linalg.norm(x1)
+    assert np.linalg.norm(x - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+def test_csr_operator():
+    import torch
+
+    import paper_2512_09642_b200 as sscg
+    nx, ny, nz, s, nu = 14, 12, 10, 6, 15
+    rp, ci, va = inputs.stencil_csr("7pt", nx, ny, nz)
+    A = orc.csr(rp, ci, va)
+    b = inputs.rhs_uniform(nx, ny, nz, seed=5)
+    lmin, lmax = inputs.analytic_bounds("7pt", nx, ny, nz)
+    x_or, tr = orc.sstep_cg(A, lmin, lmax, s, nu, b, rtol=0.0, max_outer=8, dump_iter=8)
+    dev = torch.device("cuda")
+    op = sscg.CSR(torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev), torch.from_numpy(va).to(dev))
+    with sscg.Solver(op, lmin, lmax, s, nu) as S:
+        x = S.solve(torch.from_numpy(b).to(dev), rtol=0.0, max_outer=8).cpu().numpy()
+        assert_gram(S, tr, 0)
+        assert_alpha(S, tr, 0)
+        for k in range(1, 9):
+            assert_gram(S, tr, k, tol=TOL_GRAM_DRIFT)
+        for k in range(1, 8):
+            assert_alpha(S, tr, k, tol=TOL_ALPHA_DRIFT)
+        assert_basis(S, tr, s, tol=TOL_BASIS_DRIFT)
+    assert np.linalg.norm(x - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+def test_worked_example_csr(golden):
+    """PAPER.md:31 restart step on A = diag(1,3) (tests/golden): x_1 = [0.75, 0.25]."""
+    import torch
+
+    import paper_2512_09642_b200 as sscg
+    g = golden["restart_sstep_diag13"]
+    dev = torch.device("cuda")
+    op = sscg.CSR(torch.tensor([0, 1, 2], dtype=torch.int64, device=dev),
+                  torch.tensor([0, 1], dtype=torch.int32, device=dev),
+                  torch.tensor(g["A_diag"], dtype=torch.float64, device=dev))
+    ones = torch.ones(2, dtype=torch.float64, device=dev)
+    with sscg.Solver(op, g["lmin"], g["lmax"], 2, 1, diag_M=ones) as S:
+        x = S.solve(torch.tensor(g["b"], dtype=torch.float64, device=dev), rtol=0.0, max_outer=1)
+        assert x.cpu().tolist() == g["x1_nu1"]
+        G, c = S.gram(0)
+        assert G.tolist() == [[4.0, 2.0], [2.0, 4.0]] and c.tolist() == [2.0, 0.0]
+    with sscg.Solver(op, g["lmin"], g["lmax"], 2, 2, diag_M=ones) as S:
+        x = S.solve(torch.tensor(g["b"], dtype=torch.float64, device=dev), rtol=0.0, max_outer=3)
+        f = 4.0 ** (-2 * 3)
+        assert np.allclose(x.cpu().numpy(), (1 - f) * np.array(g["x_limit"]), rtol=1e-14)
+
+
+def test_nonzero_x0_and_host_entry():
+    P = Problem("7pt", 20, 18, 16, 6, 12)
+    x3_or, _ = P.oracle(max_outer=3)
+    x6_or, _ = P.oracle(max_outer=6)
+    import torch
+    with P.gpu_solver() as S:
+        x = torch.from_numpy(x3_or.copy()).cuda()
+        S.solve(P.b_gpu(), x, rtol=0.0, max_outer=3)     # resume from the oracle's x_3
+        assert np.linalg.norm(x.cpu().numpy() - x6_or) <= 1e-9 * np.linalg.norm(x6_or)
+        xh = S.solve_host(P.b.copy(), rtol=0.0, max_outer=6)
+        assert np.linalg.norm(xh - x6_or) <= TOL_X10 * np.linalg.norm(x6_or)
+
+
+def test_edge_cases():
+    import torch
+
+    import paper_2512_09642_b200 as sscg
+    P = Problem("7pt", 8, 8, 8, 4, 5)
+    with P.gpu_solver() as S:
+        x = S.solve(torch.zeros(512, dtype=torch.float64, device="cuda"), rtol=1e-8, max_outer=10)
+        st = S.stats()
+        assert st.converged and st.outer_iterations == 0 and float(x.abs().max()) == 0.0
+    # s = 1: one basis vector (steepest-descent-like step)
+    P1 = Problem("7pt", 10, 9, 8, 1, 1)
+    x_or, tr = P1.oracle(max_outer=5)
+    with P1.gpu_solver() as S:
+        x = S.solve(P1.b_gpu(), rtol=0.0, max_outer=5).cpu().numpy()
+    assert np.linalg.norm(x - x_or) <= 1e-10 * np.linalg.norm(x_or)
+    # s = 64 (largest basis; several Gram role groups)
+    P64 = Problem("7pt", 12, 12, 12, 40, 3, bounds=(0.02, 2.2))
+    x_or, tr = P64.oracle(max_outer=0, dump_iter=0)
+    with P64.gpu_solver() as S:
+        S.solve(P64.b_gpu(), rtol=0.0, max_outer=0)
+        assert_gram(S, tr, 0)
+    # invalid arguments are reported, not crashed on
+    op = sscg.Stencil("7pt", 8, 8, 8)
+    for bad in (dict(s=0, nu=1), dict(s=65, nu=1), dict(s=4, nu=0)):
+        with pytest.raises(sscg.SSCGError) as e:
+            sscg.Solver(op, 0.1, 1.9, **bad)
+        assert e.value.code == sscg.ERR_INVALID
+    with pytest.raises(sscg.SSCGError):
+        sscg.Solver(op, 1.0, 1.0, 4, 4)
+    with pytest.raises(sscg.SSCGError):
+        sscg.Solver(sscg.Stencil("5pt", 8, 8, 2), 0.1, 1.9, 4, 4)
+    with pytest.raises(sscg.SSCGError):
+        sscg.Solver(op, 0.1, 1.9, 4, 4, slabs_per_rank=9)
