@@ -16,17 +16,20 @@ __device__ __forceinline__ double warp_sum(double v)
     return v;
 }
 
-// One warp; lane l owns rows i = l and i = l + 32.
+// One warp; lane l owns row i = l (and i = l + 32 when s > 32).
 //   d_i = Ghat_ii^{-1/2};  G = S Ghat S with G_ii := 1;  c~ = S c
 //   FGS sweep (I + L) a^(l+1) = c~ - L^T a^(l) in residual form: with
 //   rho = c~ - G a (unit diagonal), coordinate j takes a_j += rho_j and every
-//   other row updates rho_i -= G_ij rho_j (rho_j becomes 0) -- the same
-//   forward substitution a_j = c~_j - sum_{i != j} G_ji a_i,
-//   evaluated with one shuffle + one FMA per coordinate instead of a dot.
+//   row updates rho_i -= G_ij rho_j (for i = j this gives exactly 0 since
+//   G_jj = 1) -- the forward substitution a_j = c~_j - sum_{i != j} G_ji a_i
+//   of PAPER.md:94-97, one shuffle + one FMA per coordinate, branch-free.
+//   s <= 32: row i of G lives in registers of lane i; s > 32: shared memory.
+template <bool TWO>
 __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
 {
     if (st->done) return;
-    __shared__ double Gc[SMAX * SMAX];   // column-major: Gc[j*s + i] = G_ij
+    __shared__ double Gc[TWO ? SMAX * SMAX : 1];   // column-major: Gc[j*s + i] = G_ij
+    __shared__ double dsh[SMAX];
     const int s = a.s, lane = threadIdx.x;
     const int k = st->k;
     const double *Gh = a.blk, *c = a.blk + s * s;
@@ -53,59 +56,80 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
         if (lane == 0) { st->done = 1; st->outer = k; }
         return;
     }
-    // Ruhe scaling
+    // Ruhe scaling (PAPER.md:47-51)
     const int i0 = lane, i1 = lane + 32;
+    const bool v0 = i0 < s, v1 = TWO && i1 < s;
     double d0 = 0.0, d1 = 0.0;
     bool ok = true;
-    if (i0 < s) { const double gdiag = Gh[i0 * s + i0]; ok &= (gdiag > 0.0) && isfinite(gdiag); d0 = 1.0 / sqrt(gdiag); }
-    if (i1 < s) { const double gdiag = Gh[i1 * s + i1]; ok &= (gdiag > 0.0) && isfinite(gdiag); d1 = 1.0 / sqrt(gdiag); }
+    if (v0) { const double gd = Gh[i0 * s + i0]; ok &= (gd > 0.0) && isfinite(gd); d0 = 1.0 / sqrt(gd); }
+    if (v1) { const double gd = Gh[i1 * s + i1]; ok &= (gd > 0.0) && isfinite(gd); d1 = 1.0 / sqrt(gd); }
     if (!__all_sync(0xffffffffu, ok)) {
         if (lane == 0) { st->breakdown = 1; st->done = 1; st->outer = k; }
         return;
     }
-    __shared__ double dsh[SMAX];
-    if (i0 < s) dsh[i0] = d0;
-    if (i1 < s) dsh[i1] = d1;
+    if (v0) dsh[i0] = d0;
+    if (v1) dsh[i1] = d1;
     __syncwarp();
-    for (int q = lane; q < s * s; q += 32) {
-        const int i = q / s, j = q - i * s;
-        Gc[j * s + i] = (i == j) ? 1.0 : (dsh[i] * Gh[q]) * dsh[j];
-    }
-    const double ct0 = (i0 < s) ? d0 * c[i0] : 0.0;
-    const double ct1 = (i1 < s) ? d1 * c[i1] : 0.0;
-    __syncwarp();
-
+    const double ct0 = v0 ? d0 * c[i0] : 0.0;
+    const double ct1 = v1 ? d1 * c[i1] : 0.0;
     double rho0 = ct0, rho1 = ct1, al0 = 0.0, al1 = 0.0;
-    for (int sw = 0; sw < a.nu; ++sw) {
-        for (int j = 0; j < s; ++j) {
-            const int owner = j & 31;
-            const double src = (j < 32) ? rho0 : rho1;
-            const double dj = __shfl_sync(0xffffffffu, src, owner);
-            if (j < 32) {
-                if (lane == owner) { al0 += dj; rho0 = 0.0; }
-                else if (i0 < s) rho0 = fma(-Gc[j * s + i0], dj, rho0);
-                if (i1 < s) rho1 = fma(-Gc[j * s + i1], dj, rho1);
-            } else {
-                if (i0 < s) rho0 = fma(-Gc[j * s + i0], dj, rho0);
-                if (lane == owner) { al1 += dj; rho1 = 0.0; }
-                else if (i1 < s) rho1 = fma(-Gc[j * s + i1], dj, rho1);
+
+    if (!TWO) {
+        double g[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            g[j] = (v0 && j < s) ? ((j == i0) ? 1.0 : (d0 * Gh[i0 * s + j]) * dsh[j]) : 0.0;
+        for (int sw = 0; sw < a.nu; ++sw) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j < s) {
+                    const double dj = __shfl_sync(0xffffffffu, rho0, j);
+                    rho0 = fma(-g[j], dj, rho0);
+                    al0 += (lane == j) ? dj : 0.0;
+                }
             }
         }
+        double res0 = ct0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < s) res0 = fma(-g[j], __shfl_sync(0xffffffffu, al0, j), res0);
+        rho0 = res0;
+    } else {
+        for (int q = lane; q < s * s; q += 32) {
+            const int i = q / s, j = q - i * s;
+            Gc[j * s + i] = (i == j) ? 1.0 : (dsh[i] * Gh[q]) * dsh[j];
+        }
+        __syncwarp();
+        for (int sw = 0; sw < a.nu; ++sw) {
+            for (int j = 0; j < s; ++j) {
+                const bool hi = j >= 32;
+                const int owner = j & 31;
+                const double dj = __shfl_sync(0xffffffffu, hi ? rho1 : rho0, owner);
+                const double g0 = v0 ? Gc[j * s + i0] : 0.0;
+                const double g1 = v1 ? Gc[j * s + i1] : 0.0;
+                rho0 = fma(-g0, dj, rho0);
+                rho1 = fma(-g1, dj, rho1);
+                al0 += (!hi && lane == owner) ? dj : 0.0;
+                al1 += (hi && lane == owner) ? dj : 0.0;
+            }
+        }
+        double res0 = ct0, res1 = ct1;
+        for (int j = 0; j < s; ++j) {
+            const double aj = __shfl_sync(0xffffffffu, (j < 32) ? al0 : al1, j & 31);
+            if (v0) res0 = fma(-Gc[j * s + i0], aj, res0);
+            if (v1) res1 = fma(-Gc[j * s + i1], aj, res1);
+        }
+        rho0 = res0;
+        rho1 = res1;
     }
-    // explicit residual of the Gram system: delta = ||c~ - G a~|| / ||c~||
-    double res0 = ct0, res1 = ct1;
-    for (int j = 0; j < s; ++j) {
-        const double aj = __shfl_sync(0xffffffffu, (j < 32) ? al0 : al1, j & 31);
-        if (i0 < s) res0 = fma(-Gc[j * s + i0], aj, res0);
-        if (i1 < s) res1 = fma(-Gc[j * s + i1], aj, res1);
-    }
-    const double rr = warp_sum(res0 * res0 + res1 * res1);
+    // delta = ||c~ - G a~|| / ||c~||  (PAPER.md:259-262 inexactness monitor)
+    const double rr = warp_sum(rho0 * rho0 + rho1 * rho1);
     const double cc = warp_sum(ct0 * ct0 + ct1 * ct1);
-    if (i0 < s) a.alpha[i0] = d0 * al0;
-    if (i1 < s) a.alpha[i1] = d1 * al1;
+    if (v0) a.alpha[i0] = d0 * al0;
+    if (v1) a.alpha[i1] = d1 * al1;
     if (rec) {
-        if (i0 < s) { a.h_d[(int64_t)k * s + i0] = d0; a.h_at[(int64_t)k * s + i0] = al0; a.h_al[(int64_t)k * s + i0] = d0 * al0; }
-        if (i1 < s) { a.h_d[(int64_t)k * s + i1] = d1; a.h_at[(int64_t)k * s + i1] = al1; a.h_al[(int64_t)k * s + i1] = d1 * al1; }
+        if (v0) { a.h_d[(int64_t)k * s + i0] = d0; a.h_at[(int64_t)k * s + i0] = al0; a.h_al[(int64_t)k * s + i0] = d0 * al0; }
+        if (v1) { a.h_d[(int64_t)k * s + i1] = d1; a.h_at[(int64_t)k * s + i1] = al1; a.h_al[(int64_t)k * s + i1] = d1 * al1; }
         if (lane == 0) a.h_delta[k] = sqrt(rr) / sqrt(cc);
     }
     if (lane == 0) {
@@ -181,7 +205,11 @@ __global__ void __launch_bounds__(256) k5_update_gen(K5Params k, const DevState 
 
 }  // namespace
 
-void launch_k4(const K4Args &a, DevState *st, cudaStream_t s) { k4_fgs<<<1, 32, 0, s>>>(a, st); }
+void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
+{
+    if (a.s <= 32) k4_fgs<false><<<1, 32, 0, s>>>(a, st);
+    else k4_fgs<true><<<1, 32, 0, s>>>(a, st);
+}
 
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *x_slab, const DevState *st,
                cudaStream_t stream)

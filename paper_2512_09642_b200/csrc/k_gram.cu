@@ -1,86 +1,74 @@
 // K2 -- fused tall-skinny Gram pass:
 //   Ghat_ij = p_i^T w_j  (i <= j, W = AP)      c_i = p_i^T p_0  (= P^T r_k)
-// One persistent CTA per SM streams its contiguous share of the 2s basis
-// columns exactly once from HBM with 1-D bulk TMA copies
-// (cp.async.bulk ... mbarrier::complete_tx) into a 3-stage shared-memory
-// ring; consumer warps own TB x TB register tiles of the upper block
-// triangle of [Ghat | c] and read their operands from shared memory.
-// Partials are reduced with warp shuffles, then across warps in a fixed
-// order, written per CTA, and the last CTA to finish (integer ticket, no FP
-// atomics) sums all CTA partials in index order: the result is bitwise
-// deterministic for a given grid.
+//
+// One persistent CTA per SM streams a contiguous share of the basis exactly
+// once from HBM.  A producer warp issues two TMA tensor loads per stage
+// (cp.async.bulk.tensor.2d: a [s_pad x E] box of P and one of W, rows past s
+// and elements past the slab zero-filled by the TMA unit) into an
+// NS-deep shared-memory ring guarded by full/empty mbarriers.  Consumer warps
+// own TB x TB register tiles of the upper block triangle of Ghat (the
+// diagonal-tile warps also accumulate c) and read operands from shared
+// memory with compile-time offsets.  Partials are reduced with warp shuffles,
+// then across warps in a fixed order, written per CTA; the last CTA (integer
+// ticket, no FP atomics) sums the CTA partials in index order, so the block
+// is bitwise deterministic for a given grid.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "sscg_internal.cuh"
+#include "tma.cuh"
 
 namespace sscg {
 namespace {
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p)
-{
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t phase)
-{
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-constexpr int NSTAGE = 3;
+constexpr int MAX_STAGE = 8;
 
 struct K2Params {
-    const double *P;   // interior start of p_0
-    const double *W;   // interior start of w_0
-    int64_t vstride;   // doubles between basis vectors
-    int64_t N;         // interior doubles per vector (even)
-    int s;
-    int E;             // elements per stage (multiple of 64)
-    int nb;            // ceil(s / TB)
-    int nroles;        // roles in the grid (all CTAs)
+    int64_t N;         // interior doubles per vector
+    int s, s_pad;      // basis size, box rows (multiple of TB)
+    int nb;            // s_pad / TB
+    int nroles;        // roles in the grid (all role groups)
     int roles_cta;     // roles per CTA (grid.y groups)
-    int nsl;           // slices per role
-    double *part;      // [gridDim.y * gridDim.x][nent]
+    int nsl;           // consumer warps per role
+    int nstage;
+    double *part;      // [gridDim.y * gridDim.x][s*s + s]
     double *out;       // [s*s + s]
     unsigned *ticket;
 };
 
-template <int TB>
-__global__ void __launch_bounds__(256, 1) k2_gram(K2Params k, const DevState *st)
+template <int TB, int E>
+__global__ void __launch_bounds__(256, 1)
+    k2_gram(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW, K2Params k,
+            const DevState *st)
 {
     if (st && st->done) return;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ uint64_t full[NSTAGE];
+    extern __shared__ __align__(1024) double smem[];
+    __shared__ uint64_t full[MAX_STAGE], empty[MAX_STAGE];
     __shared__ bool is_last;
-    const int s = k.s, E = k.E;
-    const int ncol = 2 * s;
-    double *stage0 = reinterpret_cast<double *>(smem_raw);
-    const int64_t stage_elems = (int64_t)ncol * E;
-
+    const int s = k.s, NS = k.nstage;
+    const int stage_elems = 2 * k.s_pad * E;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // role of this warp: (I, J) with I <= J in block units
-    const int role_local = warp / k.nsl, slice = warp % k.nsl;
+    const int ncw = k.roles_cta * k.nsl;            // consumer warps
+
+    const int64_t nchunks = (k.N + E - 1) / E;
+    const int64_t c_lo = nchunks * blockIdx.x / gridDim.x;
+    const int64_t c_hi = nchunks * (blockIdx.x + 1) / gridDim.x;
+    const int nit = (int)(c_hi - c_lo);
+
+    if (tid == 0) {
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], ncw);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmP);
+        tma_prefetch_desc(&tmW);
+    }
+    __syncthreads();
+
+    // consumer role (warps 1..ncw): tile (I, J), I <= J, in block units
+    const int cw = warp - 1;
+    const int role_local = cw / k.nsl, slice = cw - role_local * k.nsl;
     const int role = blockIdx.y * k.roles_cta + role_local;
     int I = 0, J = 0;
     {
@@ -90,32 +78,9 @@ __global__ void __launch_bounds__(256, 1) k2_gram(K2Params k, const DevState *st
             r -= k.nb - a;
         }
     }
-    const bool active = role_local < k.roles_cta && role < k.nroles;
-
-    // contiguous chunk range of this CTA
-    const int64_t nchunks = (k.N + E - 1) / E;
-    const int64_t c_lo = nchunks * blockIdx.x / gridDim.x;
-    const int64_t c_hi = nchunks * (blockIdx.x + 1) / gridDim.x;
-
-    if (tid == 0) {
-        for (int i = 0; i < NSTAGE; ++i) mbar_init(&full[i], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    auto issue = [&](int64_t c, int stg) {
-        const int64_t e0 = c * E;
-        const int64_t ne = (k.N - e0 < E) ? (k.N - e0) : E;
-        const uint32_t bytes = (uint32_t)(ne * 8);
-        double *dst = stage0 + stg * stage_elems;
-        mbar_expect_tx(&full[stg], bytes * (uint32_t)ncol);
-        for (int col = 0; col < ncol; ++col) {
-            const double *src = (col < s ? k.P + (int64_t)col * k.vstride : k.W + (int64_t)(col - s) * k.vstride) + e0;
-            bulk_g2s(dst + (int64_t)col * E, src, bytes, &full[stg]);
-        }
-    };
-    if (tid == 0)
-        for (int i = 0; i < NSTAGE && c_lo + i < c_hi; ++i) issue(c_lo + i, i);
+    const bool consumer = warp >= 1 && cw < ncw;
+    const bool active = consumer && role < k.nroles;
+    const bool diag = (I == J);
 
     double acc[TB][TB];
     double cac[TB];
@@ -125,38 +90,52 @@ __global__ void __launch_bounds__(256, 1) k2_gram(K2Params k, const DevState *st
 #pragma unroll
         for (int b = 0; b < TB; ++b) acc[a][b] = 0.0;
     }
-    const bool diag = (I == J);
-    const int i0 = I * TB, j0 = J * TB;
 
-    for (int64_t c = c_lo; c < c_hi; ++c) {
-        const int it = (int)(c - c_lo);
-        const int stg = it % NSTAGE;
-        const uint32_t phase = (uint32_t)((it / NSTAGE) & 1);
-        while (!mbar_try_wait(&full[stg], phase)) {
-        }
-        const int64_t e0 = c * E;
-        const int ne = (int)((k.N - e0 < E) ? (k.N - e0) : E);
-        const double *sb = stage0 + stg * stage_elems;
-        if (active) {
-            for (int e = lane + 32 * slice; e < ne; e += 32 * k.nsl) {
-                double av[TB], bv[TB];
-#pragma unroll
-                for (int a = 0; a < TB; ++a) av[a] = (i0 + a < s) ? sb[(int64_t)(i0 + a) * E + e] : 0.0;
-#pragma unroll
-                for (int b = 0; b < TB; ++b) bv[b] = (j0 + b < s) ? sb[(int64_t)(s + j0 + b) * E + e] : 0.0;
-#pragma unroll
-                for (int a = 0; a < TB; ++a)
-#pragma unroll
-                    for (int b = 0; b < TB; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
-                if (diag) {
-                    const double p0 = sb[e];
-#pragma unroll
-                    for (int a = 0; a < TB; ++a) cac[a] = fma(av[a], p0, cac[a]);
-                }
+    if (warp == 0) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            const uint32_t bytes = (uint32_t)stage_elems * 8u;
+            for (int it = 0; it < nit; ++it) {
+                const int stg = it % NS;
+                if (it >= NS) mbar_wait(&empty[stg], (uint32_t)((it / NS - 1) & 1));
+                double *dst = smem + (size_t)stg * stage_elems;
+                const int x = (int)((c_lo + it) * E);
+                mbar_expect_tx(&full[stg], bytes);
+                tma_load_2d(dst, &tmP, x, 0, &full[stg]);
+                tma_load_2d(dst + k.s_pad * E, &tmW, x, 0, &full[stg]);
             }
         }
-        __syncthreads();   // every warp is done with this stage
-        if (tid == 0 && c + NSTAGE < c_hi) issue(c + NSTAGE, stg);
+    } else if (consumer) {
+        // ---------------- consumers ----------------
+        for (int it = 0; it < nit; ++it) {
+            const int stg = it % NS;
+            mbar_wait(&full[stg], (uint32_t)((it / NS) & 1));
+            if (active) {
+                const double *sP = smem + (size_t)stg * stage_elems;
+                const double *pa = sP + I * TB * E;
+                const double *pb = sP + (k.s_pad + J * TB) * E;
+#pragma unroll 2
+                for (int t = slice; t < E / 32; t += k.nsl) {
+                    const int e = t * 32 + lane;
+                    double av[TB], bv[TB];
+#pragma unroll
+                    for (int a = 0; a < TB; ++a) av[a] = pa[a * E + e];
+#pragma unroll
+                    for (int b = 0; b < TB; ++b) bv[b] = pb[b * E + e];
+#pragma unroll
+                    for (int a = 0; a < TB; ++a)
+#pragma unroll
+                        for (int b = 0; b < TB; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+                    if (diag) {
+                        const double p0 = sP[e];
+#pragma unroll
+                        for (int a = 0; a < TB; ++a) cac[a] = fma(av[a], p0, cac[a]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+        }
     }
 
     // warp reduction (butterfly, fixed order)
@@ -174,16 +153,15 @@ __global__ void __launch_bounds__(256, 1) k2_gram(K2Params k, const DevState *st
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         cac[a] = v;
     }
-    // per-warp results to smem (reuse stage 0), then slices summed in order
-    double *red = stage0;   // [nwarps][TB*TB + TB]
+    __syncthreads();   // all TMA traffic consumed: the ring can be reused
     constexpr int RW = TB * TB + TB;
-    __syncthreads();
-    if (lane == 0) {
+    double *red = smem;   // [ncw][RW]
+    if (consumer && lane == 0) {
 #pragma unroll
         for (int a = 0; a < TB; ++a) {
 #pragma unroll
-            for (int b = 0; b < TB; ++b) red[warp * RW + a * TB + b] = acc[a][b];
-            red[warp * RW + TB * TB + a] = cac[a];
+            for (int b = 0; b < TB; ++b) red[cw * RW + a * TB + b] = acc[a][b];
+            red[cw * RW + TB * TB + a] = cac[a];
         }
     }
     __syncthreads();
@@ -193,11 +171,11 @@ __global__ void __launch_bounds__(256, 1) k2_gram(K2Params k, const DevState *st
         for (int q = tid; q < nent; q += blockDim.x) mypart[q] = 0.0;
         __syncthreads();
     }
-    // each active role's slice-0 warp writes its entries
     if (active && slice == 0) {
+        const int i0 = I * TB, j0 = J * TB;
         for (int q = lane; q < RW; q += 32) {
             double v = 0.0;
-            for (int sl = 0; sl < k.nsl; ++sl) v += red[(warp + sl) * RW + q];
+            for (int sl = 0; sl < k.nsl; ++sl) v += red[(cw + sl) * RW + q];
             if (q < TB * TB) {
                 const int i = i0 + q / TB, j = j0 + q % TB;
                 if (i < s && j < s && i <= j) mypart[i * s + j] = v;
@@ -221,10 +199,14 @@ __global__ void __launch_bounds__(256, 1) k2_gram(K2Params k, const DevState *st
     const int nparts = gridDim.x * gridDim.y;
     for (int q = tid; q < nent; q += blockDim.x) {
         int i, j;
-        bool valid;
-        if (q < s * s) { i = q / s; j = q % s; valid = (i <= j); }
-        else { i = q - s * s; j = -1; valid = true; }
-        if (!valid) continue;
+        if (q < s * s) {
+            i = q / s;
+            j = q - i * s;
+            if (i > j) continue;
+        } else {
+            i = q - s * s;
+            j = -1;
+        }
         double v = 0.0;
         for (int b = 0; b < nparts; ++b) v += __ldcg(k.part + (int64_t)b * nent + q);
         if (j >= 0) {
@@ -251,7 +233,7 @@ __global__ void k_slab_sum(const double *const *blks, int nslab, int len, double
 int g_sms = 0;
 
 struct K2Plan {
-    int TB, nb, nroles, roles_cta, nsl, E, gy, threads;
+    int TB, E, s_pad, nb, nroles, roles_cta, nsl, gy, nstage, threads;
     size_t smem;
 };
 
@@ -259,21 +241,32 @@ K2Plan plan(int s)
 {
     K2Plan p;
     p.TB = (s <= 8) ? 4 : 8;
-    p.nb = (s + p.TB - 1) / p.TB;
+    p.E = (s <= 16) ? 256 : (s <= 32 ? 128 : 64);
+    p.s_pad = (s + p.TB - 1) / p.TB * p.TB;
+    p.nb = p.s_pad / p.TB;
     p.nroles = p.nb * (p.nb + 1) / 2;
-    p.roles_cta = p.nroles < 8 ? p.nroles : 8;
+    p.roles_cta = p.nroles < 7 ? p.nroles : 7;   // <= 8 warps: 255 registers per thread
     p.gy = (p.nroles + p.roles_cta - 1) / p.roles_cta;
     p.nsl = 1;
-    while (p.roles_cta * p.nsl * 2 <= 8) p.nsl *= 2;
-    // stage of about 64 KB: 2s columns x E doubles
-    int E = 65536 / (16 * s);
-    E = (E / 64) * 64;
-    if (E < 64) E = 64;
-    if (E > 1024) E = 1024;
-    p.E = E;
-    p.threads = 32 * p.roles_cta * p.nsl;
-    p.smem = (size_t)NSTAGE * 2 * s * E * sizeof(double);
+    while (p.roles_cta * p.nsl * 2 <= 7) p.nsl *= 2;
+    const size_t stage = (size_t)2 * p.s_pad * p.E * sizeof(double);
+    p.nstage = (int)std::min<size_t>(MAX_STAGE, (200 * 1024) / stage);
+    p.smem = stage * p.nstage;
+    p.threads = 32 * (1 + p.roles_cta * p.nsl);
     return p;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
 }
 
 }  // namespace
@@ -291,22 +284,52 @@ int k2_grid()
 
 int k2_num_entries(int s) { return s * s + s; }
 
-// partial buffer must hold k2_grid() * gy * (s*s+s) doubles; gy <= 4 for s <= 64
-void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk,
-               cudaStream_t stream)
+// 2-D tensor map over `rows` basis vectors starting at `base` (interior
+// start), `inner` doubles each, `stride` doubles apart; box [box_rows x box_inner]
+bool encode_rows_map(CUtensorMap *m, const double *base, int64_t inner, int rows, int64_t stride, int box_inner,
+                     int box_rows)
+{
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)stride * sizeof(double)};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool k2_prepare(const Geo &g, Slab &sl, int s)
+{
+    const K2Plan p = plan(s);
+    const int64_t N = (int64_t)sl.nzl * g.plane;
+    return encode_rows_map(&sl.tmP, sl.P + g.plane, N, s, g.vstride, p.E, p.s_pad) &&
+           encode_rows_map(&sl.tmW, sl.W + g.plane, N, s, g.vstride, p.E, p.s_pad);
+}
+
+template <int TB, int E>
+static void launch_t(const CUtensorMap &a, const CUtensorMap &b, const K2Params &k, const K2Plan &p, dim3 grid,
+                     const DevState *st, cudaStream_t stream)
+{
+    cudaFuncSetAttribute(k2_gram<TB, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    k2_gram<TB, E><<<grid, p.threads, p.smem, stream>>>(a, b, k, st);
+}
+
+// partial buffer must hold k2_grid() * gy * (s*s+s) doubles; gy <= 5 for s <= 64
+void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk, cudaStream_t stream)
 {
     const K2Plan p = plan(s);
     K2Params k;
-    k.P = sl.P + g.plane;
-    k.W = sl.W + g.plane;
-    k.vstride = g.vstride;
     k.N = (int64_t)sl.nzl * g.plane;
     k.s = s;
-    k.E = p.E;
+    k.s_pad = p.s_pad;
     k.nb = p.nb;
     k.nroles = p.nroles;
     k.roles_cta = p.roles_cta;
     k.nsl = p.nsl;
+    k.nstage = p.nstage;
     k.part = sl.part;
     k.out = out_blk;
     k.ticket = sl.ticket;
@@ -314,13 +337,10 @@ void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *
     int gx = k2_grid();
     if (nchunks < gx) gx = (int)nchunks;
     dim3 grid(gx, p.gy);
-    if (p.TB == 4) {
-        cudaFuncSetAttribute(k2_gram<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-        k2_gram<4><<<grid, p.threads, p.smem, stream>>>(k, st);
-    } else {
-        cudaFuncSetAttribute(k2_gram<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-        k2_gram<8><<<grid, p.threads, p.smem, stream>>>(k, st);
-    }
+    if (p.TB == 4) launch_t<4, 256>(sl.tmP, sl.tmW, k, p, grid, st, stream);
+    else if (p.E == 256) launch_t<8, 256>(sl.tmP, sl.tmW, k, p, grid, st, stream);
+    else if (p.E == 128) launch_t<8, 128>(sl.tmP, sl.tmW, k, p, grid, st, stream);
+    else launch_t<8, 64>(sl.tmP, sl.tmW, k, p, grid, st, stream);
 }
 
 void launch_slab_sum(const double *const *blks_dev, int nslab, int len, double *blk, const DevState *st,

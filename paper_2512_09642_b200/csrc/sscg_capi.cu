@@ -246,6 +246,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         TRY(dalloc(c, &sl.blk, (size_t)nent));
         TRY(dalloc(c, &sl.ticket, 1));
         CU(cudaMemsetAsync(sl.ticket, 0, sizeof(unsigned), c->stream));
+        if (!k2_prepare(g, sl, s)) return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the Gram pass");
         if (A->kind == SSCG_OP_VARCOEF7) {
             sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
             sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;

@@ -1,6 +1,7 @@
 // Internal declarations shared by the sm_100a kernels and the host driver of
 // libsscg.  Nothing here is visible through the C ABI (include/sscg.h).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -40,6 +41,7 @@ struct Slab {
     unsigned *ticket;  // last-CTA counter for K2
     const double *kx, *ky, *kz;   // VARCOEF7 faces of this slab
     const double *dinv;           // Jacobi 1/diag(M) interior layout (or nullptr)
+    CUtensorMap tmP, tmW;         // K2: [s rows x interior] views of P and W
 };
 
 struct Geo {
@@ -89,6 +91,7 @@ void launch_unpack(const Geo &g, const double *src, double *dst, int nzl, cudaSt
 void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk,
                cudaStream_t stream);
 int k2_grid();
+bool k2_prepare(const Geo &g, Slab &sl, int s);   // encode the TMA tensor maps
 int k2_num_entries(int s);
 
 // fixed-order sum of per-slab blocks into `blk`

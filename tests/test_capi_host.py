@@ -45,7 +45,7 @@ def test_sass_targets_sm100a(lib):
     out = os.popen(f"/usr/local/cuda/bin/cuobjdump -lelf {sscg.LIB_PATH}").read()
     assert "sm_100a" in out
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {sscg.LIB_PATH}").read()
-    assert "UBLKCP" in sass           # K2 streams P and W with bulk TMA copies
+    assert "UTMALDG" in sass          # K2 streams P and W with TMA tensor loads
     assert "DFMA" in sass
 
 

