@@ -152,6 +152,16 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def max_over_ranks(dist, v: float, device="cuda") -> float:
+    """Max of a per-rank time over all ranks (dist = torch.distributed or None)."""
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -212,13 +222,6 @@ def run_ours(a):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(v):
-        if not dist:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     # r_0 = b and the first basis/Gram (untimed), then W warm-up steps
     x = S.solve(b, rtol=0.0, max_outer=0)
     S.iterate(x, a.warmup)
@@ -231,7 +234,7 @@ def run_ours(a):
     st = S.stats()
     prof = S.profile()
     S.set_profiling(False)
-    ms = max_over_ranks(st.ms_total)
+    ms = max_over_ranks(dist, st.ms_total)
     value = n_global * a.steps / (ms / 1e3) / 1e9
     launches = st.kernel_launches
 
@@ -269,7 +272,7 @@ def run_ours(a):
         t0 = time.perf_counter()
         S.solve_host(bh, xh.numpy(), rtol=0.0, max_outer=a.steps)
         t1 = time.perf_counter()
-        te = max_over_ranks(t1 - t0)
+        te = max_over_ranks(dist, t1 - t0)
         e2e = {"value": n_global * a.steps / te / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 8.0 * n_local / a.steps, "d2h_bytes_per_step": 8.0 * n_local / a.steps,
                "note": f"one sscg_solve_host call: b H2D, {a.steps} outer iterations (+ final stopping-test "

@@ -116,6 +116,16 @@ typedef struct {
 SSCG_API sscg_status sscg_partition(int64_t nz, int32_t nranks, int32_t slabs_per_rank, int32_t rank,
                            int64_t *z0, int64_t *nzl);
 
+/* Halo plan of local slab `slab` (0..slabs_per_rank-1) of process `rank`:
+ * out[6] = {peer_lo, send_lo_z, recv_lo_z, peer_hi, send_hi_z, recv_hi_z}
+ * where peer_* is the process that owns the neighbouring slab (-1 at the
+ * global Dirichlet boundary; == rank for an in-process neighbour) and *_z
+ * are GLOBAL plane indices: the interior plane sent to that neighbour and
+ * the plane received into the halo.  One plane per side per basis step
+ * (7/27-point stencils reach one plane).  Pure host arithmetic. */
+SSCG_API sscg_status sscg_halo_plan(int64_t nz, int32_t nranks, int32_t slabs_per_rank, int32_t rank,
+                                    int32_t slab, int64_t *out6);
+
 /* Fill `out` (host, 128 bytes) with a fresh ncclUniqueId.  Needs no GPU. */
 SSCG_API sscg_status sscg_nccl_unique_id(void *out);
 

@@ -28,7 +28,7 @@ OP_STENCIL5_2D, OP_STENCIL7, OP_STENCIL27, OP_VARCOEF7, OP_CSR = range(5)
 INSPECT_P, INSPECT_W, INSPECT_GRAM, INSPECT_D, INSPECT_ALPHA_T, INSPECT_ALPHA, INSPECT_DELTA = range(7)
 SOLVE_X0_ZERO = 1
 
-EXPORTS = ["sscg_partition", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host", "sscg_iterate",
+EXPORTS = ["sscg_partition", "sscg_halo_plan", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host", "sscg_iterate",
            "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect", "sscg_local_shape", "sscg_destroy",
            "sscg_last_error", "sscg_version"]
 PROF_NAMES = ["basis", "gram", "allreduce", "fgs", "update", "halo"]
@@ -76,6 +76,8 @@ def load(path: str = LIB_PATH):
     L = C.CDLL(path)
     vp, i32, i64, d, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_uint32
     L.sscg_partition.argtypes = [i64, i32, i32, i32, C.POINTER(i64), C.POINTER(i64)]
+    L.sscg_halo_plan.argtypes = [i64, i32, i32, i32, i32, C.POINTER(i64)]
+    L.sscg_halo_plan.restype = C.c_int
     L.sscg_nccl_unique_id.argtypes = [vp]
     L.sscg_setup.argtypes = [C.POINTER(_Operator), vp, d, d, i32, i32, C.POINTER(_Comm), vp, C.POINTER(vp)]
     L.sscg_solve.argtypes = [vp, vp, vp, d, i32, u32]
@@ -108,6 +110,15 @@ def partition(nz: int, nranks: int, slabs_per_rank: int, rank: int) -> tuple[int
     z0, nzl = C.c_int64(), C.c_int64()
     _check(load().sscg_partition(nz, nranks, slabs_per_rank, rank, C.byref(z0), C.byref(nzl)))
     return z0.value, nzl.value
+
+
+def halo_plan(nz: int, nranks: int, slabs_per_rank: int, rank: int, slab: int = 0) -> dict:
+    """sscg_halo_plan: neighbour processes and global plane indices of one
+    local slab's halo exchange (host only)."""
+    out = (C.c_int64 * 6)()
+    _check(load().sscg_halo_plan(nz, nranks, slabs_per_rank, rank, slab, out))
+    return {"peer_lo": out[0], "send_lo_z": out[1], "recv_lo_z": out[2],
+            "peer_hi": out[3], "send_hi_z": out[4], "recv_hi_z": out[5]}
 
 
 def nccl_unique_id() -> bytes:

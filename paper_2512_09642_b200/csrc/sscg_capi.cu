@@ -106,6 +106,24 @@ extern "C" sscg_status sscg_partition(int64_t nz, int32_t nranks, int32_t spr, i
     return SSCG_OK;
 }
 
+extern "C" sscg_status sscg_halo_plan(int64_t nz, int32_t nranks, int32_t spr, int32_t rank, int32_t slab,
+                                      int64_t *out6)
+{
+    if (!out6 || slab < 0 || slab >= spr) return fail(SSCG_ERR_INVALID, "sscg_halo_plan: bad slab");
+    int64_t z0p, nzp;
+    const sscg_status ps = sscg_partition(nz, nranks, spr, rank, &z0p, &nzp);
+    if (ps != SSCG_OK) return ps;
+    const int64_t S = (int64_t)nranks * spr, g = (int64_t)rank * spr + slab;
+    const int64_t z0 = g * nz / S, z1 = (g + 1) * nz / S;   // this slab: [z0, z1)
+    out6[0] = (g > 0) ? (g - 1) / spr : -1;
+    out6[1] = z0;
+    out6[2] = z0 - 1;
+    out6[3] = (g + 1 < S) ? (g + 1) / spr : -1;
+    out6[4] = z1 - 1;
+    out6[5] = z1;
+    return SSCG_OK;
+}
+
 extern "C" sscg_status sscg_nccl_unique_id(void *out)
 {
     if (!out) return fail(SSCG_ERR_INVALID, "null output");
@@ -341,17 +359,21 @@ static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab)
         CU(cudaMemcpyAsync(lo + (int64_t)(nzl + 1) * g.plane, hi + g.plane, pb, cudaMemcpyDeviceToDevice, c->stream));
     }
     if (c->nranks > 1) {
+        // remote neighbours of the first and last local slab (sscg_halo_plan)
+        int64_t lo[6], hi[6];
+        TRY(sscg_halo_plan(c->nz_global, c->nranks, c->spr, c->rank, 0, lo));
+        TRY(sscg_halo_plan(c->nz_global, c->nranks, c->spr, c->rank, L - 1, hi));
         NC(ncclGroupStart());
-        if (c->rank > 0) {
-            double *v = vec_of_slab[0];
-            NC(ncclSend(v + g.plane, (size_t)g.plane, ncclDouble, c->rank - 1, c->comm, c->stream));
-            NC(ncclRecv(v, (size_t)g.plane, ncclDouble, c->rank - 1, c->comm, c->stream));
+        if (lo[0] >= 0 && lo[0] != c->rank) {
+            double *v = vec_of_slab[0];   // send plane lo[1] (local 1), receive plane lo[2] (local 0)
+            NC(ncclSend(v + g.plane, (size_t)g.plane, ncclDouble, (int)lo[0], c->comm, c->stream));
+            NC(ncclRecv(v, (size_t)g.plane, ncclDouble, (int)lo[0], c->comm, c->stream));
         }
-        if (c->rank < c->nranks - 1) {
+        if (hi[3] >= 0 && hi[3] != c->rank) {
             double *v = vec_of_slab[L - 1];
-            const int nzl = c->slabs[L - 1].nzl;
-            NC(ncclSend(v + (int64_t)nzl * g.plane, (size_t)g.plane, ncclDouble, c->rank + 1, c->comm, c->stream));
-            NC(ncclRecv(v + (int64_t)(nzl + 1) * g.plane, (size_t)g.plane, ncclDouble, c->rank + 1, c->comm,
+            const int nzl = c->slabs[L - 1].nzl;   // send plane hi[4] (local nzl), receive hi[5] (nzl+1)
+            NC(ncclSend(v + (int64_t)nzl * g.plane, (size_t)g.plane, ncclDouble, (int)hi[3], c->comm, c->stream));
+            NC(ncclRecv(v + (int64_t)(nzl + 1) * g.plane, (size_t)g.plane, ncclDouble, (int)hi[3], c->comm,
                         c->stream));
         }
         NC(ncclGroupEnd());
