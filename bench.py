@@ -225,18 +225,25 @@ def run_ours(a):
     # r_0 = b and the first basis/Gram (untimed), then W warm-up steps
     x = S.solve(b, rtol=0.0, max_outer=0)
     S.iterate(x, a.warmup)
-    # timed region: exactly K outer iterations, device-timed inside the library
+    # timed region: exactly K outer iterations (CUDA-graph replay), device-timed
+    # inside the library with CUDA events on its stream
     barrier()
-    S.set_profiling(True)
     with Clocks(local) as clk:
         S.iterate(x, a.steps)
         barrier()
     st = S.stats()
-    prof = S.profile()
-    S.set_profiling(False)
     ms = max_over_ranks(dist, st.ms_total)
     value = n_global * a.steps / (ms / 1e3) / 1e9
     launches = st.kernel_launches
+    # second pass of the same K steps with every launch bracketed by events
+    # (per-kernel times for the roofline; plain launches, no graph)
+    barrier()
+    S.set_profiling(True)
+    S.iterate(x, a.steps)
+    barrier()
+    st_prof = S.stats()
+    prof = S.profile()
+    S.set_profiling(False)
 
     # roofline of the dominant kernel (K1: basis step) and the others
     peak, peak_src = peaks()
@@ -249,11 +256,12 @@ def run_ours(a):
         gbs = per_launch / (t_ms / max(cnt, 1) / 1e3) / 1e9 if t_ms > 0 else None
         kern[k] = {"launches": cnt, "ms_per_launch": t_ms / max(cnt, 1), "bytes_per_launch": per_launch,
                    "achieved_gbs": gbs, "frac": (gbs / peak) if gbs else None,
-                   "share_of_step": t_ms / (st.ms_total) if st.ms_total else None}
+                   "share_of_step": t_ms / st_prof.ms_total if st_prof.ms_total else None}
     for k in ("fgs", "allreduce", "halo"):
         t_ms, cnt = prof[k]
         kern[k] = {"launches": cnt, "us_per_launch": 1e3 * t_ms / max(cnt, 1),
-                   "share_of_step": t_ms / st.ms_total if st.ms_total else None}
+                   "share_of_step": t_ms / st_prof.ms_total if st_prof.ms_total else None}
+    kern["profiled_pass_ms_per_step"] = st_prof.ms_total / a.steps
     k1 = kern["basis"]
     cfg = workload(a, world)
     roof = {"bound": "hbm", "kernel": "K1 k1_stencil<7pt> (SpMV + Jacobi + Chebyshev recurrence)",

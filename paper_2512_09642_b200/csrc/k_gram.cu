@@ -305,6 +305,13 @@ bool k2_prepare(const Geo &g, Slab &sl, int s)
 {
     const K2Plan p = plan(s);
     const int64_t N = (int64_t)sl.nzl * g.plane;
+    // opt in to the large dynamic shared memory once (outside any graph capture)
+    const int mx = 210 * 1024;   // >= every plan's ring (<= 200 KB) + static smem fits 227 KB
+    if (cudaFuncSetAttribute(k2_gram<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+        cudaFuncSetAttribute(k2_gram<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+        cudaFuncSetAttribute(k2_gram<8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+        cudaFuncSetAttribute(k2_gram<8, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess)
+        return false;
     return encode_rows_map(&sl.tmP, sl.P + g.plane, N, s, g.vstride, p.E, p.s_pad) &&
            encode_rows_map(&sl.tmW, sl.W + g.plane, N, s, g.vstride, p.E, p.s_pad);
 }
@@ -313,7 +320,6 @@ template <int TB, int E>
 static void launch_t(const CUtensorMap &a, const CUtensorMap &b, const K2Params &k, const K2Plan &p, dim3 grid,
                      const DevState *st, cudaStream_t stream)
 {
-    cudaFuncSetAttribute(k2_gram<TB, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
     k2_gram<TB, E><<<grid, p.threads, p.smem, stream>>>(a, b, k, st);
 }
 

@@ -86,6 +86,11 @@ struct sscg_ctx {
     std::vector<int> prof_cat;
     size_t prof_used = 0;
     sscg_profile_t prof{};
+    // CUDA graph of one outer iteration
+    bool use_graph = true;
+    cudaGraphExec_t gexec = nullptr;
+    double *graph_x = nullptr;
+    int64_t graph_launches = 0, graph_allreduces = 0;
 };
 
 static const char *kVersion = "sscg-b200 0.1 (sm_100a)";
@@ -235,6 +240,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
     }
+    if (const char *e = getenv("SSCG_NO_GRAPH")) c->use_graph = (e[0] == '0');
     CU(cudaEventCreate(&c->ev0));
     CU(cudaEventCreate(&c->ev1));
     CU(cudaMallocHost(&c->st_host, sizeof(DevState)));
@@ -335,6 +341,7 @@ extern "C" void sscg_destroy(sscg_ctx *c)
     if (c->st_host) cudaFreeHost(c->st_host);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto &e : c->prof_events) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -490,9 +497,53 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     return SSCG_OK;
 }
 
+// One outer iteration as a CUDA graph (captured once per x pointer): the
+// s + 3 launches (+ NCCL calls) replay with one cudaGraphLaunch, which removes
+// the per-kernel host launch cost that dominates small problems (cfg 1/2).
+// Profiling runs use plain launches so every kernel can be bracketed.
+static sscg_status run_outer(sscg_ctx *c, double *x)
+{
+    if (c->prof_on || !c->use_graph) return enqueue_outer(c, x);
+    if (!c->gexec || c->graph_x != x) {
+        if (c->gexec) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        const int64_t l0 = c->launches, a0 = c->allreduces;
+        cudaGraph_t graph = nullptr;
+        CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+        const sscg_status st = enqueue_outer(c, x);
+        const cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+        if (st != SSCG_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (e != cudaSuccess) return fail(SSCG_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+        const cudaError_t e2 = cudaGraphInstantiate(&c->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e2 != cudaSuccess) {
+            c->gexec = nullptr;
+            return fail(SSCG_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e2));
+        }
+        c->graph_launches = c->launches - l0;
+        c->graph_allreduces = c->allreduces - a0;
+        c->launches = l0;
+        c->allreduces = a0;
+        c->graph_x = x;
+    }
+    CU(cudaGraphLaunch(c->gexec, c->stream));
+    c->launches += c->graph_launches;
+    c->allreduces += c->graph_allreduces;
+    return SSCG_OK;
+}
+
 static sscg_status ensure_history(sscg_ctx *c, int cap)
 {
     if (cap <= c->hist_cap) return SSCG_OK;
+    if (c->gexec) {   // the captured K4 holds the old history pointers
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
     const int s = c->s, nent = s * s + s;
     TRY(dalloc(c, &c->h_gram, (size_t)cap * nent));
     TRY(dalloc(c, &c->h_d, (size_t)cap * s));
@@ -560,7 +611,7 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
     int chunk = 2;
     while (issued < max_outer + 1) {
         const int n = std::min(chunk, max_outer + 1 - issued);
-        for (int i = 0; i < n; ++i) TRY(enqueue_outer(c, x));
+        for (int i = 0; i < n; ++i) TRY(run_outer(c, x));
         issued += n;
         CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
@@ -691,7 +742,7 @@ extern "C" sscg_status sscg_iterate(sscg_ctx *c, double *x, int32_t nsteps)
     *c->st_host = h;
     CU(cudaEventRecord(c->ev0, c->stream));
     CU(cudaMemcpyAsync(c->st, c->st_host, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
-    for (int i = 0; i < nsteps; ++i) TRY(enqueue_outer(c, x));
+    for (int i = 0; i < nsteps; ++i) TRY(run_outer(c, x));
     CU(cudaEventRecord(c->ev1, c->stream));
     CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
