@@ -15,6 +15,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "sscg_internal.cuh"
 #include "tma.cuh"
 
@@ -50,10 +52,11 @@ __global__ void __launch_bounds__(256, 1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ncw = k.roles_cta * k.nsl;            // consumer warps
 
+    // chunks are dealt round-robin (chunk = blockIdx.x + it * gridDim.x): at any
+    // moment the grid reads one contiguous ~gridDim.x*E*8-byte window of each
+    // column, which keeps HBM streaming at full rate also for small vectors
     const int64_t nchunks = (k.N + E - 1) / E;
-    const int64_t c_lo = nchunks * blockIdx.x / gridDim.x;
-    const int64_t c_hi = nchunks * (blockIdx.x + 1) / gridDim.x;
-    const int nit = (int)(c_hi - c_lo);
+    const int nit = (int)((nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x);
 
     if (tid == 0) {
         for (int i = 0; i < NS; ++i) {
@@ -93,17 +96,21 @@ __global__ void __launch_bounds__(256, 1)
 
     if (warp == 0) {
         // ---------------- producer ----------------
-        if (lane == 0) {
-            const uint32_t bytes = (uint32_t)stage_elems * 8u;
-            for (int it = 0; it < nit; ++it) {
+        // the whole warp walks the loop (lane 0 issues) so that warp 0 is
+        // converged when it reaches the shuffles and the CTA barrier below: a
+        // diverged warp 0 there cost ~80 us per launch (measured with %globaltimer)
+        const uint32_t bytes = (uint32_t)stage_elems * 8u;
+        for (int it = 0; it < nit; ++it) {
+            if (lane == 0) {
                 const int stg = it % NS;
                 if (it >= NS) mbar_wait(&empty[stg], (uint32_t)((it / NS - 1) & 1));
                 double *dst = smem + (size_t)stg * stage_elems;
-                const int x = (int)((c_lo + it) * E);
+                const int x = (int)((blockIdx.x + (int64_t)it * gridDim.x) * E);
                 mbar_expect_tx(&full[stg], bytes);
                 tma_load_2d(dst, &tmP, x, 0, &full[stg]);
                 tma_load_2d(dst + k.s_pad * E, &tmW, x, 0, &full[stg]);
             }
+            __syncwarp();
         }
     } else if (consumer) {
         // ---------------- consumers ----------------
@@ -242,6 +249,10 @@ K2Plan plan(int s)
     K2Plan p;
     p.TB = (s <= 8) ? 4 : 8;
     p.E = (s <= 16) ? 256 : (s <= 32 ? 128 : 64);
+    if (const char *e = getenv("SSCG_K2_E")) {   // tuning override (64 / 128 / 256)
+        const int v = atoi(e);
+        if ((v == 64 || v == 128 || v == 256) && (s > 8)) p.E = v;
+    }
     p.s_pad = (s + p.TB - 1) / p.TB * p.TB;
     p.nb = p.s_pad / p.TB;
     p.nroles = p.nb * (p.nb + 1) / 2;
@@ -251,6 +262,7 @@ K2Plan plan(int s)
     while (p.roles_cta * p.nsl * 2 <= 7) p.nsl *= 2;
     const size_t stage = (size_t)2 * p.s_pad * p.E * sizeof(double);
     p.nstage = (int)std::min<size_t>(MAX_STAGE, (200 * 1024) / stage);
+    if (const char *e = getenv("SSCG_K2_NS")) p.nstage = std::max(2, std::min(p.nstage, atoi(e)));
     p.smem = stage * p.nstage;
     p.threads = 32 * (1 + p.roles_cta * p.nsl);
     return p;
@@ -341,6 +353,7 @@ void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *
     k.ticket = sl.ticket;
     const int64_t nchunks = (k.N + p.E - 1) / p.E;
     int gx = k2_grid();
+    if (const char *e = getenv("SSCG_K2_GRID")) gx = std::max(1, std::min(gx, atoi(e)));   // tuning
     if (nchunks < gx) gx = (int)nchunks;
     dim3 grid(gx, p.gy);
     if (p.TB == 4) launch_t<4, 256>(sl.tmP, sl.tmW, k, p, grid, st, stream);

@@ -259,6 +259,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         c->slabs.push_back(sl);
     }
     g.vstride = ((int64_t)(max_nzl + 2) * g.plane + 31) / 32 * 32;   // 256-B aligned vectors
+    if (getenv("SSCG_VPAD") && (g.vstride / 32) % 2 == 0) g.vstride += 32;   // odd multiple of 256 B
     const int nent = s * s + s;
     const int64_t npart = (int64_t)k2_grid() * 8 * nent;
     for (auto &sl : c->slabs) {
@@ -461,6 +462,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     for (auto &sl : c->slabs) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
         launch_k2(g, sl, s, c->st, L == 1 ? c->blk : sl.blk, c->stream);
+        if (getenv("SSCG_K2_TWICE")) launch_k2(g, sl, s, c->st, L == 1 ? c->blk : sl.blk, c->stream);   // debug
         TRY(prof_mark(c, SSCG_PROF_GRAM, false));
         ++c->launches;
     }
