@@ -203,9 +203,10 @@ class Solver:
         self.z0, self.nz_local, self.n_local = z0.value, nzp.value, nloc.value
 
     def close(self):
-        if getattr(self, "_h", None):
-            load().sscg_destroy(self._h)
-            self._h = None
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.sscg_destroy(h)
+        self._h = None
 
     __del__ = close
 
@@ -225,6 +226,9 @@ class Solver:
             x = torch.empty_like(b)
             flags = SOLVE_X0_ZERO
         assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous() and x.numel() == self.n_local
+        cur = torch.cuda.current_stream()
+        if cur.cuda_stream != 0:      # the library stream orders only after the legacy default stream
+            cur.synchronize()
         code = load().sscg_solve(self._h, _ptr(b), _ptr(x), rtol, max_outer, flags)
         if code in (ERR_BREAKDOWN, ERR_NONFINITE) and not raise_on_breakdown:
             return x

@@ -237,7 +237,10 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
     if (stream) {
         c->stream = static_cast<cudaStream_t>(stream);
     } else {
-        CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        // a BLOCKING stream: it orders after the caller's work on the legacy
+        // default stream (e.g. torch producing b), so inputs are complete
+        // before the first kernel reads them
+        CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamDefault));
         c->own_stream = true;
     }
     if (const char *e = getenv("SSCG_NO_GRAPH")) c->use_graph = (e[0] == '0');
