@@ -212,13 +212,16 @@ void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
 }
 
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *x_slab, const DevState *st,
-               cudaStream_t stream)
+               cudaStream_t stream, int zb, int ze)
 {
+    if (ze < 0) ze = sl.nzl + 1;
+    if (ze <= zb) return;
     K5Params k;
-    k.P = sl.P + g.plane;
-    k.W = sl.W + g.plane;
+    k.P = sl.P + (int64_t)zb * g.plane;
+    k.W = sl.W + (int64_t)zb * g.plane;
     k.vstride = g.vstride;
-    k.N = (int64_t)sl.nzl * g.plane;
+    k.N = (int64_t)(ze - zb) * g.plane;
+    x_slab += (int64_t)(zb - 1) * g.nx * g.ny;
     k.s = s;
     k.alpha = alpha;
     k.x = x_slab;

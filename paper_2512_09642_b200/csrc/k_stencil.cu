@@ -31,7 +31,7 @@ constexpr int BX = 32, BY = 8, CTAS_PER_SM = 8;
 __device__ __forceinline__ double ld(const double *p) { return __ldg(p); }
 
 struct K1Work {
-    int tiles_x, tiles_y, zc, nchunks;
+    int tiles_x, tiles_y, zc, nchunks, nch1;
     int64_t nitems;
 };
 
@@ -56,8 +56,14 @@ __global__ void __launch_bounds__(BX *BY, (KIND == 0 || KIND == 1) ? 8 : 5)
         const int ty = tile / wk.tiles_x, tx = tile - ty * wk.tiles_x;
         const int x = tx * BX + threadIdx.x;
         const int y = ty * BY + threadIdx.y;
-        const int z_lo = a.zb + chunk * wk.zc;
-        const int z_hi = min(a.ze, z_lo + wk.zc);
+        int z_lo, z_hi;   // chunk -> planes: range 1 [zb, ze), then range 2 [zb2, ze2)
+        if (chunk < wk.nch1) {
+            z_lo = a.zb + chunk * wk.zc;
+            z_hi = min(a.ze, z_lo + wk.zc);
+        } else {
+            z_lo = a.zb2 + (chunk - wk.nch1) * wk.zc;
+            z_hi = min(a.ze2, z_lo + wk.zc);
+        }
         if (x >= g.nx || y >= g.ny) continue;
         const bool xm = x > 0, xp = x + 1 < g.nx, ym = y > 0, yp = y + 1 < g.ny;
         int64_t i = (int64_t)z_lo * pl + (int64_t)y * pitch + x;
@@ -185,8 +191,14 @@ __global__ void __launch_bounds__(BX *BY, 4) k1_lap_vec(Geo g, K1Args a, const D
         const int ty = tile / wk.tiles_x, tx = tile - ty * wk.tiles_x;
         const int x = (tx * BX + lane) * 2;          // first of the pair
         const int y = ty * BY + threadIdx.y;
-        const int z_lo = a.zb + chunk * wk.zc;
-        const int z_hi = min(a.ze, z_lo + wk.zc);
+        int z_lo, z_hi;   // chunk -> planes: range 1 [zb, ze), then range 2 [zb2, ze2)
+        if (chunk < wk.nch1) {
+            z_lo = a.zb + chunk * wk.zc;
+            z_hi = min(a.ze, z_lo + wk.zc);
+        } else {
+            z_lo = a.zb2 + (chunk - wk.nch1) * wk.zc;
+            z_hi = min(a.ze2, z_lo + wk.zc);
+        }
         if (y >= g.ny) continue;                      // whole warp (same y)
         const bool in = x < g.nx;                     // pair starts inside the row
         const bool in1 = x + 1 < g.nx;                // second point inside
@@ -319,7 +331,8 @@ void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s
         k1_csr<<<(unsigned)blocks, 256, 0, s>>>(g, a, st);
         return;
     }
-    const int nplanes = a.ze - a.zb;
+    const int n1 = std::max(0, a.ze - a.zb), n2 = std::max(0, a.ze2 - a.zb2);
+    const int nplanes = n1 + n2;
     if (nplanes <= 0) return;
     K1Work wk;
     const bool vec = g.kind <= 1;            // 5-/7-point: two points per thread
@@ -335,13 +348,15 @@ void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s
             occ[g.kind] <= 0)
             occ[g.kind] = CTAS_PER_SM;
     }
-    const int64_t resident = (int64_t)k2_grid() * occ[g.kind];
+    const int sms = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
+    const int64_t resident = (int64_t)sms * occ[g.kind];
     // z-chunks of 16 planes by default (2-plane warm-up amortised); shorter
     // when that leaves fewer than 4 work items per resident CTA
-    int zc = std::min(nplanes, 16);
+    int zc = std::min(std::max(n1, n2), 16);
     while (zc > 2 && tiles * ((nplanes + zc - 1) / zc) < 4 * resident) zc = (zc + 1) / 2;
     wk.zc = zc;
-    wk.nchunks = (nplanes + zc - 1) / zc;
+    wk.nch1 = (n1 + zc - 1) / zc;
+    wk.nchunks = wk.nch1 + (n2 + zc - 1) / zc;
     wk.nitems = tiles * wk.nchunks;
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
     dim3 block(BX, BY);

@@ -72,6 +72,13 @@ struct sscg_ctx {
     std::vector<double> relres_host, delta_host;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // halo overlap: boundary planes first, then the exchange of
+    // the next basis vector's boundary planes on `cstream` while the interior
+    // planes run on `stream`
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool overlap = true;
+    int k1_sm_cap = 0;
     ncclComm_t comm = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double *bbuf = nullptr, *xbuf = nullptr;   // device buffers of sscg_solve_host
@@ -244,6 +251,14 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         c->own_stream = true;
     }
     if (const char *e = getenv("SSCG_NO_GRAPH")) c->use_graph = (e[0] == '0');
+    if (const char *e = getenv("SSCG_NO_OVERLAP")) c->overlap = (e[0] == '0');
+    {
+        int lo = 0, hi = 0;
+        CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CU(cudaStreamCreateWithPriority(&c->cstream, cudaStreamNonBlocking, hi));
+        CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
     CU(cudaEventCreate(&c->ev0));
     CU(cudaEventCreate(&c->ev1));
     CU(cudaMallocHost(&c->st_host, sizeof(DevState)));
@@ -307,6 +322,9 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
     }
     TRY(dalloc(c, &c->scratch, (size_t)c->n_local));
     if (c->nranks > 1) {
+        // interior K1 launches leave two SMs free so the NCCL send/recv kernels
+        // of the overlapped halo exchange can be scheduled next to them
+        c->k1_sm_cap = k2_grid() - 2;
         if (!cm->nccl_id) return fail(SSCG_ERR_INVALID, "nranks > 1 needs nccl_id");
         ncclUniqueId id;
         memcpy(&id, cm->nccl_id, sizeof id);
@@ -350,13 +368,16 @@ extern "C" void sscg_destroy(sscg_ctx *c)
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
 
 // ---------------------------------------------------------------------------
 // halo exchange of basis vector j (one plane per side)
-static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab)
+static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab, cudaStream_t strm)
 {
     const Geo &g = c->g;
     if (g.kind == SSCG_OP_CSR) return SSCG_OK;
@@ -366,8 +387,8 @@ static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab)
     for (int l = 0; l + 1 < L; ++l) {
         double *lo = vec_of_slab[l], *hi = vec_of_slab[l + 1];
         const int nzl = c->slabs[l].nzl;
-        CU(cudaMemcpyAsync(hi, lo + (int64_t)nzl * g.plane, pb, cudaMemcpyDeviceToDevice, c->stream));
-        CU(cudaMemcpyAsync(lo + (int64_t)(nzl + 1) * g.plane, hi + g.plane, pb, cudaMemcpyDeviceToDevice, c->stream));
+        CU(cudaMemcpyAsync(hi, lo + (int64_t)nzl * g.plane, pb, cudaMemcpyDeviceToDevice, strm));
+        CU(cudaMemcpyAsync(lo + (int64_t)(nzl + 1) * g.plane, hi + g.plane, pb, cudaMemcpyDeviceToDevice, strm));
     }
     if (c->nranks > 1) {
         // remote neighbours of the first and last local slab (sscg_halo_plan)
@@ -377,15 +398,15 @@ static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab)
         NC(ncclGroupStart());
         if (lo[0] >= 0 && lo[0] != c->rank) {
             double *v = vec_of_slab[0];   // send plane lo[1] (local 1), receive plane lo[2] (local 0)
-            NC(ncclSend(v + g.plane, (size_t)g.plane, ncclDouble, (int)lo[0], c->comm, c->stream));
-            NC(ncclRecv(v, (size_t)g.plane, ncclDouble, (int)lo[0], c->comm, c->stream));
+            NC(ncclSend(v + g.plane, (size_t)g.plane, ncclDouble, (int)lo[0], c->comm, strm));
+            NC(ncclRecv(v, (size_t)g.plane, ncclDouble, (int)lo[0], c->comm, strm));
         }
         if (hi[3] >= 0 && hi[3] != c->rank) {
             double *v = vec_of_slab[L - 1];
             const int nzl = c->slabs[L - 1].nzl;   // send plane hi[4] (local nzl), receive hi[5] (nzl+1)
-            NC(ncclSend(v + (int64_t)nzl * g.plane, (size_t)g.plane, ncclDouble, (int)hi[3], c->comm, c->stream));
+            NC(ncclSend(v + (int64_t)nzl * g.plane, (size_t)g.plane, ncclDouble, (int)hi[3], c->comm, strm));
             NC(ncclRecv(v + (int64_t)(nzl + 1) * g.plane, (size_t)g.plane, ncclDouble, (int)hi[3], c->comm,
-                        c->stream));
+                        strm));
         }
         NC(ncclGroupEnd());
     }
@@ -393,8 +414,9 @@ static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab)
 }
 
 // profiling: CUDA event pairs around launch groups, resolved on demand
-static sscg_status prof_mark(sscg_ctx *c, int cat, bool begin)
+static sscg_status prof_mark(sscg_ctx *c, int cat, bool begin, cudaStream_t strm = nullptr)
 {
+    if (!strm) strm = c->stream;
     if (!c->prof_on) return SSCG_OK;
     if (begin) {
         if (c->prof_used == c->prof_events.size()) {
@@ -405,9 +427,9 @@ static sscg_status prof_mark(sscg_ctx *c, int cat, bool begin)
             c->prof_cat.push_back(cat);
         }
         c->prof_cat[c->prof_used] = cat;
-        CU(cudaEventRecord(c->prof_events[c->prof_used].first, c->stream));
+        CU(cudaEventRecord(c->prof_events[c->prof_used].first, strm));
     } else {
-        CU(cudaEventRecord(c->prof_events[c->prof_used].second, c->stream));
+        CU(cudaEventRecord(c->prof_events[c->prof_used].second, strm));
         ++c->prof_used;
     }
     return SSCG_OK;
@@ -427,45 +449,96 @@ static sscg_status prof_resolve(sscg_ctx *c)
     return SSCG_OK;
 }
 
+// halo of basis column j of every local slab; with overlap the exchange runs
+// on the comm stream after the work already enqueued on the solver stream
+// (fork) and `ev_join` marks its completion
+static sscg_status halo_fork(sscg_ctx *c, int j, bool fork)
+{
+    const int L = (int)c->slabs.size();
+    std::vector<double *> vj(L);
+    for (int l = 0; l < L; ++l) vj[l] = c->slabs[l].P + (int64_t)j * c->g.vstride;
+    cudaStream_t strm = fork ? c->cstream : c->stream;
+    if (fork) {
+        CU(cudaEventRecord(c->ev_fork, c->stream));
+        CU(cudaStreamWaitEvent(c->cstream, c->ev_fork, 0));
+    }
+    TRY(prof_mark(c, SSCG_PROF_HALO, true, strm));
+    TRY(exchange(c, vj.data(), strm));
+    TRY(prof_mark(c, SSCG_PROF_HALO, false, strm));
+    if (fork) CU(cudaEventRecord(c->ev_join, c->cstream));
+    return SSCG_OK;
+}
+
+static sscg_status halo_join(sscg_ctx *c)
+{
+    CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    return SSCG_OK;
+}
+
+// K1 for step j over the planes of every local slab selected by `part`:
+//   0 = all planes, 1 = the two boundary planes (1 and nzl), 2 = the interior
+//   planes [2, nzl) that do not read a halo plane
+static sscg_status launch_basis(sscg_ctx *c, int j, int part)
+{
+    const Geo &g = c->g;
+    const int s = c->s;
+    for (auto &sl : c->slabs) {
+        K1Args a{};
+        a.p = sl.P + (int64_t)j * g.vstride;
+        a.pm = (j > 0) ? sl.P + (int64_t)(j - 1) * g.vstride : nullptr;
+        a.w = sl.W + (int64_t)j * g.vstride;
+        a.pn = (j < s - 1) ? sl.P + (int64_t)(j + 1) * g.vstride : nullptr;
+        a.kx = sl.kx; a.ky = sl.ky; a.kz = sl.kz;
+        a.dinv = sl.dinv;
+        a.dinv_c = g.dinv_c;
+        a.sigma = c->sigma;
+        a.coef = (j == 0) ? c->theta : 2.0 * c->theta;
+        a.mode = (j == s - 1) ? 0 : (j == 0 ? 1 : 2);
+        a.nzl = sl.nzl;
+        if (part == 0) {
+            a.zb = 1; a.ze = sl.nzl + 1;
+        } else if (part == 1) {
+            a.zb = 1; a.ze = 2;
+            a.zb2 = std::max(2, sl.nzl); a.ze2 = sl.nzl + 1;
+        } else {
+            a.zb = 2; a.ze = sl.nzl;
+            a.sm_cap = c->k1_sm_cap;
+            if (a.ze <= a.zb) continue;
+        }
+        TRY(prof_mark(c, SSCG_PROF_BASIS, true));
+        launch_k1(g, a, c->st, c->stream);
+        TRY(prof_mark(c, SSCG_PROF_BASIS, false));
+        ++c->launches;
+    }
+    return SSCG_OK;
+}
+
+// One outer iteration.  Precondition: the halo planes of p_0 are current.
+//   for j: K1 boundary planes -> fork halo(p_{j+1}) -> K1 interior -> join
+//   K2 (+ slab sum) -> allreduce -> K4 -> K5 boundary -> fork halo(p_0) -> K5 interior -> join
 static sscg_status enqueue_outer(sscg_ctx *c, double *x)
 {
     const Geo &g = c->g;
     const int s = c->s;
     const int L = (int)c->slabs.size();
-    std::vector<double *> vj(L);
     const bool halo = (L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR;
+    const bool ovl = halo && c->overlap;
     for (int j = 0; j < s; ++j) {
-        for (int l = 0; l < L; ++l) vj[l] = c->slabs[l].P + (int64_t)j * g.vstride;
-        if (halo) {
-            TRY(prof_mark(c, SSCG_PROF_HALO, true));
-            TRY(exchange(c, vj.data()));
-            TRY(prof_mark(c, SSCG_PROF_HALO, false));
-        }
-        for (auto &sl : c->slabs) {
-            K1Args a{};
-            a.p = sl.P + (int64_t)j * g.vstride;
-            a.pm = (j > 0) ? sl.P + (int64_t)(j - 1) * g.vstride : nullptr;
-            a.w = sl.W + (int64_t)j * g.vstride;
-            a.pn = (j < s - 1) ? sl.P + (int64_t)(j + 1) * g.vstride : nullptr;
-            a.kx = sl.kx; a.ky = sl.ky; a.kz = sl.kz;
-            a.dinv = sl.dinv;
-            a.dinv_c = g.dinv_c;
-            a.sigma = c->sigma;
-            a.coef = (j == 0) ? c->theta : 2.0 * c->theta;
-            a.mode = (j == s - 1) ? 0 : (j == 0 ? 1 : 2);
-            a.zb = 1;
-            a.ze = sl.nzl + 1;
-            a.nzl = sl.nzl;
-            TRY(prof_mark(c, SSCG_PROF_BASIS, true));
-            launch_k1(g, a, c->st, c->stream);
-            TRY(prof_mark(c, SSCG_PROF_BASIS, false));
-            ++c->launches;
+        if (!halo) {
+            TRY(launch_basis(c, j, 0));
+        } else if (!ovl) {
+            if (j > 0) TRY(halo_fork(c, j, false));
+            TRY(launch_basis(c, j, 0));
+        } else {
+            TRY(launch_basis(c, j, 1));
+            if (j < s - 1) TRY(halo_fork(c, j + 1, true));
+            TRY(launch_basis(c, j, 2));
+            if (j < s - 1) TRY(halo_join(c));
         }
     }
     for (auto &sl : c->slabs) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
         launch_k2(g, sl, s, c->st, L == 1 ? c->blk : sl.blk, c->stream);
-        if (getenv("SSCG_K2_TWICE")) launch_k2(g, sl, s, c->st, L == 1 ? c->blk : sl.blk, c->stream);   // debug
         TRY(prof_mark(c, SSCG_PROF_GRAM, false));
         ++c->launches;
     }
@@ -492,11 +565,39 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     launch_k4(a4, c->st, c->stream);
     TRY(prof_mark(c, SSCG_PROF_FGS, false));
     ++c->launches;
-    for (auto &sl : c->slabs) {
-        TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
-        launch_k5(g, sl, s, c->alpha, x + sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream);
-        TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
-        ++c->launches;
+    auto k5 = [&](int zb, int ze) -> sscg_status {
+        for (auto &sl : c->slabs) {
+            const int e = (ze == -1) ? sl.nzl + 1 : (ze == -2) ? sl.nzl : std::min(ze, sl.nzl + 1);
+            const int b = std::max(zb, 1);
+            if (e <= b) continue;
+            TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
+            launch_k5(g, sl, s, c->alpha, x + sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, b, e);
+            TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
+            ++c->launches;
+        }
+        return SSCG_OK;
+    };
+    if (!halo) {
+        TRY(k5(1, -1));
+    } else if (!ovl) {
+        TRY(k5(1, -1));
+        TRY(halo_fork(c, 0, false));
+    } else {
+        // boundary planes of r_{k+1} (= p_0 of the next outer) first, their
+        // exchange overlapping the interior update
+        for (auto &sl : c->slabs) {
+            const int top = std::max(2, sl.nzl);
+            for (int zb : {1, top}) {
+                if (zb > sl.nzl) continue;
+                TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
+                launch_k5(g, sl, s, c->alpha, x + sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, zb, zb + 1);
+                TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
+                ++c->launches;
+            }
+        }
+        TRY(halo_fork(c, 0, true));
+        TRY(k5(2, -2));
+        TRY(halo_join(c));
     }
     CU(cudaGetLastError());
     return SSCG_OK;
@@ -594,7 +695,7 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
             ++c->launches;
             w0[l] = sl.W;
         }
-        TRY(exchange(c, w0.data()));
+        TRY(exchange(c, w0.data(), c->stream));
         for (auto &sl : c->slabs) {
             K1Args a{};
             a.p = sl.W;
@@ -611,6 +712,8 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
             ++c->launches;
         }
     }
+    // halo planes of p_0 = r_0 (enqueue_outer's precondition)
+    if ((L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR) TRY(halo_fork(c, 0, false));
     // outer iterations in chunks; the device decides when to stop
     int issued = 0;
     int chunk = 2;

@@ -75,6 +75,8 @@ struct K1Args {
     double dinv_c;
     double coef, sigma;
     int zb, ze;            // padded plane indices (1..nzl)
+    int zb2, ze2;          // optional second plane range (boundary launches), empty if ze2 <= zb2
+    int sm_cap;            // > 0: use at most this many SMs (leave room for NCCL kernels)
     int mode;
     int nzl;
 };
@@ -107,8 +109,8 @@ struct K4Args {
 };
 void launch_k4(const K4Args &a, DevState *st, cudaStream_t s);
 
-// K5: x += P alpha;  p_0 -= W alpha
+// K5: x += P alpha;  p_0 -= W alpha over padded planes [zb, ze) (ze < 0: to nzl+1)
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *x_slab,
-               const DevState *st, cudaStream_t stream);
+               const DevState *st, cudaStream_t stream, int zb = 1, int ze = -1);
 
 }  // namespace sscg
