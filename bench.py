@@ -27,6 +27,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+K1_NAME = "k1_lap_vec"   # dominant kernel (basis step) as named in the ncu capture
 METRIC = "s-step CG time/outer-iter & GDOF/s at 1/2/4/8 B200; % of HBM peak"
 UNIT = "GDOF/s"
 
@@ -170,19 +171,23 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfgkey):
-    """dram bytes per launch of the dominant kernel from the committed ncu
-    capture of this workload (profiles/*ncu_summary.json), else None."""
+def ncu_traffic(n, kernel_prefix):
+    """dram bytes (read + write) per launch of the dominant kernel from the
+    latest committed `ncu --set full` capture of this workload
+    (profiles/r*_ncu_full_<n>.json, written by tools/ncu_raw_summary.py), else
+    None.  The capture is of the same bench command (one launch)."""
     import glob
-    best = None
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_summary.json"))):
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_%d.json" % n)), reverse=True):
         try:
             d = json.load(open(f))
-            if d.get("config") == cfgkey and "k1_dram_bytes_per_launch" in d:
-                best = d
         except Exception:
-            pass
-    return None if best is None else best["k1_dram_bytes_per_launch"]
+            continue
+        for name, rec in d.items():
+            if name.startswith(kernel_prefix):
+                rd, wr = rec["dram__bytes_read.sum"], rec["dram__bytes_write.sum"]
+                return rd[0] * scale.get(rd[1], 1.0) + wr[0] * scale.get(wr[1], 1.0)
+    return None
 
 
 def run_ours(a):
@@ -264,9 +269,10 @@ def run_ours(a):
     kern["profiled_pass_ms_per_step"] = st_prof.ms_total / a.steps
     k1 = kern["basis"]
     cfg = workload(a, world)
-    roof = {"bound": "hbm", "kernel": "K1 k1_stencil<7pt> (SpMV + Jacobi + Chebyshev recurrence)",
+    roof = {"bound": "hbm", "kernel": "K1 %s<7pt> (SpMV + Jacobi + Chebyshev recurrence)" % K1_NAME,
             "achieved": k1["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": k1["frac"],
-            "traffic": ncu_traffic("cfg5-%d-s%d" % (n, s)), "peak_source": peak_src,
+            "traffic": ncu_traffic(n, K1_NAME), "peak_source": peak_src,
+            "traffic_note": "ncu dram read+write of one j>=1 launch (algorithmic: 4 vectors = %.4g B)" % (4 * vec),
             "bytes_rule": "(4s-3) FP64 vectors per outer / s launches (SURVEY 8(d))",
             "path_bytes_per_step": 64.0 * s * n_local,
             "path_achieved_gbs": 64.0 * s * n_local / (st.ms_total / a.steps / 1e3) / 1e9,
