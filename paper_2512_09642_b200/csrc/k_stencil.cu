@@ -331,6 +331,10 @@ void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s
         k1_csr<<<(unsigned)blocks, 256, 0, s>>>(g, a, st);
         return;
     }
+    if (k1t_supported(g, a)) {
+        launch_k1t(g, a, st, s);
+        return;
+    }
     const int n1 = std::max(0, a.ze - a.zb), n2 = std::max(0, a.ze2 - a.zb2);
     const int nplanes = n1 + n2;
     if (nplanes <= 0) return;

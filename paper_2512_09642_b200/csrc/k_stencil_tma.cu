@@ -1,0 +1,381 @@
+// K1T -- TMA-staged basis step for the constant-coefficient 3D stencils
+// (7-point, 27-point): the same operation as K1 (§2 Def.
+// Chebyshev Polynomial Basis)
+//   w_j     = A p_j
+//   p_{j+1} = coef * (M^{-1} w_j - sigma p_j) [- p_{j-1}]
+// with the planes of p_j and p_{j-1} brought into shared memory by the
+// tensor-memory accelerator instead of per-thread loads.
+//
+// Work: tiles of TX x TY points in (x, y) times z-chunks of ZC planes,
+// chunk-major (all tiles of one chunk run at the same time, so the x/y halo
+// cells and the chunk-boundary planes that neighbouring tiles also read are
+// L2 hits), walked by a persistent grid.
+//
+// Per CTA: warp 0 is the producer -- one lane issues, per plane z, a 4-D
+// `cp.async.bulk.tensor` box of p_j covering the tile plus a 2-cell x halo
+// and a 1-row y halo (global-boundary cells come back zero: the TMA unit's
+// out-of-bounds fill is the Dirichlet ghost), and a box of p_{j-1} covering
+// the tile, into two rings of NSP / NSM slots guarded by full/empty
+// mbarriers.  It runs up to NSP-2 planes ahead of the consumers, across item
+// boundaries, so every SM keeps ~100 KB of HBM reads in flight without
+// spending registers on it.  Warps 1..8 are consumers: warp w owns tile rows
+// 2w and 2w+1, lane l the x pair (2l, 2l+1); the z-neighbours (7-point) or
+// the 3x3 in-plane box sums (27-point, A p = 27 p - box3x3x3(p)) slide
+// through registers, the x/y neighbours are read from the staged plane.
+// w_j and p_{j+1} are written with 16-byte stores straight from registers.
+//
+// Bytes per launch: p_j, p_{j-1} read, w_j, p_{j+1} written (4 vectors at
+// 1 <= j < s-1).
+#include <algorithm>
+#include <cstdlib>
+
+#include "sscg_internal.cuh"
+#include "tma.cuh"
+
+namespace sscg {
+namespace {
+
+constexpr int TX = 64, TY = 16;
+constexpr int BW = TX + 4, BH = TY + 2;                       // p box: x in [x0-2, x0+TX+2), y in [y0-1, y0+TY+1)
+constexpr int PSLOT = ((BW * BH * 8 + 127) / 128) * 128 / 8;  // doubles per p slot (128-B aligned)
+constexpr int MSLOT = TX * TY;                                // doubles per p_{j-1} slot
+constexpr int NSP = 6, NSM = 4;
+constexpr int NCW = TY / 2;                                   // consumer warps (2 rows each)
+constexpr int THREADS = 32 * (NCW + 1);
+constexpr uint32_t PBYTES = BW * BH * 8, MBYTES = TX * TY * 8;
+constexpr size_t SMEM = (size_t)(NSP * PSLOT + NSM * MSLOT) * sizeof(double);
+
+struct K1TWork {
+    int tiles_x, tiles_y, zc, nch1;
+    int64_t nitems;
+    int zb, ze, zb2, ze2;
+    int j;
+};
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int x, int y, int z, int v,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(v), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+
+__device__ __forceinline__ void item_planes(const K1TWork &wk, int64_t item, int ntiles, int &tx, int &ty, int &zlo,
+                                            int &zhi)
+{
+    const int chunk = (int)(item / ntiles);
+    const int tile = (int)(item - (int64_t)chunk * ntiles);
+    ty = tile / wk.tiles_x;
+    tx = tile - ty * wk.tiles_x;
+    if (chunk < wk.nch1) {
+        zlo = wk.zb + chunk * wk.zc;
+        zhi = min(wk.ze, zlo + wk.zc);
+    } else {
+        zlo = wk.zb2 + (chunk - wk.nch1) * wk.zc;
+        zhi = min(wk.ze2, zlo + wk.zc);
+    }
+}
+
+// 3-point row sums of the pair (x, x+1) from a staged row: (l + c.x + c.y, c.x + c.y + r)
+__device__ __forceinline__ double2 rowsum3(const double *row)
+{
+    const double l = row[-1], r = row[2];
+    const double2 c = lds2(row);
+    return make_double2(l + c.x + c.y, c.x + c.y + r);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(THREADS, 2)
+    k1t(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, K1Args a,
+        const DevState *st, K1TWork wk)
+{
+    if (st && st->done) return;
+    extern __shared__ __align__(128) double smem[];
+    double *sp = smem;
+    double *sq = smem + NSP * PSLOT;
+    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool m2 = a.mode == 2;
+    const int ntiles = wk.tiles_x * wk.tiles_y;
+
+    if (tid == 0) {
+        for (int i = 0; i < NSP; ++i) {
+            mbar_init(&fullp[i], 1);
+            mbar_init(&emptyp[i], NCW);
+        }
+        for (int i = 0; i < NSM; ++i) {
+            mbar_init(&fullm[i], 1);
+            mbar_init(&emptym[i], NCW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmP);
+        tma_prefetch_desc(&tmM);
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            uint32_t pc = 0, mc = 0;
+            for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+                int tx, ty, zlo, zhi;
+                item_planes(wk, item, ntiles, tx, ty, zlo, zhi);
+                const int x0 = tx * TX, y0 = ty * TY;
+                auto loadp = [&](int z) {
+                    const int sl = pc % NSP;
+                    if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
+                    mbar_expect_tx(&fullp[sl], PBYTES);
+                    tma_load_4d(sp + sl * PSLOT, &tmP, x0 - 2, y0 - 1, z, wk.j, &fullp[sl]);
+                    ++pc;
+                };
+                auto loadm = [&](int z) {
+                    const int sl = mc % NSM;
+                    if (mc >= NSM) mbar_wait(&emptym[sl], ((mc / NSM) - 1) & 1);
+                    mbar_expect_tx(&fullm[sl], MBYTES);
+                    tma_load_4d(sq + sl * MSLOT, &tmM, x0, y0, z, wk.j - 1, &fullm[sl]);
+                    ++mc;
+                };
+                loadp(zlo - 1);
+                loadp(zlo);
+                for (int z = zlo; z < zhi; ++z) {
+                    loadp(z + 1);
+                    if (m2) loadm(z);
+                }
+            }
+        }
+        return;   // no CTA-wide barrier follows
+    }
+
+    // ---------------- consumers ----------------
+    const int cw = warp - 1;
+    const int ra = 2 * cw;                          // tile rows ra, ra + 1
+    const int oa = (ra + 1) * BW + 2 + 2 * lane;    // pair of row ra in a p slot
+    const int ob = oa + BW;
+    const int qa = ra * TX + 2 * lane, qb = qa + TX;
+    const int64_t pl = g.plane;
+    uint32_t pc = 0, mc = 0;
+    auto waitp = [&](uint32_t c) -> const double * {
+        const int sl = c % NSP;
+        mbar_wait(&fullp[sl], (c / NSP) & 1);
+        return sp + sl * PSLOT;
+    };
+    auto relp = [&](uint32_t c) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyp[c % NSP]);
+    };
+
+    for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+        int tx, ty, zlo, zhi;
+        item_planes(wk, item, ntiles, tx, ty, zlo, zhi);
+        const int x = tx * TX + 2 * lane;
+        const int ya = ty * TY + ra, yb = ya + 1;
+        const bool inx = x < g.nx, in1 = x + 1 < g.nx;
+        const bool sa = inx && ya < g.ny, sb = inx && yb < g.ny;
+        int64_t ia = (int64_t)zlo * pl + (int64_t)ya * g.pitch + x;
+
+        double2 cma, cmb, c0a, c0b, bma = {}, bmb = {}, b0a = {}, b0b = {};
+        uint32_t c0;
+        {
+            const double *s = waitp(pc);
+            if (KIND == 2) {
+                const double2 r0 = rowsum3(s + oa - BW), r1 = rowsum3(s + oa), r2 = rowsum3(s + ob),
+                              r3 = rowsum3(s + ob + BW);
+                bma = make_double2(r0.x + r1.x + r2.x, r0.y + r1.y + r2.y);
+                bmb = make_double2(r1.x + r2.x + r3.x, r1.y + r2.y + r3.y);
+            }
+            cma = lds2(s + oa);
+            cmb = lds2(s + ob);
+            relp(pc);
+            ++pc;
+            s = waitp(pc);
+            c0a = lds2(s + oa);
+            c0b = lds2(s + ob);
+            if (KIND == 2) {
+                const double2 r0 = rowsum3(s + oa - BW), r1 = rowsum3(s + oa), r2 = rowsum3(s + ob),
+                              r3 = rowsum3(s + ob + BW);
+                b0a = make_double2(r0.x + r1.x + r2.x, r0.y + r1.y + r2.y);
+                b0b = make_double2(r1.x + r2.x + r3.x, r1.y + r2.y + r3.y);
+                relp(pc);
+            }
+            c0 = pc;
+            ++pc;
+        }
+        for (int z = zlo; z < zhi; ++z, ia += pl) {
+            const double *s0 = sp + (c0 % NSP) * PSLOT;   // plane z (7-point: still held)
+            const double *s1 = waitp(pc);                  // plane z+1
+            double2 Apa, Apb;
+            const double2 cpa = lds2(s1 + oa), cpb = lds2(s1 + ob);
+            if (KIND == 2) {
+                const double2 r0 = rowsum3(s1 + oa - BW), r1 = rowsum3(s1 + oa), r2 = rowsum3(s1 + ob),
+                              r3 = rowsum3(s1 + ob + BW);
+                const double2 bpa = make_double2(r0.x + r1.x + r2.x, r0.y + r1.y + r2.y);
+                const double2 bpb = make_double2(r1.x + r2.x + r3.x, r1.y + r2.y + r3.y);
+                relp(pc);
+                Apa.x = 27.0 * c0a.x - (bma.x + b0a.x + bpa.x);
+                Apa.y = 27.0 * c0a.y - (bma.y + b0a.y + bpa.y);
+                Apb.x = 27.0 * c0b.x - (bmb.x + b0b.x + bpb.x);
+                Apb.y = 27.0 * c0b.y - (bmb.y + b0b.y + bpb.y);
+                bma = b0a; bmb = b0b;
+                b0a = bpa; b0b = bpb;
+            } else {
+                const double2 ylo = lds2(s0 + oa - BW), yhi = lds2(s0 + ob + BW);
+                const double la = s0[oa - 1], rra = s0[oa + 2], lb = s0[ob - 1], rrb = s0[ob + 2];
+                relp(c0);
+                // centre first, then neighbours in (dz, dy, dx) order
+                Apa.x = g.center * c0a.x - (cma.x + ylo.x + la + c0a.y + c0b.x + cpa.x);
+                Apa.y = g.center * c0a.y - (cma.y + ylo.y + c0a.x + rra + c0b.y + cpa.y);
+                Apb.x = g.center * c0b.x - (cmb.x + c0a.x + lb + c0b.y + yhi.x + cpb.x);
+                Apb.y = g.center * c0b.y - (cmb.y + c0a.y + c0b.x + rrb + yhi.y + cpb.y);
+            }
+            if (!in1) {
+                Apa.y = 0.0;
+                Apb.y = 0.0;
+            }
+            double2 qa2 = {}, qb2 = {};
+            if (m2) {
+                const int sl = mc % NSM;
+                mbar_wait(&fullm[sl], (mc / NSM) & 1);
+                qa2 = lds2(sq + sl * MSLOT + qa);
+                qb2 = lds2(sq + sl * MSLOT + qb);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptym[sl]);
+                ++mc;
+            }
+            if (sa) {
+                __stcs(reinterpret_cast<double2 *>(a.w + ia), Apa);
+                if (a.mode >= 1) {
+                    const double2 dv = a.dinv ? __ldg(reinterpret_cast<const double2 *>(a.dinv + ia))
+                                              : make_double2(a.dinv_c, a.dinv_c);
+                    double v0 = a.coef * (dv.x * Apa.x - a.sigma * c0a.x);
+                    double v1 = a.coef * (dv.y * Apa.y - a.sigma * c0a.y);
+                    if (m2) {
+                        v0 -= qa2.x;
+                        v1 -= qa2.y;
+                    }
+                    if (!in1) v1 = 0.0;
+                    *reinterpret_cast<double2 *>(a.pn + ia) = make_double2(v0, v1);
+                }
+            }
+            if (sb) {
+                const int64_t ib = ia + g.pitch;
+                __stcs(reinterpret_cast<double2 *>(a.w + ib), Apb);
+                if (a.mode >= 1) {
+                    const double2 dv = a.dinv ? __ldg(reinterpret_cast<const double2 *>(a.dinv + ib))
+                                              : make_double2(a.dinv_c, a.dinv_c);
+                    double v0 = a.coef * (dv.x * Apb.x - a.sigma * c0b.x);
+                    double v1 = a.coef * (dv.y * Apb.y - a.sigma * c0b.y);
+                    if (m2) {
+                        v0 -= qb2.x;
+                        v1 -= qb2.y;
+                    }
+                    if (!in1) v1 = 0.0;
+                    *reinterpret_cast<double2 *>(a.pn + ib) = make_double2(v0, v1);
+                }
+            }
+            cma = c0a; cmb = c0b;
+            c0a = cpa; c0b = cpb;
+            c0 = pc;
+            ++pc;
+        }
+        if (KIND != 2) relp(c0);   // the last plane (z_hi) was only read for its centres
+    }
+}
+
+}  // namespace
+
+bool k1t_supported(const Geo &g, const K1Args &a)
+{
+    static int off = -1;
+    if (off < 0) {
+        const char *e = getenv("SSCG_K1_TMA");
+        off = (e && e[0] == '0') ? 1 : 0;
+    }
+    return !off && (g.kind == 1 || g.kind == 2) && a.mode <= 2 && a.tmP4 && a.tmM4;
+}
+
+bool k1t_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP4, CUtensorMap *tmM4)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+        return false;
+    auto enc = reinterpret_cast<CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                             CUtensorMapFloatOOBfill)>(fn);
+    // [x: nx][y: ny][z: nzl + 2 padded planes][v: s vectors]; out-of-range x/y read as 0
+    cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)(nzl + 2), (cuuint64_t)s};
+    cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.vstride * 8};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint32_t boxp[4] = {BW, BH, 1, 1}, boxm[4] = {TX, TY, 1, 1};
+    if (enc(tmP4, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxp, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (enc(tmM4, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxm, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (cudaFuncSetAttribute(k1t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k1t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
+        return false;
+    return true;
+}
+
+void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s)
+{
+    const int n1 = std::max(0, a.ze - a.zb), n2 = std::max(0, a.ze2 - a.zb2);
+    const int nplanes = n1 + n2;
+    if (nplanes <= 0) return;
+    K1TWork wk;
+    wk.tiles_x = (g.nx + TX - 1) / TX;
+    wk.tiles_y = (g.ny + TY - 1) / TY;
+    wk.zb = a.zb; wk.ze = a.ze; wk.zb2 = a.zb2; wk.ze2 = a.ze2;
+    wk.j = a.j;
+    const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
+    static int occ = 0, zc_env = -1;
+    if (!occ) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1t<1>, THREADS, SMEM) != cudaSuccess || occ <= 0)
+            occ = 1;
+        const char *e = getenv("SSCG_K1_ZC");
+        zc_env = e ? std::max(1, atoi(e)) : 0;
+    }
+    const int sms = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
+    const int64_t resident = (int64_t)sms * occ;
+    int zc;
+    if (zc_env > 0) {
+        zc = std::min(std::max(n1, n2), zc_env);
+    } else if (n2 > 0) {
+        zc = 1;   // boundary launch: one plane per range
+    } else {
+        // z-chunks: few and long (each chunk re-reads 2 planes of p_j that
+        // the previous chunk of the column already read, ~1/(2 zc) of the
+        // launch's bytes), sized so that tiles x chunks fills whole waves of
+        // the persistent grid
+        double best = -1.0;
+        zc = n1;
+        for (int nch = 1; nch <= 64 && (n1 + nch - 1) / nch >= 4; ++nch) {
+            const int64_t items = tiles * nch;
+            const int64_t waves = (items + resident - 1) / resident;
+            const int z = (n1 + nch - 1) / nch;
+            const double score = (double)items / (double)(waves * resident) / (1.0 + 0.5 / z);
+            if (score > best + 1e-9) {
+                best = score;
+                zc = z;
+            }
+        }
+    }
+    wk.zc = zc;
+    wk.nch1 = (n1 + zc - 1) / zc;
+    wk.nitems = tiles * (wk.nch1 + (n2 + zc - 1) / zc);
+    const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
+    if (g.kind == 1) k1t<1><<<grid, THREADS, SMEM, s>>>(*a.tmP4, *a.tmM4, g, a, st, wk);
+    else k1t<2><<<grid, THREADS, SMEM, s>>>(*a.tmP4, *a.tmM4, g, a, st, wk);
+}
+
+}  // namespace sscg

@@ -290,6 +290,11 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         TRY(dalloc(c, &sl.ticket, 1));
         CU(cudaMemsetAsync(sl.ticket, 0, sizeof(unsigned), c->stream));
         if (!k2_prepare(g, sl, s)) return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the Gram pass");
+        if (A->kind == SSCG_OP_STENCIL7 || A->kind == SSCG_OP_STENCIL27) {
+            if (!k1t_prepare(g, sl.P, sl.nzl, s, &sl.tmP4, &sl.tmM4))
+                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the basis step");
+            sl.has_k1t = true;
+        }
         if (A->kind == SSCG_OP_VARCOEF7) {
             sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
             sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;
@@ -495,6 +500,11 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
         a.coef = (j == 0) ? c->theta : 2.0 * c->theta;
         a.mode = (j == s - 1) ? 0 : (j == 0 ? 1 : 2);
         a.nzl = sl.nzl;
+        a.j = j;
+        if (sl.has_k1t) {
+            a.tmP4 = &sl.tmP4;
+            a.tmM4 = &sl.tmM4;
+        }
         if (part == 0) {
             a.zb = 1; a.ze = sl.nzl + 1;
         } else if (part == 1) {

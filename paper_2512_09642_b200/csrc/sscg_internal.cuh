@@ -42,6 +42,8 @@ struct Slab {
     const double *kx, *ky, *kz;   // VARCOEF7 faces of this slab
     const double *dinv;           // Jacobi 1/diag(M) interior layout (or nullptr)
     CUtensorMap tmP, tmW;         // K2: [s rows x interior] views of P and W
+    CUtensorMap tmP4, tmM4;       // K1T: 4-D [x][y][plane][vector] views of P (halo box / tile box)
+    bool has_k1t;
 };
 
 struct Geo {
@@ -79,9 +81,16 @@ struct K1Args {
     int sm_cap;            // > 0: use at most this many SMs (leave room for NCCL kernels)
     int mode;
     int nzl;
+    int j;                 // basis step (K1T: vector coordinate of p_j in the tensor maps)
+    const CUtensorMap *tmP4, *tmM4;   // K1T tensor maps of this slab (host memory), or nullptr
 };
 
 void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s);
+
+// K1T: TMA-staged 7-/27-point basis step (k_stencil_tma.cu)
+bool k1t_supported(const Geo &g, const K1Args &a);
+bool k1t_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP4, CUtensorMap *tmM4);
+void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s);
 
 // copy a process-layout grid function into the padded interior of `dst`
 void launch_pack(const Geo &g, const double *src, double *dst, int nzl, const DevState *st,

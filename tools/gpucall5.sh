@@ -1,0 +1,3 @@
+./tools/membw
+C="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
+$C > gpurun_out/plain5.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k1t' -s 20 -c 1 -o gpurun_out/prof_k1t $C > gpurun_out/ncu_k1t.log 2>&1; echo k1t=$?

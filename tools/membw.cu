@@ -1,0 +1,74 @@
+// HBM ceiling per read/write mix on this GPU: streams R vectors in and W
+// vectors out (FP64, n doubles each, 16-B accesses, grid-stride), timed with
+// CUDA events (best of 10).  Gives the roofline each kernel of the path can
+// actually reach for its own mix (K1: 2R/2W, K2: 32R/0W, K5: 33R/2W).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/membw tools/membw.cu && /tmp/membw
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int R, int W>
+__global__ void __launch_bounds__(256) mix(const double2 *__restrict__ in, double2 *__restrict__ out, long n2,
+                                           long stride2)
+{
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n2; e += (long)gridDim.x * blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double2 v = __ldcs(in + r * stride2 + e);
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+#pragma unroll
+        for (int w = 0; w < W; ++w) __stcs(out + w * stride2 + e, make_double2(acc.x + w, acc.y));
+    }
+}
+
+template <int R, int W>
+void run(const double2 *in, double2 *out, long n2, long stride2, int sms)
+{
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mix<R, W>, 256, 0);
+    const int grid = sms * occ;
+    float best = 1e30f;
+    for (int it = 0; it < 12; ++it) {
+        cudaEventRecord(a);
+        mix<R, W><<<grid, 256>>>(in, out, n2, stride2);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (it >= 2 && ms < best) best = ms;
+    }
+    const double bytes = (double)(R + W) * n2 * 16;
+    printf("R=%2d W=%d  %8.3f ms  %7.1f GB/s\n", R, W, best, bytes / best / 1e6);
+}
+
+int main()
+{
+    int dev = 0, sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long n = 448L * 448 * 448;   // one cfg 5 vector (89.9 M doubles, 719 MB)
+    const long n2 = n / 2, stride2 = n2 + 64;
+    double2 *in, *out;
+    if (cudaMalloc(&in, 33 * stride2 * 16) != cudaSuccess || cudaMalloc(&out, 4 * stride2 * 16) != cudaSuccess) {
+        printf("alloc failed\n");
+        return 1;
+    }
+    cudaMemset(in, 0, 33 * stride2 * 16);
+    cudaMemset(out, 0, 4 * stride2 * 16);
+    run<1, 0>(in, out, n2, stride2, sms);
+    run<4, 0>(in, out, n2, stride2, sms);
+    run<1, 1>(in, out, n2, stride2, sms);
+    run<2, 2>(in, out, n2, stride2, sms);
+    run<3, 2>(in, out, n2, stride2, sms);
+    run<2, 4>(in, out, n2, stride2, sms);
+    run<1, 2>(in, out, n2, stride2, sms);
+    run<16, 0>(in, out, n2, stride2, sms);
+    run<32, 0>(in, out, n2, stride2, sms);
+    run<17, 2>(in, out, n2, stride2, sms);
+    run<33, 2>(in, out, n2, stride2, sms);
+    return 0;
+}
