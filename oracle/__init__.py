@@ -70,6 +70,7 @@ def lib():
         L.orc_cholesky_solve.argtypes = [i, vp, vp, vp]; L.orc_cholesky_solve.restype = i
         L.orc_mgs_anorm.argtypes = [vp, i, vp, vp, vp, vp]
         L.orc_sstep_cg.argtypes = [vp, vp, d, d, i, i, vp, vp, d, i, vp]; L.orc_sstep_cg.restype = i
+        L.orc_sstep_cg_ex.argtypes = [vp, vp, d, d, i, i, vp, vp, d, i, vp, i]; L.orc_sstep_cg_ex.restype = i
         L.orc_pcg.argtypes = [vp, vp, vp, vp, d, i]; L.orc_pcg.restype = i
         L.orc_tridiag_eig.argtypes = [i, vp, vp, i]; L.orc_tridiag_eig.restype = d
         L.orc_lanczos_bounds.argtypes = [vp, vp, i, vp, d, vp, vp]; L.orc_lanczos_bounds.restype = i
@@ -229,11 +230,18 @@ class Trace:
     W: np.ndarray | None = None
 
 
+OPT_CHOLESKY, OPT_MONOMIAL = 1, 2
+
+
 def sstep_cg(A: Operator, lmin, lmax, s, nu, b, x0=None, rtol=1e-8, max_outer=1000, D=None,
-             dump_iter=-1) -> tuple[np.ndarray, Trace]:
+             dump_iter=-1, gram_solver="fgs", basis="chebyshev") -> tuple[np.ndarray, Trace]:
     """Run the oracle s-step CG; returns (x, Trace).  Trace arrays are indexed
     by outer iteration k (only the first ``outer`` (+1 for ghat/c/relres)
-    entries are meaningful)."""
+    entries are meaningful).  gram_solver 'fgs' (nu sweeps) or
+    'cholesky' (exact, PAPER.md:20); basis 'chebyshev' (PAPER.md:33-43) or
+    'monomial' (PAPER.md:31, 164)."""
+    opts = (OPT_CHOLESKY if gram_solver == "cholesky" else 0) | (OPT_MONOMIAL if basis == "monomial" else 0)
+    assert gram_solver in ("fgs", "cholesky") and basis in ("chebyshev", "monomial")
     b = _f64(b)
     n = A.n
     x = np.zeros(n) if x0 is None else _f64(x0).copy()
@@ -245,7 +253,7 @@ def sstep_cg(A: Operator, lmin, lmax, s, nu, b, x0=None, rtol=1e-8, max_outer=10
     tr = _Trace(0, 0, 0, 0.0, _p(relres), _p(ghat), _p(c), _p(d), _p(at), _p(al), _p(de), _p(en),
                 dump_iter, _p(Pd), _p(Wd))
     Dm = None if D is None else _f64(D)
-    lib().orc_sstep_cg(A.ref, _p(Dm), lmin, lmax, s, nu, _p(b), _p(x), rtol, max_outer, C.byref(tr))
+    lib().orc_sstep_cg_ex(A.ref, _p(Dm), lmin, lmax, s, nu, _p(b), _p(x), rtol, max_outer, C.byref(tr), opts)
     return x, Trace(tr.outer, bool(tr.converged), bool(tr.breakdown), tr.r0norm, relres, ghat, c, d,
                     at, al, de, en, Pd, Wd)
 

@@ -245,7 +245,7 @@ void orc_chebyshev_basis(const orc_op *A, const double *D, double lmin, double l
     }
 }
 
-/* Monomial basis p_j = (M^{-1}A)^j r, diagnostics only. */
+/* Monomial basis p_j = (M^{-1}A)^j r. */
 void orc_monomial_basis(const orc_op *A, const double *D, int s, const double *r, double *P, double *W)
 {
     const long n = orc_n(A);
@@ -384,8 +384,27 @@ void orc_mgs_anorm(const orc_op *A, int s, const double *Pt, const double *v, do
  *   e. Ruhe scaling d, G = S Ghat S, c~ = S c
  *   f. nu FGS sweeps from alpha~ = 0
  *   g. alpha = S alpha~; x += P alpha; r -= W alpha (= A P alpha)  */
+/* Restart s-step CG with the Chebyshev basis and nu FGS sweeps
+ * (the north_star path).  orc_sstep_cg_ex adds the two variants of SURVEY
+ * §8(f) NEXT-2 that share the boundary:
+ *   opts & ORC_OPT_CHOLESKY  exact Gram solve G a~ = c~ by dense Cholesky
+ *                            (the O(s^3) method FGS replaces)
+ *   opts & ORC_OPT_MONOMIAL  monomial basis p_{j+1} = M^{-1} A p_j
+ *                            ("For monomial bases")
+ * A Cholesky breakdown (non-positive pivot) is reported as a Gram breakdown. */
+#define ORC_OPT_CHOLESKY 1
+#define ORC_OPT_MONOMIAL 2
+int orc_sstep_cg_ex(const orc_op *A, const double *Dm, double lmin, double lmax, int s, int nu,
+                    const double *b, double *x, double rtol, int max_outer, orc_trace *tr, int opts);
+
 int orc_sstep_cg(const orc_op *A, const double *Dm, double lmin, double lmax, int s, int nu,
                  const double *b, double *x, double rtol, int max_outer, orc_trace *tr)
+{
+    return orc_sstep_cg_ex(A, Dm, lmin, lmax, s, nu, b, x, rtol, max_outer, tr, 0);
+}
+
+int orc_sstep_cg_ex(const orc_op *A, const double *Dm, double lmin, double lmax, int s, int nu,
+                    const double *b, double *x, double rtol, int max_outer, orc_trace *tr, int opts)
 {
     const long n = orc_n(A);
     double *D = (double *)malloc((size_t)n * sizeof(double));
@@ -409,7 +428,8 @@ int orc_sstep_cg(const orc_op *A, const double *Dm, double lmin, double lmax, in
     int k = 0, converged = 0, breakdown = 0;
     if (tr) { tr->r0norm = r0norm; }
     for (;;) {
-        orc_chebyshev_basis(A, D, lmin, lmax, s, r, P, W);
+        if (opts & ORC_OPT_MONOMIAL) orc_monomial_basis(A, D, s, r, P, W);
+        else orc_chebyshev_basis(A, D, lmin, lmax, s, r, P, W);
         orc_gram(n, s, P, W, Ghat, c);
         double rn = sqrt(c[0]);
         if (tr) {
@@ -424,7 +444,11 @@ int orc_sstep_cg(const orc_op *A, const double *Dm, double lmin, double lmax, in
         if (rn <= rtol * r0norm) { converged = 1; break; }
         if (k == max_outer) break;
         if (orc_scale(s, Ghat, c, d, G, ct) != 0) { breakdown = 1; break; }
-        orc_fgs(s, G, ct, nu, at_, NULL);
+        if (opts & ORC_OPT_CHOLESKY) {
+            if (orc_cholesky_solve(s, G, ct, at_) != 0) { breakdown = 1; break; }
+        } else {
+            orc_fgs(s, G, ct, nu, at_, NULL);
+        }
         for (int j = 0; j < s; ++j) al[j] = d[j] * at_[j];
         /* x += P alpha ; r -= A P alpha = W alpha */
 #pragma omp parallel for schedule(static)

@@ -121,3 +121,65 @@ def test_classical_pcg_reference():
     x, it = orc.pcg(A, b, rtol=1e-10)
     assert np.linalg.norm(b - orc.apply(A, x)) <= 1e-10 * np.linalg.norm(b) * 1.0001
     assert it <= 16 * 16
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2 variants on the same boundary: exact Cholesky Gram
+# solve and the monomial basis
+
+def test_cholesky_worked_example(golden):
+    """With the exact Gram solve one restart step on A = diag(1,3), s = n = 2
+    reaches the nu -> infinity limit of the worked example, x_1 = [1, 1/3]."""
+    g = golden["restart_sstep_diag13"]
+    A = diag_csr(g["A_diag"])
+    b = np.array(g["b"])
+    x, tr = orc.sstep_cg(A, 1.0, 3.0, 2, 1, b, rtol=0.0, max_outer=1, D=np.ones(2), gram_solver="cholesky")
+    assert np.allclose(x, g["x_limit"], rtol=1e-15, atol=0)
+    # alpha~ solves G a~ = c~ with G = [[1, 1/2], [1/2, 1]], c~ = [1, 0]: a~ = [4/3, -2/3]
+    assert np.allclose(tr.alpha_t[0], [4.0 / 3.0, -2.0 / 3.0], rtol=1e-15)
+    assert tr.delta[0] <= 1e-15
+
+
+def _dense(A):
+    n = A.n
+    return np.column_stack([orc.apply(A, e) for e in np.eye(n)])
+
+
+def test_monomial_basis_is_matrix_powers():
+    """p_j = (M^{-1}A)^j r, by the definition (dense matrix powers, n = 60)."""
+    A = orc.stencil(orc.KIND_5PT2D, 6, 10)
+    D = orc.diag(A)
+    r = inputs.rhs_uniform(6, 10, 1, seed=3)
+    P, W = orc.monomial_basis(A, D, 5, r)
+    Md = _dense(A) / D[:, None]
+    for j in range(5):
+        ref = np.linalg.matrix_power(Md, j) @ r
+        assert np.allclose(P[j], ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+        assert np.allclose(W[j], _dense(A) @ ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("basis", ["chebyshev", "monomial"])
+def test_full_krylov_space_exact(basis):
+    """s = n with the exact Gram solve: the basis spans R^n, so one outer step
+    gives A^{-1} b (dense direct solve), for either basis.  The tolerance is
+    kappa(G) eps: the monomial Gram matrix is far worse conditioned
+    (PAPER.md:31 kappa(G) = O(kappa(M^{-1}A)^{s-1})), the Chebyshev one is not."""
+    A = orc.stencil(orc.KIND_5PT2D, 3, 2)      # n = 6
+    b = inputs.rhs_uniform(3, 2, 1, seed=11)
+    lmin, lmax = inputs.analytic_bounds("5pt", 3, 2, 1)
+    x, tr = orc.sstep_cg(A, lmin, lmax, 6, 1, b, rtol=0.0, max_outer=1, gram_solver="cholesky", basis=basis)
+    xs = np.linalg.solve(_dense(A), b)
+    tol = 1e-12 if basis == "chebyshev" else 1e-7
+    assert np.linalg.norm(x - xs) <= tol * np.linalg.norm(xs)
+
+
+def test_fgs_many_sweeps_equals_cholesky_mode():
+    """nu_infinity FGS sweeps (R20) and the Cholesky mode give the same outer
+    iterates when kappa(G) is small (s = 4 on a 2D 16^2 Laplacian)."""
+    A = orc.stencil(orc.KIND_5PT2D, 16, 16)
+    b = inputs.rhs_uniform(16, 16, 1, seed=42)
+    lmin, lmax = inputs.analytic_bounds("5pt", 16, 16, 1)
+    x1, t1 = orc.sstep_cg(A, lmin, lmax, 4, 400, b, rtol=0.0, max_outer=5)
+    x2, t2 = orc.sstep_cg(A, lmin, lmax, 4, 1, b, rtol=0.0, max_outer=5, gram_solver="cholesky")
+    assert np.linalg.norm(x1 - x2) <= 1e-10 * np.linalg.norm(x2)
+    assert np.max(np.abs(t1.alpha[:5] - t2.alpha[:5])) <= 1e-9 * np.max(np.abs(t2.alpha[:5]))
