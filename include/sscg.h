@@ -219,6 +219,49 @@ SSCG_API sscg_status sscg_inspect(const sscg_ctx *ctx, int32_t what, int32_t ind
 /* Process-local sizes: planes [z0, z0+nz_proc) (CSR: n rows, z0 = 0). */
 SSCG_API sscg_status sscg_local_shape(const sscg_ctx *ctx, int64_t *z0, int64_t *nz_proc, int64_t *n_local);
 
+/* Replace the spectral bounds of M^{-1}A (0 < lmin < lmax):
+ * theta = 2/(lmax-lmin), sigma = (lmax+lmin)/2 for later
+ * solves.  A context created with lambda_min = lambda_max = 0 has no bounds;
+ * sscg_solve with the Chebyshev basis then returns SSCG_ERR_INVALID until
+ * this is called (e.g. with the result of sscg_estimate_bounds).
+ * Errors: SSCG_ERR_INVALID. */
+SSCG_API sscg_status sscg_set_bounds(sscg_ctx *ctx, double lambda_min, double lambda_max);
+
+/* Spectral bounds of M^{-1}A by `iters` Lanczos steps (
+ * PAPER.md:311 "Lanczos ... with a safety margin"; BASELINE cfg 3/4 use 50
+ * steps and margin 0.05) on D^{-1/2} A D^{-1/2} (D = M, the Jacobi diagonal
+ * of the context) from v0/||v0||, without reorthogonalisation; the extreme
+ * Ritz values are widened to lmin (1 - margin), lmax (1 + margin).
+ *   v0         device, process-local grid function (layout as b), not all 0
+ *   iters      1..100000;  margin in [0, 1)
+ *   lmin, lmax host outputs;  alpha_out, beta_out: optional host arrays of
+ *              `iters` doubles receiving the tridiagonal (a_k, b_k); entries
+ *              past an early stop (b_k = 0) are 0.
+ * Runs on the context's stream with two reductions per step (one NCCL
+ * allreduce each for nranks > 1); synchronous on return.  Uses its own
+ * workspace (3 vectors + D + w per slab, allocated on first use): the basis
+ * and the state of the last solve are untouched.
+ * Errors: SSCG_ERR_INVALID, SSCG_ERR_CUDA, SSCG_ERR_NCCL, SSCG_ERR_OOM,
+ * SSCG_ERR_BREAKDOWN if the Ritz interval is not positive. */
+SSCG_API sscg_status sscg_estimate_bounds(sscg_ctx *ctx, const double *v0, int32_t iters, double margin,
+                                          double *lmin, double *lmax, double *alpha_out, double *beta_out);
+
+/* Variants on the same boundary, for later solves:
+ *   SSCG_OPT_GRAM_SOLVER  SSCG_GRAM_FGS (default): nu Forward Gauss-Seidel
+ *                         sweeps;  SSCG_GRAM_CHOLESKY: the
+ *                         exact O(s^3) solve by dense Cholesky of the scaled
+ *                         Gram matrix; a non-positive pivot
+ *                         is reported as SSCG_ERR_BREAKDOWN.
+ *   SSCG_OPT_BASIS        SSCG_BASIS_CHEBYSHEV (default) or
+ *                         SSCG_BASIS_MONOMIAL p_{j+1} = M^{-1}A p_j
+ *                         (kappa(G) grows like
+ *                         kappa(M^{-1}A)^{s-1}, so only small s is usable).
+ * Errors: SSCG_ERR_INVALID for an unknown key or value. */
+enum { SSCG_OPT_GRAM_SOLVER = 0, SSCG_OPT_BASIS = 1 };
+enum { SSCG_GRAM_FGS = 0, SSCG_GRAM_CHOLESKY = 1 };
+enum { SSCG_BASIS_CHEBYSHEV = 0, SSCG_BASIS_MONOMIAL = 1 };
+SSCG_API sscg_status sscg_set_option(sscg_ctx *ctx, int32_t key, int32_t value);
+
 SSCG_API void sscg_destroy(sscg_ctx *ctx);
 
 /* Thread-local description of the last error ("" if none). */

@@ -74,6 +74,8 @@ def lib():
         L.orc_pcg.argtypes = [vp, vp, vp, vp, d, i]; L.orc_pcg.restype = i
         L.orc_tridiag_eig.argtypes = [i, vp, vp, i]; L.orc_tridiag_eig.restype = d
         L.orc_lanczos_bounds.argtypes = [vp, vp, i, vp, d, vp, vp]; L.orc_lanczos_bounds.restype = i
+        L.orc_lanczos_bounds_tri.argtypes = [vp, vp, i, vp, d, vp, vp, vp, vp]
+        L.orc_lanczos_bounds_tri.restype = i
     return _lib
 
 
@@ -271,9 +273,14 @@ def tridiag_eig(a, b, k):
     return lib().orc_tridiag_eig(a.size, _p(a), _p(b), k)
 
 
-def lanczos_bounds(A: Operator, iters, v0, margin, D=None):
+def lanczos_bounds(A: Operator, iters, v0, margin, D=None, tridiag=False):
+    """(lmin, lmax, m) -- with tridiag=True also the Lanczos coefficients
+    (alpha[:m], beta[:m-1])."""
     v0 = _f64(v0)
     lo, hi = C.c_double(), C.c_double()
     Dm = None if D is None else _f64(D)
-    m = lib().orc_lanczos_bounds(A.ref, _p(Dm), iters, _p(v0), margin, C.byref(lo), C.byref(hi))
+    al, be = np.zeros(iters), np.zeros(iters)
+    m = lib().orc_lanczos_bounds_tri(A.ref, _p(Dm), iters, _p(v0), margin, C.byref(lo), C.byref(hi), _p(al), _p(be))
+    if tridiag:
+        return lo.value, hi.value, m, al[:m], be[:max(m - 1, 0)]
     return lo.value, hi.value, m

@@ -558,8 +558,18 @@ double orc_tridiag_eig(int m, const double *a, const double *b, int kth)
  * M^{-1}A), start v0/||v0||, no reorthogonalisation.  Returns the extreme Ritz
  * values widened multiplicatively: lmin (1 - margin), lmax (1 + margin).
  * Returns the number of steps taken (fewer on breakdown beta = 0). */
+int orc_lanczos_bounds_tri(const orc_op *A, const double *Dm, int iters, const double *v0, double margin,
+                           double *lmin, double *lmax, double *al_out, double *be_out);
+
 int orc_lanczos_bounds(const orc_op *A, const double *Dm, int iters, const double *v0, double margin,
                        double *lmin, double *lmax)
+{
+    return orc_lanczos_bounds_tri(A, Dm, iters, v0, margin, lmin, lmax, NULL, NULL);
+}
+
+/* same, and copies the tridiagonal (alpha_k, k < m; beta_k, k < m-1) out */
+int orc_lanczos_bounds_tri(const orc_op *A, const double *Dm, int iters, const double *v0, double margin,
+                           double *lmin, double *lmax, double *al_out, double *be_out)
 {
     const long n = orc_n(A);
     double *D = (double *)malloc((size_t)n * sizeof(double));
@@ -588,6 +598,8 @@ int orc_lanczos_bounds(const orc_op *A, const double *Dm, int iters, const doubl
         be[k] = beta;
         for (long i = 0; i < n; ++i) { vp[i] = v[i]; v[i] = u[i] / beta; }
     }
+    if (al_out) memcpy(al_out, al, (size_t)m * sizeof(double));
+    if (be_out && m > 1) memcpy(be_out, be, (size_t)(m - 1) * sizeof(double));
     *lmin = orc_tridiag_eig(m, al, be, 0) * (1.0 - margin);
     *lmax = orc_tridiag_eig(m, al, be, m - 1) * (1.0 + margin);
     free(D); free(v); free(vp); free(u); free(t); free(al); free(be);

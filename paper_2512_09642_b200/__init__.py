@@ -27,10 +27,13 @@ OK, ERR_INVALID, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_BREAKDOWN, ERR_NONFINITE, ERR_
 OP_STENCIL5_2D, OP_STENCIL7, OP_STENCIL27, OP_VARCOEF7, OP_CSR = range(5)
 INSPECT_P, INSPECT_W, INSPECT_GRAM, INSPECT_D, INSPECT_ALPHA_T, INSPECT_ALPHA, INSPECT_DELTA = range(7)
 SOLVE_X0_ZERO = 1
+OPT_GRAM_SOLVER, OPT_BASIS = 0, 1
+GRAM_FGS, GRAM_CHOLESKY = 0, 1
+BASIS_CHEBYSHEV, BASIS_MONOMIAL = 0, 1
 
 EXPORTS = ["sscg_partition", "sscg_halo_plan", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host", "sscg_iterate",
            "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect", "sscg_local_shape", "sscg_destroy",
-           "sscg_last_error", "sscg_version"]
+           "sscg_last_error", "sscg_version", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds"]
 PROF_NAMES = ["basis", "gram", "allreduce", "fgs", "update", "halo"]
 
 
@@ -88,13 +91,16 @@ def load(path: str = LIB_PATH):
     L.sscg_stats.argtypes = [vp, C.POINTER(_Stats)]
     L.sscg_inspect.argtypes = [vp, i32, i32, vp, i64]
     L.sscg_local_shape.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+    L.sscg_set_bounds.argtypes = [vp, d, d]
+    L.sscg_set_option.argtypes = [vp, i32, i32]
+    L.sscg_estimate_bounds.argtypes = [vp, vp, i32, d, C.POINTER(d), C.POINTER(d), vp, vp]
     L.sscg_destroy.argtypes = [vp]
     L.sscg_destroy.restype = None
     L.sscg_last_error.restype = C.c_char_p
     L.sscg_version.restype = C.c_char_p
     for name in ("sscg_partition", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host",
                  "sscg_iterate", "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect",
-                 "sscg_local_shape"):
+                 "sscg_local_shape", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -186,7 +192,10 @@ class Solver:
     """One sscg context (sscg_setup ... sscg_destroy)."""
 
     def __init__(self, op, lmin: float, lmax: float, s: int, nu: int, diag_M=None, rank: int = 0,
-                 nranks: int = 1, slabs_per_rank: int = 1, nccl_id: bytes | None = None, stream=None):
+                 nranks: int = 1, slabs_per_rank: int = 1, nccl_id: bytes | None = None, stream=None,
+                 gram_solver: str = "fgs", basis: str = "chebyshev"):
+        """lmin = lmax = 0 creates the context without spectral bounds (set
+        them with set_bounds, e.g. from estimate_bounds)."""
         L = load()
         self._op = op
         self._opst = op._struct()
@@ -201,6 +210,30 @@ class Solver:
         z0, nzp, nloc = C.c_int64(), C.c_int64(), C.c_int64()
         _check(L.sscg_local_shape(h, C.byref(z0), C.byref(nzp), C.byref(nloc)))
         self.z0, self.nz_local, self.n_local = z0.value, nzp.value, nloc.value
+        if gram_solver != "fgs":
+            self.set_option(OPT_GRAM_SOLVER, {"fgs": GRAM_FGS, "cholesky": GRAM_CHOLESKY}[gram_solver])
+        if basis != "chebyshev":
+            self.set_option(OPT_BASIS, {"chebyshev": BASIS_CHEBYSHEV, "monomial": BASIS_MONOMIAL}[basis])
+
+    def set_bounds(self, lmin: float, lmax: float):
+        _check(load().sscg_set_bounds(self._h, lmin, lmax))
+
+    def set_option(self, key: int, value: int):
+        _check(load().sscg_set_option(self._h, key, value))
+
+    def estimate_bounds(self, v0, iters: int = 50, margin: float = 0.05, tridiag: bool = False):
+        """Lanczos bounds of M^{-1}A from v0 (cuda float64, process-local);
+        returns (lmin, lmax) or, with tridiag=True, (lmin, lmax, alpha, beta)."""
+        import torch
+        assert v0.is_cuda and v0.dtype == torch.float64 and v0.is_contiguous() and v0.numel() == self.n_local
+        cur = torch.cuda.current_stream()
+        if cur.cuda_stream != 0:
+            cur.synchronize()
+        lo, hi = C.c_double(), C.c_double()
+        al, be = np.zeros(iters), np.zeros(iters)
+        _check(load().sscg_estimate_bounds(self._h, _ptr(v0), iters, margin, C.byref(lo), C.byref(hi),
+                                           al.ctypes.data, be.ctypes.data))
+        return (lo.value, hi.value, al, be) if tridiag else (lo.value, hi.value)
 
     def close(self):
         h = getattr(self, "_h", None)

@@ -138,6 +138,114 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
     }
 }
 
+// K4C -- the exact Gram solve the paper's FGS replaces:
+// the same stopping test and Ruhe scaling as K4, then a dense Cholesky
+// factorisation G = R^T R of the scaled Gram matrix (left-looking, row k of R
+// by the lanes in parallel) and two triangular solves, all in shared memory
+// (s <= 64) by one warp.  O(s^3) work -- SURVEY §8(f) NEXT-2, selected with
+// SSCG_OPT_GRAM_SOLVER = SSCG_GRAM_CHOLESKY.  A non-positive pivot is a Gram
+// breakdown (R19).
+__global__ void __launch_bounds__(32) k4_chol(K4Args a, DevState *st)
+{
+    if (st->done) return;
+    // R overwrites the upper triangle of G in place (row k of R is written
+    // after row k of G was last read)
+    __shared__ double R[SMAX * SMAX], dsh[SMAX], ct[SMAX], y[SMAX], al[SMAX];
+    const int s = a.s, lane = threadIdx.x;
+    const int k = st->k;
+    const double *Gh = a.blk, *c = a.blk + s * s;
+    const int nent = s * s + s;
+    const bool rec = k < st->hist_cap;
+    if (rec)
+        for (int q = lane; q < nent; q += 32) a.h_gram[(int64_t)k * nent + q] = a.blk[q];
+    const double rn = sqrt(c[0]);
+    const double r0 = (k == 0) ? rn : st->r0norm;
+    if (lane == 0) {
+        if (k == 0) st->r0norm = rn;
+        if (rec) a.h_relres[k] = (r0 > 0.0) ? rn / r0 : 0.0;
+    }
+    if (!isfinite(rn)) {
+        if (lane == 0) { st->nonfinite = 1; st->done = 1; st->outer = k; }
+        return;
+    }
+    if (rn <= st->rtol * r0) {
+        if (lane == 0) { st->converged = 1; st->done = 1; st->outer = k; }
+        return;
+    }
+    if (k >= st->max_outer) {
+        if (lane == 0) { st->done = 1; st->outer = k; }
+        return;
+    }
+    bool ok = true;
+    for (int i = lane; i < s; i += 32) {
+        const double gd = Gh[i * s + i];
+        ok &= (gd > 0.0) && isfinite(gd);
+        dsh[i] = 1.0 / sqrt(gd);
+    }
+    if (!__all_sync(0xffffffffu, ok)) {
+        if (lane == 0) { st->breakdown = 1; st->done = 1; st->outer = k; }
+        return;
+    }
+    __syncwarp();
+    for (int q = lane; q < s * s; q += 32) {
+        const int i = q / s, j = q - i * s;
+        R[q] = (i == j) ? 1.0 : (dsh[i] * Gh[q]) * dsh[j];
+    }
+    for (int i = lane; i < s; i += 32) ct[i] = dsh[i] * c[i];
+    __syncwarp();
+    // R_kk = sqrt(G_kk - sum_{m<k} R_mk^2);  R_kj = (G_kj - sum_{m<k} R_mk R_mj) / R_kk
+    for (int kk = 0; kk < s; ++kk) {
+        double piv = R[kk * s + kk];
+        for (int m = 0; m < kk; ++m) piv -= R[m * s + kk] * R[m * s + kk];
+        if (!(piv > 0.0)) {
+            if (lane == 0) { st->breakdown = 1; st->done = 1; st->outer = k; }
+            return;
+        }
+        const double rkk = sqrt(piv);
+        for (int j = kk + 1 + lane; j < s; j += 32) {
+            double b = R[kk * s + j];
+            for (int m = 0; m < kk; ++m) b -= R[m * s + kk] * R[m * s + j];
+            R[kk * s + j] = b / rkk;
+        }
+        if (lane == 0) R[kk * s + kk] = rkk;
+        __syncwarp();
+    }
+    // R^T y = c~ (forward), R a~ = y (backward): one lane, s^2/2 FMAs each
+    if (lane == 0) {
+        for (int i = 0; i < s; ++i) {
+            double t = ct[i];
+            for (int m = 0; m < i; ++m) t -= R[m * s + i] * y[m];
+            y[i] = t / R[i * s + i];
+        }
+        for (int i = s - 1; i >= 0; --i) {
+            double t = y[i];
+            for (int m = i + 1; m < s; ++m) t -= R[i * s + m] * al[m];
+            al[i] = t / R[i * s + i];
+        }
+    }
+    __syncwarp();
+    double rr = 0.0, cc = 0.0;
+    for (int i = lane; i < s; i += 32) {
+        double ri = ct[i];
+        for (int j = 0; j < s; ++j) ri -= ((i == j) ? 1.0 : (dsh[i] * Gh[i * s + j]) * dsh[j]) * al[j];
+        rr += ri * ri;
+        cc += ct[i] * ct[i];
+        a.alpha[i] = dsh[i] * al[i];
+        if (rec) {
+            a.h_d[(int64_t)k * s + i] = dsh[i];
+            a.h_at[(int64_t)k * s + i] = al[i];
+            a.h_al[(int64_t)k * s + i] = dsh[i] * al[i];
+        }
+    }
+    rr = warp_sum(rr);
+    cc = warp_sum(cc);
+    if (lane == 0) {
+        if (rec) a.h_delta[k] = sqrt(rr) / sqrt(cc);
+        st->outer = k + 1;
+        st->k = k + 1;
+    }
+}
+
 struct K5Params {
     const double *P;   // interior start of p_0 (= r_k)
     const double *W;   // interior start of w_0
@@ -207,7 +315,8 @@ __global__ void __launch_bounds__(256) k5_update_gen(K5Params k, const DevState 
 
 void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
 {
-    if (a.s <= 32) k4_fgs<false><<<1, 32, 0, s>>>(a, st);
+    if (a.solver == 1) k4_chol<<<1, 32, 0, s>>>(a, st);
+    else if (a.s <= 32) k4_fgs<false><<<1, 32, 0, s>>>(a, st);
     else k4_fgs<true><<<1, 32, 0, s>>>(a, st);
 }
 

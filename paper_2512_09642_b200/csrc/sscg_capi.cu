@@ -79,6 +79,17 @@ struct sscg_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool overlap = true;
     int k1_sm_cap = 0;
+    // variants on the same boundary
+    int gram_solver = SSCG_GRAM_FGS;
+    int basis = SSCG_BASIS_CHEBYSHEV;
+    bool bounds_set = false;
+    // Lanczos workspace (sscg_estimate_bounds): 3 vectors + D per slab, lazily
+    std::vector<double *> lz_vec;     // [slab * 5 + {y0, y1, y2, w, D}]
+    double *lz_scal = nullptr;        // device scalars, see sscg_estimate_bounds
+    int lz_iters = 0;
+    int *lz_flags = nullptr;          // {stop, m}
+    double *lz_part = nullptr;        // dot partials [slab][grid]
+    unsigned *lz_ticket = nullptr;    // [slab]
     ncclComm_t comm = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double *bbuf = nullptr, *xbuf = nullptr;   // device buffers of sscg_solve_host
@@ -192,8 +203,13 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
     if (!A) return fail(SSCG_ERR_INVALID, "null operator");
     if (s < 1 || s > 64) return fail(SSCG_ERR_INVALID, "s = %d outside [1, 64]", s);
     if (nu < 1) return fail(SSCG_ERR_INVALID, "nu = %d < 1", nu);
-    if (!(lmin > 0.0) || !(lmax > lmin) || !std::isfinite(lmax))
+    if (lmin == 0.0 && lmax == 0.0) {
+        c->bounds_set = false;   // to be estimated (sscg_estimate_bounds) and set (sscg_set_bounds)
+    } else if (!(lmin > 0.0) || !(lmax > lmin) || !std::isfinite(lmax)) {
         return fail(SSCG_ERR_INVALID, "need 0 < lambda_min < lambda_max (got %g, %g)", lmin, lmax);
+    } else {
+        c->bounds_set = true;
+    }
     if (A->kind < 0 || A->kind > 4) return fail(SSCG_ERR_INVALID, "unknown operator kind %d", A->kind);
     c->s = s;
     c->nu = nu;
@@ -499,6 +515,11 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
         a.sigma = c->sigma;
         a.coef = (j == 0) ? c->theta : 2.0 * c->theta;
         a.mode = (j == s - 1) ? 0 : (j == 0 ? 1 : 2);
+        if (c->basis == SSCG_BASIS_MONOMIAL) {   // p_{j+1} = M^{-1} A p_j
+            a.sigma = 0.0;
+            a.coef = 1.0;
+            a.mode = (j == s - 1) ? 0 : 1;
+        }
         a.nzl = sl.nzl;
         a.j = j;
         if (sl.has_k1t) {
@@ -569,6 +590,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     a4.alpha = c->alpha;
     a4.s = s;
     a4.nu = c->nu;
+    a4.solver = (c->gram_solver == SSCG_GRAM_CHOLESKY) ? 1 : 0;
     a4.h_gram = c->h_gram; a4.h_d = c->h_d; a4.h_at = c->h_at; a4.h_al = c->h_al;
     a4.h_delta = c->h_delta; a4.h_relres = c->h_relres;
     TRY(prof_mark(c, SSCG_PROF_FGS, true));
@@ -676,6 +698,8 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
 {
     if (!c || !b || !x) return fail(SSCG_ERR_INVALID, "null argument");
     if (max_outer < 0 || !(rtol >= 0.0)) return fail(SSCG_ERR_INVALID, "bad rtol/max_outer");
+    if (!c->bounds_set && c->basis == SSCG_BASIS_CHEBYSHEV)
+        return fail(SSCG_ERR_INVALID, "spectral bounds not set (sscg_set_bounds / sscg_estimate_bounds)");
     const Geo &g = c->g;
     const int cap = std::min(max_outer + 1, 1 << 20);
     TRY(ensure_history(c, cap));
@@ -893,5 +917,153 @@ extern "C" sscg_status sscg_profile(sscg_ctx *c, sscg_profile_t *out)
     if (!c || !out) return fail(SSCG_ERR_INVALID, "null argument");
     TRY(prof_resolve(c));
     *out = c->prof;
+    return SSCG_OK;
+}
+
+static void drop_graph(sscg_ctx *c)
+{
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+}
+
+extern "C" sscg_status sscg_set_bounds(sscg_ctx *c, double lambda_min, double lambda_max)
+{
+    if (!c) return fail(SSCG_ERR_INVALID, "null ctx");
+    if (!(lambda_min > 0.0) || !(lambda_max > lambda_min) || !std::isfinite(lambda_max))
+        return fail(SSCG_ERR_INVALID, "need 0 < lambda_min < lambda_max (got %g, %g)", lambda_min, lambda_max);
+    c->lmin = lambda_min;
+    c->lmax = lambda_max;
+    c->theta = 2.0 / (lambda_max - lambda_min);
+    c->sigma = (lambda_max + lambda_min) / 2.0;
+    c->bounds_set = true;
+    drop_graph(c);                                // the captured K1 launches hold theta, sigma
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_set_option(sscg_ctx *c, int32_t key, int32_t value)
+{
+    if (!c) return fail(SSCG_ERR_INVALID, "null ctx");
+    switch (key) {
+    case SSCG_OPT_GRAM_SOLVER:
+        if (value != SSCG_GRAM_FGS && value != SSCG_GRAM_CHOLESKY) return fail(SSCG_ERR_INVALID, "bad Gram solver %d", value);
+        c->gram_solver = value;
+        break;
+    case SSCG_OPT_BASIS:
+        if (value != SSCG_BASIS_CHEBYSHEV && value != SSCG_BASIS_MONOMIAL) return fail(SSCG_ERR_INVALID, "bad basis %d", value);
+        c->basis = value;
+        break;
+    default:
+        return fail(SSCG_ERR_INVALID, "unknown option %d", key);
+    }
+    drop_graph(c);
+    return SSCG_OK;
+}
+
+// Lanczos on D^{-1/2} A D^{-1/2} (k_lanczos.cu; BASELINE cfg 3/4)
+extern "C" sscg_status sscg_estimate_bounds(sscg_ctx *c, const double *v0, int32_t iters, double margin,
+                                            double *lmin, double *lmax, double *alpha_out, double *beta_out)
+{
+    if (!c || !v0 || !lmin || !lmax) return fail(SSCG_ERR_INVALID, "null argument");
+    if (iters < 1 || iters > 100000 || !(margin >= 0.0) || !(margin < 1.0))
+        return fail(SSCG_ERR_INVALID, "bad iters (%d) or margin (%g)", iters, margin);
+    const Geo &g = c->g;
+    const int L = (int)c->slabs.size();
+    cudaStream_t st = c->stream;
+    if (c->lz_vec.empty()) {
+        c->lz_vec.assign((size_t)L * 5, nullptr);
+        for (int l = 0; l < L; ++l)
+            for (int q = 0; q < 5; ++q) TRY(dalloc(c, &c->lz_vec[(size_t)l * 5 + q], (size_t)g.vstride));
+        TRY(dalloc(c, &c->lz_part, (size_t)L * lz_grid()));
+        TRY(dalloc(c, &c->lz_ticket, (size_t)L));
+        TRY(dalloc(c, &c->lz_flags, 2));
+    }
+    if (iters > c->lz_iters) {
+        TRY(dalloc(c, &c->lz_scal, (size_t)(16 + L + 2 * iters)));
+        c->lz_iters = iters;
+    }
+    // scalars: 0 ||v0||^2, 1 a_k, 2 b_k^2, 3 b_{k-1}, 4-5 bounds, 16.. per-slab values, then alpha, beta
+    double *S = c->lz_scal, *slabv = S + 16, *alpha = S + 16 + L, *beta = alpha + iters;
+    CU(cudaMemsetAsync(S, 0, (size_t)(16 + L + 2 * iters) * sizeof(double), st));
+    CU(cudaMemsetAsync(c->lz_flags, 0, 2 * sizeof(int), st));
+    CU(cudaMemsetAsync(c->lz_ticket, 0, (size_t)L * sizeof(unsigned), st));
+    auto vec = [&](int l, int q) { return c->lz_vec[(size_t)l * 5 + q]; };
+    for (int l = 0; l < L; ++l) {
+        for (int q = 0; q < 4; ++q) CU(cudaMemsetAsync(vec(l, q), 0, (size_t)g.vstride * sizeof(double), st));
+        // D = diag(M) in the padded layout, 0 in pad columns and halos
+        double *D = vec(l, 4);
+        CU(cudaMemsetAsync(D, 0, (size_t)g.vstride * sizeof(double), st));
+        lz_diag(g, c->slabs[l], D, st);
+    }
+    CU(cudaGetLastError());
+    const int *stop = c->lz_flags;
+    const int64_t npl = g.plane;
+    // sum over slabs (fixed order) and ranks of per-slab dot products into S[idx]
+    auto reduce = [&](int idx, int mode, int qa, int qb) -> sscg_status {
+        for (int l = 0; l < L; ++l) {
+            const int64_t N = (int64_t)c->slabs[l].nzl * npl;
+            lz_dot(vec(l, qa) + npl, vec(l, qb) + npl, vec(l, 4) + npl, N, mode, c->lz_part + (size_t)l * lz_grid(),
+                   c->lz_ticket + l, slabv + l, stop, st);
+        }
+        lz_sum(slabv, L, S + idx, stop, st);
+        if (c->nranks > 1) NC(ncclAllReduce(S + idx, S + idx, 1, ncclDouble, ncclSum, c->comm, st));
+        return SSCG_OK;
+    };
+    // ||v0||^2 from a packed copy, then y_0 = v0 / (||v0|| sqrt(D))
+    for (int l = 0; l < L; ++l) {
+        auto &sl = c->slabs[l];
+        launch_pack(g, v0 + sl.zoff * (int64_t)g.nx * g.ny, vec(l, 0), sl.nzl, nullptr, st);
+    }
+    TRY(reduce(0, 0, 0, 0));
+    for (int l = 0; l < L; ++l) {
+        auto &sl = c->slabs[l];
+        lz_init(g, sl, v0 + sl.zoff * (int64_t)g.nx * g.ny, vec(l, 4), S + 0, vec(l, 0), st);
+    }
+    int iy = 0, iyp = 1, iz = 2;
+    const bool halo = (L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR;
+    std::vector<double *> yv(L);
+    for (int k = 0; k < iters; ++k) {
+        for (int l = 0; l < L; ++l) yv[l] = vec(l, iy);
+        if (halo) TRY(exchange(c, yv.data(), st));
+        for (int l = 0; l < L; ++l) {   // w = A y
+            auto &sl = c->slabs[l];
+            K1Args a{};
+            a.p = vec(l, iy);
+            a.w = vec(l, 3);
+            a.kx = sl.kx; a.ky = sl.ky; a.kz = sl.kz;
+            a.dinv = sl.dinv;
+            a.dinv_c = g.dinv_c;
+            a.mode = 0;
+            a.zb = 1;
+            a.ze = sl.nzl + 1;
+            a.nzl = sl.nzl;
+            launch_k1(g, a, nullptr, st);
+        }
+        TRY(reduce(1, 0, iy, 3));                                      // a_k = y^T A y
+        for (int l = 0; l < L; ++l) {
+            const int64_t N = (int64_t)c->slabs[l].nzl * npl;
+            lz_update(vec(l, 3) + npl, vec(l, 4) + npl, vec(l, iy) + npl, vec(l, iyp) + npl, vec(l, iz) + npl, N,
+                      S + 1, S + 3, stop, st);
+        }
+        TRY(reduce(2, 1, iz, iz));                                     // b_k^2 = z^T D z
+        lz_record(S + 1, S + 2, alpha, beta, S + 3, k, c->lz_flags, c->lz_flags + 1, st);
+        for (int l = 0; l < L; ++l) lz_scale(vec(l, iz) + npl, (int64_t)c->slabs[l].nzl * npl, S + 3, stop, st);
+        const int t = iyp;
+        iyp = iy;
+        iy = iz;
+        iz = t;
+    }
+    lz_extremes(alpha, beta, c->lz_flags + 1, margin, S + 4, st);
+    CU(cudaGetLastError());
+    double out[2];
+    CU(cudaMemcpyAsync(out, S + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (alpha_out) CU(cudaMemcpyAsync(alpha_out, alpha, (size_t)iters * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (beta_out) CU(cudaMemcpyAsync(beta_out, beta, (size_t)iters * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    *lmin = out[0];
+    *lmax = out[1];
+    if (!(out[0] > 0.0) || !(out[1] > out[0]) || !std::isfinite(out[1]))
+        return fail(SSCG_ERR_BREAKDOWN, "Lanczos gave no valid interval (%g, %g)", out[0], out[1]);
     return SSCG_OK;
 }

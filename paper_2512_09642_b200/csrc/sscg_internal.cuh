@@ -114,6 +114,7 @@ struct K4Args {
     const double *blk;     // [Ghat (s*s) | c (s)] after allreduce
     double *alpha;         // out: alpha = d o a~ (s)
     int s, nu;
+    int solver;            // 0 = nu FGS sweeps, 1 = dense Cholesky
     double *h_gram, *h_d, *h_at, *h_al, *h_delta, *h_relres;  // history [cap][...]
 };
 void launch_k4(const K4Args &a, DevState *st, cudaStream_t s);
@@ -121,5 +122,20 @@ void launch_k4(const K4Args &a, DevState *st, cudaStream_t s);
 // K5: x += P alpha;  p_0 -= W alpha over padded planes [zb, ze) (ze < 0: to nzl+1)
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *x_slab,
                const DevState *st, cudaStream_t stream, int zb = 1, int ze = -1);
+
+// Lanczos spectral bounds (k_lanczos.cu)
+int lz_grid();
+void lz_diag(const Geo &g, const Slab &sl, double *D, cudaStream_t s);
+void lz_init(const Geo &g, const Slab &sl, const double *v0, const double *D, const double *nrm2, double *y,
+             cudaStream_t s);
+void lz_dot(const double *x, const double *y, const double *D, int64_t N, int mode, double *part, unsigned *ticket,
+            double *out, const int *stop, cudaStream_t s);
+void lz_sum(const double *vals, int n, double *out, const int *stop, cudaStream_t s);
+void lz_update(const double *w, const double *D, const double *y, const double *yp, double *z, int64_t N,
+               const double *a, const double *bprev, const int *stop, cudaStream_t s);
+void lz_record(const double *a, const double *b2, double *alpha, double *beta, double *bprev, int k, int *stop, int *m,
+               cudaStream_t s);
+void lz_scale(double *z, int64_t N, const double *bprev, const int *stop, cudaStream_t s);
+void lz_extremes(const double *alpha, const double *beta, const int *m, double margin, double *out, cudaStream_t s);
 
 }  // namespace sscg

@@ -64,6 +64,10 @@ class Problem:
         return orc.sstep_cg(self.A, self.lmin, self.lmax, self.s, self.nu, self.b, rtol=rtol,
                             max_outer=max_outer, dump_iter=dump_iter)
 
+    def oracle_ex(self, max_outer, rtol=0.0, dump_iter=-1, gram_solver="fgs", basis="chebyshev"):
+        return orc.sstep_cg(self.A, self.lmin, self.lmax, self.s, self.nu, self.b, rtol=rtol,
+                            max_outer=max_outer, dump_iter=dump_iter, gram_solver=gram_solver, basis=basis)
+
 
 def rel_inf(a, ref):
     return float(np.max(np.abs(a - ref)) / max(np.max(np.abs(ref)), 1e-300))
