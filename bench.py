@@ -28,6 +28,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 K1_NAME = "k1t"   # dominant kernel (basis step) as named in the ncu capture
+
+# BASELINE.json configs (synthetic, seeded).  cfg5 is the
+# configuration the headline metric is quoted on; the others are parity-test
+# cases that bench.py can also time (--workload) for the per-kernel rooflines.
+WORKLOADS = {
+    "cfg2": {"kind": "7pt", "n": 128, "s": 16, "nu": 25, "bounds": "analytic",
+             "desc": "cfg2: 3D 7-point Poisson {n}^3 per GPU, FP64, Jacobi, analytic bounds"},
+    "cfg3": {"kind": "27pt", "n": 256, "s": 16, "nu": 30, "bounds": "lanczos",
+             "desc": "cfg3: 3D 27-point stencil {n}^3 per GPU (z-slab weak scaling), FP64, Jacobi, "
+                     "Lanczos-50 bounds widened 5% (GPU, sscg_estimate_bounds)"},
+    "cfg4": {"kind": "varcoef7", "n": 192, "s": 16, "nu": 30, "bounds": "lanczos",
+             "desc": "cfg4: 3D variable-coefficient 7-point diffusion {n}^3 (lognormal faces, seed 42), FP64, "
+                     "Jacobi, Lanczos-50 bounds widened 5% (GPU)"},
+    "cfg5": {"kind": "7pt", "n": 448, "s": 16, "nu": 30, "bounds": "analytic",
+             "desc": "cfg5: 3D 7-point Poisson {n}^3 per GPU (z-slab weak scaling), FP64, Jacobi, analytic bounds"},
+}
 METRIC = "s-step CG time/outer-iter & GDOF/s at 1/2/4/8 B200; % of HBM peak"
 UNIT = "GDOF/s"
 
@@ -38,22 +54,35 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=448, help="grid edge per GPU (cfg5: 448)")
-    ap.add_argument("--s", type=int, default=16)
-    ap.add_argument("--nu", type=int, default=30)
+    ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS),
+                    help="BASELINE.json config (default cfg5 = the headline metric's configuration)")
+    ap.add_argument("--n", type=int, default=None, help="grid edge per GPU (default: the workload's)")
+    ap.add_argument("--s", type=int, default=None)
+    ap.add_argument("--nu", type=int, default=None)
+    ap.add_argument("--strong", action="store_true", help="cfg4 (ii): fixed global n^3 split over the GPUs")
     ap.add_argument("--cpu-planes", type=int, default=16, help="z-planes of the oracle's CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    w = WORKLOADS[a.workload]
+    a.n = w["n"] if a.n is None else a.n
+    a.s = w["s"] if a.s is None else a.s
+    a.nu = w["nu"] if a.nu is None else a.nu
+    a.kind = w["kind"]
+    return a
 
 
 def workload(a, nranks):
     n = a.n
-    return {"workload": f"cfg5: 3D 7-point Poisson {n}^3 per GPU (z-slab weak scaling), FP64, Jacobi, "
-                        f"analytic bounds, s={a.s}, nu={a.nu}, x0=0, b~U[-1,1] seed 42",
-            "nx": n, "ny": n, "nz_per_gpu": n, "nz_global": n * nranks, "s": a.s, "nu": a.nu,
-            "n_global": n * n * n * nranks, "parallelism": f"z-slab x{nranks}",
-            "l2": "no flush: per-GPU working set 2*s vectors (%.1f GB) >> 126 MB L2" % (2 * a.s * n ** 3 * 8 / 1e9)}
+    nzg = n if a.strong else n * nranks
+    desc = WORKLOADS[a.workload]["desc"].format(n=n)
+    if a.strong:
+        desc = desc.replace("per GPU", "global (strong scaling)")
+    return {"workload": f"{desc}, s={a.s}, nu={a.nu}, x0=0, b~U[-1,1] seed 42",
+            "nx": n, "ny": n, "nz_per_gpu": nzg // nranks, "nz_global": nzg, "s": a.s, "nu": a.nu,
+            "n_global": n * n * nzg, "parallelism": f"z-slab x{nranks}",
+            "l2": "no flush: per-GPU working set 2*s vectors (%.2f GB) >> 126 MB L2"
+                  % (2 * a.s * n * n * (nzg // nranks) * 8 / 1e9)}
 
 
 # --------------------------------------------------------------------------
@@ -65,10 +94,14 @@ def oracle_sample(a, steps, warmup):
     (GDOF/s, seconds per step, description)."""
     import inputs
     import oracle as orc
-    n, zs = a.n, a.cpu_planes
-    A = orc.stencil(orc.KIND_7PT, n, n, zs)
+    n, zs = a.n, min(a.cpu_planes, a.n)
     b = inputs.rhs_uniform(n, n, zs, seed=42)
-    lmin, lmax = inputs.analytic_bounds("7pt", n, n, zs)
+    if a.kind == "varcoef7":
+        A = orc.stencil(orc.KIND_VARCOEF7, n, n, zs, *inputs.lognormal_faces(n, n, zs, seed=42))
+        lmin, lmax, _ = orc.lanczos_bounds(A, 50, b, 0.05)     # untimed setup
+    else:
+        A = orc.stencil({"7pt": orc.KIND_7PT, "27pt": orc.KIND_27PT}[a.kind], n, n, zs)
+        lmin, lmax = inputs.analytic_bounds(a.kind, n, n, zs)
     t0 = time.perf_counter()
     orc.sstep_cg(A, lmin, lmax, a.s, a.nu, b, rtol=0.0, max_outer=warmup)
     t1 = time.perf_counter()
@@ -76,7 +109,7 @@ def oracle_sample(a, steps, warmup):
     t2 = time.perf_counter()
     per = ((t2 - t1) - (t1 - t0)) / steps
     npts = n * n * zs
-    desc = (f"oracle/sscg_oracle.c (gcc -O2 -fopenmp, FP64) on a {n}x{n}x{zs} sample "
+    desc = (f"oracle/sscg_oracle.c (gcc -O2 -fopenmp, FP64), {a.kind}, on a {n}x{n}x{zs} sample "
             f"({npts} unknowns), {steps} outer iterations timed as t(max_outer={warmup + steps}) - "
             f"t(max_outer={warmup})")
     return npts / per / 1e9, per, desc
@@ -208,9 +241,8 @@ def run_ours(a):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, s, nu = a.n, a.s, a.nu
-    nz = n * world
+    nz = n if a.strong else n * world
     z0, nzl = sscg.partition(nz, world, 1, rank)
-    lmin, lmax = inputs.analytic_bounds("7pt", n, n, nz)
     b_host = torch.from_numpy(inputs.rhs_uniform(n, n, nz, seed=42, z0=z0, nzl=nzl)).pin_memory()
     b = b_host.cuda()
     nid = None
@@ -218,7 +250,20 @@ def run_ours(a):
         obj = [sscg.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    S = sscg.Solver(sscg.Stencil("7pt", n, n, nz), lmin, lmax, s, nu, rank=rank, nranks=world, nccl_id=nid)
+    faces = None
+    if a.kind == "varcoef7":
+        kx, ky, kz = inputs.lognormal_faces(n, n, nz, seed=42)
+        faces = [torch.from_numpy(np.ascontiguousarray(f)).cuda()
+                 for f in (kx[z0:z0 + nzl], ky[z0:z0 + nzl], kz[z0:z0 + nzl + 1])]
+        del kx, ky, kz
+        op = sscg.Stencil("varcoef7", n, n, nz, *faces)
+    else:
+        op = sscg.Stencil(a.kind, n, n, nz)
+    if WORKLOADS[a.workload]["bounds"] == "analytic":
+        S = sscg.Solver(op, *inputs.analytic_bounds(a.kind, n, n, nz), s, nu, rank=rank, nranks=world, nccl_id=nid)
+    else:   # 50 Lanczos steps on the GPU, widened 5 % (R13), untimed setup
+        S = sscg.Solver(op, 0.0, 0.0, s, nu, rank=rank, nranks=world, nccl_id=nid)
+        S.set_bounds(*S.estimate_bounds(b, 50, 0.05))
     n_local, n_global = S.n_local, n * n * nz
 
     def barrier():
@@ -253,7 +298,11 @@ def run_ours(a):
     # roofline of the dominant kernel (K1: basis step) and the others
     peak, peak_src = peaks()
     vec = 8.0 * n_local
-    bytes_per_outer = {"basis": (4 * s - 3) * vec, "gram": 2 * s * vec, "update": (2 * s + 3) * vec}
+    face_bytes = 0.0
+    if a.kind == "varcoef7":   # kx, ky, kz of this slab, read by every basis step
+        face_bytes = 8.0 * (n * (n + 1) * S.nz_local * 2 + n * n * (S.nz_local + 1))
+    bytes_per_outer = {"basis": (4 * s - 3) * vec + s * face_bytes, "gram": 2 * s * vec,
+                       "update": (2 * s + 3) * vec}
     kern = {}
     for k, byt in bytes_per_outer.items():
         t_ms, cnt = prof[k]
@@ -268,15 +317,17 @@ def run_ours(a):
                    "share_of_step": t_ms / st_prof.ms_total if st_prof.ms_total else None}
     kern["profiled_pass_ms_per_step"] = st_prof.ms_total / a.steps
     k1 = kern["basis"]
+    path_bytes = sum(bytes_per_outer.values())
     cfg = workload(a, world)
-    roof = {"bound": "hbm", "kernel": "K1 %s<7pt> (SpMV + Jacobi + Chebyshev recurrence)" % K1_NAME,
+    k1_name = {"7pt": K1_NAME, "27pt": K1_NAME, "varcoef7": "k1_stencil"}[a.kind]
+    roof = {"bound": "hbm", "kernel": "K1 %s<%s> (SpMV + Jacobi + Chebyshev recurrence)" % (k1_name, a.kind),
             "achieved": k1["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": k1["frac"],
-            "traffic": ncu_traffic(n, K1_NAME), "peak_source": peak_src,
+            "traffic": ncu_traffic(n, k1_name) if a.workload == "cfg5" else None, "peak_source": peak_src,
             "traffic_note": "ncu dram read+write of one j>=1 launch (algorithmic: 4 vectors = %.4g B)" % (4 * vec),
-            "bytes_rule": "(4s-3) FP64 vectors per outer / s launches (SURVEY 8(d))",
-            "path_bytes_per_step": 64.0 * s * n_local,
-            "path_achieved_gbs": 64.0 * s * n_local / (st.ms_total / a.steps / 1e3) / 1e9,
-            "path_frac": 64.0 * s * n_local / (st.ms_total / a.steps / 1e3) / 1e9 / peak}
+            "bytes_rule": "(4s-3) FP64 vectors (+ s face sets for varcoef7) per outer / s launches (SURVEY 8(d))",
+            "path_bytes_per_step": path_bytes,
+            "path_achieved_gbs": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9,
+            "path_frac": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9 / peak}
     # end-to-end: host b in, host x out, through the C ABI (sscg_solve_host)
     e2e = None
     if not a.no_e2e:

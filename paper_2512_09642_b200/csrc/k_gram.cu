@@ -256,8 +256,12 @@ K2Plan plan(int s)
     p.s_pad = (s + p.TB - 1) / p.TB * p.TB;
     p.nb = p.s_pad / p.TB;
     p.nroles = p.nb * (p.nb + 1) / 2;
-    p.roles_cta = p.nroles < 7 ? p.nroles : 7;   // <= 8 warps: 255 registers per thread
-    p.gy = (p.nroles + p.roles_cta - 1) / p.roles_cta;
+    // <= 7 consumer warps per CTA (255 registers per thread); more roles are
+    // split evenly over gy co-resident CTA groups that stream the same chunks
+    // (launch_k2 shrinks grid.x so that all gy groups are resident at once and
+    // the partner group's TMA loads of a chunk are L2 hits)
+    p.gy = (p.nroles + 6) / 7;
+    p.roles_cta = (p.nroles + p.gy - 1) / p.gy;
     p.nsl = 1;
     while (p.roles_cta * p.nsl * 2 <= 7) p.nsl *= 2;
     const size_t stage = (size_t)2 * p.s_pad * p.E * sizeof(double);
@@ -335,7 +339,7 @@ static void launch_t(const CUtensorMap &a, const CUtensorMap &b, const K2Params 
     k2_gram<TB, E><<<grid, p.threads, p.smem, stream>>>(a, b, k, st);
 }
 
-// partial buffer must hold k2_grid() * gy * (s*s+s) doubles; gy <= 5 for s <= 64
+// partial buffer must hold k2_grid() * (s*s+s) doubles (gx * gy <= k2_grid())
 void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk, cudaStream_t stream)
 {
     const K2Plan p = plan(s);
@@ -352,7 +356,7 @@ void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *
     k.out = out_blk;
     k.ticket = sl.ticket;
     const int64_t nchunks = (k.N + p.E - 1) / p.E;
-    int gx = k2_grid();
+    int gx = std::max(1, k2_grid() / p.gy);   // gx * gy CTAs: one per SM, all resident
     if (const char *e = getenv("SSCG_K2_GRID")) gx = std::max(1, std::min(gx, atoi(e)));   // tuning
     if (nchunks < gx) gx = (int)nchunks;
     dim3 grid(gx, p.gy);

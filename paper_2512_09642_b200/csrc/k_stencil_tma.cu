@@ -1,5 +1,5 @@
-// K1T -- TMA-staged basis step for the constant-coefficient 3D stencils
-// (7-point, 27-point): the same operation as K1 (§2 Def.
+// K1T -- TMA-staged basis step for the 3D stencils (7-point, 27-point,
+// variable-coefficient 7-point): the same operation as K1 (§2 Def.
 // Chebyshev Polynomial Basis)
 //   w_j     = A p_j
 //   p_{j+1} = coef * (M^{-1} w_j - sigma p_j) [- p_{j-1}]
@@ -89,7 +89,7 @@ __device__ __forceinline__ double2 rowsum3(const double *row)
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS, KIND == 3 ? 1 : 2)
     k1t(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, K1Args a,
         const DevState *st, K1TWork wk)
 {
@@ -178,6 +178,17 @@ __global__ void __launch_bounds__(THREADS, 2)
         int64_t ia = (int64_t)zlo * pl + (int64_t)ya * g.pitch + x;
 
         double2 cma, cmb, c0a, c0b, bma = {}, bmb = {}, b0a = {}, b0b = {};
+        // KIND 3: faces of this slab (R12), read straight from global memory
+        // (L1-cached; rows of kx have odd length, no TMA view); lower z-faces
+        // slide through registers
+        const int64_t kxs = (int64_t)g.ny * (g.nx + 1), kys = (int64_t)(g.ny + 1) * g.nx,
+                      kzs = (int64_t)g.ny * g.nx;
+        double kzma0 = 0.0, kzma1 = 0.0, kzmb0 = 0.0, kzmb1 = 0.0;
+        if (KIND == 3) {
+            const double *q = a.kz + (int64_t)(zlo - 1) * kzs + (int64_t)ya * g.nx + x;
+            if (sa) { kzma0 = __ldg(q); if (in1) kzma1 = __ldg(q + 1); }
+            if (sb) { kzmb0 = __ldg(q + g.nx); if (in1) kzmb1 = __ldg(q + g.nx + 1); }
+        }
         uint32_t c0;
         {
             const double *s = waitp(pc);
@@ -205,9 +216,32 @@ __global__ void __launch_bounds__(THREADS, 2)
             ++pc;
         }
         for (int z = zlo; z < zhi; ++z, ia += pl) {
+            // KIND 3: issue this plane's face loads before waiting on the ring
+            double kxa0 = 0, kxa1 = 0, kxa2 = 0, kxb0 = 0, kxb1 = 0, kxb2 = 0;
+            double kya0 = 0, kya1 = 0, kyb0 = 0, kyb1 = 0, kyc0 = 0, kyc1 = 0;
+            double kzpa0 = 0, kzpa1 = 0, kzpb0 = 0, kzpb1 = 0;
+            if (KIND == 3) {
+                const int zl = z - 1;
+                const double *qx = a.kx + zl * kxs + (int64_t)ya * (g.nx + 1) + x;
+                const double *qy = a.ky + zl * kys + (int64_t)ya * g.nx + x;
+                const double *qz = a.kz + (int64_t)(zl + 1) * kzs + (int64_t)ya * g.nx + x;
+                if (sa) {
+                    kxa0 = __ldg(qx); kxa1 = __ldg(qx + 1);
+                    kya0 = __ldg(qy); kyb0 = __ldg(qy + g.nx);
+                    kzpa0 = __ldg(qz);
+                    if (in1) { kxa2 = __ldg(qx + 2); kya1 = __ldg(qy + 1); kyb1 = __ldg(qy + g.nx + 1); kzpa1 = __ldg(qz + 1); }
+                }
+                if (sb) {
+                    kxb0 = __ldg(qx + g.nx + 1); kxb1 = __ldg(qx + g.nx + 2);
+                    kyc0 = __ldg(qy + 2 * g.nx);
+                    kzpb0 = __ldg(qz + g.nx);
+                    if (in1) { kxb2 = __ldg(qx + g.nx + 3); kyc1 = __ldg(qy + 2 * g.nx + 1); kzpb1 = __ldg(qz + g.nx + 1); }
+                }
+            }
             const double *s0 = sp + (c0 % NSP) * PSLOT;   // plane z (7-point: still held)
             const double *s1 = waitp(pc);                  // plane z+1
             double2 Apa, Apb;
+            double2 Da = {}, Db = {};
             const double2 cpa = lds2(s1 + oa), cpb = lds2(s1 + ob);
             if (KIND == 2) {
                 const double2 r0 = rowsum3(s1 + oa - BW), r1 = rowsum3(s1 + oa), r2 = rowsum3(s1 + ob),
@@ -221,6 +255,20 @@ __global__ void __launch_bounds__(THREADS, 2)
                 Apb.y = 27.0 * c0b.y - (bmb.y + b0b.y + bpb.y);
                 bma = b0a; bmb = b0b;
                 b0a = bpa; b0b = bpb;
+            } else if (KIND == 3) {
+                const double2 ylo = lds2(s0 + oa - BW), yhi = lds2(s0 + ob + BW);
+                const double la = s0[oa - 1], rra = s0[oa + 2], lb = s0[ob - 1], rrb = s0[ob + 2];
+                relp(c0);
+                // A_ii = sum of the six faces, A_i,nbr = -k_face (R12); order as K1
+                Da.x = kzma0 + kya0 + kxa0 + kxa1 + kyb0 + kzpa0;
+                Da.y = kzma1 + kya1 + kxa1 + kxa2 + kyb1 + kzpa1;
+                Db.x = kzmb0 + kyb0 + kxb0 + kxb1 + kyc0 + kzpb0;
+                Db.y = kzmb1 + kyb1 + kxb1 + kxb2 + kyc1 + kzpb1;
+                Apa.x = Da.x * c0a.x - (kzma0 * cma.x + kzpa0 * cpa.x + kya0 * ylo.x + kxa0 * la + kxa1 * c0a.y + kyb0 * c0b.x);
+                Apa.y = Da.y * c0a.y - (kzma1 * cma.y + kzpa1 * cpa.y + kya1 * ylo.y + kxa1 * c0a.x + kxa2 * rra + kyb1 * c0b.y);
+                Apb.x = Db.x * c0b.x - (kzmb0 * cmb.x + kzpb0 * cpb.x + kyb0 * c0a.x + kxb0 * lb + kxb1 * c0b.y + kyc0 * yhi.x);
+                Apb.y = Db.y * c0b.y - (kzmb1 * cmb.y + kzpb1 * cpb.y + kyb1 * c0a.y + kxb1 * c0b.x + kxb2 * rrb + kyc1 * yhi.y);
+                kzma0 = kzpa0; kzma1 = kzpa1; kzmb0 = kzpb0; kzmb1 = kzpb1;
             } else {
                 const double2 ylo = lds2(s0 + oa - BW), yhi = lds2(s0 + ob + BW);
                 const double la = s0[oa - 1], rra = s0[oa + 2], lb = s0[ob - 1], rrb = s0[ob + 2];
@@ -249,7 +297,8 @@ __global__ void __launch_bounds__(THREADS, 2)
                 __stcs(reinterpret_cast<double2 *>(a.w + ia), Apa);
                 if (a.mode >= 1) {
                     const double2 dv = a.dinv ? __ldg(reinterpret_cast<const double2 *>(a.dinv + ia))
-                                              : make_double2(a.dinv_c, a.dinv_c);
+                                       : (KIND == 3) ? make_double2(1.0 / Da.x, in1 ? 1.0 / Da.y : 0.0)
+                                                     : make_double2(a.dinv_c, a.dinv_c);
                     double v0 = a.coef * (dv.x * Apa.x - a.sigma * c0a.x);
                     double v1 = a.coef * (dv.y * Apa.y - a.sigma * c0a.y);
                     if (m2) {
@@ -265,7 +314,8 @@ __global__ void __launch_bounds__(THREADS, 2)
                 __stcs(reinterpret_cast<double2 *>(a.w + ib), Apb);
                 if (a.mode >= 1) {
                     const double2 dv = a.dinv ? __ldg(reinterpret_cast<const double2 *>(a.dinv + ib))
-                                              : make_double2(a.dinv_c, a.dinv_c);
+                                       : (KIND == 3) ? make_double2(1.0 / Db.x, in1 ? 1.0 / Db.y : 0.0)
+                                                     : make_double2(a.dinv_c, a.dinv_c);
                     double v0 = a.coef * (dv.x * Apb.x - a.sigma * c0b.x);
                     double v1 = a.coef * (dv.y * Apb.y - a.sigma * c0b.y);
                     if (m2) {
@@ -294,7 +344,7 @@ bool k1t_supported(const Geo &g, const K1Args &a)
         const char *e = getenv("SSCG_K1_TMA");
         off = (e && e[0] == '0') ? 1 : 0;
     }
-    return !off && (g.kind == 1 || g.kind == 2) && a.mode <= 2 && a.tmP4 && a.tmM4;
+    return !off && g.kind >= 1 && g.kind <= 3 && a.mode <= 2 && a.tmP4 && a.tmM4;
 }
 
 bool k1t_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP4, CUtensorMap *tmM4)
@@ -322,7 +372,8 @@ bool k1t_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     if (cudaFuncSetAttribute(k1t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(k1t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
+        cudaFuncSetAttribute(k1t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k1t<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
         return false;
     return true;
 }
@@ -338,9 +389,11 @@ void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t 
     wk.zb = a.zb; wk.ze = a.ze; wk.zb2 = a.zb2; wk.ze2 = a.ze2;
     wk.j = a.j;
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
-    static int occ = 0, zc_env = -1;
+    static int occs[4] = {0, 0, 0, 0}, zc_env = -1;
+    int &occ = occs[g.kind];
     if (!occ) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1t<1>, THREADS, SMEM) != cudaSuccess || occ <= 0)
+        const void *fn = g.kind == 1 ? (const void *)k1t<1> : g.kind == 2 ? (const void *)k1t<2> : (const void *)k1t<3>;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, SMEM) != cudaSuccess || occ <= 0)
             occ = 1;
         const char *e = getenv("SSCG_K1_ZC");
         zc_env = e ? std::max(1, atoi(e)) : 0;
@@ -375,7 +428,8 @@ void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t 
     wk.nitems = tiles * (wk.nch1 + (n2 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
     if (g.kind == 1) k1t<1><<<grid, THREADS, SMEM, s>>>(*a.tmP4, *a.tmM4, g, a, st, wk);
-    else k1t<2><<<grid, THREADS, SMEM, s>>>(*a.tmP4, *a.tmM4, g, a, st, wk);
+    else if (g.kind == 2) k1t<2><<<grid, THREADS, SMEM, s>>>(*a.tmP4, *a.tmM4, g, a, st, wk);
+    else k1t<3><<<grid, THREADS, SMEM, s>>>(*a.tmP4, *a.tmM4, g, a, st, wk);
 }
 
 }  // namespace sscg

@@ -306,7 +306,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         TRY(dalloc(c, &sl.ticket, 1));
         CU(cudaMemsetAsync(sl.ticket, 0, sizeof(unsigned), c->stream));
         if (!k2_prepare(g, sl, s)) return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the Gram pass");
-        if (A->kind == SSCG_OP_STENCIL7 || A->kind == SSCG_OP_STENCIL27) {
+        if (A->kind == SSCG_OP_STENCIL7 || A->kind == SSCG_OP_STENCIL27 || A->kind == SSCG_OP_VARCOEF7) {
             if (!k1t_prepare(g, sl.P, sl.nzl, s, &sl.tmP4, &sl.tmM4))
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the basis step");
             sl.has_k1t = true;
