@@ -301,7 +301,9 @@ def run_ours(a):
     face_bytes = 0.0
     if a.kind == "varcoef7":   # kx, ky, kz of this slab, read by every basis step
         face_bytes = 8.0 * (n * (n + 1) * S.nz_local * 2 + n * n * (S.nz_local + 1))
-    bytes_per_outer = {"basis": (4 * s - 3) * vec + s * face_bytes, "gram": 2 * s * vec,
+    basis_vecs = S.query(sscg.QUERY_BASIS_VECTORS)       # (4s-3), or 46 at s = 16 with K1F pairs
+    fused = bool(S.query(sscg.QUERY_BASIS_FUSED))
+    bytes_per_outer = {"basis": basis_vecs * vec + s * face_bytes, "gram": 2 * s * vec,
                        "update": (2 * s + 3) * vec}
     kern = {}
     for k, byt in bytes_per_outer.items():
@@ -319,12 +321,15 @@ def run_ours(a):
     k1 = kern["basis"]
     path_bytes = sum(bytes_per_outer.values())
     cfg = workload(a, world)
-    k1_name = {"7pt": K1_NAME, "27pt": K1_NAME, "varcoef7": "k1_stencil"}[a.kind]
-    roof = {"bound": "hbm", "kernel": "K1 %s<%s> (SpMV + Jacobi + Chebyshev recurrence)" % (k1_name, a.kind),
+    k1_name = "k1f" if fused else K1_NAME
+    roof = {"bound": "hbm", "kernel": "K1 %s<%s> (%sSpMV + Jacobi + Chebyshev recurrence)"
+                                      % (k1_name, a.kind, "two basis steps per launch: " if fused else ""),
             "achieved": k1["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": k1["frac"],
             "traffic": ncu_traffic(n, k1_name) if a.workload == "cfg5" else None, "peak_source": peak_src,
-            "traffic_note": "ncu dram read+write of one j>=1 launch (algorithmic: 4 vectors = %.4g B)" % (4 * vec),
-            "bytes_rule": "(4s-3) FP64 vectors (+ s face sets for varcoef7) per outer / s launches (SURVEY 8(d))",
+            "traffic_note": "ncu dram read+write of one interior launch (algorithmic: %d vectors = %.4g B)"
+                            % (6 if fused else 4, (6 if fused else 4) * vec),
+            "bytes_rule": "%d FP64 vectors per outer (%s) + s face sets for varcoef7, / basis launches (SURVEY 8(d))"
+                          % (basis_vecs, "K1F pairs: 6 per pair" if fused else "(4s-3)"),
             "path_bytes_per_step": path_bytes,
             "path_achieved_gbs": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9,
             "path_frac": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9 / peak}

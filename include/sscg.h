@@ -262,6 +262,16 @@ enum { SSCG_GRAM_FGS = 0, SSCG_GRAM_CHOLESKY = 1 };
 enum { SSCG_BASIS_CHEBYSHEV = 0, SSCG_BASIS_MONOMIAL = 1 };
 SSCG_API sscg_status sscg_set_option(sscg_ctx *ctx, int32_t key, int32_t value);
 
+/* Introspection of the schedule the context runs (host, no GPU work):
+ *   SSCG_QUERY_BASIS_FUSED    1 if basis steps run in pairs (K1F: p_{j+1}
+ *                             kept on chip, single-slab 7-point), else 0
+ *   SSCG_QUERY_BASIS_VECTORS  FP64 vectors of n_local the basis kernels read
+ *                             and write per outer iteration (algorithmic;
+ *                             variable-coefficient face arrays not included)
+ * Errors: SSCG_ERR_INVALID. */
+enum { SSCG_QUERY_BASIS_FUSED = 0, SSCG_QUERY_BASIS_VECTORS = 1 };
+SSCG_API sscg_status sscg_query(const sscg_ctx *ctx, int32_t what, int64_t *out);
+
 SSCG_API void sscg_destroy(sscg_ctx *ctx);
 
 /* Thread-local description of the last error ("" if none). */

@@ -30,10 +30,11 @@ SOLVE_X0_ZERO = 1
 OPT_GRAM_SOLVER, OPT_BASIS = 0, 1
 GRAM_FGS, GRAM_CHOLESKY = 0, 1
 BASIS_CHEBYSHEV, BASIS_MONOMIAL = 0, 1
+QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS = 0, 1
 
 EXPORTS = ["sscg_partition", "sscg_halo_plan", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host", "sscg_iterate",
            "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect", "sscg_local_shape", "sscg_destroy",
-           "sscg_last_error", "sscg_version", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds"]
+           "sscg_last_error", "sscg_version", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds", "sscg_query"]
 PROF_NAMES = ["basis", "gram", "allreduce", "fgs", "update", "halo"]
 
 
@@ -94,13 +95,14 @@ def load(path: str = LIB_PATH):
     L.sscg_set_bounds.argtypes = [vp, d, d]
     L.sscg_set_option.argtypes = [vp, i32, i32]
     L.sscg_estimate_bounds.argtypes = [vp, vp, i32, d, C.POINTER(d), C.POINTER(d), vp, vp]
+    L.sscg_query.argtypes = [vp, i32, C.POINTER(i64)]
     L.sscg_destroy.argtypes = [vp]
     L.sscg_destroy.restype = None
     L.sscg_last_error.restype = C.c_char_p
     L.sscg_version.restype = C.c_char_p
     for name in ("sscg_partition", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host",
                  "sscg_iterate", "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect",
-                 "sscg_local_shape", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds"):
+                 "sscg_local_shape", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds", "sscg_query"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -214,6 +216,11 @@ class Solver:
             self.set_option(OPT_GRAM_SOLVER, {"fgs": GRAM_FGS, "cholesky": GRAM_CHOLESKY}[gram_solver])
         if basis != "chebyshev":
             self.set_option(OPT_BASIS, {"chebyshev": BASIS_CHEBYSHEV, "monomial": BASIS_MONOMIAL}[basis])
+
+    def query(self, what: int) -> int:
+        v = C.c_int64()
+        _check(load().sscg_query(self._h, what, C.byref(v)))
+        return v.value
 
     def set_bounds(self, lmin: float, lmax: float):
         _check(load().sscg_set_bounds(self._h, lmin, lmax))

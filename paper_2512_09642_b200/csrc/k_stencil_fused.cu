@@ -1,0 +1,355 @@
+// K1F -- two basis steps in one pass (7-point, single slab): the pair
+// (j, j+1) of the Chebyshev recurrence
+//   w_j     = A p_j,      p_{j+1} = c_j (D^{-1} w_j - sigma p_j) [- p_{j-1}]
+//   w_{j+1} = A p_{j+1},  p_{j+2} = 2 theta (D^{-1} w_{j+1} - sigma p_{j+1}) - p_j
+// with p_{j+1} kept on chip between the two steps (SURVEY §8(f) NEXT-3,
+// "matrix-powers" blocking of depth 2).  Per pair it streams p_j and p_{j-1}
+// in and w_j, p_{j+1}, w_{j+1}, p_{j+2} out: 6 vectors instead of the 8 of two
+// K1 launches (the per-outer basis traffic drops from 4s-3 = 61 to 46 vectors
+// at s = 16).
+//
+// Same arithmetic, operand for operand, as K1T (k_stencil_tma.cu): the
+// front step computes p_{j+1} on the tile plus a one-cell x/y halo (the halo
+// values are recomputed redundantly by neighbouring tiles) from p_j staged by
+// TMA with a two-cell halo; cells outside the global grid are forced to the
+// Dirichlet value 0.
+//
+// Pipeline over the planes q of a z-chunk [zlo, zhi):
+//   front(q):  w_j(q), p_{j+1}(q) on the tile (written when zlo <= q < zhi),
+//              p_{j+1}(q) on tile + halo into the shared ring U (4 planes)
+//   back(q-1): w_{j+1}, p_{j+2} at plane q-1 from U(q-2..q) and p_j(q-1)
+// Warp 0 produces (TMA boxes of p_j and p_{j-1} into mbarrier rings), warps
+// 1..NCW consume (one front and one back task per thread and plane); one
+// named barrier per plane orders front(q) before back(q-1).  The kernel runs
+// at the HBM write-heavy mix ceiling (1 read : 2 writes, profiles/r01e).
+#include <algorithm>
+#include <cstdlib>
+
+#include "sscg_internal.cuh"
+#include "tma.cuh"
+
+namespace sscg {
+namespace {
+
+constexpr int TX = 64, TY = 16;
+constexpr int BW = TX + 4;                 // all staged planes: x in [x0-2, x0+TX+2)
+constexpr int BHP = TY + 4;                // p_j: y in [y0-2, y0+TY+2)
+constexpr int BHM = TY + 2;                // p_{j-1}: y in [y0-1, y0+TY+1)
+constexpr int PS = BW * BHP;               // doubles per p_j / U slot (10880 B, 128-B multiple)
+constexpr int MS = ((BW * BHM * 8 + 127) / 128) * 128 / 8;
+constexpr int NSP = 8, NSM = 6, NU = 4;
+constexpr int NCW = 20;
+constexpr int NCT = NCW * 32;
+constexpr int THREADS = NCT + 32;
+constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = BW * BHM * 8;
+constexpr size_t SMEM = (size_t)(NSP * PS + NSM * MS + NU * PS) * sizeof(double);
+constexpr int FRONT_TASKS = (TY + 2) * (BW / 2);   // 18 rows x 34 pairs
+constexpr int BACK_TASKS = TY * (TX / 2);          // 16 rows x 32 pairs
+
+struct K1FWork {
+    int tiles_x, tiles_y, zc;
+    int64_t nitems;
+    int nzl;
+    int j;
+    int front_pm;          // p_{j-1} term in the front step (j >= 1)
+    int back_pn;           // the back step writes p_{j+2} (j+1 < s-1)
+    double coef_front, coef_back, sigma, center, dinv_c;
+};
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int x, int y, int z, int v,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(v), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
+
+__device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+
+// planes of p_j loaded for an item: [plo, phi] (the front needs q-1..q+1 for
+// q in [zlo-1, zhi] inside the slab's padded range [0, nzl+1])
+struct ItemPlan {
+    int tx, ty, zlo, zhi, plo, phi, mlo, mhi;
+};
+
+__device__ __forceinline__ ItemPlan plan_item(const K1FWork &wk, int64_t item)
+{
+    const int ntiles = wk.tiles_x * wk.tiles_y;
+    const int chunk = (int)(item / ntiles);
+    const int tile = (int)(item - (int64_t)chunk * ntiles);
+    ItemPlan p;
+    p.ty = tile / wk.tiles_x;
+    p.tx = tile - p.ty * wk.tiles_x;
+    p.zlo = 1 + chunk * wk.zc;
+    p.zhi = min(wk.nzl + 1, p.zlo + wk.zc);
+    p.plo = max(p.zlo - 2, 0);
+    p.phi = min(p.zhi + 1, wk.nzl + 1);
+    p.mlo = max(p.zlo - 1, 1);   // p_{j-1} planes used by front(q), 1 <= q <= nzl
+    p.mhi = min(p.zhi, wk.nzl);
+    return p;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k1f(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, K1Args a,
+        const DevState *st, K1FWork wk)
+{
+    if (st && st->done) return;
+    extern __shared__ __align__(128) double smem[];
+    double *sp = smem;                       // p_j ring
+    double *sm = smem + NSP * PS;            // p_{j-1} ring
+    double *su = sm + NSM * MS;              // U = p_{j+1} on tile + halo, NU planes
+    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int i = 0; i < NSP; ++i) {
+            mbar_init(&fullp[i], 1);
+            mbar_init(&emptyp[i], NCW);
+        }
+        for (int i = 0; i < NSM; ++i) {
+            mbar_init(&fullm[i], 1);
+            mbar_init(&emptym[i], NCW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmP);
+        tma_prefetch_desc(&tmM);
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t pc = 0, mc = 0;
+            for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+                const ItemPlan it = plan_item(wk, item);
+                const int x0 = it.tx * TX, y0 = it.ty * TY;
+                int pnext = it.plo, mnext = it.mlo;
+                for (int q = it.zlo - 1; q <= it.zhi; ++q) {
+                    while (pnext <= min(q + 1, it.phi)) {
+                        const int sl = pc % NSP;
+                        if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
+                        mbar_expect_tx(&fullp[sl], PBYTES);
+                        tma_load_4d(sp + sl * PS, &tmP, x0 - 2, y0 - 2, pnext, wk.j, &fullp[sl]);
+                        ++pc;
+                        ++pnext;
+                    }
+                    if (wk.front_pm && q >= it.mlo && q <= it.mhi) {
+                        const int sl = mc % NSM;
+                        if (mc >= NSM) mbar_wait(&emptym[sl], ((mc / NSM) - 1) & 1);
+                        mbar_expect_tx(&fullm[sl], MBYTES);
+                        tma_load_4d(sm + sl * MS, &tmM, x0 - 2, y0 - 1, q, wk.j - 1, &fullm[sl]);
+                        ++mc;
+                        ++mnext;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    const int ct = tid - 32;   // consumer thread 0..255
+    uint32_t pc = 0, mc = 0;   // sequence numbers of the next p_j / p_{j-1} slot to consume
+    const int64_t pl = g.plane;
+    for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+        const ItemPlan it = plan_item(wk, item);
+        const int x0 = it.tx * TX, y0 = it.ty * TY;
+        // slot of p_j plane z: pc_base + (z - plo) while the item lasts
+        const uint32_t pbase = pc;
+        int pwaited = it.plo - 1;   // highest plane waited for
+        for (int q = it.zlo - 1; q <= it.zhi; ++q) {
+            const int need = min(q + 1, it.phi);
+            while (pwaited < need) {
+                ++pwaited;
+                const uint32_t c = pbase + (pwaited - it.plo);
+                mbar_wait(&fullp[c % NSP], (c / NSP) & 1);
+            }
+            auto pslot = [&](int z) -> const double * { return sp + ((pbase + (z - it.plo)) % NSP) * PS; };
+            double *U = su + ((q + 8) % NU) * PS;
+            // ---------------- front(q): step j on tile + halo ----------------
+            const bool inside = q >= 1 && q <= wk.nzl;
+            const bool mloaded = wk.front_pm && q >= it.mlo && q <= it.mhi;
+            const double *M = nullptr;
+            if (mloaded) {
+                mbar_wait(&fullm[mc % NSM], (mc / NSM) & 1);
+                M = sm + (mc % NSM) * MS;
+            }
+            const bool own = q >= it.zlo && q < it.zhi;
+            for (int t = ct; t < FRONT_TASKS; t += NCT) {
+                const int r = 1 + t / (BW / 2);          // box row 1..18
+                const int col = 2 * (t % (BW / 2));      // box col 0..66 (pair col, col+1)
+                const int gx = x0 - 2 + col, gy = y0 - 2 + r;
+                double2 u = make_double2(0.0, 0.0);
+                if (inside) {
+                    const double *P0 = pslot(q), *Pm = pslot(q - 1), *Pp = pslot(q + 1);
+                    const int o = r * BW + col;
+                    const double2 c = lds2(P0 + o);
+                    const double2 dn = lds2(Pm + o), up = lds2(Pp + o);
+                    const double2 ylo = lds2(P0 + o - BW), yhi = lds2(P0 + o + BW);
+                    const double l = (col > 0) ? P0[o - 1] : 0.0;
+                    const double rr = (col + 2 < BW) ? P0[o + 2] : 0.0;
+                    double2 Ap;
+                    Ap.x = wk.center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                    Ap.y = wk.center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                    double2 pm = make_double2(0.0, 0.0);
+                    if (mloaded) pm = lds2(M + (r - 1) * BW + col);
+                    u.x = wk.coef_front * (wk.dinv_c * Ap.x - wk.sigma * c.x);
+                    u.y = wk.coef_front * (wk.dinv_c * Ap.y - wk.sigma * c.y);
+                    if (wk.front_pm) {
+                        u.x -= pm.x;
+                        u.y -= pm.y;
+                    }
+                    const bool vy = gy >= 0 && gy < g.ny;
+                    const bool v0 = vy && gx >= 0 && gx < g.nx, v1 = vy && gx + 1 >= 0 && gx + 1 < g.nx;
+                    if (!v0) u.x = 0.0;
+                    if (!v1) u.y = 0.0;
+                    // the tile's own cells go to HBM (w_j and p_{j+1})
+                    if (own && r >= 2 && r < TY + 2 && col >= 2 && col < TX + 2 && v0) {
+                        const int64_t i = (int64_t)q * pl + (int64_t)gy * g.pitch + gx;
+                        if (!v1) Ap.y = 0.0;
+                        __stcs(reinterpret_cast<double2 *>(a.w + i), Ap);
+                        *reinterpret_cast<double2 *>(a.pn + i) = u;
+                    }
+                }
+                *reinterpret_cast<double2 *>(U + r * BW + col) = u;
+            }
+            if (mloaded) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptym[mc % NSM]);
+                ++mc;
+            }
+            consumers_sync();   // U(q) complete; U(q-4) no longer read
+            // ---------------- back(q-1): step j+1 on the tile ----------------
+            const int z = q - 1;
+            if (z >= it.zlo && z < it.zhi) {
+                const double *Um = su + ((z - 1 + 8) % NU) * PS, *U0 = su + ((z + 8) % NU) * PS, *Up = U;
+                const double *Pz = pslot(z);
+                for (int t = ct; t < BACK_TASKS; t += NCT) {
+                    const int r = 2 + t / (TX / 2);
+                    const int col = 2 + 2 * (t % (TX / 2));
+                    const int gx = x0 - 2 + col, gy = y0 - 2 + r;
+                    if (gy >= g.ny || gx >= g.nx) continue;
+                    const int o = r * BW + col;
+                    const double2 c = lds2(U0 + o);
+                    const double2 dn = lds2(Um + o), up = lds2(Up + o);
+                    const double2 ylo = lds2(U0 + o - BW), yhi = lds2(U0 + o + BW);
+                    const double l = U0[o - 1], rr = U0[o + 2];
+                    double2 Ap;
+                    Ap.x = wk.center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                    Ap.y = wk.center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                    const bool v1 = gx + 1 < g.nx;
+                    if (!v1) Ap.y = 0.0;
+                    const int64_t i = (int64_t)z * pl + (int64_t)gy * g.pitch + gx;
+                    __stcs(reinterpret_cast<double2 *>(a.w2 + i), Ap);
+                    if (wk.back_pn) {
+                        const double2 pj = lds2(Pz + o);
+                        double v0 = wk.coef_back * (wk.dinv_c * Ap.x - wk.sigma * c.x) - pj.x;
+                        double v1v = wk.coef_back * (wk.dinv_c * Ap.y - wk.sigma * c.y) - pj.y;
+                        if (!v1) v1v = 0.0;
+                        *reinterpret_cast<double2 *>(a.pn2 + i) = make_double2(v0, v1v);
+                    }
+                }
+            }
+            // p_j plane q-1 is no longer needed (front(q+1) reads q..q+2)
+            if (q - 1 >= it.plo) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyp[(pbase + (q - 1 - it.plo)) % NSP]);
+            }
+        }
+        // release the p_j planes of this item not released in the loop: zhi, zhi+1 (if loaded)
+        for (int z = max(it.zhi, it.plo); z <= it.phi; ++z) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&emptyp[(pbase + (z - it.plo)) % NSP]);
+        }
+        pc = pbase + (it.phi - it.plo + 1);
+    }
+}
+
+}  // namespace
+
+bool k1f_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+        return false;
+    auto enc = reinterpret_cast<CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                             CUtensorMapFloatOOBfill)>(fn);
+    cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)(nzl + 2), (cuuint64_t)s};
+    cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.vstride * 8};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint32_t boxp[4] = {BW, BHP, 1, 1}, boxm[4] = {BW, BHM, 1, 1};
+    if (enc(tmP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxp, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (enc(tmM, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxm, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    return cudaFuncSetAttribute(k1f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+}
+
+bool k1f_enabled()
+{
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("SSCG_K1_FUSE");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// steps j and j+1 over all planes of a single slab (a.p = p_j, a.pm = p_{j-1}
+// or null, a.w = w_j, a.pn = p_{j+1}, a.w2 = w_{j+1}, a.pn2 = p_{j+2} or null)
+void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm)
+{
+    K1FWork wk;
+    wk.tiles_x = (g.nx + TX - 1) / TX;
+    wk.tiles_y = (g.ny + TY - 1) / TY;
+    wk.nzl = a.nzl;
+    wk.j = a.j;
+    wk.front_pm = a.j > 0;
+    wk.back_pn = (a.j + 1 < s - 1) ? 1 : 0;
+    wk.coef_front = (a.j == 0) ? theta : 2.0 * theta;
+    wk.coef_back = 2.0 * theta;
+    wk.sigma = a.sigma;
+    wk.center = g.center;
+    wk.dinv_c = g.dinv_c;
+    const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
+    const int64_t resident = k2_grid();   // one CTA per SM
+    static int zc_env = -1;
+    if (zc_env < 0) {
+        const char *e = getenv("SSCG_K1_ZC");
+        zc_env = e ? std::max(1, atoi(e)) : 0;
+    }
+    const int n1 = a.nzl;
+    int zc = n1;
+    if (zc_env > 0) {
+        zc = std::min(n1, zc_env);
+    } else {
+        // few long chunks (each re-reads 4 planes of p_j and recomputes 2
+        // front planes), tiles x chunks filling whole waves of the grid
+        double best = -1.0;
+        for (int nch = 1; nch <= 64 && (n1 + nch - 1) / nch >= 4; ++nch) {
+            const int64_t items = tiles * nch;
+            const int64_t waves = (items + resident - 1) / resident;
+            const int z = (n1 + nch - 1) / nch;
+            const double score = (double)items / (double)(waves * resident) / (1.0 + 1.0 / z);
+            if (score > best + 1e-9) {
+                best = score;
+                zc = z;
+            }
+        }
+    }
+    wk.zc = zc;
+    wk.nitems = tiles * ((n1 + zc - 1) / zc);
+    const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
+    k1f<<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, g, a, st, wk);
+}
+
+}  // namespace sscg

@@ -311,6 +311,11 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the basis step");
             sl.has_k1t = true;
         }
+        if (A->kind == SSCG_OP_STENCIL7 && !diag_M && c->nranks * c->spr == 1 && k1f_enabled()) {
+            if (!k1f_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
+                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused basis step");
+            sl.has_k1f = true;
+        }
         if (A->kind == SSCG_OP_VARCOEF7) {
             sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
             sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;
@@ -544,6 +549,31 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
     return SSCG_OK;
 }
 
+// K1F: basis steps j, j+1 of the single slab in one launch
+static sscg_status launch_basis_pair(sscg_ctx *c, int j)
+{
+    const Geo &g = c->g;
+    const int s = c->s;
+    auto &sl = c->slabs[0];
+    K1Args a{};
+    a.p = sl.P + (int64_t)j * g.vstride;
+    a.pm = (j > 0) ? sl.P + (int64_t)(j - 1) * g.vstride : nullptr;
+    a.w = sl.W + (int64_t)j * g.vstride;
+    a.pn = sl.P + (int64_t)(j + 1) * g.vstride;
+    a.w2 = sl.W + (int64_t)(j + 1) * g.vstride;
+    a.pn2 = (j + 2 < s) ? sl.P + (int64_t)(j + 2) * g.vstride : nullptr;
+    a.sigma = c->sigma;
+    a.nzl = sl.nzl;
+    a.j = j;
+    a.tmF_P = &sl.tmF_P;
+    a.tmF_M = &sl.tmF_M;
+    TRY(prof_mark(c, SSCG_PROF_BASIS, true));
+    launch_k1f(g, a, c->theta, s, c->st, c->stream);
+    TRY(prof_mark(c, SSCG_PROF_BASIS, false));
+    ++c->launches;
+    return SSCG_OK;
+}
+
 // One outer iteration.  Precondition: the halo planes of p_0 are current.
 //   for j: K1 boundary planes -> fork halo(p_{j+1}) -> K1 interior -> join
 //   K2 (+ slab sum) -> allreduce -> K4 -> K5 boundary -> fork halo(p_0) -> K5 interior -> join
@@ -554,8 +584,12 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const int L = (int)c->slabs.size();
     const bool halo = (L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR;
     const bool ovl = halo && c->overlap;
+    const bool fuse = !halo && L == 1 && c->slabs[0].has_k1f && c->basis == SSCG_BASIS_CHEBYSHEV;
     for (int j = 0; j < s; ++j) {
-        if (!halo) {
+        if (fuse && j + 1 < s) {   // steps j and j+1 in one pass (K1F)
+            TRY(launch_basis_pair(c, j));
+            ++j;
+        } else if (!halo) {
             TRY(launch_basis(c, j, 0));
         } else if (!ovl) {
             if (j > 0) TRY(halo_fork(c, j, false));
@@ -1066,4 +1100,43 @@ extern "C" sscg_status sscg_estimate_bounds(sscg_ctx *c, const double *v0, int32
     if (!(out[0] > 0.0) || !(out[1] > out[0]) || !std::isfinite(out[1]))
         return fail(SSCG_ERR_BREAKDOWN, "Lanczos gave no valid interval (%g, %g)", out[0], out[1]);
     return SSCG_OK;
+}
+
+// algorithmic bytes per outer iteration of the basis kernels under the
+// schedule enqueue_outer uses, and whether K1F pairs are used
+static bool uses_fused(const sscg_ctx *c)
+{
+    const int L = (int)c->slabs.size();
+    return L == 1 && c->nranks == 1 && c->slabs[0].has_k1f && c->basis == SSCG_BASIS_CHEBYSHEV &&
+           c->g.kind != SSCG_OP_CSR;
+}
+
+extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
+{
+    if (!c || !out) return fail(SSCG_ERR_INVALID, "null argument");
+    const int s = c->s;
+    const bool mono = c->basis == SSCG_BASIS_MONOMIAL;
+    switch (what) {
+    case SSCG_QUERY_BASIS_FUSED:
+        *out = uses_fused(c) ? 1 : 0;
+        return SSCG_OK;
+    case SSCG_QUERY_BASIS_VECTORS: {
+        // FP64 vectors of n_local read + written by the basis steps of one outer
+        int64_t v = 0;
+        if (uses_fused(c)) {
+            int j = 0;
+            for (; j + 1 < s; j += 2) v += 1 + (j > 0) + 3 + (j + 2 < s);
+            if (j < s) v += 2;   // odd s: the last step alone (mode 0: reads p_{s-1}, writes w_{s-1})
+        } else {
+            for (int j = 0; j < s; ++j) {
+                const bool pn = j < s - 1, pm = !mono && j > 0 && pn;
+                v += 1 + pm + 1 + pn;
+            }
+        }
+        *out = v;
+        return SSCG_OK;
+    }
+    default:
+        return fail(SSCG_ERR_INVALID, "unknown query %d", what);
+    }
 }

@@ -44,6 +44,8 @@ struct Slab {
     CUtensorMap tmP, tmW;         // K2: [s rows x interior] views of P and W
     CUtensorMap tmP4, tmM4;       // K1T: 4-D [x][y][plane][vector] views of P (halo box / tile box)
     bool has_k1t;
+    CUtensorMap tmF_P, tmF_M;     // K1F: 2-cell / 1-cell halo boxes
+    bool has_k1f;
 };
 
 struct Geo {
@@ -83,6 +85,8 @@ struct K1Args {
     int nzl;
     int j;                 // basis step (K1T: vector coordinate of p_j in the tensor maps)
     const CUtensorMap *tmP4, *tmM4;   // K1T tensor maps of this slab (host memory), or nullptr
+    double *w2, *pn2;                 // K1F: w_{j+1}, p_{j+2} (nullptr at j+1 = s-1)
+    const CUtensorMap *tmF_P, *tmF_M; // K1F tensor maps
 };
 
 void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s);
@@ -91,6 +95,11 @@ void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s
 bool k1t_supported(const Geo &g, const K1Args &a);
 bool k1t_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP4, CUtensorMap *tmM4);
 void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s);
+
+// K1F: two 7-point basis steps per launch, single slab (k_stencil_fused.cu)
+bool k1f_enabled();
+bool k1f_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM);
+void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm);
 
 // copy a process-layout grid function into the padded interior of `dst`
 void launch_pack(const Geo &g, const double *src, double *dst, int nzl, const DevState *st,
