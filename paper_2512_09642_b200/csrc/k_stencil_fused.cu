@@ -50,6 +50,7 @@ struct K1FWork {
     int tiles_x, tiles_y, zc;
     int64_t nitems;
     int nzl;
+    int zb, ze;            // planes written by both steps: [zb, ze) within [1, nzl]
     int j;
     int front_pm;          // p_{j-1} term in the front step (j >= 1)
     int back_pn;           // the back step writes p_{j+2} (j+1 < s-1)
@@ -84,8 +85,8 @@ __device__ __forceinline__ ItemPlan plan_item(const K1FWork &wk, int64_t item)
     ItemPlan p;
     p.ty = tile / wk.tiles_x;
     p.tx = tile - p.ty * wk.tiles_x;
-    p.zlo = 1 + chunk * wk.zc;
-    p.zhi = min(wk.nzl + 1, p.zlo + wk.zc);
+    p.zlo = wk.zb + chunk * wk.zc;
+    p.zhi = min(wk.ze, p.zlo + wk.zc);
     p.plo = max(p.zlo - 2, 0);
     p.phi = min(p.zhi + 1, wk.nzl + 1);
     p.mlo = max(p.zlo - 1, 1);   // p_{j-1} planes used by front(q), 1 <= q <= nzl
@@ -296,22 +297,24 @@ bool k1f_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
 
 bool k1f_enabled()
 {
-    static int on = -1;
-    if (on < 0) {
-        const char *e = getenv("SSCG_K1_FUSE");
-        on = (e && e[0] == '0') ? 0 : 1;
-    }
-    return on == 1;
+    const char *e = getenv("SSCG_K1_FUSE");   // read at every sscg_setup
+    return !(e && e[0] == '0');
 }
 
-// steps j and j+1 over all planes of a single slab (a.p = p_j, a.pm = p_{j-1}
-// or null, a.w = w_j, a.pn = p_{j+1}, a.w2 = w_{j+1}, a.pn2 = p_{j+2} or null)
+// steps j and j+1 over the planes [a.zb, a.ze) of one slab (a.p = p_j, a.pm =
+// p_{j-1} or null, a.w = w_j, a.pn = p_{j+1}, a.w2 = w_{j+1}, a.pn2 = p_{j+2}
+// or null).  The halo planes of p_j must be current.  With [1, nzl+1) the
+// slab is treated as bounded by Dirichlet planes in z (p_{j+1} = 0 outside),
+// so a slab with neighbours passes [2, nzl) and runs its boundary planes with
+// single steps around the exchange of p_{j+1}.
 void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm)
 {
     K1FWork wk;
     wk.tiles_x = (g.nx + TX - 1) / TX;
     wk.tiles_y = (g.ny + TY - 1) / TY;
     wk.nzl = a.nzl;
+    wk.zb = a.zb;
+    wk.ze = a.ze;
     wk.j = a.j;
     wk.front_pm = a.j > 0;
     wk.back_pn = (a.j + 1 < s - 1) ? 1 : 0;
@@ -327,7 +330,8 @@ void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevSta
         const char *e = getenv("SSCG_K1_ZC");
         zc_env = e ? std::max(1, atoi(e)) : 0;
     }
-    const int n1 = a.nzl;
+    const int n1 = a.ze - a.zb;
+    if (n1 <= 0) return;
     int zc = n1;
     if (zc_env > 0) {
         zc = std::min(n1, zc_env);

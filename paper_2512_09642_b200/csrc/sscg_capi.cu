@@ -311,7 +311,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the basis step");
             sl.has_k1t = true;
         }
-        if (A->kind == SSCG_OP_STENCIL7 && !diag_M && c->nranks * c->spr == 1 && k1f_enabled()) {
+        if (A->kind == SSCG_OP_STENCIL7 && !diag_M && k1f_enabled()) {
             if (!k1f_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused basis step");
             sl.has_k1f = true;
@@ -549,28 +549,44 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
     return SSCG_OK;
 }
 
-// K1F: basis steps j, j+1 of the single slab in one launch
-static sscg_status launch_basis_pair(sscg_ctx *c, int j)
+// K1F pairs are used when every slab has the fused tensor maps (7-point,
+// constant diagonal) and, with neighbours, enough planes for an interior
+static bool uses_fused(const sscg_ctx *c)
+{
+    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->g.kind != SSCG_OP_STENCIL7) return false;
+    const bool halo = c->slabs.size() > 1 || c->nranks > 1;
+    for (const auto &sl : c->slabs)
+        if (!sl.has_k1f || (halo && sl.nzl < 4)) return false;
+    return true;
+}
+
+// K1F: basis steps j, j+1 in one launch per slab, over all planes (part 0,
+// a slab bounded by the global Dirichlet planes) or the planes [2, nzl) that
+// need no halo of p_{j+1} (part 2)
+static sscg_status launch_basis_pair(sscg_ctx *c, int j, int part)
 {
     const Geo &g = c->g;
     const int s = c->s;
-    auto &sl = c->slabs[0];
-    K1Args a{};
-    a.p = sl.P + (int64_t)j * g.vstride;
-    a.pm = (j > 0) ? sl.P + (int64_t)(j - 1) * g.vstride : nullptr;
-    a.w = sl.W + (int64_t)j * g.vstride;
-    a.pn = sl.P + (int64_t)(j + 1) * g.vstride;
-    a.w2 = sl.W + (int64_t)(j + 1) * g.vstride;
-    a.pn2 = (j + 2 < s) ? sl.P + (int64_t)(j + 2) * g.vstride : nullptr;
-    a.sigma = c->sigma;
-    a.nzl = sl.nzl;
-    a.j = j;
-    a.tmF_P = &sl.tmF_P;
-    a.tmF_M = &sl.tmF_M;
-    TRY(prof_mark(c, SSCG_PROF_BASIS, true));
-    launch_k1f(g, a, c->theta, s, c->st, c->stream);
-    TRY(prof_mark(c, SSCG_PROF_BASIS, false));
-    ++c->launches;
+    for (auto &sl : c->slabs) {
+        K1Args a{};
+        a.p = sl.P + (int64_t)j * g.vstride;
+        a.pm = (j > 0) ? sl.P + (int64_t)(j - 1) * g.vstride : nullptr;
+        a.w = sl.W + (int64_t)j * g.vstride;
+        a.pn = sl.P + (int64_t)(j + 1) * g.vstride;
+        a.w2 = sl.W + (int64_t)(j + 1) * g.vstride;
+        a.pn2 = (j + 2 < s) ? sl.P + (int64_t)(j + 2) * g.vstride : nullptr;
+        a.sigma = c->sigma;
+        a.nzl = sl.nzl;
+        a.zb = (part == 0) ? 1 : 2;
+        a.ze = (part == 0) ? sl.nzl + 1 : sl.nzl;
+        a.j = j;
+        a.tmF_P = &sl.tmF_P;
+        a.tmF_M = &sl.tmF_M;
+        TRY(prof_mark(c, SSCG_PROF_BASIS, true));
+        launch_k1f(g, a, c->theta, s, c->st, c->stream);
+        TRY(prof_mark(c, SSCG_PROF_BASIS, false));
+        ++c->launches;
+    }
     return SSCG_OK;
 }
 
@@ -584,10 +600,21 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const int L = (int)c->slabs.size();
     const bool halo = (L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR;
     const bool ovl = halo && c->overlap;
-    const bool fuse = !halo && L == 1 && c->slabs[0].has_k1f && c->basis == SSCG_BASIS_CHEBYSHEV;
+    const bool fuse = uses_fused(c);
     for (int j = 0; j < s; ++j) {
         if (fuse && j + 1 < s) {   // steps j and j+1 in one pass (K1F)
-            TRY(launch_basis_pair(c, j));
+            if (!halo) {
+                TRY(launch_basis_pair(c, j, 0));
+            } else {
+                // boundary planes of step j, exchange of p_{j+1} (overlapped with
+                // the interior pair), boundary planes of step j+1, exchange of p_{j+2}
+                TRY(launch_basis(c, j, 1));
+                TRY(halo_fork(c, j + 1, ovl));
+                TRY(launch_basis_pair(c, j, 2));
+                if (ovl) TRY(halo_join(c));
+                TRY(launch_basis(c, j + 1, 1));
+                if (j + 2 < s) TRY(halo_fork(c, j + 2, false));
+            }
             ++j;
         } else if (!halo) {
             TRY(launch_basis(c, j, 0));
@@ -1103,13 +1130,7 @@ extern "C" sscg_status sscg_estimate_bounds(sscg_ctx *c, const double *v0, int32
 }
 
 // algorithmic bytes per outer iteration of the basis kernels under the
-// schedule enqueue_outer uses, and whether K1F pairs are used
-static bool uses_fused(const sscg_ctx *c)
-{
-    const int L = (int)c->slabs.size();
-    return L == 1 && c->nranks == 1 && c->slabs[0].has_k1f && c->basis == SSCG_BASIS_CHEBYSHEV &&
-           c->g.kind != SSCG_OP_CSR;
-}
+// schedule enqueue_outer uses
 
 extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
 {

@@ -253,3 +253,32 @@ def test_halo_overlap_bitwise(cfg, slabs, monkeypatch):
         assert np.array_equal(a[2][j], b[2][j])
     x_or, _ = P.oracle(max_outer=5)
     assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+@pytest.mark.parametrize("cfg,slabs", [(("7pt", 70, 36, 40, 16, 25), 1), (("7pt", 33, 17, 19, 5, 10), 1),
+                                       (("7pt", 40, 36, 33, 10, 20), 3), (("7pt", 66, 20, 17, 7, 10), 2)],
+                         ids=lambda v: _ids(v) if isinstance(v, tuple) else str(v))
+def test_fused_pairs_match_single_steps(cfg, slabs, monkeypatch):
+    """K1F (two basis steps per launch, p_{j+1} on chip) against K1T single
+    steps: the same arithmetic per point, so basis, Gram and x agree to
+    rounding (FMA contraction may differ between the kernels); odd s ends
+    with a single step; several slabs run boundary single steps around the
+    exchange of p_{j+1}.  Both agree with the oracle."""
+    kind, nx, ny, nz, s, nu = cfg
+    P = Problem(kind, nx, ny, nz, s, nu)
+    out = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("SSCG_K1_FUSE", fuse)
+        import paper_2512_09642_b200 as sscg
+        with P.gpu_solver(slabs=slabs) as S:
+            assert S.query(sscg.QUERY_BASIS_FUSED) == (1 if fuse == "1" else 0)
+            x = S.solve(P.b_gpu(), rtol=0.0, max_outer=4).cpu().numpy()
+            out[fuse] = (x, S.gram(0)[0], [S.basis(j) for j in range(s)])
+    a, b = out["1"], out["0"]
+    assert np.max(np.abs(a[1] - b[1])) <= 1e-13 * np.max(np.abs(b[1]))
+    for j in range(s):
+        for q in range(2):
+            assert rel_inf(a[2][j][q], b[2][j][q]) <= 1e-12
+    assert np.linalg.norm(a[0] - b[0]) <= 1e-11 * np.linalg.norm(b[0])
+    x_or, _ = P.oracle(max_outer=4)
+    assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)

@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu12.log 2>&1; echo pytest=$?
+tail -20 gpurun_out/pytest_gpu12.log
