@@ -20,6 +20,7 @@ __global__ void __launch_bounds__(256) mix(const double2 *__restrict__ in, doubl
         }
 #pragma unroll
         for (int w = 0; w < W; ++w) __stcs(out + w * stride2 + e, make_double2(acc.x + w, acc.y));
+        if (W == 0 && acc.x == 1.2345e300) out[e] = acc;   // keeps read-only loads alive
     }
 }
 
@@ -62,13 +63,12 @@ int main()
     run<1, 0>(in, out, n2, stride2, sms);
     run<4, 0>(in, out, n2, stride2, sms);
     run<1, 1>(in, out, n2, stride2, sms);
-    run<2, 2>(in, out, n2, stride2, sms);
-    run<3, 2>(in, out, n2, stride2, sms);
-    run<2, 4>(in, out, n2, stride2, sms);
-    run<1, 2>(in, out, n2, stride2, sms);
+    run<2, 2>(in, out, n2, stride2, sms);    // K1 / K1T
+    run<1, 2>(in, out, n2, stride2, sms);    // K1F (per step)
+    run<2, 4>(in, out, n2, stride2, sms);    // K1F (per pair)
+    run<5, 2>(in, out, n2, stride2, sms);    // K1T variable coefficients (3 face streams)
     run<16, 0>(in, out, n2, stride2, sms);
-    run<32, 0>(in, out, n2, stride2, sms);
-    run<17, 2>(in, out, n2, stride2, sms);
-    run<33, 2>(in, out, n2, stride2, sms);
+    run<32, 0>(in, out, n2, stride2, sms);   // K2 (s = 16)
+    run<33, 2>(in, out, n2, stride2, sms);   // K5 (s = 16)
     return 0;
 }
