@@ -45,6 +45,7 @@ constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = BW * BHM * 8;
 constexpr size_t SMEM = (size_t)(NSP * PS + NSM * MS + NU * PS) * sizeof(double);
 constexpr int FRONT_TASKS = (TY + 2) * (BW / 2);   // 18 rows x 34 pairs
 constexpr int BACK_TASKS = TY * (TX / 2);          // 16 rows x 32 pairs
+static_assert(NCT >= FRONT_TASKS && NCT >= BACK_TASKS, "one front and one back task per consumer thread");
 
 struct K1FWork {
     int tiles_x, tiles_y, zc;
@@ -150,15 +151,31 @@ __global__ void __launch_bounds__(THREADS, 1)
         return;
     }
 
-    const int ct = tid - 32;   // consumer thread 0..255
+    // one front task (pair of a tile + halo row) and at most one back task
+    // (pair of a tile row) per consumer thread; their smem offsets and masks
+    // are fixed for the kernel, the global ones per item
+    const int ct = tid - 32;
+    const bool has_f = ct < FRONT_TASKS, has_b = ct < BACK_TASKS;
+    const int rf = 1 + ct / (BW / 2), cf = 2 * (ct % (BW / 2));        // box row 1..18, col 0..66
+    const int rb = 2 + ct / (TX / 2), cb = 2 + 2 * (ct % (TX / 2));    // box row 2..17, col 2..65
+    const int of = rf * BW + cf, ob = rb * BW + cb, omf = (rf - 1) * BW + cf;
+    const bool own_cell = rf >= 2 && rf < TY + 2 && cf >= 2 && cf < TX + 2;
+    const bool lgf = cf > 0, rgf = cf + 2 < BW;
     uint32_t pc = 0, mc = 0;   // sequence numbers of the next p_j / p_{j-1} slot to consume
     const int64_t pl = g.plane;
+    const double center = wk.center, dinv_c = wk.dinv_c, sigma = wk.sigma;
+    const double cfr = wk.coef_front, cbk = wk.coef_back;
     for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
         const ItemPlan it = plan_item(wk, item);
         const int x0 = it.tx * TX, y0 = it.ty * TY;
-        // slot of p_j plane z: pc_base + (z - plo) while the item lasts
-        const uint32_t pbase = pc;
-        int pwaited = it.plo - 1;   // highest plane waited for
+        const int gxf = x0 - 2 + cf, gyf = y0 - 2 + rf, gxb = x0 - 2 + cb, gyb = y0 - 2 + rb;
+        const bool vyf = gyf >= 0 && gyf < g.ny;
+        const bool v0f = has_f && vyf && gxf >= 0 && gxf < g.nx, v1f = has_f && vyf && gxf + 1 >= 0 && gxf + 1 < g.nx;
+        const bool wf = own_cell && v0f;                         // writes w_j, p_{j+1} of its own cell
+        const bool wb = has_b && gyb < g.ny && gxb < g.nx, v1b = gxb + 1 < g.nx;
+        const int64_t gif = (int64_t)gyf * g.pitch + gxf, gib = (int64_t)gyb * g.pitch + gxb;
+        const uint32_t pbase = pc;   // p_j plane z lives in slot (pbase + z - plo) % NSP
+        int pwaited = it.plo - 1;
         for (int q = it.zlo - 1; q <= it.zhi; ++q) {
             const int need = min(q + 1, it.phi);
             while (pwaited < need) {
@@ -166,54 +183,43 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t c = pbase + (pwaited - it.plo);
                 mbar_wait(&fullp[c % NSP], (c / NSP) & 1);
             }
-            auto pslot = [&](int z) -> const double * { return sp + ((pbase + (z - it.plo)) % NSP) * PS; };
+            const uint32_t cq = pbase + (q - it.plo);   // slot sequence of plane q (q >= plo except q = -1)
+            const double *P0 = sp + (cq % NSP) * PS;
             double *U = su + ((q + 8) % NU) * PS;
             // ---------------- front(q): step j on tile + halo ----------------
             const bool inside = q >= 1 && q <= wk.nzl;
             const bool mloaded = wk.front_pm && q >= it.mlo && q <= it.mhi;
-            const double *M = nullptr;
-            if (mloaded) {
-                mbar_wait(&fullm[mc % NSM], (mc / NSM) & 1);
-                M = sm + (mc % NSM) * MS;
-            }
-            const bool own = q >= it.zlo && q < it.zhi;
-            for (int t = ct; t < FRONT_TASKS; t += NCT) {
-                const int r = 1 + t / (BW / 2);          // box row 1..18
-                const int col = 2 * (t % (BW / 2));      // box col 0..66 (pair col, col+1)
-                const int gx = x0 - 2 + col, gy = y0 - 2 + r;
+            const double *M = sm + (mc % NSM) * MS;
+            if (mloaded) mbar_wait(&fullm[mc % NSM], (mc / NSM) & 1);
+            if (has_f) {
                 double2 u = make_double2(0.0, 0.0);
                 if (inside) {
-                    const double *P0 = pslot(q), *Pm = pslot(q - 1), *Pp = pslot(q + 1);
-                    const int o = r * BW + col;
-                    const double2 c = lds2(P0 + o);
-                    const double2 dn = lds2(Pm + o), up = lds2(Pp + o);
-                    const double2 ylo = lds2(P0 + o - BW), yhi = lds2(P0 + o + BW);
-                    const double l = (col > 0) ? P0[o - 1] : 0.0;
-                    const double rr = (col + 2 < BW) ? P0[o + 2] : 0.0;
+                    const double *Pm = sp + ((cq - 1) % NSP) * PS, *Pp = sp + ((cq + 1) % NSP) * PS;
+                    const double2 c = lds2(P0 + of);
+                    const double2 dn = lds2(Pm + of), up = lds2(Pp + of);
+                    const double2 ylo = lds2(P0 + of - BW), yhi = lds2(P0 + of + BW);
+                    const double l = lgf ? P0[of - 1] : 0.0;
+                    const double rr = rgf ? P0[of + 2] : 0.0;
                     double2 Ap;
-                    Ap.x = wk.center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
-                    Ap.y = wk.center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
-                    double2 pm = make_double2(0.0, 0.0);
-                    if (mloaded) pm = lds2(M + (r - 1) * BW + col);
-                    u.x = wk.coef_front * (wk.dinv_c * Ap.x - wk.sigma * c.x);
-                    u.y = wk.coef_front * (wk.dinv_c * Ap.y - wk.sigma * c.y);
-                    if (wk.front_pm) {
+                    Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                    Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                    u.x = cfr * (dinv_c * Ap.x - sigma * c.x);
+                    u.y = cfr * (dinv_c * Ap.y - sigma * c.y);
+                    if (mloaded) {
+                        const double2 pm = lds2(M + omf);
                         u.x -= pm.x;
                         u.y -= pm.y;
                     }
-                    const bool vy = gy >= 0 && gy < g.ny;
-                    const bool v0 = vy && gx >= 0 && gx < g.nx, v1 = vy && gx + 1 >= 0 && gx + 1 < g.nx;
-                    if (!v0) u.x = 0.0;
-                    if (!v1) u.y = 0.0;
-                    // the tile's own cells go to HBM (w_j and p_{j+1})
-                    if (own && r >= 2 && r < TY + 2 && col >= 2 && col < TX + 2 && v0) {
-                        const int64_t i = (int64_t)q * pl + (int64_t)gy * g.pitch + gx;
-                        if (!v1) Ap.y = 0.0;
+                    if (!v0f) u.x = 0.0;
+                    if (!v1f) u.y = 0.0;
+                    if (wf && q >= it.zlo && q < it.zhi) {   // the tile's own cells: w_j, p_{j+1} to HBM
+                        const int64_t i = (int64_t)q * pl + gif;
+                        if (!v1f) Ap.y = 0.0;
                         __stcs(reinterpret_cast<double2 *>(a.w + i), Ap);
                         *reinterpret_cast<double2 *>(a.pn + i) = u;
                     }
                 }
-                *reinterpret_cast<double2 *>(U + r * BW + col) = u;
+                *reinterpret_cast<double2 *>(U + of) = u;
             }
             if (mloaded) {
                 __syncwarp();
@@ -223,39 +229,30 @@ __global__ void __launch_bounds__(THREADS, 1)
             consumers_sync();   // U(q) complete; U(q-4) no longer read
             // ---------------- back(q-1): step j+1 on the tile ----------------
             const int z = q - 1;
-            if (z >= it.zlo && z < it.zhi) {
-                const double *Um = su + ((z - 1 + 8) % NU) * PS, *U0 = su + ((z + 8) % NU) * PS, *Up = U;
-                const double *Pz = pslot(z);
-                for (int t = ct; t < BACK_TASKS; t += NCT) {
-                    const int r = 2 + t / (TX / 2);
-                    const int col = 2 + 2 * (t % (TX / 2));
-                    const int gx = x0 - 2 + col, gy = y0 - 2 + r;
-                    if (gy >= g.ny || gx >= g.nx) continue;
-                    const int o = r * BW + col;
-                    const double2 c = lds2(U0 + o);
-                    const double2 dn = lds2(Um + o), up = lds2(Up + o);
-                    const double2 ylo = lds2(U0 + o - BW), yhi = lds2(U0 + o + BW);
-                    const double l = U0[o - 1], rr = U0[o + 2];
-                    double2 Ap;
-                    Ap.x = wk.center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
-                    Ap.y = wk.center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
-                    const bool v1 = gx + 1 < g.nx;
-                    if (!v1) Ap.y = 0.0;
-                    const int64_t i = (int64_t)z * pl + (int64_t)gy * g.pitch + gx;
-                    __stcs(reinterpret_cast<double2 *>(a.w2 + i), Ap);
-                    if (wk.back_pn) {
-                        const double2 pj = lds2(Pz + o);
-                        double v0 = wk.coef_back * (wk.dinv_c * Ap.x - wk.sigma * c.x) - pj.x;
-                        double v1v = wk.coef_back * (wk.dinv_c * Ap.y - wk.sigma * c.y) - pj.y;
-                        if (!v1) v1v = 0.0;
-                        *reinterpret_cast<double2 *>(a.pn2 + i) = make_double2(v0, v1v);
-                    }
+            if (wb && z >= it.zlo && z < it.zhi) {
+                const double *Um = su + ((z - 1 + 8) % NU) * PS, *U0 = su + ((z + 8) % NU) * PS;
+                const double2 c = lds2(U0 + ob);
+                const double2 dn = lds2(Um + ob), up = lds2(U + ob);
+                const double2 ylo = lds2(U0 + ob - BW), yhi = lds2(U0 + ob + BW);
+                const double l = U0[ob - 1], rr = U0[ob + 2];
+                double2 Ap;
+                Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                if (!v1b) Ap.y = 0.0;
+                const int64_t i = (int64_t)z * pl + gib;
+                __stcs(reinterpret_cast<double2 *>(a.w2 + i), Ap);
+                if (wk.back_pn) {
+                    const double2 pj = lds2(sp + ((cq - 1) % NSP) * PS + ob);   // p_j(z)
+                    const double v0 = cbk * (dinv_c * Ap.x - sigma * c.x) - pj.x;
+                    double v1 = cbk * (dinv_c * Ap.y - sigma * c.y) - pj.y;
+                    if (!v1b) v1 = 0.0;
+                    *reinterpret_cast<double2 *>(a.pn2 + i) = make_double2(v0, v1);
                 }
             }
             // p_j plane q-1 is no longer needed (front(q+1) reads q..q+2)
             if (q - 1 >= it.plo) {
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyp[(pbase + (q - 1 - it.plo)) % NSP]);
+                if (lane == 0) mbar_arrive(&emptyp[(cq - 1) % NSP]);
             }
         }
         // release the p_j planes of this item not released in the loop: zhi, zhi+1 (if loaded)
