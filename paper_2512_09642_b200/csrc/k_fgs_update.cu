@@ -258,12 +258,16 @@ struct K5Params {
 };
 
 // flat path: pitch == nx and x 16-B aligned; 2 points per thread per step.
+// S > 0: the basis size is a compile-time constant, so all 2S loads of a
+// point are issued before the first FMA (S = 0: runtime s).
+template <int S>
 __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState *st)
 {
     if (st->done) return;
     __shared__ double al[SMAX];
     for (int j = threadIdx.x; j < k.s; j += blockDim.x) al[j] = k.alpha[j];
     __syncthreads();
+    const int s = S > 0 ? S : k.s;
     const int64_t n2 = k.N >> 1;
     const double2 *P2 = reinterpret_cast<const double2 *>(k.P);
     const double2 *W2 = reinterpret_cast<const double2 *>(k.W);
@@ -273,16 +277,17 @@ __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState 
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (int64_t)gridDim.x * blockDim.x) {
         double2 ax = make_double2(0.0, 0.0), aw = make_double2(0.0, 0.0);
         const double2 p0 = __ldcs(P2 + e);
-        for (int j = 0; j < k.s; ++j) {
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
             const double2 pj = (j == 0) ? p0 : __ldcs(P2 + j * vs2 + e);
             const double2 wj = __ldcs(W2 + j * vs2 + e);
             ax.x = fma(al[j], pj.x, ax.x); ax.y = fma(al[j], pj.y, ax.y);
             aw.x = fma(al[j], wj.x, aw.x); aw.y = fma(al[j], wj.y, aw.y);
         }
-        double2 xv = x2[e];
+        double2 xv = __ldcs(x2 + e);
         xv.x += ax.x; xv.y += ax.y;
-        x2[e] = xv;
-        r2[e] = make_double2(p0.x - aw.x, p0.y - aw.y);
+        __stcs(x2 + e, xv);
+        __stcs(r2 + e, make_double2(p0.x - aw.x, p0.y - aw.y));
     }
 }
 
@@ -341,7 +346,16 @@ void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double 
     int64_t blocks = (work + 255) / 256;
     const int64_t cap = (int64_t)k2_grid() * 8;
     if (blocks > cap) blocks = cap;
-    if (vec) k5_update_vec<<<(unsigned)blocks, 256, 0, stream>>>(k, st);
+    if (vec) {
+        switch (s) {
+        case 4: k5_update_vec<4><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 8: k5_update_vec<8><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 16: k5_update_vec<16><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 24: k5_update_vec<24><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 32: k5_update_vec<32><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        default: k5_update_vec<0><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        }
+    }
     else k5_update_gen<<<(unsigned)blocks, 256, 0, stream>>>(k, st);
 }
 
