@@ -27,6 +27,7 @@
 // Bytes per launch: p_j, p_{j-1} read, w_j, p_{j+1} written (4 vectors at
 // 1 <= j < s-1).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "sscg_internal.cuh"
@@ -44,6 +45,35 @@ constexpr int NCW = TY / 2;                                   // consumer warps 
 constexpr int THREADS = 32 * (NCW + 1);
 constexpr uint32_t PBYTES = BW * BH * 8, MBYTES = TX * TY * 8;
 constexpr size_t SMEM = (size_t)(NSP * PSLOT + NSM * MSLOT) * sizeof(double);
+// KIND 4 (variable coefficients, faces staged by TMA): per plane slot
+//   KX: TY rows x 68 faces (row pitch 80 doubles: 128-B aligned TMA rows;
+//       row r starts at face x0 - parity(r), see k1t_prepare_faces)
+//   KY: TY+1 rows x TX,  KZL / KZH: TY rows x TX (lower / upper z-faces)
+constexpr int KXB = 68, KXP = 80, FKX = 0, FKY = TY * KXP, FKZL = FKY + (TY + 1) * TX, FKZH = FKZL + TY * TX;
+constexpr int FSLOT = FKZH + TY * TX;     // doubles (34,304 B)
+constexpr int NSF = 3;
+constexpr uint32_t FBYTES = (TY * KXB + (TY + 1) * TX + 2 * TY * TX) * 8;
+constexpr size_t SMEM4 = SMEM + (size_t)NSF * FSLOT * sizeof(double);
+static_assert((FKY * 8) % 128 == 0 && (FKZL * 8) % 128 == 0 && (FKZH * 8) % 128 == 0 && (FSLOT * 8) % 128 == 0,
+              "TMA destinations must be 128-B aligned");
+
+__device__ __forceinline__ void tma_load_1d(void *dst, const CUtensorMap *map, int x, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d_(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
 
 struct K1TWork {
     int tiles_x, tiles_y, zc, nch1;
@@ -89,15 +119,17 @@ __device__ __forceinline__ double2 rowsum3(const double *row)
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(THREADS, KIND == 3 ? 1 : 2)
-    k1t(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, K1Args a,
-        const DevState *st, K1TWork wk)
+__global__ void __launch_bounds__(THREADS, KIND >= 3 ? 1 : 2)
+    k1t(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM,
+        const __grid_constant__ CUtensorMap tmKX, const __grid_constant__ CUtensorMap tmKY,
+        const __grid_constant__ CUtensorMap tmKZ, Geo g, K1Args a, const DevState *st, K1TWork wk)
 {
     if (st && st->done) return;
     extern __shared__ __align__(128) double smem[];
     double *sp = smem;
     double *sq = smem + NSP * PSLOT;
-    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM];
+    double *sf = sq + NSM * MSLOT;   // KIND 4 face ring
+    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM], fullf[NSF], emptyf[NSF];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool m2 = a.mode == 2;
     const int ntiles = wk.tiles_x * wk.tiles_y;
@@ -111,39 +143,75 @@ __global__ void __launch_bounds__(THREADS, KIND == 3 ? 1 : 2)
             mbar_init(&fullm[i], 1);
             mbar_init(&emptym[i], NCW);
         }
+        for (int i = 0; i < NSF; ++i) {
+            mbar_init(&fullf[i], 1);
+            mbar_init(&emptyf[i], NCW);
+        }
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
         tma_prefetch_desc(&tmM);
+        if (KIND == 4) {
+            tma_prefetch_desc(&tmKX);
+            tma_prefetch_desc(&tmKY);
+            tma_prefetch_desc(&tmKZ);
+        }
     }
     __syncthreads();
 
     if (warp == 0) {
         // ---------------- producer ----------------
-        if (lane == 0) {
-            uint32_t pc = 0, mc = 0;
+        // lane 0 issues the p_j / p_{j-1} boxes; for KIND 4 the whole warp runs
+        // the loop and lanes 0..TY-1 issue one kx row box each
+        if (lane == 0 || KIND == 4) {
+            uint32_t pc = 0, mc = 0, fc = 0;
             for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
                 int tx, ty, zlo, zhi;
                 item_planes(wk, item, ntiles, tx, ty, zlo, zhi);
                 const int x0 = tx * TX, y0 = ty * TY;
                 auto loadp = [&](int z) {
                     const int sl = pc % NSP;
-                    if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
-                    mbar_expect_tx(&fullp[sl], PBYTES);
-                    tma_load_4d(sp + sl * PSLOT, &tmP, x0 - 2, y0 - 1, z, wk.j, &fullp[sl]);
+                    if (lane == 0) {
+                        if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
+                        mbar_expect_tx(&fullp[sl], PBYTES);
+                        tma_load_4d(sp + sl * PSLOT, &tmP, x0 - 2, y0 - 1, z, wk.j, &fullp[sl]);
+                    }
                     ++pc;
                 };
                 auto loadm = [&](int z) {
                     const int sl = mc % NSM;
-                    if (mc >= NSM) mbar_wait(&emptym[sl], ((mc / NSM) - 1) & 1);
-                    mbar_expect_tx(&fullm[sl], MBYTES);
-                    tma_load_4d(sq + sl * MSLOT, &tmM, x0, y0, z, wk.j - 1, &fullm[sl]);
+                    if (lane == 0) {
+                        if (mc >= NSM) mbar_wait(&emptym[sl], ((mc / NSM) - 1) & 1);
+                        mbar_expect_tx(&fullm[sl], MBYTES);
+                        tma_load_4d(sq + sl * MSLOT, &tmM, x0, y0, z, wk.j - 1, &fullm[sl]);
+                    }
                     ++mc;
+                };
+                auto loadf = [&](int z) {   // faces of plane z (slab-local zl = z - 1)
+                    const int sl = fc % NSF;
+                    double *d = sf + sl * FSLOT;
+                    const int zl = z - 1;
+                    if (lane == 0) {
+                        if (fc >= NSF) mbar_wait(&emptyf[sl], ((fc / NSF) - 1) & 1);
+                        mbar_expect_tx(&fullf[sl], FBYTES);
+                    }
+                    __syncwarp();
+                    if (lane < TY) {   // face row (zl, y0 + lane), from the even element at or below its x0
+                        const int e0 = (zl * g.ny + y0 + lane) * (g.nx + 1) + x0;
+                        tma_load_1d(d + FKX + lane * KXP, &tmKX, e0 & ~1, &fullf[sl]);
+                    }
+                    if (lane == 0) {
+                        tma_load_3d_(d + FKY, &tmKY, x0, y0, zl, &fullf[sl]);
+                        tma_load_3d_(d + FKZL, &tmKZ, x0, y0, zl, &fullf[sl]);
+                        tma_load_3d_(d + FKZH, &tmKZ, x0, y0, zl + 1, &fullf[sl]);
+                    }
+                    ++fc;
                 };
                 loadp(zlo - 1);
                 loadp(zlo);
                 for (int z = zlo; z < zhi; ++z) {
                     loadp(z + 1);
                     if (m2) loadm(z);
+                    if (KIND == 4) loadf(z);
                 }
             }
         }
@@ -157,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, KIND == 3 ? 1 : 2)
     const int ob = oa + BW;
     const int qa = ra * TX + 2 * lane, qb = qa + TX;
     const int64_t pl = g.plane;
-    uint32_t pc = 0, mc = 0;
+    uint32_t pc = 0, mc = 0, fc = 0;
     auto waitp = [&](uint32_t c) -> const double * {
         const int sl = c % NSP;
         mbar_wait(&fullp[sl], (c / NSP) & 1);
@@ -238,6 +306,26 @@ __global__ void __launch_bounds__(THREADS, KIND == 3 ? 1 : 2)
                     if (in1) { kxb2 = __ldg(qx + g.nx + 3); kyc1 = __ldg(qy + 2 * g.nx + 1); kzpb1 = __ldg(qz + g.nx + 1); }
                 }
             }
+            if (KIND == 4) {   // faces of plane z from the staged slot
+                const int sl = fc % NSF;
+                mbar_wait(&fullf[sl], (fc / NSF) & 1);
+                const double *F = sf + sl * FSLOT;
+                const int xa = 2 * lane;
+                const int fa = ((z - 1) * g.ny + ya) * (g.nx + 1) + tx * TX;   // first face of row ya (parity)
+                const double *fx = F + FKX + ra * KXP + xa + (fa & 1), *fy = F + FKY + ra * TX + xa;
+                const double *fxb = F + FKX + (ra + 1) * KXP + xa + ((fa + g.nx + 1) & 1);
+                kxa0 = fx[0]; kxa1 = fx[1]; kxa2 = fx[2];
+                kxb0 = fxb[0]; kxb1 = fxb[1]; kxb2 = fxb[2];
+                const double2 ya0 = lds2(fy), yb0 = lds2(fy + TX), yc0 = lds2(fy + 2 * TX);
+                kya0 = ya0.x; kya1 = ya0.y; kyb0 = yb0.x; kyb1 = yb0.y; kyc0 = yc0.x; kyc1 = yc0.y;
+                const double2 zla = lds2(F + FKZL + ra * TX + xa), zlb = lds2(F + FKZL + (ra + 1) * TX + xa);
+                const double2 zha = lds2(F + FKZH + ra * TX + xa), zhb = lds2(F + FKZH + (ra + 1) * TX + xa);
+                kzma0 = zla.x; kzma1 = zla.y; kzmb0 = zlb.x; kzmb1 = zlb.y;
+                kzpa0 = zha.x; kzpa1 = zha.y; kzpb0 = zhb.x; kzpb1 = zhb.y;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyf[sl]);
+                ++fc;
+            }
             const double *s0 = sp + (c0 % NSP) * PSLOT;   // plane z (7-point: still held)
             const double *s1 = waitp(pc);                  // plane z+1
             double2 Apa, Apb;
@@ -255,7 +343,7 @@ __global__ void __launch_bounds__(THREADS, KIND == 3 ? 1 : 2)
                 Apb.y = 27.0 * c0b.y - (bmb.y + b0b.y + bpb.y);
                 bma = b0a; bmb = b0b;
                 b0a = bpa; b0b = bpb;
-            } else if (KIND == 3) {
+            } else if (KIND == 3 || KIND == 4) {
                 const double2 ylo = lds2(s0 + oa - BW), yhi = lds2(s0 + ob + BW);
                 const double la = s0[oa - 1], rra = s0[oa + 2], lb = s0[ob - 1], rrb = s0[ob + 2];
                 relp(c0);
@@ -297,7 +385,7 @@ __global__ void __launch_bounds__(THREADS, KIND == 3 ? 1 : 2)
                 __stcs(reinterpret_cast<double2 *>(a.w + ia), Apa);
                 if (a.mode >= 1) {
                     const double2 dv = a.dinv ? __ldg(reinterpret_cast<const double2 *>(a.dinv + ia))
-                                       : (KIND == 3) ? make_double2(1.0 / Da.x, in1 ? 1.0 / Da.y : 0.0)
+                                       : (KIND >= 3) ? make_double2(1.0 / Da.x, in1 ? 1.0 / Da.y : 0.0)
                                                      : make_double2(a.dinv_c, a.dinv_c);
                     double v0 = a.coef * (dv.x * Apa.x - a.sigma * c0a.x);
                     double v1 = a.coef * (dv.y * Apa.y - a.sigma * c0a.y);
@@ -314,7 +402,7 @@ __global__ void __launch_bounds__(THREADS, KIND == 3 ? 1 : 2)
                 __stcs(reinterpret_cast<double2 *>(a.w + ib), Apb);
                 if (a.mode >= 1) {
                     const double2 dv = a.dinv ? __ldg(reinterpret_cast<const double2 *>(a.dinv + ib))
-                                       : (KIND == 3) ? make_double2(1.0 / Db.x, in1 ? 1.0 / Db.y : 0.0)
+                                       : (KIND >= 3) ? make_double2(1.0 / Db.x, in1 ? 1.0 / Db.y : 0.0)
                                                      : make_double2(a.dinv_c, a.dinv_c);
                     double v0 = a.coef * (dv.x * Apb.x - a.sigma * c0b.x);
                     double v1 = a.coef * (dv.y * Apb.y - a.sigma * c0b.y);
@@ -373,8 +461,65 @@ bool k1t_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
         return false;
     if (cudaFuncSetAttribute(k1t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
         cudaFuncSetAttribute(k1t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(k1t<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
+        cudaFuncSetAttribute(k1t<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k1t<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM4) != cudaSuccess)
         return false;
+    return true;
+}
+
+// TMA views of the variable-coefficient faces of one slab (nzl planes):
+//   kx: 1-D over the slab's (nx+1)*ny*nzl faces, one 68-element box per row
+//   ky: [nx][ny+1][nzl], box 64 x 17;  kz: [nx][ny][nzl+1], box 64 x 16
+// Needs nx even (16-B strides); otherwise K1T reads the faces directly.
+bool k1t_prepare_faces(const Geo &g, const double *kx, const double *ky, const double *kz, int nzl, CUtensorMap *mx,
+                       CUtensorMap *my, CUtensorMap *mz)
+{
+    if (g.nx % 2 != 0 || (reinterpret_cast<uintptr_t>(kx) | reinterpret_cast<uintptr_t>(ky) |
+                          reinterpret_cast<uintptr_t>(kz)) % 16 != 0)
+        return false;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+        return false;
+    auto enc = reinterpret_cast<CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                             CUtensorMapFloatOOBfill)>(fn);
+    const cuuint32_t es[3] = {1, 1, 1};
+    const bool dbg = getenv("SSCG_DEBUG") != nullptr;
+    {
+        // rows of kx have an odd length (nx+1), so every other row starts at an
+        // odd element: a 1-D view, one 68-element box per face row starting at
+        // the row's first face rounded down to an even element (TMA box
+        // starts must be 16-B aligned); the consumer adds the row's parity
+        cuuint64_t dims[1] = {(cuuint64_t)(g.nx + 1) * g.ny * nzl};
+        cuuint64_t str[1] = {0};
+        cuuint32_t box[1] = {KXB};
+        const CUresult r = enc(mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, const_cast<double *>(kx), dims, str, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (dbg) fprintf(stderr, "sscg: kx tensor map -> %d\n", (int)r);
+        if (r != CUDA_SUCCESS) return false;
+    }
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)(g.ny + 1), (cuuint64_t)nzl};
+        cuuint64_t str[2] = {(cuuint64_t)g.nx * 8, (cuuint64_t)g.nx * (g.ny + 1) * 8};
+        cuuint32_t box[3] = {TX, TY + 1, 1};
+        if (enc(my, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(ky), dims, str, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)(nzl + 1)};
+        cuuint64_t str[2] = {(cuuint64_t)g.nx * 8, (cuuint64_t)g.nx * g.ny * 8};
+        cuuint32_t box[3] = {TX, TY, 1};
+        if (enc(mz, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(kz), dims, str, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
     return true;
 }
 
@@ -389,11 +534,14 @@ void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t 
     wk.zb = a.zb; wk.ze = a.ze; wk.zb2 = a.zb2; wk.ze2 = a.ze2;
     wk.j = a.j;
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
-    static int occs[4] = {0, 0, 0, 0}, zc_env = -1;
-    int &occ = occs[g.kind];
+    const int kind = (g.kind == 3 && a.tmKX) ? 4 : g.kind;
+    static int occs[5] = {0, 0, 0, 0, 0}, zc_env = -1;
+    int &occ = occs[kind];
     if (!occ) {
-        const void *fn = g.kind == 1 ? (const void *)k1t<1> : g.kind == 2 ? (const void *)k1t<2> : (const void *)k1t<3>;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, SMEM) != cudaSuccess || occ <= 0)
+        const void *fn = kind == 1 ? (const void *)k1t<1> : kind == 2 ? (const void *)k1t<2>
+                       : kind == 3 ? (const void *)k1t<3> : (const void *)k1t<4>;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, kind == 4 ? SMEM4 : SMEM) != cudaSuccess ||
+            occ <= 0)
             occ = 1;
         const char *e = getenv("SSCG_K1_ZC");
         zc_env = e ? std::max(1, atoi(e)) : 0;
@@ -427,9 +575,11 @@ void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t 
     wk.nch1 = (n1 + zc - 1) / zc;
     wk.nitems = tiles * (wk.nch1 + (n2 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
-    if (g.kind == 1) k1t<1><<<grid, THREADS, SMEM, s>>>(*a.tmP4, *a.tmM4, g, a, st, wk);
-    else if (g.kind == 2) k1t<2><<<grid, THREADS, SMEM, s>>>(*a.tmP4, *a.tmM4, g, a, st, wk);
-    else k1t<3><<<grid, THREADS, SMEM, s>>>(*a.tmP4, *a.tmM4, g, a, st, wk);
+    const CUtensorMap &P4 = *a.tmP4, &M4 = *a.tmM4;
+    if (kind == 1) k1t<1><<<grid, THREADS, SMEM, s>>>(P4, M4, P4, P4, P4, g, a, st, wk);
+    else if (kind == 2) k1t<2><<<grid, THREADS, SMEM, s>>>(P4, M4, P4, P4, P4, g, a, st, wk);
+    else if (kind == 3) k1t<3><<<grid, THREADS, SMEM, s>>>(P4, M4, P4, P4, P4, g, a, st, wk);
+    else k1t<4><<<grid, THREADS, SMEM4, s>>>(P4, M4, *a.tmKX, *a.tmKY, *a.tmKZ, g, a, st, wk);
 }
 
 }  // namespace sscg

@@ -320,6 +320,9 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
             sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
             sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;
             sl.kz = A->kz + sl.zoff * g.ny * g.nx;
+            const char *e = getenv("SSCG_FACES_TMA");
+            sl.has_ftma = !(e && e[0] == '0') &&
+                          k1t_prepare_faces(g, sl.kx, sl.ky, sl.kz, sl.nzl, &sl.tmKX, &sl.tmKY, &sl.tmKZ);
         }
         if (diag_M || A->kind == SSCG_OP_CSR) {
             double *dv = nullptr;
@@ -530,6 +533,11 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
         if (sl.has_k1t) {
             a.tmP4 = &sl.tmP4;
             a.tmM4 = &sl.tmM4;
+        }
+        if (sl.has_ftma) {
+            a.tmKX = &sl.tmKX;
+            a.tmKY = &sl.tmKY;
+            a.tmKZ = &sl.tmKZ;
         }
         if (part == 0) {
             a.zb = 1; a.ze = sl.nzl + 1;

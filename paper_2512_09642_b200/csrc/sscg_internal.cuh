@@ -45,6 +45,8 @@ struct Slab {
     CUtensorMap tmP4, tmM4;       // K1T: 4-D [x][y][plane][vector] views of P (halo box / tile box)
     bool has_k1t;
     CUtensorMap tmF_P, tmF_M;     // K1F: 2-cell / 1-cell halo boxes
+    CUtensorMap tmKX, tmKY, tmKZ; // K1T: variable-coefficient faces (nx even)
+    bool has_ftma;
     bool has_k1f;
 };
 
@@ -85,6 +87,7 @@ struct K1Args {
     int nzl;
     int j;                 // basis step (K1T: vector coordinate of p_j in the tensor maps)
     const CUtensorMap *tmP4, *tmM4;   // K1T tensor maps of this slab (host memory), or nullptr
+    const CUtensorMap *tmKX, *tmKY, *tmKZ;   // K1T variable-coefficient face maps, or nullptr
     double *w2, *pn2;                 // K1F: w_{j+1}, p_{j+2} (nullptr at j+1 = s-1)
     const CUtensorMap *tmF_P, *tmF_M; // K1F tensor maps
 };
@@ -95,6 +98,8 @@ void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s
 bool k1t_supported(const Geo &g, const K1Args &a);
 bool k1t_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP4, CUtensorMap *tmM4);
 void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s);
+bool k1t_prepare_faces(const Geo &g, const double *kx, const double *ky, const double *kz, int nzl, CUtensorMap *mx,
+                       CUtensorMap *my, CUtensorMap *mz);
 
 // K1F: two 7-point basis steps per launch, single slab (k_stencil_fused.cu)
 bool k1f_enabled();

@@ -18,6 +18,7 @@ CASES = [
     ("27pt", 30, 28, 26, 16, 30),       # cfg 3 shape, reduced (Lanczos bounds)
     ("varcoef7", 24, 22, 20, 8, 20),    # cfg 4 shape, reduced (Lanczos bounds)
     ("7pt", 33, 17, 19, 5, 10),         # odd nx: padded row pitch, ragged tiles
+    ("varcoef7", 17, 15, 13, 6, 10),    # odd nx: faces read directly (no TMA view)
 ]
 
 
@@ -281,4 +282,22 @@ def test_fused_pairs_match_single_steps(cfg, slabs, monkeypatch):
             assert rel_inf(a[2][j][q], b[2][j][q]) <= 1e-12
     assert np.linalg.norm(a[0] - b[0]) <= 1e-11 * np.linalg.norm(b[0])
     x_or, _ = P.oracle(max_outer=4)
+    assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+def test_face_staging_matches_direct_loads(monkeypatch):
+    """K1T variable-coefficient faces staged by TMA (nx even) against the
+    same kernel reading them from global memory: identical arithmetic."""
+    P = Problem("varcoef7", 70, 34, 21, 8, 10, bounds=(0.02, 1.98))
+    out = {}
+    for ftma in ("1", "0"):
+        monkeypatch.setenv("SSCG_FACES_TMA", ftma)
+        with P.gpu_solver() as S:
+            x = S.solve(P.b_gpu(), rtol=0.0, max_outer=3).cpu().numpy()
+            out[ftma] = (x, S.gram(0)[0], S.basis(5))
+    a, b = out["1"], out["0"]
+    assert np.max(np.abs(a[1] - b[1])) <= 1e-13 * np.max(np.abs(b[1]))
+    assert rel_inf(a[2][0], b[2][0]) <= 1e-13 and rel_inf(a[2][1], b[2][1]) <= 1e-13
+    assert np.linalg.norm(a[0] - b[0]) <= 1e-12 * np.linalg.norm(b[0])
+    x_or, _ = P.oracle(max_outer=3)
     assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
