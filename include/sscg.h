@@ -206,12 +206,14 @@ SSCG_API sscg_status sscg_stats(const sscg_ctx *ctx, sscg_stats_t *out);
  *   SSCG_INSPECT_GRAM      outer `index`: [Ghat (s*s, row-major, mirrored) | c (s)]
  *                          after the allreduce
  *   SSCG_INSPECT_D, _ALPHA_T, _ALPHA   outer `index`: s doubles
- *   SSCG_INSPECT_DELTA     outer `index`: 1 double
+ *   SSCG_INSPECT_DELTA     outer `index`: 1 double (||c~ - G a~|| / ||c~||)
+ *   SSCG_INSPECT_LNORM     outer `index`: 1 double (||L||_F of the scaled Gram matrix)
  * `capacity` is the byte size of host_out; too small => SSCG_ERR_INVALID.
  * History entries exist for outer indices 0..max_outer of the last solve. */
 enum {
     SSCG_INSPECT_P = 0, SSCG_INSPECT_W = 1, SSCG_INSPECT_GRAM = 2, SSCG_INSPECT_D = 3,
-    SSCG_INSPECT_ALPHA_T = 4, SSCG_INSPECT_ALPHA = 5, SSCG_INSPECT_DELTA = 6
+    SSCG_INSPECT_ALPHA_T = 4, SSCG_INSPECT_ALPHA = 5, SSCG_INSPECT_DELTA = 6,
+    SSCG_INSPECT_LNORM = 7     /* outer `index`: ||L||_F of G = I + L + L^T, 1 double */
 };
 SSCG_API sscg_status sscg_inspect(const sscg_ctx *ctx, int32_t what, int32_t index, void *host_out,
                          int64_t capacity);

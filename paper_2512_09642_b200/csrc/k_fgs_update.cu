@@ -122,6 +122,13 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
         rho0 = res0;
         rho1 = res1;
     }
+    // ||L||_F^2 = sum_{i > j} G_ij^2 (the quantity FGS convergence depends on)
+    double ll = 0.0;
+    for (int j = 0; j < s; ++j) {
+        if (v0 && j < i0) { const double gij = (d0 * Gh[i0 * s + j]) * dsh[j]; ll = fma(gij, gij, ll); }
+        if (v1 && j < i1) { const double gij = (d1 * Gh[i1 * s + j]) * dsh[j]; ll = fma(gij, gij, ll); }
+    }
+    ll = warp_sum(ll);
     // delta = ||c~ - G a~|| / ||c~||  (PAPER.md:259-262 inexactness monitor)
     const double rr = warp_sum(rho0 * rho0 + rho1 * rho1);
     const double cc = warp_sum(ct0 * ct0 + ct1 * ct1);
@@ -130,7 +137,10 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
     if (rec) {
         if (v0) { a.h_d[(int64_t)k * s + i0] = d0; a.h_at[(int64_t)k * s + i0] = al0; a.h_al[(int64_t)k * s + i0] = d0 * al0; }
         if (v1) { a.h_d[(int64_t)k * s + i1] = d1; a.h_at[(int64_t)k * s + i1] = al1; a.h_al[(int64_t)k * s + i1] = d1 * al1; }
-        if (lane == 0) a.h_delta[k] = sqrt(rr) / sqrt(cc);
+        if (lane == 0) {
+            a.h_delta[k] = sqrt(rr) / sqrt(cc);
+            a.h_lnorm[k] = sqrt(ll);
+        }
     }
     if (lane == 0) {
         st->outer = k + 1;
@@ -237,10 +247,20 @@ __global__ void __launch_bounds__(32) k4_chol(K4Args a, DevState *st)
             a.h_al[(int64_t)k * s + i] = dsh[i] * al[i];
         }
     }
+    double ll = 0.0;
+    for (int i = lane; i < s; i += 32)
+        for (int j = 0; j < i; ++j) {
+            const double gij = (dsh[i] * Gh[i * s + j]) * dsh[j];
+            ll = fma(gij, gij, ll);
+        }
     rr = warp_sum(rr);
     cc = warp_sum(cc);
+    ll = warp_sum(ll);
     if (lane == 0) {
-        if (rec) a.h_delta[k] = sqrt(rr) / sqrt(cc);
+        if (rec) {
+            a.h_delta[k] = sqrt(rr) / sqrt(cc);
+            a.h_lnorm[k] = sqrt(ll);
+        }
         st->outer = k + 1;
         st->k = k + 1;
     }

@@ -1,4 +1,4 @@
-// K1F -- two basis steps in one pass (7-point, single slab): the pair
+// K1F -- two basis steps in one pass (7-point and 27-point): the pair
 // (j, j+1) of the Chebyshev recurrence
 //   w_j     = A p_j,      p_{j+1} = c_j (D^{-1} w_j - sigma p_j) [- p_{j-1}]
 //   w_{j+1} = A p_{j+1},  p_{j+2} = 2 theta (D^{-1} w_{j+1} - sigma p_{j+1}) - p_j
@@ -95,6 +95,22 @@ __device__ __forceinline__ ItemPlan plan_item(const K1FWork &wk, int64_t item)
     return p;
 }
 
+// 3-point row sums of the pair (c, c+1) of a staged row: (l + c.x + c.y, c.x + c.y + r)
+__device__ __forceinline__ double2 rowsum3(const double *row)
+{
+    const double l = row[-1], r = row[2];
+    const double2 c = lds2(row);
+    return make_double2(l + c.x + c.y, c.x + c.y + r);
+}
+
+// 3x3 in-plane box sums of the pair at offset o (27-point: A p = 27 p - box3x3x3(p))
+__device__ __forceinline__ double2 box9(const double *P, int o)
+{
+    const double2 r0 = rowsum3(P + o - BW), r1 = rowsum3(P + o), r2 = rowsum3(P + o + BW);
+    return make_double2(r0.x + r1.x + r2.x, r0.y + r1.y + r2.y);
+}
+
+template <int KIND>
 __global__ void __launch_bounds__(THREADS, 1)
     k1f(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, K1Args a,
         const DevState *st, K1FWork wk)
@@ -176,6 +192,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int64_t gif = (int64_t)gyf * g.pitch + gxf, gib = (int64_t)gyb * g.pitch + gxb;
         const uint32_t pbase = pc;   // p_j plane z lives in slot (pbase + z - plo) % NSP
         int pwaited = it.plo - 1;
+        double2 bf_m = {}, bf_0 = {}, bf_p = {}, bb_m = {}, bb_0 = {}, bb_p = {};   // 27-point windows
+        bool bvalid = false;
         for (int q = it.zlo - 1; q <= it.zhi; ++q) {
             const int need = min(q + 1, it.phi);
             while (pwaited < need) {
@@ -193,16 +211,29 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (mloaded) mbar_wait(&fullm[mc % NSM], (mc / NSM) & 1);
             if (has_f) {
                 double2 u = make_double2(0.0, 0.0);
+                if (KIND == 2 && inside) {
+                    // box sums of p_j slide through registers: B(q-1), B(q) kept, B(q+1) new
+                    if (q == it.zlo - 1 || !bvalid) {
+                        bf_m = box9(sp + ((cq - 1) % NSP) * PS, of);
+                        bf_0 = box9(P0, of);
+                    }
+                    bf_p = box9(sp + ((cq + 1) % NSP) * PS, of);
+                }
                 if (inside) {
-                    const double *Pm = sp + ((cq - 1) % NSP) * PS, *Pp = sp + ((cq + 1) % NSP) * PS;
                     const double2 c = lds2(P0 + of);
-                    const double2 dn = lds2(Pm + of), up = lds2(Pp + of);
-                    const double2 ylo = lds2(P0 + of - BW), yhi = lds2(P0 + of + BW);
-                    const double l = lgf ? P0[of - 1] : 0.0;
-                    const double rr = rgf ? P0[of + 2] : 0.0;
                     double2 Ap;
-                    Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
-                    Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                    if (KIND == 2) {
+                        Ap.x = 27.0 * c.x - (bf_m.x + bf_0.x + bf_p.x);
+                        Ap.y = 27.0 * c.y - (bf_m.y + bf_0.y + bf_p.y);
+                    } else {
+                        const double *Pm = sp + ((cq - 1) % NSP) * PS, *Pp = sp + ((cq + 1) % NSP) * PS;
+                        const double2 dn = lds2(Pm + of), up = lds2(Pp + of);
+                        const double2 ylo = lds2(P0 + of - BW), yhi = lds2(P0 + of + BW);
+                        const double l = lgf ? P0[of - 1] : 0.0;
+                        const double rr = rgf ? P0[of + 2] : 0.0;
+                        Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                        Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                    }
                     u.x = cfr * (dinv_c * Ap.x - sigma * c.x);
                     u.y = cfr * (dinv_c * Ap.y - sigma * c.y);
                     if (mloaded) {
@@ -220,6 +251,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                 }
                 *reinterpret_cast<double2 *>(U + of) = u;
+                if (KIND == 2) {
+                    bvalid = inside;
+                    bf_m = bf_0;
+                    bf_0 = bf_p;
+                }
             }
             if (mloaded) {
                 __syncwarp();
@@ -229,15 +265,25 @@ __global__ void __launch_bounds__(THREADS, 1)
             consumers_sync();   // U(q) complete; U(q-4) no longer read
             // ---------------- back(q-1): step j+1 on the tile ----------------
             const int z = q - 1;
+            if (KIND == 2 && wb) {   // box sums of U(q) for the back task (window U(z-1), U(z), U(q))
+                bb_m = bb_0;
+                bb_0 = bb_p;
+                bb_p = box9(U, ob);
+            }
             if (wb && z >= it.zlo && z < it.zhi) {
                 const double *Um = su + ((z - 1 + 8) % NU) * PS, *U0 = su + ((z + 8) % NU) * PS;
                 const double2 c = lds2(U0 + ob);
-                const double2 dn = lds2(Um + ob), up = lds2(U + ob);
-                const double2 ylo = lds2(U0 + ob - BW), yhi = lds2(U0 + ob + BW);
-                const double l = U0[ob - 1], rr = U0[ob + 2];
                 double2 Ap;
-                Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
-                Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                if (KIND == 2) {
+                    Ap.x = 27.0 * c.x - (bb_m.x + bb_0.x + bb_p.x);
+                    Ap.y = 27.0 * c.y - (bb_m.y + bb_0.y + bb_p.y);
+                } else {
+                    const double2 dn = lds2(Um + ob), up = lds2(U + ob);
+                    const double2 ylo = lds2(U0 + ob - BW), yhi = lds2(U0 + ob + BW);
+                    const double l = U0[ob - 1], rr = U0[ob + 2];
+                    Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                    Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                }
                 if (!v1b) Ap.y = 0.0;
                 const int64_t i = (int64_t)z * pl + gib;
                 __stcs(reinterpret_cast<double2 *>(a.w2 + i), Ap);
@@ -289,13 +335,25 @@ bool k1f_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
-    return cudaFuncSetAttribute(k1f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+    return cudaFuncSetAttribute(k1f<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess &&
+           cudaFuncSetAttribute(k1f<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
 }
 
-bool k1f_enabled()
+// SSCG_K1_FUSE (read at every sscg_setup): "0" never, "1" always (7/27-point),
+// unset: 7-point slabs with at least K1F_MIN_WORK tile-planes per SM.  K1F
+// runs one CTA per SM and re-reads 4 planes of p_j per z-chunk, so small
+// grids (cfg 2, 128^3) run faster as single K1T steps; the 27-point pair is
+// bound by its in-plane box sums and gains nothing over two K1T steps
+// (profiles/r01g_workloads.jsonl).
+constexpr int64_t K1F_MIN_WORK = 256;
+
+bool k1f_enabled(const Geo &g, int nzl)
 {
-    const char *e = getenv("SSCG_K1_FUSE");   // read at every sscg_setup
-    return !(e && e[0] == '0');
+    const char *e = getenv("SSCG_K1_FUSE");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    const int64_t tiles = (int64_t)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
+    return g.kind == 1 && tiles * nzl >= K1F_MIN_WORK * k2_grid();
 }
 
 // steps j and j+1 over the planes [a.zb, a.ze) of one slab (a.p = p_j, a.pm =
@@ -350,7 +408,8 @@ void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevSta
     wk.zc = zc;
     wk.nitems = tiles * ((n1 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
-    k1f<<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, g, a, st, wk);
+    if (g.kind == 2) k1f<2><<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, g, a, st, wk);
+    else k1f<1><<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, g, a, st, wk);
 }
 
 }  // namespace sscg

@@ -67,6 +67,7 @@ struct sscg_ctx {
     DevState *st_host = nullptr;      // pinned
     // history (device) and host copies
     int hist_cap = 0;
+    double *h_lnorm = nullptr;
     double *h_gram = nullptr, *h_d = nullptr, *h_at = nullptr, *h_al = nullptr, *h_delta = nullptr,
            *h_relres = nullptr;
     std::vector<double> relres_host, delta_host;
@@ -311,7 +312,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the basis step");
             sl.has_k1t = true;
         }
-        if (A->kind == SSCG_OP_STENCIL7 && !diag_M && k1f_enabled()) {
+        if ((A->kind == SSCG_OP_STENCIL7 || A->kind == SSCG_OP_STENCIL27) && !diag_M && k1f_enabled(g, sl.nzl)) {
             if (!k1f_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused basis step");
             sl.has_k1f = true;
@@ -561,7 +562,8 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
 // constant diagonal) and, with neighbours, enough planes for an interior
 static bool uses_fused(const sscg_ctx *c)
 {
-    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->g.kind != SSCG_OP_STENCIL7) return false;
+    if (c->basis != SSCG_BASIS_CHEBYSHEV || (c->g.kind != SSCG_OP_STENCIL7 && c->g.kind != SSCG_OP_STENCIL27))
+        return false;
     const bool halo = c->slabs.size() > 1 || c->nranks > 1;
     for (const auto &sl : c->slabs)
         if (!sl.has_k1f || (halo && sl.nzl < 4)) return false;
@@ -661,7 +663,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     a4.nu = c->nu;
     a4.solver = (c->gram_solver == SSCG_GRAM_CHOLESKY) ? 1 : 0;
     a4.h_gram = c->h_gram; a4.h_d = c->h_d; a4.h_at = c->h_at; a4.h_al = c->h_al;
-    a4.h_delta = c->h_delta; a4.h_relres = c->h_relres;
+    a4.h_delta = c->h_delta; a4.h_relres = c->h_relres; a4.h_lnorm = c->h_lnorm;
     TRY(prof_mark(c, SSCG_PROF_FGS, true));
     launch_k4(a4, c->st, c->stream);
     TRY(prof_mark(c, SSCG_PROF_FGS, false));
@@ -757,6 +759,7 @@ static sscg_status ensure_history(sscg_ctx *c, int cap)
     TRY(dalloc(c, &c->h_at, (size_t)cap * s));
     TRY(dalloc(c, &c->h_al, (size_t)cap * s));
     TRY(dalloc(c, &c->h_delta, (size_t)cap));
+    TRY(dalloc(c, &c->h_lnorm, (size_t)cap));
     TRY(dalloc(c, &c->h_relres, (size_t)cap));
     c->hist_cap = cap;
     return SSCG_OK;
@@ -931,6 +934,7 @@ extern "C" sscg_status sscg_inspect(const sscg_ctx *cc, int32_t what, int32_t in
     case SSCG_INSPECT_ALPHA_T: src = c->h_at + (int64_t)index * s; cnt = s; break;
     case SSCG_INSPECT_ALPHA: src = c->h_al + (int64_t)index * s; cnt = s; break;
     case SSCG_INSPECT_DELTA: src = c->h_delta + index; cnt = 1; break;
+    case SSCG_INSPECT_LNORM: src = c->h_lnorm + index; cnt = 1; break;
     default: return fail(SSCG_ERR_INVALID, "unknown inspect target %d", what);
     }
     if (!need(cnt * 8)) return fail(SSCG_ERR_INVALID, "buffer too small");

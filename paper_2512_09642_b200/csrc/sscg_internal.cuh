@@ -102,7 +102,7 @@ bool k1t_prepare_faces(const Geo &g, const double *kx, const double *ky, const d
                        CUtensorMap *my, CUtensorMap *mz);
 
 // K1F: two 7-point basis steps per launch, single slab (k_stencil_fused.cu)
-bool k1f_enabled();
+bool k1f_enabled(const Geo &g, int nzl);
 bool k1f_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM);
 void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm);
 
@@ -130,6 +130,7 @@ struct K4Args {
     int s, nu;
     int solver;            // 0 = nu FGS sweeps, 1 = dense Cholesky
     double *h_gram, *h_d, *h_at, *h_al, *h_delta, *h_relres;  // history [cap][...]
+    double *h_lnorm;       // ||L||_F of the scaled Gram matrix G = I + L + L^T per outer
 };
 void launch_k4(const K4Args &a, DevState *st, cudaStream_t s);
 

@@ -115,3 +115,29 @@ def test_option_errors():
         for lo, hi in ((0.0, 1.0), (1.0, 1.0), (2.0, 1.0)):
             with pytest.raises(sscg.SSCGError):
                 S.set_bounds(lo, hi)
+
+
+@pytest.mark.parametrize("kind,nx,ny,nz,s,solver", [("7pt", 30, 28, 26, 16, "fgs"), ("5pt", 64, 64, 1, 8, "fgs"),
+                                                    ("7pt", 12, 12, 12, 40, "fgs"), ("27pt", 20, 18, 17, 12, "cholesky")])
+def test_diagnostics_lnorm_delta(kind, nx, ny, nz, s, solver):
+    """Per-outer diagnostics recorded by K4/K4C: ||L||_F of the scaled Gram
+    matrix G = I + L + L^T (the quantity FGS convergence depends on,
+    PAPER.md:24-25) and delta_k = ||c~ - G a~|| / ||c~||,
+    against the same quantities from the oracle's Gram trace at outer 0."""
+    import paper_2512_09642_b200 as sscg
+    bounds = (0.02, 2.2) if s == 40 else None
+    P = Problem(kind, nx, ny, nz, s, 25, bounds=bounds, lanczos=(kind == "27pt"))
+    x_or, tr = P.oracle_ex(max_outer=3, gram_solver=solver)
+    with P.gpu_solver(gram_solver=solver) as S:
+        S.solve(P.b_gpu(), rtol=0.0, max_outer=3)
+        d, G, ct = orc.scale(tr.ghat[0], tr.c[0])
+        ln_or = np.linalg.norm(np.tril(G, -1))
+        ln = S.inspect(sscg.INSPECT_LNORM, 0)[0]
+        assert abs(ln - ln_or) <= 1e-12 * ln_or
+        de = S.inspect(sscg.INSPECT_DELTA, 0)[0]
+        if solver == "fgs":
+            assert abs(de - tr.delta[0]) <= 1e-6 * tr.delta[0]
+        else:
+            assert de <= 1e-10 and tr.delta[0] <= 1e-10
+        st = S.stats()
+        assert np.allclose(st.delta_history[:3], [S.inspect(sscg.INSPECT_DELTA, k)[0] for k in range(3)], rtol=0)
