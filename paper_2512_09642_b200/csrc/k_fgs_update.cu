@@ -273,7 +273,9 @@ struct K5Params {
     int64_t N;         // interior doubles (nzl * plane)
     int s;
     const double *alpha;
-    double *x;         // process-layout x of this slab
+    double *const *xpp;   // device cell holding the caller's x (process layout):
+    int64_t xoff;         //   this launch updates (*xpp)[xoff ...]; read per launch so one
+                          //   captured graph serves every x (sscg_solve / sscg_iterate)
     int nx, pitch;
 };
 
@@ -291,7 +293,9 @@ __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState 
     const int64_t n2 = k.N >> 1;
     const double2 *P2 = reinterpret_cast<const double2 *>(k.P);
     const double2 *W2 = reinterpret_cast<const double2 *>(k.W);
-    double2 *x2 = reinterpret_cast<double2 *>(k.x);
+    double *xs = *k.xpp + k.xoff;
+    const bool xal = (reinterpret_cast<uintptr_t>(xs) & 15) == 0;   // else two 8-B accesses
+    double2 *x2 = reinterpret_cast<double2 *>(xs);
     double2 *r2 = reinterpret_cast<double2 *>(const_cast<double *>(k.P));
     const int64_t vs2 = k.vstride >> 1;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (int64_t)gridDim.x * blockDim.x) {
@@ -304,9 +308,14 @@ __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState 
             ax.x = fma(al[j], pj.x, ax.x); ax.y = fma(al[j], pj.y, ax.y);
             aw.x = fma(al[j], wj.x, aw.x); aw.y = fma(al[j], wj.y, aw.y);
         }
-        double2 xv = __ldcs(x2 + e);
-        xv.x += ax.x; xv.y += ax.y;
-        __stcs(x2 + e, xv);
+        if (xal) {
+            double2 xv = __ldcs(x2 + e);
+            xv.x += ax.x; xv.y += ax.y;
+            __stcs(x2 + e, xv);
+        } else {
+            xs[2 * e] += ax.x;
+            xs[2 * e + 1] += ax.y;
+        }
         __stcs(r2 + e, make_double2(p0.x - aw.x, p0.y - aw.y));
     }
 }
@@ -319,6 +328,7 @@ __global__ void __launch_bounds__(256) k5_update_gen(K5Params k, const DevState 
     for (int j = threadIdx.x; j < k.s; j += blockDim.x) al[j] = k.alpha[j];
     __syncthreads();
     double *r = const_cast<double *>(k.P);
+    double *xs = *k.xpp + k.xoff;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < k.N; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = e / k.pitch;
         const int xx = (int)(e - row * k.pitch);
@@ -331,7 +341,7 @@ __global__ void __launch_bounds__(256) k5_update_gen(K5Params k, const DevState 
             aw = fma(al[j], k.W[j * k.vstride + e], aw);
         }
         const int64_t xi = row * k.nx + xx;
-        k.x[xi] += ax;
+        xs[xi] += ax;
         r[e] = p0 - aw;
     }
 }
@@ -345,8 +355,8 @@ void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
     else k4_fgs<true><<<1, 32, 0, s>>>(a, st);
 }
 
-void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *x_slab, const DevState *st,
-               cudaStream_t stream, int zb, int ze)
+void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *const *xpp, int64_t xoff,
+               const DevState *st, cudaStream_t stream, int zb, int ze)
 {
     if (ze < 0) ze = sl.nzl + 1;
     if (ze <= zb) return;
@@ -355,13 +365,13 @@ void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double 
     k.W = sl.W + (int64_t)zb * g.plane;
     k.vstride = g.vstride;
     k.N = (int64_t)(ze - zb) * g.plane;
-    x_slab += (int64_t)(zb - 1) * g.nx * g.ny;
+    k.xpp = xpp;
+    k.xoff = xoff + (int64_t)(zb - 1) * g.nx * g.ny;
     k.s = s;
     k.alpha = alpha;
-    k.x = x_slab;
     k.nx = g.nx;
     k.pitch = g.pitch;
-    const bool vec = (g.pitch == g.nx) && ((reinterpret_cast<uintptr_t>(x_slab) & 15) == 0) && (k.N % 2 == 0);
+    const bool vec = (g.pitch == g.nx) && (k.N % 2 == 0) && (k.xoff % 2 == 0);
     const int64_t work = vec ? k.N / 2 : k.N;
     int64_t blocks = (work + 255) / 256;
     const int64_t cap = (int64_t)k2_grid() * 8;

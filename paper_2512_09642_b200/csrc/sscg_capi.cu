@@ -108,7 +108,8 @@ struct sscg_ctx {
     // CUDA graph of one outer iteration
     bool use_graph = true;
     cudaGraphExec_t gexec = nullptr;
-    double *graph_x = nullptr;
+    double **xdev = nullptr;      // device cell with the current x (K5 reads it per launch)
+    double **xhost = nullptr;     // pinned staging of that pointer
     int64_t graph_launches = 0, graph_allreduces = 0;
 };
 
@@ -342,6 +343,8 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         }
     }
     TRY(dalloc(c, &c->blk, (size_t)nent));
+    TRY(dalloc(c, &c->xdev, 1));
+    CU(cudaMallocHost(&c->xhost, sizeof(double *)));
     TRY(dalloc(c, &c->alpha, 64));
     {
         std::vector<double *> ptrs;
@@ -391,6 +394,7 @@ extern "C" void sscg_destroy(sscg_ctx *c)
     if (c->comm) ncclCommDestroy(c->comm);
     for (void *p : c->allocs) cudaFree(p);
     if (c->st_host) cudaFreeHost(c->st_host);
+    if (c->xhost) cudaFreeHost(c->xhost);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -674,7 +678,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
             const int b = std::max(zb, 1);
             if (e <= b) continue;
             TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
-            launch_k5(g, sl, s, c->alpha, x + sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, b, e);
+            launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, b, e);
             TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
             ++c->launches;
         }
@@ -693,7 +697,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
             for (int zb : {1, top}) {
                 if (zb > sl.nzl) continue;
                 TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
-                launch_k5(g, sl, s, c->alpha, x + sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, zb, zb + 1);
+                launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, zb, zb + 1);
                 TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
                 ++c->launches;
             }
@@ -713,7 +717,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
 static sscg_status run_outer(sscg_ctx *c, double *x)
 {
     if (c->prof_on || !c->use_graph) return enqueue_outer(c, x);
-    if (!c->gexec || c->graph_x != x) {
+    if (!c->gexec) {
         if (c->gexec) {
             cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
@@ -738,7 +742,6 @@ static sscg_status run_outer(sscg_ctx *c, double *x)
         c->graph_allreduces = c->allreduces - a0;
         c->launches = l0;
         c->allreduces = a0;
-        c->graph_x = x;
     }
     CU(cudaGraphLaunch(c->gexec, c->stream));
     c->launches += c->graph_launches;
@@ -785,6 +788,8 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
     *c->st_host = h;
     CU(cudaEventRecord(c->ev0, c->stream));
     CU(cudaMemcpyAsync(c->st, c->st_host, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+    *c->xhost = x;   // K5 reads x through this cell: the captured outer iteration serves any x
+    CU(cudaMemcpyAsync(c->xdev, c->xhost, sizeof(double *), cudaMemcpyHostToDevice, c->stream));
     const int L = (int)c->slabs.size();
     // r_0 = b - A x_0 into p_0
     if (flags & SSCG_SOLVE_X0_ZERO) {
@@ -957,6 +962,8 @@ extern "C" sscg_status sscg_iterate(sscg_ctx *c, double *x, int32_t nsteps)
     *c->st_host = h;
     CU(cudaEventRecord(c->ev0, c->stream));
     CU(cudaMemcpyAsync(c->st, c->st_host, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+    *c->xhost = x;
+    CU(cudaMemcpyAsync(c->xdev, c->xhost, sizeof(double *), cudaMemcpyHostToDevice, c->stream));
     for (int i = 0; i < nsteps; ++i) TRY(run_outer(c, x));
     CU(cudaEventRecord(c->ev1, c->stream));
     CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));

@@ -303,3 +303,21 @@ def test_face_staging_matches_direct_loads(monkeypatch):
     assert np.linalg.norm(a[0] - b[0]) <= 1e-12 * np.linalg.norm(b[0])
     x_or, _ = P.oracle(max_outer=3)
     assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+def test_graph_reused_across_x_buffers():
+    """One captured outer iteration serves every x: K5 reads the caller's x
+    through a device cell, so solves into different (also 8-B-only aligned)
+    x buffers reuse the same CUDA graph and give the same iterates."""
+    import torch
+    P = Problem("7pt", 26, 22, 18, 6, 12)
+    x_or, _ = P.oracle(max_outer=4)
+    with P.gpu_solver() as S:
+        xa = S.solve(P.b_gpu(), rtol=0.0, max_outer=4).cpu().numpy()
+        big = torch.zeros(P.b.size + 1, dtype=torch.float64, device="cuda")
+        xv = big[1:]                                   # 8-B aligned only
+        S.solve(P.b_gpu(), xv, rtol=0.0, max_outer=4)
+        xb = xv.cpu().numpy()
+        xc = S.solve_host(P.b.copy(), rtol=0.0, max_outer=4)
+    assert np.array_equal(xa, xb) and np.array_equal(xa, xc)
+    assert np.linalg.norm(xa - x_or) <= TOL_X10 * np.linalg.norm(x_or)
