@@ -303,8 +303,9 @@ def run_ours(a):
         face_bytes = 8.0 * (n * (n + 1) * S.nz_local * 2 + n * n * (S.nz_local + 1))
     basis_vecs = S.query(sscg.QUERY_BASIS_VECTORS)       # (4s-3), or 46 at s = 16 with K1F pairs
     fused = bool(S.query(sscg.QUERY_BASIS_FUSED))
+    upd_vecs = S.query(sscg.QUERY_UPDATE_VECTORS)        # 2s+3, or s+4 with W alpha from the recurrence
     bytes_per_outer = {"basis": basis_vecs * vec + s * face_bytes, "gram": 2 * s * vec,
-                       "update": (2 * s + 3) * vec}
+                       "update": upd_vecs * vec}
     kern = {}
     for k, byt in bytes_per_outer.items():
         t_ms, cnt = prof[k]
@@ -328,8 +329,9 @@ def run_ours(a):
             "traffic": ncu_traffic(n, k1_name) if a.workload == "cfg5" else None, "peak_source": peak_src,
             "traffic_note": "ncu dram read+write of one interior launch (algorithmic: %d vectors = %.4g B)"
                             % (6 if fused else 4, (6 if fused else 4) * vec),
-            "bytes_rule": "%d FP64 vectors per outer (%s) + s face sets for varcoef7, / basis launches (SURVEY 8(d))"
-                          % (basis_vecs, "K1F pairs: 6 per pair" if fused else "(4s-3)"),
+            "bytes_rule": "%d FP64 vectors per outer (%s) + s face sets for varcoef7, / basis launches (SURVEY 8(d)); "
+                          "path: basis + 2s (Gram) + %d (update) vectors"
+                          % (basis_vecs, "K1F pairs: 6 per pair" if fused else "(4s-3)", upd_vecs),
             "path_bytes_per_step": path_bytes,
             "path_achieved_gbs": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9,
             "path_frac": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9 / peak}

@@ -30,7 +30,7 @@ SOLVE_X0_ZERO = 1
 OPT_GRAM_SOLVER, OPT_BASIS = 0, 1
 GRAM_FGS, GRAM_CHOLESKY = 0, 1
 BASIS_CHEBYSHEV, BASIS_MONOMIAL = 0, 1
-QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS = 0, 1
+QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS, QUERY_UPDATE_VECTORS = 0, 1, 2
 
 EXPORTS = ["sscg_partition", "sscg_halo_plan", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host", "sscg_iterate",
            "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect", "sscg_local_shape", "sscg_destroy",

@@ -273,6 +273,8 @@ struct K5Params {
     int64_t N;         // interior doubles (nzl * plane)
     int s;
     const double *alpha;
+    int rec;              // 1: r -= W alpha formed from the basis recurrence (k5 REC)
+    double theta, sigma, dm;   // Chebyshev parameters and the constant Jacobi diagonal M
     double *const *xpp;   // device cell holding the caller's x (process layout):
     int64_t xoff;         //   this launch updates (*xpp)[xoff ...]; read per launch so one
                           //   captured graph serves every x (sscg_solve / sscg_iterate)
@@ -282,13 +284,32 @@ struct K5Params {
 // flat path: pitch == nx and x 16-B aligned; 2 points per thread per step.
 // S > 0: the basis size is a compile-time constant, so all 2S loads of a
 // point are issued before the first FMA (S = 0: runtime s).
-template <int S>
+// REC: the Chebyshev recurrence gives, for a constant
+// Jacobi diagonal M = m I,
+//   w_0 = m (p_1/theta + sigma p_0),  w_j = m ((p_{j+1} + p_{j-1})/(2 theta) + sigma p_j)  (1 <= j <= s-2)
+// so  W alpha = m sum_k gamma_k p_k + alpha_{s-1} w_{s-1}  with gamma from alpha
+// (R21).  The update then streams P, w_{s-1} and x (s+2 vectors in,
+// 2 out) instead of P, W and x (2s+1 in): the per-point rounding is of the
+// same order as forming W alpha from the stored W (whose SpMV entries carry
+// the same m |p| cancellation), unlike the Gram dots, which keep W.
+template <int S, bool REC>
 __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState *st)
 {
     if (st->done) return;
-    __shared__ double al[SMAX];
+    __shared__ double al[SMAX], ga[SMAX];
     for (int j = threadIdx.x; j < k.s; j += blockDim.x) al[j] = k.alpha[j];
     __syncthreads();
+    if (REC) {
+        for (int j = threadIdx.x; j < k.s; j += blockDim.x) {
+            const int s1 = k.s - 1;
+            double g = (j < s1) ? k.sigma * al[j] : 0.0;
+            if (j == 1) g += al[0] / k.theta;
+            if (j - 1 >= 1 && j - 1 <= s1 - 1) g += al[j - 1] / (2.0 * k.theta);
+            if (j + 1 >= 1 && j + 1 <= s1 - 1) g += al[j + 1] / (2.0 * k.theta);
+            ga[j] = k.dm * g;
+        }
+        __syncthreads();
+    }
     const int s = S > 0 ? S : k.s;
     const int64_t n2 = k.N >> 1;
     const double2 *P2 = reinterpret_cast<const double2 *>(k.P);
@@ -301,12 +322,23 @@ __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState 
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (int64_t)gridDim.x * blockDim.x) {
         double2 ax = make_double2(0.0, 0.0), aw = make_double2(0.0, 0.0);
         const double2 p0 = __ldcs(P2 + e);
+        if (REC) {
 #pragma unroll
-        for (int j = 0; j < s; ++j) {
-            const double2 pj = (j == 0) ? p0 : __ldcs(P2 + j * vs2 + e);
-            const double2 wj = __ldcs(W2 + j * vs2 + e);
-            ax.x = fma(al[j], pj.x, ax.x); ax.y = fma(al[j], pj.y, ax.y);
-            aw.x = fma(al[j], wj.x, aw.x); aw.y = fma(al[j], wj.y, aw.y);
+            for (int j = 0; j < s; ++j) {
+                const double2 pj = (j == 0) ? p0 : __ldcs(P2 + j * vs2 + e);
+                ax.x = fma(al[j], pj.x, ax.x); ax.y = fma(al[j], pj.y, ax.y);
+                aw.x = fma(ga[j], pj.x, aw.x); aw.y = fma(ga[j], pj.y, aw.y);
+            }
+            const double2 wl = __ldcs(W2 + (s - 1) * vs2 + e);
+            aw.x = fma(al[s - 1], wl.x, aw.x); aw.y = fma(al[s - 1], wl.y, aw.y);
+        } else {
+#pragma unroll
+            for (int j = 0; j < s; ++j) {
+                const double2 pj = (j == 0) ? p0 : __ldcs(P2 + j * vs2 + e);
+                const double2 wj = __ldcs(W2 + j * vs2 + e);
+                ax.x = fma(al[j], pj.x, ax.x); ax.y = fma(al[j], pj.y, ax.y);
+                aw.x = fma(al[j], wj.x, aw.x); aw.y = fma(al[j], wj.y, aw.y);
+            }
         }
         if (xal) {
             double2 xv = __ldcs(x2 + e);
@@ -356,7 +388,7 @@ void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
 }
 
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *const *xpp, int64_t xoff,
-               const DevState *st, cudaStream_t stream, int zb, int ze)
+               const DevState *st, cudaStream_t stream, int zb, int ze, double theta, double sigma, bool rec)
 {
     if (ze < 0) ze = sl.nzl + 1;
     if (ze <= zb) return;
@@ -365,6 +397,10 @@ void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double 
     k.W = sl.W + (int64_t)zb * g.plane;
     k.vstride = g.vstride;
     k.N = (int64_t)(ze - zb) * g.plane;
+    k.rec = rec && s >= 2;
+    k.theta = theta;
+    k.sigma = sigma;
+    k.dm = g.center;
     k.xpp = xpp;
     k.xoff = xoff + (int64_t)(zb - 1) * g.nx * g.ny;
     k.s = s;
@@ -376,14 +412,23 @@ void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double 
     int64_t blocks = (work + 255) / 256;
     const int64_t cap = (int64_t)k2_grid() * 8;
     if (blocks > cap) blocks = cap;
-    if (vec) {
+    if (vec && k.rec) {
         switch (s) {
-        case 4: k5_update_vec<4><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 8: k5_update_vec<8><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 16: k5_update_vec<16><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 24: k5_update_vec<24><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 32: k5_update_vec<32><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        default: k5_update_vec<0><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 4: k5_update_vec<4, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 8: k5_update_vec<8, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 16: k5_update_vec<16, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 24: k5_update_vec<24, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 32: k5_update_vec<32, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        default: k5_update_vec<0, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        }
+    } else if (vec) {
+        switch (s) {
+        case 4: k5_update_vec<4, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 8: k5_update_vec<8, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 16: k5_update_vec<16, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 24: k5_update_vec<24, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 32: k5_update_vec<32, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        default: k5_update_vec<0, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
         }
     }
     else k5_update_gen<<<(unsigned)blocks, 256, 0, stream>>>(k, st);

@@ -574,6 +574,20 @@ static bool uses_fused(const sscg_ctx *c)
     return true;
 }
 
+// K5 forms W alpha from the Chebyshev recurrence (R21) for the
+// constant-coefficient stencils with M = diag(A) and a Chebyshev basis
+// (SSCG_K5_RECUR=0 keeps the stored-W form everywhere)
+static bool uses_rec_update(const sscg_ctx *c)
+{
+    const char *e = getenv("SSCG_K5_RECUR");
+    if (e && e[0] == '0') return false;
+    const Geo &g = c->g;
+    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2 || !(g.center > 0.0) || g.pitch != g.nx) return false;
+    for (const auto &sl : c->slabs)
+        if (sl.dinv) return false;
+    return true;
+}
+
 // K1F: basis steps j, j+1 in one launch per slab, over all planes (part 0,
 // a slab bounded by the global Dirichlet planes) or the planes [2, nzl) that
 // need no halo of p_{j+1} (part 2)
@@ -678,7 +692,8 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
             const int b = std::max(zb, 1);
             if (e <= b) continue;
             TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
-            launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, b, e);
+            launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, b, e, c->theta,
+                      c->sigma, uses_rec_update(c));
             TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
             ++c->launches;
         }
@@ -697,7 +712,8 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
             for (int zb : {1, top}) {
                 if (zb > sl.nzl) continue;
                 TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
-                launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, zb, zb + 1);
+                launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, zb, zb + 1,
+                          c->theta, c->sigma, uses_rec_update(c));
                 TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
                 ++c->launches;
             }
@@ -1176,6 +1192,11 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
         *out = v;
         return SSCG_OK;
     }
+    case SSCG_QUERY_UPDATE_VECTORS:
+        // P (s) + x in, x + r out; the stored-W form also reads W (s), the
+        // recurrence form only w_{s-1}
+        *out = uses_rec_update(c) ? (int64_t)s + 4 : 2 * (int64_t)s + 3;
+        return SSCG_OK;
     default:
         return fail(SSCG_ERR_INVALID, "unknown query %d", what);
     }

@@ -135,8 +135,9 @@ struct K4Args {
 void launch_k4(const K4Args &a, DevState *st, cudaStream_t s);
 
 // K5: x += P alpha;  p_0 -= W alpha over padded planes [zb, ze) (ze < 0: to nzl+1)
+//   rec: form W alpha from the Chebyshev recurrence (constant diagonal, vector path only)
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *const *xpp, int64_t xoff,
-               const DevState *st, cudaStream_t stream, int zb = 1, int ze = -1);
+               const DevState *st, cudaStream_t stream, int zb, int ze, double theta, double sigma, bool rec);
 
 // Lanczos spectral bounds (k_lanczos.cu)
 int lz_grid();

@@ -321,3 +321,30 @@ def test_graph_reused_across_x_buffers():
         xc = S.solve_host(P.b.copy(), rtol=0.0, max_outer=4)
     assert np.array_equal(xa, xb) and np.array_equal(xa, xc)
     assert np.linalg.norm(xa - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+@pytest.mark.parametrize("cfg", [("7pt", 40, 36, 33, 16, 25), ("27pt", 30, 28, 26, 16, 30), ("5pt", 64, 64, 1, 8, 20),
+                                 ("7pt", 34, 30, 28, 2, 5)], ids=_ids)
+def test_recurrence_update_matches_stored_w(cfg, monkeypatch):
+    """K5 forming W alpha from the Chebyshev recurrence (R21)
+    against the stored-W form and the oracle: x after 10 outer iterations to
+    the north_star 1e-8, the same outer count to rtol 1e-8 (+-1), and a true
+    residual at the tolerance."""
+    import paper_2512_09642_b200 as sscg
+    kind, nx, ny, nz, s, nu = cfg
+    P = Problem(kind, nx, ny, nz, s, nu, lanczos=(kind == "27pt"))
+    x_or, _ = P.oracle(max_outer=10)
+    res = {}
+    for rec in ("1", "0"):
+        monkeypatch.setenv("SSCG_K5_RECUR", rec)
+        with P.gpu_solver() as S:
+            assert S.query(sscg.QUERY_UPDATE_VECTORS) == (s + 4 if rec == "1" else 2 * s + 3)
+            x10 = S.solve(P.b_gpu(), rtol=0.0, max_outer=10).cpu().numpy()
+            xf = S.solve(P.b_gpu(), rtol=1e-8, max_outer=20000).cpu().numpy()
+            res[rec] = (x10, xf, S.stats().outer_iterations)
+    for rec in ("1", "0"):
+        x10, xf, it = res[rec]
+        assert np.linalg.norm(x10 - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+        tr = np.linalg.norm(P.b - orc.apply(P.A, xf)) / np.linalg.norm(P.b)
+        assert tr <= 1e-8 * 1.05, (rec, tr)
+    assert abs(res["1"][2] - res["0"][2]) <= 1
