@@ -213,7 +213,8 @@ SSCG_API sscg_status sscg_stats(const sscg_ctx *ctx, sscg_stats_t *out);
 enum {
     SSCG_INSPECT_P = 0, SSCG_INSPECT_W = 1, SSCG_INSPECT_GRAM = 2, SSCG_INSPECT_D = 3,
     SSCG_INSPECT_ALPHA_T = 4, SSCG_INSPECT_ALPHA = 5, SSCG_INSPECT_DELTA = 6,
-    SSCG_INSPECT_LNORM = 7     /* outer `index`: ||L||_F of G = I + L + L^T, 1 double */
+    SSCG_INSPECT_LNORM = 7,    /* outer `index`: ||L||_F of G = I + L + L^T, 1 double */
+    SSCG_INSPECT_KAPPA = 8     /* outer `index`: kappa(G) (with SSCG_OPT_DIAGNOSTICS, else 0), 1 double */
 };
 SSCG_API sscg_status sscg_inspect(const sscg_ctx *ctx, int32_t what, int32_t index, void *host_out,
                          int64_t capacity);
@@ -258,8 +259,12 @@ SSCG_API sscg_status sscg_estimate_bounds(sscg_ctx *ctx, const double *v0, int32
  *                         SSCG_BASIS_MONOMIAL p_{j+1} = M^{-1}A p_j
  *                         (kappa(G) grows like
  *                         kappa(M^{-1}A)^{s-1}, so only small s is usable).
+ *   SSCG_OPT_DIAGNOSTICS  0 (default) / 1: after every update also compute
+ *                         kappa(G) of the scaled Gram matrix (one-warp Jacobi
+ *                         eigensolver, off the hot path), read back with
+ *                         SSCG_INSPECT_KAPPA.
  * Errors: SSCG_ERR_INVALID for an unknown key or value. */
-enum { SSCG_OPT_GRAM_SOLVER = 0, SSCG_OPT_BASIS = 1 };
+enum { SSCG_OPT_GRAM_SOLVER = 0, SSCG_OPT_BASIS = 1, SSCG_OPT_DIAGNOSTICS = 2 };
 enum { SSCG_GRAM_FGS = 0, SSCG_GRAM_CHOLESKY = 1 };
 enum { SSCG_BASIS_CHEBYSHEV = 0, SSCG_BASIS_MONOMIAL = 1 };
 SSCG_API sscg_status sscg_set_option(sscg_ctx *ctx, int32_t key, int32_t value);

@@ -25,9 +25,10 @@ LIB_PATH = os.path.join(_HERE, "libsscg.so")
 
 OK, ERR_INVALID, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_BREAKDOWN, ERR_NONFINITE, ERR_UNSUPPORTED = range(8)
 OP_STENCIL5_2D, OP_STENCIL7, OP_STENCIL27, OP_VARCOEF7, OP_CSR = range(5)
-INSPECT_P, INSPECT_W, INSPECT_GRAM, INSPECT_D, INSPECT_ALPHA_T, INSPECT_ALPHA, INSPECT_DELTA, INSPECT_LNORM = range(8)
+(INSPECT_P, INSPECT_W, INSPECT_GRAM, INSPECT_D, INSPECT_ALPHA_T, INSPECT_ALPHA, INSPECT_DELTA, INSPECT_LNORM,
+ INSPECT_KAPPA) = range(9)
 SOLVE_X0_ZERO = 1
-OPT_GRAM_SOLVER, OPT_BASIS = 0, 1
+OPT_GRAM_SOLVER, OPT_BASIS, OPT_DIAGNOSTICS = 0, 1, 2
 GRAM_FGS, GRAM_CHOLESKY = 0, 1
 BASIS_CHEBYSHEV, BASIS_MONOMIAL = 0, 1
 QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS, QUERY_UPDATE_VECTORS = 0, 1, 2
@@ -312,7 +313,7 @@ class Solver:
     def inspect(self, what: int, index: int) -> np.ndarray:
         n = {INSPECT_P: self.n_local, INSPECT_W: self.n_local, INSPECT_GRAM: self.s * self.s + self.s,
              INSPECT_D: self.s, INSPECT_ALPHA_T: self.s, INSPECT_ALPHA: self.s, INSPECT_DELTA: 1,
-             INSPECT_LNORM: 1}[what]
+             INSPECT_LNORM: 1, INSPECT_KAPPA: 1}[what]
         out = np.empty(n, dtype=np.float64)
         _check(load().sscg_inspect(self._h, what, index, out.ctypes.data, out.nbytes))
         return out

@@ -266,6 +266,75 @@ __global__ void __launch_bounds__(32) k4_chol(K4Args a, DevState *st)
     }
 }
 
+// Diagnostics (SSCG_OPT_DIAGNOSTICS): kappa(G) of the
+// Ruhe-scaled Gram matrix of the outer iteration K4 just completed
+// ("kappa(G) = O(s^2) ... conditioning"), from its eigenvalues
+// by cyclic Jacobi rotations on one warp (each rotation's row/column update
+// spread over the lanes).  Off the hot path: launched only when enabled.
+__global__ void __launch_bounds__(32) k_kappa(const double *blk, int s, const DevState *st, double *h_kappa)
+{
+    if (st->done) return;
+    const int k = st->k - 1;
+    if (k < 0 || k >= st->hist_cap) return;
+    __shared__ double A[SMAX * SMAX], d[SMAX];
+    const int lane = threadIdx.x;
+    for (int i = lane; i < s; i += 32) d[i] = 1.0 / sqrt(blk[i * s + i]);
+    __syncwarp();
+    for (int q = lane; q < s * s; q += 32) {
+        const int i = q / s, j = q - i * s;
+        A[q] = (i == j) ? 1.0 : (d[i] * blk[q]) * d[j];
+    }
+    __syncwarp();
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        double off = 0.0, dia = 0.0;
+        for (int q = lane; q < s * s; q += 32) {
+            const int i = q / s, j = q - i * s;
+            if (i < j) off += A[q] * A[q];
+            else if (i == j) dia += A[q] * A[q];
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            off += __shfl_xor_sync(0xffffffffu, off, o);
+            dia += __shfl_xor_sync(0xffffffffu, dia, o);
+        }
+        if (off <= 1e-32 * dia) break;
+        for (int p = 0; p < s - 1; ++p)
+            for (int q = p + 1; q < s; ++q) {
+                const double apq = A[p * s + q];
+                if (apq == 0.0) continue;
+                const double app = A[p * s + p], aqq = A[q * s + q];
+                const double th = (aqq - app) / (2.0 * apq);
+                const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+                __syncwarp();
+                for (int r = lane; r < s; r += 32) {
+                    if (r == p || r == q) continue;
+                    const double arp = A[r * s + p], arq = A[r * s + q];
+                    const double np = c * arp - sn * arq, nq = sn * arp + c * arq;
+                    A[r * s + p] = np; A[p * s + r] = np;
+                    A[r * s + q] = nq; A[q * s + r] = nq;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    A[p * s + p] = app - t * apq;
+                    A[q * s + q] = aqq + t * apq;
+                    A[p * s + q] = 0.0;
+                    A[q * s + p] = 0.0;
+                }
+                __syncwarp();
+            }
+    }
+    double lo = 1e300, hi = -1e300;
+    for (int i = lane; i < s; i += 32) {
+        lo = fmin(lo, A[i * s + i]);
+        hi = fmax(hi, A[i * s + i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) h_kappa[k] = (lo > 0.0) ? hi / lo : INFINITY;
+}
+
 struct K5Params {
     const double *P;   // interior start of p_0 (= r_k)
     const double *W;   // interior start of w_0
@@ -385,6 +454,11 @@ void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
     if (a.solver == 1) k4_chol<<<1, 32, 0, s>>>(a, st);
     else if (a.s <= 32) k4_fgs<false><<<1, 32, 0, s>>>(a, st);
     else k4_fgs<true><<<1, 32, 0, s>>>(a, st);
+}
+
+void launch_kappa(const double *blk, int s, const DevState *st, double *h_kappa, cudaStream_t stream)
+{
+    k_kappa<<<1, 32, 0, stream>>>(blk, s, st, h_kappa);
 }
 
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *const *xpp, int64_t xoff,

@@ -84,6 +84,8 @@ struct sscg_ctx {
     int gram_solver = SSCG_GRAM_FGS;
     int basis = SSCG_BASIS_CHEBYSHEV;
     bool bounds_set = false;
+    bool diagnostics = false;
+    double *h_kappa = nullptr;
     // Lanczos workspace (sscg_estimate_bounds): 3 vectors + D per slab, lazily
     std::vector<double *> lz_vec;     // [slab * 5 + {y0, y1, y2, w, D}]
     double *lz_scal = nullptr;        // device scalars, see sscg_estimate_bounds
@@ -684,6 +686,10 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     a4.h_delta = c->h_delta; a4.h_relres = c->h_relres; a4.h_lnorm = c->h_lnorm;
     TRY(prof_mark(c, SSCG_PROF_FGS, true));
     launch_k4(a4, c->st, c->stream);
+    if (c->diagnostics) {
+        launch_kappa(c->blk, s, c->st, c->h_kappa, c->stream);
+        ++c->launches;
+    }
     TRY(prof_mark(c, SSCG_PROF_FGS, false));
     ++c->launches;
     auto k5 = [&](int zb, int ze) -> sscg_status {
@@ -779,6 +785,8 @@ static sscg_status ensure_history(sscg_ctx *c, int cap)
     TRY(dalloc(c, &c->h_al, (size_t)cap * s));
     TRY(dalloc(c, &c->h_delta, (size_t)cap));
     TRY(dalloc(c, &c->h_lnorm, (size_t)cap));
+    TRY(dalloc(c, &c->h_kappa, (size_t)cap));
+    CU(cudaMemset(c->h_kappa, 0, (size_t)cap * sizeof(double)));
     TRY(dalloc(c, &c->h_relres, (size_t)cap));
     c->hist_cap = cap;
     return SSCG_OK;
@@ -956,6 +964,7 @@ extern "C" sscg_status sscg_inspect(const sscg_ctx *cc, int32_t what, int32_t in
     case SSCG_INSPECT_ALPHA: src = c->h_al + (int64_t)index * s; cnt = s; break;
     case SSCG_INSPECT_DELTA: src = c->h_delta + index; cnt = 1; break;
     case SSCG_INSPECT_LNORM: src = c->h_lnorm + index; cnt = 1; break;
+    case SSCG_INSPECT_KAPPA: src = c->h_kappa + index; cnt = 1; break;
     default: return fail(SSCG_ERR_INVALID, "unknown inspect target %d", what);
     }
     if (!need(cnt * 8)) return fail(SSCG_ERR_INVALID, "buffer too small");
@@ -1045,6 +1054,10 @@ extern "C" sscg_status sscg_set_option(sscg_ctx *c, int32_t key, int32_t value)
     case SSCG_OPT_GRAM_SOLVER:
         if (value != SSCG_GRAM_FGS && value != SSCG_GRAM_CHOLESKY) return fail(SSCG_ERR_INVALID, "bad Gram solver %d", value);
         c->gram_solver = value;
+        break;
+    case SSCG_OPT_DIAGNOSTICS:
+        if (value != 0 && value != 1) return fail(SSCG_ERR_INVALID, "bad diagnostics flag %d", value);
+        c->diagnostics = value == 1;
         break;
     case SSCG_OPT_BASIS:
         if (value != SSCG_BASIS_CHEBYSHEV && value != SSCG_BASIS_MONOMIAL) return fail(SSCG_ERR_INVALID, "bad basis %d", value);

@@ -134,6 +134,9 @@ struct K4Args {
 };
 void launch_k4(const K4Args &a, DevState *st, cudaStream_t s);
 
+// diagnostics: kappa(G) of the scaled Gram matrix of the last update (one warp)
+void launch_kappa(const double *blk, int s, const DevState *st, double *h_kappa, cudaStream_t stream);
+
 // K5: x += P alpha;  p_0 -= W alpha over padded planes [zb, ze) (ze < 0: to nzl+1)
 //   rec: form W alpha from the Chebyshev recurrence (constant diagonal, vector path only)
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *const *xpp, int64_t xoff,

@@ -141,3 +141,24 @@ def test_diagnostics_lnorm_delta(kind, nx, ny, nz, s, solver):
             assert de <= 1e-10 and tr.delta[0] <= 1e-10
         st = S.stats()
         assert np.allclose(st.delta_history[:3], [S.inspect(sscg.INSPECT_DELTA, k)[0] for k in range(3)], rtol=0)
+
+
+@pytest.mark.parametrize("kind,nx,ny,nz,s", [("7pt", 30, 28, 26, 16), ("5pt", 64, 64, 1, 8), ("7pt", 24, 20, 18, 24),
+                                             ("27pt", 20, 18, 17, 5)])
+def test_diagnostics_kappa(kind, nx, ny, nz, s):
+    """kappa(G) of the Ruhe-scaled Gram matrix per outer (SSCG_OPT_DIAGNOSTICS),
+    against numpy's condition number of the oracle's scaled G at outer 0."""
+    import paper_2512_09642_b200 as sscg
+    P = Problem(kind, nx, ny, nz, s, 20, lanczos=(kind == "27pt"))
+    x_or, tr = P.oracle(max_outer=2)
+    with P.gpu_solver() as S:
+        S.set_option(sscg.OPT_DIAGNOSTICS, 1)
+        S.solve(P.b_gpu(), rtol=0.0, max_outer=2)
+        d, G, ct = orc.scale(tr.ghat[0], tr.c[0])
+        ev = np.linalg.eigvalsh(G)
+        assert ev[0] > 0
+        k_ref = ev[-1] / ev[0]
+        k_gpu = S.inspect(sscg.INSPECT_KAPPA, 0)[0]
+        # eigenvalues of G are perturbed by ~eps ||G|| (Weyl): relative accuracy of kappa ~ eps kappa
+        assert abs(k_gpu - k_ref) <= max(1e-10, 1e-14 * k_ref) * k_ref, (k_gpu, k_ref)
+        assert S.inspect(sscg.INSPECT_KAPPA, 1)[0] > 1.0
