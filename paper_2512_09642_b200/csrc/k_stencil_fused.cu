@@ -379,7 +379,8 @@ void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevSta
     wk.center = g.center;
     wk.dinv_c = g.dinv_c;
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
-    const int64_t resident = k2_grid();   // one CTA per SM
+    // one CTA per SM (fewer with a.sm_cap: SMs left to the overlapped NCCL exchange)
+    const int64_t resident = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
     static int zc_env = -1;
     if (zc_env < 0) {
         const char *e = getenv("SSCG_K1_ZC");

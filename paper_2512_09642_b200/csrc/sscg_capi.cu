@@ -609,6 +609,7 @@ static sscg_status launch_basis_pair(sscg_ctx *c, int j, int part)
         a.nzl = sl.nzl;
         a.zb = (part == 0) ? 1 : 2;
         a.ze = (part == 0) ? sl.nzl + 1 : sl.nzl;
+        if (part == 2) a.sm_cap = c->k1_sm_cap;
         a.j = j;
         a.tmF_P = &sl.tmF_P;
         a.tmF_M = &sl.tmF_M;
