@@ -278,8 +278,8 @@ SSCG_API sscg_status sscg_set_option(sscg_ctx *ctx, int32_t key, int32_t value);
  *   SSCG_QUERY_UPDATE_VECTORS FP64 vectors the update kernel moves per outer
  *                             iteration: 2s+3 (r -= W alpha from the stored
  *                             W), or s+4 when W alpha is formed from the
- *                             Chebyshev recurrence (constant Jacobi diagonal;
- *                             DESIGN.md R21)
+ *                             Chebyshev recurrence (R21; s+5 when
+ *                             the Jacobi diagonal varies and is read too)
  * Errors: SSCG_ERR_INVALID. */
 enum { SSCG_QUERY_BASIS_FUSED = 0, SSCG_QUERY_BASIS_VECTORS = 1, SSCG_QUERY_UPDATE_VECTORS = 2 };
 SSCG_API sscg_status sscg_query(const sscg_ctx *ctx, int32_t what, int64_t *out);

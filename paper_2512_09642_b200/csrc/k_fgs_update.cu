@@ -344,6 +344,7 @@ struct K5Params {
     const double *alpha;
     int rec;              // 1: r -= W alpha formed from the basis recurrence (k5 REC)
     double theta, sigma, dm;   // Chebyshev parameters and the constant Jacobi diagonal M
+    const double *dvec;        // or the diagonal M per point (padded layout, interior start), else null
     double *const *xpp;   // device cell holding the caller's x (process layout):
     int64_t xoff;         //   this launch updates (*xpp)[xoff ...]; read per launch so one
                           //   captured graph serves every x (sscg_solve / sscg_iterate)
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState 
             if (j == 1) g += al[0] / k.theta;
             if (j - 1 >= 1 && j - 1 <= s1 - 1) g += al[j - 1] / (2.0 * k.theta);
             if (j + 1 >= 1 && j + 1 <= s1 - 1) g += al[j + 1] / (2.0 * k.theta);
-            ga[j] = k.dm * g;
+            ga[j] = k.dvec ? g : k.dm * g;
         }
         __syncthreads();
     }
@@ -397,6 +398,11 @@ __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState 
                 const double2 pj = (j == 0) ? p0 : __ldcs(P2 + j * vs2 + e);
                 ax.x = fma(al[j], pj.x, ax.x); ax.y = fma(al[j], pj.y, ax.y);
                 aw.x = fma(ga[j], pj.x, aw.x); aw.y = fma(ga[j], pj.y, aw.y);
+            }
+            if (k.dvec) {   // variable diagonal: M sum gamma_k p_k pointwise
+                const double2 m = __ldcs(reinterpret_cast<const double2 *>(k.dvec) + e);
+                aw.x *= m.x;
+                aw.y *= m.y;
             }
             const double2 wl = __ldcs(W2 + (s - 1) * vs2 + e);
             aw.x = fma(al[s - 1], wl.x, aw.x); aw.y = fma(al[s - 1], wl.y, aw.y);
@@ -475,6 +481,7 @@ void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double 
     k.theta = theta;
     k.sigma = sigma;
     k.dm = g.center;
+    k.dvec = sl.dvec ? sl.dvec + (int64_t)zb * g.plane : nullptr;
     k.xpp = xpp;
     k.xoff = xoff + (int64_t)(zb - 1) * g.nx * g.ny;
     k.s = s;

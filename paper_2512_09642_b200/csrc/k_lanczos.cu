@@ -32,9 +32,10 @@ __global__ void k_lz_diag(Geo g, const double *kx, const double *ky, const doubl
         if (dinv) {
             d = 1.0 / dinv[i];
         } else if (g.kind == 3) {   // A_ii = sum of the six faces (R12)
-            d = kx[(zl * g.ny + y) * (g.nx + 1) + x] + kx[(zl * g.ny + y) * (g.nx + 1) + x + 1] +
-                ky[(zl * (g.ny + 1) + y) * g.nx + x] + ky[(zl * (g.ny + 1) + y + 1) * g.nx + x] +
-                kz[(zl * g.ny + y) * g.nx + x] + kz[((zl + 1) * g.ny + y) * g.nx + x];
+            // same summation order as the basis kernels: kz-, ky-, kx-, kx+, ky+, kz+
+            d = kz[(zl * g.ny + y) * g.nx + x] + ky[(zl * (g.ny + 1) + y) * g.nx + x] +
+                kx[(zl * g.ny + y) * (g.nx + 1) + x] + kx[(zl * g.ny + y) * (g.nx + 1) + x + 1] +
+                ky[(zl * (g.ny + 1) + y + 1) * g.nx + x] + kz[((zl + 1) * g.ny + y) * g.nx + x];
         } else {
             d = g.center;
         }

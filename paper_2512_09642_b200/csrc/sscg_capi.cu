@@ -343,6 +343,15 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
             CU(cudaGetLastError());
             sl.dinv = dv;
         }
+        if (A->kind != SSCG_OP_CSR && (diag_M || A->kind == SSCG_OP_VARCOEF7)) {
+            // diag(M) per point for the recurrence form of the update (R21)
+            double *dd = nullptr;
+            TRY(dalloc(c, &dd, (size_t)g.vstride));
+            CU(cudaMemsetAsync(dd, 0, (size_t)g.vstride * sizeof(double), c->stream));
+            lz_diag(g, sl, dd, c->stream);
+            CU(cudaGetLastError());
+            sl.dvec = dd;
+        }
     }
     TRY(dalloc(c, &c->blk, (size_t)nent));
     TRY(dalloc(c, &c->xdev, 1));
@@ -584,9 +593,9 @@ static bool uses_rec_update(const sscg_ctx *c)
     const char *e = getenv("SSCG_K5_RECUR");
     if (e && e[0] == '0') return false;
     const Geo &g = c->g;
-    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2 || !(g.center > 0.0) || g.pitch != g.nx) return false;
+    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2 || g.kind == SSCG_OP_CSR || g.pitch != g.nx) return false;
     for (const auto &sl : c->slabs)
-        if (sl.dinv) return false;
+        if (!sl.dvec && !(g.center > 0.0 && !sl.dinv)) return false;   // need m or diag(M) per point
     return true;
 }
 
@@ -1209,7 +1218,7 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
     case SSCG_QUERY_UPDATE_VECTORS:
         // P (s) + x in, x + r out; the stored-W form also reads W (s), the
         // recurrence form only w_{s-1}
-        *out = uses_rec_update(c) ? (int64_t)s + 4 : 2 * (int64_t)s + 3;
+        *out = uses_rec_update(c) ? (int64_t)s + 4 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s + 3;
         return SSCG_OK;
     default:
         return fail(SSCG_ERR_INVALID, "unknown query %d", what);

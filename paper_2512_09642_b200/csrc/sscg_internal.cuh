@@ -41,6 +41,7 @@ struct Slab {
     unsigned *ticket;  // last-CTA counter for K2
     const double *kx, *ky, *kz;   // VARCOEF7 faces of this slab
     const double *dinv;           // Jacobi 1/diag(M) interior layout (or nullptr)
+    double *dvec;                 // diag(M) in the padded layout when it is not constant (K5 REC), else nullptr
     CUtensorMap tmP, tmW;         // K2: [s rows x interior] views of P and W
     CUtensorMap tmP4, tmM4;       // K1T: 4-D [x][y][plane][vector] views of P (halo box / tile box)
     bool has_k1t;

@@ -324,7 +324,7 @@ def test_graph_reused_across_x_buffers():
 
 
 @pytest.mark.parametrize("cfg", [("7pt", 40, 36, 33, 16, 25), ("27pt", 30, 28, 26, 16, 30), ("5pt", 64, 64, 1, 8, 20),
-                                 ("7pt", 34, 30, 28, 2, 5)], ids=_ids)
+                                 ("7pt", 34, 30, 28, 2, 5), ("varcoef7", 24, 22, 20, 8, 20)], ids=_ids)
 def test_recurrence_update_matches_stored_w(cfg, monkeypatch):
     """K5 forming W alpha from the Chebyshev recurrence (R21)
     against the stored-W form and the oracle: x after 10 outer iterations to
@@ -338,7 +338,8 @@ def test_recurrence_update_matches_stored_w(cfg, monkeypatch):
     for rec in ("1", "0"):
         monkeypatch.setenv("SSCG_K5_RECUR", rec)
         with P.gpu_solver() as S:
-            assert S.query(sscg.QUERY_UPDATE_VECTORS) == (s + 4 if rec == "1" else 2 * s + 3)
+            extra = 1 if kind == "varcoef7" else 0      # diag(M) varies: read per point
+            assert S.query(sscg.QUERY_UPDATE_VECTORS) == (s + 4 + extra if rec == "1" else 2 * s + 3)
             x10 = S.solve(P.b_gpu(), rtol=0.0, max_outer=10).cpu().numpy()
             xf = S.solve(P.b_gpu(), rtol=1e-8, max_outer=20000).cpu().numpy()
             res[rec] = (x10, xf, S.stats().outer_iterations)
