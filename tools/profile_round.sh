@@ -1,0 +1,20 @@
+#!/bin/bash
+# Evidence for profiles/ (run on a B200 through gpurun; see B200_PROFILING.md):
+#   bash tools/profile_round.sh <tag>
+# 1. the bench line, 2. the per-launch device times of the same command under
+# ncu (shares, not absolutes), 3. one `ncu --set full` capture per hot kernel,
+# 4. the HBM read/write mix ceilings.  Each ncu run follows a plain run of the
+# same command that exited 0.
+set -e
+TAG=${1:-rXX}
+mkdir -p gpurun_out
+python bench.py > gpurun_out/bench_$TAG.json
+C="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
+$C > gpurun_out/plain_$TAG.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $C > /dev/null 2>&1
+for k in k1f k2_gram k5_update; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 10 -c 1 -o gpurun_out/prof_${TAG}_$k $C > /dev/null 2>&1
+done
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/membw tools/membw.cu && /tmp/membw > gpurun_out/membw_$TAG.txt
+# then, here: python tools/launch_shares.py gpurun_out/launches_$TAG.csv > profiles/${TAG}_launches448_shares.txt
+#             python tools/ncu_raw_summary.py profiles/${TAG}_ncu_full_448.json gpurun_out/prof_${TAG}_*.ncu-rep > profiles/${TAG}_ncu_full_448.txt
