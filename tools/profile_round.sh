@@ -7,14 +7,17 @@
 # same command that exited 0.
 set -e
 TAG=${1:-rXX}
+ONLY=${2:-all}
 mkdir -p gpurun_out
-python bench.py > gpurun_out/bench_$TAG.json
 C="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
+[ "$ONLY" = all ] && python bench.py > gpurun_out/bench_$TAG.json
 $C > gpurun_out/plain_$TAG.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $C > /dev/null 2>&1
-for k in k1f k2_gram k5_update; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 10 -c 1 -o gpurun_out/prof_${TAG}_$k $C > /dev/null 2>&1
+[ "$ONLY" = all ] && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $C > /dev/null 2>&1
+# skip the warm-up launches: K1F runs 8x per outer, K2/K5 once (10 outer iterations in this command)
+for ks in "k1f 10" "k2_gram 3" "k5_update 3"; do
+  set -- $ks
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 -o gpurun_out/prof_${TAG}_$1 $C > /dev/null 2>&1
 done
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/membw tools/membw.cu && /tmp/membw > gpurun_out/membw_$TAG.txt
+[ "$ONLY" = all ] && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/membw tools/membw.cu && /tmp/membw > gpurun_out/membw_$TAG.txt
 # then, here: python tools/launch_shares.py gpurun_out/launches_$TAG.csv > profiles/${TAG}_launches448_shares.txt
 #             python tools/ncu_raw_summary.py profiles/${TAG}_ncu_full_448.json gpurun_out/prof_${TAG}_*.ncu-rep > profiles/${TAG}_ncu_full_448.txt
