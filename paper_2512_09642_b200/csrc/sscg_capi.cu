@@ -77,7 +77,9 @@ struct sscg_ctx {
     // the next basis vector's boundary planes on `cstream` while the interior
     // planes run on `stream`
     cudaStream_t cstream = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_xready = nullptr;
+    double *x_host_out = nullptr;   // sscg_solve_host: copy x out as soon as it is final
+    bool x_copied = false;
     bool overlap = true;
     int k1_sm_cap = 0;
     // variants on the same boundary
@@ -278,6 +280,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         CU(cudaStreamCreateWithPriority(&c->cstream, cudaStreamNonBlocking, hi));
         CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->ev_xready, cudaEventDisableTiming));
     }
     CU(cudaEventCreate(&c->ev0));
     CU(cudaEventCreate(&c->ev1));
@@ -415,6 +418,7 @@ extern "C" void sscg_destroy(sscg_ctx *c)
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_xready) cudaEventDestroy(c->ev_xready);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -864,7 +868,18 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
     int chunk = 2;
     while (issued < max_outer + 1) {
         const int n = std::min(chunk, max_outer + 1 - issued);
-        for (int i = 0; i < n; ++i) TRY(run_outer(c, x));
+        for (int i = 0; i < n; ++i) {
+            TRY(run_outer(c, x));
+            if (c->x_host_out && issued + i + 1 == max_outer) {
+                // x is final after the max_outer-th update: copy it out (sscg_solve_host)
+                // while the last outer iteration only builds the basis/Gram of the stopping test
+                CU(cudaEventRecord(c->ev_xready, c->stream));
+                CU(cudaStreamWaitEvent(c->cstream, c->ev_xready, 0));
+                CU(cudaMemcpyAsync(c->x_host_out, x, (size_t)c->n_local * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->cstream));
+                c->x_copied = true;
+            }
+        }
         issued += n;
         CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
@@ -874,6 +889,7 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
     CU(cudaEventRecord(c->ev1, c->stream));
     CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
+    if (c->x_copied) CU(cudaStreamSynchronize(c->cstream));
     const DevState &f = *c->st_host;
     const int outer = f.outer;
     c->relres_host.assign((size_t)std::min(outer + 1, c->hist_cap), 0.0);
@@ -917,11 +933,17 @@ extern "C" sscg_status sscg_solve_host(sscg_ctx *c, const double *b_host, double
     if (!c->xbuf) TRY(dalloc(c, &c->xbuf, (size_t)c->n_local));
     CU(cudaMemcpyAsync(c->bbuf, b_host, bytes, cudaMemcpyHostToDevice, c->stream));
     if (!(flags & SSCG_SOLVE_X0_ZERO)) CU(cudaMemcpyAsync(c->xbuf, x_host, bytes, cudaMemcpyHostToDevice, c->stream));
+    c->x_host_out = x_host;
+    c->x_copied = false;
     sscg_status st = sscg_solve(c, c->bbuf, c->xbuf, rtol, max_outer, flags);
+    c->x_host_out = nullptr;
     if (st != SSCG_OK && st != SSCG_ERR_BREAKDOWN && st != SSCG_ERR_NONFINITE) return st;
     std::string keep = g_err;
-    CU(cudaMemcpyAsync(x_host, c->xbuf, bytes, cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
+    if (!c->x_copied) {   // converged (or stopped) before max_outer updates: copy now
+        CU(cudaMemcpyAsync(x_host, c->xbuf, bytes, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    c->x_copied = false;
     g_err = keep;
     return st;
 }
