@@ -10,6 +10,9 @@
 // iterations before it reads the flag back.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
+#include <unistd.h>
+#include <chrono>
 
 #include <algorithm>
 #include <cmath>
@@ -498,6 +501,39 @@ static sscg_status prof_resolve(sscg_ctx *c)
     return SSCG_OK;
 }
 
+// Wait for `strm`.  With ranks, poll instead of blocking so that an NCCL
+// failure (ncclCommGetAsyncError) or a peer that never arrives (timeout
+// SSCG_NCCL_TIMEOUT_S, default 600 s) aborts the communicator and returns
+// SSCG_ERR_NCCL instead of hanging (SURVEY §5 failure detection).
+static sscg_status wait_stream(sscg_ctx *c, cudaStream_t strm)
+{
+    if (c->nranks == 1 || !c->comm) {
+        CU(cudaStreamSynchronize(strm));
+        return SSCG_OK;
+    }
+    static double limit = -1.0;
+    if (limit < 0.0) {
+        const char *e = getenv("SSCG_NCCL_TIMEOUT_S");
+        limit = e ? atof(e) : 600.0;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(strm);
+        if (q == cudaSuccess) return SSCG_OK;
+        if (q != cudaErrorNotReady) return fail(SSCG_ERR_CUDA, "stream: %s", cudaGetErrorString(q));
+        ncclResult_t ae = ncclSuccess;
+        ncclCommGetAsyncError(c->comm, &ae);
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (ae != ncclSuccess || (limit > 0.0 && dt > limit)) {
+            ncclCommAbort(c->comm);
+            c->comm = nullptr;
+            return fail(SSCG_ERR_NCCL, "NCCL %s after %.1f s (communicator aborted)",
+                        ae != ncclSuccess ? ncclGetErrorString(ae) : "timeout", dt);
+        }
+        usleep(20);
+    }
+}
+
 // halo of basis column j of every local slab; with overlap the exchange runs
 // on the comm stream after the work already enqueued on the solver stream
 // (fork) and `ev_join` marks its completion
@@ -645,6 +681,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const bool halo = (L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR;
     const bool ovl = halo && c->overlap;
     const bool fuse = uses_fused(c);
+    nvtxRangePushA("basis");
     for (int j = 0; j < s; ++j) {
         if (fuse && j + 1 < s) {   // steps j and j+1 in one pass (K1F)
             if (!halo) {
@@ -672,6 +709,8 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
             if (j < s - 1) TRY(halo_join(c));
         }
     }
+    nvtxRangePop();
+    nvtxRangePushA("gram+allreduce+fgs");
     for (auto &sl : c->slabs) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
         launch_k2(g, sl, s, c->st, L == 1 ? c->blk : sl.blk, c->stream);
@@ -706,6 +745,8 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     }
     TRY(prof_mark(c, SSCG_PROF_FGS, false));
     ++c->launches;
+    nvtxRangePop();
+    nvtxRangePushA("update");
     auto k5 = [&](int zb, int ze) -> sscg_status {
         for (auto &sl : c->slabs) {
             const int e = (ze == -1) ? sl.nzl + 1 : (ze == -2) ? sl.nzl : std::min(ze, sl.nzl + 1);
@@ -742,6 +783,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
         TRY(k5(2, -2));
         TRY(halo_join(c));
     }
+    nvtxRangePop();
     CU(cudaGetLastError());
     return SSCG_OK;
 }
@@ -861,6 +903,7 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
             ++c->launches;
         }
     }
+    nvtxRangePushA("sscg_solve");
     // halo planes of p_0 = r_0 (enqueue_outer's precondition)
     if ((L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR) TRY(halo_fork(c, 0, false));
     // outer iterations in chunks; the device decides when to stop
@@ -882,14 +925,15 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
         }
         issued += n;
         CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
-        CU(cudaStreamSynchronize(c->stream));
+        TRY(wait_stream(c, c->stream));
         if (c->st_host->done) break;
         chunk = std::min(chunk * 2, 16);
     }
     CU(cudaEventRecord(c->ev1, c->stream));
     CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
+    TRY(wait_stream(c, c->stream));
     if (c->x_copied) CU(cudaStreamSynchronize(c->cstream));
+    nvtxRangePop();
     const DevState &f = *c->st_host;
     const int outer = f.outer;
     c->relres_host.assign((size_t)std::min(outer + 1, c->hist_cap), 0.0);
@@ -1021,10 +1065,12 @@ extern "C" sscg_status sscg_iterate(sscg_ctx *c, double *x, int32_t nsteps)
     CU(cudaMemcpyAsync(c->st, c->st_host, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
     *c->xhost = x;
     CU(cudaMemcpyAsync(c->xdev, c->xhost, sizeof(double *), cudaMemcpyHostToDevice, c->stream));
+    nvtxRangePushA("sscg_iterate");
     for (int i = 0; i < nsteps; ++i) TRY(run_outer(c, x));
     CU(cudaEventRecord(c->ev1, c->stream));
     CU(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
+    TRY(wait_stream(c, c->stream));
+    nvtxRangePop();
     float ms = 0.f;
     CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     c->stats.ms_total = ms;
