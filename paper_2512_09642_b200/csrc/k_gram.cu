@@ -328,8 +328,11 @@ bool k2_prepare(const Geo &g, Slab &sl, int s)
         cudaFuncSetAttribute(k2_gram<8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
         cudaFuncSetAttribute(k2_gram<8, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess)
         return false;
-    return encode_rows_map(&sl.tmP, sl.P + g.plane, N, s, g.vstride, p.E, p.s_pad) &&
-           encode_rows_map(&sl.tmW, sl.W + g.plane, N, s, g.vstride, p.E, p.s_pad);
+    if (!encode_rows_map(&sl.tmP, sl.P + g.plane, N, s, g.vstride, p.E, p.s_pad) ||
+        !encode_rows_map(&sl.tmW, sl.W + g.plane, N, s, g.vstride, p.E, p.s_pad))
+        return false;
+    sl.has_k2d = k2d_enabled(s);
+    return !sl.has_k2d || k2d_prepare(g, sl, s);
 }
 
 template <int TB, int E>
@@ -342,6 +345,10 @@ static void launch_t(const CUtensorMap &a, const CUtensorMap &b, const K2Params 
 // partial buffer must hold k2_grid() * (s*s+s) doubles (gx * gy <= k2_grid())
 void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk, cudaStream_t stream)
 {
+    if (sl.has_k2d) {
+        launch_k2d(g, sl, s, st, out_blk, stream);
+        return;
+    }
     const K2Plan p = plan(s);
     K2Params k;
     k.N = (int64_t)sl.nzl * g.plane;

@@ -1,0 +1,263 @@
+// K2D -- the tall-skinny Gram pass
+//   Ghat_ij = p_i^T w_j  (i <= j, W = AP)      c_i = p_i^T p_0
+// on the FP64 tensor-core path (mma.sync m8n8k4 f64, "DMMA"): Ghat = P W^T is
+// a dense contraction over the grid points, s x N times N x s.  Used for
+// s > 16, where the FP64 FMA count per byte (s(s+3)/2 per point) makes the
+// register-tiled K2 issue-bound (five consumer warps per SM at 255 registers);
+// one DMMA does 256 FMAs, so a warp carries every 8 x 8 tile of the upper
+// block triangle in 2 registers per tile and eight warps split the points.
+//
+// Same pipeline as K2: warp 0 issues two cp.async.bulk.tensor.2d boxes per
+// stage (rows = basis vectors, EP points each, OOB rows/points zero-filled)
+// into an mbarrier ring; consumer warps take k-steps of 4 points.  The box
+// row pitch EP*8 bytes is 32 mod 128, so the 8 rows x 4 points of one
+// fragment load fall on distinct banks.  Per-warp tiles are reduced across
+// warps in a fixed order, per-CTA partials by the last CTA in index order
+// (deterministic, no FP atomics).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "sscg_internal.cuh"
+#include "tma.cuh"
+
+namespace sscg {
+namespace {
+
+constexpr int NCW = 8;                 // consumer warps
+constexpr int THREADS = 32 * (NCW + 1);
+constexpr int MAXS = 4;                // ring stages
+
+struct K2DParams {
+    int64_t N;         // interior doubles per vector
+    int s, s_pad;      // s_pad = 8 * NB
+    int nstage;
+    double *part;      // [gridDim.x][s*s + s]
+    double *out;
+    unsigned *ticket;
+};
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int NB, int EP>
+__global__ void __launch_bounds__(THREADS, 1)
+    k2d(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW, K2DParams k,
+        const DevState *st)
+{
+    if (st && st->done) return;
+    constexpr int SP = 8 * NB;                 // rows per box
+    constexpr int KS = EP / 4;                 // k-steps per stage
+    constexpr int NT = NB * (NB + 1) / 2;      // upper-triangle tiles
+    extern __shared__ __align__(1024) double smem[];
+    __shared__ uint64_t full[MAXS], empty[MAXS];
+    __shared__ bool is_last;
+    const int s = k.s, NS = k.nstage;
+    const int stage_elems = 2 * SP * EP;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nchunks = (k.N + EP - 1) / EP;
+    const int nit = (int)((nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x);
+
+    if (tid == 0) {
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NCW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmP);
+        tma_prefetch_desc(&tmW);
+    }
+    __syncthreads();
+
+    double acc[NT][2];
+    double cac[NB];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) cac[i] = 0.0;
+
+    if (warp == 0) {
+        const uint32_t bytes = (uint32_t)stage_elems * 8u;
+        for (int it = 0; it < nit; ++it) {
+            if (lane == 0) {
+                const int stg = it % NS;
+                if (it >= NS) mbar_wait(&empty[stg], (uint32_t)((it / NS - 1) & 1));
+                double *dst = smem + (size_t)stg * stage_elems;
+                const int x = (int)((blockIdx.x + (int64_t)it * gridDim.x) * EP);
+                mbar_expect_tx(&full[stg], bytes);
+                tma_load_2d(dst, &tmP, x, 0, &full[stg]);
+                tma_load_2d(dst + SP * EP, &tmW, x, 0, &full[stg]);
+            }
+            __syncwarp();
+        }
+    } else {
+        const int cw = warp - 1;
+        const int r = lane >> 2, kk = lane & 3;   // fragment row (m or n) and k index
+        for (int it = 0; it < nit; ++it) {
+            const int stg = it % NS;
+            mbar_wait(&full[stg], (uint32_t)((it / NS) & 1));
+            const double *sP = smem + (size_t)stg * stage_elems;
+            const double *sW = sP + SP * EP;
+            for (int ks = cw; ks < KS; ks += NCW) {
+                const int o = r * EP + ks * 4 + kk;
+                double a[NB], b[NB];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) a[i] = sP[o + i * 8 * EP];
+#pragma unroll
+                for (int j = 0; j < NB; ++j) b[j] = sW[o + j * 8 * EP];
+                const double p0 = sP[ks * 4 + kk];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) cac[i] = fma(a[i], p0, cac[i]);
+                int t = 0;
+#pragma unroll
+                for (int i = 0; i < NB; ++i)
+#pragma unroll
+                    for (int j = i; j < NB; ++j, ++t) dmma(acc[t][0], acc[t][1], a[i], b[j]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+        }
+        // c: lanes with the same r hold partial sums over different k -> sum the 4
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            cac[i] += __shfl_xor_sync(0xffffffffu, cac[i], 1);
+            cac[i] += __shfl_xor_sync(0xffffffffu, cac[i], 2);
+        }
+    }
+    __syncthreads();   // ring drained: reuse it for the cross-warp reduction
+    // red[cw][t][lane][2] tiles, then c: red[NCW*NT*64 + cw*SP + row]
+    double *red = smem;
+    if (warp > 0) {
+        const int cw = warp - 1;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            red[((cw * NT + t) * 32 + lane) * 2 + 0] = acc[t][0];
+            red[((cw * NT + t) * 32 + lane) * 2 + 1] = acc[t][1];
+        }
+        if ((lane & 3) == 0)
+#pragma unroll
+            for (int i = 0; i < NB; ++i) red[NCW * NT * 64 + cw * SP + i * 8 + (lane >> 2)] = cac[i];
+    }
+    __syncthreads();
+    const int nent = s * s + s;
+    double *mypart = k.part + (int64_t)blockIdx.x * nent;
+    // tile t = (I, J), fragment element (lane, h): row I*8 + lane/4, col J*8 + 2*(lane%4) + h
+    for (int q = tid; q < NT * 64; q += THREADS) {
+        const int t = q >> 6, e = q & 63, ln = e >> 1, h = e & 1;
+        double v = 0.0;
+        for (int w = 0; w < NCW; ++w) v += red[((w * NT + t) * 32 + ln) * 2 + h];
+        int I = 0, J = 0, tt = t;
+        for (int a = 0; a < NB; ++a) {
+            if (tt < NB - a) { I = a; J = a + tt; break; }
+            tt -= NB - a;
+        }
+        const int i = I * 8 + (ln >> 2), j = J * 8 + 2 * (ln & 3) + h;
+        if (i < s && j < s && i <= j) mypart[i * s + j] = v;
+    }
+    for (int i = tid; i < s; i += THREADS) {
+        double v = 0.0;
+        for (int w = 0; w < NCW; ++w) v += red[NCW * NT * 64 + w * SP + i];
+        mypart[s * s + i] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) is_last = atomicAdd(k.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const int nparts = gridDim.x;
+    for (int q = tid; q < nent; q += THREADS) {
+        int i, j;
+        if (q < s * s) {
+            i = q / s;
+            j = q - i * s;
+            if (i > j) continue;
+        } else {
+            i = q - s * s;
+            j = -1;
+        }
+        double v = 0.0;
+        for (int b = 0; b < nparts; ++b) v += __ldcg(k.part + (int64_t)b * nent + q);
+        if (j >= 0) {
+            k.out[i * s + j] = v;
+            k.out[j * s + i] = v;
+        } else {
+            k.out[s * s + i] = v;
+        }
+    }
+    if (tid == 0) *k.ticket = 0u;
+}
+
+int ep_for(int s_pad) { return s_pad <= 32 ? 132 : 68; }   // row pitch 32 mod 128 bytes
+
+template <int NB, int EP>
+size_t smem_for(int ns) { return (size_t)ns * 2 * 8 * NB * EP * sizeof(double); }
+
+int stages_for(int s_pad, int ep)
+{
+    const size_t stage = (size_t)2 * s_pad * ep * sizeof(double);
+    return (int)std::max<size_t>(2, std::min<size_t>(MAXS, (200 * 1024) / stage));
+}
+
+}  // namespace
+
+bool k2d_enabled(int s)
+{
+    const char *e = getenv("SSCG_K2_DMMA");   // "0" never, "1" always, unset: s > 16
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return s >= 1;
+    return s > 16;
+}
+
+bool encode_rows_map(CUtensorMap *m, const double *base, int64_t inner, int rows, int64_t stride, int box_inner,
+                     int box_rows);
+
+bool k2d_prepare(const Geo &g, Slab &sl, int s)
+{
+    const int s_pad = (s + 7) / 8 * 8, ep = ep_for(s_pad);
+    const int64_t N = (int64_t)sl.nzl * g.plane;
+    const int mx = 210 * 1024;
+#define K2D_ATTR(NB, EP) cudaFuncSetAttribute(k2d<NB, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
+    if (K2D_ATTR(1, 132) || K2D_ATTR(2, 132) || K2D_ATTR(3, 132) || K2D_ATTR(4, 132) || K2D_ATTR(5, 68) ||
+        K2D_ATTR(6, 68) || K2D_ATTR(7, 68) || K2D_ATTR(8, 68))
+        return false;
+#undef K2D_ATTR
+    return encode_rows_map(&sl.tmPd, sl.P + g.plane, N, s, g.vstride, ep, s_pad) &&
+           encode_rows_map(&sl.tmWd, sl.W + g.plane, N, s, g.vstride, ep, s_pad);
+}
+
+void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk, cudaStream_t stream)
+{
+    const int s_pad = (s + 7) / 8 * 8, nb = s_pad / 8, ep = ep_for(s_pad);
+    K2DParams k;
+    k.N = (int64_t)sl.nzl * g.plane;
+    k.s = s;
+    k.s_pad = s_pad;
+    k.nstage = stages_for(s_pad, ep);
+    k.part = sl.part;
+    k.out = out_blk;
+    k.ticket = sl.ticket;
+    const int64_t nchunks = (k.N + ep - 1) / ep;
+    const int gx = (int)std::min<int64_t>(k2_grid(), nchunks);
+    const int nt = nb * (nb + 1) / 2;
+    const size_t ring = (size_t)k.nstage * 2 * s_pad * ep * sizeof(double);
+    const size_t red = (size_t)(NCW * nt * 64 + NCW * s_pad) * sizeof(double);   // cross-warp reduction
+    const size_t sm = std::max(ring, red);
+    switch (nb) {
+    case 1: k2d<1, 132><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 2: k2d<2, 132><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 3: k2d<3, 132><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 4: k2d<4, 132><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 5: k2d<5, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 6: k2d<6, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 7: k2d<7, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    default: k2d<8, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    }
+}
+
+}  // namespace sscg

@@ -43,6 +43,8 @@ struct Slab {
     const double *dinv;           // Jacobi 1/diag(M) interior layout (or nullptr)
     double *dvec;                 // diag(M) in the padded layout when it is not constant (K5 REC), else nullptr
     CUtensorMap tmP, tmW;         // K2: [s rows x interior] views of P and W
+    CUtensorMap tmPd, tmWd;       // K2D (DMMA Gram, s > 16): same views, box pitch 132/68
+    bool has_k2d;
     CUtensorMap tmP4, tmM4;       // K1T: 4-D [x][y][plane][vector] views of P (halo box / tile box)
     bool has_k1t;
     CUtensorMap tmF_P, tmF_M;     // K1F: 2-cell / 1-cell halo boxes
@@ -119,6 +121,10 @@ void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *
 int k2_grid();
 bool k2_prepare(const Geo &g, Slab &sl, int s);   // encode the TMA tensor maps
 int k2_num_entries(int s);
+// K2D: the Gram pass on FP64 tensor cores (k_gram_dmma.cu), s > 16 by default
+bool k2d_enabled(int s);
+bool k2d_prepare(const Geo &g, Slab &sl, int s);
+void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk, cudaStream_t stream);
 
 // fixed-order sum of per-slab blocks into `blk`
 void launch_slab_sum(const double *const *blks_dev, int nslab, int len, double *blk,

@@ -357,3 +357,25 @@ def test_recurrence_update_matches_stored_w(cfg, monkeypatch):
         tr = np.linalg.norm(P.b - orc.apply(P.A, xf)) / np.linalg.norm(P.b)
         assert tr <= 1e-8 * 1.05, (rec, tr)
     assert abs(res["1"][2] - res["0"][2]) <= 1
+
+
+@pytest.mark.parametrize("cfg", [("7pt", 30, 28, 26, 24, 20), ("varcoef7", 20, 18, 17, 32, 20), ("7pt", 14, 13, 12, 64, 3),
+                                 ("7pt", 33, 17, 19, 16, 10), ("5pt", 64, 64, 1, 5, 10)], ids=_ids)
+def test_gram_dmma_matches_register_tiles(cfg, monkeypatch):
+    """K2D (Gram pass on FP64 tensor cores, default for s > 16) against the
+    register-tiled K2 and the oracle: Gram block and c at outer 0 to the
+    north_star 1e-11, the two GPU kernels to rounding."""
+    kind, nx, ny, nz, s, nu = cfg
+    bounds = (0.02, 2.2) if s == 64 else None
+    P = Problem(kind, nx, ny, nz, s, nu, bounds=bounds, lanczos=(kind == "varcoef7"))
+    x_or, tr = P.oracle(max_outer=1, dump_iter=0)
+    out = {}
+    for dm in ("1", "0"):
+        monkeypatch.setenv("SSCG_K2_DMMA", dm)
+        with P.gpu_solver() as S:
+            S.solve(P.b_gpu(), rtol=0.0, max_outer=1)
+            out[dm] = S.gram(0)
+            assert_gram(S, tr, 0)
+    (G1, c1), (G0, c0) = out["1"], out["0"]
+    assert np.max(np.abs(G1 - G0)) <= 1e-13 * np.max(np.abs(G0))
+    assert np.max(np.abs(c1 - c0)) <= 1e-13 * np.max(np.abs(c0))
