@@ -29,14 +29,23 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
 {
     if (st->done) return;
     __shared__ double Gc[TWO ? SMAX * SMAX : 1];   // column-major: Gc[j*s + i] = G_ij
+    __shared__ double Bs[TWO ? 1 : 32 * 32 + 32];  // s <= 32: the block staged once (coalesced)
     __shared__ double dsh[SMAX];
     const int s = a.s, lane = threadIdx.x;
     const int k = st->k;
-    const double *Gh = a.blk, *c = a.blk + s * s;
     const int nent = s * s + s;
     const bool rec = k < st->hist_cap;
-    if (rec)
+    if (!TWO) {
+        for (int q = lane; q < nent; q += 32) {
+            const double v = a.blk[q];
+            Bs[q] = v;
+            if (rec) a.h_gram[(int64_t)k * nent + q] = v;
+        }
+        __syncwarp();
+    } else if (rec) {
         for (int q = lane; q < nent; q += 32) a.h_gram[(int64_t)k * nent + q] = a.blk[q];
+    }
+    const double *Gh = TWO ? a.blk : Bs, *c = Gh + s * s;
 
     const double rn = sqrt(c[0]);
     const double r0 = (k == 0) ? rn : st->r0norm;
@@ -74,11 +83,15 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
     const double ct1 = v1 ? d1 * c[i1] : 0.0;
     double rho0 = ct0, rho1 = ct1, al0 = 0.0, al1 = 0.0;
 
+    double lnorm_part = 0.0;
     if (!TWO) {
         double g[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j)
             g[j] = (v0 && j < s) ? ((j == i0) ? 1.0 : (d0 * Gh[i0 * s + j]) * dsh[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < i0) lnorm_part = fma(g[j], g[j], lnorm_part);
         for (int sw = 0; sw < a.nu; ++sw) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -124,9 +137,13 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
     }
     // ||L||_F^2 = sum_{i > j} G_ij^2 (the quantity FGS convergence depends on)
     double ll = 0.0;
-    for (int j = 0; j < s; ++j) {
-        if (v0 && j < i0) { const double gij = (d0 * Gh[i0 * s + j]) * dsh[j]; ll = fma(gij, gij, ll); }
-        if (v1 && j < i1) { const double gij = (d1 * Gh[i1 * s + j]) * dsh[j]; ll = fma(gij, gij, ll); }
+    if (!TWO) {
+        ll = lnorm_part;
+    } else {
+        for (int j = 0; j < s; ++j) {
+            if (v0 && j < i0) { const double gij = Gc[j * s + i0]; ll = fma(gij, gij, ll); }
+            if (v1 && j < i1) { const double gij = Gc[j * s + i1]; ll = fma(gij, gij, ll); }
+        }
     }
     ll = warp_sum(ll);
     // delta = ||c~ - G a~|| / ||c~||  (PAPER.md:259-262 inexactness monitor)

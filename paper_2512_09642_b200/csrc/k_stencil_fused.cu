@@ -396,9 +396,9 @@ void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevSta
         // front planes), tiles x chunks filling whole waves of the grid
         double best = -1.0;
         for (int nch = 1; nch <= 64 && (n1 + nch - 1) / nch >= 4; ++nch) {
-            const int64_t items = tiles * nch;
-            const int64_t waves = (items + resident - 1) / resident;
             const int z = (n1 + nch - 1) / nch;
+            const int64_t items = tiles * ((n1 + z - 1) / z);   // chunks actually formed with this z
+            const int64_t waves = (items + resident - 1) / resident;
             const double score = (double)items / (double)(waves * resident) / (1.0 + 1.0 / z);
             if (score > best + 1e-9) {
                 best = score;

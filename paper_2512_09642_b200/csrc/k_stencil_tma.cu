@@ -561,9 +561,9 @@ void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t 
         double best = -1.0;
         zc = n1;
         for (int nch = 1; nch <= 64 && (n1 + nch - 1) / nch >= 4; ++nch) {
-            const int64_t items = tiles * nch;
-            const int64_t waves = (items + resident - 1) / resident;
             const int z = (n1 + nch - 1) / nch;
+            const int64_t items = tiles * ((n1 + z - 1) / z);   // chunks actually formed with this z
+            const int64_t waves = (items + resident - 1) / resident;
             const double score = (double)items / (double)(waves * resident) / (1.0 + 0.5 / z);
             if (score > best + 1e-9) {
                 best = score;
