@@ -46,6 +46,9 @@ def test_sass_targets_sm100a(lib):
     assert "sm_100a" in out
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {sscg.LIB_PATH}").read()
     assert "UTMALDG" in sass          # K2 streams P and W with TMA tensor loads
+    assert "UTMALDG.4D" in sass       # K1T / K1F stage basis planes as 4-D boxes
+    assert "SYNCS.PHASECHK" in sass   # mbarrier rings
+    assert "DMMA" in sass             # K2D: Gram on FP64 tensor cores (s > 16)
     assert "DFMA" in sass
 
 
