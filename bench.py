@@ -87,14 +87,14 @@ def workload(a, nranks):
 
 # --------------------------------------------------------------------------
 # CPU oracle (the reported baseline / --impl reference arm)
-def oracle_sample(a, steps, warmup):
+def oracle_sample(a, steps, warmup, planes=None):
     """Time `steps` outer iterations of the CPU oracle on a bounded sample:
     the first `cpu_planes` z-planes of the same n x n grid (Dirichlet box of
     n x n x cpu_planes, same s, nu, seed; bounds of that box).  Returns
     (GDOF/s, seconds per step, description)."""
     import inputs
     import oracle as orc
-    n, zs = a.n, min(a.cpu_planes, a.n)
+    n, zs = a.n, min(planes or a.cpu_planes, a.n)
     b = inputs.rhs_uniform(n, n, zs, seed=42)
     if a.kind == "varcoef7":
         A = orc.stencil(orc.KIND_VARCOEF7, n, n, zs, *inputs.lognormal_faces(n, n, zs, seed=42))
@@ -225,6 +225,19 @@ def ncu_traffic(n, kernel_prefix):
     return None
 
 
+def mix_ceiling(reads, writes):
+    """Measured HBM ceiling (GB/s) of a plain streaming kernel with this
+    read:write vector mix (tools/membw.cu, committed under profiles/), or None."""
+    import glob
+    import re
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_membw_mix_ceilings.txt")), reverse=True):
+        for line in open(f):
+            m = re.match(r"R=\s*(\d+) W=(\d+)\s+[\d.]+ ms\s+([\d.]+) GB/s", line.strip())
+            if m and int(m.group(1)) == reads and int(m.group(2)) == writes:
+                return float(m.group(3)), os.path.basename(f)
+    return None, None
+
+
 def run_ours(a):
     import numpy as np
     import torch
@@ -325,6 +338,7 @@ def run_ours(a):
     path_bytes = sum(bytes_per_outer.values())
     cfg = workload(a, world)
     k1_name = "k1f" if fused else K1_NAME
+    mc = mix_ceiling(2, 4) if fused else mix_ceiling(2, 2)
     roof = {"bound": "hbm", "kernel": "K1 %s<%s> (%sSpMV + Jacobi + Chebyshev recurrence)"
                                       % (k1_name, a.kind, "two basis steps per launch: " if fused else ""),
             "achieved": k1["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": k1["frac"],
@@ -334,6 +348,9 @@ def run_ours(a):
             "bytes_rule": "%d FP64 vectors per outer (%s) + s face sets for varcoef7, / basis launches (SURVEY 8(d)); "
                           "path: basis + 2s (Gram) + %d (update) vectors"
                           % (basis_vecs, "K1F pairs: 6 per pair" if fused else "(4s-3)", upd_vecs),
+            "mix": "2 reads : 4 writes per pair" if fused else "2 reads : 2 writes",
+            "mix_ceiling_gbs": mc[0], "mix_ceiling_source": mc[1],
+            "frac_of_mix_ceiling": (k1["achieved_gbs"] / mc[0]) if (mc[0] and k1["achieved_gbs"]) else None,
             "path_bytes_per_step": path_bytes,
             "path_achieved_gbs": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9,
             "path_frac": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9 / peak}
@@ -360,7 +377,8 @@ def run_ours(a):
         return
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
-        v, per, desc = oracle_sample(a, 1, 1)
+        # ~10 s of CPU work: 64 planes of the same n x n grid, 24 timed outer iterations
+        v, per, desc = oracle_sample(a, 24, 1, planes=64)
         cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
