@@ -19,6 +19,7 @@
 
 #include "sscg_internal.cuh"
 #include "tma.cuh"
+#include "gram_reduce.cuh"
 
 namespace sscg {
 namespace {
@@ -203,26 +204,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    const int nparts = gridDim.x * gridDim.y;
-    for (int q = tid; q < nent; q += blockDim.x) {
-        int i, j;
-        if (q < s * s) {
-            i = q / s;
-            j = q - i * s;
-            if (i > j) continue;
-        } else {
-            i = q - s * s;
-            j = -1;
-        }
-        double v = 0.0;
-        for (int b = 0; b < nparts; ++b) v += __ldcg(k.part + (int64_t)b * nent + q);
-        if (j >= 0) {
-            k.out[i * s + j] = v;
-            k.out[j * s + i] = v;
-        } else {
-            k.out[s * s + i] = v;
-        }
-    }
+    last_cta_sum(k.part, gridDim.x * gridDim.y, s, k.out);
     if (tid == 0) *k.ticket = 0u;
 }
 

@@ -21,6 +21,7 @@
 
 #include "sscg_internal.cuh"
 #include "tma.cuh"
+#include "gram_reduce.cuh"
 
 namespace sscg {
 namespace {
@@ -170,26 +171,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    const int nparts = gridDim.x;
-    for (int q = tid; q < nent; q += THREADS) {
-        int i, j;
-        if (q < s * s) {
-            i = q / s;
-            j = q - i * s;
-            if (i > j) continue;
-        } else {
-            i = q - s * s;
-            j = -1;
-        }
-        double v = 0.0;
-        for (int b = 0; b < nparts; ++b) v += __ldcg(k.part + (int64_t)b * nent + q);
-        if (j >= 0) {
-            k.out[i * s + j] = v;
-            k.out[j * s + i] = v;
-        } else {
-            k.out[s * s + i] = v;
-        }
-    }
+    last_cta_sum(k.part, gridDim.x, s, k.out);
     if (tid == 0) *k.ticket = 0u;
 }
 
