@@ -1,0 +1,48 @@
+"""Randomised shapes (seeded): every operator kind, odd and tiny grids, basis
+sizes 1..40, several slabs, the schedule switches (fused pairs, TMA faces,
+recurrence update, DMMA Gram) forced both ways -- each run against the CPU
+oracle at outer 0 (north_star tolerances) and after a few outer iterations."""
+import numpy as np
+import pytest
+
+from gpu_cases import TOL_X10, Problem, assert_alpha, assert_basis, assert_gram
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ["5pt", "7pt", "27pt", "varcoef7"]
+
+
+def _cases(n=64, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        kind = KINDS[i % 4]
+        nx, ny = int(rng.integers(3, 70)), int(rng.integers(3, 40))
+        nz = 1 if kind == "5pt" else int(rng.integers(4, 30))
+        s = int(rng.choice([1, 2, 3, 5, 8, 12, 16, 17, 24, 32, 40]))
+        nu = int(rng.integers(1, 30))
+        slabs = 1 if kind == "5pt" else int(rng.choice([1, 1, 2, 3]))
+        slabs = min(slabs, nz)
+        env = {"SSCG_K1_FUSE": str(rng.integers(0, 2)), "SSCG_K5_RECUR": str(rng.integers(0, 2)),
+               "SSCG_K2_DMMA": str(rng.integers(0, 2)), "SSCG_FACES_TMA": str(rng.integers(0, 2))}
+        out.append((kind, nx, ny, nz, s, nu, slabs, env))
+    return out
+
+
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: "-".join(map(str, c[:7])) + "-" + "".join(c[7].values()))
+def test_random_shape(case, monkeypatch):
+    kind, nx, ny, nz, s, nu, slabs, env = case
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    # bounds: a safe enclosing interval of the Jacobi-scaled spectrum for every kind
+    P = Problem(kind, nx, ny, nz, s, nu, bounds=(0.02, 2.2))
+    x_or, tr = P.oracle(max_outer=3, dump_iter=0)
+    if tr.breakdown:
+        pytest.skip("oracle Gram breakdown at this basis size (numerically rank-deficient basis)")
+    with P.gpu_solver(slabs=slabs) as S:
+        S.solve(P.b_gpu(), rtol=0.0, max_outer=0)
+        assert_basis(S, tr, s)
+        assert_gram(S, tr, 0)
+        x = S.solve(P.b_gpu(), rtol=0.0, max_outer=3).cpu().numpy()
+        assert_alpha(S, tr, 0)
+    assert np.linalg.norm(x - x_or) <= TOL_X10 * np.linalg.norm(x_or)
