@@ -196,6 +196,8 @@ typedef struct {
     double ms_total;           /* device time of the last solve (CUDA events)        */
     int64_t kernel_launches;   /* library kernels launched by the last solve        */
     int64_t allreduces;        /* NCCL allreduces issued by the last solve          */
+    double budget;             /* with SSCG_OPT_DIAGNOSTICS: sum_k delta_k ||A|| ||P_k||_F
+                                  (PAPER.md:259-266 Thm Inexact Convergence), else 0 */
 } sscg_stats_t;
 
 SSCG_API sscg_status sscg_stats(const sscg_ctx *ctx, sscg_stats_t *out);
@@ -214,7 +216,9 @@ enum {
     SSCG_INSPECT_P = 0, SSCG_INSPECT_W = 1, SSCG_INSPECT_GRAM = 2, SSCG_INSPECT_D = 3,
     SSCG_INSPECT_ALPHA_T = 4, SSCG_INSPECT_ALPHA = 5, SSCG_INSPECT_DELTA = 6,
     SSCG_INSPECT_LNORM = 7,    /* outer `index`: ||L||_F of G = I + L + L^T, 1 double */
-    SSCG_INSPECT_KAPPA = 8     /* outer `index`: kappa(G) (with SSCG_OPT_DIAGNOSTICS, else 0), 1 double */
+    SSCG_INSPECT_KAPPA = 8,    /* outer `index`: kappa(G) (with SSCG_OPT_DIAGNOSTICS, else 0), 1 double */
+    SSCG_INSPECT_PNORM = 9,    /* outer `index`: ||P_k||_F (diagnostics), 1 double */
+    SSCG_INSPECT_BUDGET = 10   /* outer `index`: delta_k ||A|| ||P_k||_F, ||A|| the Gershgorin bound (diagnostics) */
 };
 SSCG_API sscg_status sscg_inspect(const sscg_ctx *ctx, int32_t what, int32_t index, void *host_out,
                          int64_t capacity);
@@ -261,8 +265,11 @@ SSCG_API sscg_status sscg_estimate_bounds(sscg_ctx *ctx, const double *v0, int32
  *                         kappa(M^{-1}A)^{s-1}, so only small s is usable).
  *   SSCG_OPT_DIAGNOSTICS  0 (default) / 1: after every update also compute
  *                         kappa(G) of the scaled Gram matrix (one-warp Jacobi
- *                         eigensolver, off the hot path), read back with
- *                         SSCG_INSPECT_KAPPA.
+ *                         eigensolver), ||P_k||_F (one extra pass over P) and
+ *                         the budget term delta_k ||A|| ||P_k||_F of
+ *                         PAPER.md:259-266 (||A||: Gershgorin bound, computed
+ *                         once), read back with SSCG_INSPECT_KAPPA / _PNORM /
+ *                         _BUDGET and stats.budget.  Off the hot path.
  * Errors: SSCG_ERR_INVALID for an unknown key or value. */
 enum { SSCG_OPT_GRAM_SOLVER = 0, SSCG_OPT_BASIS = 1, SSCG_OPT_DIAGNOSTICS = 2 };
 enum { SSCG_GRAM_FGS = 0, SSCG_GRAM_CHOLESKY = 1 };

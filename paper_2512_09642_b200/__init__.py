@@ -26,7 +26,7 @@ LIB_PATH = os.path.join(_HERE, "libsscg.so")
 OK, ERR_INVALID, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_BREAKDOWN, ERR_NONFINITE, ERR_UNSUPPORTED = range(8)
 OP_STENCIL5_2D, OP_STENCIL7, OP_STENCIL27, OP_VARCOEF7, OP_CSR = range(5)
 (INSPECT_P, INSPECT_W, INSPECT_GRAM, INSPECT_D, INSPECT_ALPHA_T, INSPECT_ALPHA, INSPECT_DELTA, INSPECT_LNORM,
- INSPECT_KAPPA) = range(9)
+ INSPECT_KAPPA, INSPECT_PNORM, INSPECT_BUDGET) = range(11)
 SOLVE_X0_ZERO = 1
 OPT_GRAM_SOLVER, OPT_BASIS, OPT_DIAGNOSTICS = 0, 1, 2
 GRAM_FGS, GRAM_CHOLESKY = 0, 1
@@ -61,7 +61,7 @@ class _Stats(C.Structure):
                 ("nonfinite", C.c_int32), ("r0_norm", C.c_double), ("relres_final", C.c_double),
                 ("history_len", C.c_int32), ("relres_history", C.POINTER(C.c_double)),
                 ("delta_history", C.POINTER(C.c_double)), ("ms_total", C.c_double),
-                ("kernel_launches", C.c_int64), ("allreduces", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("allreduces", C.c_int64), ("budget", C.c_double)]
 
 
 class _Profile(C.Structure):
@@ -189,6 +189,7 @@ class Stats:
     ms_total: float
     kernel_launches: int
     allreduces: int
+    budget: float
 
 
 class Solver:
@@ -308,12 +309,12 @@ class Solver:
         nd = max(st.history_len - 1, 0)
         dh = np.ctypeslib.as_array(st.delta_history, (nd,)).copy() if nd and bool(st.delta_history) else np.zeros(0)
         return Stats(st.outer_iterations, bool(st.converged), bool(st.breakdown), bool(st.nonfinite), st.r0_norm,
-                     st.relres_final, rh, dh, st.ms_total, st.kernel_launches, st.allreduces)
+                     st.relres_final, rh, dh, st.ms_total, st.kernel_launches, st.allreduces, st.budget)
 
     def inspect(self, what: int, index: int) -> np.ndarray:
         n = {INSPECT_P: self.n_local, INSPECT_W: self.n_local, INSPECT_GRAM: self.s * self.s + self.s,
              INSPECT_D: self.s, INSPECT_ALPHA_T: self.s, INSPECT_ALPHA: self.s, INSPECT_DELTA: 1,
-             INSPECT_LNORM: 1, INSPECT_KAPPA: 1}[what]
+             INSPECT_LNORM: 1, INSPECT_KAPPA: 1, INSPECT_PNORM: 1, INSPECT_BUDGET: 1}[what]
         out = np.empty(n, dtype=np.float64)
         _check(load().sscg_inspect(self._h, what, index, out.ctypes.data, out.nbytes))
         return out

@@ -479,6 +479,105 @@ void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
     else k4_fgs<true><<<1, 32, 0, s>>>(a, st);
 }
 
+// Diagnostics: ||P_k||_F^2 of the basis of this outer iteration (before K5
+// overwrites p_0) as per-block partials, their fixed-order sum, and the
+// inexactness budget term delta_k ||A|| ||P_k||_F of PAPER.md:259-266
+// (Thm "Inexact Convergence"; ||P_k|| taken as the Frobenius norm, SPEC.md:353,
+// ||A|| as the Gershgorin bound max_i sum_j |A_ij|).
+__global__ void __launch_bounds__(256) k_pnorm(const double *P, int64_t vstride, int64_t N, int s, double *part,
+                                               const DevState *st)
+{
+    if (st->done) return;
+    __shared__ double red[8];
+    double acc = 0.0;
+    for (int j = 0; j < s; ++j)
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+            const double v = P[j * vstride + e];
+            acc = fma(v, v, acc);
+        }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w];
+        part[blockIdx.x] = v;
+    }
+}
+
+__global__ void k_psum(const double *part, int n, double *sum, const DevState *st)
+{
+    if (st->done) return;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < n; b += 32) v += part[b];
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *sum = v;
+}
+
+__global__ void k_budget(const double *sum, double anorm, const DevState *st, const double *h_delta, double *h_pnorm,
+                         double *h_budget)
+{
+    if (st->done) return;
+    const int k = st->k - 1;
+    if (k < 0 || k >= st->hist_cap) return;
+    const double pf = sqrt(*sum);
+    h_pnorm[k] = pf;
+    h_budget[k] = h_delta[k] * anorm * pf;
+}
+
+// Gershgorin bound of ||A||_2: max over rows of sum_j |A_ij| (per-block maxima)
+__global__ void __launch_bounds__(256) k_anorm(Geo g, const double *kx, const double *ky, const double *kz, int nzl,
+                                               double *bmax)
+{
+    __shared__ double red[8];
+    double mx = 0.0;
+    if (g.kind == 4) {
+        for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < g.n; r += (int64_t)gridDim.x * blockDim.x) {
+            double a = 0.0;
+            for (int64_t q = g.rowptr[r]; q < g.rowptr[r + 1]; ++q) a += fabs(g.val[q]);
+            mx = fmax(mx, a);
+        }
+    } else if (g.kind == 3) {
+        const int64_t nxy = (int64_t)g.nx * g.ny, tot = nxy * nzl;
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t zl = e / nxy, rem = e - zl * nxy, y = rem / g.nx, x = rem - y * g.nx;
+            const double d = kx[(zl * g.ny + y) * (g.nx + 1) + x] + kx[(zl * g.ny + y) * (g.nx + 1) + x + 1] +
+                             ky[(zl * (g.ny + 1) + y) * g.nx + x] + ky[(zl * (g.ny + 1) + y + 1) * g.nx + x] +
+                             kz[(zl * g.ny + y) * g.nx + x] + kz[((zl + 1) * g.ny + y) * g.nx + x];
+            mx = fmax(mx, 2.0 * d);   // A_ii + sum of the (positive) off-diagonal faces
+        }
+    } else {
+        mx = 2.0 * g.center;          // graph-Laplacian stencils: centre + |off-diagonals|
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+        bmax[blockIdx.x] = v;
+    }
+}
+
+void launch_pnorm(const Geo &g, const Slab &sl, int s, double *part, int nblk, const DevState *st, cudaStream_t stream)
+{
+    k_pnorm<<<nblk, 256, 0, stream>>>(sl.P + g.plane, g.vstride, (int64_t)sl.nzl * g.plane, s, part, st);
+}
+
+void launch_budget(const double *part, int nparts, double *sum, double anorm, bool allreduce_needed,
+                   const DevState *st, const double *h_delta, double *h_pnorm, double *h_budget, cudaStream_t stream,
+                   int phase)
+{
+    if (phase == 0) k_psum<<<1, 32, 0, stream>>>(part, nparts, sum, st);
+    else k_budget<<<1, 1, 0, stream>>>(sum, anorm, st, h_delta, h_pnorm, h_budget);
+    (void)allreduce_needed;
+}
+
+void launch_anorm(const Geo &g, const Slab &sl, double *bmax, int nblk, cudaStream_t stream)
+{
+    k_anorm<<<nblk, 256, 0, stream>>>(g, sl.kx, sl.ky, sl.kz, sl.nzl, bmax);
+}
+
 void launch_kappa(const double *blk, int s, const DevState *st, double *h_kappa, cudaStream_t stream)
 {
     k_kappa<<<1, 32, 0, stream>>>(blk, s, st, h_kappa);

@@ -90,7 +90,9 @@ struct sscg_ctx {
     int basis = SSCG_BASIS_CHEBYSHEV;
     bool bounds_set = false;
     bool diagnostics = false;
-    double *h_kappa = nullptr;
+    double *h_kappa = nullptr, *h_pnorm = nullptr, *h_budget = nullptr;
+    double *diag_part = nullptr, *diag_sum = nullptr;   // ||P||_F partials [slab][DIAG_BLK], sum
+    double anorm = 0.0;                                  // Gershgorin bound of ||A||_2 (global)
     // Lanczos workspace (sscg_estimate_bounds): 3 vectors + D per slab, lazily
     std::vector<double *> lz_vec;     // [slab * 5 + {y0, y1, y2, w, D}]
     double *lz_scal = nullptr;        // device scalars, see sscg_estimate_bounds
@@ -121,6 +123,7 @@ struct sscg_ctx {
 };
 
 static const char *kVersion = "sscg-b200 0.1 (sm_100a)";
+static const int DIAG_BLK = 592;   // blocks of the ||P||_F diagnostic per slab
 
 extern "C" const char *sscg_version(void) { return kVersion; }
 extern "C" const char *sscg_last_error(void) { return g_err.c_str(); }
@@ -742,6 +745,16 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     if (c->diagnostics) {
         launch_kappa(c->blk, s, c->st, c->h_kappa, c->stream);
         ++c->launches;
+        for (int l = 0; l < L; ++l) {   // ||P_k||_F before K5 overwrites p_0
+            launch_pnorm(g, c->slabs[l], s, c->diag_part + (size_t)l * DIAG_BLK, DIAG_BLK, c->st, c->stream);
+            ++c->launches;
+        }
+        launch_budget(c->diag_part, L * DIAG_BLK, c->diag_sum, c->anorm, false, c->st, c->h_delta, c->h_pnorm,
+                      c->h_budget, c->stream, 0);
+        if (c->nranks > 1) NC(ncclAllReduce(c->diag_sum, c->diag_sum, 1, ncclDouble, ncclSum, c->comm, c->stream));
+        launch_budget(c->diag_part, L * DIAG_BLK, c->diag_sum, c->anorm, false, c->st, c->h_delta, c->h_pnorm,
+                      c->h_budget, c->stream, 1);
+        c->launches += 2;
     }
     TRY(prof_mark(c, SSCG_PROF_FGS, false));
     ++c->launches;
@@ -842,7 +855,11 @@ static sscg_status ensure_history(sscg_ctx *c, int cap)
     TRY(dalloc(c, &c->h_delta, (size_t)cap));
     TRY(dalloc(c, &c->h_lnorm, (size_t)cap));
     TRY(dalloc(c, &c->h_kappa, (size_t)cap));
+    TRY(dalloc(c, &c->h_pnorm, (size_t)cap));
+    TRY(dalloc(c, &c->h_budget, (size_t)cap));
     CU(cudaMemset(c->h_kappa, 0, (size_t)cap * sizeof(double)));
+    CU(cudaMemset(c->h_pnorm, 0, (size_t)cap * sizeof(double)));
+    CU(cudaMemset(c->h_budget, 0, (size_t)cap * sizeof(double)));
     TRY(dalloc(c, &c->h_relres, (size_t)cap));
     c->hist_cap = cap;
     return SSCG_OK;
@@ -960,6 +977,12 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
     S.ms_total = ms;
     S.kernel_launches = c->launches;
     S.allreduces = c->allreduces;
+    S.budget = 0.0;
+    if (c->diagnostics && outer > 0) {   // sum_k delta_k ||A|| ||P_k||_F over the applied updates
+        std::vector<double> bt((size_t)std::min(outer, c->hist_cap));
+        CU(cudaMemcpy(bt.data(), c->h_budget, bt.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        for (double v : bt) S.budget += v;
+    }
     c->solved = true;
     TRY(prof_resolve(c));
     if (f.breakdown) return fail(SSCG_ERR_BREAKDOWN, "Gram breakdown at outer %d (Ghat_ii <= 0 or non-finite)", outer);
@@ -1041,6 +1064,8 @@ extern "C" sscg_status sscg_inspect(const sscg_ctx *cc, int32_t what, int32_t in
     case SSCG_INSPECT_DELTA: src = c->h_delta + index; cnt = 1; break;
     case SSCG_INSPECT_LNORM: src = c->h_lnorm + index; cnt = 1; break;
     case SSCG_INSPECT_KAPPA: src = c->h_kappa + index; cnt = 1; break;
+    case SSCG_INSPECT_PNORM: src = c->h_pnorm + index; cnt = 1; break;
+    case SSCG_INSPECT_BUDGET: src = c->h_budget + index; cnt = 1; break;
     default: return fail(SSCG_ERR_INVALID, "unknown inspect target %d", what);
     }
     if (!need(cnt * 8)) return fail(SSCG_ERR_INVALID, "buffer too small");
@@ -1136,6 +1161,29 @@ extern "C" sscg_status sscg_set_option(sscg_ctx *c, int32_t key, int32_t value)
     case SSCG_OPT_DIAGNOSTICS:
         if (value != 0 && value != 1) return fail(SSCG_ERR_INVALID, "bad diagnostics flag %d", value);
         c->diagnostics = value == 1;
+        if (c->diagnostics && !c->diag_part) {
+            const int L = (int)c->slabs.size();
+            TRY(dalloc(c, &c->diag_part, (size_t)L * DIAG_BLK));
+            TRY(dalloc(c, &c->diag_sum, 1));
+            // ||A|| (Gershgorin, max row sum of |A_ij|) over every slab and rank, once
+            double *bmax = c->diag_part;
+            double mx = 0.0;
+            std::vector<double> h(DIAG_BLK);
+            for (int l = 0; l < L; ++l) {
+                launch_anorm(c->g, c->slabs[l], bmax, DIAG_BLK, c->stream);
+                CU(cudaGetLastError());
+                CU(cudaMemcpyAsync(h.data(), bmax, DIAG_BLK * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                CU(cudaStreamSynchronize(c->stream));
+                for (double v : h) mx = std::max(mx, v);
+            }
+            if (c->nranks > 1) {
+                CU(cudaMemcpyAsync(c->diag_sum, &mx, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+                NC(ncclAllReduce(c->diag_sum, c->diag_sum, 1, ncclDouble, ncclMax, c->comm, c->stream));
+                CU(cudaMemcpyAsync(&mx, c->diag_sum, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                CU(cudaStreamSynchronize(c->stream));
+            }
+            c->anorm = mx;
+        }
         break;
     case SSCG_OPT_BASIS:
         if (value != SSCG_BASIS_CHEBYSHEV && value != SSCG_BASIS_MONOMIAL) return fail(SSCG_ERR_INVALID, "bad basis %d", value);

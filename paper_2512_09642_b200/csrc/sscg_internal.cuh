@@ -143,6 +143,12 @@ void launch_k4(const K4Args &a, DevState *st, cudaStream_t s);
 
 // diagnostics: kappa(G) of the scaled Gram matrix of the last update (one warp)
 void launch_kappa(const double *blk, int s, const DevState *st, double *h_kappa, cudaStream_t stream);
+// diagnostics: ||P_k||_F (per-block partials, then phase 0: ordered sum, phase 1: budget term)
+void launch_pnorm(const Geo &g, const Slab &sl, int s, double *part, int nblk, const DevState *st, cudaStream_t stream);
+void launch_budget(const double *part, int nparts, double *sum, double anorm, bool allreduce_needed,
+                   const DevState *st, const double *h_delta, double *h_pnorm, double *h_budget, cudaStream_t stream,
+                   int phase);
+void launch_anorm(const Geo &g, const Slab &sl, double *bmax, int nblk, cudaStream_t stream);
 
 // K5: x += P alpha;  p_0 -= W alpha over padded planes [zb, ze) (ze < 0: to nzl+1)
 //   rec: form W alpha from the Chebyshev recurrence (constant diagonal, vector path only)

@@ -150,10 +150,20 @@ def test_diagnostics_kappa(kind, nx, ny, nz, s):
     against numpy's condition number of the oracle's scaled G at outer 0."""
     import paper_2512_09642_b200 as sscg
     P = Problem(kind, nx, ny, nz, s, 20, lanczos=(kind == "27pt"))
-    x_or, tr = P.oracle(max_outer=2)
+    x_or, tr = P.oracle(max_outer=2, dump_iter=0)
     with P.gpu_solver() as S:
         S.set_option(sscg.OPT_DIAGNOSTICS, 1)
         S.solve(P.b_gpu(), rtol=0.0, max_outer=2)
+        # ||P_0||_F and the budget term delta_0 ||A|| ||P_0||_F (PAPER.md:259-266), ||A|| = Gershgorin
+        # bound = 2 x centre for these graph-Laplacian stencils
+        pf = np.sqrt(sum(np.dot(p, p) for p in tr.P))
+        assert abs(S.inspect(sscg.INSPECT_PNORM, 0)[0] - pf) <= 1e-12 * pf
+        anorm = 2.0 * {"5pt": 4.0, "7pt": 6.0, "27pt": 26.0}[kind]
+        b0 = tr.delta[0] * anorm * pf
+        assert abs(S.inspect(sscg.INSPECT_BUDGET, 0)[0] - b0) <= 1e-6 * b0
+        st = S.stats()
+        assert st.budget == pytest.approx(S.inspect(sscg.INSPECT_BUDGET, 0)[0] + S.inspect(sscg.INSPECT_BUDGET, 1)[0],
+                                          rel=1e-14)
         d, G, ct = orc.scale(tr.ghat[0], tr.c[0])
         ev = np.linalg.eigvalsh(G)
         assert ev[0] > 0
