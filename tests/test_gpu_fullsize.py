@@ -166,3 +166,65 @@ def test_update_properties_and_iterate_path(cfg5):
     # recurrence residual (p_0 after the update) vs the true residual
     p0_next = S.basis(0)[0]    # basis of outer 1 starts with r_1 (recurrence)
     assert np.linalg.norm(p0_next - r1_true) <= 1e-12 * np.linalg.norm(b)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE cfg 3 (27-point 256^3) and cfg 4 (variable coefficients 192^3) at
+# full size in bench.py's launch configuration, by the same sampled-basis
+# argument (27-point and face stencils also reach one cell per step) and the
+# oracle's leading Gram entries on the full grid.
+
+@pytest.mark.parametrize("kind,n", [("27pt", 256), ("varcoef7", 192)])
+def test_sampled_basis_and_gram_cfg3_cfg4(kind, n):
+    import torch
+
+    import paper_2512_09642_b200 as sscg
+    s, nu = 16, 30
+    b = inputs.rhs_uniform(n, n, n, seed=42)
+    faces = inputs.lognormal_faces(n, n, n, seed=42) if kind == "varcoef7" else None
+    lmin, lmax = inputs.analytic_bounds("27pt", n, n, n) if kind == "27pt" else (0.002, 1.99)
+    dev = torch.device("cuda")
+    if faces is not None:
+        ft = [torch.from_numpy(np.ascontiguousarray(f)).to(dev) for f in faces]
+        op = sscg.Stencil(kind, n, n, n, *ft)
+    else:
+        op = sscg.Stencil(kind, n, n, n)
+    with sscg.Solver(op, lmin, lmax, s, nu) as S:
+        S.solve(torch.from_numpy(b).to(dev), rtol=0.0, max_outer=0)
+        rng = np.random.default_rng(11)
+        pts = [(0, 0, 0), (n - 1, n - 1, n - 1), (n // 2, 0, n - 1)]
+        pts += [tuple(int(v) for v in rng.integers(0, n, 3)) for _ in range(4)]
+        R = s + 1
+        flat = [x + n * (y + n * z) for x, y, z in pts]
+        got_p = [S.basis(j)[0][flat] for j in range(s)]
+        got_w = [S.basis(j)[1][flat] for j in range(s)]
+        G, c = S.gram(0)
+    for q, pt in enumerate(pts):
+        lo = [max(0, cc - R) for cc in pt]
+        hi = [min(n, cc + R + 1) for cc in pt]
+        dims = [h - l for l, h in zip(lo, hi)]
+        xs, ys, zs = np.meshgrid(np.arange(lo[0], hi[0]), np.arange(lo[1], hi[1]), np.arange(lo[2], hi[2]),
+                                 indexing="ij")
+        bb = inputs.rhs_at(n, n, xs.transpose(2, 1, 0).ravel(), ys.transpose(2, 1, 0).ravel(),
+                           zs.transpose(2, 1, 0).ravel(), seed=42)
+        if kind == "varcoef7":
+            kx, ky, kz = faces
+            sub = (np.ascontiguousarray(kx[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0] + 1]),
+                   np.ascontiguousarray(ky[lo[2]:hi[2], lo[1]:hi[1] + 1, lo[0]:hi[0]]),
+                   np.ascontiguousarray(kz[lo[2]:hi[2] + 1, lo[1]:hi[1], lo[0]:hi[0]]))
+            A = orc.stencil(orc.KIND_VARCOEF7, *dims, *sub)
+        else:
+            A = orc.stencil(orc.KIND_27PT, *dims)
+        P, W = orc.chebyshev_basis(A, orc.diag(A), lmin, lmax, s, bb)
+        cc = [p - l for p, l in zip(pt, lo)]
+        gi = cc[0] + dims[0] * (cc[1] + dims[1] * cc[2])
+        for j in range(s):
+            sp, sw = max(np.abs(P[j]).max(), 1e-300), max(np.abs(W[j]).max(), 1e-300)
+            assert abs(got_p[j][q] - P[j, gi]) <= TOL_BASIS * sp, (kind, pt, j)
+            assert abs(got_w[j][q] - W[j, gi]) <= TOL_BASIS * sw, (kind, pt, j)
+    # leading Gram entries from the oracle on the full grid
+    A = orc.stencil(orc.KIND_VARCOEF7, n, n, n, *faces) if faces is not None else orc.stencil(orc.KIND_27PT, n, n, n)
+    P, W = orc.chebyshev_basis(A, orc.diag(A), lmin, lmax, 2, b)
+    Gor, cor = orc.gram(P, W)
+    assert np.max(np.abs(G[:2, :2] - Gor)) <= TOL_GRAM * np.max(np.abs(Gor))
+    assert np.max(np.abs(c[:2] - cor)) <= TOL_GRAM * np.max(np.abs(cor))
