@@ -211,7 +211,8 @@ SSCG_API sscg_status sscg_stats(const sscg_ctx *ctx, sscg_stats_t *out);
  *   SSCG_INSPECT_DELTA     outer `index`: 1 double (||c~ - G a~|| / ||c~||)
  *   SSCG_INSPECT_LNORM     outer `index`: 1 double (||L||_F of the scaled Gram matrix)
  * `capacity` is the byte size of host_out; too small => SSCG_ERR_INVALID.
- * History entries exist for outer indices 0..max_outer of the last solve. */
+ * History entries exist for outer indices 0..max_outer of the last solve
+ * (GRAM, D, ALPHA_T, ALPHA: the first 2048 outer iterations only). */
 enum {
     SSCG_INSPECT_P = 0, SSCG_INSPECT_W = 1, SSCG_INSPECT_GRAM = 2, SSCG_INSPECT_D = 3,
     SSCG_INSPECT_ALPHA_T = 4, SSCG_INSPECT_ALPHA = 5, SSCG_INSPECT_DELTA = 6,

@@ -34,15 +34,15 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
     const int s = a.s, lane = threadIdx.x;
     const int k = st->k;
     const int nent = s * s + s;
-    const bool rec = k < st->hist_cap;
+    const bool rec = k < st->hist_cap, recg = k < st->gram_cap;
     if (!TWO) {
         for (int q = lane; q < nent; q += 32) {
             const double v = a.blk[q];
             Bs[q] = v;
-            if (rec) a.h_gram[(int64_t)k * nent + q] = v;
+            if (recg) a.h_gram[(int64_t)k * nent + q] = v;
         }
         __syncwarp();
-    } else if (rec) {
+    } else if (recg) {
         for (int q = lane; q < nent; q += 32) a.h_gram[(int64_t)k * nent + q] = a.blk[q];
     }
     const double *Gh = TWO ? a.blk : Bs, *c = Gh + s * s;
@@ -151,9 +151,11 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
     const double cc = warp_sum(ct0 * ct0 + ct1 * ct1);
     if (v0) a.alpha[i0] = d0 * al0;
     if (v1) a.alpha[i1] = d1 * al1;
-    if (rec) {
+    if (recg) {
         if (v0) { a.h_d[(int64_t)k * s + i0] = d0; a.h_at[(int64_t)k * s + i0] = al0; a.h_al[(int64_t)k * s + i0] = d0 * al0; }
         if (v1) { a.h_d[(int64_t)k * s + i1] = d1; a.h_at[(int64_t)k * s + i1] = al1; a.h_al[(int64_t)k * s + i1] = d1 * al1; }
+    }
+    if (rec) {
         if (lane == 0) {
             a.h_delta[k] = sqrt(rr) / sqrt(cc);
             a.h_lnorm[k] = sqrt(ll);
@@ -182,8 +184,8 @@ __global__ void __launch_bounds__(32) k4_chol(K4Args a, DevState *st)
     const int k = st->k;
     const double *Gh = a.blk, *c = a.blk + s * s;
     const int nent = s * s + s;
-    const bool rec = k < st->hist_cap;
-    if (rec)
+    const bool rec = k < st->hist_cap, recg = k < st->gram_cap;
+    if (recg)
         for (int q = lane; q < nent; q += 32) a.h_gram[(int64_t)k * nent + q] = a.blk[q];
     const double rn = sqrt(c[0]);
     const double r0 = (k == 0) ? rn : st->r0norm;
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(32) k4_chol(K4Args a, DevState *st)
         rr += ri * ri;
         cc += ct[i] * ct[i];
         a.alpha[i] = dsh[i] * al[i];
-        if (rec) {
+        if (recg) {
             a.h_d[(int64_t)k * s + i] = dsh[i];
             a.h_at[(int64_t)k * s + i] = al[i];
             a.h_al[(int64_t)k * s + i] = dsh[i] * al[i];

@@ -69,7 +69,7 @@ struct sscg_ctx {
     DevState *st = nullptr;
     DevState *st_host = nullptr;      // pinned
     // history (device) and host copies
-    int hist_cap = 0;
+    int hist_cap = 0, gram_cap = 0;
     double *h_lnorm = nullptr;
     double *h_gram = nullptr, *h_d = nullptr, *h_at = nullptr, *h_al = nullptr, *h_delta = nullptr,
            *h_relres = nullptr;
@@ -124,6 +124,7 @@ struct sscg_ctx {
 
 static const char *kVersion = "sscg-b200 0.1 (sm_100a)";
 static const int DIAG_BLK = 592;   // blocks of the ||P||_F diagnostic per slab
+static const int GRAM_HIST = 2048; // outer iterations whose Gram block / d / alpha are recorded
 
 extern "C" const char *sscg_version(void) { return kVersion; }
 extern "C" const char *sscg_last_error(void) { return g_err.c_str(); }
@@ -848,10 +849,16 @@ static sscg_status ensure_history(sscg_ctx *c, int cap)
         c->gexec = nullptr;
     }
     const int s = c->s, nent = s * s + s;
-    TRY(dalloc(c, &c->h_gram, (size_t)cap * nent));
-    TRY(dalloc(c, &c->h_d, (size_t)cap * s));
-    TRY(dalloc(c, &c->h_at, (size_t)cap * s));
-    TRY(dalloc(c, &c->h_al, (size_t)cap * s));
+    // per-outer vector records (Gram block, d, alpha~, alpha) are kept for the
+    // first GRAM_HIST outer iterations only: s = 64 would need 33 GB for 2^20
+    const int gcap = std::min(cap, GRAM_HIST);
+    if (gcap > c->gram_cap) {
+        TRY(dalloc(c, &c->h_gram, (size_t)gcap * nent));
+        TRY(dalloc(c, &c->h_d, (size_t)gcap * s));
+        TRY(dalloc(c, &c->h_at, (size_t)gcap * s));
+        TRY(dalloc(c, &c->h_al, (size_t)gcap * s));
+        c->gram_cap = gcap;
+    }
     TRY(dalloc(c, &c->h_delta, (size_t)cap));
     TRY(dalloc(c, &c->h_lnorm, (size_t)cap));
     TRY(dalloc(c, &c->h_kappa, (size_t)cap));
@@ -880,6 +887,7 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
     c->last_max_outer = max_outer;
     DevState h{};
     h.hist_cap = c->hist_cap;
+    h.gram_cap = c->gram_cap;
     h.rtol = rtol;
     h.max_outer = max_outer;
     *c->st_host = h;
@@ -1054,6 +1062,10 @@ extern "C" sscg_status sscg_inspect(const sscg_ctx *cc, int32_t what, int32_t in
     }
     if (index < 0 || index >= c->hist_cap || index > c->last_max_outer)
         return fail(SSCG_ERR_INVALID, "history index %d out of range", index);
+    if ((what == SSCG_INSPECT_GRAM || what == SSCG_INSPECT_D || what == SSCG_INSPECT_ALPHA_T ||
+         what == SSCG_INSPECT_ALPHA) && index >= c->gram_cap)
+        return fail(SSCG_ERR_INVALID, "outer %d: Gram/alpha records are kept for the first %d outer iterations",
+                    index, c->gram_cap);
     const double *src = nullptr;
     int64_t cnt = 0;
     switch (what) {

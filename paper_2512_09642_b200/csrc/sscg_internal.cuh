@@ -18,8 +18,8 @@ struct DevState {
     int breakdown;
     int nonfinite;
     int outer;        // updates applied
-    int hist_cap;     // history slots available
-    int pad_;
+    int hist_cap;     // scalar history slots (relres, delta, ||L||, ...)
+    int gram_cap;     // per-outer vector records (Gram block, d, alpha~, alpha): min(hist_cap, 2048)
     double r0norm;    // ||r_0||
     double rtol;
     int max_outer;

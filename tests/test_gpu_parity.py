@@ -400,3 +400,20 @@ def test_user_diagonal_preconditioner(kind, nx, ny, nz, s):
         assert_alpha(S, tr, 0)
         assert_basis(S, tr, s, tol=TOL_BASIS_DRIFT)
     assert np.linalg.norm(x - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+def test_long_run_history_caps():
+    """Scalar histories cover every outer iteration; the per-outer Gram/alpha
+    records stop after 2048 (bounded memory at s = 64), and asking beyond is
+    an error, not a crash."""
+    import paper_2512_09642_b200 as sscg
+    P = Problem("7pt", 24, 24, 24, 1, 1)      # s = 1: slow enough not to reach r = 0 in 2100 steps
+    with P.gpu_solver() as S:
+        S.solve(P.b_gpu(), rtol=0.0, max_outer=2100)
+        st = S.stats()
+        assert st.outer_iterations == 2100 and len(st.relres_history) == 2101
+        assert S.inspect(sscg.INSPECT_DELTA, 2099)[0] >= 0.0
+        G, c = S.gram(2047)
+        assert np.all(np.isfinite(G))
+        with pytest.raises(sscg.SSCGError):
+            S.gram(2048)
