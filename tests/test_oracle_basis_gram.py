@@ -166,3 +166,39 @@ def test_lower_fro_slope_2d():
     lf = [lower_fro("5pt", (64, 64, 1), s, seed=12) for s in ss]
     slope = np.polyfit(np.log(ss), np.log(lf), 1)[0]
     assert 0.4 <= slope <= 0.7, slope
+
+
+@pytest.mark.parametrize("kind,n,s,nu,it", [("7pt", 40, 16, 25, 0), ("7pt", 48, 16, 25, 25), ("27pt", 28, 16, 30, 10),
+                                            ("varcoef7", 20, 16, 20, 30), ("5pt", 64, 8, 20, 50),
+                                            ("7pt", 24, 32, 30, 8)])
+def test_w_recovered_from_recurrence(kind, n, s, nu, it):
+    """W = AP recovered POINTWISE from the Chebyshev recurrence (R23):
+      w_0 = M (p_1/theta + sigma p_0),  w_j = M ((p_{j+1} + p_{j-1})/(2 theta) + sigma p_j)
+    for j <= s-2 (PAPER.md:36-42 solved for M^{-1} A p_j) equals the SpMV W to a
+    few ulps per entry, and so does the Gram block -- also late in the solve,
+    where the residual is dominated by the low modes.  (Rebuilding G from
+    dot products of P alone, G_ij = p_i^T M p_{j+1}/(2 theta) + ..., would
+    cancel large dot products instead; that is not what is done.)"""
+    nz = 1 if kind == "5pt" else n
+    faces = inputs.lognormal_faces(n, n, nz, seed=42) if kind == "varcoef7" else None
+    A = (orc.stencil(orc.KIND_VARCOEF7, n, n, nz, *faces) if faces is not None
+         else orc.stencil({"5pt": orc.KIND_5PT2D, "7pt": orc.KIND_7PT, "27pt": orc.KIND_27PT}[kind], n, n, nz))
+    b = inputs.rhs_uniform(n, n, nz, seed=42)
+    if kind in ("27pt", "varcoef7"):
+        lmin, lmax, _ = orc.lanczos_bounds(A, 50, b, 0.05)
+    else:
+        lmin, lmax = inputs.analytic_bounds(kind, n, n, nz)
+    x, tr = orc.sstep_cg(A, lmin, lmax, s, nu, b, rtol=0.0, max_outer=it, dump_iter=it)
+    P, W, M = tr.P, tr.W, orc.diag(A)
+    th, sg = 2.0 / (lmax - lmin), (lmax + lmin) / 2.0
+    Wr = np.empty_like(W)
+    Wr[0] = M * (P[1] / th + sg * P[0])
+    for j in range(1, s - 1):
+        Wr[j] = M * ((P[j + 1] + P[j - 1]) / (2.0 * th) + sg * P[j])
+    Wr[s - 1] = W[s - 1]
+    for j in range(s - 1):
+        assert np.max(np.abs(Wr[j] - W[j])) <= 1e-14 * np.max(np.abs(W[j])), j
+    G, _ = orc.gram(P, W)
+    Gr, _ = orc.gram(P, Wr)
+    assert np.max(np.abs(Gr - G)) <= 1e-14 * np.max(np.abs(G))
+    assert np.max(np.abs(np.diag(Gr) - np.diag(G)) / np.diag(G)) <= 1e-13
