@@ -319,7 +319,8 @@ def run_ours(a):
     basis_vecs = S.query(sscg.QUERY_BASIS_VECTORS)       # (4s-3), or 46 at s = 16 with K1F pairs
     fused = bool(S.query(sscg.QUERY_BASIS_FUSED))
     upd_vecs = S.query(sscg.QUERY_UPDATE_VECTORS)        # 2s+3, or s+4 with W alpha from the recurrence
-    bytes_per_outer = {"basis": basis_vecs * vec + s * face_bytes, "gram": 2 * s * vec,
+    gram_vecs = S.query(sscg.QUERY_GRAM_VECTORS)         # 2s, or s+1 with W recovered from the recurrence
+    bytes_per_outer = {"basis": basis_vecs * vec + s * face_bytes, "gram": gram_vecs * vec,
                        "update": upd_vecs * vec}
     kern = {}
     for k, byt in bytes_per_outer.items():
@@ -338,17 +339,20 @@ def run_ours(a):
     path_bytes = sum(bytes_per_outer.values())
     cfg = workload(a, world)
     k1_name = "k1f" if fused else K1_NAME
-    mc = mix_ceiling(2, 4) if fused else mix_ceiling(2, 2)
+    # read : write vectors of one interior basis launch (W recovered in the Gram pass: p only)
+    wfree = gram_vecs < 2 * s
+    mixrw = ((2, 2) if wfree else (2, 4)) if fused else ((2, 1) if wfree else (2, 2))
+    mc = mix_ceiling(*mixrw)
     roof = {"bound": "hbm", "kernel": "K1 %s<%s> (%sSpMV + Jacobi + Chebyshev recurrence)"
                                       % (k1_name, a.kind, "two basis steps per launch: " if fused else ""),
             "achieved": k1["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": k1["frac"],
             "traffic": ncu_traffic(n, k1_name) if a.workload == "cfg5" else None, "peak_source": peak_src,
             "traffic_note": "ncu dram read+write of one interior launch (algorithmic: %d vectors = %.4g B)"
-                            % (6 if fused else 4, (6 if fused else 4) * vec),
+                            % (sum(mixrw), sum(mixrw) * vec),
             "bytes_rule": "%d FP64 vectors per outer (%s) + s face sets for varcoef7, / basis launches (SURVEY 8(d)); "
-                          "path: basis + 2s (Gram) + %d (update) vectors"
-                          % (basis_vecs, "K1F pairs: 6 per pair" if fused else "(4s-3)", upd_vecs),
-            "mix": "2 reads : 4 writes per pair" if fused else "2 reads : 2 writes",
+                          "path: basis + %d (Gram) + %d (update) vectors"
+                          % (basis_vecs, "K1F pairs" if fused else "single steps", gram_vecs, upd_vecs),
+            "mix": "%d reads : %d writes per launch" % mixrw,
             "mix_ceiling_gbs": mc[0], "mix_ceiling_source": mc[1],
             "frac_of_mix_ceiling": (k1["achieved_gbs"] / mc[0]) if (mc[0] and k1["achieved_gbs"]) else None,
             "path_bytes_per_step": path_bytes,

@@ -288,8 +288,13 @@ SSCG_API sscg_status sscg_set_option(sscg_ctx *ctx, int32_t key, int32_t value);
  *                             W), or s+4 when W alpha is formed from the
  *                             Chebyshev recurrence (R21; s+5 when
  *                             the Jacobi diagonal varies and is read too)
+ *   SSCG_QUERY_GRAM_VECTORS   FP64 vectors the Gram pass reads per outer
+ *                             iteration: 2s (P and the stored W = AP), or s+1
+ *                             (+1 for a varying diagonal) when W is recovered
+ *                             from the basis recurrence (R23)
  * Errors: SSCG_ERR_INVALID. */
-enum { SSCG_QUERY_BASIS_FUSED = 0, SSCG_QUERY_BASIS_VECTORS = 1, SSCG_QUERY_UPDATE_VECTORS = 2 };
+enum { SSCG_QUERY_BASIS_FUSED = 0, SSCG_QUERY_BASIS_VECTORS = 1, SSCG_QUERY_UPDATE_VECTORS = 2,
+       SSCG_QUERY_GRAM_VECTORS = 3 };
 SSCG_API sscg_status sscg_query(const sscg_ctx *ctx, int32_t what, int64_t *out);
 
 SSCG_API void sscg_destroy(sscg_ctx *ctx);

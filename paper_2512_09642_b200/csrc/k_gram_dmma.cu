@@ -28,7 +28,7 @@ namespace {
 
 constexpr int NCW = 8;                 // consumer warps
 constexpr int THREADS = 32 * (NCW + 1);
-constexpr int MAXS = 4;                // ring stages
+constexpr int MAXS = 8;                // ring stages
 
 struct K2DParams {
     int64_t N;         // interior doubles per vector
@@ -75,10 +75,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
 
-    double acc[NT][2];
+    // U accumulator sets: k-steps rotate over them so that U*NT independent
+    // DMMA chains hide the tensor-core latency when the tile count is small
+    constexpr int U = (NT >= 10) ? 1 : (NT >= 6) ? 2 : (NT >= 3) ? 4 : 8;
+    double acc[U][NT][2];
     double cac[NB];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
 #pragma unroll
     for (int i = 0; i < NB; ++i) cac[i] = 0.0;
 
@@ -104,21 +109,26 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_wait(&full[stg], (uint32_t)((it / NS) & 1));
             const double *sP = smem + (size_t)stg * stage_elems;
             const double *sW = sP + SP * EP;
-            for (int ks = cw; ks < KS; ks += NCW) {
-                const int o = r * EP + ks * 4 + kk;
-                double a[NB], b[NB];
+            for (int ks0 = cw; ks0 < KS; ks0 += NCW * U) {
 #pragma unroll
-                for (int i = 0; i < NB; ++i) a[i] = sP[o + i * 8 * EP];
+                for (int u = 0; u < U; ++u) {
+                    const int ks = ks0 + u * NCW;
+                    if (ks >= KS) break;
+                    const int o = r * EP + ks * 4 + kk;
+                    double a[NB], b[NB];
 #pragma unroll
-                for (int j = 0; j < NB; ++j) b[j] = sW[o + j * 8 * EP];
-                const double p0 = sP[ks * 4 + kk];
+                    for (int i = 0; i < NB; ++i) a[i] = sP[o + i * 8 * EP];
 #pragma unroll
-                for (int i = 0; i < NB; ++i) cac[i] = fma(a[i], p0, cac[i]);
-                int t = 0;
+                    for (int j = 0; j < NB; ++j) b[j] = sW[o + j * 8 * EP];
+                    const double p0 = sP[ks * 4 + kk];
 #pragma unroll
-                for (int i = 0; i < NB; ++i)
+                    for (int i = 0; i < NB; ++i) cac[i] = fma(a[i], p0, cac[i]);
+                    int t = 0;
 #pragma unroll
-                    for (int j = i; j < NB; ++j, ++t) dmma(acc[t][0], acc[t][1], a[i], b[j]);
+                    for (int i = 0; i < NB; ++i)
+#pragma unroll
+                        for (int j = i; j < NB; ++j, ++t) dmma(acc[u][t][0], acc[u][t][1], a[i], b[j]);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
@@ -137,8 +147,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int cw = warp - 1;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-            red[((cw * NT + t) * 32 + lane) * 2 + 0] = acc[t][0];
-            red[((cw * NT + t) * 32 + lane) * 2 + 1] = acc[t][1];
+#pragma unroll
+            for (int u = 1; u < U; ++u) {   // fold the accumulator sets in a fixed order
+                acc[0][t][0] += acc[u][t][0];
+                acc[0][t][1] += acc[u][t][1];
+            }
+            red[((cw * NT + t) * 32 + lane) * 2 + 0] = acc[0][t][0];
+            red[((cw * NT + t) * 32 + lane) * 2 + 1] = acc[0][t][1];
         }
         if ((lane & 3) == 0)
 #pragma unroll
@@ -156,6 +171,188 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int a = 0; a < NB; ++a) {
             if (tt < NB - a) { I = a; J = a + tt; break; }
             tt -= NB - a;
+        }
+        const int i = I * 8 + (ln >> 2), j = J * 8 + 2 * (ln & 3) + h;
+        if (i < s && j < s && i <= j) mypart[i * s + j] = v;
+    }
+    for (int i = tid; i < s; i += THREADS) {
+        double v = 0.0;
+        for (int w = 0; w < NCW; ++w) v += red[NCW * NT * 64 + w * SP + i];
+        mypart[s * s + i] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) is_last = atomicAdd(k.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    last_cta_sum(k.part, gridDim.x, s, k.out);
+    if (tid == 0) *k.ticket = 0u;
+}
+
+// K2R -- the same DMMA Gram pass when W = AP is NOT stored (R23):
+// only P (plus the stored w_{s-1}, and diag(M) per point when it varies) is
+// streamed, and each B fragment w_j(point) is recovered in registers from the
+// Chebyshev recurrence (PAPER.md:36-42 solved for M^{-1} A p_j)
+//   w_0 = m (p_1/theta + sigma p_0),  w_j = m ((p_{j+1} + p_{j-1})/(2 theta) + sigma p_j),
+// p_{j+-1} of the fragment row taken from the neighbouring lanes' A fragments
+// by two shuffles.  Half the Gram bytes of K2/K2D.
+struct K2RParams {
+    int64_t N;
+    int s, s_pad, nstage, wlp;   // wlp: padded pitch (doubles) of the w_{s-1} / diag(M) rows
+    double inv_theta, inv_2theta, sigma, dm;
+    double *part, *out;
+    unsigned *ticket;
+};
+
+template <int NB, int EP, bool VARM>
+__global__ void __launch_bounds__(THREADS, 1)
+    k2r(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmWl,
+        const __grid_constant__ CUtensorMap tmDv, K2RParams k, const DevState *st)
+{
+    if (st && st->done) return;
+    constexpr int SP = 8 * NB;
+    constexpr int KS = EP / 4;
+    constexpr int NT = NB * (NB + 1) / 2;
+    extern __shared__ __align__(1024) double smem[];
+    __shared__ uint64_t full[MAXS], empty[MAXS];
+    __shared__ bool is_last;
+    const int s = k.s, NS = k.nstage;
+    const int stage_elems = SP * EP + k.wlp * (VARM ? 2 : 1);
+    const uint32_t stage_bytes = (uint32_t)(SP * EP + EP * (VARM ? 2 : 1)) * 8u;   // bytes the TMA delivers
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nchunks = (k.N + EP - 1) / EP;
+    const int nit = (int)((nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x);
+
+    if (tid == 0) {
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NCW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmP);
+        tma_prefetch_desc(&tmWl);
+        if (VARM) tma_prefetch_desc(&tmDv);
+    }
+    __syncthreads();
+
+    // U accumulator sets: k-steps rotate over them so that U*NT independent
+    // DMMA chains hide the tensor-core latency when the tile count is small
+    constexpr int U = (NT >= 10) ? 1 : (NT >= 6) ? 2 : (NT >= 3) ? 4 : 8;
+    double acc[U][NT][2];
+    double cac[NB];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) cac[i] = 0.0;
+
+    if (warp == 0) {
+        for (int it = 0; it < nit; ++it) {
+            if (lane == 0) {
+                const int stg = it % NS;
+                if (it >= NS) mbar_wait(&empty[stg], (uint32_t)((it / NS - 1) & 1));
+                double *dst = smem + (size_t)stg * stage_elems;
+                const int x = (int)((blockIdx.x + (int64_t)it * gridDim.x) * EP);
+                mbar_expect_tx(&full[stg], stage_bytes);
+                tma_load_2d(dst, &tmP, x, 0, &full[stg]);
+                tma_load_2d(dst + SP * EP, &tmWl, x, s - 1, &full[stg]);
+                if (VARM) tma_load_2d(dst + SP * EP + k.wlp, &tmDv, x, 0, &full[stg]);
+            }
+            __syncwarp();
+        }
+    } else {
+        const int cw = warp - 1;
+        const int r = lane >> 2, kk = lane & 3;
+        // per-lane recurrence coefficients of fragment row j = J*8 + r (fixed for the kernel):
+        //   w = m (up c1 + dn c2 + sigma p_j)  (j <= s-2),  w = w_{s-1} (stored),  0 (j >= s)
+        double c1[NB], c2[NB], cs[NB], use_wl[NB];
+#pragma unroll
+        for (int J = 0; J < NB; ++J) {
+            const int j = J * 8 + r;
+            const bool rec = j < s - 1;
+            c1[J] = !rec ? 0.0 : (j == 0 ? k.inv_theta : k.inv_2theta);
+            c2[J] = (rec && j > 0) ? k.inv_2theta : 0.0;
+            cs[J] = rec ? k.sigma : 0.0;
+            use_wl[J] = (j == s - 1) ? 1.0 : 0.0;
+        }
+        for (int it = 0; it < nit; ++it) {
+            const int stg = it % NS;
+            mbar_wait(&full[stg], (uint32_t)((it / NS) & 1));
+            const double *sP = smem + (size_t)stg * stage_elems;
+            const double *sWl = sP + SP * EP, *sDv = sWl + k.wlp;
+            for (int ks0 = cw; ks0 < KS; ks0 += NCW * U) {
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const int ks = ks0 + u * NCW;
+                if (ks >= KS) break;
+                const int pt = ks * 4 + kk;
+                const int o = r * EP + pt;
+                double a[NB], b[NB];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) a[i] = sP[o + i * 8 * EP];
+                const double p0 = sP[pt];
+                const double wl = sWl[pt];
+                const double m = VARM ? sDv[pt] : k.dm;
+#pragma unroll
+                for (int J = 0; J < NB; ++J) {
+                    // row J*8+r+1: lane+4 (same block) or, for r = 7, block J+1 row 0
+                    const double su = (r == 0) ? ((J + 1 < NB) ? a[J + 1 < NB ? J + 1 : J] : 0.0) : a[J];
+                    const double up = __shfl_sync(0xffffffffu, su, (lane + 4) & 31);
+                    // row J*8+r-1: lane-4 (same block) or, for r = 0, block J-1 row 7
+                    const double sd = (r == 7) ? ((J > 0) ? a[J > 0 ? J - 1 : 0] : 0.0) : a[J];
+                    const double dn = __shfl_sync(0xffffffffu, sd, (lane + 28) & 31);
+                    const double w = m * fma(up, c1[J], fma(dn, c2[J], cs[J] * a[J]));
+                    b[J] = (use_wl[J] != 0.0) ? wl : w;   // branch-free select
+                }
+#pragma unroll
+                for (int i = 0; i < NB; ++i) cac[i] = fma(a[i], p0, cac[i]);
+                int t = 0;
+#pragma unroll
+                for (int i = 0; i < NB; ++i)
+#pragma unroll
+                    for (int J = i; J < NB; ++J, ++t) dmma(acc[u][t][0], acc[u][t][1], a[i], b[J]);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            cac[i] += __shfl_xor_sync(0xffffffffu, cac[i], 1);
+            cac[i] += __shfl_xor_sync(0xffffffffu, cac[i], 2);
+        }
+    }
+    __syncthreads();
+    double *red = smem;
+    if (warp > 0) {
+        const int cw = warp - 1;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+#pragma unroll
+            for (int u = 1; u < U; ++u) {   // fold the accumulator sets in a fixed order
+                acc[0][t][0] += acc[u][t][0];
+                acc[0][t][1] += acc[u][t][1];
+            }
+            red[((cw * NT + t) * 32 + lane) * 2 + 0] = acc[0][t][0];
+            red[((cw * NT + t) * 32 + lane) * 2 + 1] = acc[0][t][1];
+        }
+        if ((lane & 3) == 0)
+#pragma unroll
+            for (int i = 0; i < NB; ++i) red[NCW * NT * 64 + cw * SP + i * 8 + (lane >> 2)] = cac[i];
+    }
+    __syncthreads();
+    const int nent = s * s + s;
+    double *mypart = k.part + (int64_t)blockIdx.x * nent;
+    for (int q = tid; q < NT * 64; q += THREADS) {
+        const int t = q >> 6, e = q & 63, ln = e >> 1, h = e & 1;
+        double v = 0.0;
+        for (int w = 0; w < NCW; ++w) v += red[((w * NT + t) * 32 + ln) * 2 + h];
+        int I = 0, J = 0, tt = t;
+        for (int aa = 0; aa < NB; ++aa) {
+            if (tt < NB - aa) { I = aa; J = aa + tt; break; }
+            tt -= NB - aa;
         }
         const int i = I * 8 + (ln >> 2), j = J * 8 + 2 * (ln & 3) + h;
         if (i < s && j < s && i <= j) mypart[i * s + j] = v;
@@ -240,6 +437,93 @@ void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double 
     case 7: k2d<7, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
     default: k2d<8, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
     }
+}
+
+}  // namespace sscg
+
+namespace sscg {
+
+bool k2r_prepare(const Geo &g, Slab &sl, int s)
+{
+    const int s_pad = (s + 7) / 8 * 8, ep = ep_for(s_pad);
+    const int64_t N = (int64_t)sl.nzl * g.plane;
+    const int mx = 210 * 1024;
+#define K2R_ATTR(NB, EP, V) cudaFuncSetAttribute(k2r<NB, EP, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
+    if (K2R_ATTR(1, 132, false) || K2R_ATTR(2, 132, false) || K2R_ATTR(3, 132, false) || K2R_ATTR(4, 132, false) ||
+        K2R_ATTR(5, 68, false) || K2R_ATTR(6, 68, false) || K2R_ATTR(7, 68, false) || K2R_ATTR(8, 68, false) ||
+        K2R_ATTR(1, 132, true) || K2R_ATTR(2, 132, true) || K2R_ATTR(3, 132, true) || K2R_ATTR(4, 132, true) ||
+        K2R_ATTR(5, 68, true) || K2R_ATTR(6, 68, true) || K2R_ATTR(7, 68, true) || K2R_ATTR(8, 68, true))
+        return false;
+#undef K2R_ATTR
+    // P rows (as K2D), the single row w_{s-1} of W, and diag(M) (one row) when it varies
+    if (!encode_rows_map(&sl.tmPd, sl.P + g.plane, N, s, g.vstride, ep, s_pad)) return false;
+    if (!encode_rows_map(&sl.tmWl, sl.W + g.plane, N, s, g.vstride, ep, 1)) return false;
+    if (sl.dvec && !encode_rows_map(&sl.tmDv, sl.dvec + g.plane, N, 1, g.vstride, ep, 1)) return false;
+    return true;
+}
+
+namespace {
+// w_j of one slab recovered from the recurrence into `out` (padded interior),
+// the same formula as the K2R fragments (parity hooks read W through this)
+__global__ void k_wrec(const double *P, int64_t vstride, int64_t N, int j, double inv_theta, double inv_2theta,
+                       double sigma, double dm, const double *dvec, double *out)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+        const double m = dvec ? dvec[e] : dm;
+        const double pj = P[j * vstride + e], up = P[(j + 1) * vstride + e];
+        out[e] = (j == 0) ? m * (up * inv_theta + sigma * pj)
+                          : m * ((up + P[(j - 1) * vstride + e]) * inv_2theta + sigma * pj);
+    }
+}
+}  // namespace
+
+void launch_wrec(const Geo &g, const Slab &sl, int j, double theta, double sigma, double *out, cudaStream_t stream)
+{
+    const int64_t N = (int64_t)sl.nzl * g.plane;
+    const int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 16);
+    k_wrec<<<blocks, 256, 0, stream>>>(sl.P + g.plane, g.vstride, N, j, 1.0 / theta, 1.0 / (2.0 * theta), sigma,
+                                       g.center, sl.dvec ? sl.dvec + g.plane : nullptr, out + g.plane);
+}
+
+void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma, const DevState *st, double *out_blk,
+                cudaStream_t stream)
+{
+    const int s_pad = (s + 7) / 8 * 8, nb = s_pad / 8, ep = ep_for(s_pad);
+    const bool varm = sl.dvec != nullptr;
+    K2RParams k;
+    k.N = (int64_t)sl.nzl * g.plane;
+    k.s = s;
+    k.s_pad = s_pad;
+    k.wlp = (ep * 8 + 127) / 128 * 128 / 8;
+    const size_t stage = (size_t)(s_pad * ep + k.wlp * (varm ? 2 : 1)) * sizeof(double);
+    k.nstage = (int)std::max<size_t>(2, std::min<size_t>(MAXS, (200 * 1024) / stage));
+    k.inv_theta = 1.0 / theta;
+    k.inv_2theta = 1.0 / (2.0 * theta);
+    k.sigma = sigma;
+    k.dm = g.center;
+    k.part = sl.part;
+    k.out = out_blk;
+    k.ticket = sl.ticket;
+    const int64_t nchunks = (k.N + ep - 1) / ep;
+    const int gx = (int)std::min<int64_t>(k2_grid(), nchunks);
+    const int nt = nb * (nb + 1) / 2;
+    const size_t red = (size_t)(NCW * nt * 64 + NCW * s_pad) * sizeof(double);
+    const size_t sm = std::max((size_t)k.nstage * stage, red);
+    const CUtensorMap &dv = varm ? sl.tmDv : sl.tmWl;
+#define K2R_LAUNCH(NB, EP)                                                                                   \
+    if (varm) k2r<NB, EP, true><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWl, dv, k, st);                    \
+    else k2r<NB, EP, false><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWl, dv, k, st);
+    switch (nb) {
+    case 1: K2R_LAUNCH(1, 132) break;
+    case 2: K2R_LAUNCH(2, 132) break;
+    case 3: K2R_LAUNCH(3, 132) break;
+    case 4: K2R_LAUNCH(4, 132) break;
+    case 5: K2R_LAUNCH(5, 68) break;
+    case 6: K2R_LAUNCH(6, 68) break;
+    case 7: K2R_LAUNCH(7, 68) break;
+    default: K2R_LAUNCH(8, 68) break;
+    }
+#undef K2R_LAUNCH
 }
 
 }  // namespace sscg

@@ -31,14 +31,20 @@
 namespace sscg {
 namespace {
 
-constexpr int TX = 64, TY = 16;
+// Tile 64 x 8 with two CTAs per SM (two planes in flight per SM; the per-plane
+// work of one CTA is latency-bound) -- K1F_TY=16 builds the one-CTA variant.
+#ifndef K1F_TY
+#define K1F_TY 16
+#endif
+constexpr int TX = 64, TY = K1F_TY;
+constexpr int MINB = (TY <= 8) ? 2 : 1;    // CTAs per SM
 constexpr int BW = TX + 4;                 // all staged planes: x in [x0-2, x0+TX+2)
 constexpr int BHP = TY + 4;                // p_j: y in [y0-2, y0+TY+2)
 constexpr int BHM = TY + 2;                // p_{j-1}: y in [y0-1, y0+TY+1)
-constexpr int PS = BW * BHP;               // doubles per p_j / U slot (10880 B, 128-B multiple)
+constexpr int PS = ((BW * BHP * 8 + 127) / 128) * 128 / 8;   // doubles per p_j / U slot (128-B multiple)
 constexpr int MS = ((BW * BHM * 8 + 127) / 128) * 128 / 8;
-constexpr int NSP = 8, NSM = 6, NU = 4;
-constexpr int NCW = 20;
+constexpr int NSP = 8, NSM = 6, NU = 4;   // NSP, NU powers of two (slot = seq & (N - 1))
+constexpr int NCW = ((TY + 2) * (BW / 2) + 31) / 32;   // one front task per consumer thread
 constexpr int NCT = NCW * 32;
 constexpr int THREADS = NCT + 32;
 constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = BW * BHM * 8;
@@ -111,7 +117,7 @@ __device__ __forceinline__ double2 box9(const double *P, int o)
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, MINB)
     k1f(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, K1Args a,
         const DevState *st, K1FWork wk)
 {
@@ -174,13 +180,123 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool has_f = ct < FRONT_TASKS, has_b = ct < BACK_TASKS;
     const int rf = 1 + ct / (BW / 2), cf = 2 * (ct % (BW / 2));        // box row 1..18, col 0..66
     const int rb = 2 + ct / (TX / 2), cb = 2 + 2 * (ct % (TX / 2));    // box row 2..17, col 2..65
-    const int of = rf * BW + cf, ob = rb * BW + cb, omf = (rf - 1) * BW + cf;
+    const int of = rf * BW + cf, omf = (rf - 1) * BW + cf;
+    const int ob = has_b ? rb * BW + cb : 2 * BW + 2;   // threads without a back task read a safe cell
     const bool own_cell = rf >= 2 && rf < TY + 2 && cf >= 2 && cf < TX + 2;
     const bool lgf = cf > 0, rgf = cf + 2 < BW;
     uint32_t pc = 0, mc = 0;   // sequence numbers of the next p_j / p_{j-1} slot to consume
     const int64_t pl = g.plane;
     const double center = wk.center, dinv_c = wk.dinv_c, sigma = wk.sigma;
     const double cfr = wk.coef_front, cbk = wk.coef_back;
+    if (KIND == 1) {
+        // 7-point: streamlined plane loop (rotating slot pointers, pointer
+        // increments along z, parameters in registers); same arithmetic as below
+        const bool skip_w = a.skip_w, skip_w2 = a.skip_w2, back_pn = wk.back_pn, front_pm = wk.front_pm;
+        double *const gw = a.w, *const gpn = a.pn, *const gw2 = a.w2, *const gpn2 = a.pn2;
+        const int nzl = wk.nzl;
+        for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+            const ItemPlan it = plan_item(wk, item);
+            const int x0 = it.tx * TX, y0 = it.ty * TY;
+            const int gxf = x0 - 2 + cf, gyf = y0 - 2 + rf, gxb = x0 - 2 + cb, gyb = y0 - 2 + rb;
+            const bool vyf = gyf >= 0 && gyf < g.ny;
+            const bool v0f = has_f && vyf && gxf >= 0 && gxf < g.nx, v1f = has_f && vyf && gxf + 1 >= 0 && gxf + 1 < g.nx;
+            const bool wf = own_cell && v0f;
+            const bool wb = has_b && gyb < g.ny && gxb < g.nx, v1b = gxb + 1 < g.nx;
+            const uint32_t pbase = pc;   // sequence number of plane plo
+            // slot pointers of planes q-1, q, q+1 (seq = pbase + z - plo)
+            auto slotp = [&](int z) -> const double * {
+                return sp + ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1)) * PS;
+            };
+            // wait the planes front(zlo-1) needs: plo .. min(zlo, phi)
+            for (int z = it.plo; z <= min(it.zlo, it.phi); ++z) {
+                const uint32_t c = pbase + (uint32_t)(z - it.plo);
+                mbar_wait(&fullp[c & (NSP - 1)], (c / NSP) & 1);
+            }
+            const double *Pm = (it.zlo - 2 >= it.plo) ? slotp(it.zlo - 2) : sp;   // plane q-1
+            const double *P0 = slotp(it.zlo - 1);                                  // plane q
+            const double *Pp = slotp(it.zlo);                                      // plane q+1
+            int64_t off_f = (int64_t)(it.zlo - 1) * pl + (int64_t)gyf * g.pitch + gxf;   // global index, plane q
+            int64_t off_b = (int64_t)(it.zlo - 2) * pl + (int64_t)gyb * g.pitch + gxb;   // plane z = q-1
+            for (int q = it.zlo - 1; q <= it.zhi; ++q, off_f += pl, off_b += pl) {
+                if (q >= it.zlo && q + 1 <= it.phi) {   // plane q+1 (front(q) needs it)
+                    const uint32_t c = pbase + (uint32_t)(q + 1 - it.plo);
+                    mbar_wait(&fullp[c & (NSP - 1)], (c / NSP) & 1);
+                }
+                double *U = su + ((q + 8) & (NU - 1)) * PS;
+                const bool inside = q >= 1 && q <= nzl;
+                const bool mloaded = front_pm && q >= it.mlo && q <= it.mhi;
+                const double *M = sm + (mc % NSM) * MS;
+                if (mloaded) mbar_wait(&fullm[mc % NSM], (mc / NSM) & 1);
+                if (has_f) {
+                    double2 u = make_double2(0.0, 0.0);
+                    if (inside) {
+                        const double2 c = lds2(P0 + of);
+                        const double2 dn = lds2(Pm + of), up = lds2(Pp + of);
+                        const double2 ylo = lds2(P0 + of - BW), yhi = lds2(P0 + of + BW);
+                        const double l = lgf ? P0[of - 1] : 0.0;
+                        const double rr = rgf ? P0[of + 2] : 0.0;
+                        double2 Ap;
+                        Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                        Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                        u.x = cfr * (dinv_c * Ap.x - sigma * c.x);
+                        u.y = cfr * (dinv_c * Ap.y - sigma * c.y);
+                        if (mloaded) {
+                            const double2 pm = lds2(M + omf);
+                            u.x -= pm.x;
+                            u.y -= pm.y;
+                        }
+                        if (!v0f) u.x = 0.0;
+                        if (!v1f) u.y = 0.0;
+                        if (wf && q >= it.zlo && q < it.zhi) {
+                            if (!v1f) Ap.y = 0.0;
+                            if (!skip_w) __stcs(reinterpret_cast<double2 *>(gw + off_f), Ap);
+                            *reinterpret_cast<double2 *>(gpn + off_f) = u;
+                        }
+                    }
+                    *reinterpret_cast<double2 *>(U + of) = u;
+                }
+                if (mloaded) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&emptym[mc % NSM]);
+                    ++mc;
+                }
+                consumers_sync();   // U(q) complete; U(q-4) no longer read
+                const int z = q - 1;
+                if (wb && z >= it.zlo && z < it.zhi) {
+                    const double *Um = su + ((z + 7) & (NU - 1)) * PS, *U0 = su + ((z + 8) & (NU - 1)) * PS;
+                    const double2 c = lds2(U0 + ob);
+                    const double2 dn = lds2(Um + ob), up = lds2(U + ob);
+                    const double2 ylo = lds2(U0 + ob - BW), yhi = lds2(U0 + ob + BW);
+                    const double l = U0[ob - 1], rr = U0[ob + 2];
+                    double2 Ap;
+                    Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                    Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                    if (!v1b) Ap.y = 0.0;
+                    if (!skip_w2) __stcs(reinterpret_cast<double2 *>(gw2 + off_b), Ap);
+                    if (back_pn) {
+                        const double2 pj = lds2(Pm + ob);   // p_j(z), z = q-1
+                        const double v0 = cbk * (dinv_c * Ap.x - sigma * c.x) - pj.x;
+                        double v1 = cbk * (dinv_c * Ap.y - sigma * c.y) - pj.y;
+                        if (!v1b) v1 = 0.0;
+                        *reinterpret_cast<double2 *>(gpn2 + off_b) = make_double2(v0, v1);
+                    }
+                }
+                if (q - 1 >= it.plo) {   // p_j plane q-1 is no longer needed
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&emptyp[(pbase + (uint32_t)(q - 1 - it.plo)) & (NSP - 1)]);
+                }
+                Pm = P0;
+                P0 = Pp;
+                if (q + 2 <= it.phi) Pp = slotp(q + 2);
+            }
+            for (int z = max(it.zhi, it.plo); z <= it.phi; ++z) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyp[(pbase + (uint32_t)(z - it.plo)) & (NSP - 1)]);
+            }
+            pc = pbase + (it.phi - it.plo + 1);
+        }
+        return;
+    }
     for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
         const ItemPlan it = plan_item(wk, item);
         const int x0 = it.tx * TX, y0 = it.ty * TY;
@@ -246,7 +362,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (wf && q >= it.zlo && q < it.zhi) {   // the tile's own cells: w_j, p_{j+1} to HBM
                         const int64_t i = (int64_t)q * pl + gif;
                         if (!v1f) Ap.y = 0.0;
-                        __stcs(reinterpret_cast<double2 *>(a.w + i), Ap);
+                        if (!a.skip_w) __stcs(reinterpret_cast<double2 *>(a.w + i), Ap);
                         *reinterpret_cast<double2 *>(a.pn + i) = u;
                     }
                 }
@@ -286,7 +402,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 if (!v1b) Ap.y = 0.0;
                 const int64_t i = (int64_t)z * pl + gib;
-                __stcs(reinterpret_cast<double2 *>(a.w2 + i), Ap);
+                if (!a.skip_w2) __stcs(reinterpret_cast<double2 *>(a.w2 + i), Ap);
                 if (wk.back_pn) {
                     const double2 pj = lds2(sp + ((cq - 1) % NSP) * PS + ob);   // p_j(z)
                     const double v0 = cbk * (dinv_c * Ap.x - sigma * c.x) - pj.x;
@@ -380,7 +496,7 @@ void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevSta
     wk.dinv_c = g.dinv_c;
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
     // one CTA per SM (fewer with a.sm_cap: SMs left to the overlapped NCCL exchange)
-    const int64_t resident = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
+    const int64_t resident = (int64_t)MINB * ((a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid());
     static int zc_env = -1;
     if (zc_env < 0) {
         const char *e = getenv("SSCG_K1_ZC");

@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(THREADS, KIND >= 3 ? 1 : 2)
                 ++mc;
             }
             if (sa) {
-                __stcs(reinterpret_cast<double2 *>(a.w + ia), Apa);
+                if (!a.skip_w) __stcs(reinterpret_cast<double2 *>(a.w + ia), Apa);
                 if (a.mode >= 1) {
                     const double2 dv = a.dinv ? __ldg(reinterpret_cast<const double2 *>(a.dinv + ia))
                                        : (KIND >= 3) ? make_double2(1.0 / Da.x, in1 ? 1.0 / Da.y : 0.0)
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(THREADS, KIND >= 3 ? 1 : 2)
             }
             if (sb) {
                 const int64_t ib = ia + g.pitch;
-                __stcs(reinterpret_cast<double2 *>(a.w + ib), Apb);
+                if (!a.skip_w) __stcs(reinterpret_cast<double2 *>(a.w + ib), Apb);
                 if (a.mode >= 1) {
                     const double2 dv = a.dinv ? __ldg(reinterpret_cast<const double2 *>(a.dinv + ib))
                                        : (KIND >= 3) ? make_double2(1.0 / Db.x, in1 ? 1.0 / Db.y : 0.0)

@@ -362,6 +362,10 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
             CU(cudaGetLastError());
             sl.dvec = dd;
         }
+        if (A->kind == SSCG_OP_STENCIL7 || A->kind == SSCG_OP_STENCIL27 || A->kind == SSCG_OP_VARCOEF7) {
+            if (!k2r_prepare(g, sl, s)) return fail(SSCG_ERR_CUDA, "tensor maps for the recovered-W Gram pass");
+            sl.has_k2r = true;
+        }
     }
     TRY(dalloc(c, &c->blk, (size_t)nent));
     TRY(dalloc(c, &c->xdev, 1));
@@ -564,6 +568,33 @@ static sscg_status halo_join(sscg_ctx *c)
     return SSCG_OK;
 }
 
+// K5 forms W alpha from the Chebyshev recurrence (DESIGN.md R21) for the
+// constant-coefficient stencils with M = diag(A) and a Chebyshev basis
+// (SSCG_K5_RECUR=0 keeps the stored-W form everywhere)
+static bool uses_rec_update(const sscg_ctx *c)
+{
+    const char *e = getenv("SSCG_K5_RECUR");
+    if (e && e[0] == '0') return false;
+    const Geo &g = c->g;
+    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2 || g.kind == SSCG_OP_CSR || g.pitch != g.nx) return false;
+    for (const auto &sl : c->slabs)
+        if (!sl.dvec && !(g.center > 0.0 && !sl.dinv)) return false;   // need m or diag(M) per point
+    return true;
+}
+
+// W = AP is not stored (except w_{s-1}) and the Gram pass recovers it from the
+// basis recurrence (K2R, R23) when the basis kernels are K1T/K1F
+// and the basis is Chebyshev (SSCG_WFREE=0 keeps the stored-W schedule)
+static bool uses_wfree(const sscg_ctx *c)
+{
+    const char *e = getenv("SSCG_WFREE");
+    if (e && e[0] == '0') return false;
+    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2) return false;
+    for (const auto &sl : c->slabs)
+        if (!sl.has_k2r || !sl.has_k1t) return false;
+    return uses_rec_update(c);   // the update must not need the stored W either
+}
+
 // K1 for step j over the planes of every local slab selected by `part`:
 //   0 = all planes, 1 = the two boundary planes (1 and nzl), 2 = the interior
 //   planes [2, nzl) that do not read a halo plane
@@ -590,6 +621,7 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
         }
         a.nzl = sl.nzl;
         a.j = j;
+        a.skip_w = (uses_wfree(c) && j < s - 1) ? 1 : 0;
         if (sl.has_k1t) {
             a.tmP4 = &sl.tmP4;
             a.tmM4 = &sl.tmM4;
@@ -629,20 +661,6 @@ static bool uses_fused(const sscg_ctx *c)
     return true;
 }
 
-// K5 forms W alpha from the Chebyshev recurrence (DESIGN.md R21) for the
-// constant-coefficient stencils with M = diag(A) and a Chebyshev basis
-// (SSCG_K5_RECUR=0 keeps the stored-W form everywhere)
-static bool uses_rec_update(const sscg_ctx *c)
-{
-    const char *e = getenv("SSCG_K5_RECUR");
-    if (e && e[0] == '0') return false;
-    const Geo &g = c->g;
-    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2 || g.kind == SSCG_OP_CSR || g.pitch != g.nx) return false;
-    for (const auto &sl : c->slabs)
-        if (!sl.dvec && !(g.center > 0.0 && !sl.dinv)) return false;   // need m or diag(M) per point
-    return true;
-}
-
 // K1F: basis steps j, j+1 in one launch per slab, over all planes (part 0,
 // a slab bounded by the global Dirichlet planes) or the planes [2, nzl) that
 // need no halo of p_{j+1} (part 2)
@@ -660,6 +678,8 @@ static sscg_status launch_basis_pair(sscg_ctx *c, int j, int part)
         a.pn2 = (j + 2 < s) ? sl.P + (int64_t)(j + 2) * g.vstride : nullptr;
         a.sigma = c->sigma;
         a.nzl = sl.nzl;
+        a.skip_w = uses_wfree(c) ? 1 : 0;                         // j <= s-2 here
+        a.skip_w2 = (uses_wfree(c) && j + 1 < s - 1) ? 1 : 0;
         a.zb = (part == 0) ? 1 : 2;
         a.ze = (part == 0) ? sl.nzl + 1 : sl.nzl;
         if (part == 2) a.sm_cap = c->k1_sm_cap;
@@ -715,9 +735,11 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     }
     nvtxRangePop();
     nvtxRangePushA("gram+allreduce+fgs");
+    const bool wfree = uses_wfree(c);
     for (auto &sl : c->slabs) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
-        launch_k2(g, sl, s, c->st, L == 1 ? c->blk : sl.blk, c->stream);
+        if (wfree) launch_k2r(g, sl, s, c->theta, c->sigma, c->st, L == 1 ? c->blk : sl.blk, c->stream);
+        else launch_k2(g, sl, s, c->st, L == 1 ? c->blk : sl.blk, c->stream);
         TRY(prof_mark(c, SSCG_PROF_GRAM, false));
         ++c->launches;
     }
@@ -1052,7 +1074,9 @@ extern "C" sscg_status sscg_inspect(const sscg_ctx *cc, int32_t what, int32_t in
         if (index < 0 || index >= s) return fail(SSCG_ERR_INVALID, "column %d out of range", index);
         if (!need(c->n_local * 8)) return fail(SSCG_ERR_INVALID, "buffer too small");
         for (auto &sl : c->slabs) {
-            const double *v = (what == SSCG_INSPECT_P ? sl.P : sl.W) + (int64_t)index * g.vstride;
+            double *v = (what == SSCG_INSPECT_P ? sl.P : sl.W) + (int64_t)index * g.vstride;
+            if (what == SSCG_INSPECT_W && uses_wfree(c) && index < s - 1)   // not stored: recover it (R23)
+                launch_wrec(g, sl, index, c->theta, c->sigma, v, c->stream);
             launch_unpack(g, v, c->scratch + sl.zoff * (int64_t)g.nx * g.ny, sl.nzl, c->stream);
         }
         CU(cudaGetLastError());
@@ -1329,20 +1353,26 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
         return SSCG_OK;
     case SSCG_QUERY_BASIS_VECTORS: {
         // FP64 vectors of n_local read + written by the basis steps of one outer
+        const bool wf = uses_wfree(c);
+        auto wst = [&](int j) { return (!wf || j == s - 1) ? 1 : 0; };   // w_j stored?
         int64_t v = 0;
         if (uses_fused(c)) {
             int j = 0;
-            for (; j + 1 < s; j += 2) v += 1 + (j > 0) + 3 + (j + 2 < s);
+            for (; j + 1 < s; j += 2) v += 1 + (j > 0) + 1 + (j + 2 < s) + wst(j) + wst(j + 1);
             if (j < s) v += 2;   // odd s: the last step alone (mode 0: reads p_{s-1}, writes w_{s-1})
         } else {
             for (int j = 0; j < s; ++j) {
                 const bool pn = j < s - 1, pm = !mono && j > 0 && pn;
-                v += 1 + pm + 1 + pn;
+                v += 1 + pm + wst(j) + pn;
             }
         }
         *out = v;
         return SSCG_OK;
     }
+    case SSCG_QUERY_GRAM_VECTORS:
+        // stored W: P and W (2s); recovered W: P, w_{s-1} and diag(M) when it varies
+        *out = uses_wfree(c) ? (int64_t)s + 1 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s;
+        return SSCG_OK;
     case SSCG_QUERY_UPDATE_VECTORS:
         // P (s) + x in, x + r out; the stored-W form also reads W (s), the
         // recurrence form only w_{s-1}

@@ -45,6 +45,8 @@ struct Slab {
     CUtensorMap tmP, tmW;         // K2: [s rows x interior] views of P and W
     CUtensorMap tmPd, tmWd;       // K2D (DMMA Gram, s > 16): same views, box pitch 132/68
     bool has_k2d;
+    CUtensorMap tmWl, tmDv;       // K2R: the row w_{s-1} of W, diag(M) (one row)
+    bool has_k2r;
     CUtensorMap tmP4, tmM4;       // K1T: 4-D [x][y][plane][vector] views of P (halo box / tile box)
     bool has_k1t;
     CUtensorMap tmF_P, tmF_M;     // K1F: 2-cell / 1-cell halo boxes
@@ -89,6 +91,8 @@ struct K1Args {
     int mode;
     int nzl;
     int j;                 // basis step (K1T: vector coordinate of p_j in the tensor maps)
+    int skip_w;            // 1: w_j is not stored (the Gram pass recovers it, R23; K1T/K1F)
+    int skip_w2;           // K1F: same for w_{j+1}
     const CUtensorMap *tmP4, *tmM4;   // K1T tensor maps of this slab (host memory), or nullptr
     const CUtensorMap *tmKX, *tmKY, *tmKZ;   // K1T variable-coefficient face maps, or nullptr
     double *w2, *pn2;                 // K1F: w_{j+1}, p_{j+2} (nullptr at j+1 = s-1)
@@ -123,6 +127,12 @@ bool k2_prepare(const Geo &g, Slab &sl, int s);   // encode the TMA tensor maps
 int k2_num_entries(int s);
 // K2D: the Gram pass on FP64 tensor cores (k_gram_dmma.cu), s > 16 by default
 bool k2d_enabled(int s);
+// K2R: DMMA Gram pass recovering W = AP from the basis recurrence (W not stored, R23)
+bool k2r_prepare(const Geo &g, Slab &sl, int s);
+void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma, const DevState *st, double *out_blk,
+                cudaStream_t stream);
+// w_j (j < s-1) from the recurrence into `out` (a vector in the padded layout) -- parity hooks
+void launch_wrec(const Geo &g, const Slab &sl, int j, double theta, double sigma, double *out, cudaStream_t stream);
 bool k2d_prepare(const Geo &g, Slab &sl, int s);
 void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk, cudaStream_t stream);
 
