@@ -26,8 +26,10 @@
 namespace sscg {
 namespace {
 
-constexpr int NCW = 8;                 // consumer warps
-constexpr int THREADS = 32 * (NCW + 1);
+// consumer warps: 16 while the accumulators are small (s <= 32), 8 above
+// (register budget); one producer warp
+__host__ __device__ constexpr int ncw_for(int nb) { return nb >= 5 ? 8 : 16; }
+__host__ __device__ constexpr int threads_for(int nb) { return 32 * (ncw_for(nb) + 1); }
 constexpr int MAXS = 8;                // ring stages
 
 struct K2DParams {
@@ -47,12 +49,13 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 }
 
 template <int NB, int EP>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(threads_for(NB), 1)
     k2d(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW, K2DParams k,
         const DevState *st)
 {
     if (st && st->done) return;
     constexpr int SP = 8 * NB;                 // rows per box
+    constexpr int NCW = ncw_for(NB), THREADS = threads_for(NB);
     constexpr int KS = EP / 4;                 // k-steps per stage
     constexpr int NT = NB * (NB + 1) / 2;      // upper-triangle tiles
     extern __shared__ __align__(1024) double smem[];
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid == 0) {
         for (int i = 0; i < NS; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], NCW);
+            mbar_init(&empty[i], NCW / min(NS, NCW));
         }
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
@@ -104,15 +107,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else {
         const int cw = warp - 1;
         const int r = lane >> 2, kk = lane & 3;   // fragment row (m or n) and k index
-        for (int it = 0; it < nit; ++it) {
+        // warps form min(NS, NCW) groups; group g takes stages g, g + ngroups, ...
+        // and its wpg warps split the k-steps of a stage
+        const int ngroups = min(NS, NCW), wpg = NCW / ngroups;
+        const int grp = cw / wpg, wig = cw - grp * wpg;
+        for (int it = (grp < ngroups ? grp : nit); it < nit; it += ngroups) {
             const int stg = it % NS;
             mbar_wait(&full[stg], (uint32_t)((it / NS) & 1));
             const double *sP = smem + (size_t)stg * stage_elems;
             const double *sW = sP + SP * EP;
-            for (int ks0 = cw; ks0 < KS; ks0 += NCW * U) {
+            for (int ks0 = wig; ks0 < KS; ks0 += wpg * U) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int ks = ks0 + u * NCW;
+                    const int ks = ks0 + u * wpg;
                     if (ks >= KS) break;
                     const int o = r * EP + ks * 4 + kk;
                     double a[NB], b[NB];
@@ -206,12 +213,13 @@ struct K2RParams {
 };
 
 template <int NB, int EP, bool VARM>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(threads_for(NB), 1)
     k2r(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmWl,
         const __grid_constant__ CUtensorMap tmDv, K2RParams k, const DevState *st)
 {
     if (st && st->done) return;
     constexpr int SP = 8 * NB;
+    constexpr int NCW = ncw_for(NB), THREADS = threads_for(NB);
     constexpr int KS = EP / 4;
     constexpr int NT = NB * (NB + 1) / 2;
     extern __shared__ __align__(1024) double smem[];
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid == 0) {
         for (int i = 0; i < NS; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], NCW);
+            mbar_init(&empty[i], NCW / min(NS, NCW));
         }
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
@@ -265,6 +273,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else {
         const int cw = warp - 1;
         const int r = lane >> 2, kk = lane & 3;
+        const int ngroups = min(NS, NCW), wpg = NCW / ngroups;   // as in k2d
+        const int grp = cw / wpg, wig = cw - grp * wpg;
         // per-lane recurrence coefficients of fragment row j = J*8 + r (fixed for the kernel):
         //   w = m (up c1 + dn c2 + sigma p_j)  (j <= s-2),  w = w_{s-1} (stored),  0 (j >= s)
         double c1[NB], c2[NB], cs[NB], use_wl[NB];
@@ -277,15 +287,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             cs[J] = rec ? k.sigma : 0.0;
             use_wl[J] = (j == s - 1) ? 1.0 : 0.0;
         }
-        for (int it = 0; it < nit; ++it) {
+        for (int it = (grp < ngroups ? grp : nit); it < nit; it += ngroups) {
             const int stg = it % NS;
             mbar_wait(&full[stg], (uint32_t)((it / NS) & 1));
             const double *sP = smem + (size_t)stg * stage_elems;
             const double *sWl = sP + SP * EP, *sDv = sWl + k.wlp;
-            for (int ks0 = cw; ks0 < KS; ks0 += NCW * U) {
+            for (int ks0 = wig; ks0 < KS; ks0 += wpg * U) {
 #pragma unroll
               for (int u = 0; u < U; ++u) {
-                const int ks = ks0 + u * NCW;
+                const int ks = ks0 + u * wpg;
                 if (ks >= KS) break;
                 const int pt = ks * 4 + kk;
                 const int o = r * EP + pt;
@@ -297,12 +307,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const double m = VARM ? sDv[pt] : k.dm;
 #pragma unroll
                 for (int J = 0; J < NB; ++J) {
-                    // row J*8+r+1: lane+4 (same block) or, for r = 7, block J+1 row 0
-                    const double su = (r == 0) ? ((J + 1 < NB) ? a[J + 1 < NB ? J + 1 : J] : 0.0) : a[J];
-                    const double up = __shfl_sync(0xffffffffu, su, (lane + 4) & 31);
-                    // row J*8+r-1: lane-4 (same block) or, for r = 0, block J-1 row 7
-                    const double sd = (r == 7) ? ((J > 0) ? a[J > 0 ? J - 1 : 0] : 0.0) : a[J];
-                    const double dn = __shfl_sync(0xffffffffu, sd, (lane + 28) & 31);
+                    // rows j+1 and j-1 of the staged P (pitch EP keeps the fragment loads
+                    // conflict-free); row -1 / row s_pad read neighbouring smem whose
+                    // values are discarded by the selects
+                    const double up = sP[o + J * 8 * EP + EP];
+                    const double dn0 = sP[o + J * 8 * EP - EP];
+                    const double dn = (c2[J] != 0.0) ? dn0 : 0.0;
                     const double w = m * fma(up, c1[J], fma(dn, c2[J], cs[J] * a[J]));
                     b[J] = (use_wl[J] != 0.0) ? wl : w;   // branch-free select
                 }
@@ -425,17 +435,17 @@ void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double 
     const int gx = (int)std::min<int64_t>(k2_grid(), nchunks);
     const int nt = nb * (nb + 1) / 2;
     const size_t ring = (size_t)k.nstage * 2 * s_pad * ep * sizeof(double);
-    const size_t red = (size_t)(NCW * nt * 64 + NCW * s_pad) * sizeof(double);   // cross-warp reduction
+    const size_t red = (size_t)(ncw_for(nb) * nt * 64 + ncw_for(nb) * s_pad) * sizeof(double);   // cross-warp reduction
     const size_t sm = std::max(ring, red);
     switch (nb) {
-    case 1: k2d<1, 132><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 2: k2d<2, 132><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 3: k2d<3, 132><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 4: k2d<4, 132><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 5: k2d<5, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 6: k2d<6, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 7: k2d<7, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    default: k2d<8, 68><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 1: k2d<1, 132><<<gx, threads_for(1), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 2: k2d<2, 132><<<gx, threads_for(2), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 3: k2d<3, 132><<<gx, threads_for(3), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 4: k2d<4, 132><<<gx, threads_for(4), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 5: k2d<5, 68><<<gx, threads_for(5), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 6: k2d<6, 68><<<gx, threads_for(6), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 7: k2d<7, 68><<<gx, threads_for(7), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    default: k2d<8, 68><<<gx, threads_for(8), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
     }
 }
 
@@ -507,12 +517,12 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     const int64_t nchunks = (k.N + ep - 1) / ep;
     const int gx = (int)std::min<int64_t>(k2_grid(), nchunks);
     const int nt = nb * (nb + 1) / 2;
-    const size_t red = (size_t)(NCW * nt * 64 + NCW * s_pad) * sizeof(double);
+    const size_t red = (size_t)(ncw_for(nb) * nt * 64 + ncw_for(nb) * s_pad) * sizeof(double);
     const size_t sm = std::max((size_t)k.nstage * stage, red);
     const CUtensorMap &dv = varm ? sl.tmDv : sl.tmWl;
 #define K2R_LAUNCH(NB, EP)                                                                                   \
-    if (varm) k2r<NB, EP, true><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWl, dv, k, st);                    \
-    else k2r<NB, EP, false><<<gx, THREADS, sm, stream>>>(sl.tmPd, sl.tmWl, dv, k, st);
+    if (varm) k2r<NB, EP, true><<<gx, threads_for(NB), sm, stream>>>(sl.tmPd, sl.tmWl, dv, k, st);          \
+    else k2r<NB, EP, false><<<gx, threads_for(NB), sm, stream>>>(sl.tmPd, sl.tmWl, dv, k, st);
     switch (nb) {
     case 1: K2R_LAUNCH(1, 132) break;
     case 2: K2R_LAUNCH(2, 132) break;

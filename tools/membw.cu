@@ -67,7 +67,10 @@ int main()
     run<1, 2>(in, out, n2, stride2, sms);    // K1F (per step)
     run<2, 4>(in, out, n2, stride2, sms);    // K1F (per pair)
     run<5, 2>(in, out, n2, stride2, sms);    // K1T variable coefficients (3 face streams)
+    run<2, 1>(in, out, n2, stride2, sms);    // K1T, W not stored (W-free schedule)
     run<16, 0>(in, out, n2, stride2, sms);
+    run<18, 0>(in, out, n2, stride2, sms);   // K2R (s = 16: 17 basis + w_last)
+    run<18, 2>(in, out, n2, stride2, sms);   // K5, W-free schedule (s = 16)
     run<32, 0>(in, out, n2, stride2, sms);   // K2 (s = 16)
     run<33, 2>(in, out, n2, stride2, sms);   // K5 (s = 16)
     return 0;
