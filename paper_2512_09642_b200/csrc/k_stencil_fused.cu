@@ -44,7 +44,9 @@ constexpr int BHM = TY + 2;                // p_{j-1}: y in [y0-1, y0+TY+1)
 constexpr int PS = ((BW * BHP * 8 + 127) / 128) * 128 / 8;   // doubles per p_j / U slot (128-B multiple)
 constexpr int MS = ((BW * BHM * 8 + 127) / 128) * 128 / 8;
 constexpr int NSP = 8, NSM = 6, NU = 4;   // NSP, NU powers of two (slot = seq & (N - 1))
-constexpr int NCW = ((TY + 2) * (BW / 2) + 31) / 32;   // one front task per consumer thread
+// one front task per consumer thread (27-point), or TY+2 row warps plus the
+// halo-column warps (7-point)
+constexpr int NCW = std::max(((TY + 2) * (BW / 2) + 31) / 32, (TY + 2) + (2 * (TY + 2) + 31) / 32);
 constexpr int NCT = NCW * 32;
 constexpr int THREADS = NCT + 32;
 constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = BW * BHM * 8;
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     double *sp = smem;                       // p_j ring
     double *sm = smem + NSP * PS;            // p_{j-1} ring
     double *su = sm + NSM * MS;              // U = p_{j+1} on tile + halo, NU planes
-    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM];
+    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM], ufull[NU];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int i = 0; i < NSP; ++i) {
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             mbar_init(&fullm[i], 1);
             mbar_init(&emptym[i], NCW);
         }
+        for (int i = 0; i < NU; ++i) mbar_init(&ufull[i], NCW);
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
         tma_prefetch_desc(&tmM);
@@ -189,110 +192,139 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const double center = wk.center, dinv_c = wk.dinv_c, sigma = wk.sigma;
     const double cfr = wk.coef_front, cbk = wk.coef_back;
     if (KIND == 1) {
-        // 7-point: streamlined plane loop (rotating slot pointers, pointer
-        // increments along z, parameters in registers); same arithmetic as below
+        // 7-point: row-aligned tasks with the z-column in registers.  Warps
+        // 1..TY+2 take box row r = warp and the tile's 32 pairs c = 2 + 2*lane;
+        // the warps after them the halo pairs c = 0 and c = TX+2 of rows
+        // 1..TY+2.  Each task's front and back cell are the same cell, so
+        // p_j(q-1), p_j(q), u(z-1), u(z) and u(q) at the own cell roll through
+        // registers along z and only the in-plane neighbours come from shared
+        // memory.  U(q) is published per warp through ufull (split barrier: a
+        // warp waits for U(q-1) of all warps, not for everyone's U(q)); with
+        // NU = 4 slots a warp that waited U(q-2) knows every read of U(q-4)
+        // is done before it overwrites that slot.
+        int rk, ck;
+        bool task;
+        if (warp <= TY + 2) {
+            rk = warp;
+            ck = 2 + 2 * lane;
+            task = true;
+        } else {
+            const int h = (warp - TY - 3) * 32 + lane;
+            task = h < 2 * (TY + 2);
+            rk = task ? 1 + (h >> 1) : 1;
+            ck = (h & 1) ? TX + 2 : 0;
+        }
+        const int ok = rk * BW + ck, omk = (rk - 1) * BW + ck;
+        const bool ownk = task && rk >= 2 && rk < TY + 2 && ck >= 2 && ck < TX + 2;
+        const bool lgk = ck > 0, rgk = ck + 2 < BW;
         const bool skip_w = a.skip_w, skip_w2 = a.skip_w2, back_pn = wk.back_pn, front_pm = wk.front_pm;
         double *const gw = a.w, *const gpn = a.pn, *const gw2 = a.w2, *const gpn2 = a.pn2;
         const int nzl = wk.nzl;
+        uint32_t uc = 0;   // sequence number of the next U plane (slot uc % NU)
         for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
             const ItemPlan it = plan_item(wk, item);
             const int x0 = it.tx * TX, y0 = it.ty * TY;
-            const int gxf = x0 - 2 + cf, gyf = y0 - 2 + rf, gxb = x0 - 2 + cb, gyb = y0 - 2 + rb;
-            const bool vyf = gyf >= 0 && gyf < g.ny;
-            const bool v0f = has_f && vyf && gxf >= 0 && gxf < g.nx, v1f = has_f && vyf && gxf + 1 >= 0 && gxf + 1 < g.nx;
-            const bool wf = own_cell && v0f;
-            const bool wb = has_b && gyb < g.ny && gxb < g.nx, v1b = gxb + 1 < g.nx;
-            const uint32_t pbase = pc;   // sequence number of plane plo
-            // slot pointers of planes q-1, q, q+1 (seq = pbase + z - plo)
+            const int gx = x0 - 2 + ck, gy = y0 - 2 + rk;
+            const bool vy = gy >= 0 && gy < g.ny;
+            const bool v0 = task && vy && gx >= 0 && gx < g.nx, v1 = task && vy && gx + 1 >= 0 && gx + 1 < g.nx;
+            const bool wown = ownk && v0;   // the tile's own cell: all four outputs go to HBM
+            const uint32_t pbase = pc;      // sequence number of plane plo
             auto slotp = [&](int z) -> const double * {
                 return sp + ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1)) * PS;
             };
-            // wait the planes front(zlo-1) needs: plo .. min(zlo, phi)
+            auto release = [&](int z) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyp[(pbase + (uint32_t)(z - it.plo)) & (NSP - 1)]);
+            };
             for (int z = it.plo; z <= min(it.zlo, it.phi); ++z) {
                 const uint32_t c = pbase + (uint32_t)(z - it.plo);
                 mbar_wait(&fullp[c & (NSP - 1)], (c / NSP) & 1);
             }
-            const double *Pm = (it.zlo - 2 >= it.plo) ? slotp(it.zlo - 2) : sp;   // plane q-1
-            const double *P0 = slotp(it.zlo - 1);                                  // plane q
-            const double *Pp = slotp(it.zlo);                                      // plane q+1
-            int64_t off_f = (int64_t)(it.zlo - 1) * pl + (int64_t)gyf * g.pitch + gxf;   // global index, plane q
-            int64_t off_b = (int64_t)(it.zlo - 2) * pl + (int64_t)gyb * g.pitch + gxb;   // plane z = q-1
-            for (int q = it.zlo - 1; q <= it.zhi; ++q, off_f += pl, off_b += pl) {
-                if (q >= it.zlo && q + 1 <= it.phi) {   // plane q+1 (front(q) needs it)
-                    const uint32_t c = pbase + (uint32_t)(q + 1 - it.plo);
-                    mbar_wait(&fullp[c & (NSP - 1)], (c / NSP) & 1);
-                }
-                double *U = su + ((q + 8) & (NU - 1)) * PS;
+            double2 pdn = make_double2(0.0, 0.0);   // p_j(q-1), own cell
+            if (it.zlo - 2 >= it.plo) {
+                pdn = lds2(slotp(it.zlo - 2) + ok);
+                release(it.zlo - 2);
+            }
+            double2 pc0 = lds2(slotp(it.zlo - 1) + ok);   // p_j(q)
+            double2 um2 = make_double2(0.0, 0.0), um1 = make_double2(0.0, 0.0);   // u(q-2), u(q-1)
+            const double *P0 = slotp(it.zlo - 1);
+            int64_t off = (int64_t)(it.zlo - 1) * pl + (int64_t)gy * g.pitch + gx;   // global index, plane q
+            for (int q = it.zlo - 1; q <= it.zhi; ++q, off += pl) {
                 const bool inside = q >= 1 && q <= nzl;
+                double2 pup = make_double2(0.0, 0.0);   // p_j(q+1)
+                if (q + 1 <= it.phi) {
+                    if (q >= it.zlo) {
+                        const uint32_t c = pbase + (uint32_t)(q + 1 - it.plo);
+                        mbar_wait(&fullp[c & (NSP - 1)], (c / NSP) & 1);
+                    }
+                    pup = lds2(slotp(q + 1) + ok);
+                }
                 const bool mloaded = front_pm && q >= it.mlo && q <= it.mhi;
                 const double *M = sm + (mc % NSM) * MS;
                 if (mloaded) mbar_wait(&fullm[mc % NSM], (mc / NSM) & 1);
-                if (has_f) {
-                    double2 u = make_double2(0.0, 0.0);
-                    if (inside) {
-                        const double2 c = lds2(P0 + of);
-                        const double2 dn = lds2(Pm + of), up = lds2(Pp + of);
-                        const double2 ylo = lds2(P0 + of - BW), yhi = lds2(P0 + of + BW);
-                        const double l = lgf ? P0[of - 1] : 0.0;
-                        const double rr = rgf ? P0[of + 2] : 0.0;
-                        double2 Ap;
-                        Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
-                        Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
-                        u.x = cfr * (dinv_c * Ap.x - sigma * c.x);
-                        u.y = cfr * (dinv_c * Ap.y - sigma * c.y);
-                        if (mloaded) {
-                            const double2 pm = lds2(M + omf);
-                            u.x -= pm.x;
-                            u.y -= pm.y;
-                        }
-                        if (!v0f) u.x = 0.0;
-                        if (!v1f) u.y = 0.0;
-                        if (wf && q >= it.zlo && q < it.zhi) {
-                            if (!v1f) Ap.y = 0.0;
-                            if (!skip_w) __stcs(reinterpret_cast<double2 *>(gw + off_f), Ap);
-                            *reinterpret_cast<double2 *>(gpn + off_f) = u;
-                        }
-                    }
-                    *reinterpret_cast<double2 *>(U + of) = u;
-                }
-                if (mloaded) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&emptym[mc % NSM]);
-                    ++mc;
-                }
-                consumers_sync();   // U(q) complete; U(q-4) no longer read
-                const int z = q - 1;
-                if (wb && z >= it.zlo && z < it.zhi) {
-                    const double *Um = su + ((z + 7) & (NU - 1)) * PS, *U0 = su + ((z + 8) & (NU - 1)) * PS;
-                    const double2 c = lds2(U0 + ob);
-                    const double2 dn = lds2(Um + ob), up = lds2(U + ob);
-                    const double2 ylo = lds2(U0 + ob - BW), yhi = lds2(U0 + ob + BW);
-                    const double l = U0[ob - 1], rr = U0[ob + 2];
+                // ---------------- front(q): step j on tile + halo ----------------
+                double2 u = make_double2(0.0, 0.0);
+                if (inside) {
+                    const double2 c = pc0, dn = pdn, up = pup;
+                    const double2 ylo = lds2(P0 + ok - BW), yhi = lds2(P0 + ok + BW);
+                    const double l = lgk ? P0[ok - 1] : 0.0;
+                    const double rr = rgk ? P0[ok + 2] : 0.0;
                     double2 Ap;
                     Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
                     Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
-                    if (!v1b) Ap.y = 0.0;
-                    if (!skip_w2) __stcs(reinterpret_cast<double2 *>(gw2 + off_b), Ap);
-                    if (back_pn) {
-                        const double2 pj = lds2(Pm + ob);   // p_j(z), z = q-1
-                        const double v0 = cbk * (dinv_c * Ap.x - sigma * c.x) - pj.x;
-                        double v1 = cbk * (dinv_c * Ap.y - sigma * c.y) - pj.y;
-                        if (!v1b) v1 = 0.0;
-                        *reinterpret_cast<double2 *>(gpn2 + off_b) = make_double2(v0, v1);
+                    u.x = cfr * (dinv_c * Ap.x - sigma * c.x);
+                    u.y = cfr * (dinv_c * Ap.y - sigma * c.y);
+                    if (mloaded) {
+                        const double2 pm = lds2(M + omk);
+                        u.x -= pm.x;
+                        u.y -= pm.y;
+                    }
+                    if (!v0) u.x = 0.0;
+                    if (!v1) u.y = 0.0;
+                    if (wown && q >= it.zlo && q < it.zhi) {
+                        if (!v1) Ap.y = 0.0;
+                        if (!skip_w) __stcs(reinterpret_cast<double2 *>(gw + off), Ap);
+                        *reinterpret_cast<double2 *>(gpn + off) = u;
                     }
                 }
-                if (q - 1 >= it.plo) {   // p_j plane q-1 is no longer needed
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&emptyp[(pbase + (uint32_t)(q - 1 - it.plo)) & (NSP - 1)]);
-                }
-                Pm = P0;
-                P0 = Pp;
-                if (q + 2 <= it.phi) Pp = slotp(q + 2);
-            }
-            for (int z = max(it.zhi, it.plo); z <= it.phi; ++z) {
+                double *U = su + (uc & (NU - 1)) * PS;
+                if (task) *reinterpret_cast<double2 *>(U + ok) = u;
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyp[(pbase + (uint32_t)(z - it.plo)) & (NSP - 1)]);
+                if (lane == 0) {
+                    mbar_arrive(&ufull[uc & (NU - 1)]);
+                    if (mloaded) mbar_arrive(&emptym[mc % NSM]);
+                }
+                if (mloaded) ++mc;
+                if (q >= it.plo) release(q);   // p_j plane q is done (front(q+1) reads q+1, q+2)
+                // ---------------- back(z = q-1): step j+1 on the tile ----------------
+                if (uc > 0) mbar_wait(&ufull[(uc - 1) & (NU - 1)], ((uc - 1) / NU) & 1);
+                const int z = q - 1;
+                if (wown && z >= it.zlo && z < it.zhi) {
+                    const double *U0 = su + ((uc - 1) & (NU - 1)) * PS;
+                    const double2 c = um1, dn = um2, up = u;
+                    const double2 ylo = lds2(U0 + ok - BW), yhi = lds2(U0 + ok + BW);
+                    const double l = U0[ok - 1], rr = U0[ok + 2];
+                    double2 Ap;
+                    Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                    Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+                    if (!v1) Ap.y = 0.0;
+                    if (!skip_w2) __stcs(reinterpret_cast<double2 *>(gw2 + off - pl), Ap);
+                    if (back_pn) {
+                        const double2 pj = pdn;   // p_j(z)
+                        const double v0b = cbk * (dinv_c * Ap.x - sigma * c.x) - pj.x;
+                        double v1b = cbk * (dinv_c * Ap.y - sigma * c.y) - pj.y;
+                        if (!v1) v1b = 0.0;
+                        *reinterpret_cast<double2 *>(gpn2 + off - pl) = make_double2(v0b, v1b);
+                    }
+                }
+                ++uc;
+                um2 = um1;
+                um1 = u;
+                pdn = pc0;
+                pc0 = pup;
+                if (q + 1 <= it.phi) P0 = slotp(q + 1);
             }
+            if (it.zhi + 1 <= it.phi) release(it.zhi + 1);
             pc = pbase + (it.phi - it.plo + 1);
         }
         return;
