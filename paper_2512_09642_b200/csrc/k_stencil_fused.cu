@@ -131,15 +131,17 @@ __global__ void __launch_bounds__(THREADS, MINB)
     __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM], ufull[NU];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
+        // 7-point: every consumer thread arrives; 27-point: one arrival per warp
+        const int consumers = (KIND == 1) ? NCT : NCW;
         for (int i = 0; i < NSP; ++i) {
             mbar_init(&fullp[i], 1);
-            mbar_init(&emptyp[i], NCW);
+            mbar_init(&emptyp[i], consumers);
         }
         for (int i = 0; i < NSM; ++i) {
             mbar_init(&fullm[i], 1);
-            mbar_init(&emptym[i], NCW);
+            mbar_init(&emptym[i], consumers);
         }
-        for (int i = 0; i < NU; ++i) mbar_init(&ufull[i], NCW);
+        for (int i = 0; i < NU; ++i) mbar_init(&ufull[i], consumers);
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
         tma_prefetch_desc(&tmM);
@@ -221,6 +223,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
         double *const gw = a.w, *const gpn = a.pn, *const gw2 = a.w2, *const gpn2 = a.pn2;
         const int nzl = wk.nzl;
         uint32_t uc = 0;   // sequence number of the next U plane (slot uc % NU)
+        const uint32_t fp_a = smem_u32(fullp), ep_a = smem_u32(emptyp), fm_a = smem_u32(fullm),
+                       em_a = smem_u32(emptym), uf_a = smem_u32(ufull);
         for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
             const ItemPlan it = plan_item(wk, item);
             const int x0 = it.tx * TX, y0 = it.ty * TY;
@@ -232,14 +236,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
             auto slotp = [&](int z) -> const double * {
                 return sp + ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1)) * PS;
             };
-            auto release = [&](int z) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyp[(pbase + (uint32_t)(z - it.plo)) & (NSP - 1)]);
-            };
-            for (int z = it.plo; z <= min(it.zlo, it.phi); ++z) {
+            auto release = [&](int z) { mbar_arrive_a(ep_a + 8 * ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1))); };
+            auto waitp = [&](int z) {
                 const uint32_t c = pbase + (uint32_t)(z - it.plo);
-                mbar_wait(&fullp[c & (NSP - 1)], (c / NSP) & 1);
-            }
+                mbar_wait_a(fp_a + 8 * (c & (NSP - 1)), (c / NSP) & 1);
+            };
+            for (int z = it.plo; z <= min(it.zlo, it.phi); ++z) waitp(z);
             double2 pdn = make_double2(0.0, 0.0);   // p_j(q-1), own cell
             if (it.zlo - 2 >= it.plo) {
                 pdn = lds2(slotp(it.zlo - 2) + ok);
@@ -253,15 +255,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 const bool inside = q >= 1 && q <= nzl;
                 double2 pup = make_double2(0.0, 0.0);   // p_j(q+1)
                 if (q + 1 <= it.phi) {
-                    if (q >= it.zlo) {
-                        const uint32_t c = pbase + (uint32_t)(q + 1 - it.plo);
-                        mbar_wait(&fullp[c & (NSP - 1)], (c / NSP) & 1);
-                    }
+                    if (q >= it.zlo) waitp(q + 1);
                     pup = lds2(slotp(q + 1) + ok);
                 }
                 const bool mloaded = front_pm && q >= it.mlo && q <= it.mhi;
                 const double *M = sm + (mc % NSM) * MS;
-                if (mloaded) mbar_wait(&fullm[mc % NSM], (mc / NSM) & 1);
+                if (mloaded) mbar_wait_a(fm_a + 8 * (mc % NSM), (mc / NSM) & 1);
                 // ---------------- front(q): step j on tile + halo ----------------
                 double2 u = make_double2(0.0, 0.0);
                 if (inside) {
@@ -289,15 +288,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 }
                 double *U = su + (uc & (NU - 1)) * PS;
                 if (task) *reinterpret_cast<double2 *>(U + ok) = u;
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&ufull[uc & (NU - 1)]);
-                    if (mloaded) mbar_arrive(&emptym[mc % NSM]);
+                mbar_arrive_a(uf_a + 8 * (uc & (NU - 1)));
+                if (mloaded) {
+                    mbar_arrive_a(em_a + 8 * (mc % NSM));
+                    ++mc;
                 }
-                if (mloaded) ++mc;
                 if (q >= it.plo) release(q);   // p_j plane q is done (front(q+1) reads q+1, q+2)
                 // ---------------- back(z = q-1): step j+1 on the tile ----------------
-                if (uc > 0) mbar_wait(&ufull[(uc - 1) & (NU - 1)], ((uc - 1) / NU) & 1);
+                if (uc > 0) mbar_wait_a(uf_a + 8 * ((uc - 1) & (NU - 1)), ((uc - 1) / NU) & 1);
                 const int z = q - 1;
                 if (wown && z >= it.zlo && z < it.zhi) {
                     const double *U0 = su + ((uc - 1) & (NU - 1)) * PS;

@@ -52,6 +52,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
     }
 }
 
+// the same on a precomputed shared-window address (saves the generic ->
+// shared conversion per call inside hot loops)
+__device__ __forceinline__ void mbar_arrive_a(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t phase)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+}
+
 // 2-D tensor tile load global -> shared, completion counted on `bar`
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar)
 {
