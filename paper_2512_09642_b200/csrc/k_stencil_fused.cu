@@ -24,6 +24,7 @@
 // at the HBM write-heavy mix ceiling (1 read : 2 writes, profiles/r01e).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "sscg_internal.cuh"
 #include "tma.cuh"
@@ -43,7 +44,7 @@ constexpr int BHP = TY + 4;                // p_j: y in [y0-2, y0+TY+2)
 constexpr int BHM = TY + 2;                // p_{j-1}: y in [y0-1, y0+TY+1)
 constexpr int PS = ((BW * BHP * 8 + 127) / 128) * 128 / 8;   // doubles per p_j / U slot (128-B multiple)
 constexpr int MS = ((BW * BHM * 8 + 127) / 128) * 128 / 8;
-constexpr int NSP = 8, NSM = 6, NU = 4;   // NSP, NU powers of two (slot = seq & (N - 1))
+constexpr int NSP = 8, NSM = 8, NU = 4;   // powers of two (slot = seq & (N - 1))
 // one front task per consumer thread (27-point), or TY+2 row warps plus the
 // halo-column warps (7-point)
 constexpr int NCW = std::max(((TY + 2) * (BW / 2) + 31) / 32, (TY + 2) + (2 * (TY + 2) + 31) / 32);
@@ -77,6 +78,14 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, i
 }
 
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
+
+// an opaque copy: keeps a value the compiler would rematerialise in a register
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v)
+{
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
 
 __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 
@@ -200,10 +209,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
         // 1..TY+2.  Each task's front and back cell are the same cell, so
         // p_j(q-1), p_j(q), u(z-1), u(z) and u(q) at the own cell roll through
         // registers along z and only the in-plane neighbours come from shared
-        // memory.  U(q) is published per warp through ufull (split barrier: a
-        // warp waits for U(q-1) of all warps, not for everyone's U(q)); with
-        // NU = 4 slots a warp that waited U(q-2) knows every read of U(q-4)
-        // is done before it overwrites that slot.
+        // memory.  U(q) is published through ufull (split barrier: a thread
+        // waits for U(q-1) of all threads, not for everyone's U(q)); with
+        // NU = 4 slots a thread that waited U(q-2) knows every read of U(q-4)
+        // is done before it overwrites that slot.  Every consumer thread
+        // arrives on the mbarriers itself (no warp elect).
         int rk, ck;
         bool task;
         if (warp <= TY + 2) {
@@ -223,8 +233,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
         double *const gw = a.w, *const gpn = a.pn, *const gw2 = a.w2, *const gpn2 = a.pn2;
         const int nzl = wk.nzl;
         uint32_t uc = 0;   // sequence number of the next U plane (slot uc % NU)
-        const uint32_t fp_a = smem_u32(fullp), ep_a = smem_u32(emptyp), fm_a = smem_u32(fullm),
-                       em_a = smem_u32(emptym), uf_a = smem_u32(ufull);
+        // shared-window addresses, pinned in registers
+        const uint32_t fp_a = pin_u32(smem_u32(fullp)), ep_a = pin_u32(smem_u32(emptyp)),
+                       fm_a = pin_u32(smem_u32(fullm)), em_a = pin_u32(smem_u32(emptym)),
+                       uf_a = pin_u32(smem_u32(ufull));
         for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
             const ItemPlan it = plan_item(wk, item);
             const int x0 = it.tx * TX, y0 = it.ty * TY;
@@ -249,18 +261,22 @@ __global__ void __launch_bounds__(THREADS, MINB)
             }
             double2 pc0 = lds2(slotp(it.zlo - 1) + ok);   // p_j(q)
             double2 um2 = make_double2(0.0, 0.0), um1 = make_double2(0.0, 0.0);   // u(q-2), u(q-1)
-            const double *P0 = slotp(it.zlo - 1);
             int64_t off = (int64_t)(it.zlo - 1) * pl + (int64_t)gy * g.pitch + gx;   // global index, plane q
-            for (int q = it.zlo - 1; q <= it.zhi; ++q, off += pl) {
-                const bool inside = q >= 1 && q <= nzl;
+            // one plane: front(q), then back(q-1).  STEADY: zlo < q < zhi, where
+            // every plane condition below is known to hold.
+            auto plane = [&](int q, auto steady) {
+                constexpr bool S = decltype(steady)::value;
+                const bool inside = S || (q >= 1 && q <= nzl);
+                const bool has_up = S || q + 1 <= it.phi;
+                const double *P0 = slotp(q);
                 double2 pup = make_double2(0.0, 0.0);   // p_j(q+1)
-                if (q + 1 <= it.phi) {
-                    if (q >= it.zlo) waitp(q + 1);
+                if (has_up) {
+                    if (S || q >= it.zlo) waitp(q + 1);
                     pup = lds2(slotp(q + 1) + ok);
                 }
-                const bool mloaded = front_pm && q >= it.mlo && q <= it.mhi;
-                const double *M = sm + (mc % NSM) * MS;
-                if (mloaded) mbar_wait_a(fm_a + 8 * (mc % NSM), (mc / NSM) & 1);
+                const bool mloaded = front_pm && (S || (q >= it.mlo && q <= it.mhi));
+                const uint32_t ms = mc & (NSM - 1);
+                if (mloaded) mbar_wait_a(fm_a + 8 * ms, (mc / NSM) & 1);
                 // ---------------- front(q): step j on tile + halo ----------------
                 double2 u = make_double2(0.0, 0.0);
                 if (inside) {
@@ -274,30 +290,28 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     u.x = cfr * (dinv_c * Ap.x - sigma * c.x);
                     u.y = cfr * (dinv_c * Ap.y - sigma * c.y);
                     if (mloaded) {
-                        const double2 pm = lds2(M + omk);
+                        const double2 pm = lds2(sm + ms * MS + omk);
                         u.x -= pm.x;
                         u.y -= pm.y;
                     }
                     if (!v0) u.x = 0.0;
                     if (!v1) u.y = 0.0;
-                    if (wown && q >= it.zlo && q < it.zhi) {
+                    if (wown && (S || (q >= it.zlo && q < it.zhi))) {
                         if (!v1) Ap.y = 0.0;
                         if (!skip_w) __stcs(reinterpret_cast<double2 *>(gw + off), Ap);
                         *reinterpret_cast<double2 *>(gpn + off) = u;
                     }
                 }
-                double *U = su + (uc & (NU - 1)) * PS;
-                if (task) *reinterpret_cast<double2 *>(U + ok) = u;
+                if (task) *reinterpret_cast<double2 *>(su + (uc & (NU - 1)) * PS + ok) = u;
                 mbar_arrive_a(uf_a + 8 * (uc & (NU - 1)));
                 if (mloaded) {
-                    mbar_arrive_a(em_a + 8 * (mc % NSM));
+                    mbar_arrive_a(em_a + 8 * ms);
                     ++mc;
                 }
-                if (q >= it.plo) release(q);   // p_j plane q is done (front(q+1) reads q+1, q+2)
+                release(q);   // p_j plane q is done (front(q+1) reads q+1, q+2)
                 // ---------------- back(z = q-1): step j+1 on the tile ----------------
-                if (uc > 0) mbar_wait_a(uf_a + 8 * ((uc - 1) & (NU - 1)), ((uc - 1) / NU) & 1);
-                const int z = q - 1;
-                if (wown && z >= it.zlo && z < it.zhi) {
+                if (S || uc > 0) mbar_wait_a(uf_a + 8 * ((uc - 1) & (NU - 1)), ((uc - 1) / NU) & 1);
+                if (wown && (S || (q - 1 >= it.zlo && q - 1 < it.zhi))) {
                     const double *U0 = su + ((uc - 1) & (NU - 1)) * PS;
                     const double2 c = um1, dn = um2, up = u;
                     const double2 ylo = lds2(U0 + ok - BW), yhi = lds2(U0 + ok + BW);
@@ -320,8 +334,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 um1 = u;
                 pdn = pc0;
                 pc0 = pup;
-                if (q + 1 <= it.phi) P0 = slotp(q + 1);
-            }
+                off += pl;
+            };
+            using Gen = std::integral_constant<bool, false>;
+            using Steady = std::integral_constant<bool, true>;
+            int q = it.zlo - 1;
+            plane(q++, Gen());
+            if (q < it.zhi) plane(q++, Gen());   // q = zlo: no back output yet
+#pragma unroll 1
+            for (; q < it.zhi; ++q) plane(q, Steady());
+            for (; q <= it.zhi; ++q) plane(q, Gen());
             if (it.zhi + 1 <= it.phi) release(it.zhi + 1);
             pc = pbase + (it.phi - it.plo + 1);
         }
