@@ -30,12 +30,13 @@ namespace {
 // (register budget); one producer warp
 __host__ __device__ constexpr int ncw_for(int nb) { return nb >= 5 ? 8 : 16; }
 __host__ __device__ constexpr int threads_for(int nb) { return 32 * (ncw_for(nb) + 1); }
-constexpr int MAXS = 8;                // ring stages
+constexpr int MAXS = 16;               // ring stages
 
 struct K2DParams {
     int64_t N;         // interior doubles per vector
     int s, s_pad;      // s_pad = 8 * NB
     int nstage;
+    int ngroups;       // consumer warp groups (a divisor of NCW, <= nstage)
     double *part;      // [gridDim.x][s*s + s]
     double *out;
     unsigned *ticket;
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
     if (tid == 0) {
         for (int i = 0; i < NS; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], NCW / min(NS, NCW));
+            mbar_init(&empty[i], NCW / k.ngroups);
         }
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
         const int r = lane >> 2, kk = lane & 3;   // fragment row (m or n) and k index
         // warps form min(NS, NCW) groups; group g takes stages g, g + ngroups, ...
         // and its wpg warps split the k-steps of a stage
-        const int ngroups = min(NS, NCW), wpg = NCW / ngroups;
+        const int ngroups = k.ngroups, wpg = NCW / ngroups;
         const int grp = cw / wpg, wig = cw - grp * wpg;
         for (int it = (grp < ngroups ? grp : nit); it < nit; it += ngroups) {
             const int stg = it % NS;
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
 struct K2RParams {
     int64_t N;
     int s, s_pad, nstage, wlp;   // wlp: padded pitch (doubles) of the w_{s-1} / diag(M) rows
+    int ngroups;                 // consumer warp groups (a divisor of NCW, <= nstage)
     double inv_theta, inv_2theta, sigma, dm;
     double *part, *out;
     unsigned *ticket;
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
     if (tid == 0) {
         for (int i = 0; i < NS; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], NCW / min(NS, NCW));
+            mbar_init(&empty[i], NCW / k.ngroups);
         }
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
@@ -273,19 +275,31 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
     } else {
         const int cw = warp - 1;
         const int r = lane >> 2, kk = lane & 3;
-        const int ngroups = min(NS, NCW), wpg = NCW / ngroups;   // as in k2d
+        const int ngroups = k.ngroups, wpg = NCW / ngroups;   // as in k2d
         const int grp = cw / wpg, wig = cw - grp * wpg;
         // per-lane recurrence coefficients of fragment row j = J*8 + r (fixed for the kernel):
-        //   w = m (up c1 + dn c2 + sigma p_j)  (j <= s-2),  w = w_{s-1} (stored),  0 (j >= s)
+        //   w = m (up c1 + dn c2 + sigma p_j)  (j <= s-2),  w = w_{s-1} (stored),  0 (j >= s).
+        // Constant m (VARM false): m is folded into c1, c2, cs, and row j = s-1
+        // reads its "up" operand from the staged w_{s-1} row with c1 = 1,
+        // c2 = cs = 0 (exactly w_{s-1}); row 0 reads its "dn" operand from row
+        // 0 itself with c2 = 0.  Both are per-lane smem offsets, no selects.
         double c1[NB], c2[NB], cs[NB], use_wl[NB];
+        int upd[NB], dnd[NB];
 #pragma unroll
         for (int J = 0; J < NB; ++J) {
             const int j = J * 8 + r;
             const bool rec = j < s - 1;
-            c1[J] = !rec ? 0.0 : (j == 0 ? k.inv_theta : k.inv_2theta);
-            c2[J] = (rec && j > 0) ? k.inv_2theta : 0.0;
-            cs[J] = rec ? k.sigma : 0.0;
+            const double mf = VARM ? 1.0 : k.dm;
+            c1[J] = !rec ? 0.0 : (j == 0 ? k.inv_theta : k.inv_2theta) * mf;
+            c2[J] = (rec && j > 0) ? k.inv_2theta * mf : 0.0;
+            cs[J] = rec ? k.sigma * mf : 0.0;
             use_wl[J] = (j == s - 1) ? 1.0 : 0.0;
+            upd[J] = J * 8 * EP + EP;
+            dnd[J] = J * 8 * EP - ((j == 0) ? 0 : EP);
+            if (!VARM && j == s - 1) {
+                c1[J] = 1.0;
+                upd[J] = (SP - r) * EP;   // the w_{s-1} row: SP*EP + pt = o + (SP - r)*EP
+            }
         }
         for (int it = (grp < ngroups ? grp : nit); it < nit; it += ngroups) {
             const int stg = it % NS;
@@ -303,18 +317,17 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
 #pragma unroll
                 for (int i = 0; i < NB; ++i) a[i] = sP[o + i * 8 * EP];
                 const double p0 = sP[pt];
-                const double wl = sWl[pt];
-                const double m = VARM ? sDv[pt] : k.dm;
 #pragma unroll
                 for (int J = 0; J < NB; ++J) {
-                    // rows j+1 and j-1 of the staged P (pitch EP keeps the fragment loads
-                    // conflict-free); row -1 / row s_pad read neighbouring smem whose
-                    // values are discarded by the selects
-                    const double up = sP[o + J * 8 * EP + EP];
-                    const double dn0 = sP[o + J * 8 * EP - EP];
-                    const double dn = (c2[J] != 0.0) ? dn0 : 0.0;
-                    const double w = m * fma(up, c1[J], fma(dn, c2[J], cs[J] * a[J]));
-                    b[J] = (use_wl[J] != 0.0) ? wl : w;   // branch-free select
+                    const double up = sP[o + upd[J]];
+                    const double dn = sP[o + dnd[J]];
+                    if (VARM) {
+                        const double m = sDv[pt];
+                        const double w = m * fma(up, c1[J], fma(dn, c2[J], cs[J] * a[J]));
+                        b[J] = (use_wl[J] != 0.0) ? sWl[pt] : w;   // branch-free select
+                    } else {
+                        b[J] = fma(up, c1[J], fma(dn, c2[J], cs[J] * a[J]));
+                    }
                 }
 #pragma unroll
                 for (int i = 0; i < NB; ++i) cac[i] = fma(a[i], p0, cac[i]);
@@ -384,6 +397,20 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
 
 int ep_for(int s_pad) { return s_pad <= 32 ? 132 : 68; }   // row pitch 32 mod 128 bytes
 
+// consumer warp groups: each group works on its own stage, so the ring keeps
+// nstage - ngroups stages in flight for TMA.  SSCG_K2_GROUPS overrides.
+int groups_for(int ns, int ncw, int dflt)
+{
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("SSCG_K2_GROUPS");
+        env = e ? std::max(1, atoi(e)) : 0;
+    }
+    int g = std::min(env > 0 ? env : dflt, std::min(ns, ncw));
+    while (ncw % g) --g;
+    return std::max(g, 1);
+}
+
 template <int NB, int EP>
 size_t smem_for(int ns) { return (size_t)ns * 2 * 8 * NB * EP * sizeof(double); }
 
@@ -428,6 +455,7 @@ void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double 
     k.s = s;
     k.s_pad = s_pad;
     k.nstage = stages_for(s_pad, ep);
+    k.ngroups = groups_for(k.nstage, ncw_for(nb), k.nstage);
     k.part = sl.part;
     k.out = out_blk;
     k.ticket = sl.ticket;
@@ -507,6 +535,7 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     k.wlp = (ep * 8 + 127) / 128 * 128 / 8;
     const size_t stage = (size_t)(s_pad * ep + k.wlp * (varm ? 2 : 1)) * sizeof(double);
     k.nstage = (int)std::max<size_t>(2, std::min<size_t>(MAXS, (200 * 1024) / stage));
+    k.ngroups = groups_for(k.nstage, ncw_for(nb), k.nstage / 2);
     k.inv_theta = 1.0 / theta;
     k.inv_2theta = 1.0 / (2.0 * theta);
     k.sigma = sigma;
