@@ -485,7 +485,7 @@ bool k2r_prepare(const Geo &g, Slab &sl, int s)
 {
     const int s_pad = (s + 7) / 8 * 8, ep = ep_for(s_pad);
     const int64_t N = (int64_t)sl.nzl * g.plane;
-    const int mx = 210 * 1024;
+    const int mx = 225 * 1024;
 #define K2R_ATTR(NB, EP, V) cudaFuncSetAttribute(k2r<NB, EP, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
     if (K2R_ATTR(1, 132, false) || K2R_ATTR(2, 132, false) || K2R_ATTR(3, 132, false) || K2R_ATTR(4, 132, false) ||
         K2R_ATTR(5, 68, false) || K2R_ATTR(6, 68, false) || K2R_ATTR(7, 68, false) || K2R_ATTR(8, 68, false) ||
@@ -534,7 +534,12 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     k.s_pad = s_pad;
     k.wlp = (ep * 8 + 127) / 128 * 128 / 8;
     const size_t stage = (size_t)(s_pad * ep + k.wlp * (varm ? 2 : 1)) * sizeof(double);
-    k.nstage = (int)std::max<size_t>(2, std::min<size_t>(MAXS, (200 * 1024) / stage));
+    static int smem_kb = -1;
+    if (smem_kb < 0) {
+        const char *e = getenv("SSCG_K2_SMEM_KB");
+        smem_kb = e ? std::min(224, std::max(64, atoi(e))) : 200;
+    }
+    k.nstage = (int)std::max<size_t>(2, std::min<size_t>(MAXS, ((size_t)smem_kb * 1024) / stage));
     k.ngroups = groups_for(k.nstage, ncw_for(nb), k.nstage / 2);
     k.inv_theta = 1.0 / theta;
     k.inv_2theta = 1.0 / (2.0 * theta);
