@@ -21,7 +21,9 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsscg.so")
+# SSCG_LIB selects another in-tree build of the same library (variant builds
+# from `python -m paper_2512_09642_b200.build --variant NAME -D...`, for sweeps)
+LIB_PATH = os.environ.get("SSCG_LIB") or os.path.join(_HERE, "libsscg.so")
 
 OK, ERR_INVALID, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_BREAKDOWN, ERR_NONFINITE, ERR_UNSUPPORTED = range(8)
 OP_STENCIL5_2D, OP_STENCIL7, OP_STENCIL27, OP_VARCOEF7, OP_CSR = range(5)

@@ -39,28 +39,36 @@ def deps():
     return sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "sscg.h"), __file__]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
+def build(force: bool = False, verbose: bool = False, defs=(), variant: str = "") -> str:
+    """Compile libsscg.so; with `variant`, compile libsscg_<variant>.so with the
+    extra -D flags `defs` (tuning experiments; load it with SSCG_LIB=<path>)."""
+    lib = os.path.join(HERE, "libsscg_%s.so" % variant) if variant else LIB
+    bdir = os.path.join(BUILD, variant) if variant else BUILD
+    if not force and os.path.exists(lib):
+        t = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= t for d in deps()):
-            return LIB
-    os.makedirs(BUILD, exist_ok=True)
+            return lib
+    os.makedirs(bdir, exist_ok=True)
     inc, libdir = nccl_dirs()
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
                      "-I", inc, "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
     if verbose:
         common += ["-Xptxas", "-v"]
+    common += list(defs)
     objs = []
     for src in sources():
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
         cmd = [NVCC] + common + ["-c", src, "-o", obj]
         subprocess.check_call(cmd)
         objs.append(obj)
-    link = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-L", libdir, "-l:libnccl.so.2",
+    link = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-L", libdir, "-l:libnccl.so.2",
                                                            "-Xlinker", "-rpath=" + libdir, "-cudart", "static"]
     subprocess.check_call(link)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    a = sys.argv[1:]
+    var = a[a.index("--variant") + 1] if "--variant" in a else ""
+    print(build(force="--force" in a or bool(var), verbose="-v" in a, defs=[x for x in a if x.startswith("-D")],
+                variant=var))

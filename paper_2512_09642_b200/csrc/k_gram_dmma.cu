@@ -28,7 +28,19 @@ namespace {
 
 // consumer warps: 16 while the accumulators are small (s <= 32), 8 above
 // (register budget); one producer warp
-__host__ __device__ constexpr int ncw_for(int nb) { return nb >= 5 ? 8 : 16; }
+#ifndef K2_NCW_SMALL
+#define K2_NCW_SMALL 24
+#endif
+#ifndef K2R_U3
+#define K2R_U3 2
+#endif
+// consumer warps: 24 for s <= 16 (few accumulator tiles), 12 for s <= 32, 8
+// above (register budget); measured: cfg 5 16 warps x U=4 2.10 ms, 24 x U=2 2.06 ms;
+// cfg 4 s = 32 16 warps 0.553 ms, 8 0.500, 12 0.453
+#ifndef K2_NCW_MID
+#define K2_NCW_MID 12
+#endif
+__host__ __device__ constexpr int ncw_for(int nb) { return nb >= 5 ? 8 : nb >= 3 ? K2_NCW_MID : K2_NCW_SMALL; }
 __host__ __device__ constexpr int threads_for(int nb) { return 32 * (ncw_for(nb) + 1); }
 constexpr int MAXS = 16;               // ring stages
 
@@ -248,7 +260,7 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
 
     // U accumulator sets: k-steps rotate over them so that U*NT independent
     // DMMA chains hide the tensor-core latency when the tile count is small
-    constexpr int U = (NT >= 10) ? 1 : (NT >= 6) ? 2 : (NT >= 3) ? 4 : 8;
+    constexpr int U = (NT >= 10) ? 1 : (NT >= 6) ? 2 : (NT >= 3) ? K2R_U3 : 8;
     double acc[U][NT][2];
     double cac[NB];
 #pragma unroll
@@ -397,22 +409,31 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
 
 int ep_for(int s_pad) { return s_pad <= 32 ? 132 : 68; }   // row pitch 32 mod 128 bytes
 
-// consumer warp groups: each group works on its own stage, so the ring keeps
-// nstage - ngroups stages in flight for TMA.  SSCG_K2_GROUPS overrides.
-int groups_for(int ns, int ncw, int dflt)
+// consumer warp groups: each group works on its own stages, so the ring keeps
+// nstage - ngroups stages in flight for TMA.  ngroups must divide both the
+// consumer warps and nstage: then slot `it % nstage` is always consumed by
+// group `it % ngroups`, in order, and a group can never wait on a slot whose
+// previous phase (another group's) is still pending -- with shared slots a
+// group running a full ring ahead would match the parity of an older phase.
+int gcd_int(int a, int b) { return b ? gcd_int(b, a % b) : a; }
+
+int env_groups()
 {
     static int env = -1;
     if (env < 0) {
-        const char *e = getenv("SSCG_K2_GROUPS");
+        const char *e = getenv("SSCG_K2_GROUPS");   // tuning override
         env = e ? std::max(1, atoi(e)) : 0;
     }
-    int g = std::min(env > 0 ? env : dflt, std::min(ns, ncw));
-    while (ncw % g) --g;
-    return std::max(g, 1);
+    return env;
 }
 
-template <int NB, int EP>
-size_t smem_for(int ns) { return (size_t)ns * 2 * 8 * NB * EP * sizeof(double); }
+// largest g <= want dividing every value in {a, b}
+int common_divisor_le(int want, int a, int b)
+{
+    int g = std::max(1, std::min(want, gcd_int(a, b)));
+    while (a % g || b % g) --g;
+    return g;
+}
 
 int stages_for(int s_pad, int ep)
 {
@@ -455,7 +476,7 @@ void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double 
     k.s = s;
     k.s_pad = s_pad;
     k.nstage = stages_for(s_pad, ep);
-    k.ngroups = groups_for(k.nstage, ncw_for(nb), k.nstage);
+    k.ngroups = common_divisor_le(env_groups() ? env_groups() : k.nstage, k.nstage, ncw_for(nb));
     k.part = sl.part;
     k.out = out_blk;
     k.ticket = sl.ticket;
@@ -485,7 +506,7 @@ bool k2r_prepare(const Geo &g, Slab &sl, int s)
 {
     const int s_pad = (s + 7) / 8 * 8, ep = ep_for(s_pad);
     const int64_t N = (int64_t)sl.nzl * g.plane;
-    const int mx = 225 * 1024;
+    const int mx = 226 * 1024;
 #define K2R_ATTR(NB, EP, V) cudaFuncSetAttribute(k2r<NB, EP, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
     if (K2R_ATTR(1, 132, false) || K2R_ATTR(2, 132, false) || K2R_ATTR(3, 132, false) || K2R_ATTR(4, 132, false) ||
         K2R_ATTR(5, 68, false) || K2R_ATTR(6, 68, false) || K2R_ATTR(7, 68, false) || K2R_ATTR(8, 68, false) ||
@@ -537,10 +558,16 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     static int smem_kb = -1;
     if (smem_kb < 0) {
         const char *e = getenv("SSCG_K2_SMEM_KB");
-        smem_kb = e ? std::min(224, std::max(64, atoi(e))) : 200;
+        smem_kb = e ? std::min(224, std::max(64, atoi(e))) : 216;
     }
-    k.nstage = (int)std::max<size_t>(2, std::min<size_t>(MAXS, ((size_t)smem_kb * 1024) / stage));
-    k.ngroups = groups_for(k.nstage, ncw_for(nb), k.nstage / 2);
+    {
+        // 4 groups by default (each with nstage/4 slots), nstage a multiple of the groups
+        const int nsmax = (int)std::max<size_t>(1, std::min<size_t>(MAXS, ((size_t)smem_kb * 1024) / stage));
+        const int g = common_divisor_le(env_groups() ? env_groups() : 4, ncw_for(nb), ncw_for(nb));
+        k.ngroups = std::min(g, nsmax);
+        while (ncw_for(nb) % k.ngroups) --k.ngroups;
+        k.nstage = std::max(k.ngroups, nsmax / k.ngroups * k.ngroups);
+    }
     k.inv_theta = 1.0 / theta;
     k.inv_2theta = 1.0 / (2.0 * theta);
     k.sigma = sigma;
