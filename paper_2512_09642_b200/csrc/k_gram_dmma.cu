@@ -54,6 +54,8 @@ struct K2DParams {
     unsigned *ticket;
 };
 
+__device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
     if (st && st->done) return;
     constexpr int SP = 8 * NB;
     constexpr int NCW = ncw_for(NB), THREADS = threads_for(NB);
-    constexpr int KS = EP / 4;
+    constexpr int KS2 = EP / 8;   // k-step pairs per stage (EP = 136 or 72: row pitch 64 mod 128 B)
     constexpr int NT = NB * (NB + 1) / 2;
     extern __shared__ __align__(1024) double smem[];
     __shared__ uint64_t full[MAXS], empty[MAXS];
@@ -261,6 +263,7 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
     // U accumulator sets: k-steps rotate over them so that U*NT independent
     // DMMA chains hide the tensor-core latency when the tile count is small
     constexpr int U = (NT >= 10) ? 1 : (NT >= 6) ? 2 : (NT >= 3) ? K2R_U3 : 8;
+    constexpr int UP = (U >= 2) ? U / 2 : 1;   // k-step pairs per unrolled block
     double acc[U][NT][2];
     double cac[NB];
 #pragma unroll
@@ -318,36 +321,47 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
             mbar_wait(&full[stg], (uint32_t)((it / NS) & 1));
             const double *sP = smem + (size_t)stg * stage_elems;
             const double *sWl = sP + SP * EP, *sDv = sWl + k.wlp;
-            for (int ks0 = wig; ks0 < KS; ks0 += wpg * U) {
+            // k-step pairs: lane (r, kk) loads the points 2kk, 2kk+1 of an 8-point
+            // block with one 16-B load per row; k-step A takes the even points,
+            // k-step B the odd ones (the dot over points is order-free), into
+            // accumulator sets 2u and 2u+1
+            for (int kp0 = wig; kp0 < KS2; kp0 += wpg * UP) {
 #pragma unroll
-              for (int u = 0; u < U; ++u) {
-                const int ks = ks0 + u * wpg;
-                if (ks >= KS) break;
-                const int pt = ks * 4 + kk;
+              for (int u = 0; u < UP; ++u) {
+                const int kp = kp0 + u * wpg;
+                if (kp >= KS2) break;
+                const int pt = kp * 8 + 2 * kk;
                 const int o = r * EP + pt;
-                double a[NB], b[NB];
+                double2 a[NB], b[NB];
 #pragma unroll
-                for (int i = 0; i < NB; ++i) a[i] = sP[o + i * 8 * EP];
-                const double p0 = sP[pt];
+                for (int i = 0; i < NB; ++i) a[i] = lds2(sP + o + i * 8 * EP);
+                const double2 p0 = lds2(sP + pt);
 #pragma unroll
                 for (int J = 0; J < NB; ++J) {
-                    const double up = sP[o + upd[J]];
-                    const double dn = sP[o + dnd[J]];
+                    const double2 up = lds2(sP + o + upd[J]);
+                    const double2 dn = lds2(sP + o + dnd[J]);
                     if (VARM) {
-                        const double m = sDv[pt];
-                        const double w = m * fma(up, c1[J], fma(dn, c2[J], cs[J] * a[J]));
-                        b[J] = (use_wl[J] != 0.0) ? sWl[pt] : w;   // branch-free select
+                        const double2 m = lds2(sDv + pt), wl = lds2(sWl + pt);
+                        const double wx = m.x * fma(up.x, c1[J], fma(dn.x, c2[J], cs[J] * a[J].x));
+                        const double wy = m.y * fma(up.y, c1[J], fma(dn.y, c2[J], cs[J] * a[J].y));
+                        b[J].x = (use_wl[J] != 0.0) ? wl.x : wx;   // branch-free select
+                        b[J].y = (use_wl[J] != 0.0) ? wl.y : wy;
                     } else {
-                        b[J] = fma(up, c1[J], fma(dn, c2[J], cs[J] * a[J]));
+                        b[J].x = fma(up.x, c1[J], fma(dn.x, c2[J], cs[J] * a[J].x));
+                        b[J].y = fma(up.y, c1[J], fma(dn.y, c2[J], cs[J] * a[J].y));
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < NB; ++i) cac[i] = fma(a[i], p0, cac[i]);
+                for (int i = 0; i < NB; ++i) cac[i] = fma(a[i].y, p0.y, fma(a[i].x, p0.x, cac[i]));
+                constexpr int SX = 0, SY = (U > 1) ? 1 : 0;
                 int t = 0;
 #pragma unroll
                 for (int i = 0; i < NB; ++i)
 #pragma unroll
-                    for (int J = i; J < NB; ++J, ++t) dmma(acc[u][t][0], acc[u][t][1], a[i], b[J]);
+                    for (int J = i; J < NB; ++J, ++t) {
+                        dmma(acc[(2 * u + SX) % U][t][0], acc[(2 * u + SX) % U][t][1], a[i].x, b[J].x);
+                        dmma(acc[(2 * u + SY) % U][t][0], acc[(2 * u + SY) % U][t][1], a[i].y, b[J].y);
+                    }
               }
             }
             __syncwarp();
@@ -407,7 +421,108 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
     if (tid == 0) *k.ticket = 0u;
 }
 
-int ep_for(int s_pad) { return s_pad <= 32 ? 132 : 68; }   // row pitch 32 mod 128 bytes
+// K2S -- the W-free Gram pass for small bases (s <= 8): a plain streaming
+// kernel.  With one 8x8 DMMA tile per point the tensor-core pass is bound by
+// its per-chunk pipeline, while here every thread streams point pairs with
+// 16-B loads (s + 1 rows, + diag(M)), recovers w_j from the recurrence as
+// K2R does, and keeps the s(s+1)/2 + s partial sums in registers.  Warp
+// shuffles, then a fixed-order sum over the warps, then the last-CTA sum:
+// deterministic for a given grid.
+__host__ __device__ constexpr int k2s_threads(int S) { return S >= 7 ? 256 : 512; }   // registers
+
+template <int S, bool VARM>
+__global__ void __launch_bounds__(k2s_threads(S), 1)
+    k2s(const double *__restrict__ P, const double *__restrict__ Wl, const double *__restrict__ Dv, int64_t vstride,
+        K2RParams k, const DevState *st)
+{
+    if (st && st->done) return;
+    constexpr int K2S_THREADS = k2s_threads(S);
+    constexpr int NUP = S * (S + 1) / 2, NACC = NUP + S;
+    __shared__ double red[K2S_THREADS / 32][NACC];
+    __shared__ bool is_last;
+    double g[NACC];
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) g[q] = 0.0;
+    double c1[S], c2[S], cs[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+        const bool rec = j < S - 1;
+        const double mf = VARM ? 1.0 : k.dm;
+        c1[j] = !rec ? 0.0 : (j == 0 ? k.inv_theta : k.inv_2theta) * mf;
+        c2[j] = (rec && j > 0) ? k.inv_2theta * mf : 0.0;
+        cs[j] = rec ? k.sigma * mf : 0.0;
+    }
+    const int64_t n2 = k.N >> 1, vs2 = vstride >> 1;
+    const double2 *P2 = reinterpret_cast<const double2 *>(P);
+    const double2 *W2 = reinterpret_cast<const double2 *>(Wl);
+    const double2 *D2 = reinterpret_cast<const double2 *>(Dv);
+    for (int64_t e = (int64_t)blockIdx.x * K2S_THREADS + threadIdx.x; e < n2; e += (int64_t)gridDim.x * K2S_THREADS) {
+        double2 p[S + 1], w[S];
+#pragma unroll
+        for (int j = 0; j < S; ++j) p[j] = __ldcs(P2 + j * vs2 + e);
+        p[S] = make_double2(0.0, 0.0);
+        const double2 wl = __ldcs(W2 + e);
+        const double2 m = VARM ? __ldcs(D2 + e) : make_double2(1.0, 1.0);
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            if (j == S - 1) {
+                w[j] = wl;
+            } else {
+                const double2 up = p[j + 1], dn = (j > 0) ? p[j - 1] : make_double2(0.0, 0.0);
+                double wx = fma(up.x, c1[j], fma(dn.x, c2[j], cs[j] * p[j].x));
+                double wy = fma(up.y, c1[j], fma(dn.y, c2[j], cs[j] * p[j].y));
+                if (VARM) {
+                    wx *= m.x;
+                    wy *= m.y;
+                }
+                w[j] = make_double2(wx, wy);
+            }
+        }
+        int t = 0;
+#pragma unroll
+        for (int i = 0; i < S; ++i)
+#pragma unroll
+            for (int j = i; j < S; ++j, ++t) g[t] = fma(p[i].y, w[j].y, fma(p[i].x, w[j].x, g[t]));
+#pragma unroll
+        for (int i = 0; i < S; ++i) g[NUP + i] = fma(p[i].y, p[0].y, fma(p[i].x, p[0].x, g[NUP + i]));
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) {
+        double v = g[q];
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (lane == 0) red[warp][q] = v;
+    }
+    __syncthreads();
+    const int s = S, nent = s * s + s;
+    double *mypart = k.part + (int64_t)blockIdx.x * nent;
+    for (int q = threadIdx.x; q < NACC; q += K2S_THREADS) {
+        double v = 0.0;
+        for (int w8 = 0; w8 < K2S_THREADS / 32; ++w8) v += red[w8][q];
+        if (q < NUP) {
+            int i = 0, rem = q;
+            while (rem >= s - i) { rem -= s - i; ++i; }
+            mypart[i * s + i + rem] = v;
+        } else {
+            mypart[s * s + (q - NUP)] = v;
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(k.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    last_cta_sum(k.part, gridDim.x, s, k.out);
+    if (threadIdx.x == 0) *k.ticket = 0u;
+}
+
+int ep_for(int s_pad) { return s_pad <= 32 ? 132 : 68; }   // row pitch 32 mod 128 bytes (8-B fragment loads)
+int ep_for_k2r(int s_pad) { return s_pad <= 32 ? 136 : 72; }   // 64 mod 128 bytes (16-B loads of point pairs)
 
 // consumer warp groups: each group works on its own stages, so the ring keeps
 // nstage - ngroups stages in flight for TMA.  ngroups must divide both the
@@ -504,18 +619,18 @@ namespace sscg {
 
 bool k2r_prepare(const Geo &g, Slab &sl, int s)
 {
-    const int s_pad = (s + 7) / 8 * 8, ep = ep_for(s_pad);
+    const int s_pad = (s + 7) / 8 * 8, ep = ep_for_k2r(s_pad);
     const int64_t N = (int64_t)sl.nzl * g.plane;
     const int mx = 226 * 1024;
 #define K2R_ATTR(NB, EP, V) cudaFuncSetAttribute(k2r<NB, EP, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
-    if (K2R_ATTR(1, 132, false) || K2R_ATTR(2, 132, false) || K2R_ATTR(3, 132, false) || K2R_ATTR(4, 132, false) ||
-        K2R_ATTR(5, 68, false) || K2R_ATTR(6, 68, false) || K2R_ATTR(7, 68, false) || K2R_ATTR(8, 68, false) ||
-        K2R_ATTR(1, 132, true) || K2R_ATTR(2, 132, true) || K2R_ATTR(3, 132, true) || K2R_ATTR(4, 132, true) ||
-        K2R_ATTR(5, 68, true) || K2R_ATTR(6, 68, true) || K2R_ATTR(7, 68, true) || K2R_ATTR(8, 68, true))
+    if (K2R_ATTR(1, 136, false) || K2R_ATTR(2, 136, false) || K2R_ATTR(3, 136, false) || K2R_ATTR(4, 136, false) ||
+        K2R_ATTR(5, 72, false) || K2R_ATTR(6, 72, false) || K2R_ATTR(7, 72, false) || K2R_ATTR(8, 72, false) ||
+        K2R_ATTR(1, 136, true) || K2R_ATTR(2, 136, true) || K2R_ATTR(3, 136, true) || K2R_ATTR(4, 136, true) ||
+        K2R_ATTR(5, 72, true) || K2R_ATTR(6, 72, true) || K2R_ATTR(7, 72, true) || K2R_ATTR(8, 72, true))
         return false;
 #undef K2R_ATTR
-    // P rows (as K2D), the single row w_{s-1} of W, and diag(M) (one row) when it varies
-    if (!encode_rows_map(&sl.tmPd, sl.P + g.plane, N, s, g.vstride, ep, s_pad)) return false;
+    // P rows (own map: K2D's pitch differs), the single row w_{s-1} of W, and diag(M) (one row) when it varies
+    if (!encode_rows_map(&sl.tmPr, sl.P + g.plane, N, s, g.vstride, ep, s_pad)) return false;
     if (!encode_rows_map(&sl.tmWl, sl.W + g.plane, N, s, g.vstride, ep, 1)) return false;
     if (sl.dvec && !encode_rows_map(&sl.tmDv, sl.dvec + g.plane, N, 1, g.vstride, ep, 1)) return false;
     return true;
@@ -547,10 +662,43 @@ void launch_wrec(const Geo &g, const Slab &sl, int j, double theta, double sigma
 void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma, const DevState *st, double *out_blk,
                 cudaStream_t stream)
 {
-    const int s_pad = (s + 7) / 8 * 8, nb = s_pad / 8, ep = ep_for(s_pad);
+    const int s_pad = (s + 7) / 8 * 8, nb = s_pad / 8, ep = ep_for_k2r(s_pad);
     const bool varm = sl.dvec != nullptr;
     K2RParams k;
     k.N = (int64_t)sl.nzl * g.plane;
+    static int k2s_env = -1;
+    if (k2s_env < 0) {
+        const char *e = getenv("SSCG_K2S");   // "0": keep the tensor-core pass for s <= 8
+        k2s_env = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (k2s_env && s >= 2 && s <= 8) {
+        k.s = s;
+        k.inv_theta = 1.0 / theta;
+        k.inv_2theta = 1.0 / (2.0 * theta);
+        k.sigma = sigma;
+        k.dm = g.center;
+        k.part = sl.part;
+        k.out = out_blk;
+        k.ticket = sl.ticket;
+        const double *P = sl.P + g.plane, *Wl = sl.W + (int64_t)(s - 1) * g.vstride + g.plane;
+        const double *Dv = varm ? sl.dvec + g.plane : nullptr;
+        const int nth = k2s_threads(s);
+        const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(k2_grid(), (k.N / 2 + nth - 1) / nth));
+#define K2S_LAUNCH(S)                                                                                            \
+        if (varm) k2s<S, true><<<gx, nth, 0, stream>>>(P, Wl, Dv, g.vstride, k, st);                            \
+        else k2s<S, false><<<gx, nth, 0, stream>>>(P, Wl, Dv, g.vstride, k, st);
+        switch (s) {
+        case 2: K2S_LAUNCH(2) break;
+        case 3: K2S_LAUNCH(3) break;
+        case 4: K2S_LAUNCH(4) break;
+        case 5: K2S_LAUNCH(5) break;
+        case 6: K2S_LAUNCH(6) break;
+        case 7: K2S_LAUNCH(7) break;
+        default: K2S_LAUNCH(8) break;
+        }
+#undef K2S_LAUNCH
+        return;
+    }
     k.s = s;
     k.s_pad = s_pad;
     k.wlp = (ep * 8 + 127) / 128 * 128 / 8;
@@ -582,17 +730,17 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     const size_t sm = std::max((size_t)k.nstage * stage, red);
     const CUtensorMap &dv = varm ? sl.tmDv : sl.tmWl;
 #define K2R_LAUNCH(NB, EP)                                                                                   \
-    if (varm) k2r<NB, EP, true><<<gx, threads_for(NB), sm, stream>>>(sl.tmPd, sl.tmWl, dv, k, st);          \
-    else k2r<NB, EP, false><<<gx, threads_for(NB), sm, stream>>>(sl.tmPd, sl.tmWl, dv, k, st);
+    if (varm) k2r<NB, EP, true><<<gx, threads_for(NB), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);          \
+    else k2r<NB, EP, false><<<gx, threads_for(NB), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);
     switch (nb) {
-    case 1: K2R_LAUNCH(1, 132) break;
-    case 2: K2R_LAUNCH(2, 132) break;
-    case 3: K2R_LAUNCH(3, 132) break;
-    case 4: K2R_LAUNCH(4, 132) break;
-    case 5: K2R_LAUNCH(5, 68) break;
-    case 6: K2R_LAUNCH(6, 68) break;
-    case 7: K2R_LAUNCH(7, 68) break;
-    default: K2R_LAUNCH(8, 68) break;
+    case 1: K2R_LAUNCH(1, 136) break;
+    case 2: K2R_LAUNCH(2, 136) break;
+    case 3: K2R_LAUNCH(3, 136) break;
+    case 4: K2R_LAUNCH(4, 136) break;
+    case 5: K2R_LAUNCH(5, 72) break;
+    case 6: K2R_LAUNCH(6, 72) break;
+    case 7: K2R_LAUNCH(7, 72) break;
+    default: K2R_LAUNCH(8, 72) break;
     }
 #undef K2R_LAUNCH
 }

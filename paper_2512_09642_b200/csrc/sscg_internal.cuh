@@ -46,6 +46,7 @@ struct Slab {
     CUtensorMap tmPd, tmWd;       // K2D (DMMA Gram, s > 16): same views, box pitch 132/68
     bool has_k2d;
     CUtensorMap tmWl, tmDv;       // K2R: the row w_{s-1} of W, diag(M) (one row)
+    CUtensorMap tmPr;             // K2R: P rows, box pitch 136/72 (16-B point-pair loads)
     bool has_k2r;
     CUtensorMap tmP4, tmM4;       // K1T: 4-D [x][y][plane][vector] views of P (halo box / tile box)
     bool has_k1t;

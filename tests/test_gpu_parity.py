@@ -381,6 +381,34 @@ def test_gram_dmma_matches_register_tiles(cfg, monkeypatch):
     assert np.max(np.abs(c1 - c0)) <= 1e-13 * np.max(np.abs(c0))
 
 
+@pytest.mark.parametrize("cfg", [("7pt", 30, 28, 26, 2, 10), ("7pt", 34, 17, 19, 4, 20), ("7pt", 24, 22, 21, 8, 20),
+                                 ("varcoef7", 20, 18, 17, 3, 10), ("varcoef7", 22, 20, 19, 8, 20),
+                                 ("27pt", 20, 18, 17, 5, 20)], ids=_ids)
+def test_gram_small_s_streaming_matches_tensor_pass(cfg, monkeypatch):
+    """W-free Gram pass for s <= 8: the streaming kernel K2S (registers, one
+    pass of point pairs) against the tensor-core K2R (SSCG_K2S=0) and the
+    oracle -- Gram block and c at outer 0 to the north_star 1e-11, the two GPU
+    kernels to rounding -- and the same iterate after a few outer steps."""
+    import paper_2512_09642_b200 as sscg
+    kind, nx, ny, nz, s, nu = cfg
+    P = Problem(kind, nx, ny, nz, s, nu, lanczos=(kind != "7pt"))
+    x_or, tr = P.oracle(max_outer=1, dump_iter=0)
+    out = {}
+    for k2s in ("1", "0"):
+        monkeypatch.setenv("SSCG_K2S", k2s)
+        with P.gpu_solver() as S:
+            assert S.query(sscg.QUERY_GRAM_VECTORS) == s + 1 + (1 if kind == "varcoef7" else 0)   # W-free
+            S.solve(P.b_gpu(), rtol=0.0, max_outer=1)
+            out[k2s] = S.gram(0)
+            assert_gram(S, tr, 0)
+            x4 = S.solve(P.b_gpu(), rtol=0.0, max_outer=4).cpu().numpy()
+            out[k2s + "x"] = x4
+    (G1, c1), (G0, c0) = out["1"], out["0"]
+    assert np.max(np.abs(G1 - G0)) <= 1e-13 * np.max(np.abs(G0))
+    assert np.max(np.abs(c1 - c0)) <= 1e-13 * np.max(np.abs(c0))
+    assert np.linalg.norm(out["1x"] - out["0x"]) <= 1e-10 * np.linalg.norm(out["0x"])
+
+
 @pytest.mark.parametrize("kind,nx,ny,nz,s", [("7pt", 26, 24, 22, 8), ("27pt", 20, 18, 17, 6), ("varcoef7", 18, 16, 15, 6)])
 def test_user_diagonal_preconditioner(kind, nx, ny, nz, s):
     """A caller-supplied Jacobi diagonal M (here a spatially varying multiple
