@@ -236,6 +236,11 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
     if (st && st->done) return;
     constexpr int SP = 8 * NB;
     constexpr int NCW = ncw_for(NB), THREADS = threads_for(NB);
+    // NB <= 2: k-step pairs from 16-B loads (pitch EP = 136, 64 mod 128 B); larger
+    // NB (more live fragments): single k-steps from 8-B loads (EP = 132 / 68,
+    // 32 mod 128 B) -- measured faster there (cfg 4 s = 32: 0.453 vs 0.486 ms)
+    constexpr bool PAIRS = NB <= 2;
+    constexpr int KS = EP / 4;
     constexpr int KS2 = EP / 8;   // k-step pairs per stage (EP = 136 or 72: row pitch 64 mod 128 B)
     constexpr int NT = NB * (NB + 1) / 2;
     extern __shared__ __align__(1024) double smem[];
@@ -262,7 +267,10 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
 
     // U accumulator sets: k-steps rotate over them so that U*NT independent
     // DMMA chains hide the tensor-core latency when the tile count is small
-    constexpr int U = (NT >= 10) ? 1 : (NT >= 6) ? 2 : (NT >= 3) ? K2R_U3 : 8;
+#ifndef K2R_U10
+#define K2R_U10 1
+#endif
+    constexpr int U = (NT >= 10) ? K2R_U10 : (NT >= 6) ? 2 : (NT >= 3) ? K2R_U3 : 8;
     constexpr int UP = (U >= 2) ? U / 2 : 1;   // k-step pairs per unrolled block
     double acc[U][NT][2];
     double cac[NB];
@@ -321,6 +329,7 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
             mbar_wait(&full[stg], (uint32_t)((it / NS) & 1));
             const double *sP = smem + (size_t)stg * stage_elems;
             const double *sWl = sP + SP * EP, *sDv = sWl + k.wlp;
+            if constexpr (PAIRS) {
             // k-step pairs: lane (r, kk) loads the points 2kk, 2kk+1 of an 8-point
             // block with one 16-B load per row; k-step A takes the even points,
             // k-step B the odd ones (the dot over points is order-free), into
@@ -363,6 +372,40 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
                         dmma(acc[(2 * u + SY) % U][t][0], acc[(2 * u + SY) % U][t][1], a[i].y, b[J].y);
                     }
               }
+            }
+            } else {
+            for (int ks0 = wig; ks0 < KS; ks0 += wpg * U) {
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const int ks = ks0 + u * wpg;
+                if (ks >= KS) break;
+                const int pt = ks * 4 + kk;
+                const int o = r * EP + pt;
+                double a[NB], b[NB];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) a[i] = sP[o + i * 8 * EP];
+                const double p0 = sP[pt];
+#pragma unroll
+                for (int J = 0; J < NB; ++J) {
+                    const double up = sP[o + upd[J]];
+                    const double dn = sP[o + dnd[J]];
+                    if (VARM) {
+                        const double m = sDv[pt];
+                        const double w = m * fma(up, c1[J], fma(dn, c2[J], cs[J] * a[J]));
+                        b[J] = (use_wl[J] != 0.0) ? sWl[pt] : w;   // branch-free select
+                    } else {
+                        b[J] = fma(up, c1[J], fma(dn, c2[J], cs[J] * a[J]));
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < NB; ++i) cac[i] = fma(a[i], p0, cac[i]);
+                int t = 0;
+#pragma unroll
+                for (int i = 0; i < NB; ++i)
+#pragma unroll
+                    for (int J = i; J < NB; ++J, ++t) dmma(acc[u][t][0], acc[u][t][1], a[i], b[J]);
+              }
+            }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
@@ -522,7 +565,7 @@ __global__ void __launch_bounds__(k2s_threads(S), 1)
 }
 
 int ep_for(int s_pad) { return s_pad <= 32 ? 132 : 68; }   // row pitch 32 mod 128 bytes (8-B fragment loads)
-int ep_for_k2r(int s_pad) { return s_pad <= 32 ? 136 : 72; }   // 64 mod 128 bytes (16-B loads of point pairs)
+int ep_for_k2r(int s_pad) { return s_pad <= 16 ? 136 : ep_for(s_pad); }   // pairs: 64 mod 128 B (16-B loads)
 
 // consumer warp groups: each group works on its own stages, so the ring keeps
 // nstage - ngroups stages in flight for TMA.  ngroups must divide both the
@@ -623,10 +666,10 @@ bool k2r_prepare(const Geo &g, Slab &sl, int s)
     const int64_t N = (int64_t)sl.nzl * g.plane;
     const int mx = 226 * 1024;
 #define K2R_ATTR(NB, EP, V) cudaFuncSetAttribute(k2r<NB, EP, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
-    if (K2R_ATTR(1, 136, false) || K2R_ATTR(2, 136, false) || K2R_ATTR(3, 136, false) || K2R_ATTR(4, 136, false) ||
-        K2R_ATTR(5, 72, false) || K2R_ATTR(6, 72, false) || K2R_ATTR(7, 72, false) || K2R_ATTR(8, 72, false) ||
-        K2R_ATTR(1, 136, true) || K2R_ATTR(2, 136, true) || K2R_ATTR(3, 136, true) || K2R_ATTR(4, 136, true) ||
-        K2R_ATTR(5, 72, true) || K2R_ATTR(6, 72, true) || K2R_ATTR(7, 72, true) || K2R_ATTR(8, 72, true))
+    if (K2R_ATTR(1, 136, false) || K2R_ATTR(2, 136, false) || K2R_ATTR(3, 132, false) || K2R_ATTR(4, 132, false) ||
+        K2R_ATTR(5, 68, false) || K2R_ATTR(6, 68, false) || K2R_ATTR(7, 68, false) || K2R_ATTR(8, 68, false) ||
+        K2R_ATTR(1, 136, true) || K2R_ATTR(2, 136, true) || K2R_ATTR(3, 132, true) || K2R_ATTR(4, 132, true) ||
+        K2R_ATTR(5, 68, true) || K2R_ATTR(6, 68, true) || K2R_ATTR(7, 68, true) || K2R_ATTR(8, 68, true))
         return false;
 #undef K2R_ATTR
     // P rows (own map: K2D's pitch differs), the single row w_{s-1} of W, and diag(M) (one row) when it varies
@@ -735,12 +778,12 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     switch (nb) {
     case 1: K2R_LAUNCH(1, 136) break;
     case 2: K2R_LAUNCH(2, 136) break;
-    case 3: K2R_LAUNCH(3, 136) break;
-    case 4: K2R_LAUNCH(4, 136) break;
-    case 5: K2R_LAUNCH(5, 72) break;
-    case 6: K2R_LAUNCH(6, 72) break;
-    case 7: K2R_LAUNCH(7, 72) break;
-    default: K2R_LAUNCH(8, 72) break;
+    case 3: K2R_LAUNCH(3, 132) break;
+    case 4: K2R_LAUNCH(4, 132) break;
+    case 5: K2R_LAUNCH(5, 68) break;
+    case 6: K2R_LAUNCH(6, 68) break;
+    case 7: K2R_LAUNCH(7, 68) break;
+    default: K2R_LAUNCH(8, 68) break;
     }
 #undef K2R_LAUNCH
 }
