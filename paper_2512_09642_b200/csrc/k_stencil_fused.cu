@@ -508,12 +508,12 @@ bool k1f_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
 }
 
 // SSCG_K1_FUSE (read at every sscg_setup): "0" never, "1" always (7/27-point),
-// unset: 7-point slabs with at least K1F_MIN_WORK tile-planes per SM.  K1F
-// runs one CTA per SM and re-reads 4 planes of p_j per z-chunk, so small
-// grids (cfg 2, 128^3) run faster as single K1T steps; the 27-point pair is
-// bound by its in-plane box sums and gains nothing over two K1T steps
-// (profiles/r01g_workloads.jsonl).
-constexpr int64_t K1F_MIN_WORK = 256;
+// unset: 7-point slabs with at least K1F_MIN_WORK tile-planes per SM.  Since
+// the register-column K1F (z-columns in registers, per-thread mbarriers) the
+// fused pair beats two K1T steps down to cfg 2 (128^3: 0.243 vs 0.263 ms per
+// outer, profiles/r01r_*); the 27-point pair is bound by its in-plane box sums
+// and gains nothing over two K1T steps (profiles/r01g_workloads.jsonl).
+constexpr int64_t K1F_MIN_WORK = 8;
 
 bool k1f_enabled(const Geo &g, int nzl)
 {
