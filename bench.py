@@ -316,8 +316,9 @@ def run_ours(a):
     face_bytes = 0.0
     if a.kind == "varcoef7":   # kx, ky, kz of this slab, read by every basis step
         face_bytes = 8.0 * (n * (n + 1) * S.nz_local * 2 + n * n * (S.nz_local + 1))
-    basis_vecs = S.query(sscg.QUERY_BASIS_VECTORS)       # (4s-3), or 46 at s = 16 with K1F pairs
-    fused = bool(S.query(sscg.QUERY_BASIS_FUSED))
+    basis_vecs = S.query(sscg.QUERY_BASIS_VECTORS)       # (4s-3) single steps, fewer with pairs / triples
+    depth = S.query(sscg.QUERY_BASIS_FUSED)               # basis steps per launch: 1, 2 (K1F) or 3 (K1M)
+    fused = depth > 1
     upd_vecs = S.query(sscg.QUERY_UPDATE_VECTORS)        # 2s+3, or s+4 with W alpha from the recurrence
     gram_vecs = S.query(sscg.QUERY_GRAM_VECTORS)         # 2s, or s+1 with W recovered from the recurrence
     bytes_per_outer = {"basis": basis_vecs * vec + s * face_bytes, "gram": gram_vecs * vec,
@@ -338,20 +339,22 @@ def run_ours(a):
     k1 = kern["basis"]
     path_bytes = sum(bytes_per_outer.values())
     cfg = workload(a, world)
-    k1_name = "k1f" if fused else K1_NAME
+    k1_name = {3: "k1m", 2: "k1f"}.get(depth, K1_NAME)
     # read : write vectors of one interior basis launch (W recovered in the Gram pass: p only)
     wfree = gram_vecs < 2 * s
-    mixrw = ((2, 2) if wfree else (2, 4)) if fused else ((2, 1) if wfree else (2, 2))
+    mixrw = (2, depth) if wfree else (2, 2 * depth)
     mc = mix_ceiling(*mixrw)
     roof = {"bound": "hbm", "kernel": "K1 %s<%s> (%sSpMV + Jacobi + Chebyshev recurrence)"
-                                      % (k1_name, a.kind, "two basis steps per launch: " if fused else ""),
+                                      % (k1_name, a.kind, {3: "three basis steps per launch: ",
+                                                           2: "two basis steps per launch: "}.get(depth, "")),
             "achieved": k1["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": k1["frac"],
             "traffic": ncu_traffic(n, k1_name) if a.workload == "cfg5" else None, "peak_source": peak_src,
             "traffic_note": "ncu dram read+write of one interior launch (algorithmic: %d vectors = %.4g B)"
                             % (sum(mixrw), sum(mixrw) * vec),
             "bytes_rule": "%d FP64 vectors per outer (%s) + s face sets for varcoef7, / basis launches (SURVEY 8(d)); "
                           "path: basis + %d (Gram) + %d (update) vectors"
-                          % (basis_vecs, "K1F pairs" if fused else "single steps", gram_vecs, upd_vecs),
+                          % (basis_vecs, {3: "K1M triples", 2: "K1F pairs"}.get(depth, "single steps"), gram_vecs,
+                             upd_vecs),
             "mix": "%d reads : %d writes per launch" % mixrw,
             "mix_ceiling_gbs": mc[0], "mix_ceiling_source": mc[1],
             "frac_of_mix_ceiling": (k1["achieved_gbs"] / mc[0]) if (mc[0] and k1["achieved_gbs"]) else None,

@@ -278,8 +278,10 @@ enum { SSCG_BASIS_CHEBYSHEV = 0, SSCG_BASIS_MONOMIAL = 1 };
 SSCG_API sscg_status sscg_set_option(sscg_ctx *ctx, int32_t key, int32_t value);
 
 /* Introspection of the schedule the context runs (host, no GPU work):
- *   SSCG_QUERY_BASIS_FUSED    1 if basis steps run in pairs (K1F: p_{j+1}
- *                             kept on chip, single-slab 7-point), else 0
+ *   SSCG_QUERY_BASIS_FUSED    basis steps per launch of the schedule's main
+ *                             basis kernel: 3 (K1M triples, p_{j+1}, p_{j+2}
+ *                             kept on chip; one 7-point slab), 2 (K1F pairs),
+ *                             1 (single steps)
  *   SSCG_QUERY_BASIS_VECTORS  FP64 vectors of n_local the basis kernels read
  *                             and write per outer iteration (algorithmic;
  *                             variable-coefficient face arrays not included)

@@ -1,0 +1,417 @@
+// K1M -- three basis steps in one pass (7-point): steps j, j+1, j+2 of the
+// Chebyshev recurrence
+//   w_j = A p_j,  p_{j+1} = c_j (D^{-1} w_j - sigma p_j) [- p_{j-1}],
+// and the same for j+1 and j+2, with p_{j+1} and p_{j+2} kept on chip
+// (matrix-powers blocking of depth 3).  Per triple it
+// streams p_j and p_{j-1} in and p_{j+1}, p_{j+2}, p_{j+3} out (w only where
+// the schedule stores it): 5 vectors for three steps instead of 6 for a K1F
+// pair plus half of the next one.
+//
+// Same per-point arithmetic, operand for operand, as K1T/K1F.  Level l = 1..3
+// computes step j+l-1 on the tile (56 x 16) plus a (3-l)-cell halo in y and a
+// 2(3-l)-cell halo in x (x work is done in pairs of cells); p_j is staged by
+// TMA with a 3-cell y / 6-cell x halo.  Cells outside the grid are forced to
+// the Dirichlet value 0, planes outside [1, nzl] likewise.
+//
+// Thread map: consumer warp r (1..20) owns box row r, lane l the cell pair
+// at box column 2 + 2l -- every thread computes all the levels its cell
+// belongs to, so the z-columns p_j(q-1..q+1), p_{j+1}(q-2..q) and
+// p_{j+2}(q-3..q-1) of its own cell roll through registers; only in-plane
+// neighbours come from shared memory (rings U1, U2 of the level-1/2
+// outputs).  Plane q of the march runs level 1 at q, level 2 at q-1, level 3
+// at q-2.  U1/U2 planes are published through per-plane mbarriers (every
+// consumer thread arrives); with 4 slots per ring a thread that waited for
+// U1(q-2) / U2(q-3) knows every read of the slot it overwrites is done.
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include "sscg_internal.cuh"
+#include "tma.cuh"
+
+namespace sscg {
+namespace {
+
+constexpr int TX = 56, TY = 16;
+constexpr int BW = TX + 12;    // p_j box: x in [x0-6, x0+TX+6)  (68)
+constexpr int BHP = TY + 6;    // p_j box: y in [y0-3, y0+TY+3)  (22)
+constexpr int MW = TX + 8;     // p_{j-1} box: x in [x0-4, x0+TX+4) (64), the level-1 cells
+constexpr int MH = TY + 4;     // y in [y0-2, y0+TY+2) (20)
+constexpr int U1H = TY + 4;    // level-1 rows 1..TY+4 of the p_j box, pitch BW
+constexpr int U2H = TY + 2;    // level-2 rows 2..TY+3
+constexpr int r128(int d) { return ((d * 8 + 127) / 128) * 128 / 8; }
+constexpr int PS = r128(BW * BHP), MS = r128(MW * MH), U1S = r128(BW * U1H), U2S = r128(BW * U2H);
+constexpr int NSP = 8, NSM = 4, NU = 4;   // powers of two (slot = seq & (N - 1))
+constexpr int NCW = TY + 4;               // one consumer warp per level-1 row
+constexpr int NCT = NCW * 32;
+constexpr int THREADS = NCT + 32;
+constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = MW * MH * 8;
+constexpr size_t SMEM = (size_t)(NSP * PS + NSM * MS + NU * U1S + NU * U2S) * sizeof(double);
+static_assert(SMEM <= 227 * 1024, "shared memory");
+static_assert(BW / 2 - 2 == 32, "one lane per level-1 pair");
+
+struct K1MWork {
+    int tiles_x, tiles_y, zc;
+    int64_t nitems;
+    int nzl;
+    int zb[3], ze[3];      // write range of each level (level 3's range is the one chunked)
+    int j;                 // vector coordinate of p_j in the tensor maps
+    int front_pm;          // level 1 subtracts p_{j-1} (j >= 1)
+    double coef1, coef, sigma, center, dinv_c;
+};
+
+struct Outs {
+    double *w[3], *pn[3];  // null: not stored
+};
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int x, int y, int z, int v,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(v), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v)
+{
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
+__device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+
+struct ItemPlan {
+    int tx, ty, zlo, zhi;      // level-3 planes [zlo, zhi)
+    int q0, q1;                // march: level-1 planes q0..q1
+    int plo, phi, mlo, mhi;    // p_j / p_{j-1} planes loaded
+    int first, last;           // first / last chunk (levels 1, 2 write their range's ends)
+};
+
+__device__ __forceinline__ ItemPlan plan_item(const K1MWork &wk, int64_t item)
+{
+    const int ntiles = wk.tiles_x * wk.tiles_y;
+    const int chunk = (int)(item / ntiles);
+    const int tile = (int)(item - (int64_t)chunk * ntiles);
+    ItemPlan p;
+    p.ty = tile / wk.tiles_x;
+    p.tx = tile - p.ty * wk.tiles_x;
+    p.zlo = wk.zb[2] + chunk * wk.zc;
+    p.zhi = min(wk.ze[2], p.zlo + wk.zc);
+    p.first = p.zlo == wk.zb[2];
+    p.last = p.zhi == wk.ze[2];
+    p.q0 = max(p.zlo - 2, 0);
+    p.q1 = p.zhi + 1;   // level 3 reaches zhi - 1 at q = zhi + 1 (level 1 is outside past nzl)
+    p.plo = max(p.q0 - 1, 0);
+    p.phi = min(p.q1 + 1, wk.nzl + 1);
+    p.mlo = max(p.q0, 1);
+    p.mhi = min(p.q1, wk.nzl);
+    return p;
+}
+
+// 7-point A p on the pair at smem offset o of plane P0, own z-neighbours given
+__device__ __forceinline__ double2 stencil(const double *P0, int o, double2 c, double2 dn, double2 up, double center)
+{
+    const double2 ylo = lds2(P0 + o - BW), yhi = lds2(P0 + o + BW);
+    const double l = P0[o - 1], rr = P0[o + 2];
+    double2 Ap;
+    Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+    Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+    return Ap;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k1m(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, Outs out,
+        const DevState *st, K1MWork wk)
+{
+    if (st && st->done) return;
+    extern __shared__ __align__(128) double smem[];
+    double *sp = smem;                 // p_j ring
+    double *sm = sp + NSP * PS;        // p_{j-1} ring
+    double *su1 = sm + NSM * MS;       // level-1 outputs (p_{j+1})
+    double *su2 = su1 + NU * U1S;      // level-2 outputs (p_{j+2})
+    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM], u1full[NU], u2full[NU];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int i = 0; i < NSP; ++i) {
+            mbar_init(&fullp[i], 1);
+            mbar_init(&emptyp[i], NCT);
+        }
+        for (int i = 0; i < NSM; ++i) {
+            mbar_init(&fullm[i], 1);
+            mbar_init(&emptym[i], NCT);
+        }
+        for (int i = 0; i < NU; ++i) {
+            mbar_init(&u1full[i], NCT);
+            mbar_init(&u2full[i], NCT);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmP);
+        tma_prefetch_desc(&tmM);
+    }
+    __syncthreads();
+
+    if (warp == 0) {   // producer: p_j planes [plo, phi] and p_{j-1} planes [mlo, mhi] in march order
+        if (lane == 0) {
+            uint32_t pc = 0, mc = 0;
+            for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+                const ItemPlan it = plan_item(wk, item);
+                const int x0 = it.tx * TX, y0 = it.ty * TY;
+                int pnext = it.plo;
+                for (int q = it.q0; q <= it.q1; ++q) {
+                    while (pnext <= min(q + 1, it.phi)) {
+                        const int sl = pc & (NSP - 1);
+                        if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
+                        mbar_expect_tx(&fullp[sl], PBYTES);
+                        tma_load_4d(sp + sl * PS, &tmP, x0 - 6, y0 - 3, pnext, wk.j, &fullp[sl]);
+                        ++pc;
+                        ++pnext;
+                    }
+                    if (wk.front_pm && q >= it.mlo && q <= it.mhi) {
+                        const int sl = mc & (NSM - 1);
+                        if (mc >= NSM) mbar_wait(&emptym[sl], ((mc / NSM) - 1) & 1);
+                        mbar_expect_tx(&fullm[sl], MBYTES);
+                        tma_load_4d(sm + sl * MS, &tmM, x0 - 4, y0 - 2, q, wk.j - 1, &fullm[sl]);
+                        ++mc;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    const int rk = warp, ck = 2 + 2 * lane;                  // box row 1..20, column 2..64
+    const int ok = rk * BW + ck;                             // p_j slot offset
+    const int o1 = (rk - 1) * BW + ck;                       // U1 offset (rows from 1)
+    const int o2 = (rk - 2) * BW + ck;                       // U2 offset (rows from 2)
+    const int om = (rk - 1) * MW + (ck - 2);                 // p_{j-1} offset
+    const bool in2 = rk >= 2 && rk <= TY + 3 && lane >= 1 && lane <= 30;   // level-2 cell
+    const bool in3 = rk >= 3 && rk <= TY + 2 && lane >= 2 && lane <= 29;   // level 3 = the tile
+    const bool front_pm = wk.front_pm;
+    const int nzl = wk.nzl;
+    const double center = wk.center, dinv_c = wk.dinv_c, sigma = wk.sigma, cf1 = wk.coef1, cf = wk.coef;
+    const int64_t pl = g.plane;
+    const uint32_t fp_a = pin_u32(smem_u32(fullp)), ep_a = pin_u32(smem_u32(emptyp)),
+                   fm_a = pin_u32(smem_u32(fullm)), em_a = pin_u32(smem_u32(emptym)),
+                   u1_a = pin_u32(smem_u32(u1full)), u2_a = pin_u32(smem_u32(u2full));
+    uint32_t pc = 0, mc = 0, uc = 0;   // p_j / p_{j-1} / U sequence numbers
+    for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+        const ItemPlan it = plan_item(wk, item);
+        const int x0 = it.tx * TX, y0 = it.ty * TY;
+        const int gx = x0 - 6 + ck, gy = y0 - 3 + rk;
+        const bool vy = gy >= 0 && gy < g.ny;
+        const bool v0 = vy && gx >= 0 && gx < g.nx, v1 = vy && gx + 1 >= 0 && gx + 1 < g.nx;
+        const bool own = in3 && v0;   // the tile's own cell: outputs go to HBM
+        // write ranges of this item per level
+        const int wb1 = it.first ? wk.zb[0] : it.zlo, we1 = it.last ? wk.ze[0] : it.zhi;
+        const int wb2 = it.first ? wk.zb[1] : it.zlo, we2 = it.last ? wk.ze[1] : it.zhi;
+        const uint32_t pbase = pc;
+        auto slotp = [&](int z) -> const double * {
+            return sp + ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1)) * PS;
+        };
+        auto release = [&](int z) { mbar_arrive_a(ep_a + 8 * ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1))); };
+        auto waitp = [&](int z) {
+            const uint32_t c = pbase + (uint32_t)(z - it.plo);
+            mbar_wait_a(fp_a + 8 * (c & (NSP - 1)), (c / NSP) & 1);
+        };
+        for (int z = it.plo; z <= min(it.q0, it.phi); ++z) waitp(z);
+        double2 pdn = make_double2(0.0, 0.0);     // p_j(q-1), own cell
+        if (it.q0 - 1 >= it.plo) {
+            pdn = lds2(slotp(it.q0 - 1) + ok);
+            release(it.q0 - 1);
+        }
+        double2 pc0 = lds2(slotp(it.q0) + ok);   // p_j(q)
+        double2 u1m2 = make_double2(0.0, 0.0), u1m1 = make_double2(0.0, 0.0);   // p_{j+1}(q-2), (q-1)
+        double2 u2m2 = make_double2(0.0, 0.0), u2m1 = make_double2(0.0, 0.0);   // p_{j+2}(q-3), (q-2)
+        int64_t off = (int64_t)it.q0 * pl + (int64_t)gy * g.pitch + gx;   // global index, plane q
+        for (int q = it.q0; q <= it.q1; ++q, off += pl) {
+            // ---------------- level 1: step j at plane q ----------------
+            const bool inside1 = q >= 1 && q <= nzl;
+            double2 pup = make_double2(0.0, 0.0);   // p_j(q+1)
+            if (q + 1 <= it.phi) {
+                if (q + 1 > it.q0) waitp(q + 1);
+                pup = lds2(slotp(q + 1) + ok);
+            }
+            const bool mloaded = front_pm && q >= it.mlo && q <= it.mhi;
+            const uint32_t ms = mc & (NSM - 1);
+            if (mloaded) mbar_wait_a(fm_a + 8 * ms, (mc / NSM) & 1);
+            double2 u1 = make_double2(0.0, 0.0);
+            if (inside1) {
+                const double2 c = pc0;
+                double2 Ap = stencil(slotp(q), ok, c, pdn, pup, center);
+                u1.x = cf1 * (dinv_c * Ap.x - sigma * c.x);
+                u1.y = cf1 * (dinv_c * Ap.y - sigma * c.y);
+                if (mloaded) {
+                    const double2 pm = lds2(sm + ms * MS + om);
+                    u1.x -= pm.x;
+                    u1.y -= pm.y;
+                }
+                if (!v0) u1.x = 0.0;
+                if (!v1) u1.y = 0.0;
+                if (own && q >= wb1 && q < we1) {
+                    if (!v1) Ap.y = 0.0;
+                    if (out.w[0]) __stcs(reinterpret_cast<double2 *>(out.w[0] + off), Ap);
+                    if (out.pn[0]) *reinterpret_cast<double2 *>(out.pn[0] + off) = u1;
+                }
+            }
+            *reinterpret_cast<double2 *>(su1 + (uc & (NU - 1)) * U1S + o1) = u1;
+            mbar_arrive_a(u1_a + 8 * (uc & (NU - 1)));
+            if (mloaded) {
+                mbar_arrive_a(em_a + 8 * ms);
+                ++mc;
+            }
+            if (q >= it.plo && q <= it.phi) release(q);
+            // ---------------- level 2: step j+1 at plane q-1 ----------------
+            const int z2 = q - 1;
+            double2 u2 = make_double2(0.0, 0.0);
+            if (uc > 0) mbar_wait_a(u1_a + 8 * ((uc - 1) & (NU - 1)), ((uc - 1) / NU) & 1);
+            if (in2 && z2 >= 1 && z2 <= nzl) {
+                const double *U = su1 + ((uc - 1) & (NU - 1)) * U1S;
+                const double2 c = u1m1;
+                double2 Ap = stencil(U, o1, c, u1m2, u1, center);
+                u2.x = cf * (dinv_c * Ap.x - sigma * c.x) - pdn.x;   // pdn = p_j(q-1)
+                u2.y = cf * (dinv_c * Ap.y - sigma * c.y) - pdn.y;
+                if (!v0) u2.x = 0.0;
+                if (!v1) u2.y = 0.0;
+                if (own && z2 >= wb2 && z2 < we2) {
+                    if (!v1) Ap.y = 0.0;
+                    if (out.w[1]) __stcs(reinterpret_cast<double2 *>(out.w[1] + off - pl), Ap);
+                    if (out.pn[1]) *reinterpret_cast<double2 *>(out.pn[1] + off - pl) = u2;
+                }
+            }
+            if (in2 && uc > 0) *reinterpret_cast<double2 *>(su2 + ((uc - 1) & (NU - 1)) * U2S + o2) = u2;
+            if (uc > 0) mbar_arrive_a(u2_a + 8 * ((uc - 1) & (NU - 1)));
+            // ---------------- level 3: step j+2 at plane q-2 ----------------
+            const int z3 = q - 2;
+            if (uc > 1) mbar_wait_a(u2_a + 8 * ((uc - 2) & (NU - 1)), ((uc - 2) / NU) & 1);
+            if (own && z3 >= it.zlo && z3 < it.zhi) {
+                const double *U = su2 + ((uc - 2) & (NU - 1)) * U2S;
+                const double2 c = u2m1;
+                double2 Ap = stencil(U, o2, c, u2m2, u2, center);
+                if (!v1) Ap.y = 0.0;
+                if (out.w[2]) __stcs(reinterpret_cast<double2 *>(out.w[2] + off - 2 * pl), Ap);
+                if (out.pn[2]) {
+                    const double v0b = cf * (dinv_c * Ap.x - sigma * c.x) - u1m2.x;   // u1m2 = p_{j+1}(q-2)
+                    double v1b = cf * (dinv_c * Ap.y - sigma * c.y) - u1m2.y;
+                    if (!v1) v1b = 0.0;
+                    *reinterpret_cast<double2 *>(out.pn[2] + off - 2 * pl) = make_double2(v0b, v1b);
+                }
+            }
+            ++uc;
+            u2m2 = u2m1;
+            u2m1 = u2;
+            u1m2 = u1m1;
+            u1m1 = u1;
+            pdn = pc0;
+            pc0 = pup;
+        }
+        for (int z = max(it.q1 + 1, it.plo); z <= it.phi; ++z) release(z);
+        pc = pbase + (it.phi - it.plo + 1);
+    }
+}
+
+}  // namespace
+
+bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+        return false;
+    auto enc = reinterpret_cast<CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                             CUtensorMapFloatOOBfill)>(fn);
+    cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)(nzl + 2), (cuuint64_t)s};
+    cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.vstride * 8};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint32_t boxp[4] = {BW, BHP, 1, 1}, boxm[4] = {MW, MH, 1, 1};
+    if (enc(tmP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxp, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (enc(tmM, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxm, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    return cudaFuncSetAttribute(k1m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+}
+
+// SSCG_K1_MP3 (read at every sscg_setup): "1" enables the triples for 7-point
+// single-slab solves; default off.  Measured at cfg 5 (profiles/r01s_*): one
+// triple takes 1.006 ms against 0.53 ms per K1F pair (0.335 vs 0.266 ms per
+// basis step) -- the byte saving (26 vs 31 vectors per outer) is lost to
+// instruction issue: the level-1/2 halos add redundant stencil work (1.21 vs
+// 1.10 evaluations per output point and step) and the kernel is issue-bound
+// (62 % issue-active, 12 % of the instructions FP64 arithmetic).
+bool k1m_enabled(const Geo &g, int nzl)
+{
+    const char *e = getenv("SSCG_K1_MP3");
+    if (!(e && e[0] == '1')) return false;
+    (void)nzl;
+    return g.kind == 1;
+}
+
+// steps j, j+1, j+2 of one slab.  a.zb[l] / a.ze[l]: planes level l writes
+// (level 3's range is split into z-chunks; levels 1 and 2 may extend it at
+// either end by up to 2 / 1 planes).  The tensor maps view P with the vector
+// index as the 4th coordinate, so one pair of maps serves every j.
+void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st, cudaStream_t strm)
+{
+    K1MWork wk;
+    wk.tiles_x = (g.nx + TX - 1) / TX;
+    wk.tiles_y = (g.ny + TY - 1) / TY;
+    wk.nzl = a.nzl;
+    for (int l = 0; l < 3; ++l) {
+        wk.zb[l] = a.zb[l];
+        wk.ze[l] = a.ze[l];
+    }
+    wk.j = a.j;
+    wk.front_pm = a.j > 0;
+    wk.coef1 = (a.j == 0) ? theta : 2.0 * theta;
+    wk.coef = 2.0 * theta;
+    wk.sigma = a.sigma;
+    wk.center = g.center;
+    wk.dinv_c = g.dinv_c;
+    Outs out;
+    for (int l = 0; l < 3; ++l) {
+        out.w[l] = a.w[l];
+        out.pn[l] = a.pn[l];
+    }
+    const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
+    const int64_t resident = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
+    static int zc_env = -1;
+    if (zc_env < 0) {
+        const char *e = getenv("SSCG_K1_ZC");
+        zc_env = e ? std::max(1, atoi(e)) : 0;
+    }
+    const int n1 = a.ze[2] - a.zb[2];
+    if (n1 <= 0) return;
+    int zc = n1;
+    if (zc_env > 0) {
+        zc = std::min(n1, zc_env);
+    } else {
+        // each chunk re-reads 5 planes of p_j and recomputes 4 level-1/2 planes:
+        // few long chunks, tiles x chunks filling whole waves
+        double best = -1.0;
+        for (int nch = 1; nch <= 64 && (n1 + nch - 1) / nch >= 6; ++nch) {
+            const int z = (n1 + nch - 1) / nch;
+            const int64_t items = tiles * ((n1 + z - 1) / z);
+            const int64_t waves = (items + resident - 1) / resident;
+            const double score = (double)items / (double)(waves * resident) / (1.0 + 2.0 / z);
+            if (score > best + 1e-9) {
+                best = score;
+                zc = z;
+            }
+        }
+    }
+    wk.zc = zc;
+    wk.nitems = tiles * ((n1 + zc - 1) / zc);
+    const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
+    k1m<<<grid, THREADS, SMEM, strm>>>(*a.tmP, *a.tmM, g, out, st, wk);
+}
+
+}  // namespace sscg

@@ -330,6 +330,11 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused basis step");
             sl.has_k1f = true;
         }
+        if (A->kind == SSCG_OP_STENCIL7 && !diag_M && k1m_enabled(g, sl.nzl)) {
+            if (!k1m_prepare(g, sl.P, sl.nzl, s, &sl.tmM3_P, &sl.tmM3_M))
+                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the depth-3 basis step");
+            sl.has_k1m = true;
+        }
         if (A->kind == SSCG_OP_VARCOEF7) {
             sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
             sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;
@@ -661,6 +666,42 @@ static bool uses_fused(const sscg_ctx *c)
     return true;
 }
 
+// K1M triples (three basis steps per launch): 7-point, one slab without
+// neighbours (with halos the pairs' boundary schedule is used)
+static bool uses_mp3(const sscg_ctx *c)
+{
+    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->g.kind != SSCG_OP_STENCIL7) return false;
+    if (c->slabs.size() != 1 || c->nranks > 1) return false;
+    return c->slabs[0].has_k1m;
+}
+
+static sscg_status launch_basis_triple(sscg_ctx *c, int j)
+{
+    const Geo &g = c->g;
+    const int s = c->s;
+    const bool wf = uses_wfree(c);
+    for (auto &sl : c->slabs) {
+        K1MArgs a{};
+        for (int l = 0; l < 3; ++l) {
+            const int jl = j + l;   // step of level l+1
+            a.w[l] = (!wf || jl == s - 1) ? sl.W + (int64_t)jl * g.vstride : nullptr;
+            a.pn[l] = (jl + 1 <= s - 1) ? sl.P + (int64_t)(jl + 1) * g.vstride : nullptr;
+            a.zb[l] = 1;
+            a.ze[l] = sl.nzl + 1;
+        }
+        a.nzl = sl.nzl;
+        a.j = j;
+        a.sigma = c->sigma;
+        a.tmP = &sl.tmM3_P;
+        a.tmM = &sl.tmM3_M;
+        TRY(prof_mark(c, SSCG_PROF_BASIS, true));
+        launch_k1m(g, a, c->theta, c->st, c->stream);
+        TRY(prof_mark(c, SSCG_PROF_BASIS, false));
+        ++c->launches;
+    }
+    return SSCG_OK;
+}
+
 // K1F: basis steps j, j+1 in one launch per slab, over all planes (part 0,
 // a slab bounded by the global Dirichlet planes) or the planes [2, nzl) that
 // need no halo of p_{j+1} (part 2)
@@ -704,10 +745,13 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const int L = (int)c->slabs.size();
     const bool halo = (L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR;
     const bool ovl = halo && c->overlap;
-    const bool fuse = uses_fused(c);
+    const bool fuse = uses_fused(c), mp3 = uses_mp3(c);
     nvtxRangePushA("basis");
     for (int j = 0; j < s; ++j) {
-        if (fuse && j + 1 < s) {   // steps j and j+1 in one pass (K1F)
+        if (mp3 && j + 2 < s) {   // steps j, j+1, j+2 in one pass (K1M; no halos)
+            TRY(launch_basis_triple(c, j));
+            j += 2;
+        } else if (fuse && j + 1 < s) {   // steps j and j+1 in one pass (K1F)
             if (!halo) {
                 TRY(launch_basis_pair(c, j, 0));
             } else {
@@ -1348,15 +1392,21 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
     const int s = c->s;
     const bool mono = c->basis == SSCG_BASIS_MONOMIAL;
     switch (what) {
-    case SSCG_QUERY_BASIS_FUSED:
-        *out = uses_fused(c) ? 1 : 0;
+    case SSCG_QUERY_BASIS_FUSED:   // basis steps per launch of the schedule's main kernel
+        *out = uses_mp3(c) ? 3 : uses_fused(c) ? 2 : 1;
         return SSCG_OK;
     case SSCG_QUERY_BASIS_VECTORS: {
         // FP64 vectors of n_local read + written by the basis steps of one outer
         const bool wf = uses_wfree(c);
         auto wst = [&](int j) { return (!wf || j == s - 1) ? 1 : 0; };   // w_j stored?
         int64_t v = 0;
-        if (uses_fused(c)) {
+        if (uses_mp3(c)) {
+            int j = 0;
+            for (; j + 2 < s; j += 3)   // p_j, p_{j-1} in; p_{j+1..j+3} and stored w out
+                v += 1 + (j > 0) + (j + 1 < s) + (j + 2 < s) + (j + 3 < s) + wst(j) + wst(j + 1) + wst(j + 2);
+            if (j + 1 < s) { v += 1 + (j > 0) + 1 + (j + 2 < s) + wst(j) + wst(j + 1); j += 2; }   // a K1F pair
+            if (j < s) v += 1 + (j > 0 && j < s - 1) + wst(j) + (j < s - 1);                       // a single step
+        } else if (uses_fused(c)) {
             int j = 0;
             for (; j + 1 < s; j += 2) v += 1 + (j > 0) + 1 + (j + 2 < s) + wst(j) + wst(j + 1);
             if (j < s) v += 2;   // odd s: the last step alone (mode 0: reads p_{s-1}, writes w_{s-1})

@@ -51,6 +51,8 @@ struct Slab {
     CUtensorMap tmP4, tmM4;       // K1T: 4-D [x][y][plane][vector] views of P (halo box / tile box)
     bool has_k1t;
     CUtensorMap tmF_P, tmF_M;     // K1F: 2-cell / 1-cell halo boxes
+    CUtensorMap tmM3_P, tmM3_M;   // K1M (depth-3 basis): 3/6-cell and 2/4-cell halo boxes
+    bool has_k1m;
     CUtensorMap tmKX, tmKY, tmKZ; // K1T: variable-coefficient faces (nx even)
     bool has_ftma;
     bool has_k1f;
@@ -111,6 +113,19 @@ bool k1t_prepare_faces(const Geo &g, const double *kx, const double *ky, const d
 
 // K1F: two 7-point basis steps per launch, single slab (k_stencil_fused.cu)
 bool k1f_enabled(const Geo &g, int nzl);
+
+// K1M: three basis steps per launch (7-point, constant diagonal; k_stencil_mp3.cu)
+struct K1MArgs {
+    double *w[3];          // w_j, w_{j+1}, w_{j+2} (null: not stored)
+    double *pn[3];         // p_{j+1}, p_{j+2}, p_{j+3} (null: not stored)
+    int zb[3], ze[3];      // padded planes each level writes
+    int nzl, j, sm_cap;
+    double sigma;
+    const CUtensorMap *tmP, *tmM;
+};
+bool k1m_enabled(const Geo &g, int nzl);
+bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM);
+void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st, cudaStream_t strm);
 bool k1f_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM);
 void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm);
 

@@ -278,11 +278,12 @@ def test_fused_pairs_match_single_steps(cfg, slabs, monkeypatch):
     kind, nx, ny, nz, s, nu = cfg
     P = Problem(kind, nx, ny, nz, s, nu)
     out = {}
+    monkeypatch.setenv("SSCG_K1_MP3", "0")   # pairs here; triples: test_triples_match_single_steps
     for fuse in ("1", "0"):
         monkeypatch.setenv("SSCG_K1_FUSE", fuse)
         import paper_2512_09642_b200 as sscg
         with P.gpu_solver(slabs=slabs) as S:
-            assert S.query(sscg.QUERY_BASIS_FUSED) == (1 if fuse == "1" else 0)
+            assert S.query(sscg.QUERY_BASIS_FUSED) == (2 if fuse == "1" else 1)
             x = S.solve(P.b_gpu(), rtol=0.0, max_outer=4).cpu().numpy()
             out[fuse] = (x, S.gram(0)[0], [S.basis(j) for j in range(s)])
     a, b = out["1"], out["0"]
@@ -292,6 +293,38 @@ def test_fused_pairs_match_single_steps(cfg, slabs, monkeypatch):
             assert rel_inf(a[2][j][q], b[2][j][q]) <= 1e-12
     assert np.linalg.norm(a[0] - b[0]) <= 1e-11 * np.linalg.norm(b[0])
     x_or, _ = P.oracle(max_outer=4)
+    assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+@pytest.mark.parametrize("cfg", [("7pt", 40, 36, 33, 16, 25), ("7pt", 64, 40, 30, 9, 20), ("7pt", 60, 49, 23, 11, 20),
+                                 ("7pt", 112, 33, 70, 3, 10), ("7pt", 26, 24, 22, 8, 20)], ids=_ids)
+def test_triples_match_single_steps(cfg, monkeypatch):
+    """K1M (three basis steps per launch, p_{j+1} and p_{j+2} on chip) against
+    K1T single steps and K1F pairs: the same arithmetic per point, so basis,
+    Gram and x agree to rounding; s = 16 / 9 / 11 / 3 / 8 end with a single
+    step, a pair, or nothing after the triples; ragged tiles in x and y and
+    z-chunks of several lengths.  All agree with the oracle."""
+    import paper_2512_09642_b200 as sscg
+    kind, nx, ny, nz, s, nu = cfg
+    P = Problem(kind, nx, ny, nz, s, nu)
+    out = {}
+    for mode, env in (("mp3", {"SSCG_K1_MP3": "1", "SSCG_K1_FUSE": "1"}), ("pairs", {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "1"}),
+                      ("single", {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "0"})):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with P.gpu_solver() as S:
+            assert S.query(sscg.QUERY_BASIS_FUSED) == {"mp3": 3, "pairs": 2, "single": 1}[mode]
+            x = S.solve(P.b_gpu(), rtol=0.0, max_outer=4).cpu().numpy()
+            out[mode] = (x, S.gram(0)[0], [S.basis(j) for j in range(s)], S.gram(4)[0])
+    a = out["mp3"]
+    for ref in ("pairs", "single"):
+        b = out[ref]
+        assert np.max(np.abs(a[1] - b[1])) <= 1e-13 * np.max(np.abs(b[1])), ref
+        for j in range(s):
+            for q in range(2):
+                assert rel_inf(a[2][j][q], b[2][j][q]) <= 1e-12, (ref, j, q)
+        assert np.linalg.norm(a[0] - b[0]) <= 1e-11 * np.linalg.norm(b[0]), ref
+    x_or, tr = P.oracle(max_outer=4, dump_iter=0)
     assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
 
 

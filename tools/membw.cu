@@ -68,6 +68,7 @@ int main()
     run<2, 4>(in, out, n2, stride2, sms);    // K1F (per pair)
     run<5, 2>(in, out, n2, stride2, sms);    // K1T variable coefficients (3 face streams)
     run<2, 1>(in, out, n2, stride2, sms);    // K1T, W not stored (W-free schedule)
+    run<2, 3>(in, out, n2, stride2, sms);    // K1M triple, W-free
     run<16, 0>(in, out, n2, stride2, sms);
     run<18, 0>(in, out, n2, stride2, sms);   // K2R (s = 16: 17 basis + w_last)
     run<18, 2>(in, out, n2, stride2, sms);   // K5, W-free schedule (s = 16)
