@@ -41,12 +41,13 @@ constexpr int U1H = TY + 4;    // level-1 rows 1..TY+4 of the p_j box, pitch BW
 constexpr int U2H = TY + 2;    // level-2 rows 2..TY+3
 constexpr int r128(int d) { return ((d * 8 + 127) / 128) * 128 / 8; }
 constexpr int PS = r128(BW * BHP), MS = r128(MW * MH), U1S = r128(BW * U1H), U2S = r128(BW * U2H);
-constexpr int NSP = 8, NSM = 4, NU = 4;   // powers of two (slot = seq & (N - 1))
+constexpr int STG = PS + MS;              // one stage: p_j(z) and p_{j-1}(z-1), one barrier
+constexpr int NST = 4, NU = 4;            // powers of two (slot = seq & (N - 1))
 constexpr int NCW = TY + 4;               // one consumer warp per level-1 row
 constexpr int NCT = NCW * 32;
 constexpr int THREADS = NCT + 32;
 constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = MW * MH * 8;
-constexpr size_t SMEM = (size_t)(NSP * PS + NSM * MS + NU * U1S + NU * U2S) * sizeof(double);
+constexpr size_t SMEM = (size_t)(NST * STG + NU * U1S + NU * U2S) * sizeof(double);
 static_assert(SMEM <= 227 * 1024, "shared memory");
 static_assert(BW / 2 - 2 == 32, "one lane per level-1 pair");
 
@@ -128,54 +129,36 @@ __global__ void __launch_bounds__(THREADS, 1)
 {
     if (st && st->done) return;
     extern __shared__ __align__(128) double smem[];
-    double *sp = smem;                 // p_j ring
-    double *sm = sp + NSP * PS;        // p_{j-1} ring
-    double *su1 = sm + NSM * MS;       // level-1 outputs (p_{j+1})
-    double *su2 = su1 + NU * U1S;      // level-2 outputs (p_{j+2})
-    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM], u1full[NU], u2full[NU];
+    double *sstg = smem;                 // stages: [p_j(z) box | p_{j-1}(z-1) box]
+    double *su1 = sstg + NST * STG;      // level-1 outputs (p_{j+1})
+    double *su2 = su1 + NU * U1S;        // level-2 outputs (p_{j+2})
+    __shared__ uint64_t full[NST], empty[NST], ubar[NU];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int i = 0; i < NSP; ++i) {
-            mbar_init(&fullp[i], 1);
-            mbar_init(&emptyp[i], NCT);
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], NCT);
         }
-        for (int i = 0; i < NSM; ++i) {
-            mbar_init(&fullm[i], 1);
-            mbar_init(&emptym[i], NCT);
-        }
-        for (int i = 0; i < NU; ++i) {
-            mbar_init(&u1full[i], NCT);
-            mbar_init(&u2full[i], NCT);
-        }
+        for (int i = 0; i < NU; ++i) mbar_init(&ubar[i], NCT);
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
         tma_prefetch_desc(&tmM);
     }
     __syncthreads();
 
-    if (warp == 0) {   // producer: p_j planes [plo, phi] and p_{j-1} planes [mlo, mhi] in march order
+    if (warp == 0) {   // producer: stage z = p_j(z) [+ p_{j-1}(z-1)], z = plo..phi, in march order
         if (lane == 0) {
-            uint32_t pc = 0, mc = 0;
+            uint32_t sc = 0;
             for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
                 const ItemPlan it = plan_item(wk, item);
                 const int x0 = it.tx * TX, y0 = it.ty * TY;
-                int pnext = it.plo;
-                for (int q = it.q0; q <= it.q1; ++q) {
-                    while (pnext <= min(q + 1, it.phi)) {
-                        const int sl = pc & (NSP - 1);
-                        if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
-                        mbar_expect_tx(&fullp[sl], PBYTES);
-                        tma_load_4d(sp + sl * PS, &tmP, x0 - 6, y0 - 3, pnext, wk.j, &fullp[sl]);
-                        ++pc;
-                        ++pnext;
-                    }
-                    if (wk.front_pm && q >= it.mlo && q <= it.mhi) {
-                        const int sl = mc & (NSM - 1);
-                        if (mc >= NSM) mbar_wait(&emptym[sl], ((mc / NSM) - 1) & 1);
-                        mbar_expect_tx(&fullm[sl], MBYTES);
-                        tma_load_4d(sm + sl * MS, &tmM, x0 - 4, y0 - 2, q, wk.j - 1, &fullm[sl]);
-                        ++mc;
-                    }
+                for (int z = it.plo; z <= it.phi; ++z, ++sc) {
+                    const int sl = sc & (NST - 1);
+                    if (sc >= NST) mbar_wait(&empty[sl], ((sc / NST) - 1) & 1);
+                    const bool m = wk.front_pm && z - 1 >= it.mlo && z - 1 <= it.mhi;
+                    mbar_expect_tx(&full[sl], PBYTES + (m ? MBYTES : 0u));
+                    tma_load_4d(sstg + sl * STG, &tmP, x0 - 6, y0 - 3, z, wk.j, &full[sl]);
+                    if (m) tma_load_4d(sstg + sl * STG + PS, &tmM, x0 - 4, y0 - 2, z - 1, wk.j - 1, &full[sl]);
                 }
             }
         }
@@ -183,20 +166,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 
     const int rk = warp, ck = 2 + 2 * lane;                  // box row 1..20, column 2..64
-    const int ok = rk * BW + ck;                             // p_j slot offset
+    const int ok = rk * BW + ck;                             // p_j offset in a stage
+    const int omk = PS + (rk - 1) * MW + (ck - 2);           // p_{j-1} offset in a stage
     const int o1 = (rk - 1) * BW + ck;                       // U1 offset (rows from 1)
     const int o2 = (rk - 2) * BW + ck;                       // U2 offset (rows from 2)
-    const int om = (rk - 1) * MW + (ck - 2);                 // p_{j-1} offset
     const bool in2 = rk >= 2 && rk <= TY + 3 && lane >= 1 && lane <= 30;   // level-2 cell
     const bool in3 = rk >= 3 && rk <= TY + 2 && lane >= 2 && lane <= 29;   // level 3 = the tile
     const bool front_pm = wk.front_pm;
     const int nzl = wk.nzl;
     const double center = wk.center, dinv_c = wk.dinv_c, sigma = wk.sigma, cf1 = wk.coef1, cf = wk.coef;
+    double *const w0 = out.w[0], *const w1 = out.w[1], *const w2 = out.w[2];
+    double *const n0 = out.pn[0], *const n1 = out.pn[1], *const n2 = out.pn[2];
     const int64_t pl = g.plane;
-    const uint32_t fp_a = pin_u32(smem_u32(fullp)), ep_a = pin_u32(smem_u32(emptyp)),
-                   fm_a = pin_u32(smem_u32(fullm)), em_a = pin_u32(smem_u32(emptym)),
-                   u1_a = pin_u32(smem_u32(u1full)), u2_a = pin_u32(smem_u32(u2full));
-    uint32_t pc = 0, mc = 0, uc = 0;   // p_j / p_{j-1} / U sequence numbers
+    const uint32_t full_a = pin_u32(smem_u32(full)), empty_a = pin_u32(smem_u32(empty)),
+                   ubar_a = pin_u32(smem_u32(ubar));
+    uint32_t sc = 0, uc = 0;   // stage / U sequence numbers
     for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
         const ItemPlan it = plan_item(wk, item);
         const int x0 = it.tx * TX, y0 = it.ty * TY;
@@ -204,70 +188,68 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool vy = gy >= 0 && gy < g.ny;
         const bool v0 = vy && gx >= 0 && gx < g.nx, v1 = vy && gx + 1 >= 0 && gx + 1 < g.nx;
         const bool own = in3 && v0;   // the tile's own cell: outputs go to HBM
-        // write ranges of this item per level
         const int wb1 = it.first ? wk.zb[0] : it.zlo, we1 = it.last ? wk.ze[0] : it.zhi;
         const int wb2 = it.first ? wk.zb[1] : it.zlo, we2 = it.last ? wk.ze[1] : it.zhi;
-        const uint32_t pbase = pc;
-        auto slotp = [&](int z) -> const double * {
-            return sp + ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1)) * PS;
+        const uint32_t sbase = sc;   // sequence number of stage plo
+        auto stg = [&](int z) -> const double * {
+            return sstg + ((sbase + (uint32_t)(z - it.plo)) & (NST - 1)) * STG;
         };
-        auto release = [&](int z) { mbar_arrive_a(ep_a + 8 * ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1))); };
-        auto waitp = [&](int z) {
-            const uint32_t c = pbase + (uint32_t)(z - it.plo);
-            mbar_wait_a(fp_a + 8 * (c & (NSP - 1)), (c / NSP) & 1);
+        auto release = [&](int z) { mbar_arrive_a(empty_a + 8 * ((sbase + (uint32_t)(z - it.plo)) & (NST - 1))); };
+        auto waits = [&](int z) {
+            const uint32_t c = sbase + (uint32_t)(z - it.plo);
+            mbar_wait_a(full_a + 8 * (c & (NST - 1)), (c / NST) & 1);
         };
-        for (int z = it.plo; z <= min(it.q0, it.phi); ++z) waitp(z);
+        for (int z = it.plo; z <= min(it.q0, it.phi); ++z) waits(z);
         double2 pdn = make_double2(0.0, 0.0);     // p_j(q-1), own cell
         if (it.q0 - 1 >= it.plo) {
-            pdn = lds2(slotp(it.q0 - 1) + ok);
+            pdn = lds2(stg(it.q0 - 1) + ok);
             release(it.q0 - 1);
         }
-        double2 pc0 = lds2(slotp(it.q0) + ok);   // p_j(q)
+        double2 pc0 = lds2(stg(it.q0) + ok);     // p_j(q)
         double2 u1m2 = make_double2(0.0, 0.0), u1m1 = make_double2(0.0, 0.0);   // p_{j+1}(q-2), (q-1)
         double2 u2m2 = make_double2(0.0, 0.0), u2m1 = make_double2(0.0, 0.0);   // p_{j+2}(q-3), (q-2)
         int64_t off = (int64_t)it.q0 * pl + (int64_t)gy * g.pitch + gx;   // global index, plane q
-        for (int q = it.q0; q <= it.q1; ++q, off += pl) {
+        // one plane of the march; S: zlo + 2 <= q < zhi, where every plane
+        // condition below is known to hold
+        auto plane = [&](int q, auto steady) {
+            constexpr bool S = decltype(steady)::value;
             // ---------------- level 1: step j at plane q ----------------
-            const bool inside1 = q >= 1 && q <= nzl;
+            const bool inside1 = S || (q >= 1 && q <= nzl);
+            const bool has_up = S || q + 1 <= it.phi;
+            const double *P0 = stg(q), *P1 = stg(q + 1);
             double2 pup = make_double2(0.0, 0.0);   // p_j(q+1)
-            if (q + 1 <= it.phi) {
-                if (q + 1 > it.q0) waitp(q + 1);
-                pup = lds2(slotp(q + 1) + ok);
+            if (has_up) {
+                waits(q + 1);
+                pup = lds2(P1 + ok);
             }
-            const bool mloaded = front_pm && q >= it.mlo && q <= it.mhi;
-            const uint32_t ms = mc & (NSM - 1);
-            if (mloaded) mbar_wait_a(fm_a + 8 * ms, (mc / NSM) & 1);
+            const bool mloaded = front_pm && (S || (q >= it.mlo && q <= it.mhi));
             double2 u1 = make_double2(0.0, 0.0);
             if (inside1) {
                 const double2 c = pc0;
-                double2 Ap = stencil(slotp(q), ok, c, pdn, pup, center);
+                double2 Ap = stencil(P0, ok, c, pdn, pup, center);
                 u1.x = cf1 * (dinv_c * Ap.x - sigma * c.x);
                 u1.y = cf1 * (dinv_c * Ap.y - sigma * c.y);
                 if (mloaded) {
-                    const double2 pm = lds2(sm + ms * MS + om);
+                    const double2 pm = lds2(P1 + omk);   // p_{j-1}(q) rides in stage q+1
                     u1.x -= pm.x;
                     u1.y -= pm.y;
                 }
                 if (!v0) u1.x = 0.0;
                 if (!v1) u1.y = 0.0;
-                if (own && q >= wb1 && q < we1) {
+                if (own && (S || (q >= wb1 && q < we1))) {
                     if (!v1) Ap.y = 0.0;
-                    if (out.w[0]) __stcs(reinterpret_cast<double2 *>(out.w[0] + off), Ap);
-                    if (out.pn[0]) *reinterpret_cast<double2 *>(out.pn[0] + off) = u1;
+                    if (w0) __stcs(reinterpret_cast<double2 *>(w0 + off), Ap);
+                    if (n0) *reinterpret_cast<double2 *>(n0 + off) = u1;
                 }
             }
             *reinterpret_cast<double2 *>(su1 + (uc & (NU - 1)) * U1S + o1) = u1;
-            mbar_arrive_a(u1_a + 8 * (uc & (NU - 1)));
-            if (mloaded) {
-                mbar_arrive_a(em_a + 8 * ms);
-                ++mc;
-            }
-            if (q >= it.plo && q <= it.phi) release(q);
+            if (S || (q >= it.plo && q <= it.phi)) release(q);
+            // one barrier per plane: U1(q-1) and U2(q-2) of every thread are written
+            if (S || uc > 0) mbar_wait_a(ubar_a + 8 * ((uc - 1) & (NU - 1)), ((uc - 1) / NU) & 1);
             // ---------------- level 2: step j+1 at plane q-1 ----------------
             const int z2 = q - 1;
             double2 u2 = make_double2(0.0, 0.0);
-            if (uc > 0) mbar_wait_a(u1_a + 8 * ((uc - 1) & (NU - 1)), ((uc - 1) / NU) & 1);
-            if (in2 && z2 >= 1 && z2 <= nzl) {
+            if (in2 && (S || (z2 >= 1 && z2 <= nzl))) {
                 const double *U = su1 + ((uc - 1) & (NU - 1)) * U1S;
                 const double2 c = u1m1;
                 double2 Ap = stencil(U, o1, c, u1m2, u1, center);
@@ -275,30 +257,29 @@ __global__ void __launch_bounds__(THREADS, 1)
                 u2.y = cf * (dinv_c * Ap.y - sigma * c.y) - pdn.y;
                 if (!v0) u2.x = 0.0;
                 if (!v1) u2.y = 0.0;
-                if (own && z2 >= wb2 && z2 < we2) {
+                if (own && (S || (z2 >= wb2 && z2 < we2))) {
                     if (!v1) Ap.y = 0.0;
-                    if (out.w[1]) __stcs(reinterpret_cast<double2 *>(out.w[1] + off - pl), Ap);
-                    if (out.pn[1]) *reinterpret_cast<double2 *>(out.pn[1] + off - pl) = u2;
+                    if (w1) __stcs(reinterpret_cast<double2 *>(w1 + off - pl), Ap);
+                    if (n1) *reinterpret_cast<double2 *>(n1 + off - pl) = u2;
                 }
             }
-            if (in2 && uc > 0) *reinterpret_cast<double2 *>(su2 + ((uc - 1) & (NU - 1)) * U2S + o2) = u2;
-            if (uc > 0) mbar_arrive_a(u2_a + 8 * ((uc - 1) & (NU - 1)));
+            if (in2) *reinterpret_cast<double2 *>(su2 + ((uc - 1) & (NU - 1)) * U2S + o2) = u2;
             // ---------------- level 3: step j+2 at plane q-2 ----------------
             const int z3 = q - 2;
-            if (uc > 1) mbar_wait_a(u2_a + 8 * ((uc - 2) & (NU - 1)), ((uc - 2) / NU) & 1);
-            if (own && z3 >= it.zlo && z3 < it.zhi) {
+            if (own && (S || (z3 >= it.zlo && z3 < it.zhi))) {
                 const double *U = su2 + ((uc - 2) & (NU - 1)) * U2S;
                 const double2 c = u2m1;
                 double2 Ap = stencil(U, o2, c, u2m2, u2, center);
                 if (!v1) Ap.y = 0.0;
-                if (out.w[2]) __stcs(reinterpret_cast<double2 *>(out.w[2] + off - 2 * pl), Ap);
-                if (out.pn[2]) {
+                if (w2) __stcs(reinterpret_cast<double2 *>(w2 + off - 2 * pl), Ap);
+                if (n2) {
                     const double v0b = cf * (dinv_c * Ap.x - sigma * c.x) - u1m2.x;   // u1m2 = p_{j+1}(q-2)
                     double v1b = cf * (dinv_c * Ap.y - sigma * c.y) - u1m2.y;
                     if (!v1) v1b = 0.0;
-                    *reinterpret_cast<double2 *>(out.pn[2] + off - 2 * pl) = make_double2(v0b, v1b);
+                    *reinterpret_cast<double2 *>(n2 + off - 2 * pl) = make_double2(v0b, v1b);
                 }
             }
+            mbar_arrive_a(ubar_a + 8 * (uc & (NU - 1)));   // this thread's U1(q), U2(q-1) are written
             ++uc;
             u2m2 = u2m1;
             u2m1 = u2;
@@ -306,9 +287,17 @@ __global__ void __launch_bounds__(THREADS, 1)
             u1m1 = u1;
             pdn = pc0;
             pc0 = pup;
-        }
+            off += pl;
+        };
+        using Gen = std::integral_constant<bool, false>;
+        using Steady = std::integral_constant<bool, true>;
+        int q = it.q0;
+        for (; q < it.zlo + 2 && q <= it.q1; ++q) plane(q, Gen());
+#pragma unroll 1
+        for (; q < it.zhi; ++q) plane(q, Steady());
+        for (; q <= it.q1; ++q) plane(q, Gen());
         for (int z = max(it.q1 + 1, it.plo); z <= it.phi; ++z) release(z);
-        pc = pbase + (it.phi - it.plo + 1);
+        sc = sbase + (it.phi - it.plo + 1);
     }
 }
 
@@ -341,12 +330,15 @@ bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
 }
 
 // SSCG_K1_MP3 (read at every sscg_setup): "1" enables the triples for 7-point
-// single-slab solves; default off.  Measured at cfg 5 (profiles/r01s_*): one
-// triple takes 1.006 ms against 0.53 ms per K1F pair (0.335 vs 0.266 ms per
-// basis step) -- the byte saving (26 vs 31 vectors per outer) is lost to
-// instruction issue: the level-1/2 halos add redundant stencil work (1.21 vs
-// 1.10 evaluations per output point and step) and the kernel is issue-bound
-// (62 % issue-active, 12 % of the instructions FP64 arithmetic).
+// single-slab solves; default off.  Measured at cfg 5: the first version
+// (separate p_j / p_{j-1} rings, two barriers per plane) took 1.006 ms per
+// triple, issue-bound (profiles/r01s_*); with p_{j-1} riding in the p_j stage,
+// one barrier per plane and a compile-time steady state it takes ~0.74 ms
+// (0.25 ms per step vs 0.265 for a K1F pair), but the outer iteration is the
+// same within noise (8.34 vs 8.36 ms over three A/B runs): the byte saving
+// (26 vs 31 vectors per outer) is spent on redundant halo work (1.21 vs 1.10
+// stencil evaluations per output point and step) and on shared-memory
+// bandwidth (l1tex 79 %).
 bool k1m_enabled(const Geo &g, int nzl)
 {
     const char *e = getenv("SSCG_K1_MP3");
