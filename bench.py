@@ -8,8 +8,9 @@ unknowns per GPU stacked in z (weak scaling, ~90M unknowns per GPU), FP64,
 Jacobi, b ~ U[-1,1] (SplitMix64 on the global index, seed 42), x0 = 0,
 analytic global spectral bounds, s = 16, nu = 30.  One "step" = one outer
 iteration: s basis SpMVs (+halo exchange), the fused Gram pass + the single
-allreduce, the FGS solve and the update.  The working set (P and W: 23 GB per
-GPU) is ~180x the 126 MB L2, so no flush is needed between steps.
+allreduce, the FGS solve and the update.  Each step streams ~68 vectors of
+0.72 GB (the basis P, w_{s-1}, x: ~13 GB touched per GPU, ~100x the 126 MB
+L2), so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
@@ -81,8 +82,8 @@ def workload(a, nranks):
     return {"workload": f"{desc}, s={a.s}, nu={a.nu}, x0=0, b~U[-1,1] seed 42",
             "nx": n, "ny": n, "nz_per_gpu": nzg // nranks, "nz_global": nzg, "s": a.s, "nu": a.nu,
             "n_global": n * n * nzg, "parallelism": f"z-slab x{nranks}",
-            "l2": "no flush: per-GPU working set 2*s vectors (%.2f GB) >> 126 MB L2"
-                  % (2 * a.s * n * n * (nzg // nranks) * 8 / 1e9)}
+            "l2": "no flush: per-GPU working set >= s+2 vectors (%.2f GB: basis, w_{s-1}, x) >> 126 MB L2"
+                  % ((a.s + 2) * n * n * (nzg // nranks) * 8 / 1e9)}
 
 
 # --------------------------------------------------------------------------
