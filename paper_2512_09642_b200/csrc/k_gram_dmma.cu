@@ -40,8 +40,16 @@ namespace {
 #ifndef K2_NCW_MID
 #define K2_NCW_MID 12
 #endif
-__host__ __device__ constexpr int ncw_for(int nb) { return nb >= 5 ? 8 : nb >= 3 ? K2_NCW_MID : K2_NCW_SMALL; }
-__host__ __device__ constexpr int threads_for(int nb) { return 32 * (ncw_for(nb) + 1); }
+#ifndef K2_NCW_VARM
+#define K2_NCW_VARM 20
+#endif
+// varm: K2R with a varying diagonal (more live values per fragment: fewer
+// warps; cfg 4 s = 16: 24 warps 0.196 ms (spilling), 20 0.185, 16 0.193, 12 0.187)
+__host__ __device__ constexpr int ncw_for(int nb, bool varm = false)
+{
+    return nb >= 5 ? 8 : nb >= 3 ? K2_NCW_MID : (varm ? K2_NCW_VARM : K2_NCW_SMALL);
+}
+__host__ __device__ constexpr int threads_for(int nb, bool varm = false) { return 32 * (ncw_for(nb, varm) + 1); }
 constexpr int MAXS = 16;               // ring stages
 
 struct K2DParams {
@@ -229,13 +237,13 @@ struct K2RParams {
 };
 
 template <int NB, int EP, bool VARM>
-__global__ void __launch_bounds__(threads_for(NB), 1)
+__global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     k2r(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmWl,
         const __grid_constant__ CUtensorMap tmDv, K2RParams k, const DevState *st)
 {
     if (st && st->done) return;
     constexpr int SP = 8 * NB;
-    constexpr int NCW = ncw_for(NB), THREADS = threads_for(NB);
+    constexpr int NCW = ncw_for(NB, VARM), THREADS = threads_for(NB, VARM);
     // NB <= 2: k-step pairs from 16-B loads (pitch EP = 136, 64 mod 128 B); larger
     // NB (more live fragments): single k-steps from 8-B loads (EP = 132 / 68,
     // 32 mod 128 B) -- measured faster there (cfg 4 s = 32: 0.453 vs 0.486 ms)
@@ -754,9 +762,9 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     {
         // 4 groups by default (each with nstage/4 slots), nstage a multiple of the groups
         const int nsmax = (int)std::max<size_t>(1, std::min<size_t>(MAXS, ((size_t)smem_kb * 1024) / stage));
-        const int g = common_divisor_le(env_groups() ? env_groups() : 4, ncw_for(nb), ncw_for(nb));
+        const int g = common_divisor_le(env_groups() ? env_groups() : 4, ncw_for(nb, varm), ncw_for(nb, varm));
         k.ngroups = std::min(g, nsmax);
-        while (ncw_for(nb) % k.ngroups) --k.ngroups;
+        while (ncw_for(nb, varm) % k.ngroups) --k.ngroups;
         k.nstage = std::max(k.ngroups, nsmax / k.ngroups * k.ngroups);
     }
     k.inv_theta = 1.0 / theta;
@@ -769,12 +777,12 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     const int64_t nchunks = (k.N + ep - 1) / ep;
     const int gx = (int)std::min<int64_t>(k2_grid(), nchunks);
     const int nt = nb * (nb + 1) / 2;
-    const size_t red = (size_t)(ncw_for(nb) * nt * 64 + ncw_for(nb) * s_pad) * sizeof(double);
+    const size_t red = (size_t)(ncw_for(nb, varm) * nt * 64 + ncw_for(nb, varm) * s_pad) * sizeof(double);
     const size_t sm = std::max((size_t)k.nstage * stage, red);
     const CUtensorMap &dv = varm ? sl.tmDv : sl.tmWl;
 #define K2R_LAUNCH(NB, EP)                                                                                   \
-    if (varm) k2r<NB, EP, true><<<gx, threads_for(NB), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);          \
-    else k2r<NB, EP, false><<<gx, threads_for(NB), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);
+    if (varm) k2r<NB, EP, true><<<gx, threads_for(NB, true), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);          \
+    else k2r<NB, EP, false><<<gx, threads_for(NB, false), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);
     switch (nb) {
     case 1: K2R_LAUNCH(1, 136) break;
     case 2: K2R_LAUNCH(2, 136) break;
