@@ -573,7 +573,13 @@ __global__ void __launch_bounds__(k2s_threads(S), 1)
 }
 
 int ep_for(int s_pad) { return s_pad <= 32 ? 132 : 68; }   // row pitch 32 mod 128 bytes (8-B fragment loads)
-int ep_for_k2r(int s_pad) { return s_pad <= 16 ? 136 : ep_for(s_pad); }   // pairs: 64 mod 128 B (16-B loads)
+#ifndef K2R_EP_MID
+#define K2R_EP_MID 132
+#endif
+int ep_for_k2r(int s_pad)   // pairs: 64 mod 128 B (16-B loads); single k-steps: 32 mod 128 B
+{
+    return s_pad <= 16 ? 136 : s_pad <= 32 ? K2R_EP_MID : 68;
+}
 
 // consumer warp groups: each group works on its own stages, so the ring keeps
 // nstage - ngroups stages in flight for TMA.  ngroups must divide both the
@@ -674,9 +680,9 @@ bool k2r_prepare(const Geo &g, Slab &sl, int s)
     const int64_t N = (int64_t)sl.nzl * g.plane;
     const int mx = 226 * 1024;
 #define K2R_ATTR(NB, EP, V) cudaFuncSetAttribute(k2r<NB, EP, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
-    if (K2R_ATTR(1, 136, false) || K2R_ATTR(2, 136, false) || K2R_ATTR(3, 132, false) || K2R_ATTR(4, 132, false) ||
+    if (K2R_ATTR(1, 136, false) || K2R_ATTR(2, 136, false) || K2R_ATTR(3, K2R_EP_MID, false) || K2R_ATTR(4, K2R_EP_MID, false) ||
         K2R_ATTR(5, 68, false) || K2R_ATTR(6, 68, false) || K2R_ATTR(7, 68, false) || K2R_ATTR(8, 68, false) ||
-        K2R_ATTR(1, 136, true) || K2R_ATTR(2, 136, true) || K2R_ATTR(3, 132, true) || K2R_ATTR(4, 132, true) ||
+        K2R_ATTR(1, 136, true) || K2R_ATTR(2, 136, true) || K2R_ATTR(3, K2R_EP_MID, true) || K2R_ATTR(4, K2R_EP_MID, true) ||
         K2R_ATTR(5, 68, true) || K2R_ATTR(6, 68, true) || K2R_ATTR(7, 68, true) || K2R_ATTR(8, 68, true))
         return false;
 #undef K2R_ATTR
@@ -786,8 +792,8 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     switch (nb) {
     case 1: K2R_LAUNCH(1, 136) break;
     case 2: K2R_LAUNCH(2, 136) break;
-    case 3: K2R_LAUNCH(3, 132) break;
-    case 4: K2R_LAUNCH(4, 132) break;
+    case 3: K2R_LAUNCH(3, K2R_EP_MID) break;
+    case 4: K2R_LAUNCH(4, K2R_EP_MID) break;
     case 5: K2R_LAUNCH(5, 68) break;
     case 6: K2R_LAUNCH(6, 68) break;
     case 7: K2R_LAUNCH(7, 68) break;
