@@ -92,13 +92,40 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
 #pragma unroll
         for (int j = 0; j < 32; ++j)
             if (j < i0) lnorm_part = fma(g[j], g[j], lnorm_part);
+        // Coordinates in blocks of four: the four residual entries of a block
+        // come over in four independent shuffles, every lane forms the block's
+        // corrections d_j..d_j+3 by forward substitution with the block's
+        // strictly lower entries (broadcast once), then applies them.  Each
+        // rho_i sees the same FMAs in the same order as coordinate-by-
+        // coordinate FGS (bitwise equal), but the dependent chain per block is
+        // one shuffle + three FMAs instead of four shuffles + four FMAs.
+        double Lb[8][6];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int j = 4 * b;
+            Lb[b][0] = __shfl_sync(0xffffffffu, g[j], j + 1);       // G_{j+1,j}
+            Lb[b][1] = __shfl_sync(0xffffffffu, g[j], j + 2);       // G_{j+2,j}
+            Lb[b][2] = __shfl_sync(0xffffffffu, g[j + 1], j + 2);   // G_{j+2,j+1}
+            Lb[b][3] = __shfl_sync(0xffffffffu, g[j], j + 3);       // G_{j+3,j}
+            Lb[b][4] = __shfl_sync(0xffffffffu, g[j + 1], j + 3);   // G_{j+3,j+1}
+            Lb[b][5] = __shfl_sync(0xffffffffu, g[j + 2], j + 3);   // G_{j+3,j+2}
+        }
         for (int sw = 0; sw < a.nu; ++sw) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int b = 0; b < 8; ++b) {
+                const int j = 4 * b;
                 if (j < s) {
-                    const double dj = __shfl_sync(0xffffffffu, rho0, j);
-                    rho0 = fma(-g[j], dj, rho0);
-                    al0 += (lane == j) ? dj : 0.0;
+                    const double r0 = __shfl_sync(0xffffffffu, rho0, j), r1 = __shfl_sync(0xffffffffu, rho0, j + 1),
+                                 r2 = __shfl_sync(0xffffffffu, rho0, j + 2), r3 = __shfl_sync(0xffffffffu, rho0, j + 3);
+                    const double d0 = r0;
+                    const double d1 = fma(-Lb[b][0], d0, r1);
+                    const double d2 = fma(-Lb[b][2], d1, fma(-Lb[b][1], d0, r2));
+                    const double d3 = fma(-Lb[b][5], d2, fma(-Lb[b][4], d1, fma(-Lb[b][3], d0, r3)));
+                    rho0 = fma(-g[j], d0, rho0);
+                    al0 += (lane == j) ? d0 : 0.0;
+                    if (j + 1 < s) { rho0 = fma(-g[j + 1], d1, rho0); al0 += (lane == j + 1) ? d1 : 0.0; }
+                    if (j + 2 < s) { rho0 = fma(-g[j + 2], d2, rho0); al0 += (lane == j + 2) ? d2 : 0.0; }
+                    if (j + 3 < s) { rho0 = fma(-g[j + 3], d3, rho0); al0 += (lane == j + 3) ? d3 : 0.0; }
                 }
             }
         }
