@@ -322,7 +322,8 @@ def run_ours(a):
     fused = depth > 1
     upd_vecs = S.query(sscg.QUERY_UPDATE_VECTORS)        # 2s+3, or s+4 with W alpha from the recurrence
     gram_vecs = S.query(sscg.QUERY_GRAM_VECTORS)         # 2s, or s+1 with W recovered from the recurrence
-    bytes_per_outer = {"basis": basis_vecs * vec + s * face_bytes, "gram": gram_vecs * vec,
+    face_passes = s if depth == 1 else (s + 1) // 2   # fused pairs read the faces once per pair
+    bytes_per_outer = {"basis": basis_vecs * vec + face_passes * face_bytes, "gram": gram_vecs * vec,
                        "update": upd_vecs * vec}
     kern = {}
     for k, byt in bytes_per_outer.items():

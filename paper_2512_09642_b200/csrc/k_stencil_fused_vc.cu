@@ -1,0 +1,445 @@
+// K1FV -- two basis steps in one pass for the variable-coefficient 7-point
+// operator (BASELINE cfg 4; R12): the pair (j, j+1) of the Chebyshev
+// recurrence
+//   w_j = A p_j,  p_{j+1} = c_j (D^{-1} w_j - sigma p_j) [- p_{j-1}],
+//   w_{j+1} = A p_{j+1},  p_{j+2} = 2 theta (D^{-1} w_{j+1} - sigma p_{j+1}) - p_j,
+// with p_{j+1} kept on chip, as K1F does for the constant stencils.  The six
+// face coefficients of a cell (A_ii = their sum, A_i,nbr = -k_face) are the
+// same for both steps, so a pair streams them once: per pair p_j, p_{j-1}
+// and the faces kx, ky, kz in, p_{j+1}, p_{j+2} out -- 7 vectors instead of
+// 12 for two K1T steps (W-free schedule).
+//
+// Same per-point arithmetic, operand for operand, as K1T KIND 3.  Structure
+// as K1F KIND 1 (k_stencil_fused.cu): warp r (1..TY+2) owns box row r, lane l
+// the pair at column 2 + 2l, the last consumer warp the halo pairs; each
+// thread's front cell (step j on tile + 1-cell halo) and back cell (step j+1
+// on the tile) coincide, so the z-columns of p_j and p_{j+1} roll through
+// registers.  The faces of a thread's own cells come straight from global
+// memory one plane ahead (no neighbour reads them) and stay in registers for
+// the back step one plane later, so the tile is 64 x 8 with 12 warps: the
+// register budget (152 per thread) is what the faces need.
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include "sscg_internal.cuh"
+#include "tma.cuh"
+
+namespace sscg {
+namespace {
+
+constexpr int TX = 64, TY = 8;
+constexpr int BW = TX + 4;                 // staged planes: x in [x0-2, x0+TX+2)
+constexpr int BHP = TY + 4;                // p_j: y in [y0-2, y0+TY+2)
+constexpr int BHM = TY + 2;                // p_{j-1}: y in [y0-1, y0+TY+1)
+constexpr int r128(int d) { return ((d * 8 + 127) / 128) * 128 / 8; }
+constexpr int PS = r128(BW * BHP), MS = r128(BW * BHM);
+constexpr int NSP = 8, NSM = 8, NU = 4;   // powers of two
+constexpr int NROW = TY + 2;               // row warps 1..TY+2
+constexpr int NCW = NROW + 1;              // + one warp for the 2*(TY+2) halo pairs
+constexpr int NCT = NCW * 32;
+constexpr int THREADS = NCT + 32;
+constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = BW * BHM * 8;
+constexpr size_t SMEM = (size_t)(NSP * PS + NSM * MS + NU * PS) * sizeof(double);
+static_assert(2 * NROW <= 32, "halo pairs fit one warp");
+
+struct K1FVWork {
+    int tiles_x, tiles_y, zc;
+    int64_t nitems;
+    int nzl;
+    int zb, ze;            // planes written by both steps: [zb, ze) within [1, nzl]
+    int j;
+    int front_pm;          // p_{j-1} term in the front step (j >= 1)
+    int back_pn;           // the back step writes p_{j+2} (j+1 < s-1)
+    double coef_front, coef_back, sigma;
+};
+
+struct Faces {
+    const double *kx, *ky, *kz;   // this slab (R12): kx[nzl][ny][nx+1], ky[nzl][ny+1][nx], kz[nzl+1][ny][nx]
+};
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int x, int y, int z, int v,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(v), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v)
+{
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
+__device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+
+struct ItemPlan {
+    int tx, ty, zlo, zhi, plo, phi, mlo, mhi;
+};
+
+__device__ __forceinline__ ItemPlan plan_item(const K1FVWork &wk, int64_t item)
+{
+    const int ntiles = wk.tiles_x * wk.tiles_y;
+    const int chunk = (int)(item / ntiles);
+    const int tile = (int)(item - (int64_t)chunk * ntiles);
+    ItemPlan p;
+    p.ty = tile / wk.tiles_x;
+    p.tx = tile - p.ty * wk.tiles_x;
+    p.zlo = wk.zb + chunk * wk.zc;
+    p.zhi = min(wk.ze, p.zlo + wk.zc);
+    p.plo = max(p.zlo - 2, 0);
+    p.phi = min(p.zhi + 1, wk.nzl + 1);
+    p.mlo = max(p.zlo - 1, 1);
+    p.mhi = min(p.zhi, wk.nzl);
+    return p;
+}
+
+// the faces of a cell pair at one plane (R12), and its diagonal
+struct PairFaces {
+    double kxw0, kxe0, kxe1;   // kx[x], kx[x+1] (= west of x+1), kx[x+2]
+    double2 kys, kyn;          // ky[y], ky[y+1]
+    double2 kzu;               // kz[z+1] (the upper face; the lower one is the previous plane's upper)
+};
+
+__device__ __forceinline__ PairFaces load_faces(const Faces &f, const Geo &g, int zl, int gy, int gx, bool v0,
+                                                bool v1)
+{
+    PairFaces r;
+    r.kxw0 = r.kxe0 = r.kxe1 = 0.0;
+    r.kys = r.kyn = r.kzu = make_double2(0.0, 0.0);
+    if (v0) {
+        const double *qx = f.kx + ((int64_t)zl * g.ny + gy) * (g.nx + 1) + gx;
+        const double *qy = f.ky + ((int64_t)zl * (g.ny + 1) + gy) * g.nx + gx;
+        const double *qz = f.kz + ((int64_t)(zl + 1) * g.ny + gy) * g.nx + gx;
+        r.kxw0 = __ldg(qx);
+        r.kxe0 = __ldg(qx + 1);
+        r.kys.x = __ldg(qy);
+        r.kyn.x = __ldg(qy + g.nx);
+        r.kzu.x = __ldg(qz);
+        if (v1) {
+            r.kxe1 = __ldg(qx + 2);
+            r.kys.y = __ldg(qy + 1);
+            r.kyn.y = __ldg(qy + g.nx + 1);
+            r.kzu.y = __ldg(qz + 1);
+        }
+    }
+    return r;
+}
+
+// A p on the pair (order as K1T KIND 3) and the diagonal
+__device__ __forceinline__ double2 vc_apply(const PairFaces &F, double2 kzd, double2 c, double2 dn, double2 up,
+                                            double2 ylo, double2 yhi, double l, double rr, double2 &D)
+{
+    D.x = kzd.x + F.kys.x + F.kxw0 + F.kxe0 + F.kyn.x + F.kzu.x;
+    D.y = kzd.y + F.kys.y + F.kxe0 + F.kxe1 + F.kyn.y + F.kzu.y;
+    double2 Ap;
+    Ap.x = D.x * c.x - (kzd.x * dn.x + F.kzu.x * up.x + F.kys.x * ylo.x + F.kxw0 * l + F.kxe0 * c.y + F.kyn.x * yhi.x);
+    Ap.y = D.y * c.y - (kzd.y * dn.y + F.kzu.y * up.y + F.kys.y * ylo.y + F.kxe0 * c.x + F.kxe1 * rr + F.kyn.y * yhi.y);
+    return Ap;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k1fv(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, K1Args a,
+         Faces fc, const DevState *st, K1FVWork wk)
+{
+    if (st && st->done) return;
+    extern __shared__ __align__(128) double smem[];
+    double *sp = smem;                       // p_j ring
+    double *sm = smem + NSP * PS;            // p_{j-1} ring
+    double *su = sm + NSM * MS;              // U = p_{j+1} on tile + halo, NU planes
+    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM], ufull[NU];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int i = 0; i < NSP; ++i) {
+            mbar_init(&fullp[i], 1);
+            mbar_init(&emptyp[i], NCT);
+        }
+        for (int i = 0; i < NSM; ++i) {
+            mbar_init(&fullm[i], 1);
+            mbar_init(&emptym[i], NCT);
+        }
+        for (int i = 0; i < NU; ++i) mbar_init(&ufull[i], NCT);
+        mbar_fence_init();
+        tma_prefetch_desc(&tmP);
+        tma_prefetch_desc(&tmM);
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t pc = 0, mc = 0;
+            for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+                const ItemPlan it = plan_item(wk, item);
+                const int x0 = it.tx * TX, y0 = it.ty * TY;
+                int pnext = it.plo;
+                for (int q = it.zlo - 1; q <= it.zhi; ++q) {
+                    while (pnext <= min(q + 1, it.phi)) {
+                        const int sl = pc & (NSP - 1);
+                        if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
+                        mbar_expect_tx(&fullp[sl], PBYTES);
+                        tma_load_4d(sp + sl * PS, &tmP, x0 - 2, y0 - 2, pnext, wk.j, &fullp[sl]);
+                        ++pc;
+                        ++pnext;
+                    }
+                    if (wk.front_pm && q >= it.mlo && q <= it.mhi) {
+                        const int sl = mc & (NSM - 1);
+                        if (mc >= NSM) mbar_wait(&emptym[sl], ((mc / NSM) - 1) & 1);
+                        mbar_expect_tx(&fullm[sl], MBYTES);
+                        tma_load_4d(sm + sl * MS, &tmM, x0 - 2, y0 - 1, q, wk.j - 1, &fullm[sl]);
+                        ++mc;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    int rk, ck;
+    bool task;
+    if (warp <= NROW) {
+        rk = warp;
+        ck = 2 + 2 * lane;
+        task = true;
+    } else {
+        const int h = lane;
+        task = h < 2 * NROW;
+        rk = task ? 1 + (h >> 1) : 1;
+        ck = (h & 1) ? TX + 2 : 0;
+    }
+    const int ok = rk * BW + ck, omk = (rk - 1) * BW + ck;
+    const bool ownk = task && rk >= 2 && rk < TY + 2 && ck >= 2 && ck < TX + 2;
+    const bool lgk = ck > 0, rgk = ck + 2 < BW;
+    const bool skip_w = a.skip_w, skip_w2 = a.skip_w2, back_pn = wk.back_pn, front_pm = wk.front_pm;
+    double *const gw = a.w, *const gpn = a.pn, *const gw2 = a.w2, *const gpn2 = a.pn2;
+    const int nzl = wk.nzl;
+    const double sigma = wk.sigma, cfr = wk.coef_front, cbk = wk.coef_back;
+    const int64_t pl = g.plane;
+    uint32_t pc = 0, mc = 0, uc = 0;
+    const uint32_t fp_a = pin_u32(smem_u32(fullp)), ep_a = pin_u32(smem_u32(emptyp)),
+                   fm_a = pin_u32(smem_u32(fullm)), em_a = pin_u32(smem_u32(emptym)),
+                   uf_a = pin_u32(smem_u32(ufull));
+    for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+        const ItemPlan it = plan_item(wk, item);
+        const int x0 = it.tx * TX, y0 = it.ty * TY;
+        const int gx = x0 - 2 + ck, gy = y0 - 2 + rk;
+        const bool vy = gy >= 0 && gy < g.ny;
+        const bool v0 = task && vy && gx >= 0 && gx < g.nx, v1 = task && vy && gx + 1 >= 0 && gx + 1 < g.nx;
+        const bool wown = ownk && v0;
+        const uint32_t pbase = pc;
+        auto slotp = [&](int z) -> const double * {
+            return sp + ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1)) * PS;
+        };
+        auto release = [&](int z) { mbar_arrive_a(ep_a + 8 * ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1))); };
+        auto waitp = [&](int z) {
+            const uint32_t c = pbase + (uint32_t)(z - it.plo);
+            mbar_wait_a(fp_a + 8 * (c & (NSP - 1)), (c / NSP) & 1);
+        };
+        for (int z = it.plo; z <= min(it.zlo, it.phi); ++z) waitp(z);
+        double2 pdn = make_double2(0.0, 0.0);
+        if (it.zlo - 2 >= it.plo) {
+            pdn = lds2(slotp(it.zlo - 2) + ok);
+            release(it.zlo - 2);
+        }
+        double2 pc0 = lds2(slotp(it.zlo - 1) + ok);
+        double2 um2 = make_double2(0.0, 0.0), um1 = make_double2(0.0, 0.0);
+        // faces: F of plane q (front), Fb / kzdb / Db of plane q-1 (back, one
+        // plane later), Fn of plane q+1 in flight; kzd = lower face of plane q
+        const int q0 = it.zlo - 1;
+        const bool in0 = q0 >= 1 && q0 <= nzl;
+        PairFaces F = in0 ? load_faces(fc, g, q0 - 1, gy, gx, v0, v1) : PairFaces{};
+        double2 kzd = make_double2(0.0, 0.0);
+        if (in0 && v0) {
+            const double *qz = fc.kz + ((int64_t)(q0 - 1) * g.ny + gy) * g.nx + gx;
+            kzd.x = __ldg(qz);
+            if (v1) kzd.y = __ldg(qz + 1);
+        }
+        PairFaces Fb{};
+        double2 kzdb = make_double2(0.0, 0.0), dinvb = make_double2(0.0, 0.0);
+        int64_t off = (int64_t)q0 * pl + (int64_t)gy * g.pitch + gx;
+        auto plane = [&](int q, auto steady) {
+            constexpr bool S = decltype(steady)::value;
+            const bool inside = S || (q >= 1 && q <= nzl);
+            const bool has_up = S || q + 1 <= it.phi;
+            // faces of plane q+1 (used by the next front), issued first
+            const bool in_n = q + 1 >= 1 && q + 1 <= nzl && q + 1 <= it.zhi;   // the next front is inside
+            const PairFaces Fn = in_n ? load_faces(fc, g, q, gy, gx, v0, v1) : PairFaces{};
+            const double *P0 = slotp(q);
+            double2 pup = make_double2(0.0, 0.0);
+            if (has_up) {
+                if (S || q >= it.zlo) waitp(q + 1);
+                pup = lds2(slotp(q + 1) + ok);
+            }
+            const bool mloaded = front_pm && (S || (q >= it.mlo && q <= it.mhi));
+            const uint32_t ms = mc & (NSM - 1);
+            if (mloaded) mbar_wait_a(fm_a + 8 * ms, (mc / NSM) & 1);
+            // ---------------- front(q): step j on tile + halo ----------------
+            double2 u = make_double2(0.0, 0.0), dinv = make_double2(0.0, 0.0);
+            if (inside) {
+                const double2 c = pc0;
+                const double2 ylo = lds2(P0 + ok - BW), yhi = lds2(P0 + ok + BW);
+                const double l = lgk ? P0[ok - 1] : 0.0;
+                const double rr = rgk ? P0[ok + 2] : 0.0;
+                double2 D;
+                double2 Ap = vc_apply(F, kzd, c, pdn, pup, ylo, yhi, l, rr, D);
+                dinv = make_double2(v0 ? 1.0 / D.x : 0.0, v1 ? 1.0 / D.y : 0.0);
+                u.x = cfr * (dinv.x * Ap.x - sigma * c.x);
+                u.y = cfr * (dinv.y * Ap.y - sigma * c.y);
+                if (mloaded) {
+                    const double2 pm = lds2(sm + ms * MS + omk);
+                    u.x -= pm.x;
+                    u.y -= pm.y;
+                }
+                if (!v0) u.x = 0.0;
+                if (!v1) u.y = 0.0;
+                if (wown && (S || (q >= it.zlo && q < it.zhi))) {
+                    if (!v1) Ap.y = 0.0;
+                    if (!skip_w) __stcs(reinterpret_cast<double2 *>(gw + off), Ap);
+                    *reinterpret_cast<double2 *>(gpn + off) = u;
+                }
+            }
+            if (task) *reinterpret_cast<double2 *>(su + (uc & (NU - 1)) * PS + ok) = u;
+            mbar_arrive_a(uf_a + 8 * (uc & (NU - 1)));
+            if (mloaded) {
+                mbar_arrive_a(em_a + 8 * ms);
+                ++mc;
+            }
+            release(q);
+            // ---------------- back(z = q-1): step j+1 on the tile ----------------
+            if (S || uc > 0) mbar_wait_a(uf_a + 8 * ((uc - 1) & (NU - 1)), ((uc - 1) / NU) & 1);
+            if (wown && (S || (q - 1 >= it.zlo && q - 1 < it.zhi))) {
+                const double *U0 = su + ((uc - 1) & (NU - 1)) * PS;
+                const double2 c = um1, dn = um2, up = u;
+                const double2 ylo = lds2(U0 + ok - BW), yhi = lds2(U0 + ok + BW);
+                const double l = U0[ok - 1], rr = U0[ok + 2];
+                double2 D;
+                double2 Ap = vc_apply(Fb, kzdb, c, dn, up, ylo, yhi, l, rr, D);
+                if (!v1) Ap.y = 0.0;
+                if (!skip_w2) __stcs(reinterpret_cast<double2 *>(gw2 + off - pl), Ap);
+                if (back_pn) {
+                    const double2 pj = pdn;
+                    const double v0b = cbk * (dinvb.x * Ap.x - sigma * c.x) - pj.x;
+                    double v1b = cbk * (dinvb.y * Ap.y - sigma * c.y) - pj.y;
+                    if (!v1) v1b = 0.0;
+                    *reinterpret_cast<double2 *>(gpn2 + off - pl) = make_double2(v0b, v1b);
+                }
+            }
+            ++uc;
+            um2 = um1;
+            um1 = u;
+            pdn = pc0;
+            pc0 = pup;
+            Fb = F;
+            kzdb = kzd;
+            dinvb = dinv;
+            if (S || inside) {
+                kzd = F.kzu;   // the lower face of plane q+1 is the upper face of plane q
+            } else {
+                kzd = make_double2(0.0, 0.0);
+                if (in_n && v0) {   // plane q is a halo / Dirichlet plane: read kz(q+1)'s lower face
+                    const double *qz = fc.kz + ((int64_t)q * g.ny + gy) * g.nx + gx;
+                    kzd.x = __ldg(qz);
+                    if (v1) kzd.y = __ldg(qz + 1);
+                }
+            }
+            F = Fn;
+            off += pl;
+        };
+        using Gen = std::integral_constant<bool, false>;
+        using Steady = std::integral_constant<bool, true>;
+        int q = it.zlo - 1;
+        plane(q++, Gen());
+        if (q < it.zhi) plane(q++, Gen());
+#pragma unroll 1
+        for (; q < it.zhi; ++q) plane(q, Steady());
+        for (; q <= it.zhi; ++q) plane(q, Gen());
+        for (int z = max(it.zhi + 1, it.plo); z <= it.phi; ++z) release(z);
+        pc = pbase + (it.phi - it.plo + 1);
+    }
+}
+
+}  // namespace
+
+bool k1fv_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+        return false;
+    auto enc = reinterpret_cast<CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                             CUtensorMapFloatOOBfill)>(fn);
+    cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)(nzl + 2), (cuuint64_t)s};
+    cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.vstride * 8};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint32_t boxp[4] = {BW, BHP, 1, 1}, boxm[4] = {BW, BHM, 1, 1};
+    if (enc(tmP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxp, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (enc(tmM, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxm, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    return cudaFuncSetAttribute(k1fv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+}
+
+// SSCG_K1_FUSE applies as for K1F ("0" never, "1" always).  Unset: slabs with
+// 8 .. 400 tile-planes per SM.  The pair saves 5 of 12 vectors per two steps
+// but runs 12 warps per SM (the faces' registers) and is latency-bound: at
+// cfg 4 (192^3, ~95 tile-planes per SM) it takes 0.118 ms against 2 x 0.063 ms
+// for two K1T steps; at 384^3 (~750 per SM, where K1T streams at 0.89 of the
+// copy peak) 0.99 ms against 2 x 0.457 ms.
+bool k1fv_enabled(const Geo &g, int nzl)
+{
+    const char *e = getenv("SSCG_K1_FUSE");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    const int64_t tiles = (int64_t)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
+    const int64_t per_sm = tiles * nzl / k2_grid();
+    return per_sm >= 8 && per_sm <= 400;
+}
+
+void launch_k1fv(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm)
+{
+    K1FVWork wk;
+    wk.tiles_x = (g.nx + TX - 1) / TX;
+    wk.tiles_y = (g.ny + TY - 1) / TY;
+    wk.nzl = a.nzl;
+    wk.zb = a.zb;
+    wk.ze = a.ze;
+    wk.j = a.j;
+    wk.front_pm = a.j > 0;
+    wk.back_pn = (a.j + 1 < s - 1) ? 1 : 0;
+    wk.coef_front = (a.j == 0) ? theta : 2.0 * theta;
+    wk.coef_back = 2.0 * theta;
+    wk.sigma = a.sigma;
+    Faces fc{a.kx, a.ky, a.kz};
+    const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
+    const int64_t resident = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
+    const int n1 = a.ze - a.zb;
+    if (n1 <= 0) return;
+    int zc = n1;
+    double best = -1.0;
+    for (int nch = 1; nch <= 64 && (n1 + nch - 1) / nch >= 4; ++nch) {
+        const int z = (n1 + nch - 1) / nch;
+        const int64_t items = tiles * ((n1 + z - 1) / z);
+        const int64_t waves = (items + resident - 1) / resident;
+        const double score = (double)items / (double)(waves * resident) / (1.0 + 1.0 / z);
+        if (score > best + 1e-9) {
+            best = score;
+            zc = z;
+        }
+    }
+    wk.zc = zc;
+    wk.nitems = tiles * ((n1 + zc - 1) / zc);
+    const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
+    k1fv<<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, g, a, fc, st, wk);
+}
+
+}  // namespace sscg

@@ -335,6 +335,11 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the depth-3 basis step");
             sl.has_k1m = true;
         }
+        if (A->kind == SSCG_OP_VARCOEF7 && !diag_M && k1fv_enabled(g, sl.nzl)) {
+            if (!k1fv_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
+                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused variable-coefficient step");
+            sl.has_k1f = true;
+        }
         if (A->kind == SSCG_OP_VARCOEF7) {
             sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
             sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;
@@ -658,7 +663,8 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
 // constant diagonal) and, with neighbours, enough planes for an interior
 static bool uses_fused(const sscg_ctx *c)
 {
-    if (c->basis != SSCG_BASIS_CHEBYSHEV || (c->g.kind != SSCG_OP_STENCIL7 && c->g.kind != SSCG_OP_STENCIL27))
+    if (c->basis != SSCG_BASIS_CHEBYSHEV ||
+        (c->g.kind != SSCG_OP_STENCIL7 && c->g.kind != SSCG_OP_STENCIL27 && c->g.kind != SSCG_OP_VARCOEF7))
         return false;
     const bool halo = c->slabs.size() > 1 || c->nranks > 1;
     for (const auto &sl : c->slabs)
@@ -727,8 +733,10 @@ static sscg_status launch_basis_pair(sscg_ctx *c, int j, int part)
         a.j = j;
         a.tmF_P = &sl.tmF_P;
         a.tmF_M = &sl.tmF_M;
+        a.kx = sl.kx; a.ky = sl.ky; a.kz = sl.kz;
         TRY(prof_mark(c, SSCG_PROF_BASIS, true));
-        launch_k1f(g, a, c->theta, s, c->st, c->stream);
+        if (g.kind == SSCG_OP_VARCOEF7) launch_k1fv(g, a, c->theta, s, c->st, c->stream);
+        else launch_k1f(g, a, c->theta, s, c->st, c->stream);
         TRY(prof_mark(c, SSCG_PROF_BASIS, false));
         ++c->launches;
     }

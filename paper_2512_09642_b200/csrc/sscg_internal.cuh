@@ -113,6 +113,10 @@ bool k1t_prepare_faces(const Geo &g, const double *kx, const double *ky, const d
 
 // K1F: two 7-point basis steps per launch, single slab (k_stencil_fused.cu)
 bool k1f_enabled(const Geo &g, int nzl);
+// K1FV: the pair for variable coefficients (k_stencil_fused_vc.cu; maps in tmF_P / tmF_M)
+bool k1fv_enabled(const Geo &g, int nzl);
+bool k1fv_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM);
+void launch_k1fv(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm);
 
 // K1M: three basis steps per launch (7-point, constant diagonal; k_stencil_mp3.cu)
 struct K1MArgs {

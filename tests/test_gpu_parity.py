@@ -267,7 +267,9 @@ def test_halo_overlap_bitwise(cfg, slabs, monkeypatch):
 @pytest.mark.parametrize("cfg,slabs", [(("7pt", 70, 36, 40, 16, 25), 1), (("7pt", 33, 17, 19, 5, 10), 1),
                                        (("7pt", 40, 36, 33, 10, 20), 3), (("7pt", 66, 20, 17, 7, 10), 2),
                                        (("27pt", 70, 36, 30, 16, 30), 1), (("27pt", 33, 19, 21, 7, 10), 1),
-                                       (("27pt", 40, 34, 26, 8, 20), 3)],
+                                       (("27pt", 40, 34, 26, 8, 20), 3),
+                                       (("varcoef7", 70, 36, 30, 16, 20), 1), (("varcoef7", 33, 19, 21, 7, 10), 1),
+                                       (("varcoef7", 40, 26, 28, 8, 20), 3), (("varcoef7", 64, 17, 19, 6, 10), 2)],
                          ids=lambda v: _ids(v) if isinstance(v, tuple) else str(v))
 def test_fused_pairs_match_single_steps(cfg, slabs, monkeypatch):
     """K1F (two basis steps per launch, p_{j+1} on chip) against K1T single
@@ -276,7 +278,7 @@ def test_fused_pairs_match_single_steps(cfg, slabs, monkeypatch):
     with a single step; several slabs run boundary single steps around the
     exchange of p_{j+1}.  Both agree with the oracle."""
     kind, nx, ny, nz, s, nu = cfg
-    P = Problem(kind, nx, ny, nz, s, nu)
+    P = Problem(kind, nx, ny, nz, s, nu, lanczos=(kind == "varcoef7"))
     out = {}
     monkeypatch.setenv("SSCG_K1_MP3", "0")   # pairs here; triples: test_triples_match_single_steps
     for fuse in ("1", "0"):
