@@ -389,20 +389,20 @@ bool k1fv_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tm
     return cudaFuncSetAttribute(k1fv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
 }
 
-// SSCG_K1_FUSE applies as for K1F ("0" never, "1" always).  Unset: slabs with
-// 8 .. 400 tile-planes per SM.  The pair saves 5 of 12 vectors per two steps
-// but runs 12 warps per SM (the faces' registers) and is latency-bound: at
-// cfg 4 (192^3, ~95 tile-planes per SM) it takes 0.118 ms against 2 x 0.063 ms
-// for two K1T steps; at 384^3 (~750 per SM, where K1T streams at 0.89 of the
-// copy peak) 0.99 ms against 2 x 0.457 ms.
+// SSCG_K1_FUSE_VC=1 enables the pair (SSCG_K1_FUSE=0 still forbids every
+// fused pair); default off.  The pair saves 5 of 12 vectors per two steps but
+// runs 12 warps per SM (the faces' registers) and is latency-bound: at cfg 4
+// (192^3) it takes 0.118 ms against 2 x 0.063 ms for two K1T steps -- 1.5 %
+// of the outer iteration, at 0.50 instead of 0.81 of the copy peak -- and at
+// 384^3 (where K1T streams at 0.89 of copy) 0.99 ms against 2 x 0.457 ms.
 bool k1fv_enabled(const Geo &g, int nzl)
 {
-    const char *e = getenv("SSCG_K1_FUSE");
-    if (e && e[0] == '0') return false;
-    if (e && e[0] == '1') return true;
-    const int64_t tiles = (int64_t)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
-    const int64_t per_sm = tiles * nzl / k2_grid();
-    return per_sm >= 8 && per_sm <= 400;
+    const char *f = getenv("SSCG_K1_FUSE");
+    if (f && f[0] == '0') return false;
+    const char *e = getenv("SSCG_K1_FUSE_VC");
+    (void)g;
+    (void)nzl;
+    return e && e[0] == '1';
 }
 
 void launch_k1fv(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm)

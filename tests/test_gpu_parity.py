@@ -283,6 +283,7 @@ def test_fused_pairs_match_single_steps(cfg, slabs, monkeypatch):
     monkeypatch.setenv("SSCG_K1_MP3", "0")   # pairs here; triples: test_triples_match_single_steps
     for fuse in ("1", "0"):
         monkeypatch.setenv("SSCG_K1_FUSE", fuse)
+        monkeypatch.setenv("SSCG_K1_FUSE_VC", fuse)   # K1FV (variable coefficients) is opt-in
         import paper_2512_09642_b200 as sscg
         with P.gpu_solver(slabs=slabs) as S:
             assert S.query(sscg.QUERY_BASIS_FUSED) == (2 if fuse == "1" else 1)
