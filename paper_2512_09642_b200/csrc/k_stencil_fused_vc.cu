@@ -14,10 +14,11 @@
 // the pair at column 2 + 2l, the last consumer warp the halo pairs; each
 // thread's front cell (step j on tile + 1-cell halo) and back cell (step j+1
 // on the tile) coincide, so the z-columns of p_j and p_{j+1} roll through
-// registers.  The faces of a thread's own cells come straight from global
-// memory one plane ahead (no neighbour reads them) and stay in registers for
-// the back step one plane later, so the tile is 64 x 8 with 12 warps: the
-// register budget (152 per thread) is what the faces need.
+// registers.  The faces of the front region (kx rows as 1-D boxes from the
+// even element at or below x0-2, ky and kz as 3-D boxes) are staged per plane
+// by TMA into a 4-slot ring; a thread reads its own cells' faces of plane q
+// (front) and again of plane q-1 (back) from it, and keeps only D^{-1} of its
+// cells from the front for the back.  Tile 64 x 12, 16 warps, 115 registers.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -28,20 +29,28 @@
 namespace sscg {
 namespace {
 
-constexpr int TX = 64, TY = 8;
+constexpr int TX = 64, TY = 12;
 constexpr int BW = TX + 4;                 // staged planes: x in [x0-2, x0+TX+2)
 constexpr int BHP = TY + 4;                // p_j: y in [y0-2, y0+TY+2)
 constexpr int BHM = TY + 2;                // p_{j-1}: y in [y0-1, y0+TY+1)
 constexpr int r128(int d) { return ((d * 8 + 127) / 128) * 128 / 8; }
 constexpr int PS = r128(BW * BHP), MS = r128(BW * BHM);
-constexpr int NSP = 8, NSM = 8, NU = 4;   // powers of two
+constexpr int NSP = 4, NSM = 4, NU = 4;   // powers of two
 constexpr int NROW = TY + 2;               // row warps 1..TY+2
 constexpr int NCW = NROW + 1;              // + one warp for the 2*(TY+2) halo pairs
 constexpr int NCT = NCW * 32;
 constexpr int THREADS = NCT + 32;
 constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = BW * BHM * 8;
-constexpr size_t SMEM = (size_t)(NSP * PS + NSM * MS + NU * PS) * sizeof(double);
+// face slots (per plane z of the march, the front cells' rows y0-1 .. y0+TY):
+//   KX: TY+2 rows of 70 faces from the even element at or below x0-2 (pitch 80)
+//   KY: TY+3 rows x BW (ky rows y0-1 .. y0+TY+1),  KZ: TY+2 rows x BW (kz[z-1], the lower faces)
+constexpr int KXN = 70, KXP = 80;
+constexpr int FKX = 0, FKY = r128(FKX + (TY + 2) * KXP), FKZ = FKY + r128((TY + 3) * BW), FS = FKZ + r128((TY + 2) * BW);
+constexpr uint32_t KXBYTES = (TY + 2) * KXN * 8, KYBYTES = (TY + 3) * BW * 8, KZBYTES = (TY + 2) * BW * 8;
+constexpr int NSF = 4;
+constexpr size_t SMEM = (size_t)(NSP * PS + NSM * MS + NU * PS + NSF * FS) * sizeof(double);
 static_assert(2 * NROW <= 32, "halo pairs fit one warp");
+static_assert(SMEM <= 227 * 1024, "shared memory");
 
 struct K1FVWork {
     int tiles_x, tiles_y, zc;
@@ -51,12 +60,10 @@ struct K1FVWork {
     int j;
     int front_pm;          // p_{j-1} term in the front step (j >= 1)
     int back_pn;           // the back step writes p_{j+2} (j+1 < s-1)
+    int kx_shift;          // elements the 1-D kx view starts before the slab's kx (16-B alignment)
     double coef_front, coef_back, sigma;
 };
 
-struct Faces {
-    const double *kx, *ky, *kz;   // this slab (R12): kx[nzl][ny][nx+1], ky[nzl][ny+1][nx], kz[nzl+1][ny][nx]
-};
 
 __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int x, int y, int z, int v,
                                             uint64_t *bar)
@@ -78,7 +85,7 @@ __device__ __forceinline__ uint32_t pin_u32(uint32_t v)
 __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 
 struct ItemPlan {
-    int tx, ty, zlo, zhi, plo, phi, mlo, mhi;
+    int tx, ty, zlo, zhi, plo, phi, mlo, mhi, flo, fhi;   // face slots [flo, fhi]
 };
 
 __device__ __forceinline__ ItemPlan plan_item(const K1FVWork &wk, int64_t item)
@@ -95,6 +102,8 @@ __device__ __forceinline__ ItemPlan plan_item(const K1FVWork &wk, int64_t item)
     p.phi = min(p.zhi + 1, wk.nzl + 1);
     p.mlo = max(p.zlo - 1, 1);
     p.mhi = min(p.zhi, wk.nzl);
+    p.flo = max(p.zlo - 1, 1);            // the fronts at [zlo-1, zhi] inside [1, nzl] read slots q, q+1
+    p.fhi = min(p.zhi + 1, wk.nzl + 1);
     return p;
 }
 
@@ -104,31 +113,6 @@ struct PairFaces {
     double2 kys, kyn;          // ky[y], ky[y+1]
     double2 kzu;               // kz[z+1] (the upper face; the lower one is the previous plane's upper)
 };
-
-__device__ __forceinline__ PairFaces load_faces(const Faces &f, const Geo &g, int zl, int gy, int gx, bool v0,
-                                                bool v1)
-{
-    PairFaces r;
-    r.kxw0 = r.kxe0 = r.kxe1 = 0.0;
-    r.kys = r.kyn = r.kzu = make_double2(0.0, 0.0);
-    if (v0) {
-        const double *qx = f.kx + ((int64_t)zl * g.ny + gy) * (g.nx + 1) + gx;
-        const double *qy = f.ky + ((int64_t)zl * (g.ny + 1) + gy) * g.nx + gx;
-        const double *qz = f.kz + ((int64_t)(zl + 1) * g.ny + gy) * g.nx + gx;
-        r.kxw0 = __ldg(qx);
-        r.kxe0 = __ldg(qx + 1);
-        r.kys.x = __ldg(qy);
-        r.kyn.x = __ldg(qy + g.nx);
-        r.kzu.x = __ldg(qz);
-        if (v1) {
-            r.kxe1 = __ldg(qx + 2);
-            r.kys.y = __ldg(qy + 1);
-            r.kyn.y = __ldg(qy + g.nx + 1);
-            r.kzu.y = __ldg(qz + 1);
-        }
-    }
-    return r;
-}
 
 // A p on the pair (order as K1T KIND 3) and the diagonal
 __device__ __forceinline__ double2 vc_apply(const PairFaces &F, double2 kzd, double2 c, double2 dn, double2 up,
@@ -142,16 +126,39 @@ __device__ __forceinline__ double2 vc_apply(const PairFaces &F, double2 kzd, dou
     return Ap;
 }
 
+__device__ __forceinline__ void tma_load_1d(void *dst, const CUtensorMap *map, int x, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct FaceMaps {
+    CUtensorMap kx, ky, kz;
+};
+
 __global__ void __launch_bounds__(THREADS, 1)
-    k1fv(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, K1Args a,
-         Faces fc, const DevState *st, K1FVWork wk)
+    k1fv(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM,
+         const __grid_constant__ FaceMaps fm, Geo g, K1Args a, const DevState *st, K1FVWork wk)
 {
     if (st && st->done) return;
     extern __shared__ __align__(128) double smem[];
     double *sp = smem;                       // p_j ring
     double *sm = smem + NSP * PS;            // p_{j-1} ring
     double *su = sm + NSM * MS;              // U = p_{j+1} on tile + halo, NU planes
-    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM], ufull[NU];
+    double *sf = su + NU * PS;               // face slots
+    __shared__ uint64_t fullp[NSP], emptyp[NSP], fullm[NSM], emptym[NSM], ufull[NU], fullf[NSF], emptyf[NSF];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int i = 0; i < NSP; ++i) {
@@ -162,21 +169,28 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&fullm[i], 1);
             mbar_init(&emptym[i], NCT);
         }
+        for (int i = 0; i < NSF; ++i) {
+            mbar_init(&fullf[i], 1);
+            mbar_init(&emptyf[i], NCT);
+        }
         for (int i = 0; i < NU; ++i) mbar_init(&ufull[i], NCT);
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
         tma_prefetch_desc(&tmM);
+        tma_prefetch_desc(&fm.kx);
+        tma_prefetch_desc(&fm.ky);
+        tma_prefetch_desc(&fm.kz);
     }
     __syncthreads();
 
-    if (warp == 0) {
-        if (lane == 0) {
-            uint32_t pc = 0, mc = 0;
-            for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
-                const ItemPlan it = plan_item(wk, item);
-                const int x0 = it.tx * TX, y0 = it.ty * TY;
-                int pnext = it.plo;
-                for (int q = it.zlo - 1; q <= it.zhi; ++q) {
+    if (warp == 0) {   // producer warp: lane 0 issues, lanes 0..TY+1 the kx face rows
+        uint32_t pc = 0, mc = 0, fc = 0;
+        for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+            const ItemPlan it = plan_item(wk, item);
+            const int x0 = it.tx * TX, y0 = it.ty * TY;
+            int pnext = it.plo, fnext = it.flo;
+            for (int q = it.zlo - 1; q <= it.zhi; ++q) {
+                if (lane == 0) {
                     while (pnext <= min(q + 1, it.phi)) {
                         const int sl = pc & (NSP - 1);
                         if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
@@ -192,6 +206,29 @@ __global__ void __launch_bounds__(THREADS, 1)
                         tma_load_4d(sm + sl * MS, &tmM, x0 - 2, y0 - 1, q, wk.j - 1, &fullm[sl]);
                         ++mc;
                     }
+                }
+                // face slot z holds kx(z), ky(z) (1 <= z <= nzl) and kz(z-1) (1 <= z <= nzl+1)
+                while (fnext <= min(q + 1, it.fhi)) {
+                    const int sl = fc & (NSF - 1);
+                    const int z = fnext, zl = z - 1;
+                    const bool xy = z <= wk.nzl;
+                    double *d = sf + sl * FS;
+                    if (lane == 0) {
+                        if (fc >= NSF) mbar_wait(&emptyf[sl], ((fc / NSF) - 1) & 1);
+                        mbar_expect_tx(&fullf[sl], (xy ? KXBYTES + KYBYTES : 0u) + KZBYTES);
+                    }
+                    __syncwarp();
+                    if (xy && lane < TY + 2) {   // kx row (zl, y0-1+lane) from the even element at or below x0-2
+                        const int64_t e0 = ((int64_t)zl * g.ny + (y0 - 1 + lane)) * (g.nx + 1) + x0 - 2 + wk.kx_shift;
+                        tma_load_1d(d + FKX + lane * KXP, &fm.kx, (int)(e0 & ~(int64_t)1), &fullf[sl]);
+                    }
+                    if (lane == 0) {
+                        if (xy) tma_load_3d(d + FKY, &fm.ky, x0 - 2, y0 - 1, zl, &fullf[sl]);
+                        tma_load_3d(d + FKZ, &fm.kz, x0 - 2, y0 - 1, zl, &fullf[sl]);
+                    }
+                    __syncwarp();
+                    ++fc;
+                    ++fnext;
                 }
             }
         }
@@ -211,6 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         ck = (h & 1) ? TX + 2 : 0;
     }
     const int ok = rk * BW + ck, omk = (rk - 1) * BW + ck;
+    const int ofy = FKY + (rk - 1) * BW + ck, ofz = FKZ + (rk - 1) * BW + ck;   // own ky (south) / kz rows
     const bool ownk = task && rk >= 2 && rk < TY + 2 && ck >= 2 && ck < TX + 2;
     const bool lgk = ck > 0, rgk = ck + 2 < BW;
     const bool skip_w = a.skip_w, skip_w2 = a.skip_w2, back_pn = wk.back_pn, front_pm = wk.front_pm;
@@ -218,10 +256,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int nzl = wk.nzl;
     const double sigma = wk.sigma, cfr = wk.coef_front, cbk = wk.coef_back;
     const int64_t pl = g.plane;
-    uint32_t pc = 0, mc = 0, uc = 0;
+    uint32_t pc = 0, mc = 0, uc = 0, fc = 0;
     const uint32_t fp_a = pin_u32(smem_u32(fullp)), ep_a = pin_u32(smem_u32(emptyp)),
                    fm_a = pin_u32(smem_u32(fullm)), em_a = pin_u32(smem_u32(emptym)),
-                   uf_a = pin_u32(smem_u32(ufull));
+                   uf_a = pin_u32(smem_u32(ufull)), ff_a = pin_u32(smem_u32(fullf)), ef_a = pin_u32(smem_u32(emptyf));
     for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
         const ItemPlan it = plan_item(wk, item);
         const int x0 = it.tx * TX, y0 = it.ty * TY;
@@ -229,16 +267,28 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool vy = gy >= 0 && gy < g.ny;
         const bool v0 = task && vy && gx >= 0 && gx < g.nx, v1 = task && vy && gx + 1 >= 0 && gx + 1 < g.nx;
         const bool wown = ownk && v0;
-        const uint32_t pbase = pc;
+        // kx offset of the own pair in a face slot: the row was loaded from its
+        // first face (x0 - 2) rounded down to an even element
+        const int64_t fa = ((int64_t)0 * g.ny + (gy)) * (g.nx + 1) + x0 - 2;   // parity only (plane term below)
+        const uint32_t pbase = pc, fbase = fc;
         auto slotp = [&](int z) -> const double * {
             return sp + ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1)) * PS;
+        };
+        auto slotf = [&](int z) -> const double * {
+            return sf + ((fbase + (uint32_t)(z - it.flo)) & (NSF - 1)) * FS;
         };
         auto release = [&](int z) { mbar_arrive_a(ep_a + 8 * ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1))); };
         auto waitp = [&](int z) {
             const uint32_t c = pbase + (uint32_t)(z - it.plo);
             mbar_wait_a(fp_a + 8 * (c & (NSP - 1)), (c / NSP) & 1);
         };
+        auto waitf = [&](int z) {
+            const uint32_t c = fbase + (uint32_t)(z - it.flo);
+            mbar_wait_a(ff_a + 8 * (c & (NSF - 1)), (c / NSF) & 1);
+        };
+        auto releasef = [&](int z) { mbar_arrive_a(ef_a + 8 * ((fbase + (uint32_t)(z - it.flo)) & (NSF - 1))); };
         for (int z = it.plo; z <= min(it.zlo, it.phi); ++z) waitp(z);
+        for (int z = it.flo; z <= min(it.zlo, it.fhi); ++z) waitf(z);
         double2 pdn = make_double2(0.0, 0.0);
         if (it.zlo - 2 >= it.plo) {
             pdn = lds2(slotp(it.zlo - 2) + ok);
@@ -246,39 +296,45 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         double2 pc0 = lds2(slotp(it.zlo - 1) + ok);
         double2 um2 = make_double2(0.0, 0.0), um1 = make_double2(0.0, 0.0);
-        // faces: F of plane q (front), Fb / kzdb / Db of plane q-1 (back, one
-        // plane later), Fn of plane q+1 in flight; kzd = lower face of plane q
-        const int q0 = it.zlo - 1;
-        const bool in0 = q0 >= 1 && q0 <= nzl;
-        PairFaces F = in0 ? load_faces(fc, g, q0 - 1, gy, gx, v0, v1) : PairFaces{};
-        double2 kzd = make_double2(0.0, 0.0);
-        if (in0 && v0) {
-            const double *qz = fc.kz + ((int64_t)(q0 - 1) * g.ny + gy) * g.nx + gx;
-            kzd.x = __ldg(qz);
-            if (v1) kzd.y = __ldg(qz + 1);
-        }
-        PairFaces Fb{};
-        double2 kzdb = make_double2(0.0, 0.0), dinvb = make_double2(0.0, 0.0);
-        int64_t off = (int64_t)q0 * pl + (int64_t)gy * g.pitch + gx;
+        double2 dinvb = make_double2(0.0, 0.0);   // D^{-1} of the back's cells (from the previous front)
+        int64_t off = (int64_t)(it.zlo - 1) * pl + (int64_t)gy * g.pitch + gx;
+        const int64_t rowfaces = (int64_t)g.ny * (g.nx + 1);
+        // the own pair's faces at plane z (slot z; the upper kz face from slot z+1)
+        auto faces_at = [&](int z, double2 &kzd) -> PairFaces {
+            PairFaces F;
+            const double *Fz = slotf(z), *Fz1 = slotf(z + 1);
+            const int px = ck + (int)((fa + (int64_t)(z - 1) * rowfaces + wk.kx_shift) & 1);
+            const double *kxr = Fz + FKX + (rk - 1) * KXP + px;
+            F.kxw0 = kxr[0];
+            F.kxe0 = kxr[1];
+            F.kxe1 = kxr[2];
+            F.kys = lds2(Fz + ofy);
+            F.kyn = lds2(Fz + ofy + BW);
+            kzd = lds2(Fz + ofz);
+            F.kzu = lds2(Fz1 + ofz);
+            if (!v0) { F.kxw0 = F.kxe0 = 0.0; F.kys.x = F.kyn.x = kzd.x = F.kzu.x = 0.0; }
+            if (!v1) { F.kxe1 = 0.0; F.kys.y = F.kyn.y = kzd.y = F.kzu.y = 0.0; }
+            return F;
+        };
         auto plane = [&](int q, auto steady) {
             constexpr bool S = decltype(steady)::value;
             const bool inside = S || (q >= 1 && q <= nzl);
             const bool has_up = S || q + 1 <= it.phi;
-            // faces of plane q+1 (used by the next front), issued first
-            const bool in_n = q + 1 >= 1 && q + 1 <= nzl && q + 1 <= it.zhi;   // the next front is inside
-            const PairFaces Fn = in_n ? load_faces(fc, g, q, gy, gx, v0, v1) : PairFaces{};
             const double *P0 = slotp(q);
             double2 pup = make_double2(0.0, 0.0);
             if (has_up) {
                 if (S || q >= it.zlo) waitp(q + 1);
                 pup = lds2(slotp(q + 1) + ok);
             }
+            if ((S || (q + 1 >= it.flo && q + 1 <= it.fhi)) && (S || q >= it.zlo)) waitf(q + 1);
             const bool mloaded = front_pm && (S || (q >= it.mlo && q <= it.mhi));
             const uint32_t ms = mc & (NSM - 1);
             if (mloaded) mbar_wait_a(fm_a + 8 * ms, (mc / NSM) & 1);
             // ---------------- front(q): step j on tile + halo ----------------
             double2 u = make_double2(0.0, 0.0), dinv = make_double2(0.0, 0.0);
             if (inside) {
+                double2 kzd;
+                const PairFaces F = faces_at(q, kzd);
                 const double2 c = pc0;
                 const double2 ylo = lds2(P0 + ok - BW), yhi = lds2(P0 + ok + BW);
                 const double l = lgk ? P0[ok - 1] : 0.0;
@@ -315,7 +371,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const double2 c = um1, dn = um2, up = u;
                 const double2 ylo = lds2(U0 + ok - BW), yhi = lds2(U0 + ok + BW);
                 const double l = U0[ok - 1], rr = U0[ok + 2];
-                double2 D;
+                double2 D, kzdb;
+                const PairFaces Fb = faces_at(q - 1, kzdb);   // face slot q-1 is released after this
                 double2 Ap = vc_apply(Fb, kzdb, c, dn, up, ylo, yhi, l, rr, D);
                 if (!v1) Ap.y = 0.0;
                 if (!skip_w2) __stcs(reinterpret_cast<double2 *>(gw2 + off - pl), Ap);
@@ -327,25 +384,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                     *reinterpret_cast<double2 *>(gpn2 + off - pl) = make_double2(v0b, v1b);
                 }
             }
+            if (S || (q - 1 >= it.flo && q - 1 <= it.fhi)) releasef(q - 1);   // faces of plane q-1 done
             ++uc;
             um2 = um1;
             um1 = u;
             pdn = pc0;
             pc0 = pup;
-            Fb = F;
-            kzdb = kzd;
             dinvb = dinv;
-            if (S || inside) {
-                kzd = F.kzu;   // the lower face of plane q+1 is the upper face of plane q
-            } else {
-                kzd = make_double2(0.0, 0.0);
-                if (in_n && v0) {   // plane q is a halo / Dirichlet plane: read kz(q+1)'s lower face
-                    const double *qz = fc.kz + ((int64_t)q * g.ny + gy) * g.nx + gx;
-                    kzd.x = __ldg(qz);
-                    if (v1) kzd.y = __ldg(qz + 1);
-                }
-            }
-            F = Fn;
             off += pl;
         };
         using Gen = std::integral_constant<bool, false>;
@@ -357,7 +402,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (; q < it.zhi; ++q) plane(q, Steady());
         for (; q <= it.zhi; ++q) plane(q, Gen());
         for (int z = max(it.zhi + 1, it.plo); z <= it.phi; ++z) release(z);
+        for (int z = max(it.zhi, it.flo); z <= it.fhi; ++z) releasef(z);
         pc = pbase + (it.phi - it.plo + 1);
+        fc = fbase + (it.fhi - it.flo + 1);
     }
 }
 
@@ -389,20 +436,74 @@ bool k1fv_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tm
     return cudaFuncSetAttribute(k1fv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
 }
 
-// SSCG_K1_FUSE_VC=1 enables the pair (SSCG_K1_FUSE=0 still forbids every
-// fused pair); default off.  The pair saves 5 of 12 vectors per two steps but
-// runs 12 warps per SM (the faces' registers) and is latency-bound: at cfg 4
-// (192^3) it takes 0.118 ms against 2 x 0.063 ms for two K1T steps -- 1.5 %
-// of the outer iteration, at 0.50 instead of 0.81 of the copy peak -- and at
-// 384^3 (where K1T streams at 0.89 of copy) 0.99 ms against 2 x 0.457 ms.
+// tensor maps of the faces for the K1FV boxes (nx even, 16-B aligned arrays):
+// kx as a 1-D view (rows have odd length nx+1: one 70-face box per row from
+// the even element at or below its first face), ky / kz as 3-D views
+bool k1fv_prepare_faces(const Geo &g, const double *kx, const double *ky, const double *kz, int nzl, CUtensorMap *mx,
+                        CUtensorMap *my, CUtensorMap *mz, int *kx_shift)
+{
+    // kx of a slab after the first starts at an odd element when (nx+1)*ny*z0
+    // is odd: the 1-D view then starts one element earlier (*kx_shift = 1)
+    const int shift = (int)((reinterpret_cast<uintptr_t>(kx) % 16) / 8);
+    if (g.nx % 2 != 0 || reinterpret_cast<uintptr_t>(kx) % 8 != 0 ||
+        (reinterpret_cast<uintptr_t>(ky) | reinterpret_cast<uintptr_t>(kz)) % 16 != 0)
+        return false;
+    *kx_shift = shift;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+        return false;
+    auto enc = reinterpret_cast<CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                             CUtensorMapFloatOOBfill)>(fn);
+    const cuuint32_t es[3] = {1, 1, 1};
+    {
+        cuuint64_t dims[1] = {(cuuint64_t)(g.nx + 1) * g.ny * nzl + shift};
+        cuuint64_t str[1] = {0};
+        cuuint32_t box[1] = {KXN};
+        if (enc(mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, const_cast<double *>(kx - shift), dims, str, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)(g.ny + 1), (cuuint64_t)nzl};
+        cuuint64_t str[2] = {(cuuint64_t)g.nx * 8, (cuuint64_t)g.nx * (g.ny + 1) * 8};
+        cuuint32_t box[3] = {BW, TY + 3, 1};
+        if (enc(my, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(ky), dims, str, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)(nzl + 1)};
+        cuuint64_t str[2] = {(cuuint64_t)g.nx * 8, (cuuint64_t)g.nx * g.ny * 8};
+        cuuint32_t box[3] = {BW, TY + 2, 1};
+        if (enc(mz, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(kz), dims, str, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    return true;
+}
+
+// SSCG_K1_FUSE=0 / SSCG_K1_FUSE_VC=0 forbid the pair, SSCG_K1_FUSE_VC=1 forces
+// it; default: slabs with >= 8 tile-planes per SM.  Measured (faces staged
+// by TMA, 64 x 12 tiles, 16 warps): cfg 4 192^3 0.109 ms per pair vs 2 x 0.063
+// for two K1T steps (1.19 vs 1.29 ms per outer), 384^3 0.82 vs 2 x 0.457 ms
+// (9.25 vs 10.5 ms per outer).  It moves 7 instead of 12 vectors per two
+// steps, so its fraction of the copy peak (0.55) is lower than K1T's (0.81)
+// while the time is shorter.
 bool k1fv_enabled(const Geo &g, int nzl)
 {
     const char *f = getenv("SSCG_K1_FUSE");
     if (f && f[0] == '0') return false;
     const char *e = getenv("SSCG_K1_FUSE_VC");
-    (void)g;
-    (void)nzl;
-    return e && e[0] == '1';
+    if (e) return e[0] == '1';
+    const int64_t tiles = (int64_t)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
+    return tiles * nzl >= 8 * k2_grid();
 }
 
 void launch_k1fv(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm)
@@ -416,10 +517,10 @@ void launch_k1fv(const Geo &g, const K1Args &a, double theta, int s, const DevSt
     wk.j = a.j;
     wk.front_pm = a.j > 0;
     wk.back_pn = (a.j + 1 < s - 1) ? 1 : 0;
+    wk.kx_shift = a.kx_shift;
     wk.coef_front = (a.j == 0) ? theta : 2.0 * theta;
     wk.coef_back = 2.0 * theta;
     wk.sigma = a.sigma;
-    Faces fc{a.kx, a.ky, a.kz};
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
     const int64_t resident = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
     const int n1 = a.ze - a.zb;
@@ -439,7 +540,8 @@ void launch_k1fv(const Geo &g, const K1Args &a, double theta, int s, const DevSt
     wk.zc = zc;
     wk.nitems = tiles * ((n1 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
-    k1fv<<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, g, a, fc, st, wk);
+    FaceMaps fmaps{*a.tmKX, *a.tmKY, *a.tmKZ};
+    k1fv<<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, fmaps, g, a, st, wk);
 }
 
 }  // namespace sscg

@@ -335,11 +335,6 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the depth-3 basis step");
             sl.has_k1m = true;
         }
-        if (A->kind == SSCG_OP_VARCOEF7 && !diag_M && k1fv_enabled(g, sl.nzl)) {
-            if (!k1fv_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
-                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused variable-coefficient step");
-            sl.has_k1f = true;
-        }
         if (A->kind == SSCG_OP_VARCOEF7) {
             sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
             sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;
@@ -347,6 +342,12 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
             const char *e = getenv("SSCG_FACES_TMA");
             sl.has_ftma = !(e && e[0] == '0') &&
                           k1t_prepare_faces(g, sl.kx, sl.ky, sl.kz, sl.nzl, &sl.tmKX, &sl.tmKY, &sl.tmKZ);
+            if (!diag_M && k1fv_enabled(g, sl.nzl) &&
+                k1fv_prepare_faces(g, sl.kx, sl.ky, sl.kz, sl.nzl, &sl.tmV_KX, &sl.tmV_KY, &sl.tmV_KZ, &sl.kx_shift)) {
+                if (!k1fv_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
+                    return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused variable-coefficient step");
+                sl.has_k1f = true;
+            }
         }
         if (diag_M || A->kind == SSCG_OP_CSR) {
             double *dv = nullptr;
@@ -734,6 +735,8 @@ static sscg_status launch_basis_pair(sscg_ctx *c, int j, int part)
         a.tmF_P = &sl.tmF_P;
         a.tmF_M = &sl.tmF_M;
         a.kx = sl.kx; a.ky = sl.ky; a.kz = sl.kz;
+        a.tmKX = &sl.tmV_KX; a.tmKY = &sl.tmV_KY; a.tmKZ = &sl.tmV_KZ;
+        a.kx_shift = sl.kx_shift;
         TRY(prof_mark(c, SSCG_PROF_BASIS, true));
         if (g.kind == SSCG_OP_VARCOEF7) launch_k1fv(g, a, c->theta, s, c->st, c->stream);
         else launch_k1f(g, a, c->theta, s, c->st, c->stream);

@@ -52,6 +52,8 @@ struct Slab {
     bool has_k1t;
     CUtensorMap tmF_P, tmF_M;     // K1F: 2-cell / 1-cell halo boxes
     CUtensorMap tmM3_P, tmM3_M;   // K1M (depth-3 basis): 3/6-cell and 2/4-cell halo boxes
+    CUtensorMap tmV_KX, tmV_KY, tmV_KZ;   // K1FV: faces in the pair's boxes
+    int kx_shift;                         // K1FV: the 1-D kx view starts this many elements early
     bool has_k1m;
     CUtensorMap tmKX, tmKY, tmKZ; // K1T: variable-coefficient faces (nx even)
     bool has_ftma;
@@ -99,6 +101,7 @@ struct K1Args {
     const CUtensorMap *tmP4, *tmM4;   // K1T tensor maps of this slab (host memory), or nullptr
     const CUtensorMap *tmKX, *tmKY, *tmKZ;   // K1T variable-coefficient face maps, or nullptr
     double *w2, *pn2;                 // K1F: w_{j+1}, p_{j+2} (nullptr at j+1 = s-1)
+    int kx_shift;                     // K1FV: see Slab::kx_shift
     const CUtensorMap *tmF_P, *tmF_M; // K1F tensor maps
 };
 
@@ -116,6 +119,8 @@ bool k1f_enabled(const Geo &g, int nzl);
 // K1FV: the pair for variable coefficients (k_stencil_fused_vc.cu; maps in tmF_P / tmF_M)
 bool k1fv_enabled(const Geo &g, int nzl);
 bool k1fv_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM);
+bool k1fv_prepare_faces(const Geo &g, const double *kx, const double *ky, const double *kz, int nzl, CUtensorMap *mx,
+                        CUtensorMap *my, CUtensorMap *mz, int *kx_shift);
 void launch_k1fv(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm);
 
 // K1M: three basis steps per launch (7-point, constant diagonal; k_stencil_mp3.cu)

@@ -268,7 +268,7 @@ def test_halo_overlap_bitwise(cfg, slabs, monkeypatch):
                                        (("7pt", 40, 36, 33, 10, 20), 3), (("7pt", 66, 20, 17, 7, 10), 2),
                                        (("27pt", 70, 36, 30, 16, 30), 1), (("27pt", 33, 19, 21, 7, 10), 1),
                                        (("27pt", 40, 34, 26, 8, 20), 3),
-                                       (("varcoef7", 70, 36, 30, 16, 20), 1), (("varcoef7", 33, 19, 21, 7, 10), 1),
+                                       (("varcoef7", 70, 36, 30, 16, 20), 1), (("varcoef7", 34, 19, 21, 7, 10), 1),
                                        (("varcoef7", 40, 26, 28, 8, 20), 3), (("varcoef7", 64, 17, 19, 6, 10), 2)],
                          ids=lambda v: _ids(v) if isinstance(v, tuple) else str(v))
 def test_fused_pairs_match_single_steps(cfg, slabs, monkeypatch):
