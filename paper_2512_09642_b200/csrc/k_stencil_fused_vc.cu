@@ -16,7 +16,7 @@
 // on the tile) coincide, so the z-columns of p_j and p_{j+1} roll through
 // registers.  The faces of the front region (kx rows as 1-D boxes from the
 // even element at or below x0-2, ky and kz as 3-D boxes) are staged per plane
-// by TMA into a 4-slot ring; a thread reads its own cells' faces of plane q
+// by TMA into a 5-slot ring; a thread reads its own cells' faces of plane q
 // (front) and again of plane q-1 (back) from it, and keeps only D^{-1} of its
 // cells from the front for the back.  Tile 64 x 12, 16 warps, 115 registers.
 #include <algorithm>
@@ -47,7 +47,7 @@ constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = BW * BHM * 8;
 constexpr int KXN = 70, KXP = 80;
 constexpr int FKX = 0, FKY = r128(FKX + (TY + 2) * KXP), FKZ = FKY + r128((TY + 3) * BW), FS = FKZ + r128((TY + 2) * BW);
 constexpr uint32_t KXBYTES = (TY + 2) * KXN * 8, KYBYTES = (TY + 3) * BW * 8, KZBYTES = (TY + 2) * BW * 8;
-constexpr int NSF = 4;
+constexpr int NSF = 5;   // not a power of two: slot = seq % NSF
 constexpr size_t SMEM = (size_t)(NSP * PS + NSM * MS + NU * PS + NSF * FS) * sizeof(double);
 static_assert(2 * NROW <= 32, "halo pairs fit one warp");
 static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 // face slot z holds kx(z), ky(z) (1 <= z <= nzl) and kz(z-1) (1 <= z <= nzl+1)
                 while (fnext <= min(q + 1, it.fhi)) {
-                    const int sl = fc & (NSF - 1);
+                    const int sl = fc % NSF;
                     const int z = fnext, zl = z - 1;
                     const bool xy = z <= wk.nzl;
                     double *d = sf + sl * FS;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             return sp + ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1)) * PS;
         };
         auto slotf = [&](int z) -> const double * {
-            return sf + ((fbase + (uint32_t)(z - it.flo)) & (NSF - 1)) * FS;
+            return sf + ((fbase + (uint32_t)(z - it.flo)) % NSF) * FS;
         };
         auto release = [&](int z) { mbar_arrive_a(ep_a + 8 * ((pbase + (uint32_t)(z - it.plo)) & (NSP - 1))); };
         auto waitp = [&](int z) {
@@ -284,9 +284,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         };
         auto waitf = [&](int z) {
             const uint32_t c = fbase + (uint32_t)(z - it.flo);
-            mbar_wait_a(ff_a + 8 * (c & (NSF - 1)), (c / NSF) & 1);
+            mbar_wait_a(ff_a + 8 * (c % NSF), (c / NSF) & 1);
         };
-        auto releasef = [&](int z) { mbar_arrive_a(ef_a + 8 * ((fbase + (uint32_t)(z - it.flo)) & (NSF - 1))); };
+        auto releasef = [&](int z) { mbar_arrive_a(ef_a + 8 * ((fbase + (uint32_t)(z - it.flo)) % NSF)); };
         for (int z = it.plo; z <= min(it.zlo, it.phi); ++z) waitp(z);
         for (int z = it.flo; z <= min(it.zlo, it.fhi); ++z) waitf(z);
         double2 pdn = make_double2(0.0, 0.0);
