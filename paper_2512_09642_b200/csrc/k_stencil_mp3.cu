@@ -42,7 +42,10 @@ constexpr int U2H = TY + 2;    // level-2 rows 2..TY+3
 constexpr int r128(int d) { return ((d * 8 + 127) / 128) * 128 / 8; }
 constexpr int PS = r128(BW * BHP), MS = r128(MW * MH), U1S = r128(BW * U1H), U2S = r128(BW * U2H);
 constexpr int STG = PS + MS;              // one stage: p_j(z) and p_{j-1}(z-1), one barrier
-constexpr int NST = 4, NU = 4;            // powers of two (slot = seq & (N - 1))
+#ifndef K1M_NST
+#define K1M_NST 6
+#endif
+constexpr int NST = K1M_NST, NU = 4;       // stages: slot = seq % NST;  U rings: power of two
 constexpr int NCW = TY + 4;               // one consumer warp per level-1 row
 constexpr int NCT = NCW * 32;
 constexpr int THREADS = NCT + 32;
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const ItemPlan it = plan_item(wk, item);
                 const int x0 = it.tx * TX, y0 = it.ty * TY;
                 for (int z = it.plo; z <= it.phi; ++z, ++sc) {
-                    const int sl = sc & (NST - 1);
+                    const int sl = sc % NST;
                     if (sc >= NST) mbar_wait(&empty[sl], ((sc / NST) - 1) & 1);
                     const bool m = wk.front_pm && z - 1 >= it.mlo && z - 1 <= it.mhi;
                     mbar_expect_tx(&full[sl], PBYTES + (m ? MBYTES : 0u));
@@ -192,12 +195,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int wb2 = it.first ? wk.zb[1] : it.zlo, we2 = it.last ? wk.ze[1] : it.zhi;
         const uint32_t sbase = sc;   // sequence number of stage plo
         auto stg = [&](int z) -> const double * {
-            return sstg + ((sbase + (uint32_t)(z - it.plo)) & (NST - 1)) * STG;
+            return sstg + ((sbase + (uint32_t)(z - it.plo)) % NST) * STG;
         };
-        auto release = [&](int z) { mbar_arrive_a(empty_a + 8 * ((sbase + (uint32_t)(z - it.plo)) & (NST - 1))); };
+        auto release = [&](int z) { mbar_arrive_a(empty_a + 8 * ((sbase + (uint32_t)(z - it.plo)) % NST)); };
         auto waits = [&](int z) {
             const uint32_t c = sbase + (uint32_t)(z - it.plo);
-            mbar_wait_a(full_a + 8 * (c & (NST - 1)), (c / NST) & 1);
+            mbar_wait_a(full_a + 8 * (c % NST), (c / NST) & 1);
         };
         for (int z = it.plo; z <= min(it.q0, it.phi); ++z) waits(z);
         double2 pdn = make_double2(0.0, 0.0);     // p_j(q-1), own cell
@@ -329,22 +332,23 @@ bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
     return cudaFuncSetAttribute(k1m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
 }
 
-// SSCG_K1_MP3 (read at every sscg_setup): "1" enables the triples for 7-point
-// single-slab solves; default off.  Measured at cfg 5: the first version
-// (separate p_j / p_{j-1} rings, two barriers per plane) took 1.006 ms per
-// triple, issue-bound (profiles/r01s_*); with p_{j-1} riding in the p_j stage,
-// one barrier per plane and a compile-time steady state it takes ~0.74 ms
-// (0.25 ms per step vs 0.265 for a K1F pair), but the outer iteration is the
-// same within noise (8.34 vs 8.36 ms over three A/B runs): the byte saving
-// (26 vs 31 vectors per outer) is spent on redundant halo work (1.21 vs 1.10
-// stencil evaluations per output point and step) and on shared-memory
-// bandwidth (l1tex 79 %).
+// SSCG_K1_MP3 (read at every sscg_setup): "1" / "0" force / forbid the
+// triples; unset: 7-point slabs with at least 8 tile-planes per SM (as K1F).
+// Measured at cfg 5: 8.06-8.12 ms per outer with triples against 8.36-8.39
+// with K1F pairs.  The first version (separate p_j / p_{j-1} rings, two
+// barriers per plane) took 1.006 ms per triple and was issue-bound
+// (profiles/r01s_*); p_{j-1} riding in the p_j stage, one barrier per plane, a
+// compile-time steady state and a 6-stage ring (4 stages left two planes of
+// prefetch) brought it to ~0.70 ms.
 bool k1m_enabled(const Geo &g, int nzl)
 {
     const char *e = getenv("SSCG_K1_MP3");
-    if (!(e && e[0] == '1')) return false;
-    (void)nzl;
-    return g.kind == 1;
+    if (g.kind != 1) return false;
+    if (e) return e[0] == '1';
+    const char *f = getenv("SSCG_K1_FUSE");   // "0": no fused basis kernels at all
+    if (f && f[0] == '0') return false;
+    const int64_t tiles = (int64_t)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
+    return tiles * nzl >= 8 * k2_grid();
 }
 
 // steps j, j+1, j+2 of one slab.  a.zb[l] / a.ze[l]: planes level l writes

@@ -608,7 +608,8 @@ static bool uses_wfree(const sscg_ctx *c)
 
 // K1 for step j over the planes of every local slab selected by `part`:
 //   0 = all planes, 1 = the two boundary planes (1 and nzl), 2 = the interior
-//   planes [2, nzl) that do not read a halo plane
+//   planes [2, nzl) that do not read a halo plane, 3 = the two planes next to
+//   each boundary (1, 2, nzl-1, nzl; the third step of a K1M triple)
 static sscg_status launch_basis(sscg_ctx *c, int j, int part)
 {
     const Geo &g = c->g;
@@ -647,6 +648,9 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
         } else if (part == 1) {
             a.zb = 1; a.ze = 2;
             a.zb2 = std::max(2, sl.nzl); a.ze2 = sl.nzl + 1;
+        } else if (part == 3) {
+            a.zb = 1; a.ze = std::min(3, sl.nzl + 1);
+            a.zb2 = std::max(a.ze, sl.nzl - 1); a.ze2 = sl.nzl + 1;
         } else {
             a.zb = 2; a.ze = sl.nzl;
             a.sm_cap = c->k1_sm_cap;
@@ -673,16 +677,23 @@ static bool uses_fused(const sscg_ctx *c)
     return true;
 }
 
-// K1M triples (three basis steps per launch): 7-point, one slab without
-// neighbours (with halos the pairs' boundary schedule is used)
+// K1M triples (three basis steps per launch): 7-point; with neighbours each
+// slab needs an interior for the third level ([3, nzl-1))
 static bool uses_mp3(const sscg_ctx *c)
 {
     if (c->basis != SSCG_BASIS_CHEBYSHEV || c->g.kind != SSCG_OP_STENCIL7) return false;
-    if (c->slabs.size() != 1 || c->nranks > 1) return false;
-    return c->slabs[0].has_k1m;
+    const bool halo = c->slabs.size() > 1 || c->nranks > 1;
+    for (const auto &sl : c->slabs)
+        if (!sl.has_k1m || (halo && sl.nzl < 8)) return false;
+    return true;
 }
 
-static sscg_status launch_basis_triple(sscg_ctx *c, int j)
+// halo = false: all planes of a slab bounded by Dirichlet planes; true: the
+// planes each level can form from p_j with its halo planes current (level 1
+// [2, nzl) -- its planes 1 and nzl come from the boundary single step --,
+// level 2 [2, nzl), level 3 [3, nzl-1)); the rest runs as single steps
+// around the exchanges (enqueue_outer)
+static sscg_status launch_basis_triple(sscg_ctx *c, int j, bool halo = false)
 {
     const Geo &g = c->g;
     const int s = c->s;
@@ -693,9 +704,10 @@ static sscg_status launch_basis_triple(sscg_ctx *c, int j)
             const int jl = j + l;   // step of level l+1
             a.w[l] = (!wf || jl == s - 1) ? sl.W + (int64_t)jl * g.vstride : nullptr;
             a.pn[l] = (jl + 1 <= s - 1) ? sl.P + (int64_t)(jl + 1) * g.vstride : nullptr;
-            a.zb[l] = 1;
-            a.ze[l] = sl.nzl + 1;
+            a.zb[l] = halo ? (l == 2 ? 3 : 2) : 1;
+            a.ze[l] = halo ? (l == 2 ? sl.nzl - 1 : sl.nzl) : sl.nzl + 1;
         }
+        if (halo) a.sm_cap = c->k1_sm_cap;
         a.nzl = sl.nzl;
         a.j = j;
         a.sigma = c->sigma;
@@ -759,8 +771,22 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const bool fuse = uses_fused(c), mp3 = uses_mp3(c);
     nvtxRangePushA("basis");
     for (int j = 0; j < s; ++j) {
-        if (mp3 && j + 2 < s) {   // steps j, j+1, j+2 in one pass (K1M; no halos)
-            TRY(launch_basis_triple(c, j));
+        if (mp3 && j + 2 < s) {   // steps j, j+1, j+2 in one pass (K1M)
+            if (!halo) {
+                TRY(launch_basis_triple(c, j));
+            } else {
+                // boundary planes of step j, exchange of p_{j+1} (overlapped with the
+                // interior triple), boundary planes of step j+1, exchange of p_{j+2},
+                // the two planes next to each boundary of step j+2, exchange of p_{j+3}
+                TRY(launch_basis(c, j, 1));
+                TRY(halo_fork(c, j + 1, ovl));
+                TRY(launch_basis_triple(c, j, true));
+                if (ovl) TRY(halo_join(c));
+                TRY(launch_basis(c, j + 1, 1));
+                TRY(halo_fork(c, j + 2, false));
+                TRY(launch_basis(c, j + 2, 3));
+                if (j + 3 < s) TRY(halo_fork(c, j + 3, false));
+            }
             j += 2;
         } else if (fuse && j + 1 < s) {   // steps j and j+1 in one pass (K1F)
             if (!halo) {

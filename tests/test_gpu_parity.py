@@ -299,14 +299,19 @@ def test_fused_pairs_match_single_steps(cfg, slabs, monkeypatch):
     assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
 
 
-@pytest.mark.parametrize("cfg", [("7pt", 40, 36, 33, 16, 25), ("7pt", 64, 40, 30, 9, 20), ("7pt", 60, 49, 23, 11, 20),
-                                 ("7pt", 112, 33, 70, 3, 10), ("7pt", 26, 24, 22, 8, 20)], ids=_ids)
-def test_triples_match_single_steps(cfg, monkeypatch):
+@pytest.mark.parametrize("cfg,slabs", [(("7pt", 40, 36, 33, 16, 25), 1), (("7pt", 64, 40, 30, 9, 20), 1),
+                                       (("7pt", 60, 49, 23, 11, 20), 1), (("7pt", 112, 33, 70, 3, 10), 1),
+                                       (("7pt", 26, 24, 22, 8, 20), 1), (("7pt", 40, 36, 33, 16, 25), 3),
+                                       (("7pt", 58, 30, 37, 10, 20), 2), (("7pt", 26, 24, 40, 7, 15), 4)],
+                         ids=lambda v: _ids(v) if isinstance(v, tuple) else str(v))
+def test_triples_match_single_steps(cfg, slabs, monkeypatch):
     """K1M (three basis steps per launch, p_{j+1} and p_{j+2} on chip) against
     K1T single steps and K1F pairs: the same arithmetic per point, so basis,
-    Gram and x agree to rounding; s = 16 / 9 / 11 / 3 / 8 end with a single
-    step, a pair, or nothing after the triples; ragged tiles in x and y and
-    z-chunks of several lengths.  All agree with the oracle."""
+    Gram and x agree to rounding; s = 16 / 9 / 11 / 3 / 8 / 10 / 7 end with a
+    single step, a pair, or nothing after the triples; ragged tiles in x and y
+    and z-chunks of several lengths; with several slabs the triple runs on the
+    interior and single steps on the planes next to each boundary around the
+    exchanges of p_{j+1}, p_{j+2}, p_{j+3}.  All agree with the oracle."""
     import paper_2512_09642_b200 as sscg
     kind, nx, ny, nz, s, nu = cfg
     P = Problem(kind, nx, ny, nz, s, nu)
@@ -315,7 +320,7 @@ def test_triples_match_single_steps(cfg, monkeypatch):
                       ("single", {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "0"})):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
-        with P.gpu_solver() as S:
+        with P.gpu_solver(slabs=slabs) as S:
             assert S.query(sscg.QUERY_BASIS_FUSED) == {"mp3": 3, "pairs": 2, "single": 1}[mode]
             x = S.solve(P.b_gpu(), rtol=0.0, max_outer=4).cpu().numpy()
             out[mode] = (x, S.gram(0)[0], [S.basis(j) for j in range(s)], S.gram(4)[0])
