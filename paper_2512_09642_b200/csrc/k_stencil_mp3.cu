@@ -333,7 +333,8 @@ bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
 }
 
 // SSCG_K1_MP3 (read at every sscg_setup): "1" / "0" force / forbid the
-// triples; unset: 7-point slabs with at least 8 tile-planes per SM (as K1F).
+// triples; unset: 7-point slabs with at least 64 tile-planes per SM (cfg 2,
+// 128^3 with ~21, runs faster with K1F pairs: 0.234 vs 0.267 ms per outer).
 // Measured at cfg 5: 8.06-8.12 ms per outer with triples against 8.36-8.39
 // with K1F pairs.  The first version (separate p_j / p_{j-1} rings, two
 // barriers per plane) took 1.006 ms per triple and was issue-bound
@@ -348,7 +349,7 @@ bool k1m_enabled(const Geo &g, int nzl)
     const char *f = getenv("SSCG_K1_FUSE");   // "0": no fused basis kernels at all
     if (f && f[0] == '0') return false;
     const int64_t tiles = (int64_t)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
-    return tiles * nzl >= 8 * k2_grid();
+    return tiles * nzl >= 64 * k2_grid();
 }
 
 // steps j, j+1, j+2 of one slab.  a.zb[l] / a.ze[l]: planes level l writes

@@ -13,8 +13,8 @@ C="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
 [ "$ONLY" = all ] && python bench.py > gpurun_out/bench_$TAG.json
 $C > gpurun_out/plain_$TAG.log 2>&1
 [ "$ONLY" = all ] && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $C > /dev/null 2>&1
-# skip the warm-up launches: K1F runs 8x per outer, K2R/K5 once (10 outer iterations in this command)
-for ks in "k1f 10" "k2r 3" "k5_update 3"; do
+# skip the warm-up launches: K1M runs 5x per outer (s = 16), K2R/K5 once (10 outer iterations in this command)
+for ks in "k1m 8" "k2r 3" "k5_update 3"; do
   set -- $ks
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 -o gpurun_out/prof_${TAG}_$1 $C > /dev/null 2>&1
 done
