@@ -40,7 +40,10 @@ constexpr int TX = 64, TY = 16;
 constexpr int BW = TX + 4, BH = TY + 2;                       // p box: x in [x0-2, x0+TX+2), y in [y0-1, y0+TY+1)
 constexpr int PSLOT = ((BW * BH * 8 + 127) / 128) * 128 / 8;  // doubles per p slot (128-B aligned)
 constexpr int MSLOT = TX * TY;                                // doubles per p_{j-1} slot
-constexpr int NSP = 6, NSM = 4;
+#ifndef K1T_NSP
+#define K1T_NSP 6
+#endif
+constexpr int NSP = K1T_NSP, NSM = 4;
 constexpr int NCW = TY / 2;                                   // consumer warps (2 rows each)
 constexpr int THREADS = 32 * (NCW + 1);
 constexpr uint32_t PBYTES = BW * BH * 8, MBYTES = TX * TY * 8;
