@@ -45,7 +45,14 @@ constexpr int STG = PS + MS;              // one stage: p_j(z) and p_{j-1}(z-1),
 #ifndef K1M_NST
 #define K1M_NST 6
 #endif
-constexpr int NST = K1M_NST, NU = 4;       // stages: slot = seq % NST;  U rings: power of two
+#ifndef K1M_NU
+#define K1M_NU 4
+#endif
+// stages: slot = seq % NST.  U rings: one barrier per plane orders every
+// access of plane n-1 before any of plane n+1 (a thread arrives for plane n
+// only after finishing it), so 3 slots would suffice; measured 6 stages / 4 U
+// slots 0.641 ms per launch, 7 / 3 0.656, 6 / 3 0.646
+constexpr int NST = K1M_NST, NU = K1M_NU;
 constexpr int NCW = TY + 4;               // one consumer warp per level-1 row
 constexpr int NCT = NCW * 32;
 constexpr int THREADS = NCT + 32;
@@ -245,15 +252,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (n0) *reinterpret_cast<double2 *>(n0 + off) = u1;
                 }
             }
-            *reinterpret_cast<double2 *>(su1 + (uc & (NU - 1)) * U1S + o1) = u1;
+            *reinterpret_cast<double2 *>(su1 + (uc % NU) * U1S + o1) = u1;
             if (S || (q >= it.plo && q <= it.phi)) release(q);
             // one barrier per plane: U1(q-1) and U2(q-2) of every thread are written
-            if (S || uc > 0) mbar_wait_a(ubar_a + 8 * ((uc - 1) & (NU - 1)), ((uc - 1) / NU) & 1);
+            if (S || uc > 0) mbar_wait_a(ubar_a + 8 * ((uc - 1) % NU), ((uc - 1) / NU) & 1);
             // ---------------- level 2: step j+1 at plane q-1 ----------------
             const int z2 = q - 1;
             double2 u2 = make_double2(0.0, 0.0);
             if (in2 && (S || (z2 >= 1 && z2 <= nzl))) {
-                const double *U = su1 + ((uc - 1) & (NU - 1)) * U1S;
+                const double *U = su1 + ((uc - 1) % NU) * U1S;
                 const double2 c = u1m1;
                 double2 Ap = stencil(U, o1, c, u1m2, u1, center);
                 u2.x = cf * (dinv_c * Ap.x - sigma * c.x) - pdn.x;   // pdn = p_j(q-1)
@@ -266,11 +273,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (n1) *reinterpret_cast<double2 *>(n1 + off - pl) = u2;
                 }
             }
-            if (in2) *reinterpret_cast<double2 *>(su2 + ((uc - 1) & (NU - 1)) * U2S + o2) = u2;
+            if (in2) *reinterpret_cast<double2 *>(su2 + ((uc - 1) % NU) * U2S + o2) = u2;
             // ---------------- level 3: step j+2 at plane q-2 ----------------
             const int z3 = q - 2;
             if (own && (S || (z3 >= it.zlo && z3 < it.zhi))) {
-                const double *U = su2 + ((uc - 2) & (NU - 1)) * U2S;
+                const double *U = su2 + ((uc - 2) % NU) * U2S;
                 const double2 c = u2m1;
                 double2 Ap = stencil(U, o2, c, u2m2, u2, center);
                 if (!v1) Ap.y = 0.0;
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     *reinterpret_cast<double2 *>(n2 + off - 2 * pl) = make_double2(v0b, v1b);
                 }
             }
-            mbar_arrive_a(ubar_a + 8 * (uc & (NU - 1)));   // this thread's U1(q), U2(q-1) are written
+            mbar_arrive_a(ubar_a + 8 * (uc % NU));   // this thread's U1(q), U2(q-1) are written
             ++uc;
             u2m2 = u2m1;
             u2m1 = u2;
