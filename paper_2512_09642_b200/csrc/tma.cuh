@@ -66,8 +66,23 @@ __device__ __forceinline__ void mbar_arrive_a(uint32_t bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+#ifndef SSCG_MBAR_SUSPEND_NS
+#define SSCG_MBAR_SUSPEND_NS 0
+#endif
+// waits on a precomputed shared address; with SSCG_MBAR_SUSPEND_NS > 0 the
+// try_wait carries a suspend-time hint (the warp sleeps in the barrier unit
+// instead of re-issuing the probe)
 __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t phase)
 {
+#if SSCG_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(phase), "n"(SSCG_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
@@ -75,6 +90,7 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t phase)
         "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
         "r"(phase)
         : "memory");
+#endif
 }
 
 // 2-D tensor tile load global -> shared, completion counted on `bar`
