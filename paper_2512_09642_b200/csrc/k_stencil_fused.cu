@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const int64_t pl = g.plane;
     const double center = wk.center, dinv_c = wk.dinv_c, sigma = wk.sigma;
     const double cfr = wk.coef_front, cbk = wk.coef_back;
-    if (KIND == 1) {
+    if constexpr (KIND == 1) {
         // 7-point: row-aligned tasks with the z-column in registers.  Warps
         // 1..TY+2 take box row r = warp and the tile's 32 pairs c = 2 + 2*lane;
         // the warps after them the halo pairs c = 0 and c = TX+2 of rows
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             pc = pbase + (it.phi - it.plo + 1);
         }
         return;
-    }
+    } else {
     for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
         const ItemPlan it = plan_item(wk, item);
         const int x0 = it.tx * TX, y0 = it.ty * TY;
@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         }
         pc = pbase + (it.phi - it.plo + 1);
     }
+    }   // KIND != 1
 }
 
 }  // namespace
