@@ -60,6 +60,7 @@ struct sscg_ctx {
     int s = 0, nu = 0;
     double lmin = 0, lmax = 0, theta = 0, sigma = 0;
     int rank = 0, nranks = 1, spr = 1;
+    bool nccl_self = false;   // SSCG_NCCL_SELF=1 with one rank: the NCCL paths on a 1-rank communicator
     int64_t nz_global = 1, z0_proc = 0, nzl_proc = 1, n_local = 0;
     std::vector<Slab> slabs;
     std::vector<void *> allocs;
@@ -398,6 +399,17 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         ncclUniqueId id;
         memcpy(&id, cm->nccl_id, sizeof id);
         NC(ncclCommInitRank(&c->comm, c->nranks, id, c->rank));
+    } else if (const char *e = getenv("SSCG_NCCL_SELF"); e && e[0] == '1') {
+        // test mode for a one-GPU box: a one-rank communicator carries the
+        // allreduces, and the halos of in-process slabs move by NCCL send/recv
+        // to self -- the NCCL calls, their graph capture and the polled waits
+        // of the multi-rank path, on data that makes the result bitwise equal
+        // to the plain in-process run
+        c->k1_sm_cap = k2_grid() - 2;
+        ncclUniqueId id;
+        NC(ncclGetUniqueId(&id));
+        NC(ncclCommInitRank(&c->comm, 1, id, 0));
+        c->nccl_self = true;
     }
     CU(cudaStreamSynchronize(c->stream));
     return SSCG_OK;
@@ -427,13 +439,17 @@ extern "C" void sscg_destroy(sscg_ctx *c)
 {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->cstream) cudaStreamSynchronize(c->cstream);
+    // the captured outer iteration holds NCCL's persistent plans: release it
+    // before the communicator (ncclCommDestroy waits for them otherwise)
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
     if (c->comm) ncclCommDestroy(c->comm);
     for (void *p : c->allocs) cudaFree(p);
     if (c->st_host) cudaFreeHost(c->st_host);
     if (c->xhost) cudaFreeHost(c->xhost);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto &e : c->prof_events) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -454,13 +470,22 @@ static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab, cudaStream_
     if (g.kind == SSCG_OP_CSR) return SSCG_OK;
     const size_t pb = (size_t)g.plane * sizeof(double);
     const int L = (int)c->slabs.size();
-    // in-process neighbours
+    // in-process neighbours (SSCG_NCCL_SELF: by NCCL send/recv to self, in order)
+    if (c->nccl_self && L > 1) NC(ncclGroupStart());
     for (int l = 0; l + 1 < L; ++l) {
         double *lo = vec_of_slab[l], *hi = vec_of_slab[l + 1];
         const int nzl = c->slabs[l].nzl;
+        if (c->nccl_self) {
+            NC(ncclSend(lo + (int64_t)nzl * g.plane, (size_t)g.plane, ncclDouble, 0, c->comm, strm));
+            NC(ncclRecv(hi, (size_t)g.plane, ncclDouble, 0, c->comm, strm));
+            NC(ncclSend(hi + g.plane, (size_t)g.plane, ncclDouble, 0, c->comm, strm));
+            NC(ncclRecv(lo + (int64_t)(nzl + 1) * g.plane, (size_t)g.plane, ncclDouble, 0, c->comm, strm));
+            continue;
+        }
         CU(cudaMemcpyAsync(hi, lo + (int64_t)nzl * g.plane, pb, cudaMemcpyDeviceToDevice, strm));
         CU(cudaMemcpyAsync(lo + (int64_t)(nzl + 1) * g.plane, hi + g.plane, pb, cudaMemcpyDeviceToDevice, strm));
     }
+    if (c->nccl_self && L > 1) NC(ncclGroupEnd());
     if (c->nranks > 1) {
         // remote neighbours of the first and last local slab (sscg_halo_plan)
         int64_t lo[6], hi[6];
@@ -526,7 +551,7 @@ static sscg_status prof_resolve(sscg_ctx *c)
 // SSCG_ERR_NCCL instead of hanging (SURVEY §5 failure detection).
 static sscg_status wait_stream(sscg_ctx *c, cudaStream_t strm)
 {
-    if (c->nranks == 1 || !c->comm) {
+    if (!c->comm) {
         CU(cudaStreamSynchronize(strm));
         return SSCG_OK;
     }
@@ -830,7 +855,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
         TRY(prof_mark(c, SSCG_PROF_GRAM, false));
         ++c->launches;
     }
-    if (c->nranks > 1) {
+    if (c->comm) {   // ranks (or the SSCG_NCCL_SELF test mode)
         TRY(prof_mark(c, SSCG_PROF_ALLREDUCE, true));
         NC(ncclAllReduce(c->blk, c->blk, (size_t)(s * s + s), ncclDouble, ncclSum, c->comm, c->stream));
         TRY(prof_mark(c, SSCG_PROF_ALLREDUCE, false));
@@ -855,7 +880,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
         }
         launch_budget(c->diag_part, L * DIAG_BLK, c->diag_sum, c->anorm, false, c->st, c->h_delta, c->h_pnorm,
                       c->h_budget, c->stream, 0);
-        if (c->nranks > 1) NC(ncclAllReduce(c->diag_sum, c->diag_sum, 1, ncclDouble, ncclSum, c->comm, c->stream));
+        if (c->comm) NC(ncclAllReduce(c->diag_sum, c->diag_sum, 1, ncclDouble, ncclSum, c->comm, c->stream));
         launch_budget(c->diag_part, L * DIAG_BLK, c->diag_sum, c->anorm, false, c->st, c->h_delta, c->h_pnorm,
                       c->h_budget, c->stream, 1);
         c->launches += 2;
@@ -1293,7 +1318,7 @@ extern "C" sscg_status sscg_set_option(sscg_ctx *c, int32_t key, int32_t value)
                 CU(cudaStreamSynchronize(c->stream));
                 for (double v : h) mx = std::max(mx, v);
             }
-            if (c->nranks > 1) {
+            if (c->comm) {
                 CU(cudaMemcpyAsync(c->diag_sum, &mx, sizeof(double), cudaMemcpyHostToDevice, c->stream));
                 NC(ncclAllReduce(c->diag_sum, c->diag_sum, 1, ncclDouble, ncclMax, c->comm, c->stream));
                 CU(cudaMemcpyAsync(&mx, c->diag_sum, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1359,7 +1384,7 @@ extern "C" sscg_status sscg_estimate_bounds(sscg_ctx *c, const double *v0, int32
                    c->lz_ticket + l, slabv + l, stop, st);
         }
         lz_sum(slabv, L, S + idx, stop, st);
-        if (c->nranks > 1) NC(ncclAllReduce(S + idx, S + idx, 1, ncclDouble, ncclSum, c->comm, st));
+        if (c->comm) NC(ncclAllReduce(S + idx, S + idx, 1, ncclDouble, ncclSum, c->comm, st));
         return SSCG_OK;
     };
     // ||v0||^2 from a packed copy, then y_0 = v0 / (||v0|| sqrt(D))

@@ -143,6 +143,39 @@ def test_slab_decomposition(cfg, slabs):
     assert np.linalg.norm(x - x_or) <= TOL_X10 * np.linalg.norm(x_or)
 
 
+@pytest.mark.parametrize("cfg,slabs,env", [(("7pt", 40, 36, 33, 10, 20), 3, {}),
+                                           (("7pt", 58, 30, 37, 10, 20), 2, {"SSCG_K1_MP3": "1"}),
+                                           (("varcoef7", 40, 26, 28, 8, 20), 3, {}),
+                                           (("27pt", 24, 20, 30, 8, 20), 4, {}),
+                                           (("7pt", 34, 18, 20, 5, 10), 2, {"SSCG_NO_OVERLAP": "1"})],
+                         ids=lambda v: _ids(v) if isinstance(v, tuple) else (str(v) if not isinstance(v, dict) else
+                                                                             "-".join(v) or "default"))
+def test_nccl_self_path(cfg, slabs, env, monkeypatch):
+    """The NCCL code of the multi-rank path on one GPU (SSCG_NCCL_SELF=1): a
+    one-rank communicator carries the Gram allreduce (and the Lanczos and
+    diagnostics reductions), the halos of in-process slabs move by
+    ncclSend/ncclRecv to self inside CUDA graphs, waits poll the
+    communicator.  A one-rank allreduce and a send/recv are exact copies, so
+    the solve must equal the plain in-process run bit for bit."""
+    kind, nx, ny, nz, s, nu = cfg
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    P = Problem(kind, nx, ny, nz, s, nu, lanczos=(kind != "7pt"))
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SSCG_NCCL_SELF", mode)
+        with P.gpu_solver(slabs=slabs) as S:
+            lb = S.estimate_bounds(P.b_gpu(), 20, 0.05) if kind != "7pt" else None
+            x = S.solve(P.b_gpu(), rtol=0.0, max_outer=5).cpu().numpy()
+            st = S.stats()
+            out[mode] = (x, S.gram(3)[0], st.allreduces, lb)
+    assert out["1"][2] == 6 and out["0"][2] == 0      # one allreduce per outer (+ the final stopping test)
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1])
+    if out["0"][3] is not None:
+        assert tuple(out["1"][3]) == tuple(out["0"][3])
+
+
 def test_csr_operator():
     import torch
 
