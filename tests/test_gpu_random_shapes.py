@@ -1,7 +1,9 @@
 """Randomised shapes (seeded): every operator kind, odd and tiny grids, basis
-sizes 1..40, several slabs, the schedule switches (fused pairs, TMA faces,
-recurrence update, DMMA Gram) forced both ways -- each run against the CPU
-oracle at outer 0 (north_star tolerances) and after a few outer iterations."""
+sizes 1..40, several slabs, the schedule switches (fused triples and pairs,
+the variable-coefficient pair, TMA faces, recurrence update, W-free Gram,
+streaming small-s Gram, DMMA Gram) forced both ways -- each run against the
+CPU oracle at outer 0 (north_star tolerances) and after a few outer
+iterations."""
 import numpy as np
 import pytest
 
@@ -12,7 +14,7 @@ pytestmark = pytest.mark.gpu
 KINDS = ["5pt", "7pt", "27pt", "varcoef7"]
 
 
-def _cases(n=64, seed=2024):
+def _cases(n=80, seed=2024):
     rng = np.random.default_rng(seed)
     out = []
     for i in range(n):
@@ -24,7 +26,9 @@ def _cases(n=64, seed=2024):
         slabs = 1 if kind == "5pt" else int(rng.choice([1, 1, 2, 3]))
         slabs = min(slabs, nz)
         env = {"SSCG_K1_FUSE": str(rng.integers(0, 2)), "SSCG_K5_RECUR": str(rng.integers(0, 2)),
-               "SSCG_K2_DMMA": str(rng.integers(0, 2)), "SSCG_FACES_TMA": str(rng.integers(0, 2))}
+               "SSCG_K2_DMMA": str(rng.integers(0, 2)), "SSCG_FACES_TMA": str(rng.integers(0, 2)),
+               "SSCG_K1_MP3": str(rng.integers(0, 2)), "SSCG_K1_FUSE_VC": str(rng.integers(0, 2)),
+               "SSCG_WFREE": str(rng.integers(0, 2)), "SSCG_K2S": str(rng.integers(0, 2))}
         out.append((kind, nx, ny, nz, s, nu, slabs, env))
     return out
 
