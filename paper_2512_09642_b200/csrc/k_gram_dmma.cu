@@ -1,6 +1,9 @@
-// K2D -- the tall-skinny Gram pass
+// K2D / K2R / K2S -- the tall-skinny Gram pass
 //   Ghat_ij = p_i^T w_j  (i <= j, W = AP)      c_i = p_i^T p_0
-// on the FP64 tensor-core path (mma.sync m8n8k4 f64, "DMMA"): Ghat = P W^T is
+// K2R (W-free schedule, the default): W recovered per point from the basis
+// recurrence (R23), below; K2S: the same for s <= 8 as a streaming
+// register-accumulator pass; K2D (stored W): this kernel.
+// K2D on the FP64 tensor-core path (mma.sync m8n8k4 f64, "DMMA"): Ghat = P W^T is
 // a dense contraction over the grid points, s x N times N x s.  Used for
 // s > 16, where the FP64 FMA count per byte (s(s+3)/2 per point) makes the
 // register-tiled K2 issue-bound (five consumer warps per SM at 255 registers);

@@ -4,9 +4,10 @@
 //   w_{j+1} = A p_{j+1},  p_{j+2} = 2 theta (D^{-1} w_{j+1} - sigma p_{j+1}) - p_j
 // with p_{j+1} kept on chip between the two steps (SURVEY §8(f) NEXT-3,
 // "matrix-powers" blocking of depth 2).  Per pair it streams p_j and p_{j-1}
-// in and w_j, p_{j+1}, w_{j+1}, p_{j+2} out: 6 vectors instead of the 8 of two
-// K1 launches (the per-outer basis traffic drops from 4s-3 = 61 to 46 vectors
-// at s = 16).
+// in and p_{j+1}, p_{j+2} out (+ w_j, w_{j+1} when the schedule stores W): 4
+// vectors instead of the 6 of two single steps in the W-free schedule (the
+// default for small 7-point slabs and every slab with neighbours; large
+// single slabs run K1M triples, k_stencil_mp3.cu).
 //
 // Same arithmetic, operand for operand, as K1T (k_stencil_tma.cu): the
 // front step computes p_{j+1} on the tile plus a one-cell x/y halo (the halo
@@ -19,9 +20,11 @@
 //              p_{j+1}(q) on tile + halo into the shared ring U (4 planes)
 //   back(q-1): w_{j+1}, p_{j+2} at plane q-1 from U(q-2..q) and p_j(q-1)
 // Warp 0 produces (TMA boxes of p_j and p_{j-1} into mbarrier rings), warps
-// 1..NCW consume (one front and one back task per thread and plane); one
-// named barrier per plane orders front(q) before back(q-1).  The kernel runs
-// at the HBM write-heavy mix ceiling (1 read : 2 writes, profiles/r01e).
+// 1..NCW consume.  7-point: row-aligned tasks whose front and back cells
+// coincide, z-columns in registers, per-plane mbarriers on U (see the KIND 1
+// branch); 27-point: one front and one back task per thread and plane with
+// one named barrier per plane.  7-point at 0.92 of its 2:2 mix ceiling
+// (DESIGN.md §6).
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
