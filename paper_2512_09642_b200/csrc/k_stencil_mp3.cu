@@ -32,7 +32,10 @@
 namespace sscg {
 namespace {
 
-constexpr int TX = 56, TY = 16;
+#ifndef K1M_TY
+#define K1M_TY 16
+#endif
+constexpr int TX = 56, TY = K1M_TY;
 constexpr int BW = TX + 12;    // p_j box: x in [x0-6, x0+TX+6)  (68)
 constexpr int BHP = TY + 6;    // p_j box: y in [y0-3, y0+TY+3)  (22)
 constexpr int MW = TX + 8;     // p_{j-1} box: x in [x0-4, x0+TX+4) (64), the level-1 cells
