@@ -31,6 +31,9 @@ namespace {
 
 // consumer warps: 16 while the accumulators are small (s <= 32), 8 above
 // (register budget); one producer warp
+#ifndef K2_DMMA_ASM
+#define K2_DMMA_ASM asm volatile
+#endif
 #ifndef K2_NCW_SMALL
 #define K2_NCW_SMALL 24
 #endif
@@ -69,7 +72,7 @@ __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_c
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+    K2_DMMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
