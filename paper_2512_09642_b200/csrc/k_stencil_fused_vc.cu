@@ -29,13 +29,19 @@
 namespace sscg {
 namespace {
 
-constexpr int TX = 64, TY = 12;
+#ifndef K1FV_TY
+#define K1FV_TY 12
+#endif
+#ifndef K1FV_NSP
+#define K1FV_NSP 4
+#endif
+constexpr int TX = 64, TY = K1FV_TY;
 constexpr int BW = TX + 4;                 // staged planes: x in [x0-2, x0+TX+2)
 constexpr int BHP = TY + 4;                // p_j: y in [y0-2, y0+TY+2)
 constexpr int BHM = TY + 2;                // p_{j-1}: y in [y0-1, y0+TY+1)
 constexpr int r128(int d) { return ((d * 8 + 127) / 128) * 128 / 8; }
 constexpr int PS = r128(BW * BHP), MS = r128(BW * BHM);
-constexpr int NSP = 4, NSM = 4, NU = 4;   // powers of two
+constexpr int NSP = K1FV_NSP, NSM = 4, NU = 4;   // powers of two
 constexpr int NROW = TY + 2;               // row warps 1..TY+2
 constexpr int NCW = NROW + 1;              // + one warp for the 2*(TY+2) halo pairs
 constexpr int NCT = NCW * 32;
