@@ -144,7 +144,7 @@ class Clocks:
     """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw,power.limit,clocks.mem")
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
@@ -170,7 +170,7 @@ class Clocks:
                 self.p.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
+        sm, mx, reasons, pw, pl, mem = [], [], set(), [], [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in (self.out or "").splitlines():
             f = [x.strip() for x in line.split(",")]
@@ -183,10 +183,22 @@ class Clocks:
             for nm, v in zip(names, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
+            for lst, k in ((pw, 8), (pl, 9), (mem, 10)):   # informational: power and memory clock
+                try:
+                    lst.append(float(f[k]))
+                except (ValueError, IndexError):
+                    pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if pw:
+            out["power_w"] = statistics.median(pw)
+        if pl:
+            out["power_limit_w"] = max(pl)
+        if mem:
+            out["mem_mhz"] = statistics.median(mem)
+        return out
 
 
 def max_over_ranks(dist, v: float, device="cuda") -> float:
