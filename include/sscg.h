@@ -8,7 +8,9 @@
  *        p_0 = r_k, p_1 = theta (M^{-1}A - sigma I) p_0,
  *        p_{j+1} = 2 theta (M^{-1}A - sigma I) p_j - p_{j-1}
  *      with theta = 2/(lmax-lmin), sigma = (lmax+lmin)/2,
- *      together with W = A P;
+ *      together with W = A P (the default schedule stores only w_{s-1}: the
+ *      Gram pass and the update recover every other w_j per point from the
+ *      recurrence, R21/R23);
  *   2. Ghat = P^T A P and c = P^T r_k in one pass, summed over all ranks with
  *      exactly one allreduce of the s x (s+1) block;
  *   3. the Ruhe scaling d_i = Ghat_ii^{-1/2}, G = S Ghat S = I + L + L^T,
