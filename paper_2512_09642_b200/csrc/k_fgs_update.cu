@@ -636,7 +636,10 @@ void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double 
     const bool vec = (g.pitch == g.nx) && (k.N % 2 == 0) && (k.xoff % 2 == 0);
     const int64_t work = vec ? k.N / 2 : k.N;
     int64_t blocks = (work + 255) / 256;
-    const int64_t cap = (int64_t)k2_grid() * 8;
+#ifndef K5_BLOCKS_PER_SM
+#define K5_BLOCKS_PER_SM 256   // measured at cfg 5: 8 -> 2.22 ms, 64 -> 2.13, 256 -> 2.09, 4096 -> 2.11
+#endif
+    const int64_t cap = (int64_t)k2_grid() * K5_BLOCKS_PER_SM;
     if (blocks > cap) blocks = cap;
     if (vec && k.rec) {
         switch (s) {
