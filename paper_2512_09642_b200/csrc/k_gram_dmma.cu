@@ -746,7 +746,12 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
         const double *P = sl.P + g.plane, *Wl = sl.W + (int64_t)(s - 1) * g.vstride + g.plane;
         const double *Dv = varm ? sl.dvec + g.plane : nullptr;
         const int nth = k2s_threads(s);
-        const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(k2_grid(), (k.N / 2 + nth - 1) / nth));
+#ifndef K2S_BLOCKS_PER_SM
+#define K2S_BLOCKS_PER_SM 1   // measured: 2, 4, 8 slower (the last-CTA sum grows)
+#endif
+        // the partial buffer holds 8 blocks per SM
+        const int gx = (int)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)k2_grid() * std::min(8, K2S_BLOCKS_PER_SM), (k.N / 2 + nth - 1) / nth));
 #define K2S_LAUNCH(S)                                                                                            \
         if (varm) k2s<S, true><<<gx, nth, 0, stream>>>(P, Wl, Dv, g.vstride, k, st);                            \
         else k2s<S, false><<<gx, nth, 0, stream>>>(P, Wl, Dv, g.vstride, k, st);
