@@ -582,9 +582,12 @@ int ep_for(int s_pad) { return s_pad <= 32 ? 132 : 68; }   // row pitch 32 mod 1
 #ifndef K2R_EP_MID
 #define K2R_EP_MID 132
 #endif
+#ifndef K2R_EP_PAIRS
+#define K2R_EP_PAIRS 184   // 23 k-step pairs per stage; cfg 5: 136 -> 2.04 ms, 184 -> 2.00, 216 -> 2.20
+#endif
 int ep_for_k2r(int s_pad)   // pairs: 64 mod 128 B (16-B loads); single k-steps: 32 mod 128 B
 {
-    return s_pad <= 16 ? 136 : s_pad <= 32 ? K2R_EP_MID : 68;
+    return s_pad <= 16 ? K2R_EP_PAIRS : s_pad <= 32 ? K2R_EP_MID : 68;
 }
 
 // consumer warp groups: each group works on its own stages, so the ring keeps
@@ -686,9 +689,9 @@ bool k2r_prepare(const Geo &g, Slab &sl, int s)
     const int64_t N = (int64_t)sl.nzl * g.plane;
     const int mx = 226 * 1024;
 #define K2R_ATTR(NB, EP, V) cudaFuncSetAttribute(k2r<NB, EP, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
-    if (K2R_ATTR(1, 136, false) || K2R_ATTR(2, 136, false) || K2R_ATTR(3, K2R_EP_MID, false) || K2R_ATTR(4, K2R_EP_MID, false) ||
+    if (K2R_ATTR(1, K2R_EP_PAIRS, false) || K2R_ATTR(2, K2R_EP_PAIRS, false) || K2R_ATTR(3, K2R_EP_MID, false) || K2R_ATTR(4, K2R_EP_MID, false) ||
         K2R_ATTR(5, 68, false) || K2R_ATTR(6, 68, false) || K2R_ATTR(7, 68, false) || K2R_ATTR(8, 68, false) ||
-        K2R_ATTR(1, 136, true) || K2R_ATTR(2, 136, true) || K2R_ATTR(3, K2R_EP_MID, true) || K2R_ATTR(4, K2R_EP_MID, true) ||
+        K2R_ATTR(1, K2R_EP_PAIRS, true) || K2R_ATTR(2, K2R_EP_PAIRS, true) || K2R_ATTR(3, K2R_EP_MID, true) || K2R_ATTR(4, K2R_EP_MID, true) ||
         K2R_ATTR(5, 68, true) || K2R_ATTR(6, 68, true) || K2R_ATTR(7, 68, true) || K2R_ATTR(8, 68, true))
         return false;
 #undef K2R_ATTR
@@ -801,8 +804,8 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     if (varm) k2r<NB, EP, true><<<gx, threads_for(NB, true), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);          \
     else k2r<NB, EP, false><<<gx, threads_for(NB, false), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);
     switch (nb) {
-    case 1: K2R_LAUNCH(1, 136) break;
-    case 2: K2R_LAUNCH(2, 136) break;
+    case 1: K2R_LAUNCH(1, K2R_EP_PAIRS) break;
+    case 2: K2R_LAUNCH(2, K2R_EP_PAIRS) break;
     case 3: K2R_LAUNCH(3, K2R_EP_MID) break;
     case 4: K2R_LAUNCH(4, K2R_EP_MID) break;
     case 5: K2R_LAUNCH(5, 68) break;
