@@ -52,7 +52,7 @@ UNIT = "GDOF/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)   # BASELINE cfg 5: "50 outer iterations timed"
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS),
@@ -141,16 +141,21 @@ def run_reference(a):
 
 # --------------------------------------------------------------------------
 class Clocks:
-    """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi sampler (B200_PROFILING.md): started before the warm-up so the
+    tool is already emitting when the timed region begins; samples whose
+    timestamps fall in the timed region are summarised (all samples under load
+    if the region is shorter than the 100 ms sampling interval)."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap,power.draw,power.limit,clocks.mem")
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.p = None
+        self.t0 = self.t1 = None
+        self.out = ""
 
-    def __enter__(self):
+    def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                        "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE,
@@ -159,8 +164,13 @@ class Clocks:
             self.p = None
         return self
 
-    def __exit__(self, *exc):
-        self.out = ""
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
+
+    def stop(self):
         if self.p:
             time.sleep(0.25)
             self.p.terminate()
@@ -170,15 +180,27 @@ class Clocks:
                 self.p.kill()
 
     def summary(self):
-        sm, mx, reasons, pw, pl, mem = [], [], set(), [], [], []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        import datetime
+        rows = []
         for line in (self.out or "").splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 8:
+            if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[1])); mx.append(float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
             except ValueError:
+                ts = None
+            rows.append((ts, f[1:]))
+        window = "timed region"
+        sel = [r for ts, r in rows if ts is not None and self.t0 is not None and self.t0 - 0.05 <= ts <= self.t1 + 0.05]
+        if not sel:
+            sel, window = [r for _, r in rows], "warm-up + timed region"
+        sm, mx, reasons, pw, pl, mem = [], [], set(), [], [], []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for f in sel:
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2]))
+            except (ValueError, IndexError):
                 continue
             for nm, v in zip(names, f[4:8]):
                 if v.lower().startswith("active"):
@@ -191,7 +213,7 @@ class Clocks:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-               "samples": len(sm)}
+               "samples": len(sm), "window": window}
         if pw:
             out["power_w"] = statistics.median(pw)
         if pl:
@@ -301,14 +323,17 @@ def run_ours(a):
         torch.cuda.synchronize()
 
     # r_0 = b and the first basis/Gram (untimed), then W warm-up steps
+    clk = Clocks(local).start()
     x = S.solve(b, rtol=0.0, max_outer=0)
     S.iterate(x, a.warmup)
     # timed region: exactly K outer iterations (CUDA-graph replay), device-timed
     # inside the library with CUDA events on its stream
     barrier()
-    with Clocks(local) as clk:
-        S.iterate(x, a.steps)
-        barrier()
+    clk.begin()
+    S.iterate(x, a.steps)
+    barrier()
+    clk.end()
+    clk.stop()
     st = S.stats()
     ms = max_over_ranks(dist, st.ms_total)
     value = n_global * a.steps / (ms / 1e3) / 1e9
