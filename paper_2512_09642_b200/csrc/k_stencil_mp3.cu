@@ -97,6 +97,19 @@ __device__ __forceinline__ uint32_t pin_u32(uint32_t v)
 
 __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 
+#ifndef K1M_PN_STCS
+#define K1M_PN_STCS 0
+#endif
+// store of a p_{j+l} pair (K1M_PN_STCS: evict-first)
+__device__ __forceinline__ void st_pn(double *p, double2 v)
+{
+#if K1M_PN_STCS
+    __stcs(reinterpret_cast<double2 *>(p), v);
+#else
+    *reinterpret_cast<double2 *>(p) = v;
+#endif
+}
+
 struct ItemPlan {
     int tx, ty, zlo, zhi;      // level-3 planes [zlo, zhi)
     int q0, q1;                // march: level-1 planes q0..q1
@@ -252,7 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (own && (S || (q >= wb1 && q < we1))) {
                     if (!v1) Ap.y = 0.0;
                     if (w0) __stcs(reinterpret_cast<double2 *>(w0 + off), Ap);
-                    if (n0) *reinterpret_cast<double2 *>(n0 + off) = u1;
+                    if (n0) st_pn(n0 + off, u1);
                 }
             }
             *reinterpret_cast<double2 *>(su1 + (uc % NU) * U1S + o1) = u1;
@@ -273,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (own && (S || (z2 >= wb2 && z2 < we2))) {
                     if (!v1) Ap.y = 0.0;
                     if (w1) __stcs(reinterpret_cast<double2 *>(w1 + off - pl), Ap);
-                    if (n1) *reinterpret_cast<double2 *>(n1 + off - pl) = u2;
+                    if (n1) st_pn(n1 + off - pl, u2);
                 }
             }
             if (in2) *reinterpret_cast<double2 *>(su2 + ((uc - 1) % NU) * U2S + o2) = u2;
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const double v0b = cf * (dinv_c * Ap.x - sigma * c.x) - u1m2.x;   // u1m2 = p_{j+1}(q-2)
                     double v1b = cf * (dinv_c * Ap.y - sigma * c.y) - u1m2.y;
                     if (!v1) v1b = 0.0;
-                    *reinterpret_cast<double2 *>(n2 + off - 2 * pl) = make_double2(v0b, v1b);
+                    st_pn(n2 + off - 2 * pl, make_double2(v0b, v1b));
                 }
             }
             mbar_arrive_a(ubar_a + 8 * (uc % NU));   // this thread's U1(q), U2(q-1) are written
@@ -316,6 +329,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 }  // namespace
 
+// TMA L2 promotion of the p_j / p_{j-1} boxes; 128 B or none measured the same
+// as 256 B (0.652-0.655 vs 0.656-0.660 ms per launch, within box noise), as
+// did evict-first stores of p_{j+l} (K1M_PN_STCS: 0.660-0.664 ms)
+#ifndef K1M_L2P
+#define K1M_L2P CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+
 bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM)
 {
     void *fn = nullptr;
@@ -332,11 +352,11 @@ bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
     cuuint32_t es[4] = {1, 1, 1, 1};
     cuuint32_t boxp[4] = {BW, BHP, 1, 1}, boxm[4] = {MW, MH, 1, 1};
     if (enc(tmP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxp, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, K1M_L2P,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     if (enc(tmM, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxm, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, K1M_L2P,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     return cudaFuncSetAttribute(k1m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
