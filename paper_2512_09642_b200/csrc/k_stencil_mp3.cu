@@ -20,7 +20,8 @@
 // neighbours come from shared memory (rings U1, U2 of the level-1/2
 // outputs).  Plane q of the march runs level 1 at q, level 2 at q-1, level 3
 // at q-2.  U1/U2 planes are published through per-plane mbarriers (every
-// consumer thread arrives); with 4 slots per ring a thread that waited for
+// consumer thread arrives -- one elected lane per warp after __syncwarp measured
+// 0.69-0.70 vs 0.65 ms per launch); with 4 slots per ring a thread that waited for
 // U1(q-2) / U2(q-3) knows every read of the slot it overwrites is done.
 #include <algorithm>
 #include <cstdlib>
