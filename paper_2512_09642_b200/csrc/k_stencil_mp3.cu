@@ -7,7 +7,8 @@
 // the schedule stores it): 5 vectors for three steps instead of 6 for a K1F
 // pair plus half of the next one.
 //
-// Same per-point arithmetic, operand for operand, as K1T/K1F.  Level l = 1..3
+// Same per-point arithmetic as K1T/K1F, with the six neighbour terms of A p
+// summed as a tree (K1M_TREE) rather than left to right.  Level l = 1..3
 // computes step j+l-1 on the tile (56 x 16) plus a (3-l)-cell halo in y and a
 // 2(3-l)-cell halo in x (x work is done in pairs of cells); p_j is staged by
 // TMA with a 3-cell y / 6-cell x halo.  Cells outside the grid are forced to
@@ -139,14 +140,26 @@ __device__ __forceinline__ ItemPlan plan_item(const K1MWork &wk, int64_t item)
     return p;
 }
 
+// K1M_TREE: the six neighbour terms summed as a tree (depth 3) instead of a
+// chain (depth 5); rounds differently from K1T/K1F in the last bits (within
+// the parity tolerances), measured 0.632-0.641 vs 0.652-0.653 ms per launch
+#ifndef K1M_TREE
+#define K1M_TREE 1
+#endif
+
 // 7-point A p on the pair at smem offset o of plane P0, own z-neighbours given
 __device__ __forceinline__ double2 stencil(const double *P0, int o, double2 c, double2 dn, double2 up, double center)
 {
     const double2 ylo = lds2(P0 + o - BW), yhi = lds2(P0 + o + BW);
     const double l = P0[o - 1], rr = P0[o + 2];
     double2 Ap;
+#if K1M_TREE
+    Ap.x = center * c.x - (((dn.x + up.x) + (ylo.x + yhi.x)) + (l + c.y));
+    Ap.y = center * c.y - (((dn.y + up.y) + (ylo.y + yhi.y)) + (c.x + rr));
+#else
     Ap.x = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
     Ap.y = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+#endif
     return Ap;
 }
 
@@ -165,8 +178,13 @@ __device__ __forceinline__ double2 stencil_eo(const double *U, int oe, double2 c
     const double ylx = U[oe - BW], yly = U[oe - BW + HW], yhx = U[oe + BW], yhy = U[oe + BW + HW];
     const double l = U[oe + HW - 1], rr = U[oe + 1];
     double2 Ap;
+#if K1M_TREE
+    Ap.x = center * c.x - (((dn.x + up.x) + (ylx + yhx)) + (l + c.y));
+    Ap.y = center * c.y - (((dn.y + up.y) + (yly + yhy)) + (c.x + rr));
+#else
     Ap.x = center * c.x - (dn.x + ylx + l + c.y + yhx + up.x);
     Ap.y = center * c.y - (dn.y + yly + c.x + rr + yhy + up.y);
+#endif
     return Ap;
 }
 
