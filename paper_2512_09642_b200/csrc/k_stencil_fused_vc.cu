@@ -26,6 +26,12 @@
 #include "sscg_internal.cuh"
 #include "tma.cuh"
 
+// K1FV_TREE=1: the face terms summed as a tree, as K1M/K1F do; measured neutral
+// at cfg 4 (0.0964-0.0966 ms per pair either way), so the chain is kept
+#ifndef K1FV_TREE
+#define K1FV_TREE 0
+#endif
+
 namespace sscg {
 namespace {
 
@@ -127,8 +133,16 @@ __device__ __forceinline__ double2 vc_apply(const PairFaces &F, double2 kzd, dou
     D.x = kzd.x + F.kys.x + F.kxw0 + F.kxe0 + F.kyn.x + F.kzu.x;
     D.y = kzd.y + F.kys.y + F.kxe0 + F.kxe1 + F.kyn.y + F.kzu.y;
     double2 Ap;
+#if K1FV_TREE
+    // z, y, x face pairs summed as a tree (depth 4 instead of a 6-long FMA chain)
+    Ap.x = D.x * c.x - (((kzd.x * dn.x + F.kzu.x * up.x) + (F.kys.x * ylo.x + F.kyn.x * yhi.x)) +
+                        (F.kxw0 * l + F.kxe0 * c.y));
+    Ap.y = D.y * c.y - (((kzd.y * dn.y + F.kzu.y * up.y) + (F.kys.y * ylo.y + F.kyn.y * yhi.y)) +
+                        (F.kxe0 * c.x + F.kxe1 * rr));
+#else
     Ap.x = D.x * c.x - (kzd.x * dn.x + F.kzu.x * up.x + F.kys.x * ylo.x + F.kxw0 * l + F.kxe0 * c.y + F.kyn.x * yhi.x);
     Ap.y = D.y * c.y - (kzd.y * dn.y + F.kzu.y * up.y + F.kys.y * ylo.y + F.kxe0 * c.x + F.kxe1 * rr + F.kyn.y * yhi.y);
+#endif
     return Ap;
 }
 
