@@ -142,7 +142,9 @@ __device__ __forceinline__ ItemPlan plan_item(const K1MWork &wk, int64_t item)
 
 // K1M_TREE: the six neighbour terms summed as a tree (depth 3) instead of a
 // chain (depth 5); rounds differently from K1T/K1F in the last bits (within
-// the parity tolerances), measured 0.632-0.641 vs 0.652-0.653 ms per launch
+// the parity tolerances), measured 0.632-0.641 vs 0.652-0.653 ms per launch.
+// Folding the recurrence as fma(c D^{-1}, A p, fma(-c sigma, p, -p_prev)) (one
+// FMA after A p instead of three operations) measured slower: 0.68 vs 0.64 ms
 #ifndef K1M_TREE
 #define K1M_TREE 1
 #endif
