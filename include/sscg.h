@@ -162,7 +162,10 @@ SSCG_API sscg_status sscg_solve(sscg_ctx *ctx, const double *b, double *x, doubl
 
 /* Same as sscg_solve with HOST b and x (process-local, pageable or pinned):
  * b is copied to the device, x is copied in (unless X0_ZERO) and back out.
- * The copies are part of the call (end-to-end path). */
+ * The copies are part of the call (end-to-end path).  With a page-locked
+ * x_host (cudaMallocHost / cudaHostRegister) the copy of x out overlaps the
+ * last outer iteration (the one that only evaluates the stopping test); a
+ * pageable x_host is copied after the solve completes. */
 SSCG_API sscg_status sscg_solve_host(sscg_ctx *ctx, const double *b_host, double *x_host, double rtol,
                             int32_t max_outer, uint32_t flags);
 

@@ -138,6 +138,20 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def _check_dev(name, t, n):
+    """A process-local float64 CUDA vector of n elements (ValueError otherwise:
+    the library writes n doubles through the raw pointer)."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+            and t.numel() == n):
+        raise ValueError(f"{name}: need a contiguous float64 CUDA tensor of {n} elements")
+
+
+def _check_host(name, a, n):
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and a.size == n):
+        raise ValueError(f"{name}: need a C-contiguous float64 numpy array of {n} elements")
+
+
 def _ptr(t):
     """Device/host pointer of a torch tensor or numpy array (no copies)."""
     if t is None:
@@ -236,7 +250,7 @@ class Solver:
         """Lanczos bounds of M^{-1}A from v0 (cuda float64, process-local);
         returns (lmin, lmax) or, with tridiag=True, (lmin, lmax, alpha, beta)."""
         import torch
-        assert v0.is_cuda and v0.dtype == torch.float64 and v0.is_contiguous() and v0.numel() == self.n_local
+        _check_dev("v0", v0, self.n_local)
         cur = torch.cuda.current_stream()
         if cur.cuda_stream != 0:
             cur.synchronize()
@@ -264,12 +278,14 @@ class Solver:
         """b, x: float64 CUDA tensors (process-local).  x=None => x_0 = 0 and a
         new tensor is returned; otherwise x is updated in place."""
         import torch
-        assert b.is_cuda and b.dtype == torch.float64 and b.is_contiguous() and b.numel() == self.n_local
+        _check_dev("b", b, self.n_local)
         flags = 0
         if x is None:
             x = torch.empty_like(b)
             flags = SOLVE_X0_ZERO
-        assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous() and x.numel() == self.n_local
+        _check_dev("x", x, self.n_local)
+        if x.device != b.device:
+            raise ValueError("b and x must be on the same device")
         cur = torch.cuda.current_stream()
         if cur.cuda_stream != 0:      # the library stream orders only after the legacy default stream
             cur.synchronize()
@@ -281,16 +297,18 @@ class Solver:
 
     def solve_host(self, b: np.ndarray, x: np.ndarray | None = None, rtol: float = 1e-8, max_outer: int = 1000):
         """End-to-end call with host buffers (copies are inside the call)."""
-        assert b.dtype == np.float64 and b.flags.c_contiguous and b.size == self.n_local
+        _check_host("b", b, self.n_local)
         flags = 0
         if x is None:
             x = np.empty_like(b)
             flags = SOLVE_X0_ZERO
+        _check_host("x", x, self.n_local)
         _check(load().sscg_solve_host(self._h, _ptr(b), _ptr(x), rtol, max_outer, flags))
         return x
 
     def iterate(self, x, nsteps: int):
         """Exactly nsteps more outer iterations from the last solve's state."""
+        _check_dev("x", x, self.n_local)
         _check(load().sscg_iterate(self._h, _ptr(x), nsteps))
         return x
 

@@ -55,12 +55,12 @@ def build(force: bool = False, verbose: bool = False, defs=(), variant: str = ""
     if verbose:
         common += ["-Xptxas", "-v"]
     common += list(defs)
-    objs = []
-    for src in sources():
-        obj = os.path.join(bdir, os.path.basename(src) + ".o")
-        cmd = [NVCC] + common + ["-c", src, "-o", obj]
-        subprocess.check_call(cmd)
-        objs.append(obj)
+    objs = [os.path.join(bdir, os.path.basename(src) + ".o") for src in sources()]
+    cmds = [[NVCC] + common + ["-c", src, "-o", obj] for src, obj in zip(sources(), objs)]
+    # one nvcc per source, in parallel (each is single-threaded)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        list(ex.map(subprocess.check_call, cmds))
     link = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-L", libdir, "-l:libnccl.so.2",
                                                            "-Xlinker", "-rpath=" + libdir, "-cudart", "static"]
     subprocess.check_call(link)

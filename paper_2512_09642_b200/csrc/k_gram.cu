@@ -226,13 +226,13 @@ struct K2Plan {
     size_t smem;
 };
 
-K2Plan plan(int s)
+K2Plan plan(const Geo &g, int s)
 {
     K2Plan p;
     p.TB = (s <= 8) ? 4 : 8;
     p.E = (s <= 16) ? 256 : (s <= 32 ? 128 : 64);
-    if (const char *e = getenv("SSCG_K2_E")) {   // tuning override (64 / 128 / 256)
-        const int v = atoi(e);
+    if (g.kn.k2_e) {   // tuning override (64 / 128 / 256)
+        const int v = g.kn.k2_e;
         if ((v == 64 || v == 128 || v == 256) && (s > 8)) p.E = v;
     }
     p.s_pad = (s + p.TB - 1) / p.TB * p.TB;
@@ -248,7 +248,7 @@ K2Plan plan(int s)
     while (p.roles_cta * p.nsl * 2 <= 7) p.nsl *= 2;
     const size_t stage = (size_t)2 * p.s_pad * p.E * sizeof(double);
     p.nstage = (int)std::min<size_t>(MAX_STAGE, (200 * 1024) / stage);
-    if (const char *e = getenv("SSCG_K2_NS")) p.nstage = std::max(2, std::min(p.nstage, atoi(e)));
+    if (g.kn.k2_ns) p.nstage = std::max(2, std::min(p.nstage, g.kn.k2_ns));
     p.smem = stage * p.nstage;
     p.threads = 32 * (1 + p.roles_cta * p.nsl);
     return p;
@@ -301,7 +301,7 @@ bool encode_rows_map(CUtensorMap *m, const double *base, int64_t inner, int rows
 
 bool k2_prepare(const Geo &g, Slab &sl, int s)
 {
-    const K2Plan p = plan(s);
+    const K2Plan p = plan(g, s);
     const int64_t N = (int64_t)sl.nzl * g.plane;
     // opt in to the large dynamic shared memory once (outside any graph capture)
     const int mx = 210 * 1024;   // >= every plan's ring (<= 200 KB) + static smem fits 227 KB
@@ -313,7 +313,7 @@ bool k2_prepare(const Geo &g, Slab &sl, int s)
     if (!encode_rows_map(&sl.tmP, sl.P + g.plane, N, s, g.vstride, p.E, p.s_pad) ||
         !encode_rows_map(&sl.tmW, sl.W + g.plane, N, s, g.vstride, p.E, p.s_pad))
         return false;
-    sl.has_k2d = k2d_enabled(s);
+    sl.has_k2d = k2d_enabled(g, s);
     return !sl.has_k2d || k2d_prepare(g, sl, s);
 }
 
@@ -331,7 +331,7 @@ void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *
         launch_k2d(g, sl, s, st, out_blk, stream);
         return;
     }
-    const K2Plan p = plan(s);
+    const K2Plan p = plan(g, s);
     K2Params k;
     k.N = (int64_t)sl.nzl * g.plane;
     k.s = s;
@@ -346,7 +346,7 @@ void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *
     k.ticket = sl.ticket;
     const int64_t nchunks = (k.N + p.E - 1) / p.E;
     int gx = std::max(1, k2_grid() / p.gy);   // gx * gy CTAs: one per SM, all resident
-    if (const char *e = getenv("SSCG_K2_GRID")) gx = std::max(1, std::min(gx, atoi(e)));   // tuning
+    if (g.kn.k2_grid) gx = std::max(1, std::min(gx, g.kn.k2_grid));   // tuning
     if (nchunks < gx) gx = (int)nchunks;
     dim3 grid(gx, p.gy);
     if (p.TB == 4) launch_t<4, 256>(sl.tmP, sl.tmW, k, p, grid, st, stream);

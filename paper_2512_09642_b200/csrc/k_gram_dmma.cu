@@ -598,15 +598,6 @@ int ep_for_k2r(int s_pad)   // pairs: 64 mod 128 B (16-B loads); single k-steps:
 // group running a full ring ahead would match the parity of an older phase.
 int gcd_int(int a, int b) { return b ? gcd_int(b, a % b) : a; }
 
-int env_groups()
-{
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("SSCG_K2_GROUPS");   // tuning override
-        env = e ? std::max(1, atoi(e)) : 0;
-    }
-    return env;
-}
 
 // largest g <= want dividing every value in {a, b}
 int common_divisor_le(int want, int a, int b)
@@ -624,11 +615,10 @@ int stages_for(int s_pad, int ep)
 
 }  // namespace
 
-bool k2d_enabled(int s)
+bool k2d_enabled(const Geo &g, int s)
 {
-    const char *e = getenv("SSCG_K2_DMMA");   // "0" never, "1" always, unset: s > 16
-    if (e && e[0] == '0') return false;
-    if (e && e[0] == '1') return s >= 1;
+    if (g.kn.k2_dmma == 0) return false;   // SSCG_K2_DMMA: "0" never, "1" always, unset: s > 16
+    if (g.kn.k2_dmma == 1) return s >= 1;
     return s > 16;
 }
 
@@ -657,7 +647,7 @@ void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double 
     k.s = s;
     k.s_pad = s_pad;
     k.nstage = stages_for(s_pad, ep);
-    k.ngroups = common_divisor_le(env_groups() ? env_groups() : k.nstage, k.nstage, ncw_for(nb));
+    k.ngroups = common_divisor_le(g.kn.k2_groups ? g.kn.k2_groups : k.nstage, k.nstage, ncw_for(nb));
     k.part = sl.part;
     k.out = out_blk;
     k.ticket = sl.ticket;
@@ -732,12 +722,7 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     const bool varm = sl.dvec != nullptr;
     K2RParams k;
     k.N = (int64_t)sl.nzl * g.plane;
-    static int k2s_env = -1;
-    if (k2s_env < 0) {
-        const char *e = getenv("SSCG_K2S");   // "0": keep the tensor-core pass for s <= 8
-        k2s_env = (e && e[0] == '0') ? 0 : 1;
-    }
-    if (k2s_env && s >= 2 && s <= 8) {
+    if (g.kn.k2s && s >= 2 && s <= 8) {
         k.s = s;
         k.inv_theta = 1.0 / theta;
         k.inv_2theta = 1.0 / (2.0 * theta);
@@ -774,16 +759,12 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     k.s_pad = s_pad;
     k.wlp = (ep * 8 + 127) / 128 * 128 / 8;
     const size_t stage = (size_t)(s_pad * ep + k.wlp * (varm ? 2 : 1)) * sizeof(double);
-    static int smem_kb = -1;
-    if (smem_kb < 0) {
-        const char *e = getenv("SSCG_K2_SMEM_KB");
-        smem_kb = e ? std::min(224, std::max(64, atoi(e))) : 216;
-    }
+    const int smem_kb = g.kn.k2_smem_kb;
     {
         // 4 groups by default (each with nstage/4 slots), nstage a multiple of the groups
         const int nsmax = (int)std::max<size_t>(1, std::min<size_t>(MAXS, ((size_t)smem_kb * 1024) / stage));
-        const int g = common_divisor_le(env_groups() ? env_groups() : 4, ncw_for(nb, varm), ncw_for(nb, varm));
-        k.ngroups = std::min(g, nsmax);
+        const int gr = common_divisor_le(g.kn.k2_groups ? g.kn.k2_groups : 4, ncw_for(nb, varm), ncw_for(nb, varm));
+        k.ngroups = std::min(gr, nsmax);
         while (ncw_for(nb, varm) % k.ngroups) --k.ngroups;
         k.nstage = std::max(k.ngroups, nsmax / k.ngroups * k.ngroups);
     }

@@ -533,9 +533,8 @@ constexpr int64_t K1F_MIN_WORK = 8;
 
 bool k1f_enabled(const Geo &g, int nzl)
 {
-    const char *e = getenv("SSCG_K1_FUSE");
-    if (e && e[0] == '0') return false;
-    if (e && e[0] == '1') return true;
+    if (g.kn.k1_fuse == 0) return false;
+    if (g.kn.k1_fuse == 1) return true;
     const int64_t tiles = (int64_t)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
     return g.kind == 1 && tiles * nzl >= K1F_MIN_WORK * k2_grid();
 }
@@ -565,11 +564,7 @@ void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevSta
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
     // one CTA per SM (fewer with a.sm_cap: SMs left to the overlapped NCCL exchange)
     const int64_t resident = (int64_t)MINB * ((a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid());
-    static int zc_env = -1;
-    if (zc_env < 0) {
-        const char *e = getenv("SSCG_K1_ZC");
-        zc_env = e ? std::max(1, atoi(e)) : 0;
-    }
+    const int zc_env = g.kn.k1_zc;
     const int n1 = a.ze - a.zb;
     if (n1 <= 0) return;
     int zc = n1;

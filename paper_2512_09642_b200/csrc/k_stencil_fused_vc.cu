@@ -518,10 +518,8 @@ bool k1fv_prepare_faces(const Geo &g, const double *kx, const double *ky, const 
 // while the time is shorter.
 bool k1fv_enabled(const Geo &g, int nzl)
 {
-    const char *f = getenv("SSCG_K1_FUSE");
-    if (f && f[0] == '0') return false;
-    const char *e = getenv("SSCG_K1_FUSE_VC");
-    if (e) return e[0] == '1';
+    if (g.kn.k1_fuse == 0) return false;
+    if (g.kn.k1_fuse_vc >= 0) return g.kn.k1_fuse_vc == 1;
     const int64_t tiles = (int64_t)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
     return tiles * nzl >= 8 * k2_grid();
 }

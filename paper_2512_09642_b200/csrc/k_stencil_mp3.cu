@@ -436,11 +436,9 @@ bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
 // prefetch) brought it to ~0.70 ms.
 bool k1m_enabled(const Geo &g, int nzl)
 {
-    const char *e = getenv("SSCG_K1_MP3");
     if (g.kind != 1) return false;
-    if (e) return e[0] == '1';
-    const char *f = getenv("SSCG_K1_FUSE");   // "0": no fused basis kernels at all
-    if (f && f[0] == '0') return false;
+    if (g.kn.k1_mp3 >= 0) return g.kn.k1_mp3 == 1;
+    if (g.kn.k1_fuse == 0) return false;   // SSCG_K1_FUSE=0: no fused basis kernels at all
     const int64_t tiles = (int64_t)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
     return tiles * nzl >= 64 * k2_grid();
 }
@@ -473,11 +471,7 @@ void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st
     }
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
     const int64_t resident = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
-    static int zc_env = -1;
-    if (zc_env < 0) {
-        const char *e = getenv("SSCG_K1_ZC");
-        zc_env = e ? std::max(1, atoi(e)) : 0;
-    }
+    const int zc_env = g.kn.k1_zc;
     const int n1 = a.ze[2] - a.zb[2];
     if (n1 <= 0) return;
     int zc = n1;

@@ -430,12 +430,7 @@ __global__ void __launch_bounds__(THREADS, KIND >= 3 ? 1 : 2)
 
 bool k1t_supported(const Geo &g, const K1Args &a)
 {
-    static int off = -1;
-    if (off < 0) {
-        const char *e = getenv("SSCG_K1_TMA");
-        off = (e && e[0] == '0') ? 1 : 0;
-    }
-    return !off && g.kind >= 1 && g.kind <= 3 && a.mode <= 2 && a.tmP4 && a.tmM4;
+    return g.kn.k1_tma && g.kind >= 1 && g.kind <= 3 && a.mode <= 2 && a.tmP4 && a.tmM4;
 }
 
 bool k1t_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP4, CUtensorMap *tmM4)
@@ -490,7 +485,7 @@ bool k1t_prepare_faces(const Geo &g, const double *kx, const double *ky, const d
                                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                                              CUtensorMapFloatOOBfill)>(fn);
     const cuuint32_t es[3] = {1, 1, 1};
-    const bool dbg = getenv("SSCG_DEBUG") != nullptr;
+    const bool dbg = g.kn.debug != 0;
     {
         // rows of kx have an odd length (nx+1), so every other row starts at an
         // odd element: a 1-D view, one 68-element box per face row starting at
@@ -538,7 +533,8 @@ void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t 
     wk.j = a.j;
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
     const int kind = (g.kind == 3 && a.tmKX) ? 4 : g.kind;
-    static int occs[5] = {0, 0, 0, 0, 0}, zc_env = -1;
+    static int occs[5] = {0, 0, 0, 0, 0};
+    const int zc_env = g.kn.k1_zc;
     int &occ = occs[kind];
     if (!occ) {
         const void *fn = kind == 1 ? (const void *)k1t<1> : kind == 2 ? (const void *)k1t<2>
@@ -546,8 +542,6 @@ void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t 
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, kind == 4 ? SMEM4 : SMEM) != cudaSuccess ||
             occ <= 0)
             occ = 1;
-        const char *e = getenv("SSCG_K1_ZC");
-        zc_env = e ? std::max(1, atoi(e)) : 0;
     }
     const int sms = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
     const int64_t resident = (int64_t)sms * occ;

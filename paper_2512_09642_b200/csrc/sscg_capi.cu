@@ -85,6 +85,8 @@ struct sscg_ctx {
     double *x_host_out = nullptr;   // sscg_solve_host: copy x out as soon as it is final
     bool x_copied = false;
     bool overlap = true;
+    bool failed = false;            // an NCCL abort left the context unusable (every call: SSCG_ERR_NCCL)
+    double nccl_timeout_s = 600.0;  // SSCG_NCCL_TIMEOUT_S, read at setup
     int k1_sm_cap = 0;
     // variants on the same boundary
     int gram_solver = SSCG_GRAM_FGS;
@@ -211,6 +213,36 @@ __global__ void k_csr_dinv(Geo g, double *dinv)
     dinv[g.plane + r] = 1.0 / d;
 }
 
+Knobs sscg::read_knobs()
+{
+    Knobs k;
+    auto tri = [](const char *name, int dflt) {
+        const char *e = getenv(name);
+        return e ? (e[0] == '1' ? 1 : e[0] == '0' ? 0 : dflt) : dflt;
+    };
+    auto num = [](const char *name, int dflt) {
+        const char *e = getenv(name);
+        return e ? atoi(e) : dflt;
+    };
+    k.k1_fuse = tri("SSCG_K1_FUSE", -1);
+    k.k1_mp3 = tri("SSCG_K1_MP3", -1);
+    k.k1_fuse_vc = tri("SSCG_K1_FUSE_VC", -1);
+    k.k1_tma = tri("SSCG_K1_TMA", 1) != 0;
+    k.k1_zc = std::max(0, num("SSCG_K1_ZC", 0));
+    k.faces_tma = tri("SSCG_FACES_TMA", 1) != 0;
+    k.k2_dmma = tri("SSCG_K2_DMMA", -1);
+    k.k2s = tri("SSCG_K2S", 1) != 0;
+    k.k2_e = num("SSCG_K2_E", 0);
+    k.k2_ns = num("SSCG_K2_NS", 0);
+    k.k2_grid = num("SSCG_K2_GRID", 0);
+    k.k2_groups = std::max(0, num("SSCG_K2_GROUPS", 0));
+    k.k2_smem_kb = std::min(224, std::max(64, num("SSCG_K2_SMEM_KB", 216)));
+    k.wfree = tri("SSCG_WFREE", 1) != 0;
+    k.k5_recur = tri("SSCG_K5_RECUR", 1) != 0;
+    k.debug = getenv("SSCG_DEBUG") != nullptr;
+    return k;
+}
+
 static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, double lmin, double lmax, int s,
                               int nu, const sscg_comm *cm, void *stream, sscg_ctx *c)
 {
@@ -240,6 +272,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         return fail(SSCG_ERR_INVALID, "bad comm (rank %d of %d, %d slabs per rank)", c->rank, c->nranks, c->spr);
 
     Geo &g = c->g;
+    g.kn = read_knobs();
     g.kind = A->kind;
     if (A->kind == SSCG_OP_CSR) {
         if (c->nranks * c->spr != 1) return fail(SSCG_ERR_INVALID, "CSR operator supports a single slab only");
@@ -282,6 +315,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
     }
     if (const char *e = getenv("SSCG_NO_GRAPH")) c->use_graph = (e[0] == '0');
     if (const char *e = getenv("SSCG_NO_OVERLAP")) c->overlap = (e[0] == '0');
+    if (const char *e = getenv("SSCG_NCCL_TIMEOUT_S")) c->nccl_timeout_s = atof(e);
     {
         int lo = 0, hi = 0;
         CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -340,8 +374,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
             sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
             sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;
             sl.kz = A->kz + sl.zoff * g.ny * g.nx;
-            const char *e = getenv("SSCG_FACES_TMA");
-            sl.has_ftma = !(e && e[0] == '0') &&
+            sl.has_ftma = g.kn.faces_tma &&
                           k1t_prepare_faces(g, sl.kx, sl.ky, sl.kz, sl.nzl, &sl.tmKX, &sl.tmKY, &sl.tmKZ);
             if (!diag_M && k1fv_enabled(g, sl.nzl) &&
                 k1fv_prepare_faces(g, sl.kx, sl.ky, sl.kz, sl.nzl, &sl.tmV_KX, &sl.tmV_KY, &sl.tmV_KZ, &sl.kx_shift)) {
@@ -545,6 +578,14 @@ static sscg_status prof_resolve(sscg_ctx *c)
     return SSCG_OK;
 }
 
+static void drop_graph(sscg_ctx *c)
+{
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+}
+
 // Wait for `strm`.  With ranks, poll instead of blocking so that an NCCL
 // failure (ncclCommGetAsyncError) or a peer that never arrives (timeout
 // SSCG_NCCL_TIMEOUT_S, default 600 s) aborts the communicator and returns
@@ -555,11 +596,7 @@ static sscg_status wait_stream(sscg_ctx *c, cudaStream_t strm)
         CU(cudaStreamSynchronize(strm));
         return SSCG_OK;
     }
-    static double limit = -1.0;
-    if (limit < 0.0) {
-        const char *e = getenv("SSCG_NCCL_TIMEOUT_S");
-        limit = e ? atof(e) : 600.0;
-    }
+    const double limit = c->nccl_timeout_s;
     const auto t0 = std::chrono::steady_clock::now();
     for (;;) {
         const cudaError_t q = cudaStreamQuery(strm);
@@ -569,8 +606,12 @@ static sscg_status wait_stream(sscg_ctx *c, cudaStream_t strm)
         ncclCommGetAsyncError(c->comm, &ae);
         const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (ae != ncclSuccess || (limit > 0.0 && dt > limit)) {
+            // the captured outer iteration holds NCCL nodes of this communicator:
+            // drop it with the communicator, and refuse every later call
+            drop_graph(c);
             ncclCommAbort(c->comm);
             c->comm = nullptr;
+            c->failed = true;
             return fail(SSCG_ERR_NCCL, "NCCL %s after %.1f s (communicator aborted)",
                         ae != ncclSuccess ? ncclGetErrorString(ae) : "timeout", dt);
         }
@@ -609,9 +650,8 @@ static sscg_status halo_join(sscg_ctx *c)
 // (SSCG_K5_RECUR=0 keeps the stored-W form everywhere)
 static bool uses_rec_update(const sscg_ctx *c)
 {
-    const char *e = getenv("SSCG_K5_RECUR");
-    if (e && e[0] == '0') return false;
     const Geo &g = c->g;
+    if (!g.kn.k5_recur) return false;
     if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2 || g.kind == SSCG_OP_CSR || g.pitch != g.nx) return false;
     for (const auto &sl : c->slabs)
         if (!sl.dvec && !(g.center > 0.0 && !sl.dinv)) return false;   // need m or diag(M) per point
@@ -623,8 +663,7 @@ static bool uses_rec_update(const sscg_ctx *c)
 // and the basis is Chebyshev (SSCG_WFREE=0 keeps the stored-W schedule)
 static bool uses_wfree(const sscg_ctx *c)
 {
-    const char *e = getenv("SSCG_WFREE");
-    if (e && e[0] == '0') return false;
+    if (!c->g.kn.wfree) return false;
     if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2) return false;
     for (const auto &sl : c->slabs)
         if (!sl.has_k2r || !sl.has_k1t) return false;
@@ -969,9 +1008,24 @@ static sscg_status run_outer(sscg_ctx *c, double *x)
     return SSCG_OK;
 }
 
+// free a device buffer allocated by dalloc (and forget it)
+static void dfree(sscg_ctx *c, void *p)
+{
+    if (!p) return;
+    for (auto &q : c->allocs)
+        if (q == p) {
+            cudaFree(q);
+            q = c->allocs.back();
+            c->allocs.pop_back();
+            return;
+        }
+}
+
 static sscg_status ensure_history(sscg_ctx *c, int cap)
 {
     if (cap <= c->hist_cap) return SSCG_OK;
+    cap = std::max(cap, std::min(2 * c->hist_cap, 1 << 20));   // grow geometrically
+    CU(cudaStreamSynchronize(c->stream));                       // old buffers may still be written
     if (c->gexec) {   // the captured K4 holds the old history pointers
         cudaGraphExecDestroy(c->gexec);
         c->gexec = nullptr;
@@ -981,12 +1035,14 @@ static sscg_status ensure_history(sscg_ctx *c, int cap)
     // first GRAM_HIST outer iterations only: s = 64 would need 33 GB for 2^20
     const int gcap = std::min(cap, GRAM_HIST);
     if (gcap > c->gram_cap) {
+        for (double *q : {c->h_gram, c->h_d, c->h_at, c->h_al}) dfree(c, q);
         TRY(dalloc(c, &c->h_gram, (size_t)gcap * nent));
         TRY(dalloc(c, &c->h_d, (size_t)gcap * s));
         TRY(dalloc(c, &c->h_at, (size_t)gcap * s));
         TRY(dalloc(c, &c->h_al, (size_t)gcap * s));
         c->gram_cap = gcap;
     }
+    for (double *q : {c->h_delta, c->h_lnorm, c->h_kappa, c->h_pnorm, c->h_budget, c->h_relres}) dfree(c, q);
     TRY(dalloc(c, &c->h_delta, (size_t)cap));
     TRY(dalloc(c, &c->h_lnorm, (size_t)cap));
     TRY(dalloc(c, &c->h_kappa, (size_t)cap));
@@ -1004,6 +1060,7 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
                                   uint32_t flags)
 {
     if (!c || !b || !x) return fail(SSCG_ERR_INVALID, "null argument");
+    if (c->failed) return fail(SSCG_ERR_NCCL, "context unusable after an NCCL abort; destroy it");
     if (max_outer < 0 || !(rtol >= 0.0)) return fail(SSCG_ERR_INVALID, "bad rtol/max_outer");
     if (!c->bounds_set && c->basis == SSCG_BASIS_CHEBYSHEV)
         return fail(SSCG_ERR_INVALID, "spectral bounds not set (sscg_set_bounds / sscg_estimate_bounds)");
@@ -1131,12 +1188,18 @@ extern "C" sscg_status sscg_solve_host(sscg_ctx *c, const double *b_host, double
                                        int32_t max_outer, uint32_t flags)
 {
     if (!c || !b_host || !x_host) return fail(SSCG_ERR_INVALID, "null argument");
+    if (c->failed) return fail(SSCG_ERR_NCCL, "context unusable after an NCCL abort; destroy it");
     const size_t bytes = (size_t)c->n_local * sizeof(double);
     if (!c->bbuf) TRY(dalloc(c, &c->bbuf, (size_t)c->n_local));
     if (!c->xbuf) TRY(dalloc(c, &c->xbuf, (size_t)c->n_local));
     CU(cudaMemcpyAsync(c->bbuf, b_host, bytes, cudaMemcpyHostToDevice, c->stream));
     if (!(flags & SSCG_SOLVE_X0_ZERO)) CU(cudaMemcpyAsync(c->xbuf, x_host, bytes, cudaMemcpyHostToDevice, c->stream));
-    c->x_host_out = x_host;
+    // the early copy of x (overlapping the last stopping-test iteration) needs
+    // page-locked memory; a pageable x_host is copied after the solve instead
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, x_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    c->x_host_out = pinned ? x_host : nullptr;
     c->x_copied = false;
     sscg_status st = sscg_solve(c, c->bbuf, c->xbuf, rtol, max_outer, flags);
     c->x_host_out = nullptr;
@@ -1218,6 +1281,7 @@ extern "C" sscg_status sscg_inspect(const sscg_ctx *cc, int32_t what, int32_t in
 extern "C" sscg_status sscg_iterate(sscg_ctx *c, double *x, int32_t nsteps)
 {
     if (!c || !x || nsteps < 0) return fail(SSCG_ERR_INVALID, "bad argument");
+    if (c->failed) return fail(SSCG_ERR_NCCL, "context unusable after an NCCL abort; destroy it");
     if (!c->solved) return fail(SSCG_ERR_INVALID, "sscg_iterate needs a preceding sscg_solve");
     if (c->st_host->breakdown || c->st_host->nonfinite) return fail(SSCG_ERR_INVALID, "last solve broke down");
     c->launches = 0;
@@ -1268,14 +1332,6 @@ extern "C" sscg_status sscg_profile(sscg_ctx *c, sscg_profile_t *out)
     TRY(prof_resolve(c));
     *out = c->prof;
     return SSCG_OK;
-}
-
-static void drop_graph(sscg_ctx *c)
-{
-    if (c->gexec) {
-        cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
-    }
 }
 
 extern "C" sscg_status sscg_set_bounds(sscg_ctx *c, double lambda_min, double lambda_max)
@@ -1343,6 +1399,7 @@ extern "C" sscg_status sscg_estimate_bounds(sscg_ctx *c, const double *v0, int32
                                             double *lmin, double *lmax, double *alpha_out, double *beta_out)
 {
     if (!c || !v0 || !lmin || !lmax) return fail(SSCG_ERR_INVALID, "null argument");
+    if (c->failed) return fail(SSCG_ERR_NCCL, "context unusable after an NCCL abort; destroy it");
     if (iters < 1 || iters > 100000 || !(margin >= 0.0) || !(margin < 1.0))
         return fail(SSCG_ERR_INVALID, "bad iters (%d) or margin (%g)", iters, margin);
     const Geo &g = c->g;

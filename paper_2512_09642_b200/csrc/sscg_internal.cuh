@@ -60,7 +60,28 @@ struct Slab {
     bool has_k1f;
 };
 
+// Schedule and tuning switches (DESIGN.md §1 table), read from the
+// environment once per context by sscg_setup (read_knobs) and carried in Geo,
+// so a context keeps the switches it was created with and two contexts of
+// one process may differ (the parity tests force both sides of a choice).
+struct Knobs {
+    int k1_fuse = -1;      // SSCG_K1_FUSE      -1 auto, 0 forbid, 1 force (K1F pairs)
+    int k1_mp3 = -1;       // SSCG_K1_MP3       same for K1M triples
+    int k1_fuse_vc = -1;   // SSCG_K1_FUSE_VC   same for K1FV
+    int k1_tma = 1;        // SSCG_K1_TMA       0: direct-load K1
+    int k1_zc = 0;         // SSCG_K1_ZC        z-chunk length (0 auto)
+    int faces_tma = 1;     // SSCG_FACES_TMA    0: direct face loads
+    int k2_dmma = -1;      // SSCG_K2_DMMA      stored-W Gram on tensor cores (-1: s > 16)
+    int k2s = 1;           // SSCG_K2S          0: tensor-core K2R also for s <= 8
+    int k2_e = 0, k2_ns = 0, k2_grid = 0, k2_groups = 0, k2_smem_kb = 216;   // Gram-pass sweeps
+    int wfree = 1;         // SSCG_WFREE        0: stored-W schedule
+    int k5_recur = 1;      // SSCG_K5_RECUR     0: update with the stored W
+    int debug = 0;         // SSCG_DEBUG
+};
+Knobs read_knobs();
+
 struct Geo {
+    Knobs kn;
     int kind;          // sscg_op_kind
     int nx, ny;        // grid in x, y
     int pitch;         // row pitch (doubles)
@@ -151,7 +172,7 @@ int k2_grid();
 bool k2_prepare(const Geo &g, Slab &sl, int s);   // encode the TMA tensor maps
 int k2_num_entries(int s);
 // K2D: the Gram pass on FP64 tensor cores (k_gram_dmma.cu), s > 16 by default
-bool k2d_enabled(int s);
+bool k2d_enabled(const Geo &g, int s);
 // K2R: DMMA Gram pass recovering W = AP from the basis recurrence (W not stored, R23)
 bool k2r_prepare(const Geo &g, Slab &sl, int s);
 void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma, const DevState *st, double *out_blk,

@@ -126,6 +126,61 @@ def test_gram_closed_form_full_size():
     assert np.max(np.abs(c - ccf)) <= TOL_GRAM * np.max(np.abs(ccf))
 
 
+def _mem_available_gb():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) / 2 ** 20
+    except OSError:
+        pass
+    return 0.0
+
+
+def test_oracle_full_gram_alpha_x10_full_size(cfg5, monkeypatch):
+    """The whole oracle at BASELINE cfg 5's full size (448^3, s = 16, nu = 30,
+    seeded b, x_0 = 0), under the bench's default schedule (K1M triples, the
+    W-free Gram K2R, K4, K5 with the recurrence update): the full 16x16 Gram
+    block and c of outer 0 (1e-11 of max|Ghat|), alpha~ / alpha of outer 0
+    (1e-10), and x after 10 outer iterations (1e-8, north_star).  The oracle
+    needs ~25 GB of host memory here; with less than 40 GB available the same
+    check runs at 384^3 with the triples forced on (R15)."""
+    import torch
+
+    import paper_2512_09642_b200 as sscg
+    from gpu_cases import TOL_ALPHA, TOL_X10
+    if _mem_available_gb() >= 40.0:
+        n, S, b, bt = N, cfg5["S"], cfg5["b"], cfg5["bt"]
+        lmin, lmax = cfg5["lmin"], cfg5["lmax"]
+        own = None
+    else:
+        n = 384
+        monkeypatch.setenv("SSCG_K1_MP3", "1")
+        lmin, lmax = inputs.analytic_bounds("7pt", n, n, n)
+        b = inputs.rhs_uniform(n, n, n, seed=42)
+        bt = torch.from_numpy(b).cuda()
+        own = S = sscg.Solver(sscg.Stencil("7pt", n, n, n), lmin, lmax, S_, NU)
+    try:
+        assert S.query(sscg.QUERY_BASIS_FUSED) == 3          # the bench's triples
+        x = S.solve(bt, rtol=0.0, max_outer=10).cpu().numpy()
+        G0, c0 = S.gram(0)
+        at0 = S.inspect(sscg.INSPECT_ALPHA_T, 0)
+        al0 = S.inspect(sscg.INSPECT_ALPHA, 0)
+    finally:
+        if own is not None:
+            own.close()
+    del bt
+    A = orc.stencil(orc.KIND_7PT, n, n, n)
+    x_or, tr = orc.sstep_cg(A, lmin, lmax, S_, NU, b, rtol=0.0, max_outer=10)
+    scale = np.max(np.abs(tr.ghat[0]))
+    assert np.max(np.abs(G0 - tr.ghat[0])) <= TOL_GRAM * scale, np.max(np.abs(G0 - tr.ghat[0])) / scale
+    assert np.max(np.abs(c0 - tr.c[0])) <= TOL_GRAM * np.max(np.abs(tr.c[0]))
+    assert np.max(np.abs(at0 - tr.alpha_t[0])) <= TOL_ALPHA * np.max(np.abs(tr.alpha_t[0]))
+    assert np.max(np.abs(al0 - tr.alpha[0])) <= TOL_ALPHA * np.max(np.abs(tr.alpha[0]))
+    ex = np.linalg.norm(x - x_or) / np.linalg.norm(x_or)
+    assert ex <= TOL_X10, ex
+
+
 def _apply7(x):
     """Independent numpy 7-point Dirichlet Laplacian (test-side property check)."""
     u = x.reshape(N, N, N)

@@ -54,6 +54,35 @@ def test_exact_in_one_outer_with_s_modes():
     assert np.linalg.norm(x - xstar) <= 1e-8 * np.linalg.norm(xstar)
 
 
+@pytest.mark.parametrize("nu", [1, 2, 3, 5])
+def test_worked_example_delta(golden, nu):
+    """delta_k = ||c~ - G a~|| / ||c~|| on the worked example,
+    by hand: G = [[1, 1/2], [1/2, 1]], c~ = [1, 0] at every outer iteration
+    (r_k is a multiple of [1, 1]); each FGS sweep maps the error of a~ to a
+    quarter of itself and leaves the residual c~ - G a~ = [4^-nu, 0], so
+    delta_k = 4^-nu exactly (pins the normalisation and the square root)."""
+    g = golden["restart_sstep_diag13"]
+    A = diag_csr(g["A_diag"])
+    b = np.array(g["b"])
+    x, tr = orc.sstep_cg(A, 1.0, 3.0, 2, nu, b, rtol=0.0, max_outer=3, D=np.ones(2))
+    for k in range(3):
+        assert tr.delta[k] == pytest.approx(4.0 ** (-nu), rel=1e-13), (k, tr.delta[k])
+    # and a non-trivial case: delta equals the definition evaluated by numpy on
+    # the oracle's own G, c~, a~ of a 2D Laplacian outer iteration
+    A2 = orc.stencil(orc.KIND_5PT2D, 12, 11, 1)
+    b2 = inputs.rhs_uniform(12, 11, 1, seed=5)
+    lmin, lmax = inputs.analytic_bounds("5pt", 12, 11)
+    _, t2 = orc.sstep_cg(A2, lmin, lmax, 5, nu, b2, rtol=0.0, max_outer=2, dump_iter=1)
+    for k in range(2):
+        d = 1.0 / np.sqrt(np.diag(t2.ghat[k]))
+        G = d[:, None] * t2.ghat[k] * d[None, :]
+        np.fill_diagonal(G, 1.0)
+        ct = d * t2.c[k]
+        res = ct - G @ t2.alpha_t[k]
+        assert t2.delta[k] == pytest.approx(np.linalg.norm(res) / np.linalg.norm(ct), rel=1e-10)
+        assert t2.delta[k] > 0.0
+
+
 @pytest.mark.parametrize("nu", [1, 3, 20])
 def test_energy_identity(nu):
     """||e_k||_A^2 - ||e_{k+1}||_A^2 = 2 a~^T c~ - a~^T G a~ > 0 (each unit-
@@ -207,3 +236,22 @@ def test_cfg2_count_sensitivity():
     k = min(t0.outer, t1.outer)
     assert abs(t0.relres[10] - t1.relres[10]) <= 1e-10 * t0.relres[10]
     assert np.max(np.abs(t0.relres[k - 10:k] - t1.relres[k - 10:k]) / t0.relres[k - 10:k]) > 1e-3
+
+
+def test_restart_from_recurrence_residual_is_outer_k():
+    """b := r_k (the oracle's recurrence residual after k outer iterations),
+    x_0 = 0 makes outer 0 of the restart bitwise identical to outer k of the
+    original solve (basis, Gram block, alpha): the GPU deep-parity tests
+    (tests/test_gpu_deep_parity.py) rely on this to give both sides
+    identical inputs at any depth."""
+    A = orc.stencil(orc.KIND_7PT, 13, 11, 9)
+    b = inputs.rhs_uniform(13, 11, 9, seed=42)
+    lmin, lmax = inputs.analytic_bounds("7pt", 13, 11, 9)
+    s, nu, k = 6, 10, 7
+    _, trk = orc.sstep_cg(A, lmin, lmax, s, nu, b, rtol=0.0, max_outer=k + 1, dump_iter=k)
+    rk = trk.P[0].copy()
+    _, tr1 = orc.sstep_cg(A, lmin, lmax, s, nu, rk, rtol=0.0, max_outer=1, dump_iter=0)
+    assert np.array_equal(tr1.P, trk.P) and np.array_equal(tr1.W, trk.W)
+    assert np.array_equal(tr1.ghat[0], trk.ghat[k]) and np.array_equal(tr1.c[0], trk.c[k])
+    assert np.array_equal(tr1.alpha_t[0], trk.alpha_t[k]) and np.array_equal(tr1.alpha[0], trk.alpha[k])
+    assert tr1.delta[0] == trk.delta[k]
