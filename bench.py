@@ -34,6 +34,9 @@ K1_NAME = "k1t"   # dominant kernel (basis step) as named in the ncu capture
 # configuration the headline metric is quoted on; the others are parity-test
 # cases that bench.py can also time (--workload) for the per-kernel rooflines.
 WORKLOADS = {
+    "cfg1": {"kind": "5pt", "n": 64, "s": 8, "nu": 20, "bounds": "analytic",
+             "desc": "cfg1: 2D 5-point Poisson {n}x{n} (n=4096), FP64, Jacobi, analytic bounds; latency: "
+                     "microseconds per outer iteration under CUDA-graph replay (SURVEY 8(d))"},
     "cfg2": {"kind": "7pt", "n": 128, "s": 16, "nu": 25, "bounds": "analytic",
              "desc": "cfg2: 3D 7-point Poisson {n}^3 per GPU, FP64, Jacobi, analytic bounds"},
     "cfg3": {"kind": "27pt", "n": 256, "s": 16, "nu": 30, "bounds": "lanczos",
@@ -75,6 +78,12 @@ def parse():
 
 def workload(a, nranks):
     n = a.n
+    if a.kind == "5pt":   # 2D: one n x n grid per GPU (cfg 1 stays on one GPU; N > 1 runs replicas)
+        return {"workload": WORKLOADS[a.workload]["desc"].format(n=n) + f", s={a.s}, nu={a.nu}, x0=0, "
+                "b~U[-1,1] seed 42", "nx": n, "ny": n, "nz_per_gpu": 1, "nz_global": 1, "s": a.s, "nu": a.nu,
+                "n_global": n * n * nranks, "parallelism": f"replicas x{nranks}" if nranks > 1 else "single GPU",
+                "l2": "working set (%.2f MB) resident in the 126 MB L2: a latency measurement, no roofline claim"
+                      % ((2 * a.s + 2) * n * n * 8 / 1e6)}
     nzg = n if a.strong else n * nranks
     desc = WORKLOADS[a.workload]["desc"].format(n=n)
     if a.strong:
@@ -96,8 +105,13 @@ def oracle_sample(a, steps, warmup, planes=None):
     import inputs
     import oracle as orc
     n, zs = a.n, min(planes or a.cpu_planes, a.n)
+    if a.kind == "5pt":
+        zs = 1
     b = inputs.rhs_uniform(n, n, zs, seed=42)
-    if a.kind == "varcoef7":
+    if a.kind == "5pt":
+        A = orc.stencil(orc.KIND_5PT2D, n, n, 1)
+        lmin, lmax = inputs.analytic_bounds("5pt", n, n)
+    elif a.kind == "varcoef7":
         A = orc.stencil(orc.KIND_VARCOEF7, n, n, zs, *inputs.lognormal_faces(n, n, zs, seed=42))
         lmin, lmax, _ = orc.lanczos_bounds(A, 50, b, 0.05)     # untimed setup
     else:
@@ -116,6 +130,35 @@ def oracle_sample(a, steps, warmup, planes=None):
             f"({npts} unknowns), {steps} outer iterations timed as t(max_outer={warmup + steps}) - "
             f"t(max_outer={warmup})")
     return npts / per / 1e9, per, desc
+
+
+def host_info():
+    """MemTotal / MemAvailable and a host copy-bandwidth probe (numpy copy of
+    a 1 GiB array, best of 3; read + write bytes) -- SURVEY 8(d) asks for both
+    beside the oracle baseline."""
+    import numpy as np
+    info = {}
+    try:
+        for line in open("/proc/meminfo"):
+            k, v = line.split(":", 1)
+            if k in ("MemTotal", "MemAvailable"):
+                info[k + "_GB"] = round(int(v.split()[0]) / 2 ** 20, 1)
+    except OSError:
+        pass
+    try:
+        src = np.ones(1 << 27)   # 1 GiB
+        dst = np.empty_like(src)
+        best = None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            np.copyto(dst, src)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        info["host_copy_gbs"] = round(2 * src.nbytes / best / 1e9, 2)
+        info["host_copy_note"] = "numpy copy of 1 GiB, one thread, best of 3 (read + write bytes)"
+    except MemoryError:
+        pass
+    return info
 
 
 def cpu_cores():
@@ -142,6 +185,8 @@ def run_reference(a):
         return
     value, per, desc = oracle_sample(a, a.steps, a.warmup)
     cfg = workload(a, a.gpus)
+    if a.kind == "5pt":
+        cfg["us_per_outer"] = per * 1e6
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference", "config": cfg,
@@ -303,12 +348,13 @@ def run_ours(a):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, s, nu = a.n, a.s, a.nu
-    nz = n if a.strong else n * world
-    z0, nzl = sscg.partition(nz, world, 1, rank)
+    twod = a.kind == "5pt"          # cfg 1: one 2D grid per GPU (replicas for N > 1)
+    nz = 1 if twod else (n if a.strong else n * world)
+    z0, nzl = (0, 1) if twod else sscg.partition(nz, world, 1, rank)
     b_host = torch.from_numpy(inputs.rhs_uniform(n, n, nz, seed=42, z0=z0, nzl=nzl)).pin_memory()
     b = b_host.cuda()
     nid = None
-    if world > 1:
+    if world > 1 and not twod:
         obj = [sscg.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
@@ -321,12 +367,14 @@ def run_ours(a):
         op = sscg.Stencil("varcoef7", n, n, nz, *faces)
     else:
         op = sscg.Stencil(a.kind, n, n, nz)
-    if WORKLOADS[a.workload]["bounds"] == "analytic":
+    if twod:
+        S = sscg.Solver(op, *inputs.analytic_bounds(a.kind, n, n), s, nu)
+    elif WORKLOADS[a.workload]["bounds"] == "analytic":
         S = sscg.Solver(op, *inputs.analytic_bounds(a.kind, n, n, nz), s, nu, rank=rank, nranks=world, nccl_id=nid)
     else:   # 50 Lanczos steps on the GPU, widened 5 % (R13), untimed setup
         S = sscg.Solver(op, 0.0, 0.0, s, nu, rank=rank, nranks=world, nccl_id=nid)
         S.set_bounds(*S.estimate_bounds(b, 50, 0.05))
-    n_local, n_global = S.n_local, n * n * nz
+    n_local, n_global = S.n_local, n * n * nz * (world if twod else 1)
 
     def barrier():
         torch.cuda.synchronize()
@@ -412,6 +460,28 @@ def run_ours(a):
             "path_bytes_per_step": path_bytes,
             "path_achieved_gbs": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9,
             "path_frac": path_bytes / (st.ms_total / a.steps / 1e3) / 1e9 / peak}
+    # SURVEY 8(d)'s byte contract as written (single steps with stored W: 4 vectors per basis step,
+    # 3 at j = 0 and 2 at j = s-1; Gram 2s; update 2s+3; 8s per outer, + s face sets for varcoef7)
+    # beside the schedule's own bytes above: the schedule moves fewer vectors
+    # (W-free Gram, recurrence update, K1M triples), so against 8(d) a fraction above 1 is expected
+    t_outer = st.ms_total / a.steps / 1e3
+    c8_basis = (4 * s - 3) * vec + s * face_bytes
+    c8 = {"basis": c8_basis, "gram": 2 * s * vec, "update": (2 * s + 3) * vec}
+    roof["contracts"] = {
+        "schedule": {"vectors_per_outer": {"basis": basis_vecs, "gram": gram_vecs, "update": upd_vecs},
+                     "bytes_per_outer": path_bytes, "achieved_gbs": path_bytes / t_outer / 1e9,
+                     "frac": path_bytes / t_outer / 1e9 / peak,
+                     "dominant_kernel_frac": k1["frac"]},
+        "survey_8d": {"vectors_per_outer": {"basis": 4 * s - 3, "gram": 2 * s, "update": 2 * s + 3},
+                      "bytes_per_outer": sum(c8.values()), "achieved_gbs": sum(c8.values()) / t_outer / 1e9,
+                      "frac": sum(c8.values()) / t_outer / 1e9 / peak,
+                      "dominant_kernel_frac": (c8_basis * a.steps / max(k1["launches"], 1)) /
+                                              (k1["ms_per_launch"] / 1e3) / 1e9 / peak if k1["ms_per_launch"] else None,
+                      "note": "SURVEY 8(d) counts as written (stored W, single basis steps); the kernels move the "
+                              "schedule's vectors, so this 'fraction' is not a physical bandwidth (> 1 possible)"}}
+    if a.kind == "5pt":
+        roof["us_per_outer"] = 1e3 * st.ms_total / a.steps
+        roof["note"] = "cfg 1: the working set lives in L2; the metric is latency per outer iteration (SURVEY 8(d))"
     # end-to-end: host b in, host x out, through the C ABI (sscg_solve_host)
     e2e = None
     if not a.no_e2e:
@@ -436,9 +506,19 @@ def run_ours(a):
         return
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
-        # ~10 s of CPU work: 64 planes of the same n x n grid, 24 timed outer iterations
-        v, per, desc = oracle_sample(a, 24, 1, planes=64)
-        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc, "cpu": cpu_model()}
+        hi = host_info()
+        # the oracle at the full one-GPU size, 3 outer iterations,
+        # when the host has the memory (the oracle holds P and W: 2s+4 vectors);
+        # else ~10 s of CPU work on 64 planes of the same n x n grid
+        need_gb = (2 * s + 6) * 8.0 * n * n * (1 if a.kind == "5pt" else n) / 1e9
+        if a.kind == "5pt":
+            v, per, desc = oracle_sample(a, 200, 5)
+        elif hi.get("MemAvailable_GB", 0.0) >= 1.6 * need_gb and not a.strong:
+            v, per, desc = oracle_sample(a, 3, 0, planes=n)
+        else:
+            v, per, desc = oracle_sample(a, 24, 1, planes=64)
+        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": desc, "cpu": cpu_model(),
+               "ms_per_outer": per * 1e3, "host": hi}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg, "roofline": roof,

@@ -27,7 +27,7 @@ __device__ __forceinline__ double warp_sum(double v)
 template <bool TWO>
 __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
 {
-    if (st->done) return;
+    PDL_ENTRY(st);
     __shared__ double Gc[TWO ? SMAX * SMAX : 1];   // column-major: Gc[j*s + i] = G_ij
     __shared__ double Bs[TWO ? 1 : 32 * 32 + 32];  // s <= 32: the block staged once (coalesced)
     __shared__ double dsh[SMAX];
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
 // breakdown (R19).
 __global__ void __launch_bounds__(32) k4_chol(K4Args a, DevState *st)
 {
-    if (st->done) return;
+    PDL_ENTRY(st);
     // R overwrites the upper triangle of G in place (row k of R is written
     // after row k of G was last read)
     __shared__ double R[SMAX * SMAX], dsh[SMAX], ct[SMAX], y[SMAX], al[SMAX];
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(32) k4_chol(K4Args a, DevState *st)
 // spread over the lanes).  Off the hot path: launched only when enabled.
 __global__ void __launch_bounds__(32) k_kappa(const double *blk, int s, const DevState *st, double *h_kappa)
 {
-    if (st->done) return;
+    PDL_ENTRY(st);
     const int k = st->k - 1;
     if (k < 0 || k >= st->hist_cap) return;
     __shared__ double A[SMAX * SMAX], d[SMAX];
@@ -411,7 +411,7 @@ struct K5Params {
 template <int S, bool REC>
 __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState *st)
 {
-    if (st->done) return;
+    PDL_ENTRY(st);
     __shared__ double al[SMAX], ga[SMAX];
     for (int j = threadIdx.x; j < k.s; j += blockDim.x) al[j] = k.alpha[j];
     __syncthreads();
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState 
 // generic path (odd nx / unaligned x): scalar, skips the pad column.
 __global__ void __launch_bounds__(256) k5_update_gen(K5Params k, const DevState *st)
 {
-    if (st->done) return;
+    PDL_ENTRY(st);
     __shared__ double al[SMAX];
     for (int j = threadIdx.x; j < k.s; j += blockDim.x) al[j] = k.alpha[j];
     __syncthreads();
@@ -503,9 +503,9 @@ __global__ void __launch_bounds__(256) k5_update_gen(K5Params k, const DevState 
 
 void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
 {
-    if (a.solver == 1) k4_chol<<<1, 32, 0, s>>>(a, st);
-    else if (a.s <= 32) k4_fgs<false><<<1, 32, 0, s>>>(a, st);
-    else k4_fgs<true><<<1, 32, 0, s>>>(a, st);
+    if (a.solver == 1) launch_pdl(a.pdl, k4_chol, dim3(1), dim3(32), 0, s, a, st);
+    else if (a.s <= 32) launch_pdl(a.pdl, k4_fgs<false>, dim3(1), dim3(32), 0, s, a, st);
+    else launch_pdl(a.pdl, k4_fgs<true>, dim3(1), dim3(32), 0, s, a, st);
 }
 
 // Diagnostics: ||P_k||_F^2 of the basis of this outer iteration (before K5
@@ -516,7 +516,7 @@ void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
 __global__ void __launch_bounds__(256) k_pnorm(const double *P, int64_t vstride, int64_t N, int s, double *part,
                                                const DevState *st)
 {
-    if (st->done) return;
+    PDL_ENTRY(st);
     __shared__ double red[8];
     double acc = 0.0;
     for (int j = 0; j < s; ++j)
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(256) k_pnorm(const double *P, int64_t vstride,
 
 __global__ void k_psum(const double *part, int n, double *sum, const DevState *st)
 {
-    if (st->done) return;
+    PDL_ENTRY(st);
     double v = 0.0;
     for (int b = threadIdx.x; b < n; b += 32) v += part[b];
     v = warp_sum(v);
@@ -546,7 +546,7 @@ __global__ void k_psum(const double *part, int n, double *sum, const DevState *s
 __global__ void k_budget(const double *sum, double anorm, const DevState *st, const double *h_delta, double *h_pnorm,
                          double *h_budget)
 {
-    if (st->done) return;
+    PDL_ENTRY(st);
     const int k = st->k - 1;
     if (k < 0 || k >= st->hist_cap) return;
     const double pf = sqrt(*sum);
@@ -643,24 +643,24 @@ void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double 
     if (blocks > cap) blocks = cap;
     if (vec && k.rec) {
         switch (s) {
-        case 4: k5_update_vec<4, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 8: k5_update_vec<8, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 16: k5_update_vec<16, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 24: k5_update_vec<24, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 32: k5_update_vec<32, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        default: k5_update_vec<0, true><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 4: launch_pdl(g.kn.pdl, k5_update_vec<4, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 8: launch_pdl(g.kn.pdl, k5_update_vec<8, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 16: launch_pdl(g.kn.pdl, k5_update_vec<16, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 24: launch_pdl(g.kn.pdl, k5_update_vec<24, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 32: launch_pdl(g.kn.pdl, k5_update_vec<32, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        default: launch_pdl(g.kn.pdl, k5_update_vec<0, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
         }
     } else if (vec) {
         switch (s) {
-        case 4: k5_update_vec<4, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 8: k5_update_vec<8, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 16: k5_update_vec<16, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 24: k5_update_vec<24, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        case 32: k5_update_vec<32, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
-        default: k5_update_vec<0, false><<<(unsigned)blocks, 256, 0, stream>>>(k, st); break;
+        case 4: launch_pdl(g.kn.pdl, k5_update_vec<4, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 8: launch_pdl(g.kn.pdl, k5_update_vec<8, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 16: launch_pdl(g.kn.pdl, k5_update_vec<16, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 24: launch_pdl(g.kn.pdl, k5_update_vec<24, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 32: launch_pdl(g.kn.pdl, k5_update_vec<32, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        default: launch_pdl(g.kn.pdl, k5_update_vec<0, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
         }
     }
-    else k5_update_gen<<<(unsigned)blocks, 256, 0, stream>>>(k, st);
+    else launch_pdl(g.kn.pdl, k5_update_gen, dim3((unsigned)blocks), dim3(256), 0, stream, k, st);
 }
 
 }  // namespace sscg

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256, 1)
     k2_gram(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW, K2Params k,
             const DevState *st)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     extern __shared__ __align__(1024) double smem[];
     __shared__ uint64_t full[MAX_STAGE], empty[MAX_STAGE];
     __shared__ bool is_last;
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256, 1)
 // fixed-order sum of the per-slab blocks of one process
 __global__ void k_slab_sum(const double *const *blks, int nslab, int len, double *out, const DevState *st)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < len; q += gridDim.x * blockDim.x) {
         double v = 0.0;
         for (int b = 0; b < nslab; ++b) v += blks[b][q];
@@ -318,10 +318,10 @@ bool k2_prepare(const Geo &g, Slab &sl, int s)
 }
 
 template <int TB, int E>
-static void launch_t(const CUtensorMap &a, const CUtensorMap &b, const K2Params &k, const K2Plan &p, dim3 grid,
-                     const DevState *st, cudaStream_t stream)
+static void launch_t(bool pdl, const CUtensorMap &a, const CUtensorMap &b, const K2Params &k, const K2Plan &p,
+                     dim3 grid, const DevState *st, cudaStream_t stream)
 {
-    k2_gram<TB, E><<<grid, p.threads, p.smem, stream>>>(a, b, k, st);
+    launch_pdl(pdl, k2_gram<TB, E>, dim3(grid), dim3(p.threads), p.smem, stream, a, b, k, st);
 }
 
 // partial buffer must hold k2_grid() * (s*s+s) doubles (gx * gy <= k2_grid())
@@ -349,10 +349,10 @@ void launch_k2(const Geo &g, const Slab &sl, int s, const DevState *st, double *
     if (g.kn.k2_grid) gx = std::max(1, std::min(gx, g.kn.k2_grid));   // tuning
     if (nchunks < gx) gx = (int)nchunks;
     dim3 grid(gx, p.gy);
-    if (p.TB == 4) launch_t<4, 256>(sl.tmP, sl.tmW, k, p, grid, st, stream);
-    else if (p.E == 256) launch_t<8, 256>(sl.tmP, sl.tmW, k, p, grid, st, stream);
-    else if (p.E == 128) launch_t<8, 128>(sl.tmP, sl.tmW, k, p, grid, st, stream);
-    else launch_t<8, 64>(sl.tmP, sl.tmW, k, p, grid, st, stream);
+    if (p.TB == 4) launch_t<4, 256>(g.kn.pdl, sl.tmP, sl.tmW, k, p, grid, st, stream);
+    else if (p.E == 256) launch_t<8, 256>(g.kn.pdl, sl.tmP, sl.tmW, k, p, grid, st, stream);
+    else if (p.E == 128) launch_t<8, 128>(g.kn.pdl, sl.tmP, sl.tmW, k, p, grid, st, stream);
+    else launch_t<8, 64>(g.kn.pdl, sl.tmP, sl.tmW, k, p, grid, st, stream);
 }
 
 void launch_slab_sum(const double *const *blks_dev, int nslab, int len, double *blk, const DevState *st,

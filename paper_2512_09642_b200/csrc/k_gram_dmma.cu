@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(threads_for(NB), 1)
     k2d(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW, K2DParams k,
         const DevState *st)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     constexpr int SP = 8 * NB;                 // rows per box
     constexpr int NCW = ncw_for(NB), THREADS = threads_for(NB);
     constexpr int KS = EP / 4;                 // k-steps per stage
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     k2r(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmWl,
         const __grid_constant__ CUtensorMap tmDv, K2RParams k, const DevState *st)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     constexpr int SP = 8 * NB;
     constexpr int NCW = ncw_for(NB, VARM), THREADS = threads_for(NB, VARM);
     // NB <= 2: k-step pairs from 16-B loads (pitch EP = 136, 64 mod 128 B); larger
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(k2s_threads(S), 1)
     k2s(const double *__restrict__ P, const double *__restrict__ Wl, const double *__restrict__ Dv, int64_t vstride,
         K2RParams k, const DevState *st)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     constexpr int K2S_THREADS = k2s_threads(S);
     constexpr int NUP = S * (S + 1) / 2, NACC = NUP + S;
     __shared__ double red[K2S_THREADS / 32][NACC];
@@ -658,14 +658,14 @@ void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double 
     const size_t red = (size_t)(ncw_for(nb) * nt * 64 + ncw_for(nb) * s_pad) * sizeof(double);   // cross-warp reduction
     const size_t sm = std::max(ring, red);
     switch (nb) {
-    case 1: k2d<1, 132><<<gx, threads_for(1), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 2: k2d<2, 132><<<gx, threads_for(2), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 3: k2d<3, 132><<<gx, threads_for(3), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 4: k2d<4, 132><<<gx, threads_for(4), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 5: k2d<5, 68><<<gx, threads_for(5), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 6: k2d<6, 68><<<gx, threads_for(6), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    case 7: k2d<7, 68><<<gx, threads_for(7), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
-    default: k2d<8, 68><<<gx, threads_for(8), sm, stream>>>(sl.tmPd, sl.tmWd, k, st); break;
+    case 1: launch_pdl(g.kn.pdl, k2d<1, 132>, dim3(gx), dim3(threads_for(1)), sm, stream, sl.tmPd, sl.tmWd, k, st); break;
+    case 2: launch_pdl(g.kn.pdl, k2d<2, 132>, dim3(gx), dim3(threads_for(2)), sm, stream, sl.tmPd, sl.tmWd, k, st); break;
+    case 3: launch_pdl(g.kn.pdl, k2d<3, 132>, dim3(gx), dim3(threads_for(3)), sm, stream, sl.tmPd, sl.tmWd, k, st); break;
+    case 4: launch_pdl(g.kn.pdl, k2d<4, 132>, dim3(gx), dim3(threads_for(4)), sm, stream, sl.tmPd, sl.tmWd, k, st); break;
+    case 5: launch_pdl(g.kn.pdl, k2d<5, 68>, dim3(gx), dim3(threads_for(5)), sm, stream, sl.tmPd, sl.tmWd, k, st); break;
+    case 6: launch_pdl(g.kn.pdl, k2d<6, 68>, dim3(gx), dim3(threads_for(6)), sm, stream, sl.tmPd, sl.tmWd, k, st); break;
+    case 7: launch_pdl(g.kn.pdl, k2d<7, 68>, dim3(gx), dim3(threads_for(7)), sm, stream, sl.tmPd, sl.tmWd, k, st); break;
+    default: launch_pdl(g.kn.pdl, k2d<8, 68>, dim3(gx), dim3(threads_for(8)), sm, stream, sl.tmPd, sl.tmWd, k, st); break;
     }
 }
 
@@ -741,8 +741,8 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
         const int gx = (int)std::max<int64_t>(
             1, std::min<int64_t>((int64_t)k2_grid() * std::min(8, K2S_BLOCKS_PER_SM), (k.N / 2 + nth - 1) / nth));
 #define K2S_LAUNCH(S)                                                                                            \
-        if (varm) k2s<S, true><<<gx, nth, 0, stream>>>(P, Wl, Dv, g.vstride, k, st);                            \
-        else k2s<S, false><<<gx, nth, 0, stream>>>(P, Wl, Dv, g.vstride, k, st);
+        if (varm) launch_pdl(g.kn.pdl, k2s<S, true>, dim3(gx), dim3(nth), 0, stream, P, Wl, Dv, g.vstride, k, st);                            \
+        else launch_pdl(g.kn.pdl, k2s<S, false>, dim3(gx), dim3(nth), 0, stream, P, Wl, Dv, g.vstride, k, st);
         switch (s) {
         case 2: K2S_LAUNCH(2) break;
         case 3: K2S_LAUNCH(3) break;
@@ -782,8 +782,8 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     const size_t sm = std::max((size_t)k.nstage * stage, red);
     const CUtensorMap &dv = varm ? sl.tmDv : sl.tmWl;
 #define K2R_LAUNCH(NB, EP)                                                                                   \
-    if (varm) k2r<NB, EP, true><<<gx, threads_for(NB, true), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);          \
-    else k2r<NB, EP, false><<<gx, threads_for(NB, false), sm, stream>>>(sl.tmPr, sl.tmWl, dv, k, st);
+    if (varm) launch_pdl(g.kn.pdl, k2r<NB, EP, true>, dim3(gx), dim3(threads_for(NB, true)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st);          \
+    else launch_pdl(g.kn.pdl, k2r<NB, EP, false>, dim3(gx), dim3(threads_for(NB, false)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st);
     switch (nb) {
     case 1: K2R_LAUNCH(1, K2R_EP_PAIRS) break;
     case 2: K2R_LAUNCH(2, K2R_EP_PAIRS) break;

@@ -39,7 +39,7 @@ template <int KIND>
 __global__ void __launch_bounds__(BX *BY, (KIND == 0 || KIND == 1) ? 8 : 5)
     k1_stencil(Geo g, K1Args a, const DevState *st, K1Work wk)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     const double *__restrict__ p = a.p;
     const double *__restrict__ pm = a.pm;
     double *__restrict__ w = a.w;
@@ -173,7 +173,7 @@ __device__ __forceinline__ double2 ld2cs(const double *p) { return __ldcs(reinte
 template <int KIND>
 __global__ void __launch_bounds__(BX *BY, 4) k1_lap_vec(Geo g, K1Args a, const DevState *st, K1Work wk)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     const double *__restrict__ p = a.p;
     const double *__restrict__ pm = a.pm;
     double *__restrict__ w = a.w;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(BX *BY, 4) k1_lap_vec(Geo g, K1Args a, const D
 // "plane" (= n doubles) in, like the stencil layout).
 __global__ void __launch_bounds__(256) k1_csr(Geo g, K1Args a, const DevState *st)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= g.n) return;
     const double *p = a.p + g.plane;
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(256) k1_csr(Geo g, K1Args a, const DevState *s
 
 __global__ void k_pack(Geo g, const double *src, double *dst, int nzl, const DevState *st)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     const int64_t nxy = (int64_t)g.nx * g.ny, tot = nxy * nzl;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t zl = e / nxy, rem = e - zl * nxy;
@@ -328,7 +328,7 @@ void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s
 {
     if (g.kind == 4) {
         const int64_t blocks = (g.n + 255) / 256;
-        k1_csr<<<(unsigned)blocks, 256, 0, s>>>(g, a, st);
+        launch_pdl(g.kn.pdl, k1_csr, dim3((unsigned)blocks), dim3(256), 0, s, g, a, st);
         return;
     }
     if (k1t_supported(g, a)) {
@@ -365,10 +365,10 @@ void launch_k1(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t s
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
     dim3 block(BX, BY);
     switch (g.kind) {
-    case 0: k1_lap_vec<0><<<grid, block, 0, s>>>(g, a, st, wk); break;
-    case 1: k1_lap_vec<1><<<grid, block, 0, s>>>(g, a, st, wk); break;
-    case 2: k1_stencil<2><<<grid, block, 0, s>>>(g, a, st, wk); break;
-    case 3: k1_stencil<3><<<grid, block, 0, s>>>(g, a, st, wk); break;
+    case 0: launch_pdl(g.kn.pdl, k1_lap_vec<0>, dim3(grid), dim3(block), 0, s, g, a, st, wk); break;
+    case 1: launch_pdl(g.kn.pdl, k1_lap_vec<1>, dim3(grid), dim3(block), 0, s, g, a, st, wk); break;
+    case 2: launch_pdl(g.kn.pdl, k1_stencil<2>, dim3(grid), dim3(block), 0, s, g, a, st, wk); break;
+    case 3: launch_pdl(g.kn.pdl, k1_stencil<3>, dim3(grid), dim3(block), 0, s, g, a, st, wk); break;
     }
 }
 
@@ -380,7 +380,7 @@ void launch_pack(const Geo &g, const double *src, double *dst, int nzl, const De
     }
     const int64_t tot = (int64_t)g.nx * g.ny * nzl;
     const int64_t blocks = std::min<int64_t>((tot + 255) / 256, 148 * 16);
-    k_pack<<<(unsigned)blocks, 256, 0, s>>>(g, src, dst, nzl, st);
+    launch_pdl(g.kn.pdl, k_pack, dim3((unsigned)blocks), dim3(256), 0, s, g, src, dst, nzl, st);
 }
 
 void launch_unpack(const Geo &g, const double *src, double *dst, int nzl, cudaStream_t s)

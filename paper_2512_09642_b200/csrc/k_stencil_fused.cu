@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     k1f(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, K1Args a,
         const DevState *st, K1FWork wk)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     extern __shared__ __align__(128) double smem[];
     double *sp = smem;                       // p_j ring
     double *sm = smem + NSP * PS;            // p_{j-1} ring
@@ -588,8 +588,8 @@ void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevSta
     wk.zc = zc;
     wk.nitems = tiles * ((n1 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
-    if (g.kind == 2) k1f<2><<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, g, a, st, wk);
-    else k1f<1><<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, g, a, st, wk);
+    if (g.kind == 2) launch_pdl(g.kn.pdl, k1f<2>, dim3(grid), dim3(THREADS), SMEM, strm, *a.tmF_P, *a.tmF_M, g, a, st, wk);
+    else launch_pdl(g.kn.pdl, k1f<1>, dim3(grid), dim3(THREADS), SMEM, strm, *a.tmF_P, *a.tmF_M, g, a, st, wk);
 }
 
 }  // namespace sscg

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     k1fv(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM,
          const __grid_constant__ FaceMaps fm, Geo g, K1Args a, const DevState *st, K1FVWork wk)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     extern __shared__ __align__(128) double smem[];
     double *sp = smem;                       // p_j ring
     double *sm = smem + NSP * PS;            // p_{j-1} ring
@@ -559,7 +559,7 @@ void launch_k1fv(const Geo &g, const K1Args &a, double theta, int s, const DevSt
     wk.nitems = tiles * ((n1 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
     FaceMaps fmaps{*a.tmKX, *a.tmKY, *a.tmKZ};
-    k1fv<<<grid, THREADS, SMEM, strm>>>(*a.tmF_P, *a.tmF_M, fmaps, g, a, st, wk);
+    launch_pdl(g.kn.pdl, k1fv, dim3(grid), dim3(THREADS), SMEM, strm, *a.tmF_P, *a.tmF_M, fmaps, g, a, st, wk);
 }
 
 }  // namespace sscg

@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     k1m(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, Outs out,
         const DevState *st, K1MWork wk)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     extern __shared__ __align__(128) double smem[];
     double *sstg = smem;                 // stages: [p_j(z) box | p_{j-1}(z-1) box]
     double *su1 = sstg + NST * STG;      // level-1 outputs (p_{j+1})
@@ -495,7 +495,7 @@ void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st
     wk.zc = zc;
     wk.nitems = tiles * ((n1 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
-    k1m<<<grid, THREADS, SMEM, strm>>>(*a.tmP, *a.tmM, g, out, st, wk);
+    launch_pdl(g.kn.pdl, k1m, dim3(grid), dim3(THREADS), SMEM, strm, *a.tmP, *a.tmM, g, out, st, wk);
 }
 
 }  // namespace sscg

@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(THREADS, KIND >= 3 ? 1 : 2)
         const __grid_constant__ CUtensorMap tmKX, const __grid_constant__ CUtensorMap tmKY,
         const __grid_constant__ CUtensorMap tmKZ, Geo g, K1Args a, const DevState *st, K1TWork wk)
 {
-    if (st && st->done) return;
+    PDL_ENTRY(st);
     extern __shared__ __align__(128) double smem[];
     double *sp = smem;
     double *sq = smem + NSP * PSLOT;
@@ -573,10 +573,10 @@ void launch_k1t(const Geo &g, const K1Args &a, const DevState *st, cudaStream_t 
     wk.nitems = tiles * (wk.nch1 + (n2 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
     const CUtensorMap &P4 = *a.tmP4, &M4 = *a.tmM4;
-    if (kind == 1) k1t<1><<<grid, THREADS, SMEM, s>>>(P4, M4, P4, P4, P4, g, a, st, wk);
-    else if (kind == 2) k1t<2><<<grid, THREADS, SMEM, s>>>(P4, M4, P4, P4, P4, g, a, st, wk);
-    else if (kind == 3) k1t<3><<<grid, THREADS, SMEM, s>>>(P4, M4, P4, P4, P4, g, a, st, wk);
-    else k1t<4><<<grid, THREADS, SMEM4, s>>>(P4, M4, *a.tmKX, *a.tmKY, *a.tmKZ, g, a, st, wk);
+    if (kind == 1) launch_pdl(g.kn.pdl, k1t<1>, dim3(grid), dim3(THREADS), SMEM, s, P4, M4, P4, P4, P4, g, a, st, wk);
+    else if (kind == 2) launch_pdl(g.kn.pdl, k1t<2>, dim3(grid), dim3(THREADS), SMEM, s, P4, M4, P4, P4, P4, g, a, st, wk);
+    else if (kind == 3) launch_pdl(g.kn.pdl, k1t<3>, dim3(grid), dim3(THREADS), SMEM, s, P4, M4, P4, P4, P4, g, a, st, wk);
+    else launch_pdl(g.kn.pdl, k1t<4>, dim3(grid), dim3(THREADS), SMEM4, s, P4, M4, *a.tmKX, *a.tmKY, *a.tmKZ, g, a, st, wk);
 }
 
 }  // namespace sscg

@@ -240,6 +240,7 @@ Knobs sscg::read_knobs()
     k.wfree = tri("SSCG_WFREE", 1) != 0;
     k.k5_recur = tri("SSCG_K5_RECUR", 1) != 0;
     k.debug = getenv("SSCG_DEBUG") != nullptr;
+    k.pdl = tri("SSCG_PDL", 1) != 0;
     return k;
 }
 
@@ -906,6 +907,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     a4.s = s;
     a4.nu = c->nu;
     a4.solver = (c->gram_solver == SSCG_GRAM_CHOLESKY) ? 1 : 0;
+    a4.pdl = g.kn.pdl;
     a4.h_gram = c->h_gram; a4.h_d = c->h_d; a4.h_at = c->h_at; a4.h_al = c->h_al;
     a4.h_delta = c->h_delta; a4.h_relres = c->h_relres; a4.h_lnorm = c->h_lnorm;
     TRY(prof_mark(c, SSCG_PROF_FGS, true));

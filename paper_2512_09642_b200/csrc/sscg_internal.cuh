@@ -5,7 +5,44 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace sscg {
+
+// Programmatic dependent launch (PDL).  The hot kernels are launched with the
+// programmatic-stream-serialization attribute (launch_pdl), so a kernel's
+// CTAs are scheduled while its predecessor in the stream (or the captured
+// graph) is still running.  Each such kernel starts with PDL_ENTRY: it waits
+// (griddepcontrol.wait) until the predecessor grid has completed and its
+// writes are visible -- no global memory is touched before that -- then lets
+// its own dependents launch, then reads the device stop flag.  The launch
+// latency of every kernel boundary is hidden behind the previous kernel's
+// tail.  A kernel launched without the attribute passes the wait at once.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#define PDL_ENTRY(st)                     \
+    do {                                  \
+        ::sscg::pdl_wait();               \
+        ::sscg::pdl_trigger();            \
+        if ((st) && (st)->done) return;   \
+    } while (0)
+
+template <typename... K, typename... A>
+inline cudaError_t launch_pdl(bool pdl, void (*kern)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t strm,
+                              A &&...args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = strm;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
 
 // Device-resident solver state.  K4 (FGS) is the only writer of the control
 // fields; every hot kernel reads `done` first and exits if it is set, so the
@@ -77,6 +114,7 @@ struct Knobs {
     int wfree = 1;         // SSCG_WFREE        0: stored-W schedule
     int k5_recur = 1;      // SSCG_K5_RECUR     0: update with the stored W
     int debug = 0;         // SSCG_DEBUG
+    int pdl = 1;           // SSCG_PDL          0: plain stream-ordered launches (no programmatic dependent launch)
 };
 Knobs read_knobs();
 
@@ -192,6 +230,7 @@ struct K4Args {
     double *alpha;         // out: alpha = d o a~ (s)
     int s, nu;
     int solver;            // 0 = nu FGS sweeps, 1 = dense Cholesky
+    int pdl;               // launch with programmatic dependent launch (Knobs::pdl)
     double *h_gram, *h_d, *h_at, *h_al, *h_delta, *h_relres;  // history [cap][...]
     double *h_lnorm;       // ||L||_F of the scaled Gram matrix G = I + L + L^T per outer
 };
