@@ -3,6 +3,7 @@
 // K5 -- fused solution/residual update x += P alpha, r -= (AP) alpha
 //       (r is stored in place of p_0).
 #include "sscg_internal.cuh"
+#include "k4_small.cuh"
 
 namespace sscg {
 namespace {
@@ -16,36 +17,21 @@ __device__ __forceinline__ double warp_sum(double v)
     return v;
 }
 
-// One warp; lane l owns row i = l (and i = l + 32 when s > 32).
-//   d_i = Ghat_ii^{-1/2};  G = S Ghat S with G_ii := 1;  c~ = S c
-//   FGS sweep (I + L) a^(l+1) = c~ - L^T a^(l) in residual form: with
-//   rho = c~ - G a (unit diagonal), coordinate j takes a_j += rho_j and every
-//   row updates rho_i -= G_ij rho_j (for i = j this gives exactly 0 since
-//   G_jj = 1) -- the forward substitution a_j = c~_j - sum_{i != j} G_ji a_i
-//   of PAPER.md:94-97, one shuffle + one FMA per coordinate, branch-free.
-//   s <= 32: row i of G lives in registers of lane i; s > 32: shared memory.
-template <bool TWO>
-__global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
+// s > 32 (up to 64): one warp, lane l owns rows l and l + 32; the scaled G
+// lives in shared memory (column-major), coordinate by coordinate in residual
+// form (see k4_small.cuh for the method and the s <= 32 kernel).
+__global__ void __launch_bounds__(32) k4_fgs_big(K4Args a, DevState *st)
 {
     PDL_ENTRY(st);
-    __shared__ double Gc[TWO ? SMAX * SMAX : 1];   // column-major: Gc[j*s + i] = G_ij
-    __shared__ double Bs[TWO ? 1 : 32 * 32 + 32];  // s <= 32: the block staged once (coalesced)
+    __shared__ double Gc[SMAX * SMAX];   // column-major: Gc[j*s + i] = G_ij
     __shared__ double dsh[SMAX];
     const int s = a.s, lane = threadIdx.x;
     const int k = st->k;
     const int nent = s * s + s;
     const bool rec = k < st->hist_cap, recg = k < st->gram_cap;
-    if (!TWO) {
-        for (int q = lane; q < nent; q += 32) {
-            const double v = a.blk[q];
-            Bs[q] = v;
-            if (recg) a.h_gram[(int64_t)k * nent + q] = v;
-        }
-        __syncwarp();
-    } else if (recg) {
+    if (recg)
         for (int q = lane; q < nent; q += 32) a.h_gram[(int64_t)k * nent + q] = a.blk[q];
-    }
-    const double *Gh = TWO ? a.blk : Bs, *c = Gh + s * s;
+    const double *Gh = a.blk, *c = Gh + s * s;
 
     const double rn = sqrt(c[0]);
     const double r0 = (k == 0) ? rn : st->r0norm;
@@ -67,7 +53,7 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
     }
     // Ruhe scaling
     const int i0 = lane, i1 = lane + 32;
-    const bool v0 = i0 < s, v1 = TWO && i1 < s;
+    const bool v0 = i0 < s, v1 = i1 < s;
     double d0 = 0.0, d1 = 0.0;
     bool ok = true;
     if (v0) { const double gd = Gh[i0 * s + i0]; ok &= (gd > 0.0) && isfinite(gd); d0 = 1.0 / sqrt(gd); }
@@ -82,99 +68,39 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
     const double ct0 = v0 ? d0 * c[i0] : 0.0;
     const double ct1 = v1 ? d1 * c[i1] : 0.0;
     double rho0 = ct0, rho1 = ct1, al0 = 0.0, al1 = 0.0;
-
-    double lnorm_part = 0.0;
-    if (!TWO) {
-        double g[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            g[j] = (v0 && j < s) ? ((j == i0) ? 1.0 : (d0 * Gh[i0 * s + j]) * dsh[j]) : 0.0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j < i0) lnorm_part = fma(g[j], g[j], lnorm_part);
-        // Coordinates in blocks of four: the four residual entries of a block
-        // come over in four independent shuffles, every lane forms the block's
-        // corrections d_j..d_j+3 by forward substitution with the block's
-        // strictly lower entries (broadcast once), then applies them.  Each
-        // rho_i sees the same FMAs in the same order as coordinate-by-
-        // coordinate FGS (bitwise equal), but the dependent chain per block is
-        // one shuffle + three FMAs instead of four shuffles + four FMAs.
-        double Lb[8][6];
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            const int j = 4 * b;
-            Lb[b][0] = __shfl_sync(0xffffffffu, g[j], j + 1);       // G_{j+1,j}
-            Lb[b][1] = __shfl_sync(0xffffffffu, g[j], j + 2);       // G_{j+2,j}
-            Lb[b][2] = __shfl_sync(0xffffffffu, g[j + 1], j + 2);   // G_{j+2,j+1}
-            Lb[b][3] = __shfl_sync(0xffffffffu, g[j], j + 3);       // G_{j+3,j}
-            Lb[b][4] = __shfl_sync(0xffffffffu, g[j + 1], j + 3);   // G_{j+3,j+1}
-            Lb[b][5] = __shfl_sync(0xffffffffu, g[j + 2], j + 3);   // G_{j+3,j+2}
-        }
-        for (int sw = 0; sw < a.nu; ++sw) {
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const int j = 4 * b;
-                if (j < s) {
-                    const double r0 = __shfl_sync(0xffffffffu, rho0, j), r1 = __shfl_sync(0xffffffffu, rho0, j + 1),
-                                 r2 = __shfl_sync(0xffffffffu, rho0, j + 2), r3 = __shfl_sync(0xffffffffu, rho0, j + 3);
-                    const double d0 = r0;
-                    const double d1 = fma(-Lb[b][0], d0, r1);
-                    const double d2 = fma(-Lb[b][2], d1, fma(-Lb[b][1], d0, r2));
-                    const double d3 = fma(-Lb[b][5], d2, fma(-Lb[b][4], d1, fma(-Lb[b][3], d0, r3)));
-                    rho0 = fma(-g[j], d0, rho0);
-                    al0 += (lane == j) ? d0 : 0.0;
-                    if (j + 1 < s) { rho0 = fma(-g[j + 1], d1, rho0); al0 += (lane == j + 1) ? d1 : 0.0; }
-                    if (j + 2 < s) { rho0 = fma(-g[j + 2], d2, rho0); al0 += (lane == j + 2) ? d2 : 0.0; }
-                    if (j + 3 < s) { rho0 = fma(-g[j + 3], d3, rho0); al0 += (lane == j + 3) ? d3 : 0.0; }
-                }
-            }
-        }
-        double res0 = ct0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j < s) res0 = fma(-g[j], __shfl_sync(0xffffffffu, al0, j), res0);
-        rho0 = res0;
-    } else {
-        for (int q = lane; q < s * s; q += 32) {
-            const int i = q / s, j = q - i * s;
-            Gc[j * s + i] = (i == j) ? 1.0 : (dsh[i] * Gh[q]) * dsh[j];
-        }
-        __syncwarp();
-        for (int sw = 0; sw < a.nu; ++sw) {
-            for (int j = 0; j < s; ++j) {
-                const bool hi = j >= 32;
-                const int owner = j & 31;
-                const double dj = __shfl_sync(0xffffffffu, hi ? rho1 : rho0, owner);
-                const double g0 = v0 ? Gc[j * s + i0] : 0.0;
-                const double g1 = v1 ? Gc[j * s + i1] : 0.0;
-                rho0 = fma(-g0, dj, rho0);
-                rho1 = fma(-g1, dj, rho1);
-                al0 += (!hi && lane == owner) ? dj : 0.0;
-                al1 += (hi && lane == owner) ? dj : 0.0;
-            }
-        }
-        double res0 = ct0, res1 = ct1;
+    for (int q = lane; q < s * s; q += 32) {
+        const int i = q / s, j = q - i * s;
+        Gc[j * s + i] = (i == j) ? 1.0 : (dsh[i] * Gh[q]) * dsh[j];
+    }
+    __syncwarp();
+    for (int sw = 0; sw < a.nu; ++sw) {
         for (int j = 0; j < s; ++j) {
-            const double aj = __shfl_sync(0xffffffffu, (j < 32) ? al0 : al1, j & 31);
-            if (v0) res0 = fma(-Gc[j * s + i0], aj, res0);
-            if (v1) res1 = fma(-Gc[j * s + i1], aj, res1);
+            const bool hi = j >= 32;
+            const int owner = j & 31;
+            const double dj = __shfl_sync(0xffffffffu, hi ? rho1 : rho0, owner);
+            const double g0 = v0 ? Gc[j * s + i0] : 0.0;
+            const double g1 = v1 ? Gc[j * s + i1] : 0.0;
+            rho0 = fma(-g0, dj, rho0);
+            rho1 = fma(-g1, dj, rho1);
+            al0 += (!hi && lane == owner) ? dj : 0.0;
+            al1 += (hi && lane == owner) ? dj : 0.0;
         }
-        rho0 = res0;
-        rho1 = res1;
+    }
+    double res0 = ct0, res1 = ct1;
+    for (int j = 0; j < s; ++j) {
+        const double aj = __shfl_sync(0xffffffffu, (j < 32) ? al0 : al1, j & 31);
+        if (v0) res0 = fma(-Gc[j * s + i0], aj, res0);
+        if (v1) res1 = fma(-Gc[j * s + i1], aj, res1);
     }
     // ||L||_F^2 = sum_{i > j} G_ij^2 (the quantity FGS convergence depends on)
     double ll = 0.0;
-    if (!TWO) {
-        ll = lnorm_part;
-    } else {
-        for (int j = 0; j < s; ++j) {
-            if (v0 && j < i0) { const double gij = Gc[j * s + i0]; ll = fma(gij, gij, ll); }
-            if (v1 && j < i1) { const double gij = Gc[j * s + i1]; ll = fma(gij, gij, ll); }
-        }
+    for (int j = 0; j < s; ++j) {
+        if (v0 && j < i0) { const double gij = Gc[j * s + i0]; ll = fma(gij, gij, ll); }
+        if (v1 && j < i1) { const double gij = Gc[j * s + i1]; ll = fma(gij, gij, ll); }
     }
     ll = warp_sum(ll);
     // delta = ||c~ - G a~|| / ||c~||  (PAPER.md:259-262 inexactness monitor)
-    const double rr = warp_sum(rho0 * rho0 + rho1 * rho1);
+    const double rr = warp_sum(res0 * res0 + res1 * res1);
     const double cc = warp_sum(ct0 * ct0 + ct1 * ct1);
     if (v0) a.alpha[i0] = d0 * al0;
     if (v1) a.alpha[i1] = d1 * al1;
@@ -182,11 +108,9 @@ __global__ void __launch_bounds__(32) k4_fgs(K4Args a, DevState *st)
         if (v0) { a.h_d[(int64_t)k * s + i0] = d0; a.h_at[(int64_t)k * s + i0] = al0; a.h_al[(int64_t)k * s + i0] = d0 * al0; }
         if (v1) { a.h_d[(int64_t)k * s + i1] = d1; a.h_at[(int64_t)k * s + i1] = al1; a.h_al[(int64_t)k * s + i1] = d1 * al1; }
     }
-    if (rec) {
-        if (lane == 0) {
-            a.h_delta[k] = sqrt(rr) / sqrt(cc);
-            a.h_lnorm[k] = sqrt(ll);
-        }
+    if (rec && lane == 0) {
+        a.h_delta[k] = sqrt(rr) / sqrt(cc);
+        a.h_lnorm[k] = sqrt(ll);
     }
     if (lane == 0) {
         st->outer = k + 1;
@@ -501,11 +425,20 @@ __global__ void __launch_bounds__(256) k5_update_gen(K5Params k, const DevState 
 
 }  // namespace
 
+// s <= 32: the one-warp FGS of k4_small.cuh (the same body the Gram pass runs
+// when it is fused there)
+__global__ void __launch_bounds__(32) k4_fgs_warp(K4Args a, DevState *st)
+{
+    PDL_ENTRY(st);
+    __shared__ double scratch[32 * 32 + 32 + 32];
+    k4_fgs_dispatch(a, st, scratch);
+}
+
 void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
 {
     if (a.solver == 1) launch_pdl(a.pdl, k4_chol, dim3(1), dim3(32), 0, s, a, st);
-    else if (a.s <= 32) launch_pdl(a.pdl, k4_fgs<false>, dim3(1), dim3(32), 0, s, a, st);
-    else launch_pdl(a.pdl, k4_fgs<true>, dim3(1), dim3(32), 0, s, a, st);
+    else if (a.s <= 32) launch_pdl(a.pdl, k4_fgs_warp, dim3(1), dim3(32), 0, s, a, st);
+    else launch_pdl(a.pdl, k4_fgs_big, dim3(1), dim3(32), 0, s, a, st);
 }
 
 // Diagnostics: ||P_k||_F^2 of the basis of this outer iteration (before K5

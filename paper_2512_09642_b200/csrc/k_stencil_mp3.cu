@@ -70,7 +70,17 @@ struct K1MWork {
     int tiles_x, tiles_y, zc;
     int64_t nitems;
     int nzl;
-    int zb[3], ze[3];      // write range of each level (level 3's range is the one chunked)
+    // up to two level-3 plane ranges per launch (the boundary launch of the deep
+    // halo schedule covers both ends of the slab): write range of each level,
+    // level 3's range the one chunked; range 1 is empty when nch[1] == 0
+    int zb[2][3], ze[2][3];
+    int nch0;              // chunks of range 0 (items: tiles x (nch0 + chunks of range 1))
+    // planes where level 1 / level 2 are formed (outside: the Dirichlet value 0):
+    // [1, nzl] against the global boundary, extended by 2 / 1 ghost planes on a
+    // side whose 3-plane halo of p_j (and 2 planes of p_{j-1}) is current
+    // (deep halos)
+    int lo1, hi1, lo2, hi2;
+    int zoff;              // tensor-map plane coordinate of plane 0 (2 with guard planes)
     int j;                 // vector coordinate of p_j in the tensor maps
     int front_pm;          // level 1 subtracts p_{j-1} (j >= 1)
     double coef1, coef, sigma, center, dinv_c;
@@ -114,6 +124,7 @@ __device__ __forceinline__ void st_pn(double *p, double2 v)
 
 struct ItemPlan {
     int tx, ty, zlo, zhi;      // level-3 planes [zlo, zhi)
+    int r;                     // plane range of the launch
     int q0, q1;                // march: level-1 planes q0..q1
     int plo, phi, mlo, mhi;    // p_j / p_{j-1} planes loaded
     int first, last;           // first / last chunk (levels 1, 2 write their range's ends)
@@ -127,16 +138,18 @@ __device__ __forceinline__ ItemPlan plan_item(const K1MWork &wk, int64_t item)
     ItemPlan p;
     p.ty = tile / wk.tiles_x;
     p.tx = tile - p.ty * wk.tiles_x;
-    p.zlo = wk.zb[2] + chunk * wk.zc;
-    p.zhi = min(wk.ze[2], p.zlo + wk.zc);
-    p.first = p.zlo == wk.zb[2];
-    p.last = p.zhi == wk.ze[2];
-    p.q0 = max(p.zlo - 2, 0);
-    p.q1 = p.zhi + 1;   // level 3 reaches zhi - 1 at q = zhi + 1 (level 1 is outside past nzl)
-    p.plo = max(p.q0 - 1, 0);
-    p.phi = min(p.q1 + 1, wk.nzl + 1);
-    p.mlo = max(p.q0, 1);
-    p.mhi = min(p.q1, wk.nzl);
+    p.r = chunk >= wk.nch0;
+    const int c = chunk - (p.r ? wk.nch0 : 0);
+    p.zlo = wk.zb[p.r][2] + c * wk.zc;
+    p.zhi = min(wk.ze[p.r][2], p.zlo + wk.zc);
+    p.first = p.zlo == wk.zb[p.r][2];
+    p.last = p.zhi == wk.ze[p.r][2];
+    p.q0 = max(p.zlo - 2, wk.lo1 - 1);
+    p.q1 = p.zhi + 1;   // level 3 reaches zhi - 1 at q = zhi + 1 (level 1 is outside past hi1)
+    p.plo = max(p.q0 - 1, wk.lo1 - 1);
+    p.phi = min(p.q1 + 1, wk.hi1 + 1);
+    p.mlo = max(p.q0, wk.lo1);
+    p.mhi = min(p.q1, wk.hi1);
     return p;
 }
 
@@ -234,8 +247,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (sc >= NST) mbar_wait(&empty[sl], ((sc / NST) - 1) & 1);
                     const bool m = wk.front_pm && z - 1 >= it.mlo && z - 1 <= it.mhi;
                     mbar_expect_tx(&full[sl], PBYTES + (m ? MBYTES : 0u));
-                    tma_load_4d(sstg + sl * STG, &tmP, x0 - 6, y0 - 3, z, wk.j, &full[sl]);
-                    if (m) tma_load_4d(sstg + sl * STG + PS, &tmM, x0 - 4, y0 - 2, z - 1, wk.j - 1, &full[sl]);
+                    tma_load_4d(sstg + sl * STG, &tmP, x0 - 6, y0 - 3, z + wk.zoff, wk.j, &full[sl]);
+                    if (m)
+                        tma_load_4d(sstg + sl * STG + PS, &tmM, x0 - 4, y0 - 2, z - 1 + wk.zoff, wk.j - 1, &full[sl]);
                 }
             }
         }
@@ -251,7 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool in2 = rk >= 2 && rk <= TY + 3 && lane >= 1 && lane <= 30;   // level-2 cell
     const bool in3 = rk >= 3 && rk <= TY + 2 && lane >= 2 && lane <= 29;   // level 3 = the tile
     const bool front_pm = wk.front_pm;
-    const int nzl = wk.nzl;
+    const int lo1 = wk.lo1, hi1 = wk.hi1, lo2 = wk.lo2, hi2 = wk.hi2;
     const double center = wk.center, dinv_c = wk.dinv_c, sigma = wk.sigma, cf1 = wk.coef1, cf = wk.coef;
     double *const w0 = out.w[0], *const w1 = out.w[1], *const w2 = out.w[2];
     double *const n0 = out.pn[0], *const n1 = out.pn[1], *const n2 = out.pn[2];
@@ -266,8 +280,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool vy = gy >= 0 && gy < g.ny;
         const bool v0 = vy && gx >= 0 && gx < g.nx, v1 = vy && gx + 1 >= 0 && gx + 1 < g.nx;
         const bool own = in3 && v0;   // the tile's own cell: outputs go to HBM
-        const int wb1 = it.first ? wk.zb[0] : it.zlo, we1 = it.last ? wk.ze[0] : it.zhi;
-        const int wb2 = it.first ? wk.zb[1] : it.zlo, we2 = it.last ? wk.ze[1] : it.zhi;
+        const int wb1 = it.first ? wk.zb[it.r][0] : it.zlo, we1 = it.last ? wk.ze[it.r][0] : it.zhi;
+        const int wb2 = it.first ? wk.zb[it.r][1] : it.zlo, we2 = it.last ? wk.ze[it.r][1] : it.zhi;
         // stage slots and phases are recomputed from sequence numbers per plane;
         // rolling them plane by plane (no division by NST) cost registers (28 B
         // of spill) and measured 0.70 vs 0.655 ms per launch
@@ -295,7 +309,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         auto plane = [&](int q, auto steady) {
             constexpr bool S = decltype(steady)::value;
             // ---------------- level 1: step j at plane q ----------------
-            const bool inside1 = S || (q >= 1 && q <= nzl);
+            const bool inside1 = S || (q >= lo1 && q <= hi1);
             const bool has_up = S || q + 1 <= it.phi;
             const double *P0 = stg(q), *P1 = stg(q + 1);
             double2 pup = make_double2(0.0, 0.0);   // p_j(q+1)
@@ -330,7 +344,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // ---------------- level 2: step j+1 at plane q-1 ----------------
             const int z2 = q - 1;
             double2 u2 = make_double2(0.0, 0.0);
-            if (in2 && (S || (z2 >= 1 && z2 <= nzl))) {
+            if (in2 && (S || (z2 >= lo2 && z2 <= hi2))) {
                 const double *U = su1 + ((uc - 1) % NU) * U1S;
                 const double2 c = u1m1;
 #if K1M_EO
@@ -399,7 +413,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 #define K1M_L2P CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
 
-bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM)
+// guard: planes allocated below plane 0 (and above nzl+1) of every vector --
+// the deep halo's ghost planes; the maps then start `guard` planes early
+bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM, int guard)
 {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -410,10 +426,11 @@ bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
                                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
                                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                                              CUtensorMapFloatOOBfill)>(fn);
-    cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)(nzl + 2), (cuuint64_t)s};
+    cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)(nzl + 2 + 2 * guard), (cuuint64_t)s};
     cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.vstride * 8};
     cuuint32_t es[4] = {1, 1, 1, 1};
     cuuint32_t boxp[4] = {BW, BHP, 1, 1}, boxm[4] = {MW, MH, 1, 1};
+    P -= (int64_t)guard * g.plane;
     if (enc(tmP, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(P), dims, strides, boxp, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, K1M_L2P,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -454,9 +471,16 @@ void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st
     wk.tiles_y = (g.ny + TY - 1) / TY;
     wk.nzl = a.nzl;
     for (int l = 0; l < 3; ++l) {
-        wk.zb[l] = a.zb[l];
-        wk.ze[l] = a.ze[l];
+        wk.zb[0][l] = a.zb[l];
+        wk.ze[0][l] = a.ze[l];
+        wk.zb[1][l] = a.zb2[l];
+        wk.ze[1][l] = a.ze2[l];
     }
+    wk.lo1 = a.deep_lo ? -1 : 1;
+    wk.lo2 = a.deep_lo ? 0 : 1;
+    wk.hi1 = a.deep_hi ? a.nzl + 2 : a.nzl;
+    wk.hi2 = a.deep_hi ? a.nzl + 1 : a.nzl;
+    wk.zoff = a.guard;
     wk.j = a.j;
     wk.front_pm = a.j > 0;
     wk.coef1 = (a.j == 0) ? theta : 2.0 * theta;
@@ -472,11 +496,13 @@ void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
     const int64_t resident = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
     const int zc_env = g.kn.k1_zc;
-    const int n1 = a.ze[2] - a.zb[2];
+    const int n1 = std::max(0, a.ze[2] - a.zb[2]), n2 = std::max(0, a.ze2[2] - a.zb2[2]);
     if (n1 <= 0) return;
     int zc = n1;
     if (zc_env > 0) {
         zc = std::min(n1, zc_env);
+    } else if (n2 > 0) {
+        zc = std::max(n1, n2);   // boundary launch (deep halos): one chunk per range
     } else {
         // each chunk re-reads 5 planes of p_j and recomputes 4 level-1/2 planes:
         // few long chunks, tiles x chunks filling whole waves
@@ -493,7 +519,8 @@ void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st
         }
     }
     wk.zc = zc;
-    wk.nitems = tiles * ((n1 + zc - 1) / zc);
+    wk.nch0 = (n1 + zc - 1) / zc;
+    wk.nitems = tiles * (wk.nch0 + (n2 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
     launch_pdl(g.kn.pdl, k1m, dim3(grid), dim3(THREADS), SMEM, strm, *a.tmP, *a.tmM, g, out, st, wk);
 }

@@ -239,6 +239,8 @@ Knobs sscg::read_knobs()
     k.k2_smem_kb = std::min(224, std::max(64, num("SSCG_K2_SMEM_KB", 216)));
     k.wfree = tri("SSCG_WFREE", 1) != 0;
     k.k5_recur = tri("SSCG_K5_RECUR", 1) != 0;
+    k.deep_halo = tri("SSCG_DEEP_HALO", 1) != 0;
+    k.deep_overlap = tri("SSCG_DEEP_OVERLAP", 0) != 0;
     k.debug = getenv("SSCG_DEBUG") != nullptr;
     k.pdl = tri("SSCG_PDL", 1) != 0;
     return k;
@@ -339,10 +341,16 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         sl.z0 = (int64_t)gidx * c->nz_global / S;
         sl.nzl = (int)((int64_t)(gidx + 1) * c->nz_global / S - sl.z0);
         sl.zoff = sl.z0 - c->z0_proc;
+        sl.has_lo = gidx > 0;
+        sl.has_hi = gidx + 1 < S;
         max_nzl = std::max(max_nzl, sl.nzl);
         c->slabs.push_back(sl);
     }
-    g.vstride = ((int64_t)(max_nzl + 2) * g.plane + 31) / 32 * 32;   // 256-B aligned vectors
+    // deep halos: 7-point slabs with neighbours keep 3 ghost
+    // planes per side for the K1M triples -- two guard planes allocated beyond
+    // the 1-plane halo on each side of every vector
+    g.guard = (A->kind == SSCG_OP_STENCIL7 && !diag_M && S > 1 && g.kn.deep_halo) ? 2 : 0;
+    g.vstride = ((int64_t)(max_nzl + 2 + 2 * g.guard) * g.plane + 31) / 32 * 32;   // 256-B aligned vectors
     if (getenv("SSCG_VPAD") && (g.vstride / 32) % 2 == 0) g.vstride += 32;   // odd multiple of 256 B
     const int nent = s * s + s;
     const int64_t npart = (int64_t)k2_grid() * 8 * nent;
@@ -351,6 +359,8 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         TRY(dalloc(c, &sl.W, (size_t)g.vstride * s));
         CU(cudaMemsetAsync(sl.P, 0, (size_t)g.vstride * s * sizeof(double), c->stream));
         CU(cudaMemsetAsync(sl.W, 0, (size_t)g.vstride * s * sizeof(double), c->stream));
+        sl.P += (int64_t)g.guard * g.plane;   // vectors address plane 0; planes -guard.. lie before it
+        sl.W += (int64_t)g.guard * g.plane;
         TRY(dalloc(c, &sl.part, (size_t)npart));
         TRY(dalloc(c, &sl.blk, (size_t)nent));
         TRY(dalloc(c, &sl.ticket, 1));
@@ -367,7 +377,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
             sl.has_k1f = true;
         }
         if (A->kind == SSCG_OP_STENCIL7 && !diag_M && k1m_enabled(g, sl.nzl)) {
-            if (!k1m_prepare(g, sl.P, sl.nzl, s, &sl.tmM3_P, &sl.tmM3_M))
+            if (!k1m_prepare(g, sl.P, sl.nzl, s, &sl.tmM3_P, &sl.tmM3_M, g.guard))
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the depth-3 basis step");
             sl.has_k1m = true;
         }
@@ -497,27 +507,34 @@ extern "C" void sscg_destroy(sscg_ctx *c)
 }
 
 // ---------------------------------------------------------------------------
-// halo exchange of basis vector j (one plane per side)
-static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab, cudaStream_t strm)
+// halo exchange of one basis vector: np planes per side --
+// the slab's planes [1, np] go to the lower neighbour's planes [nzl'+1,
+// nzl'+np], its planes [nzl-np+1, nzl] to the upper neighbour's [1-np, 0].
+// np = 1 is the 1-plane halo of a single basis step; np = 3 (p_j) and 2
+// (p_{j-1}) the deep halo of a K1M triple (planes below 0 and
+// above nzl+1 are the guard planes, Geo::guard >= np - 1)
+static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab, cudaStream_t strm, int np = 1)
 {
     const Geo &g = c->g;
     if (g.kind == SSCG_OP_CSR) return SSCG_OK;
-    const size_t pb = (size_t)g.plane * sizeof(double);
+    const size_t cnt = (size_t)np * g.plane, pb = cnt * sizeof(double);
     const int L = (int)c->slabs.size();
     // in-process neighbours (SSCG_NCCL_SELF: by NCCL send/recv to self, in order)
     if (c->nccl_self && L > 1) NC(ncclGroupStart());
     for (int l = 0; l + 1 < L; ++l) {
         double *lo = vec_of_slab[l], *hi = vec_of_slab[l + 1];
         const int nzl = c->slabs[l].nzl;
+        double *lo_src = lo + (int64_t)(nzl - np + 1) * g.plane, *hi_dst = hi + (int64_t)(1 - np) * g.plane;
+        double *hi_src = hi + g.plane, *lo_dst = lo + (int64_t)(nzl + 1) * g.plane;
         if (c->nccl_self) {
-            NC(ncclSend(lo + (int64_t)nzl * g.plane, (size_t)g.plane, ncclDouble, 0, c->comm, strm));
-            NC(ncclRecv(hi, (size_t)g.plane, ncclDouble, 0, c->comm, strm));
-            NC(ncclSend(hi + g.plane, (size_t)g.plane, ncclDouble, 0, c->comm, strm));
-            NC(ncclRecv(lo + (int64_t)(nzl + 1) * g.plane, (size_t)g.plane, ncclDouble, 0, c->comm, strm));
+            NC(ncclSend(lo_src, cnt, ncclDouble, 0, c->comm, strm));
+            NC(ncclRecv(hi_dst, cnt, ncclDouble, 0, c->comm, strm));
+            NC(ncclSend(hi_src, cnt, ncclDouble, 0, c->comm, strm));
+            NC(ncclRecv(lo_dst, cnt, ncclDouble, 0, c->comm, strm));
             continue;
         }
-        CU(cudaMemcpyAsync(hi, lo + (int64_t)nzl * g.plane, pb, cudaMemcpyDeviceToDevice, strm));
-        CU(cudaMemcpyAsync(lo + (int64_t)(nzl + 1) * g.plane, hi + g.plane, pb, cudaMemcpyDeviceToDevice, strm));
+        CU(cudaMemcpyAsync(hi_dst, lo_src, pb, cudaMemcpyDeviceToDevice, strm));
+        CU(cudaMemcpyAsync(lo_dst, hi_src, pb, cudaMemcpyDeviceToDevice, strm));
     }
     if (c->nccl_self && L > 1) NC(ncclGroupEnd());
     if (c->nranks > 1) {
@@ -527,16 +544,17 @@ static sscg_status exchange(sscg_ctx *c, double *const *vec_of_slab, cudaStream_
         TRY(sscg_halo_plan(c->nz_global, c->nranks, c->spr, c->rank, L - 1, hi));
         NC(ncclGroupStart());
         if (lo[0] >= 0 && lo[0] != c->rank) {
-            double *v = vec_of_slab[0];   // send plane lo[1] (local 1), receive plane lo[2] (local 0)
-            NC(ncclSend(v + g.plane, (size_t)g.plane, ncclDouble, (int)lo[0], c->comm, strm));
-            NC(ncclRecv(v, (size_t)g.plane, ncclDouble, (int)lo[0], c->comm, strm));
+            // send planes from lo[1] (local 1) up, receive the planes below lo[2] + 1 (local 0 down)
+            double *v = vec_of_slab[0];
+            NC(ncclSend(v + g.plane, cnt, ncclDouble, (int)lo[0], c->comm, strm));
+            NC(ncclRecv(v + (int64_t)(1 - np) * g.plane, cnt, ncclDouble, (int)lo[0], c->comm, strm));
         }
         if (hi[3] >= 0 && hi[3] != c->rank) {
+            // send the planes up to hi[4] (local nzl), receive from hi[5] (local nzl+1) up
             double *v = vec_of_slab[L - 1];
-            const int nzl = c->slabs[L - 1].nzl;   // send plane hi[4] (local nzl), receive hi[5] (nzl+1)
-            NC(ncclSend(v + (int64_t)nzl * g.plane, (size_t)g.plane, ncclDouble, (int)hi[3], c->comm, strm));
-            NC(ncclRecv(v + (int64_t)(nzl + 1) * g.plane, (size_t)g.plane, ncclDouble, (int)hi[3], c->comm,
-                        strm));
+            const int nzl = c->slabs[L - 1].nzl;
+            NC(ncclSend(v + (int64_t)(nzl - np + 1) * g.plane, cnt, ncclDouble, (int)hi[3], c->comm, strm));
+            NC(ncclRecv(v + (int64_t)(nzl + 1) * g.plane, cnt, ncclDouble, (int)hi[3], c->comm, strm));
         }
         NC(ncclGroupEnd());
     }
@@ -623,18 +641,24 @@ static sscg_status wait_stream(sscg_ctx *c, cudaStream_t strm)
 // halo of basis column j of every local slab; with overlap the exchange runs
 // on the comm stream after the work already enqueued on the solver stream
 // (fork) and `ev_join` marks its completion
-static sscg_status halo_fork(sscg_ctx *c, int j, bool fork)
+// np planes of basis column j; with j2 >= 0 also np2 planes of column j2 (the
+// deep halo of a K1M triple: p_j on 3 planes, p_{j-1} on 2)
+static sscg_status halo_fork(sscg_ctx *c, int j, bool fork, int np = 1, int j2 = -1, int np2 = 0)
 {
     const int L = (int)c->slabs.size();
-    std::vector<double *> vj(L);
-    for (int l = 0; l < L; ++l) vj[l] = c->slabs[l].P + (int64_t)j * c->g.vstride;
+    std::vector<double *> vj(L), vj2(L);
+    for (int l = 0; l < L; ++l) {
+        vj[l] = c->slabs[l].P + (int64_t)j * c->g.vstride;
+        vj2[l] = c->slabs[l].P + (int64_t)std::max(j2, 0) * c->g.vstride;
+    }
     cudaStream_t strm = fork ? c->cstream : c->stream;
     if (fork) {
         CU(cudaEventRecord(c->ev_fork, c->stream));
         CU(cudaStreamWaitEvent(c->cstream, c->ev_fork, 0));
     }
     TRY(prof_mark(c, SSCG_PROF_HALO, true, strm));
-    TRY(exchange(c, vj.data(), strm));
+    TRY(exchange(c, vj.data(), strm, np));
+    if (j2 >= 0 && np2 > 0) TRY(exchange(c, vj2.data(), strm, np2));
     TRY(prof_mark(c, SSCG_PROF_HALO, false, strm));
     if (fork) CU(cudaEventRecord(c->ev_join, c->cstream));
     return SSCG_OK;
@@ -753,6 +777,62 @@ static bool uses_mp3(const sscg_ctx *c)
     return true;
 }
 
+// deep halos: with neighbours, the K1M triples run on slabs
+// whose p_j carries 3 ghost planes and p_{j-1} 2 (one exchange per triple, no
+// boundary single steps); needs the guard planes allocated at setup
+static bool uses_deep(const sscg_ctx *c)
+{
+    const bool halo = c->slabs.size() > 1 || c->nranks > 1;
+    return halo && c->g.guard >= 2 && uses_mp3(c);
+}
+
+// deep-halo triple of steps j..j+2 on every slab.  part 0: all planes (levels 1
+// and 2 formed on the ghost planes of a side with a neighbour); part 1: the
+// planes the next exchange sends (level 3 on [1, 4) and [nzl-2, nzl], levels 1
+// and 2 on [1, 3) and [nzl-1, nzl]); part 2: the rest (level 3 [4, nzl-2),
+// levels 1 and 2 [3, nzl-1))
+static sscg_status launch_basis_triple_deep(sscg_ctx *c, int j, int part)
+{
+    const Geo &g = c->g;
+    const int s = c->s;
+    const bool wf = uses_wfree(c);
+    for (auto &sl : c->slabs) {
+        K1MArgs a{};
+        const int n = sl.nzl;
+        for (int l = 0; l < 3; ++l) {
+            const int jl = j + l;
+            a.w[l] = (!wf || jl == s - 1) ? sl.W + (int64_t)jl * g.vstride : nullptr;
+            a.pn[l] = (jl + 1 <= s - 1) ? sl.P + (int64_t)(jl + 1) * g.vstride : nullptr;
+            if (part == 0) {
+                a.zb[l] = 1;
+                a.ze[l] = n + 1;
+            } else if (part == 1) {
+                a.zb[l] = 1;
+                a.ze[l] = (l == 2) ? 4 : 3;
+                a.zb2[l] = (l == 2) ? n - 2 : n - 1;
+                a.ze2[l] = n + 1;
+            } else {
+                a.zb[l] = (l == 2) ? 4 : 3;
+                a.ze[l] = (l == 2) ? n - 2 : n - 1;
+            }
+        }
+        if (part == 2) a.sm_cap = c->k1_sm_cap;
+        a.deep_lo = sl.has_lo;
+        a.deep_hi = sl.has_hi;
+        a.guard = g.guard;
+        a.nzl = n;
+        a.j = j;
+        a.sigma = c->sigma;
+        a.tmP = &sl.tmM3_P;
+        a.tmM = &sl.tmM3_M;
+        TRY(prof_mark(c, SSCG_PROF_BASIS, true));
+        launch_k1m(g, a, c->theta, c->st, c->stream);
+        TRY(prof_mark(c, SSCG_PROF_BASIS, false));
+        ++c->launches;
+    }
+    return SSCG_OK;
+}
+
 // halo = false: all planes of a slab bounded by Dirichlet planes; true: the
 // planes each level can form from p_j with its halo planes current (level 1
 // [2, nzl) -- its planes 1 and nzl come from the boundary single step --,
@@ -773,6 +853,7 @@ static sscg_status launch_basis_triple(sscg_ctx *c, int j, bool halo = false)
             a.ze[l] = halo ? (l == 2 ? sl.nzl - 1 : sl.nzl) : sl.nzl + 1;
         }
         if (halo) a.sm_cap = c->k1_sm_cap;
+        a.guard = g.guard;
         a.nzl = sl.nzl;
         a.j = j;
         a.sigma = c->sigma;
@@ -833,12 +914,31 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const int L = (int)c->slabs.size();
     const bool halo = (L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR;
     const bool ovl = halo && c->overlap;
-    const bool fuse = uses_fused(c), mp3 = uses_mp3(c);
+    const bool fuse = uses_fused(c), mp3 = uses_mp3(c), deep = uses_deep(c);
     nvtxRangePushA("basis");
     for (int j = 0; j < s; ++j) {
         if (mp3 && j + 2 < s) {   // steps j, j+1, j+2 in one pass (K1M)
             if (!halo) {
                 TRY(launch_basis_triple(c, j));
+            } else if (deep) {
+                // p_j is current on 3 ghost planes, p_{j-1} on 2: the triple forms
+                // levels 1 and 2 on the ghost planes itself.  Its outputs feed the next
+                // triple (p_{j+3} on 3 planes, p_{j+2} on 2) or the remaining single /
+                // paired steps (p_{j+3} on 1 plane): one exchange after the triple.
+                // SSCG_DEEP_OVERLAP=1: the planes the exchange sends go first and the
+                // exchange overlaps the rest of the triple (an extra launch per triple;
+                // measured slower on one GPU, tools/slab_overhead.py)
+                const bool next3 = j + 5 < s;
+                const int np3 = (j + 3 < s) ? (next3 ? 3 : 1) : 0, np2 = next3 ? 2 : 0;
+                if (ovl && np3 > 0 && g.kn.deep_overlap) {
+                    TRY(launch_basis_triple_deep(c, j, 1));
+                    TRY(halo_fork(c, j + 3, true, np3, j + 2, np2));
+                    TRY(launch_basis_triple_deep(c, j, 2));
+                    TRY(halo_join(c));
+                } else {
+                    TRY(launch_basis_triple_deep(c, j, 0));
+                    if (np3 > 0) TRY(halo_fork(c, j + 3, false, np3, j + 2, np2));
+                }
             } else {
                 // boundary planes of step j, exchange of p_{j+1} (overlapped with the
                 // interior triple), boundary planes of step j+1, exchange of p_{j+2},
@@ -882,6 +982,15 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     nvtxRangePop();
     nvtxRangePushA("gram+allreduce+fgs");
     const bool wfree = uses_wfree(c);
+    K4Args a4{};
+    a4.blk = c->blk;
+    a4.alpha = c->alpha;
+    a4.s = s;
+    a4.nu = c->nu;
+    a4.solver = (c->gram_solver == SSCG_GRAM_CHOLESKY) ? 1 : 0;
+    a4.pdl = g.kn.pdl;
+    a4.h_gram = c->h_gram; a4.h_d = c->h_d; a4.h_at = c->h_at; a4.h_al = c->h_al;
+    a4.h_delta = c->h_delta; a4.h_relres = c->h_relres; a4.h_lnorm = c->h_lnorm;
     for (auto &sl : c->slabs) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
         if (wfree) launch_k2r(g, sl, s, c->theta, c->sigma, c->st, L == 1 ? c->blk : sl.blk, c->stream);
@@ -901,15 +1010,6 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
         TRY(prof_mark(c, SSCG_PROF_ALLREDUCE, false));
         ++c->allreduces;
     }
-    K4Args a4{};
-    a4.blk = c->blk;
-    a4.alpha = c->alpha;
-    a4.s = s;
-    a4.nu = c->nu;
-    a4.solver = (c->gram_solver == SSCG_GRAM_CHOLESKY) ? 1 : 0;
-    a4.pdl = g.kn.pdl;
-    a4.h_gram = c->h_gram; a4.h_d = c->h_d; a4.h_at = c->h_at; a4.h_al = c->h_al;
-    a4.h_delta = c->h_delta; a4.h_relres = c->h_relres; a4.h_lnorm = c->h_lnorm;
     TRY(prof_mark(c, SSCG_PROF_FGS, true));
     launch_k4(a4, c->st, c->stream);
     if (c->diagnostics) {
@@ -932,7 +1032,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     nvtxRangePushA("update");
     auto k5 = [&](int zb, int ze) -> sscg_status {
         for (auto &sl : c->slabs) {
-            const int e = (ze == -1) ? sl.nzl + 1 : (ze == -2) ? sl.nzl : std::min(ze, sl.nzl + 1);
+            const int e = (ze < 0) ? sl.nzl + 2 + ze : std::min(ze, sl.nzl + 1);   // ze = -m: nzl + 2 - m
             const int b = std::max(zb, 1);
             if (e <= b) continue;
             TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
@@ -943,27 +1043,30 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
         }
         return SSCG_OK;
     };
+    // r_{k+1} = p_0 of the next outer needs 3 ghost planes for a deep-halo triple
+    const int np0 = deep ? 3 : 1;
     if (!halo) {
         TRY(k5(1, -1));
-    } else if (!ovl) {
+    } else if (!ovl || (deep && !g.kn.deep_overlap)) {
         TRY(k5(1, -1));
-        TRY(halo_fork(c, 0, false));
+        TRY(halo_fork(c, 0, false, np0));
     } else {
-        // boundary planes of r_{k+1} (= p_0 of the next outer) first, their
-        // exchange overlapping the interior update
+        // boundary planes of r_{k+1} first, their exchange overlapping the
+        // interior update
         for (auto &sl : c->slabs) {
-            const int top = std::max(2, sl.nzl);
+            const int top = std::max(1 + np0, sl.nzl - np0 + 1);
             for (int zb : {1, top}) {
-                if (zb > sl.nzl) continue;
+                const int ze = std::min(zb + np0, sl.nzl + 1);
+                if (zb >= ze) continue;
                 TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
-                launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, zb, zb + 1,
+                launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, zb, ze,
                           c->theta, c->sigma, uses_rec_update(c));
                 TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
                 ++c->launches;
             }
         }
-        TRY(halo_fork(c, 0, true));
-        TRY(k5(2, -2));
+        TRY(halo_fork(c, 0, true, np0));
+        TRY(k5(1 + np0, -(1 + np0)));
         TRY(halo_join(c));
     }
     nvtxRangePop();
@@ -1117,7 +1220,7 @@ extern "C" sscg_status sscg_solve(sscg_ctx *c, const double *b, double *x, doubl
     }
     nvtxRangePushA("sscg_solve");
     // halo planes of p_0 = r_0 (enqueue_outer's precondition)
-    if ((L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR) TRY(halo_fork(c, 0, false));
+    if ((L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR) TRY(halo_fork(c, 0, false, uses_deep(c) ? 3 : 1));
     // outer iterations in chunks; the device decides when to stop
     int issued = 0;
     int chunk = 2;

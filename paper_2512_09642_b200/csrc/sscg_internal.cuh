@@ -66,10 +66,14 @@ struct DevState {
 // One z-slab of the decomposition in the workspace layout.
 //   plane  = ny * pitch doubles; pitch = nx rounded up to even (16-B rows)
 //   vector = (nzl + 2) planes: plane 0 = lower halo, 1..nzl interior,
-//            nzl+1 = upper halo (zero at global boundaries).
+//            nzl+1 = upper halo (zero at global boundaries); with deep halos
+//            (Geo::guard = 2) two more ghost planes are allocated on each
+//            side (planes -2, -1 and nzl+2, nzl+3), so a vector spans
+//            nzl + 6 planes and its base pointer still addresses plane 0.
 struct Slab {
     int64_t z0;        // first global plane
     int nzl;           // interior planes
+    int has_lo, has_hi;   // a neighbour slab (this or another rank) below / above
     int64_t zoff;      // first plane relative to the process-local range
     double *P;         // s vectors, stride vstride
     double *W;         // s vectors, stride vstride
@@ -113,6 +117,8 @@ struct Knobs {
     int k2_e = 0, k2_ns = 0, k2_grid = 0, k2_groups = 0, k2_smem_kb = 216;   // Gram-pass sweeps
     int wfree = 1;         // SSCG_WFREE        0: stored-W schedule
     int k5_recur = 1;      // SSCG_K5_RECUR     0: update with the stored W
+    int deep_halo = 1;     // SSCG_DEEP_HALO    0: 1-plane halos around every K1M triple (boundary single steps)
+    int deep_overlap = 0;  // SSCG_DEEP_OVERLAP 1: deep-halo exchange overlapped with the triple / update interior
     int debug = 0;         // SSCG_DEBUG
     int pdl = 1;           // SSCG_PDL          0: plain stream-ordered launches (no programmatic dependent launch)
 };
@@ -125,6 +131,7 @@ struct Geo {
     int pitch;         // row pitch (doubles)
     int64_t plane;     // ny * pitch
     int64_t vstride;   // doubles between consecutive basis vectors
+    int guard;         // ghost planes allocated beyond the 1-plane halo on each side (0, or 2 for deep halos)
     double center;     // 4, 6, 26 for constant stencils
     double dinv_c;     // 1/center
     // CSR
@@ -187,12 +194,18 @@ struct K1MArgs {
     double *w[3];          // w_j, w_{j+1}, w_{j+2} (null: not stored)
     double *pn[3];         // p_{j+1}, p_{j+2}, p_{j+3} (null: not stored)
     int zb[3], ze[3];      // padded planes each level writes
+    int zb2[3], ze2[3];    // optional second range (deep-halo boundary launch), empty if ze2[2] <= zb2[2]
     int nzl, j, sm_cap;
+    // deep halos: a side with deep_* set has p_j current on 3
+    // ghost planes and p_{j-1} on 2; levels 1 and 2 are then formed on 2 / 1
+    // ghost planes there instead of taking the Dirichlet value
+    int deep_lo, deep_hi;
+    int guard;             // guard planes allocated below plane 0 (tensor-map offset)
     double sigma;
     const CUtensorMap *tmP, *tmM;
 };
 bool k1m_enabled(const Geo &g, int nzl);
-bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM);
+bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM, int guard);
 void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st, cudaStream_t strm);
 bool k1f_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP, CUtensorMap *tmM);
 void launch_k1f(const Geo &g, const K1Args &a, double theta, int s, const DevState *st, cudaStream_t strm);

@@ -43,7 +43,7 @@ SHAPES = {
 SWITCHES = {
     "7pt": [{}, {"SSCG_K1_MP3": "1"}, {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "1"}, {"SSCG_K1_FUSE": "0"},
             {"SSCG_WFREE": "0"}, {"SSCG_WFREE": "0", "SSCG_K2_DMMA": "1"}, {"SSCG_K5_RECUR": "0"},
-            {"SSCG_K1_TMA": "0", "SSCG_K1_FUSE": "0"}],
+            {"SSCG_K1_TMA": "0", "SSCG_K1_FUSE": "0"}, {"SSCG_PDL": "0"}],
     "7pt_mid": [{}, {"SSCG_K1_MP3": "1"}, {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "1"}, {"SSCG_WFREE": "0"}],
     "cfg2": [{}, {"SSCG_K1_MP3": "1"}, {"SSCG_K5_RECUR": "0"}, {"SSCG_WFREE": "0"}],
     "27pt": [{}, {"SSCG_K1_FUSE": "1"}, {"SSCG_WFREE": "0"}, {"SSCG_WFREE": "0", "SSCG_K2_DMMA": "1"},

@@ -369,6 +369,50 @@ def test_triples_match_single_steps(cfg, slabs, monkeypatch):
     assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
 
 
+@pytest.mark.parametrize("cfg,slabs", [(("7pt", 40, 36, 33, 16, 25), 3), (("7pt", 58, 30, 37, 10, 20), 2),
+                                       (("7pt", 26, 24, 40, 7, 15), 4), (("7pt", 33, 17, 27, 11, 10), 3)],
+                         ids=lambda v: _ids(v) if isinstance(v, tuple) else str(v))
+def test_deep_halo_triples(cfg, slabs, monkeypatch):
+    """Deep halos: with neighbours, each K1M triple gets p_j on
+    3 ghost planes and p_{j-1} on 2 in ONE exchange and forms levels 1 and 2
+    on the ghost planes itself, instead of single steps on the boundary planes
+    around three 1-plane exchanges.  Against the 1-plane schedule and the
+    one-slab solve: agreement to rounding (the ghost levels are summed by K1M,
+    the boundary single steps by K1T); the serial deep schedule (triple, then
+    the exchange; the default) and the overlapped one (SSCG_DEEP_OVERLAP=1:
+    the planes the exchange sends first, the exchange during the rest):
+    bitwise equal.
+    All agree with the oracle."""
+    import paper_2512_09642_b200 as sscg
+    kind, nx, ny, nz, s, nu = cfg
+    P = Problem(kind, nx, ny, nz, s, nu)
+    monkeypatch.setenv("SSCG_K1_MP3", "1")
+    out = {}
+    for mode, env, sl in (("deep", {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "1"}, slabs),
+                          ("deep_serial", {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "0"}, slabs),
+                          ("plane1", {"SSCG_DEEP_HALO": "0", "SSCG_DEEP_OVERLAP": "0"}, slabs),
+                          ("one", {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "0"}, 1)):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with P.gpu_solver(slabs=sl) as S:
+            assert S.query(sscg.QUERY_BASIS_FUSED) == 3
+            x = S.solve(P.b_gpu(), rtol=0.0, max_outer=5).cpu().numpy()
+            out[mode] = (x, [S.gram(k)[0] for k in range(6)], [S.basis(j) for j in range(s)])
+    a, b = out["deep"], out["deep_serial"]
+    assert np.array_equal(a[0], b[0])
+    for k in range(6):
+        assert np.array_equal(a[1][k], b[1][k])
+    for ref in ("plane1", "one"):
+        r = out[ref]
+        assert np.max(np.abs(a[1][0] - r[1][0])) <= 1e-13 * np.max(np.abs(r[1][0])), ref
+        for j in range(s):
+            for q in range(2):
+                assert rel_inf(a[2][j][q], r[2][j][q]) <= 1e-11, (ref, j, q)
+        assert np.linalg.norm(a[0] - r[0]) <= 1e-10 * np.linalg.norm(r[0]), ref
+    x_or, tr = P.oracle(max_outer=5, dump_iter=0)
+    assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
 def test_face_staging_matches_direct_loads(monkeypatch):
     """K1T variable-coefficient faces staged by TMA (nx even) against the
     same kernel reading them from global memory: identical arithmetic."""
