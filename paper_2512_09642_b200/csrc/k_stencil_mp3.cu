@@ -213,6 +213,11 @@ __device__ __forceinline__ void st_u(double *U, int o, int oe, double2 v)
 #endif
 }
 
+// HASW: some level stores w (the stored-W schedule, or a triple that ends at
+// step s-1); HASN2: level 3 stores p_{j+3} (j+3 <= s-1).  p_{j+1} and p_{j+2}
+// are always stored.  Compile-time, so the common W-free triple carries no
+// per-plane tests of the output pointers.
+template <bool HASW, bool HASN2>
 __global__ void __launch_bounds__(THREADS, 1)
     k1m(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmM, Geo g, Outs out,
         const DevState *st, K1MWork wk)
@@ -333,8 +338,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (!v1) u1.y = 0.0;
                 if (own && (S || (q >= wb1 && q < we1))) {
                     if (!v1) Ap.y = 0.0;
-                    if (w0) __stcs(reinterpret_cast<double2 *>(w0 + off), Ap);
-                    if (n0) st_pn(n0 + off, u1);
+                    if (HASW && w0) __stcs(reinterpret_cast<double2 *>(w0 + off), Ap);
+                    st_pn(n0 + off, u1);
                 }
             }
             st_u(su1 + (uc % NU) * U1S, o1, oe1, u1);
@@ -358,8 +363,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (!v1) u2.y = 0.0;
                 if (own && (S || (z2 >= wb2 && z2 < we2))) {
                     if (!v1) Ap.y = 0.0;
-                    if (w1) __stcs(reinterpret_cast<double2 *>(w1 + off - pl), Ap);
-                    if (n1) st_pn(n1 + off - pl, u2);
+                    if (HASW && w1) __stcs(reinterpret_cast<double2 *>(w1 + off - pl), Ap);
+                    st_pn(n1 + off - pl, u2);
                 }
             }
             if (in2) st_u(su2 + ((uc - 1) % NU) * U2S, o2, oe2, u2);
@@ -374,8 +379,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 double2 Ap = stencil(U, o2, c, u2m2, u2, center);
 #endif
                 if (!v1) Ap.y = 0.0;
-                if (w2) __stcs(reinterpret_cast<double2 *>(w2 + off - 2 * pl), Ap);
-                if (n2) {
+                if (HASW && w2) __stcs(reinterpret_cast<double2 *>(w2 + off - 2 * pl), Ap);
+                if (HASN2) {
                     const double v0b = cf * (dinv_c * Ap.x - sigma * c.x) - u1m2.x;   // u1m2 = p_{j+1}(q-2)
                     double v1b = cf * (dinv_c * Ap.y - sigma * c.y) - u1m2.y;
                     if (!v1) v1b = 0.0;
@@ -439,7 +444,10 @@ bool k1m_prepare(const Geo &g, const double *P, int nzl, int s, CUtensorMap *tmP
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, K1M_L2P,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
-    return cudaFuncSetAttribute(k1m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
+    return cudaFuncSetAttribute(k1m<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess &&
+           cudaFuncSetAttribute(k1m<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess &&
+           cudaFuncSetAttribute(k1m<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess &&
+           cudaFuncSetAttribute(k1m<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) == cudaSuccess;
 }
 
 // SSCG_K1_MP3 (read at every sscg_setup): "1" / "0" force / forbid the
@@ -522,7 +530,10 @@ void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st
     wk.nch0 = (n1 + zc - 1) / zc;
     wk.nitems = tiles * (wk.nch0 + (n2 + zc - 1) / zc);
     const unsigned grid = (unsigned)std::min<int64_t>(wk.nitems, resident);
-    launch_pdl(g.kn.pdl, k1m, dim3(grid), dim3(THREADS), SMEM, strm, *a.tmP, *a.tmM, g, out, st, wk);
+    // p_{j+1} and p_{j+2} always exist in a triple (j + 2 <= s - 1)
+    const bool hasw = out.w[0] || out.w[1] || out.w[2], hasn2 = out.pn[2] != nullptr;
+    auto kern = hasw ? (hasn2 ? k1m<true, true> : k1m<true, false>) : (hasn2 ? k1m<false, true> : k1m<false, false>);
+    launch_pdl(g.kn.pdl, kern, dim3(grid), dim3(THREADS), SMEM, strm, *a.tmP, *a.tmM, g, out, st, wk);
 }
 
 }  // namespace sscg
