@@ -46,7 +46,7 @@ class _Trace(C.Structure):
                 ("relres", C.c_void_p), ("ghat", C.c_void_p), ("c", C.c_void_p), ("d", C.c_void_p),
                 ("alpha_t", C.c_void_p), ("alpha", C.c_void_p), ("delta", C.c_void_p),
                 ("energy", C.c_void_p), ("dump_iter", C.c_int), ("P_dump", C.c_void_p),
-                ("W_dump", C.c_void_p)]
+                ("W_dump", C.c_void_p), ("gconj", C.c_void_p), ("cconj", C.c_void_p)]
 
 
 _lib = None
@@ -230,19 +230,24 @@ class Trace:
     energy: np.ndarray
     P: np.ndarray | None = None
     W: np.ndarray | None = None
+    gconj: np.ndarray | None = None   # block-conjugate mode: G_k = Q_k^T A Q_k
+    cconj: np.ndarray | None = None   # and c_k = Q_k^T r_k
 
 
-OPT_CHOLESKY, OPT_MONOMIAL = 1, 2
+OPT_CHOLESKY, OPT_MONOMIAL, OPT_BLOCKCG = 1, 2, 4
 
 
 def sstep_cg(A: Operator, lmin, lmax, s, nu, b, x0=None, rtol=1e-8, max_outer=1000, D=None,
-             dump_iter=-1, gram_solver="fgs", basis="chebyshev") -> tuple[np.ndarray, Trace]:
+             dump_iter=-1, gram_solver="fgs", basis="chebyshev", block=False) -> tuple[np.ndarray, Trace]:
     """Run the oracle s-step CG; returns (x, Trace).  Trace arrays are indexed
     by outer iteration k (only the first ``outer`` (+1 for ghat/c/relres)
     entries are meaningful).  gram_solver 'fgs' (nu sweeps) or
     'cholesky' (exact, PAPER.md:20); basis 'chebyshev' (PAPER.md:33-43) or
-    'monomial' (PAPER.md:31, 164)."""
+    'monomial'; block=True: block-conjugate s-step CG
+    (sscg_oracle.c ORC_OPT_BLOCKCG, R24) instead of the restart form
+    (the basis dump holds the raw basis P_k, W_k before the conjugation)."""
     opts = (OPT_CHOLESKY if gram_solver == "cholesky" else 0) | (OPT_MONOMIAL if basis == "monomial" else 0)
+    opts |= OPT_BLOCKCG if block else 0
     assert gram_solver in ("fgs", "cholesky") and basis in ("chebyshev", "monomial")
     b = _f64(b)
     n = A.n
@@ -252,12 +257,14 @@ def sstep_cg(A: Operator, lmin, lmax, s, nu, b, x0=None, rtol=1e-8, max_outer=10
     at = np.zeros((K, s)); al = np.zeros((K, s)); de = np.zeros(K); en = np.zeros(K)
     Pd = np.zeros((s, n)) if dump_iter >= 0 else None
     Wd = np.zeros((s, n)) if dump_iter >= 0 else None
+    gq = np.zeros((K, s, s)) if block else None
+    cq = np.zeros((K, s)) if block else None
     tr = _Trace(0, 0, 0, 0.0, _p(relres), _p(ghat), _p(c), _p(d), _p(at), _p(al), _p(de), _p(en),
-                dump_iter, _p(Pd), _p(Wd))
+                dump_iter, _p(Pd), _p(Wd), _p(gq), _p(cq))
     Dm = None if D is None else _f64(D)
     lib().orc_sstep_cg_ex(A.ref, _p(Dm), lmin, lmax, s, nu, _p(b), _p(x), rtol, max_outer, C.byref(tr), opts)
     return x, Trace(tr.outer, bool(tr.converged), bool(tr.breakdown), tr.r0norm, relres, ghat, c, d,
-                    at, al, de, en, Pd, Wd)
+                    at, al, de, en, Pd, Wd, gq, cq)
 
 
 def pcg(A: Operator, b, rtol=1e-8, max_iter=100000, D=None):

@@ -66,6 +66,9 @@ typedef struct {
     int dump_iter;      /* outer index whose basis is copied out (-1: none)    */
     double *P_dump;     /* n*s column-major                                    */
     double *W_dump;     /* n*s column-major                                    */
+    /* block-conjugate mode (ORC_OPT_BLOCKCG): the Gram system actually solved */
+    double *gconj;      /* [k*s*s] G_k = Q_k^T A Q_k (= Ghat at k = 0)          */
+    double *cconj;      /* [k*s]   c_k = Q_k^T r_k                             */
 } orc_trace;
 
 /* ------------------------------------------------------------------ */
@@ -392,8 +395,24 @@ void orc_mgs_anorm(const orc_op *A, int s, const double *Pt, const double *v, do
  *   opts & ORC_OPT_MONOMIAL  monomial basis p_{j+1} = M^{-1} A p_j
  *                            ("For monomial bases")
  * A Cholesky breakdown (non-positive pivot) is reported as a Gram breakdown. */
+/*   opts & ORC_OPT_BLOCKCG   block-conjugate s-step CG (
+ *                            the paper updates only
+ *                            x += P alpha, i.e. the restart
+ *                            form; this is the classical alternative, DESIGN.md
+ *                            R24).  With the previous search block Q' and
+ *                            Z' = A Q' kept, per outer k >= 1:
+ *                              G' = Q'^T Z',  C = Z'^T P_k,  e = Q'^T r_k
+ *                              B  = G'^{-1} C                (Cholesky of G')
+ *                              Q_k = P_k - Q' B,  Z_k = W_k - Z' B
+ *                              G_k = Ghat - C^T B,  c_k = c - B^T e
+ *                            (G_k = Q_k^T A Q_k and c_k = Q_k^T r_k, expanded
+ *                            with B^T G' B = C^T B, so one Gram pass over
+ *                            [P_k | Q'] gives every entry); then the same
+ *                            scaling + FGS / Cholesky on (G_k, c_k), and
+ *                            x += Q_k alpha, r -= Z_k alpha.  k = 0: Q = P. */
 #define ORC_OPT_CHOLESKY 1
 #define ORC_OPT_MONOMIAL 2
+#define ORC_OPT_BLOCKCG 4
 int orc_sstep_cg_ex(const orc_op *A, const double *Dm, double lmin, double lmax, int s, int nu,
                     const double *b, double *x, double rtol, int max_outer, orc_trace *tr, int opts);
 
@@ -420,6 +439,22 @@ int orc_sstep_cg_ex(const orc_op *A, const double *Dm, double lmin, double lmax,
     double *ct = (double *)malloc((size_t)s * sizeof(double));
     double *at_ = (double *)malloc((size_t)s * sizeof(double));
     double *al = (double *)malloc((size_t)s * sizeof(double));
+    /* block-conjugate mode: previous search block Q', Z' = A Q' and the work arrays */
+    const int blockcg = (opts & ORC_OPT_BLOCKCG) != 0;
+    double *Qp = NULL, *Zp = NULL, *Gp = NULL, *Cx = NULL, *Bm = NULL, *e = NULL, *Gk = NULL, *ck = NULL,
+           *colb = NULL, *colx = NULL;
+    if (blockcg) {
+        Qp = (double *)malloc((size_t)n * s * sizeof(double));
+        Zp = (double *)malloc((size_t)n * s * sizeof(double));
+        Gp = (double *)malloc((size_t)s * s * sizeof(double));
+        Cx = (double *)malloc((size_t)s * s * sizeof(double));
+        Bm = (double *)malloc((size_t)s * s * sizeof(double));
+        e = (double *)malloc((size_t)s * sizeof(double));
+        Gk = (double *)malloc((size_t)s * s * sizeof(double));
+        ck = (double *)malloc((size_t)s * sizeof(double));
+        colb = (double *)malloc((size_t)s * sizeof(double));
+        colx = (double *)malloc((size_t)s * sizeof(double));
+    }
 
     /* r_0 = b - A x_0 */
     orc_apply(A, x, r);
@@ -443,7 +478,65 @@ int orc_sstep_cg_ex(const orc_op *A, const double *Dm, double lmin, double lmax,
         }
         if (rn <= rtol * r0norm) { converged = 1; break; }
         if (k == max_outer) break;
-        if (orc_scale(s, Ghat, c, d, G, ct) != 0) { breakdown = 1; break; }
+        const double *Gsys = Ghat, *csys = c;   /* the Gram system solved this outer */
+        if (blockcg && k > 0) {
+            /* G' = Q'^T Z' (i <= j, mirrored), C = Z'^T P_k, e = Q'^T r_k */
+            for (int i = 0; i < s; ++i)
+                for (int j = i; j < s; ++j) {
+                    const double v = orc_dot(n, Qp + (long)i * n, Zp + (long)j * n);
+                    Gp[i * s + j] = v;
+                    Gp[j * s + i] = v;
+                }
+            for (int i = 0; i < s; ++i) {
+                for (int j = 0; j < s; ++j) Cx[i * s + j] = orc_dot(n, Zp + (long)i * n, P + (long)j * n);
+                e[i] = orc_dot(n, Qp + (long)i * n, r);
+            }
+            /* B = G'^{-1} C, column by column */
+            for (int j = 0; j < s; ++j) {
+                for (int i = 0; i < s; ++i) colb[i] = Cx[i * s + j];
+                if (orc_cholesky_solve(s, Gp, colb, colx) != 0) { breakdown = 1; break; }
+                for (int i = 0; i < s; ++i) Bm[i * s + j] = colx[i];
+            }
+            if (breakdown) break;
+            /* G_k = Ghat - C^T B (i <= j, mirrored),  c_k = c - B^T e */
+            for (int i = 0; i < s; ++i)
+                for (int j = i; j < s; ++j) {
+                    double v = 0.0;
+                    for (int m = 0; m < s; ++m) v += Cx[m * s + i] * Bm[m * s + j];
+                    Gk[i * s + j] = Ghat[i * s + j] - v;
+                    Gk[j * s + i] = Gk[i * s + j];
+                }
+            for (int i = 0; i < s; ++i) {
+                double v = 0.0;
+                for (int m = 0; m < s; ++m) v += Bm[m * s + i] * e[m];
+                ck[i] = c[i] - v;
+            }
+            /* Q_k = P_k - Q' B,  Z_k = W_k - Z' B, in place of P, W */
+#pragma omp parallel for schedule(static)
+            for (long q = 0; q < n; ++q) {
+                double pq[64], wq[64];
+                for (int j = 0; j < s; ++j) {
+                    double sp = 0.0, sw = 0.0;
+                    for (int m = 0; m < s; ++m) {
+                        sp += Qp[(long)m * n + q] * Bm[m * s + j];
+                        sw += Zp[(long)m * n + q] * Bm[m * s + j];
+                    }
+                    pq[j] = P[(long)j * n + q] - sp;
+                    wq[j] = W[(long)j * n + q] - sw;
+                }
+                for (int j = 0; j < s; ++j) {
+                    P[(long)j * n + q] = pq[j];
+                    W[(long)j * n + q] = wq[j];
+                }
+            }
+            Gsys = Gk;
+            csys = ck;
+        }
+        if (blockcg && tr) {
+            if (tr->gconj) memcpy(tr->gconj + (long)k * s * s, Gsys, (size_t)s * s * sizeof(double));
+            if (tr->cconj) memcpy(tr->cconj + (long)k * s, csys, (size_t)s * sizeof(double));
+        }
+        if (orc_scale(s, Gsys, csys, d, G, ct) != 0) { breakdown = 1; break; }
         if (opts & ORC_OPT_CHOLESKY) {
             if (orc_cholesky_solve(s, G, ct, at_) != 0) { breakdown = 1; break; }
         } else {
@@ -460,6 +553,10 @@ int orc_sstep_cg_ex(const orc_op *A, const double *Dm, double lmin, double lmax,
             }
             x[i] = x[i] + ax;
             r[i] = r[i] - aw;
+        }
+        if (blockcg) {   /* this block becomes Q', Z' of the next outer */
+            memcpy(Qp, P, (size_t)n * s * sizeof(double));
+            memcpy(Zp, W, (size_t)n * s * sizeof(double));
         }
         if (tr) {
             if (tr->d) memcpy(tr->d + (long)k * s, d, (size_t)s * sizeof(double));
@@ -483,6 +580,9 @@ int orc_sstep_cg_ex(const orc_op *A, const double *Dm, double lmin, double lmax,
     }
     if (tr) { tr->outer = k; tr->converged = converged; tr->breakdown = breakdown; }
     free(D); free(r); free(P); free(W); free(Ghat); free(G); free(c); free(d); free(ct); free(at_); free(al);
+    if (blockcg) {
+        free(Qp); free(Zp); free(Gp); free(Cx); free(Bm); free(e); free(Gk); free(ck); free(colb); free(colx);
+    }
     return breakdown;
 }
 
