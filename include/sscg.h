@@ -276,8 +276,24 @@ SSCG_API sscg_status sscg_estimate_bounds(sscg_ctx *ctx, const double *v0, int32
  *                         PAPER.md:259-266 (||A||: Gershgorin bound, computed
  *                         once), read back with SSCG_INSPECT_KAPPA / _PNORM /
  *                         _BUDGET and stats.budget.  Off the hot path.
+ *   SSCG_OPT_BLOCKCG      0 (default): the restart form x += P~ alpha
+ *                         (PAPER.md:31);  1: block-conjugate s-step CG
+ *                         (R24): each outer block
+ *                         Q_k = P_k - Q_{k-1} B_k is made A-conjugate to the
+ *                         previous one, B_k = G_{k-1}^{-1} (A Q_{k-1})^T P_k;
+ *                         the cross-block entries come from the same single
+ *                         Gram pass and allreduce (over the 2s vectors
+ *                         [P_k | Q_{k-1}]), K4 solves Q_k^T A Q_k a =
+ *                         Q_k^T r_k with the selected Gram solver (pair it
+ *                         with SSCG_GRAM_CHOLESKY: inexact FGS solves break
+ *                         the conjugacy), and the update is x += Q_k alpha,
+ *                         r -= A Q_k alpha.  Needs s <= 32; uses the stored-W
+ *                         schedule and twice the basis storage (reallocated
+ *                         here; the next solve starts a new block sequence).
+ *                         SSCG_INSPECT_GRAM then returns [G_k | c_k] of the
+ *                         conjugated system.
  * Errors: SSCG_ERR_INVALID for an unknown key or value. */
-enum { SSCG_OPT_GRAM_SOLVER = 0, SSCG_OPT_BASIS = 1, SSCG_OPT_DIAGNOSTICS = 2 };
+enum { SSCG_OPT_GRAM_SOLVER = 0, SSCG_OPT_BASIS = 1, SSCG_OPT_DIAGNOSTICS = 2, SSCG_OPT_BLOCKCG = 3 };
 enum { SSCG_GRAM_FGS = 0, SSCG_GRAM_CHOLESKY = 1 };
 enum { SSCG_BASIS_CHEBYSHEV = 0, SSCG_BASIS_MONOMIAL = 1 };
 SSCG_API sscg_status sscg_set_option(sscg_ctx *ctx, int32_t key, int32_t value);

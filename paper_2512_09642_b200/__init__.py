@@ -30,7 +30,7 @@ OP_STENCIL5_2D, OP_STENCIL7, OP_STENCIL27, OP_VARCOEF7, OP_CSR = range(5)
 (INSPECT_P, INSPECT_W, INSPECT_GRAM, INSPECT_D, INSPECT_ALPHA_T, INSPECT_ALPHA, INSPECT_DELTA, INSPECT_LNORM,
  INSPECT_KAPPA, INSPECT_PNORM, INSPECT_BUDGET) = range(11)
 SOLVE_X0_ZERO = 1
-OPT_GRAM_SOLVER, OPT_BASIS, OPT_DIAGNOSTICS = 0, 1, 2
+OPT_GRAM_SOLVER, OPT_BASIS, OPT_DIAGNOSTICS, OPT_BLOCKCG = 0, 1, 2, 3
 GRAM_FGS, GRAM_CHOLESKY = 0, 1
 BASIS_CHEBYSHEV, BASIS_MONOMIAL = 0, 1
 QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS, QUERY_UPDATE_VECTORS, QUERY_GRAM_VECTORS = 0, 1, 2, 3
@@ -213,7 +213,7 @@ class Solver:
 
     def __init__(self, op, lmin: float, lmax: float, s: int, nu: int, diag_M=None, rank: int = 0,
                  nranks: int = 1, slabs_per_rank: int = 1, nccl_id: bytes | None = None, stream=None,
-                 gram_solver: str = "fgs", basis: str = "chebyshev"):
+                 gram_solver: str = "fgs", basis: str = "chebyshev", block: bool = False):
         """lmin = lmax = 0 creates the context without spectral bounds (set
         them with set_bounds, e.g. from estimate_bounds)."""
         L = load()
@@ -234,6 +234,8 @@ class Solver:
             self.set_option(OPT_GRAM_SOLVER, {"fgs": GRAM_FGS, "cholesky": GRAM_CHOLESKY}[gram_solver])
         if basis != "chebyshev":
             self.set_option(OPT_BASIS, {"chebyshev": BASIS_CHEBYSHEV, "monomial": BASIS_MONOMIAL}[basis])
+        if block:
+            self.set_option(OPT_BLOCKCG, 1)
 
     def query(self, what: int) -> int:
         v = C.c_int64()

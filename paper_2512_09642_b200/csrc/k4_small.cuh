@@ -54,7 +54,7 @@ __device__ __forceinline__ void k4_fgs_small(const K4Args &a, DevState *st, doub
         for (int q = lane; q < nent; q += 32) a.h_gram[(int64_t)k * nent + q] = Bs[q];
     const double *Gh = Bs, *c = Bs + s * s;
 
-    const double rn = sqrt(c[0]);
+    const double rn = sqrt(a.rn2 ? __ldcg(a.rn2) : c[0]);
     const double r0 = (k == 0) ? rn : S.r0norm;
     if (lane == 0) {
         if (k == 0) st->r0norm = rn;

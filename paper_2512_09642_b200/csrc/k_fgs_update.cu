@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(32) k4_fgs_big(K4Args a, DevState *st)
         for (int q = lane; q < nent; q += 32) a.h_gram[(int64_t)k * nent + q] = a.blk[q];
     const double *Gh = a.blk, *c = Gh + s * s;
 
-    const double rn = sqrt(c[0]);
+    const double rn = sqrt(a.rn2 ? *a.rn2 : c[0]);
     const double r0 = (k == 0) ? rn : st->r0norm;
     if (lane == 0) {
         if (k == 0) st->r0norm = rn;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(32) k4_chol(K4Args a, DevState *st)
     const bool rec = k < st->hist_cap, recg = k < st->gram_cap;
     if (recg)
         for (int q = lane; q < nent; q += 32) a.h_gram[(int64_t)k * nent + q] = a.blk[q];
-    const double rn = sqrt(c[0]);
+    const double rn = sqrt(a.rn2 ? *a.rn2 : c[0]);
     const double r0 = (k == 0) ? rn : st->r0norm;
     if (lane == 0) {
         if (k == 0) st->r0norm = rn;

@@ -65,6 +65,10 @@ struct sscg_ctx {
     std::vector<Slab> slabs;
     std::vector<void *> allocs;
     double *blk = nullptr;            // final [Ghat | c]
+    int nvec = 0;                     // vectors of P and W per slab (s; 2s in the block-conjugate mode)
+    bool blockcg = false;             // block-conjugate s-step CG (SSCG_OPT_BLOCKCG, R24)
+    double *blk2 = nullptr;           // block mode: [G_k | c_k], the conjugated system K4 solves
+    double *bmat = nullptr;           // block mode: B_k (s x s)
     double **blkptrs = nullptr;       // device array of slab block pointers
     double *alpha = nullptr;
     DevState *st = nullptr;
@@ -213,6 +217,82 @@ __global__ void k_csr_dinv(Geo g, double *dinv)
     dinv[g.plane + r] = 1.0 / d;
 }
 
+static void dfree(sscg_ctx *c, void *p);
+
+// (Re)build the basis store of every slab: P and W with nvec vectors (s; 2s in
+// the block-conjugate mode, whose upper halves hold Q_{k-1} and A Q_{k-1}) and
+// every tensor map over them.  Device work is ordered on the solver stream.
+static sscg_status build_basis_store(sscg_ctx *c, int nvec)
+{
+    Geo &g = c->g;
+    const int s = c->s;
+    for (auto &sl : c->slabs) {
+        if (sl.Palloc) {
+            CU(cudaStreamSynchronize(c->stream));
+            dfree(c, sl.Palloc);
+            dfree(c, sl.Walloc);
+        }
+        TRY(dalloc(c, &sl.Palloc, (size_t)g.vstride * nvec));
+        TRY(dalloc(c, &sl.Walloc, (size_t)g.vstride * nvec));
+        CU(cudaMemsetAsync(sl.Palloc, 0, (size_t)g.vstride * nvec * sizeof(double), c->stream));
+        CU(cudaMemsetAsync(sl.Walloc, 0, (size_t)g.vstride * nvec * sizeof(double), c->stream));
+        sl.P = sl.Palloc + (int64_t)g.guard * g.plane;   // vectors address plane 0; planes -guard.. lie before it
+        sl.W = sl.Walloc + (int64_t)g.guard * g.plane;
+        // the stored-W Gram pass runs over all nvec rows ([P | Q'] x [W | Z'] in the block mode)
+        if (!k2_prepare(g, sl, nvec)) return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the Gram pass");
+        const int kind = g.kind;
+        if (kind == SSCG_OP_STENCIL7 || kind == SSCG_OP_STENCIL27 || kind == SSCG_OP_VARCOEF7) {
+            if (!k1t_prepare(g, sl.P, sl.nzl, s, &sl.tmP4, &sl.tmM4))
+                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the basis step");
+            sl.has_k1t = true;
+        }
+        if (sl.want_k1f) {
+            if (!k1f_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
+                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused basis step");
+            sl.has_k1f = true;
+        }
+        if (sl.want_k1m) {
+            if (!k1m_prepare(g, sl.P, sl.nzl, s, &sl.tmM3_P, &sl.tmM3_M, g.guard))
+                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the depth-3 basis step");
+            sl.has_k1m = true;
+        }
+        if (sl.want_k1fv) {
+            if (!k1fv_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
+                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused variable-coefficient step");
+            sl.has_k1f = true;
+        }
+        if (kind == SSCG_OP_STENCIL7 || kind == SSCG_OP_STENCIL27 || kind == SSCG_OP_VARCOEF7) {
+            if (!k2r_prepare(g, sl, s)) return fail(SSCG_ERR_CUDA, "tensor maps for the recovered-W Gram pass");
+            sl.has_k2r = true;
+        }
+    }
+    c->nvec = nvec;
+    return SSCG_OK;
+}
+
+// Gram-pass partials and blocks for `rows` basis rows (rows^2 + rows entries)
+static sscg_status alloc_gram_buffers(sscg_ctx *c, int rows)
+{
+    const int nent = rows * rows + rows;
+    const int64_t npart = (int64_t)k2_grid() * 8 * nent;
+    CU(cudaStreamSynchronize(c->stream));
+    for (auto &sl : c->slabs) {
+        dfree(c, sl.part);
+        dfree(c, sl.blk);
+        TRY(dalloc(c, &sl.part, (size_t)npart));
+        TRY(dalloc(c, &sl.blk, (size_t)nent));
+    }
+    dfree(c, c->blk);
+    TRY(dalloc(c, &c->blk, (size_t)nent));
+    std::vector<double *> ptrs;
+    for (auto &sl : c->slabs) ptrs.push_back(sl.blk);
+    dfree(c, c->blkptrs);
+    TRY(dalloc(c, &c->blkptrs, ptrs.size()));
+    CU(cudaMemcpyAsync(c->blkptrs, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return SSCG_OK;
+}
+
 Knobs sscg::read_knobs()
 {
     Knobs k;
@@ -352,48 +432,19 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
     g.guard = (A->kind == SSCG_OP_STENCIL7 && !diag_M && S > 1 && g.kn.deep_halo) ? 2 : 0;
     g.vstride = ((int64_t)(max_nzl + 2 + 2 * g.guard) * g.plane + 31) / 32 * 32;   // 256-B aligned vectors
     if (getenv("SSCG_VPAD") && (g.vstride / 32) % 2 == 0) g.vstride += 32;   // odd multiple of 256 B
-    const int nent = s * s + s;
-    const int64_t npart = (int64_t)k2_grid() * 8 * nent;
     for (auto &sl : c->slabs) {
-        TRY(dalloc(c, &sl.P, (size_t)g.vstride * s));
-        TRY(dalloc(c, &sl.W, (size_t)g.vstride * s));
-        CU(cudaMemsetAsync(sl.P, 0, (size_t)g.vstride * s * sizeof(double), c->stream));
-        CU(cudaMemsetAsync(sl.W, 0, (size_t)g.vstride * s * sizeof(double), c->stream));
-        sl.P += (int64_t)g.guard * g.plane;   // vectors address plane 0; planes -guard.. lie before it
-        sl.W += (int64_t)g.guard * g.plane;
-        TRY(dalloc(c, &sl.part, (size_t)npart));
-        TRY(dalloc(c, &sl.blk, (size_t)nent));
-        TRY(dalloc(c, &sl.ticket, 1));
-        CU(cudaMemsetAsync(sl.ticket, 0, sizeof(unsigned), c->stream));
-        if (!k2_prepare(g, sl, s)) return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the Gram pass");
-        if (A->kind == SSCG_OP_STENCIL7 || A->kind == SSCG_OP_STENCIL27 || A->kind == SSCG_OP_VARCOEF7) {
-            if (!k1t_prepare(g, sl.P, sl.nzl, s, &sl.tmP4, &sl.tmM4))
-                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the basis step");
-            sl.has_k1t = true;
-        }
-        if ((A->kind == SSCG_OP_STENCIL7 || A->kind == SSCG_OP_STENCIL27) && !diag_M && k1f_enabled(g, sl.nzl)) {
-            if (!k1f_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
-                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused basis step");
-            sl.has_k1f = true;
-        }
-        if (A->kind == SSCG_OP_STENCIL7 && !diag_M && k1m_enabled(g, sl.nzl)) {
-            if (!k1m_prepare(g, sl.P, sl.nzl, s, &sl.tmM3_P, &sl.tmM3_M, g.guard))
-                return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the depth-3 basis step");
-            sl.has_k1m = true;
-        }
         if (A->kind == SSCG_OP_VARCOEF7) {
             sl.kx = A->kx + sl.zoff * g.ny * (g.nx + 1);
             sl.ky = A->ky + sl.zoff * (g.ny + 1) * g.nx;
             sl.kz = A->kz + sl.zoff * g.ny * g.nx;
             sl.has_ftma = g.kn.faces_tma &&
                           k1t_prepare_faces(g, sl.kx, sl.ky, sl.kz, sl.nzl, &sl.tmKX, &sl.tmKY, &sl.tmKZ);
-            if (!diag_M && k1fv_enabled(g, sl.nzl) &&
-                k1fv_prepare_faces(g, sl.kx, sl.ky, sl.kz, sl.nzl, &sl.tmV_KX, &sl.tmV_KY, &sl.tmV_KZ, &sl.kx_shift)) {
-                if (!k1fv_prepare(g, sl.P, sl.nzl, s, &sl.tmF_P, &sl.tmF_M))
-                    return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused variable-coefficient step");
-                sl.has_k1f = true;
-            }
+            sl.want_k1fv = !diag_M && k1fv_enabled(g, sl.nzl) &&
+                           k1fv_prepare_faces(g, sl.kx, sl.ky, sl.kz, sl.nzl, &sl.tmV_KX, &sl.tmV_KY, &sl.tmV_KZ,
+                                              &sl.kx_shift);
         }
+        sl.want_k1f = (A->kind == SSCG_OP_STENCIL7 || A->kind == SSCG_OP_STENCIL27) && !diag_M && k1f_enabled(g, sl.nzl);
+        sl.want_k1m = A->kind == SSCG_OP_STENCIL7 && !diag_M && k1m_enabled(g, sl.nzl);
         if (diag_M || A->kind == SSCG_OP_CSR) {
             double *dv = nullptr;
             TRY(dalloc(c, &dv, (size_t)g.vstride));
@@ -418,22 +469,14 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
             CU(cudaGetLastError());
             sl.dvec = dd;
         }
-        if (A->kind == SSCG_OP_STENCIL7 || A->kind == SSCG_OP_STENCIL27 || A->kind == SSCG_OP_VARCOEF7) {
-            if (!k2r_prepare(g, sl, s)) return fail(SSCG_ERR_CUDA, "tensor maps for the recovered-W Gram pass");
-            sl.has_k2r = true;
-        }
+        TRY(dalloc(c, &sl.ticket, 1));
+        CU(cudaMemsetAsync(sl.ticket, 0, sizeof(unsigned), c->stream));
     }
-    TRY(dalloc(c, &c->blk, (size_t)nent));
+    TRY(build_basis_store(c, s));
+    TRY(alloc_gram_buffers(c, s));
     TRY(dalloc(c, &c->xdev, 1));
     CU(cudaMallocHost(&c->xhost, sizeof(double *)));
     TRY(dalloc(c, &c->alpha, 64));
-    {
-        std::vector<double *> ptrs;
-        for (auto &sl : c->slabs) ptrs.push_back(sl.blk);
-        TRY(dalloc(c, &c->blkptrs, ptrs.size()));
-        CU(cudaMemcpyAsync(c->blkptrs, ptrs.data(), ptrs.size() * sizeof(double *), cudaMemcpyHostToDevice,
-                           c->stream));
-    }
     TRY(dalloc(c, &c->scratch, (size_t)c->n_local));
     if (c->nranks > 1) {
         // interior K1 launches leave two SMs free so the NCCL send/recv kernels
@@ -676,7 +719,7 @@ static sscg_status halo_join(sscg_ctx *c)
 static bool uses_rec_update(const sscg_ctx *c)
 {
     const Geo &g = c->g;
-    if (!g.kn.k5_recur) return false;
+    if (!g.kn.k5_recur || c->blockcg) return false;
     if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2 || g.kind == SSCG_OP_CSR || g.pitch != g.nx) return false;
     for (const auto &sl : c->slabs)
         if (!sl.dvec && !(g.center > 0.0 && !sl.dinv)) return false;   // need m or diag(M) per point
@@ -688,7 +731,7 @@ static bool uses_rec_update(const sscg_ctx *c)
 // and the basis is Chebyshev (SSCG_WFREE=0 keeps the stored-W schedule)
 static bool uses_wfree(const sscg_ctx *c)
 {
-    if (!c->g.kn.wfree) return false;
+    if (!c->g.kn.wfree || c->blockcg) return false;
     if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2) return false;
     for (const auto &sl : c->slabs)
         if (!sl.has_k2r || !sl.has_k1t) return false;
@@ -991,29 +1034,39 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     a4.pdl = g.kn.pdl;
     a4.h_gram = c->h_gram; a4.h_d = c->h_d; a4.h_at = c->h_at; a4.h_al = c->h_al;
     a4.h_delta = c->h_delta; a4.h_relres = c->h_relres; a4.h_lnorm = c->h_lnorm;
+    // block-conjugate mode: the Gram pass runs over the 2s rows [P_k | Q'] x [W_k | Z']
+    const int rows = c->blockcg ? 2 * s : s, nent = rows * rows + rows;
     for (auto &sl : c->slabs) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
         if (wfree) launch_k2r(g, sl, s, c->theta, c->sigma, c->st, L == 1 ? c->blk : sl.blk, c->stream);
-        else launch_k2(g, sl, s, c->st, L == 1 ? c->blk : sl.blk, c->stream);
+        else launch_k2(g, sl, rows, c->st, L == 1 ? c->blk : sl.blk, c->stream);
         TRY(prof_mark(c, SSCG_PROF_GRAM, false));
         ++c->launches;
     }
     if (L > 1) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
-        launch_slab_sum(c->blkptrs, L, s * s + s, c->blk, c->st, c->stream);
+        launch_slab_sum(c->blkptrs, L, nent, c->blk, c->st, c->stream);
         TRY(prof_mark(c, SSCG_PROF_GRAM, false));
         ++c->launches;
     }
-    if (c->comm) {   // ranks (or the SSCG_NCCL_SELF test mode)
+    if (c->comm) {   // ranks (or the SSCG_NCCL_SELF test mode): the one allreduce of the outer iteration
         TRY(prof_mark(c, SSCG_PROF_ALLREDUCE, true));
-        NC(ncclAllReduce(c->blk, c->blk, (size_t)(s * s + s), ncclDouble, ncclSum, c->comm, c->stream));
+        NC(ncclAllReduce(c->blk, c->blk, (size_t)nent, ncclDouble, ncclSum, c->comm, c->stream));
         TRY(prof_mark(c, SSCG_PROF_ALLREDUCE, false));
         ++c->allreduces;
+    }
+    if (c->blockcg) {   // B_k, then K4 on the conjugated system; the stopping test reads ||r_k||^2 of the raw block
+        TRY(prof_mark(c, SSCG_PROF_FGS, true));
+        launch_bcg_prep(c->blk, s, c->blk2, c->bmat, c->st, g.kn.pdl, c->stream);
+        TRY(prof_mark(c, SSCG_PROF_FGS, false));
+        ++c->launches;
+        a4.blk = c->blk2;
+        a4.rn2 = c->blk + (int64_t)rows * rows;
     }
     TRY(prof_mark(c, SSCG_PROF_FGS, true));
     launch_k4(a4, c->st, c->stream);
     if (c->diagnostics) {
-        launch_kappa(c->blk, s, c->st, c->h_kappa, c->stream);
+        launch_kappa(a4.blk, s, c->st, c->h_kappa, c->stream);
         ++c->launches;
         for (int l = 0; l < L; ++l) {   // ||P_k||_F before K5 overwrites p_0
             launch_pnorm(g, c->slabs[l], s, c->diag_part + (size_t)l * DIAG_BLK, DIAG_BLK, c->st, c->stream);
@@ -1036,8 +1089,12 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
             const int b = std::max(zb, 1);
             if (e <= b) continue;
             TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
-            launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, b, e, c->theta,
-                      c->sigma, uses_rec_update(c));
+            if (c->blockcg)
+                launch_k5_block(g, sl, s, c->alpha, c->bmat, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream,
+                                b, e);
+            else
+                launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, b, e,
+                          c->theta, c->sigma, uses_rec_update(c));
             TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
             ++c->launches;
         }
@@ -1047,7 +1104,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const int np0 = deep ? 3 : 1;
     if (!halo) {
         TRY(k5(1, -1));
-    } else if (!ovl || (deep && !g.kn.deep_overlap)) {
+    } else if (!ovl || (deep && !g.kn.deep_overlap) || c->blockcg) {
         TRY(k5(1, -1));
         TRY(halo_fork(c, 0, false, np0));
     } else {
@@ -1492,6 +1549,22 @@ extern "C" sscg_status sscg_set_option(sscg_ctx *c, int32_t key, int32_t value)
         if (value != SSCG_BASIS_CHEBYSHEV && value != SSCG_BASIS_MONOMIAL) return fail(SSCG_ERR_INVALID, "bad basis %d", value);
         c->basis = value;
         break;
+    case SSCG_OPT_BLOCKCG:
+        if (value != 0 && value != 1) return fail(SSCG_ERR_INVALID, "bad block-conjugate flag %d", value);
+        if (value == 1 && c->s > 32) return fail(SSCG_ERR_INVALID, "block-conjugate mode needs s <= 32 (s = %d)", c->s);
+        if ((value == 1) != c->blockcg) {
+            // the store holds [P | Q'] and [W | Z'] (2s vectors) in the block mode
+            drop_graph(c);
+            TRY(build_basis_store(c, value ? 2 * c->s : c->s));
+            TRY(alloc_gram_buffers(c, value ? 2 * c->s : c->s));
+            if (value && !c->blk2) {
+                TRY(dalloc(c, &c->blk2, (size_t)c->s * c->s + c->s));
+                TRY(dalloc(c, &c->bmat, (size_t)c->s * c->s));
+            }
+            c->blockcg = value == 1;
+            c->solved = false;
+        }
+        break;
     default:
         return fail(SSCG_ERR_INVALID, "unknown option %d", key);
     }
@@ -1644,13 +1717,16 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
         return SSCG_OK;
     }
     case SSCG_QUERY_GRAM_VECTORS:
-        // stored W: P and W (2s); recovered W: P, w_{s-1} and diag(M) when it varies
-        *out = uses_wfree(c) ? (int64_t)s + 1 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s;
+        // stored W: P and W (2s); recovered W: P, w_{s-1} and diag(M) when it varies;
+        // block-conjugate: [P | Q'] and [W | Z'] (4s)
+        *out = c->blockcg ? 4 * (int64_t)s : uses_wfree(c) ? (int64_t)s + 1 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s;
         return SSCG_OK;
     case SSCG_QUERY_UPDATE_VECTORS:
         // P (s) + x in, x + r out; the stored-W form also reads W (s), the
         // recurrence form only w_{s-1}
-        *out = uses_rec_update(c) ? (int64_t)s + 4 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s + 3;
+        // block-conjugate: P, W, Q', Z', x in; Q, Z, x, r out
+        *out = c->blockcg ? 6 * (int64_t)s + 3 :
+               uses_rec_update(c) ? (int64_t)s + 4 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s + 3;
         return SSCG_OK;
     default:
         return fail(SSCG_ERR_INVALID, "unknown query %d", what);

@@ -75,8 +75,10 @@ struct Slab {
     int nzl;           // interior planes
     int has_lo, has_hi;   // a neighbour slab (this or another rank) below / above
     int64_t zoff;      // first plane relative to the process-local range
-    double *P;         // s vectors, stride vstride
-    double *W;         // s vectors, stride vstride
+    double *P;         // s vectors, stride vstride (2s in the block-conjugate mode: [P_k | Q_{k-1}])
+    double *W;         // s vectors, stride vstride (2s: [W_k | Z_{k-1} = A Q_{k-1}])
+    double *Palloc, *Walloc;      // the allocations (P, W start Geo::guard planes in)
+    bool want_k1f, want_k1m, want_k1fv;   // basis kernels whose tensor maps the store needs
     double *part;      // Gram partials [grid][nent]
     double *blk;       // this slab's reduced block (s*s + s)
     unsigned *ticket;  // last-CTA counter for K2
@@ -244,6 +246,8 @@ struct K4Args {
     int s, nu;
     int solver;            // 0 = nu FGS sweeps, 1 = dense Cholesky
     int pdl;               // launch with programmatic dependent launch (Knobs::pdl)
+    const double *rn2;     // ||r_k||^2 for the stopping test, or nullptr: c_0 of blk (the block-conjugate
+                           // mode solves Q_k^T A Q_k a = Q_k^T r_k, whose c_0 is not ||r_k||^2)
     double *h_gram, *h_d, *h_at, *h_al, *h_delta, *h_relres;  // history [cap][...]
     double *h_lnorm;       // ||L||_F of the scaled Gram matrix G = I + L + L^T per outer
 };
@@ -262,6 +266,11 @@ void launch_anorm(const Geo &g, const Slab &sl, double *bmax, int nblk, cudaStre
 //   rec: form W alpha from the Chebyshev recurrence (constant diagonal, vector path only)
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *const *xpp, int64_t xoff,
                const DevState *st, cudaStream_t stream, int zb, int ze, double theta, double sigma, bool rec);
+
+// block-conjugate s-step CG (k_blockcg.cu, R24)
+void launch_bcg_prep(const double *big, int s, double *blk2, double *Bm, DevState *st, bool pdl, cudaStream_t strm);
+void launch_k5_block(const Geo &g, const Slab &sl, int s, const double *alpha, const double *B, double *const *xpp,
+                     int64_t xoff, const DevState *st, cudaStream_t stream, int zb, int ze);
 
 // Lanczos spectral bounds (k_lanczos.cu)
 int lz_grid();
