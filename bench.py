@@ -415,16 +415,21 @@ def run_ours(a):
     if a.kind == "varcoef7":   # kx, ky, kz of this slab, read by every basis step
         face_bytes = 8.0 * (n * (n + 1) * S.nz_local * 2 + n * n * (S.nz_local + 1))
     basis_vecs = S.query(sscg.QUERY_BASIS_VECTORS)       # (4s-3) single steps, fewer with pairs / triples
+    single_vecs = S.query(sscg.QUERY_BASIS_SINGLE_VECTORS)   # the single steps of a fused schedule (j = s-1)
     depth = S.query(sscg.QUERY_BASIS_FUSED)               # basis steps per launch: 1, 2 (K1F) or 3 (K1M)
     fused = depth > 1
     upd_vecs = S.query(sscg.QUERY_UPDATE_VECTORS)        # 2s+3, or s+4 with W alpha from the recurrence
     gram_vecs = S.query(sscg.QUERY_GRAM_VECTORS)         # 2s, or s+1 with W recovered from the recurrence
     face_passes = s if depth == 1 else (s + 1) // 2   # fused pairs read the faces once per pair
-    bytes_per_outer = {"basis": basis_vecs * vec + face_passes * face_bytes, "gram": gram_vecs * vec,
-                       "update": upd_vecs * vec}
+    # "basis": the fused basis launches (K1M triples / K1F pairs) -- the dominant
+    # kernel; "basis_single": the single steps around them (the last step j = s-1)
+    bytes_per_outer = {"basis": (basis_vecs - single_vecs) * vec + face_passes * face_bytes,
+                       "basis_single": single_vecs * vec, "gram": gram_vecs * vec, "update": upd_vecs * vec}
     kern = {}
     for k, byt in bytes_per_outer.items():
         t_ms, cnt = prof[k]
+        if cnt == 0:
+            continue
         per_launch = byt * a.steps / max(cnt, 1)
         gbs = per_launch / (t_ms / max(cnt, 1) / 1e3) / 1e9 if t_ms > 0 else None
         kern[k] = {"launches": cnt, "ms_per_launch": t_ms / max(cnt, 1), "bytes_per_launch": per_launch,
@@ -450,10 +455,10 @@ def run_ours(a):
             "traffic": ncu_traffic(n, k1_name) if a.workload == "cfg5" else None, "peak_source": peak_src,
             "traffic_note": "ncu dram read+write of one interior launch (algorithmic: %d vectors = %.4g B)"
                             % (sum(mixrw), sum(mixrw) * vec),
-            "bytes_rule": "%d FP64 vectors per outer (%s) + s face sets for varcoef7, / basis launches (SURVEY 8(d)); "
-                          "path: basis + %d (Gram) + %d (update) vectors"
-                          % (basis_vecs, {3: "K1M triples", 2: "K1F pairs"}.get(depth, "single steps"), gram_vecs,
-                             upd_vecs),
+            "bytes_rule": "%d FP64 vectors per outer in the %s (+ s face sets for varcoef7), / their launches; "
+                          "path: + %d (single basis steps) + %d (Gram) + %d (update) vectors"
+                          % (basis_vecs - single_vecs, {3: "K1M triples", 2: "K1F pairs"}.get(depth, "single steps"),
+                             single_vecs, gram_vecs, upd_vecs),
             "mix": "%d reads : %d writes per launch" % mixrw,
             "mix_ceiling_gbs": mc[0], "mix_ceiling_source": mc[1],
             "frac_of_mix_ceiling": (k1["achieved_gbs"] / mc[0]) if (mc[0] and k1["achieved_gbs"]) else None,
@@ -467,6 +472,8 @@ def run_ours(a):
     t_outer = st.ms_total / a.steps / 1e3
     c8_basis = (4 * s - 3) * vec + s * face_bytes
     c8 = {"basis": c8_basis, "gram": 2 * s * vec, "update": (2 * s + 3) * vec}
+    # 8(d)'s per-launch K1 bytes for the dominant kernel: 4 vectors per basis step it runs
+    c8_k1 = 4 * depth * vec
     roof["contracts"] = {
         "schedule": {"vectors_per_outer": {"basis": basis_vecs, "gram": gram_vecs, "update": upd_vecs},
                      "bytes_per_outer": path_bytes, "achieved_gbs": path_bytes / t_outer / 1e9,
@@ -475,8 +482,8 @@ def run_ours(a):
         "survey_8d": {"vectors_per_outer": {"basis": 4 * s - 3, "gram": 2 * s, "update": 2 * s + 3},
                       "bytes_per_outer": sum(c8.values()), "achieved_gbs": sum(c8.values()) / t_outer / 1e9,
                       "frac": sum(c8.values()) / t_outer / 1e9 / peak,
-                      "dominant_kernel_frac": (c8_basis * a.steps / max(k1["launches"], 1)) /
-                                              (k1["ms_per_launch"] / 1e3) / 1e9 / peak if k1["ms_per_launch"] else None,
+                      "dominant_kernel_frac": c8_k1 / (k1["ms_per_launch"] / 1e3) / 1e9 / peak
+                                              if k1["ms_per_launch"] else None,
                       "note": "SURVEY 8(d) counts as written (stored W, single basis steps); the kernels move the "
                               "schedule's vectors, so this 'fraction' is not a physical bandwidth (> 1 possible)"}}
     if a.kind == "5pt":

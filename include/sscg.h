@@ -178,9 +178,13 @@ SSCG_API sscg_status sscg_solve_host(sscg_ctx *ctx, const double *b_host, double
 SSCG_API sscg_status sscg_iterate(sscg_ctx *ctx, double *x, int32_t nsteps);
 
 /* Per-kernel device time: with profiling on, every launch group is bracketed
- * by CUDA events on the solver stream and accumulated per category. */
+ * by CUDA events on the solver stream and accumulated per category.  When the
+ * schedule runs fused basis kernels (K1M triples / K1F pairs), SSCG_PROF_BASIS
+ * counts those and SSCG_PROF_BASIS_SINGLE the single basis steps around them
+ * (the last step j = s-1, boundary planes); otherwise every basis launch is
+ * SSCG_PROF_BASIS. */
 enum { SSCG_PROF_BASIS = 0, SSCG_PROF_GRAM = 1, SSCG_PROF_ALLREDUCE = 2, SSCG_PROF_FGS = 3,
-       SSCG_PROF_UPDATE = 4, SSCG_PROF_HALO = 5, SSCG_PROF_N = 6 };
+       SSCG_PROF_UPDATE = 4, SSCG_PROF_HALO = 5, SSCG_PROF_BASIS_SINGLE = 6, SSCG_PROF_N = 7 };
 typedef struct {
     double ms[SSCG_PROF_N];          /* accumulated device milliseconds           */
     int64_t launches[SSCG_PROF_N];   /* events pairs (= launches, or NCCL groups)  */
@@ -314,10 +318,13 @@ SSCG_API sscg_status sscg_set_option(sscg_ctx *ctx, int32_t key, int32_t value);
  *   SSCG_QUERY_GRAM_VECTORS   FP64 vectors the Gram pass reads per outer
  *                             iteration: 2s (P and the stored W = AP), or s+1
  *                             (+1 for a varying diagonal) when W is recovered
- *                             from the basis recurrence (R23)
+ *                             from the basis recurrence (R23);
+ *                             4s in the block-conjugate mode
+ *   SSCG_QUERY_BASIS_SINGLE_VECTORS  the part of BASIS_VECTORS moved by the
+ *                             single steps of a fused schedule (0 without)
  * Errors: SSCG_ERR_INVALID. */
 enum { SSCG_QUERY_BASIS_FUSED = 0, SSCG_QUERY_BASIS_VECTORS = 1, SSCG_QUERY_UPDATE_VECTORS = 2,
-       SSCG_QUERY_GRAM_VECTORS = 3 };
+       SSCG_QUERY_GRAM_VECTORS = 3, SSCG_QUERY_BASIS_SINGLE_VECTORS = 4 };
 SSCG_API sscg_status sscg_query(const sscg_ctx *ctx, int32_t what, int64_t *out);
 
 SSCG_API void sscg_destroy(sscg_ctx *ctx);

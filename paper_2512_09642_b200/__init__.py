@@ -33,12 +33,12 @@ SOLVE_X0_ZERO = 1
 OPT_GRAM_SOLVER, OPT_BASIS, OPT_DIAGNOSTICS, OPT_BLOCKCG = 0, 1, 2, 3
 GRAM_FGS, GRAM_CHOLESKY = 0, 1
 BASIS_CHEBYSHEV, BASIS_MONOMIAL = 0, 1
-QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS, QUERY_UPDATE_VECTORS, QUERY_GRAM_VECTORS = 0, 1, 2, 3
+QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS, QUERY_UPDATE_VECTORS, QUERY_GRAM_VECTORS, QUERY_BASIS_SINGLE_VECTORS = 0, 1, 2, 3, 4
 
 EXPORTS = ["sscg_partition", "sscg_halo_plan", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host", "sscg_iterate",
            "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect", "sscg_local_shape", "sscg_destroy",
            "sscg_last_error", "sscg_version", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds", "sscg_query"]
-PROF_NAMES = ["basis", "gram", "allreduce", "fgs", "update", "halo"]
+PROF_NAMES = ["basis", "gram", "allreduce", "fgs", "update", "halo", "basis_single"]
 
 
 class SSCGError(RuntimeError):
@@ -67,7 +67,7 @@ class _Stats(C.Structure):
 
 
 class _Profile(C.Structure):
-    _fields_ = [("ms", C.c_double * 6), ("launches", C.c_int64 * 6)]
+    _fields_ = [("ms", C.c_double * 7), ("launches", C.c_int64 * 7)]
 
 
 _lib = None

@@ -738,6 +738,9 @@ static bool uses_wfree(const sscg_ctx *c)
     return uses_rec_update(c);   // the update must not need the stored W either
 }
 
+static bool uses_mp3(const sscg_ctx *c);
+static bool uses_fused(const sscg_ctx *c);
+
 // K1 for step j over the planes of every local slab selected by `part`:
 //   0 = all planes, 1 = the two boundary planes (1 and nzl), 2 = the interior
 //   planes [2, nzl) that do not read a halo plane, 3 = the two planes next to
@@ -788,9 +791,10 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
             a.sm_cap = c->k1_sm_cap;
             if (a.ze <= a.zb) continue;
         }
-        TRY(prof_mark(c, SSCG_PROF_BASIS, true));
+        const int cat = (uses_mp3(c) || uses_fused(c)) ? SSCG_PROF_BASIS_SINGLE : SSCG_PROF_BASIS;
+        TRY(prof_mark(c, cat, true));
         launch_k1(g, a, c->st, c->stream);
-        TRY(prof_mark(c, SSCG_PROF_BASIS, false));
+        TRY(prof_mark(c, cat, false));
         ++c->launches;
     }
     return SSCG_OK;
@@ -1692,28 +1696,30 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
     case SSCG_QUERY_BASIS_FUSED:   // basis steps per launch of the schedule's main kernel
         *out = uses_mp3(c) ? 3 : uses_fused(c) ? 2 : 1;
         return SSCG_OK;
-    case SSCG_QUERY_BASIS_VECTORS: {
+    case SSCG_QUERY_BASIS_VECTORS:
+    case SSCG_QUERY_BASIS_SINGLE_VECTORS: {
         // FP64 vectors of n_local read + written by the basis steps of one outer
+        // (_SINGLE: by the single steps of a fused schedule, the SSCG_PROF_BASIS_SINGLE launches)
         const bool wf = uses_wfree(c);
         auto wst = [&](int j) { return (!wf || j == s - 1) ? 1 : 0; };   // w_j stored?
-        int64_t v = 0;
+        int64_t v = 0, v1 = 0;
         if (uses_mp3(c)) {
             int j = 0;
             for (; j + 2 < s; j += 3)   // p_j, p_{j-1} in; p_{j+1..j+3} and stored w out
                 v += 1 + (j > 0) + (j + 1 < s) + (j + 2 < s) + (j + 3 < s) + wst(j) + wst(j + 1) + wst(j + 2);
             if (j + 1 < s) { v += 1 + (j > 0) + 1 + (j + 2 < s) + wst(j) + wst(j + 1); j += 2; }   // a K1F pair
-            if (j < s) v += 1 + (j > 0 && j < s - 1) + wst(j) + (j < s - 1);                       // a single step
+            if (j < s) v1 += 1 + (j > 0 && j < s - 1) + wst(j) + (j < s - 1);                      // a single step
         } else if (uses_fused(c)) {
             int j = 0;
             for (; j + 1 < s; j += 2) v += 1 + (j > 0) + 1 + (j + 2 < s) + wst(j) + wst(j + 1);
-            if (j < s) v += 2;   // odd s: the last step alone (mode 0: reads p_{s-1}, writes w_{s-1})
+            if (j < s) v1 += 2;   // odd s: the last step alone (mode 0: reads p_{s-1}, writes w_{s-1})
         } else {
             for (int j = 0; j < s; ++j) {
                 const bool pn = j < s - 1, pm = !mono && j > 0 && pn;
                 v += 1 + pm + wst(j) + pn;
             }
         }
-        *out = v;
+        *out = (what == SSCG_QUERY_BASIS_VECTORS) ? v + v1 : v1;
         return SSCG_OK;
     }
     case SSCG_QUERY_GRAM_VECTORS:
