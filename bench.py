@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--cpu-planes", type=int, default=16, help="z-planes of the oracle's CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gram-solver", default="fgs", choices=["fgs", "cholesky"],
+                    help="K4: nu FGS sweeps (the paper's method, default) or the exact Cholesky solve (NEXT-2)")
+    ap.add_argument("--block", action="store_true",
+                    help="block-conjugate s-step CG (NEXT-2, DESIGN.md R24) instead of the restart form")
     a = ap.parse_args()
     w = WORKLOADS[a.workload]
     a.n = w["n"] if a.n is None else a.n
@@ -88,6 +92,8 @@ def workload(a, nranks):
     desc = WORKLOADS[a.workload]["desc"].format(n=n)
     if a.strong:
         desc = desc.replace("per GPU", "global (strong scaling)")
+    if a.block or a.gram_solver != "fgs":
+        desc += "; variant: %s%s" % ("block-conjugate s-step CG, " if a.block else "", a.gram_solver + " Gram solve")
     return {"workload": f"{desc}, s={a.s}, nu={a.nu}, x0=0, b~U[-1,1] seed 42",
             "nx": n, "ny": n, "nz_per_gpu": nzg // nranks, "nz_global": nzg, "s": a.s, "nu": a.nu,
             "n_global": n * n * nzg, "parallelism": f"z-slab x{nranks}",
@@ -367,12 +373,14 @@ def run_ours(a):
         op = sscg.Stencil("varcoef7", n, n, nz, *faces)
     else:
         op = sscg.Stencil(a.kind, n, n, nz)
+    variant = {"gram_solver": a.gram_solver, "block": a.block}
     if twod:
-        S = sscg.Solver(op, *inputs.analytic_bounds(a.kind, n, n), s, nu)
+        S = sscg.Solver(op, *inputs.analytic_bounds(a.kind, n, n), s, nu, **variant)
     elif WORKLOADS[a.workload]["bounds"] == "analytic":
-        S = sscg.Solver(op, *inputs.analytic_bounds(a.kind, n, n, nz), s, nu, rank=rank, nranks=world, nccl_id=nid)
+        S = sscg.Solver(op, *inputs.analytic_bounds(a.kind, n, n, nz), s, nu, rank=rank, nranks=world, nccl_id=nid,
+                        **variant)
     else:   # 50 Lanczos steps on the GPU, widened 5 % (R13), untimed setup
-        S = sscg.Solver(op, 0.0, 0.0, s, nu, rank=rank, nranks=world, nccl_id=nid)
+        S = sscg.Solver(op, 0.0, 0.0, s, nu, rank=rank, nranks=world, nccl_id=nid, **variant)
         S.set_bounds(*S.estimate_bounds(b, 50, 0.05))
     n_local, n_global = S.n_local, n * n * nz * (world if twod else 1)
 

@@ -104,16 +104,51 @@ struct K5BParams {
     int64_t xoff;
 };
 
-// one point per thread (grid-stride): Q' and Z' of the point are loaded before
-// the point's Q_k, Z_k overwrite them
+// one phase of the update at one point: y_j = v_j - sum_m o_m B_mj for the s
+// columns j (v = P_k or W_k, o = Q' or Z' of the point, already in registers),
+// y_j stored over o_j's slot, returns sum_j alpha_j y_j.  Columns in groups of
+// four whose loads are issued together; the restrict pointers tell the
+// compiler the basis loads and the block stores never overlap (they are
+// different vectors), so loads are not held behind earlier stores.
+template <int S>
+__device__ __forceinline__ double bcg_phase(const double *__restrict__ v, double *__restrict__ y, int64_t vs,
+                                            int s, const double (&o)[S], const double *Bsh, const double *al)
+{
+    double acc = 0.0;
+#pragma unroll 1
+    for (int j0 = 0; j0 < s; j0 += 4) {
+        double vj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) vj[u] = (j0 + u < s) ? v[(int64_t)(j0 + u) * vs] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u;
+            double sp = 0.0;
+#pragma unroll
+            for (int m = 0; m < S; ++m) sp = fma(o[m], Bsh[m * S + j], sp);
+            const double yj = vj[u] - sp;
+            if (j < s) {
+                y[(int64_t)j * vs] = yj;
+                acc = fma(al[j], yj, acc);
+            }
+        }
+    }
+    return acc;
+}
+
+// one point per thread (grid-stride): Q' (Z') of the point is loaded before
+// Q_k (Z_k) overwrites it
 template <int S>
 __global__ void __launch_bounds__(256) k5_block(K5BParams k, const DevState *st)
 {
     PDL_ENTRY(st);
-    __shared__ double Bsh[S * S], al[S];
+    __shared__ double Bsh[S * (S + 4)], al[S + 4];   // padded: groups of four columns past s read zeros
     const int s = k.s;
-    for (int q = threadIdx.x; q < s * s; q += blockDim.x) Bsh[(q / s) * S + q % s] = k.B[q];
-    for (int q = threadIdx.x; q < s; q += blockDim.x) al[q] = k.alpha[q];
+    for (int q = threadIdx.x; q < S * (S + 4); q += blockDim.x) {
+        const int i = q / S, j = q % S;
+        Bsh[q] = (i < s && j < s) ? k.B[i * s + j] : 0.0;
+    }
+    for (int q = threadIdx.x; q < S + 4; q += blockDim.x) al[q] = (q < s) ? k.alpha[q] : 0.0;
     __syncthreads();
     double *x = *k.xpp + k.xoff;
     const int64_t vs = k.vstride;
@@ -126,35 +161,11 @@ __global__ void __launch_bounds__(256) k5_block(K5BParams k, const DevState *st)
 #pragma unroll
         for (int i = 0; i < S; ++i) o[i] = (i < s) ? k.P[(int64_t)(s + i) * vs + e] : 0.0;
         const double p0 = k.P[e];
-        double ax = 0.0;
-#pragma unroll
-        for (int j = 0; j < S; ++j) {
-            if (j < s) {
-                double sp = 0.0;
-#pragma unroll
-                for (int m = 0; m < S; ++m)
-                    if (m < s) sp = fma(o[m], Bsh[m * S + j], sp);
-                const double qn = k.P[(int64_t)j * vs + e] - sp;
-                k.P[(int64_t)(s + j) * vs + e] = qn;
-                ax = fma(al[j], qn, ax);
-            }
-        }
+        const double ax = bcg_phase<S>(k.P + e, k.P + (int64_t)s * vs + e, vs, s, o, Bsh, al);
         // r_{k+1} = p_0 - Z_k alpha with Z_k = W_k - Z' B
 #pragma unroll
         for (int i = 0; i < S; ++i) o[i] = (i < s) ? k.W[(int64_t)(s + i) * vs + e] : 0.0;
-        double aw = 0.0;
-#pragma unroll
-        for (int j = 0; j < S; ++j) {
-            if (j < s) {
-                double sw = 0.0;
-#pragma unroll
-                for (int m = 0; m < S; ++m)
-                    if (m < s) sw = fma(o[m], Bsh[m * S + j], sw);
-                const double zn = k.W[(int64_t)j * vs + e] - sw;
-                k.W[(int64_t)(s + j) * vs + e] = zn;
-                aw = fma(al[j], zn, aw);
-            }
-        }
+        const double aw = bcg_phase<S>(k.W + e, k.W + (int64_t)s * vs + e, vs, s, o, Bsh, al);
         const int64_t xi = row * k.nx + xx;
         x[xi] = x[xi] + ax;
         k.P[e] = p0 - aw;
