@@ -1,10 +1,11 @@
-for w in "--workload cfg2" "--workload cfg3" "--workload cfg4 --s 4" "--workload cfg4 --s 8" "--workload cfg4" "--workload cfg4 --s 24" "--workload cfg4 --s 32" "--workload cfg4 --n 384 --strong" "--workload cfg5 --nu 20"; do
+for w in "--workload cfg1" "--workload cfg2" "--workload cfg3" "--workload cfg4 --s 4" "--workload cfg4 --s 8" "--workload cfg4" "--workload cfg4 --s 24" "--workload cfg4 --s 32" "--workload cfg4 --n 384 --strong" "--workload cfg5 --nu 20"; do
   timeout 400 python bench.py $w --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > /tmp/w.json 2>/tmp/w.err || { echo "$w FAILED"; tail -3 /tmp/w.err; continue; }
   tail -1 /tmp/w.json >> gpurun_out/workloads_final.jsonl
   python - "$w" <<'PY'
 import json, sys
 d = json.loads(open('/tmp/w.json').read().strip().splitlines()[-1])
 k = d['kernels']
-print("%-34s GDOF/s %7.3f ms/step %8.4f path %.3f | K1 %.3f | K2 %.3f | K5 %.3f | K4 %.1f us" % (sys.argv[1], d['value'], d['ms_per_step'], d['roofline']['path_frac'], k['basis']['frac'], k['gram']['frac'], k['update']['frac'], k['fgs']['us_per_launch']))
+k1s = k.get('basis_single', {}).get('frac')
+print("%-34s GDOF/s %7.3f ms/step %8.4f path %.3f | K1 %.3f | K1 single %s | K2 %.3f | K5 %.3f | K4 %.1f us" % (sys.argv[1], d['value'], d['ms_per_step'], d['roofline']['path_frac'], k['basis']['frac'], "%.3f" % k1s if k1s else "-", k['gram']['frac'], k['update']['frac'], k['fgs']['us_per_launch']))
 PY
 done
