@@ -36,8 +36,10 @@ __device__ __forceinline__ double k4_warp_sum(double v)
     return v;
 }
 
-// scratch: >= s*s + s + 32 doubles of shared memory owned by this warp
-template <int NB4>
+// scratch: >= s*s + s + 32 doubles of shared memory owned by this warp.
+// STAGED: the caller has already put the block [Ghat | c] at scratch (KS, the
+// single-CTA outer iteration, reduces it there); otherwise it is read from a.blk
+template <int NB4, bool STAGED = false>
 __device__ __forceinline__ void k4_fgs_small(const K4Args &a, DevState *st, double *scratch)
 {
     constexpr int SP = 4 * NB4;
@@ -47,7 +49,8 @@ __device__ __forceinline__ void k4_fgs_small(const K4Args &a, DevState *st, doub
     const int k = S.k;
     const int nent = s * s + s;
     double *Bs = scratch, *dsh = scratch + nent;
-    for (int q = lane; q < nent; q += 32) Bs[q] = __ldcg(a.blk + q);
+    if (!STAGED)
+        for (int q = lane; q < nent; q += 32) Bs[q] = __ldcg(a.blk + q);
     __syncwarp();
     const bool rec = k < S.hist_cap, recg = k < S.gram_cap;
     if (recg)

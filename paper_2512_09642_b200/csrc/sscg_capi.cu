@@ -321,6 +321,7 @@ Knobs sscg::read_knobs()
     k.k5_recur = tri("SSCG_K5_RECUR", 1) != 0;
     k.deep_halo = tri("SSCG_DEEP_HALO", 1) != 0;
     k.deep_overlap = tri("SSCG_DEEP_OVERLAP", 0) != 0;
+    k.small = tri("SSCG_SMALL", -1);
     k.debug = getenv("SSCG_DEBUG") != nullptr;
     k.pdl = tri("SSCG_PDL", 1) != 0;
     return k;
@@ -474,6 +475,8 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
     }
     TRY(build_basis_store(c, s));
     TRY(alloc_gram_buffers(c, s));
+    if ((A->kind == SSCG_OP_STENCIL5_2D || A->kind == SSCG_OP_STENCIL7) && !ks_prepare())
+        return fail(SSCG_ERR_CUDA, "shared-memory opt-in of the single-CTA outer iteration");
     TRY(dalloc(c, &c->xdev, 1));
     CU(cudaMallocHost(&c->xhost, sizeof(double *)));
     TRY(dalloc(c, &c->alpha, 64));
@@ -741,6 +744,21 @@ static bool uses_wfree(const sscg_ctx *c)
 static bool uses_mp3(const sscg_ctx *c);
 static bool uses_fused(const sscg_ctx *c);
 
+// KS (k_small.cu): the whole outer iteration in one single-CTA launch, for a
+// single slab whose working set lives in L2, 5-/7-point constant stencil,
+// Chebyshev basis, s <= 8, FGS solver (auto: the 2D 5-point operator up to
+// 16384 points -- BASELINE cfg 1; SSCG_SMALL=1 forces it for any supported slab)
+static bool uses_small(const sscg_ctx *c)
+{
+    const Geo &g = c->g;
+    if (c->g.kn.small == 0 || c->slabs.size() != 1 || c->comm || c->basis != SSCG_BASIS_CHEBYSHEV ||
+        c->gram_solver != SSCG_GRAM_FGS || c->blockcg || c->diagnostics || c->slabs[0].dinv)
+        return false;
+    const int64_t npts = (int64_t)g.nx * g.ny * c->slabs[0].nzl;
+    if (!ks_supported(g, c->s, npts)) return false;
+    return c->g.kn.small == 1 || (g.kind == SSCG_OP_STENCIL5_2D && npts <= 16384);
+}
+
 // K1 for step j over the planes of every local slab selected by `part`:
 //   0 = all planes, 1 = the two boundary planes (1 and nzl), 2 = the interior
 //   planes [2, nzl) that do not read a halo plane, 3 = the two planes next to
@@ -962,6 +980,22 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const bool halo = (L > 1 || c->nranks > 1) && g.kind != SSCG_OP_CSR;
     const bool ovl = halo && c->overlap;
     const bool fuse = uses_fused(c), mp3 = uses_mp3(c), deep = uses_deep(c);
+    if (uses_small(c)) {   // the whole outer iteration in one launch (KS)
+        K4Args a4{};
+        a4.blk = c->blk;
+        a4.alpha = c->alpha;
+        a4.s = s;
+        a4.nu = c->nu;
+        a4.pdl = g.kn.pdl;
+        a4.h_gram = c->h_gram; a4.h_d = c->h_d; a4.h_at = c->h_at; a4.h_al = c->h_al;
+        a4.h_delta = c->h_delta; a4.h_relres = c->h_relres; a4.h_lnorm = c->h_lnorm;
+        TRY(prof_mark(c, SSCG_PROF_BASIS, true));
+        launch_ks(g, c->slabs[0], s, c->theta, c->sigma, c->xdev, c->blk, a4, c->st, c->stream);
+        TRY(prof_mark(c, SSCG_PROF_BASIS, false));
+        ++c->launches;
+        CU(cudaGetLastError());
+        return SSCG_OK;
+    }
     nvtxRangePushA("basis");
     for (int j = 0; j < s; ++j) {
         if (mp3 && j + 2 < s) {   // steps j, j+1, j+2 in one pass (K1M)

@@ -50,9 +50,10 @@ SWITCHES = {
              {"SSCG_K5_RECUR": "0"}],
     "varcoef7": [{}, {"SSCG_K1_FUSE_VC": "1"}, {"SSCG_K1_FUSE_VC": "0"}, {"SSCG_K2S": "0"}, {"SSCG_WFREE": "0"},
                  {"SSCG_K5_RECUR": "0"}, {"SSCG_FACES_TMA": "0"}],
-    "cfg1": [{}, {"SSCG_K5_RECUR": "0"}],
+    # cfg 1 runs the single-CTA outer iteration (KS) by default; SSCG_SMALL=0 the multi-kernel path
+    "cfg1": [{}, {"SSCG_SMALL": "0"}, {"SSCG_SMALL": "0", "SSCG_K5_RECUR": "0"}],
     # odd nx: padded row pitch, so the stored-W schedule and the stored-W update always
-    "7pt_odd": [{}, {"SSCG_K1_FUSE": "1"}, {"SSCG_K1_TMA": "0", "SSCG_K1_FUSE": "0"}],
+    "7pt_odd": [{}, {"SSCG_K1_FUSE": "1"}, {"SSCG_K1_TMA": "0", "SSCG_K1_FUSE": "0"}, {"SSCG_SMALL": "1"}],
 }
 
 _problems = {}

@@ -460,6 +460,7 @@ def test_recurrence_update_matches_stored_w(cfg, monkeypatch):
     kind, nx, ny, nz, s, nu = cfg
     P = Problem(kind, nx, ny, nz, s, nu, lanczos=(kind == "27pt"))
     x_or, _ = P.oracle(max_outer=10)
+    monkeypatch.setenv("SSCG_SMALL", "0")   # the multi-kernel path (cfg 1 would run KS)
     res = {}
     for rec in ("1", "0"):
         monkeypatch.setenv("SSCG_K5_RECUR", rec)
@@ -487,6 +488,7 @@ def test_gram_dmma_matches_register_tiles(cfg, monkeypatch):
     bounds = (0.02, 2.2) if s == 64 else None
     P = Problem(kind, nx, ny, nz, s, nu, bounds=bounds, lanczos=(kind == "varcoef7"))
     x_or, tr = P.oracle(max_outer=1, dump_iter=0)
+    monkeypatch.setenv("SSCG_SMALL", "0")   # the multi-kernel path (cfg 1 would run KS)
     out = {}
     for dm in ("1", "0"):
         monkeypatch.setenv("SSCG_K2_DMMA", dm)

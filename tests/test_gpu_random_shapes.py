@@ -1,7 +1,8 @@
 """Randomised shapes (seeded): every operator kind, odd and tiny grids, basis
 sizes 1..40, several slabs, the schedule switches (fused triples and pairs,
 the variable-coefficient pair, TMA faces, recurrence update, W-free Gram,
-streaming small-s Gram, DMMA Gram) forced both ways -- each run against the
+streaming small-s Gram, DMMA Gram, the single-CTA outer iteration KS) forced
+both ways -- each run against the
 CPU oracle at outer 0 (north_star tolerances) and after a few outer
 iterations."""
 import numpy as np
@@ -29,6 +30,7 @@ def _cases(n=80, seed=2024):
                "SSCG_K2_DMMA": str(rng.integers(0, 2)), "SSCG_FACES_TMA": str(rng.integers(0, 2)),
                "SSCG_K1_MP3": str(rng.integers(0, 2)), "SSCG_K1_FUSE_VC": str(rng.integers(0, 2)),
                "SSCG_WFREE": str(rng.integers(0, 2)), "SSCG_K2S": str(rng.integers(0, 2))}
+        env["SSCG_SMALL"] = str(rng.integers(0, 2))   # drawn last: the earlier draws keep their values
         out.append((kind, nx, ny, nz, s, nu, slabs, env))
     return out
 
