@@ -744,10 +744,11 @@ static bool uses_wfree(const sscg_ctx *c)
 static bool uses_mp3(const sscg_ctx *c);
 static bool uses_fused(const sscg_ctx *c);
 
-// KS (k_small.cu): the whole outer iteration in one single-CTA launch, for a
-// single slab whose working set lives in L2, 5-/7-point constant stencil,
-// Chebyshev basis, s <= 8, FGS solver (auto: the 2D 5-point operator up to
-// 16384 points -- BASELINE cfg 1; SSCG_SMALL=1 forces it for any supported slab)
+// KS (k_small.cu): the whole outer iteration in one launch of one 8-CTA
+// cluster, for a single slab of at most 8192 points (its P and W fit the
+// cluster's shared memory), 5-/7-point constant stencil, Chebyshev basis,
+// s <= 8, FGS solver (auto: the 2D 5-point operator -- BASELINE cfg 1;
+// SSCG_SMALL=1 forces it for any supported slab)
 static bool uses_small(const sscg_ctx *c)
 {
     const Geo &g = c->g;
@@ -756,7 +757,7 @@ static bool uses_small(const sscg_ctx *c)
         return false;
     const int64_t npts = (int64_t)g.nx * g.ny * c->slabs[0].nzl;
     if (!ks_supported(g, c->s, npts)) return false;
-    return c->g.kn.small == 1 || (g.kind == SSCG_OP_STENCIL5_2D && npts <= 16384);
+    return c->g.kn.small == 1 || g.kind == SSCG_OP_STENCIL5_2D;
 }
 
 // K1 for step j over the planes of every local slab selected by `part`:

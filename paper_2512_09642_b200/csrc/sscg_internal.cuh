@@ -121,7 +121,7 @@ struct Knobs {
     int k5_recur = 1;      // SSCG_K5_RECUR     0: update with the stored W
     int deep_halo = 1;     // SSCG_DEEP_HALO    0: 1-plane halos around every K1M triple (boundary single steps)
     int deep_overlap = 0;  // SSCG_DEEP_OVERLAP 1: deep-halo exchange overlapped with the triple / update interior
-    int small = -1;        // SSCG_SMALL        -1 auto (L2-resident grids), 0 forbid, 1 force the single-CTA outer iteration
+    int small = -1;        // SSCG_SMALL        -1 auto (2D grids <= 8192 points), 0 forbid, 1 force the single-cluster outer iteration
     int debug = 0;         // SSCG_DEBUG
     int pdl = 1;           // SSCG_PDL          0: plain stream-ordered launches (no programmatic dependent launch)
 };
@@ -268,7 +268,7 @@ void launch_anorm(const Geo &g, const Slab &sl, double *bmax, int nblk, cudaStre
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *const *xpp, int64_t xoff,
                const DevState *st, cudaStream_t stream, int zb, int ze, double theta, double sigma, bool rec);
 
-// KS: one whole outer iteration in one single-CTA launch for L2-resident problems (k_small.cu)
+// KS: one whole outer iteration in one launch of one 8-CTA cluster for small problems (k_small.cu)
 bool ks_supported(const Geo &g, int s, int64_t npts);
 bool ks_prepare();   // opt in to the shared-memory ring (once per process)
 void launch_ks(const Geo &g, const Slab &sl, int s, double theta, double sigma, double *const *xpp, double *blk,
