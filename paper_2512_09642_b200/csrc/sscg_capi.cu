@@ -90,6 +90,10 @@ struct sscg_ctx {
     bool x_copied = false;
     bool overlap = true;
     bool failed = false;            // an NCCL abort left the context unusable (every call: SSCG_ERR_NCCL)
+    // the fused basis schedules every rank can run (AND over ranks at setup: slabs of
+    // different depth may cross a kernel's size threshold, and the halo exchanges of
+    // all ranks must match step for step)
+    bool all_mp3 = true, all_fused = true;
     double nccl_timeout_s = 600.0;  // SSCG_NCCL_TIMEOUT_S, read at setup
     int k1_sm_cap = 0;
     // variants on the same boundary
@@ -489,6 +493,20 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         ncclUniqueId id;
         memcpy(&id, cm->nccl_id, sizeof id);
         NC(ncclCommInitRank(&c->comm, c->nranks, id, c->rank));
+        // agree on the fused basis schedules (minimum over ranks of the local capability)
+        int flags[2] = {1, 1};
+        for (const auto &sl : c->slabs) {
+            if (!sl.has_k1m || sl.nzl < 8) flags[0] = 0;
+            if (!sl.has_k1f || sl.nzl < 4) flags[1] = 0;
+        }
+        int *dflags = nullptr;
+        TRY(dalloc(c, &dflags, 2));
+        CU(cudaMemcpyAsync(dflags, flags, sizeof flags, cudaMemcpyHostToDevice, c->stream));
+        NC(ncclAllReduce(dflags, dflags, 2, ncclInt32, ncclMin, c->comm, c->stream));
+        CU(cudaMemcpyAsync(flags, dflags, sizeof flags, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        c->all_mp3 = flags[0] != 0;
+        c->all_fused = flags[1] != 0;
     } else if (const char *e = getenv("SSCG_NCCL_SELF"); e && e[0] == '1') {
         // test mode for a one-GPU box: a one-rank communicator carries the
         // allreduces, and the halos of in-process slabs move by NCCL send/recv
@@ -826,6 +844,7 @@ static bool uses_fused(const sscg_ctx *c)
     if (c->basis != SSCG_BASIS_CHEBYSHEV ||
         (c->g.kind != SSCG_OP_STENCIL7 && c->g.kind != SSCG_OP_STENCIL27 && c->g.kind != SSCG_OP_VARCOEF7))
         return false;
+    if (!c->all_fused) return false;   // some rank's slabs cannot (every rank must run the same schedule)
     const bool halo = c->slabs.size() > 1 || c->nranks > 1;
     for (const auto &sl : c->slabs)
         if (!sl.has_k1f || (halo && sl.nzl < 4)) return false;
@@ -836,7 +855,7 @@ static bool uses_fused(const sscg_ctx *c)
 // slab needs an interior for the third level ([3, nzl-1))
 static bool uses_mp3(const sscg_ctx *c)
 {
-    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->g.kind != SSCG_OP_STENCIL7) return false;
+    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->g.kind != SSCG_OP_STENCIL7 || !c->all_mp3) return false;
     const bool halo = c->slabs.size() > 1 || c->nranks > 1;
     for (const auto &sl : c->slabs)
         if (!sl.has_k1m || (halo && sl.nzl < 8)) return false;
