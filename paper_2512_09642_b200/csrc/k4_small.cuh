@@ -44,6 +44,10 @@ __device__ __forceinline__ void k4_fgs_small(const K4Args &a, DevState *st, doub
 {
     constexpr int SP = 4 * NB4;
     const int s = a.s, lane = threadIdx.x & 31;
+#ifdef K4_TIMING
+    unsigned long long t00;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t00));
+#endif
     // every input in flight at once: the device state (one struct copy) and the block
     const DevState S = *st;
     const int k = S.k;
@@ -75,6 +79,10 @@ __device__ __forceinline__ void k4_fgs_small(const K4Args &a, DevState *st, doub
         if (lane == 0) { st->done = 1; st->outer = k; }
         return;
     }
+#ifdef K4_TIMING
+    unsigned long long ta, tb, tc;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta));
+#endif
     // Ruhe scaling
     const bool v0 = lane < s;
     double d0 = 0.0;
@@ -93,8 +101,8 @@ __device__ __forceinline__ void k4_fgs_small(const K4Args &a, DevState *st, doub
     const double ct0 = v0 ? d0 * c[lane] : 0.0;
     double g[SP];
 #pragma unroll
-    for (int j = 0; j < SP; ++j)
-        g[j] = (v0 && j < s) ? ((j == lane) ? 1.0 : (d0 * Gh[lane * s + j]) * dsh[j]) : 0.0;
+    for (int j = 0; j < SP; ++j)   // G_ij read as G_ji (the block is mirrored): lanes on consecutive banks
+        g[j] = (v0 && j < s) ? ((j == lane) ? 1.0 : (d0 * Gh[j * s + lane]) * dsh[j]) : 0.0;
     double lnorm_part = 0.0;
 #pragma unroll
     for (int j = 0; j < SP; ++j)
@@ -112,6 +120,9 @@ __device__ __forceinline__ void k4_fgs_small(const K4Args &a, DevState *st, doub
         Lb[b][5] = __shfl_sync(0xffffffffu, g[j + 2], j + 3);   // G_{j+3,j+2}
     }
     double rho = ct0, al0 = 0.0;
+#ifdef K4_TIMING
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb));
+#endif
     for (int sw = 0; sw < a.nu; ++sw) {
 #pragma unroll
         for (int b = 0; b < NB4; ++b) {
@@ -132,6 +143,10 @@ __device__ __forceinline__ void k4_fgs_small(const K4Args &a, DevState *st, doub
             al0 += (lane == j + 3) ? e3 : 0.0;
         }
     }
+#ifdef K4_TIMING
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tc));
+    if (lane == 0) printf("K4 phases ns: loads+stop test %llu  scaling %llu  sweeps %llu\n", ta - t00, tb - ta, tc - tb);
+#endif
     // residual c~ - G a~ of the final iterate, this lane's row (PAPER.md:259-262 monitor)
     double res0 = ct0;
 #pragma unroll

@@ -2,6 +2,8 @@
 //       system, stopping test and history (single warp).
 // K5 -- fused solution/residual update x += P alpha, r -= (AP) alpha
 //       (r is stored in place of p_0).
+#include <cstdio>
+
 #include "sscg_internal.cuh"
 #include "k4_small.cuh"
 
@@ -431,7 +433,15 @@ __global__ void __launch_bounds__(32) k4_fgs_warp(K4Args a, DevState *st)
 {
     PDL_ENTRY(st);
     __shared__ double scratch[32 * 32 + 32 + 32];
+#ifdef K4_TIMING   // variant builds only: the kernel's own duration at the clocks of the real schedule
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
     k4_fgs_dispatch(a, st, scratch);
+#ifdef K4_TIMING
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (threadIdx.x == 0) printf("K4 ns %llu (s %d nu %d)\n", t1 - t0, a.s, a.nu);
+#endif
 }
 
 void launch_k4(const K4Args &a, DevState *st, cudaStream_t s)
