@@ -88,6 +88,9 @@ struct K1MWork {
 
 struct Outs {
     double *w[3], *pn[3];  // null: not stored
+    // peer-store halos: p_{j+2}, p_{j+3} of the neighbour below / above, offset so
+    // that own offset + pointer is the neighbour's ghost cell (null: none)
+    double *lo[2], *hi[2];
 };
 
 __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int x, int y, int z, int v,
@@ -365,6 +368,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (!v1) Ap.y = 0.0;
                     if (HASW && w1) __stcs(reinterpret_cast<double2 *>(w1 + off - pl), Ap);
                     st_pn(n1 + off - pl, u2);
+                    if (!S) {   // peer-store halo (the steady range excludes these planes)
+                        if (out.lo[0] && z2 <= 2) st_pn(out.lo[0] + off - pl, u2);
+                        if (out.hi[0] && z2 >= wk.nzl - 1) st_pn(out.hi[0] + off - pl, u2);
+                    }
                 }
             }
             if (in2) st_u(su2 + ((uc - 1) % NU) * U2S, o2, oe2, u2);
@@ -385,6 +392,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                     double v1b = cf * (dinv_c * Ap.y - sigma * c.y) - u1m2.y;
                     if (!v1) v1b = 0.0;
                     st_pn(n2 + off - 2 * pl, make_double2(v0b, v1b));
+                    if (!S) {
+                        if (out.lo[1] && z3 <= 3) st_pn(out.lo[1] + off - 2 * pl, make_double2(v0b, v1b));
+                        if (out.hi[1] && z3 >= wk.nzl - 2) st_pn(out.hi[1] + off - 2 * pl, make_double2(v0b, v1b));
+                    }
                 }
             }
             mbar_arrive_a(ubar_a + 8 * (uc % NU));   // this thread's U1(q), U2(q-1) are written
@@ -399,10 +410,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         };
         using Gen = std::integral_constant<bool, false>;
         using Steady = std::integral_constant<bool, true>;
+        // steady planes [qs, qe): with peer stores, level 2 / 3 planes the
+        // neighbours take (1..3, nzl-2..nzl) run in the general form
+        const int qs = out.lo[0] ? max(it.zlo + 2, 6) : it.zlo + 2;
+        const int qe = out.hi[0] ? min(it.zhi, wk.nzl) : it.zhi;
         int q = it.q0;
-        for (; q < it.zlo + 2 && q <= it.q1; ++q) plane(q, Gen());
+        for (; q < qs && q <= it.q1; ++q) plane(q, Gen());
 #pragma unroll 1
-        for (; q < it.zhi; ++q) plane(q, Steady());
+        for (; q < qe; ++q) plane(q, Steady());
         for (; q <= it.q1; ++q) plane(q, Gen());
         for (int z = max(it.q1 + 1, it.plo); z <= it.phi; ++z) release(z);
         sc = sbase + (it.phi - it.plo + 1);
@@ -501,6 +516,15 @@ void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st
         out.w[l] = a.w[l];
         out.pn[l] = a.pn[l];
     }
+    // peer-store halos: own plane z -> plane nzl_lo + z of the slab below,
+    // plane z - nzl of the slab above (p_{j+3} only when this triple forms it)
+    for (int l = 0; l < 2; ++l) {
+        const bool formed = l == 0 || a.pn[2];
+        out.lo[l] = (formed && a.peer_lo[l]) ? a.peer_lo[l] + (int64_t)a.peer_nzl_lo * g.plane : nullptr;
+        out.hi[l] = (formed && a.peer_hi[l]) ? a.peer_hi[l] - (int64_t)a.nzl * g.plane : nullptr;
+    }
+    if (!out.lo[0]) out.lo[1] = nullptr;   // the kernel keys the steady range on level 2's pointer
+    if (!out.hi[0]) out.hi[1] = nullptr;
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;
     const int64_t resident = (a.sm_cap > 0 && a.sm_cap < k2_grid()) ? a.sm_cap : k2_grid();
     const int zc_env = g.kn.k1_zc;

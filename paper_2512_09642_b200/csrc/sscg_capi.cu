@@ -325,6 +325,7 @@ Knobs sscg::read_knobs()
     k.k5_recur = tri("SSCG_K5_RECUR", 1) != 0;
     k.deep_halo = tri("SSCG_DEEP_HALO", 1) != 0;
     k.deep_overlap = tri("SSCG_DEEP_OVERLAP", 0) != 0;
+    k.peer_halo = tri("SSCG_PEER_HALO", 1) != 0;
     k.small = tri("SSCG_SMALL", -1);
     k.debug = getenv("SSCG_DEBUG") != nullptr;
     k.pdl = tri("SSCG_PDL", 1) != 0;
@@ -871,6 +872,15 @@ static bool uses_deep(const sscg_ctx *c)
     return halo && c->g.guard >= 2 && uses_mp3(c);
 }
 
+// peer-store halos: with in-process neighbours only, each deep
+// triple stores the planes its neighbours need straight into their ghost
+// planes (K1M), so no exchange follows it
+static bool uses_peer(const sscg_ctx *c)
+{
+    return c->g.kn.peer_halo && c->nranks == 1 && c->slabs.size() > 1 && !c->nccl_self && uses_deep(c) &&
+           !c->g.kn.deep_overlap;
+}
+
 // deep-halo triple of steps j..j+2 on every slab.  part 0: all planes (levels 1
 // and 2 formed on the ghost planes of a side with a neighbour); part 1: the
 // planes the next exchange sends (level 3 on [1, 4) and [nzl-2, nzl], levels 1
@@ -902,6 +912,16 @@ static sscg_status launch_basis_triple_deep(sscg_ctx *c, int j, int part)
             }
         }
         if (part == 2) a.sm_cap = c->k1_sm_cap;
+        if (part == 0 && uses_peer(c)) {
+            const size_t l = &sl - c->slabs.data();
+            for (int v = 0; v < 2; ++v) {
+                const int jv = j + 2 + v;   // p_{j+2}, p_{j+3}
+                if (jv > s - 1) continue;
+                if (l > 0) a.peer_lo[v] = c->slabs[l - 1].P + (int64_t)jv * g.vstride;
+                if (l + 1 < c->slabs.size()) a.peer_hi[v] = c->slabs[l + 1].P + (int64_t)jv * g.vstride;
+            }
+            if (l > 0) a.peer_nzl_lo = c->slabs[l - 1].nzl;
+        }
         a.deep_lo = sl.has_lo;
         a.deep_hi = sl.has_hi;
         a.guard = g.guard;
@@ -1038,7 +1058,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
                     TRY(halo_join(c));
                 } else {
                     TRY(launch_basis_triple_deep(c, j, 0));
-                    if (np3 > 0) TRY(halo_fork(c, j + 3, false, np3, j + 2, np2));
+                    if (np3 > 0 && !uses_peer(c)) TRY(halo_fork(c, j + 3, false, np3, j + 2, np2));
                 }
             } else {
                 // boundary planes of step j, exchange of p_{j+1} (overlapped with the

@@ -121,6 +121,7 @@ struct Knobs {
     int k5_recur = 1;      // SSCG_K5_RECUR     0: update with the stored W
     int deep_halo = 1;     // SSCG_DEEP_HALO    0: 1-plane halos around every K1M triple (boundary single steps)
     int deep_overlap = 0;  // SSCG_DEEP_OVERLAP 1: deep-halo exchange overlapped with the triple / update interior
+    int peer_halo = 1;     // SSCG_PEER_HALO    0: in-process deep halos by copies after each triple instead of K1M peer stores
     int small = -1;        // SSCG_SMALL        -1 auto (2D grids <= 8192 points), 0 forbid, 1 force the single-cluster outer iteration
     int debug = 0;         // SSCG_DEBUG
     int pdl = 1;           // SSCG_PDL          0: plain stream-ordered launches (no programmatic dependent launch)
@@ -204,6 +205,13 @@ struct K1MArgs {
     // ghost planes there instead of taking the Dirichlet value
     int deep_lo, deep_hi;
     int guard;             // guard planes allocated below plane 0 (tensor-map offset)
+    // peer-store halos: p_{j+2} / p_{j+3} of the neighbouring
+    // slab below (lo) / above (hi), null for none.  Level 2 also stores its
+    // planes 1, 2 (nzl-1, nzl) and level 3 its planes 1..3 (nzl-2..nzl) into the
+    // neighbour's ghost planes (its nzl_lo+1.. / -2..0), which replaces the
+    // exchange after the triple
+    double *peer_lo[2], *peer_hi[2];
+    int peer_nzl_lo;       // nzl of the slab below
     double sigma;
     const CUtensorMap *tmP, *tmM;
 };

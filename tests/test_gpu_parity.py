@@ -381,7 +381,10 @@ def test_deep_halo_triples(cfg, slabs, monkeypatch):
     the boundary single steps by K1T); the serial deep schedule (triple, then
     the exchange; the default) and the overlapped one (SSCG_DEEP_OVERLAP=1:
     the planes the exchange sends first, the exchange during the rest):
-    bitwise equal.
+    bitwise equal; and the serial schedule with in-process peer stores (the
+    default: K1M writes the planes the neighbours need into their ghost
+    planes, no exchange after the triple) bitwise equal to it with the copies
+    (SSCG_PEER_HALO=0).
     All agree with the oracle."""
     import paper_2512_09642_b200 as sscg
     kind, nx, ny, nz, s, nu = cfg
@@ -390,18 +393,21 @@ def test_deep_halo_triples(cfg, slabs, monkeypatch):
     out = {}
     for mode, env, sl in (("deep", {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "1"}, slabs),
                           ("deep_serial", {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "0"}, slabs),
-                          ("plane1", {"SSCG_DEEP_HALO": "0", "SSCG_DEEP_OVERLAP": "0"}, slabs),
-                          ("one", {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "0"}, 1)):
+                          ("deep_copies", {"SSCG_DEEP_HALO": "1", "SSCG_PEER_HALO": "0"}, slabs),
+                          ("plane1", {"SSCG_DEEP_HALO": "0", "SSCG_PEER_HALO": "1"}, slabs),
+                          ("one", {"SSCG_DEEP_HALO": "1"}, 1)):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         with P.gpu_solver(slabs=sl) as S:
             assert S.query(sscg.QUERY_BASIS_FUSED) == 3
             x = S.solve(P.b_gpu(), rtol=0.0, max_outer=5).cpu().numpy()
             out[mode] = (x, [S.gram(k)[0] for k in range(6)], [S.basis(j) for j in range(s)])
-    a, b = out["deep"], out["deep_serial"]
-    assert np.array_equal(a[0], b[0])
-    for k in range(6):
-        assert np.array_equal(a[1][k], b[1][k])
+    a = out["deep"]
+    for other in ("deep_serial", "deep_copies"):
+        b = out[other]
+        assert np.array_equal(a[0], b[0]), other
+        for k in range(6):
+            assert np.array_equal(a[1][k], b[1][k]), other
     for ref in ("plane1", "one"):
         r = out[ref]
         assert np.max(np.abs(a[1][0] - r[1][0])) <= 1e-13 * np.max(np.abs(r[1][0])), ref

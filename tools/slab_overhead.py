@@ -8,7 +8,9 @@ schedule's extra launches and copies; relative_to_1 = t(1 slab) / that.  The
 NCCL transfers themselves are not in it (the copies are device-to-device).
 
 Schedules with several slabs: "deep" (the default: each K1M triple in one
-launch, then one 3 + 2-plane exchange), "deep_overlap" (SSCG_DEEP_OVERLAP=1:
+launch storing the planes its neighbours need straight into their ghost
+planes -- peer-store halos, no exchange after the triple), "deep_copies"
+(SSCG_PEER_HALO=0: the triple, then one 3 + 2-plane exchange by copies), "deep_overlap" (SSCG_DEEP_OVERLAP=1:
 the planes the exchange sends computed first, the exchange overlapped with
 the rest of the triple), "plane1" (SSCG_DEEP_HALO=0: single steps on the
 boundary planes around three 1-plane exchanges per triple).  usage: python tools/slab_overhead.py [n] [steps]"""
@@ -24,7 +26,8 @@ import paper_2512_09642_b200 as sscg  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 448
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-MODES = {"deep": {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "0", "SSCG_NO_OVERLAP": "0"},
+MODES = {"deep": {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "0", "SSCG_NO_OVERLAP": "0", "SSCG_PEER_HALO": "1"},
+         "deep_copies": {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "0", "SSCG_NO_OVERLAP": "0", "SSCG_PEER_HALO": "0"},
          "deep_overlap": {"SSCG_DEEP_HALO": "1", "SSCG_DEEP_OVERLAP": "1", "SSCG_NO_OVERLAP": "0"},
          "plane1": {"SSCG_DEEP_HALO": "0", "SSCG_DEEP_OVERLAP": "0", "SSCG_NO_OVERLAP": "0"}}
 runs = [(1, "deep")] + [(sl, m) for sl in (2, 4) for m in MODES]
