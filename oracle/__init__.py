@@ -76,6 +76,11 @@ def lib():
         L.orc_lanczos_bounds.argtypes = [vp, vp, i, vp, d, vp, vp]; L.orc_lanczos_bounds.restype = i
         L.orc_lanczos_bounds_tri.argtypes = [vp, vp, i, vp, d, vp, vp, vp, vp]
         L.orc_lanczos_bounds_tri.restype = i
+        L.orc_coarse_n.argtypes = [vp, i, i, i]; L.orc_coarse_n.restype = l
+        L.orc_coarse_restrict.argtypes = [vp, i, i, i, vp, vp]
+        L.orc_coarse_prolong_add.argtypes = [vp, i, i, i, vp, vp]
+        L.orc_coarse_galerkin.argtypes = [vp, i, i, i, vp, vp, vp, l]; L.orc_coarse_galerkin.restype = l
+        L.orc_coarse_fgs.argtypes = [l, vp, vp, vp, vp, i, vp]
     return _lib
 
 
@@ -291,3 +296,64 @@ def lanczos_bounds(A: Operator, iters, v0, margin, D=None, tridiag=False):
     if tridiag:
         return lo.value, hi.value, m, al[:m], be[:max(m - 1, 0)]
     return lo.value, hi.value, m
+
+
+# --------------------------------------------------------------------------
+# AMG coarse grid (R25): aggregates of
+# b = (bx, by, bz) fine cells, A_c = P^T A_f P, Forward Gauss-Seidel on A_c
+# --------------------------------------------------------------------------
+
+def coarse_dims(A: Operator, b=(2, 2, 2)):
+    bx, by, bz = b
+    return (-(-A.nx // bx), -(-A.ny // by), -(-A.nz // bz))
+
+
+def coarse_restrict(A: Operator, rf, b=(2, 2, 2)) -> np.ndarray:
+    """r_c = P^T r_f."""
+    rf = _f64(rf)
+    rc = np.empty(int(np.prod(coarse_dims(A, b))))
+    lib().orc_coarse_restrict(A.ref, *b, _p(rf), _p(rc))
+    return rc
+
+
+def coarse_prolong_add(A: Operator, y, xf, b=(2, 2, 2)) -> np.ndarray:
+    """Returns x_f + P y (xf is not modified)."""
+    y = _f64(y)
+    out = _f64(xf).copy()
+    lib().orc_coarse_prolong_add(A.ref, *b, _p(y), _p(out))
+    return out
+
+
+@dataclass
+class CoarseMatrix:
+    n: int
+    rowptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+
+    def dense(self) -> np.ndarray:
+        M = np.zeros((self.n, self.n))
+        for i in range(self.n):
+            for q in range(self.rowptr[i], self.rowptr[i + 1]):
+                M[i, self.col[q]] = self.val[q]
+        return M
+
+
+def coarse_galerkin(A: Operator, b=(2, 2, 2)) -> CoarseMatrix:
+    """A_c = P^T A_f P, column by column (sscg_oracle.c orc_coarse_galerkin)."""
+    nc = lib().orc_coarse_n(A.ref, *b)
+    cap = 27 * nc + 64
+    rowptr = np.zeros(nc + 1, dtype=np.int64)
+    col = np.zeros(cap, dtype=np.int64)
+    val = np.zeros(cap)
+    nnz = lib().orc_coarse_galerkin(A.ref, *b, _p(rowptr), _p(col), _p(val), cap)
+    assert nnz >= 0
+    return CoarseMatrix(nc, rowptr, col[:nnz].copy(), val[:nnz].copy())
+
+
+def coarse_fgs(Ac: CoarseMatrix, rc, nu, y0=None) -> np.ndarray:
+    """nu Forward Gauss-Seidel sweeps on A_c y = r_c from y0 (default 0)."""
+    rc = _f64(rc)
+    y = np.zeros(Ac.n) if y0 is None else _f64(y0).copy()
+    lib().orc_coarse_fgs(Ac.n, _p(Ac.rowptr), _p(Ac.col), _p(Ac.val), _p(rc), nu, _p(y))
+    return y

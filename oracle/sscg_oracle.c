@@ -705,3 +705,110 @@ int orc_lanczos_bounds_tri(const orc_op *A, const double *Dm, int iters, const d
     free(D); free(v); free(vp); free(u); free(t); free(al); free(be);
     return m;
 }
+
+/* ------------------------------------------------------------------ */
+/* AMG coarse grid: Galerkin operator A_c = P^T A_f P and Forward      */
+/* Gauss-Seidel on it (§6 "AMG Coarse-Grid            */
+/* Extension", §8; R25) */
+/* ------------------------------------------------------------------ */
+
+/* R25: P is the piecewise-constant (unsmoothed aggregation) prolongation of
+ * bx x by x bz blocks of fine cells: coarse point (I, J, K) aggregates the
+ * fine cells x in [bx I, min(bx I + bx, nx)), likewise y, z; the last block
+ * of each axis may be partial.  P_{g, c} = 1 if fine cell g lies in aggregate
+ * c, else 0.  Coarse points are numbered c = I + ncx (J + ncy K). */
+static long cdiv(long a, long b) { return (a + b - 1) / b; }
+
+long orc_coarse_n(const orc_op *A, int bx, int by, int bz)
+{
+    return cdiv(A->nx, bx) * cdiv(A->ny, by) * cdiv(A->nz, bz);
+}
+
+static long agg_of(const orc_op *A, int bx, int by, int bz, long g)
+{
+    const long i = g % A->nx, j = (g / A->nx) % A->ny, k = g / (A->nx * A->ny);
+    const long ncx = cdiv(A->nx, bx), ncy = cdiv(A->ny, by);
+    return i / bx + ncx * (j / by + ncy * (k / bz));
+}
+
+/* r_c = P^T r_f: r_c[c] = sum of r_f over the cells of aggregate c, added in
+ * ascending fine index */
+void orc_coarse_restrict(const orc_op *A, int bx, int by, int bz, const double *rf, double *rc)
+{
+    const long nf = orc_n(A), nc = orc_coarse_n(A, bx, by, bz);
+    for (long c = 0; c < nc; ++c) rc[c] = 0.0;
+    for (long g = 0; g < nf; ++g) rc[agg_of(A, bx, by, bz, g)] += rf[g];
+}
+
+/* x_f += P y: every fine cell gets the value of its aggregate */
+void orc_coarse_prolong_add(const orc_op *A, int bx, int by, int bz, const double *y, double *xf)
+{
+    const long nf = orc_n(A);
+    for (long g = 0; g < nf; ++g) xf[g] += y[agg_of(A, bx, by, bz, g)];
+}
+
+/* A_c = P^T A_f P formed column by column, as the definition reads: column c
+ * is P^T (A_f p_c), p_c = P e_c the indicator of aggregate c (one full fine
+ * operator application and one restriction per column).  Stored as CSR of
+ * its rows -- entry (i, c) is the i-th component of column c; the nonzero
+ * entries of each row in ascending column order (a row of the CSR is filled
+ * by walking the columns in order: data movement only).  rowptr[nc + 1],
+ * col / val with room for `cap` entries.  Returns nnz, or -1 if cap is too
+ * small.  Cost O(n_c n_f): test sizes only. */
+long orc_coarse_galerkin(const orc_op *A, int bx, int by, int bz, long *rowptr, long *col, double *val, long cap)
+{
+    const long nf = orc_n(A), nc = orc_coarse_n(A, bx, by, bz);
+    double *p = (double *)calloc((size_t)nf, sizeof(double));
+    double *w = (double *)malloc((size_t)nf * sizeof(double));
+    double *t = (double *)malloc((size_t)nc * sizeof(double));
+    long *ccol = (long *)malloc((size_t)cap * sizeof(long)), *crow = (long *)malloc((size_t)cap * sizeof(long));
+    double *cval = (double *)malloc((size_t)cap * sizeof(double));
+    long nnz = 0;
+    for (long c = 0; c < nc && nnz >= 0; ++c) {
+        for (long g = 0; g < nf; ++g) p[g] = (agg_of(A, bx, by, bz, g) == c) ? 1.0 : 0.0;
+        orc_apply(A, p, w);
+        orc_coarse_restrict(A, bx, by, bz, w, t);
+        for (long i = 0; i < nc; ++i) {
+            if (t[i] == 0.0) continue;
+            if (nnz == cap) { nnz = -1; break; }
+            crow[nnz] = i; ccol[nnz] = c; cval[nnz] = t[i];
+            ++nnz;
+        }
+    }
+    if (nnz >= 0) {
+        /* CSC (column-major walk) -> CSR: count per row, prefix, fill */
+        for (long i = 0; i <= nc; ++i) rowptr[i] = 0;
+        for (long q = 0; q < nnz; ++q) rowptr[crow[q] + 1] += 1;
+        for (long i = 0; i < nc; ++i) rowptr[i + 1] += rowptr[i];
+        long *fill = (long *)malloc((size_t)(nc + 1) * sizeof(long));
+        for (long i = 0; i <= nc; ++i) fill[i] = rowptr[i];
+        for (long q = 0; q < nnz; ++q) {   /* columns ascending */
+            const long d = fill[crow[q]]++;
+            col[d] = ccol[q];
+            val[d] = cval[q];
+        }
+        free(fill);
+    }
+    free(p); free(w); free(t); free(ccol); free(crow); free(cval);
+    return nnz;
+}
+
+/* Forward Gauss-Seidel on A_c y = r_c ("FGS converges
+ * uniformly ... requiring nu = 10-30 iterations"; §8 nu_coarse = 20 at the
+ * coarsest level): nu sweeps, each over i = 0 .. n_c-1 in order,
+ *     y_i <- (r_i - sum_{j != i} a_ij y_j) / a_ii,
+ * the sum over row i's entries in ascending j (the latest y_j: updated for
+ * j < i in this sweep).  y holds the initial guess on entry. */
+void orc_coarse_fgs(long nc, const long *rowptr, const long *col, const double *val, const double *rc, int nu,
+                    double *y)
+{
+    for (int sweep = 0; sweep < nu; ++sweep)
+        for (long i = 0; i < nc; ++i) {
+            double acc = rc[i], aii = 0.0;
+            for (long q = rowptr[i]; q < rowptr[i + 1]; ++q) {
+                if (col[q] == i) aii = val[q];
+                else acc -= val[q] * y[col[q]];
+            }
+            y[i] = acc / aii;
+        }
+}
