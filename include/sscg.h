@@ -329,6 +329,67 @@ SSCG_API sscg_status sscg_query(const sscg_ctx *ctx, int32_t what, int64_t *out)
 
 SSCG_API void sscg_destroy(sscg_ctx *ctx);
 
+/* ------------------------------------------------------------------------
+ * AMG coarse-grid Forward Gauss-Seidel (§6 "AMG Coarse-Grid
+ * Extension": FGS on A_c = P^T A_f P, "implemented in a streaming
+ * (matrix-free) fashion to avoid forming A_c explicitly"
+ * §8: nu_coarse = 20 at the coarsest level, n_c ~ 5000; R25).
+ *
+ * One coarse level of unsmoothed aggregation: P is piecewise constant on
+ * bx x by x bz blocks of fine cells (the last block of an axis may be
+ * partial); coarse point (I, J, K), I < ncx = ceil(nx/bx) etc., has index
+ * I + ncx (J + ncy K) and aggregates fine cells x in [bx I, min(bx I + bx, nx)),
+ * likewise y, z.  A_f: SSCG_OP_STENCIL5_2D (bz must be 1), SSCG_OP_STENCIL7
+ * or SSCG_OP_VARCOEF7 on one process (z0 = 0, nz_proc = nz; face arrays as
+ * for sscg_setup, device, owned by the caller and kept valid for the
+ * handle's lifetime).  Their A_c couples only face-adjacent aggregates.
+ *
+ * Modes:
+ *   SSCG_COARSE_STREAMING  A_c is never stored: every visit of a coarse row
+ *                          recomputes its (at most 7) entries from the fine
+ *                          operator -- entry (I, J) is the sum over the cells
+ *                          a of aggregate I of (A_f p_J)_a, p_J = P e_J.
+ *   SSCG_COARSE_ASSEMBLED  the entries are formed once at create (7 n_c
+ *                          doubles, the same arithmetic) and read by FGS.
+ * Both give results bitwise equal to the definition written out in the
+ * oracle (entry sums in ascending fine index, Gauss-Seidel row sums in
+ * ascending coarse index, no fused multiply-add).
+ *
+ * Calls are asynchronous on `stream` (a cudaStream_t; NULL = the legacy
+ * default stream); vectors are device pointers.  The FGS kernel keeps r_c and
+ * y in one CTA's shared memory: n_c <= SSCG_COARSE_MAX_N.
+ * Errors: SSCG_ERR_INVALID (null pointers, b < 1, nu < 0, bz != 1 for the 2D
+ * operator), SSCG_ERR_UNSUPPORTED (other operator kinds, n_c too large),
+ * SSCG_ERR_CUDA / SSCG_ERR_OOM.
+ * ------------------------------------------------------------------------ */
+typedef struct sscg_coarse sscg_coarse;
+enum { SSCG_COARSE_STREAMING = 0, SSCG_COARSE_ASSEMBLED = 1 };
+#define SSCG_COARSE_MAX_N 11000
+SSCG_API sscg_status sscg_coarse_create(const sscg_operator *A_f, int32_t bx, int32_t by, int32_t bz, int32_t mode,
+                                        sscg_coarse **out);
+/* r_c = P^T r_f (n_f -> n_c; each aggregate summed in ascending fine index) */
+SSCG_API sscg_status sscg_coarse_restrict(sscg_coarse *h, const double *r_f, double *r_c, void *stream);
+/* x_f += P y (n_c -> n_f) */
+SSCG_API sscg_status sscg_coarse_prolong_add(sscg_coarse *h, const double *y, double *x_f, void *stream);
+/* nu forward Gauss-Seidel sweeps on A_c y = r_c; y holds the initial guess on
+ * entry and the result on return (nu = 10-30) */
+SSCG_API sscg_status sscg_coarse_fgs(sscg_coarse *h, const double *r_c, double *y, int32_t nu, void *stream);
+/* the (at most 7) entries of every coarse row, device out[7 * n_c]: out[d *
+ * n_c + c] = A_c(c, neighbour d of c), d = 0..6 for the neighbours at
+ * z-1, y-1, x-1, c itself, x+1, y+1, z+1 (0 where absent) -- computed by the
+ * same routine FGS uses (streaming) or copied (assembled) */
+SSCG_API sscg_status sscg_coarse_entries(sscg_coarse *h, double *out, void *stream);
+/*   SSCG_COARSE_QUERY_N              n_c
+ *   SSCG_COARSE_QUERY_NCX / _NCY / _NCZ  the coarse grid
+ *   SSCG_COARSE_QUERY_WAVEFRONTS     T = ncx + ncy + ncz - 2 wavefronts t = I + J + K;
+ *                                    an FGS call of nu sweeps runs T + 2 (nu - 1)
+ *                                    barrier-separated steps (sweeps pipelined)
+ *   SSCG_COARSE_QUERY_MATRIX_BYTES   device bytes holding A_c (0 when streaming) */
+enum { SSCG_COARSE_QUERY_N = 0, SSCG_COARSE_QUERY_NCX = 1, SSCG_COARSE_QUERY_NCY = 2, SSCG_COARSE_QUERY_NCZ = 3,
+       SSCG_COARSE_QUERY_WAVEFRONTS = 4, SSCG_COARSE_QUERY_MATRIX_BYTES = 5 };
+SSCG_API sscg_status sscg_coarse_query(const sscg_coarse *h, int32_t what, int64_t *out);
+SSCG_API void sscg_coarse_destroy(sscg_coarse *h);
+
 /* Thread-local description of the last error ("" if none). */
 SSCG_API const char *sscg_last_error(void);
 

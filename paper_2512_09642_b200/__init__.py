@@ -37,7 +37,12 @@ QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS, QUERY_UPDATE_VECTORS, QUERY_GRAM_VECTORS
 
 EXPORTS = ["sscg_partition", "sscg_halo_plan", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host", "sscg_iterate",
            "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect", "sscg_local_shape", "sscg_destroy",
-           "sscg_last_error", "sscg_version", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds", "sscg_query"]
+           "sscg_last_error", "sscg_version", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds", "sscg_query",
+           "sscg_coarse_create", "sscg_coarse_restrict", "sscg_coarse_prolong_add", "sscg_coarse_fgs",
+           "sscg_coarse_entries", "sscg_coarse_query", "sscg_coarse_destroy"]
+COARSE_STREAMING, COARSE_ASSEMBLED = 0, 1
+(COARSE_QUERY_N, COARSE_QUERY_NCX, COARSE_QUERY_NCY, COARSE_QUERY_NCZ, COARSE_QUERY_WAVEFRONTS,
+ COARSE_QUERY_MATRIX_BYTES) = range(6)
 PROF_NAMES = ["basis", "gram", "allreduce", "fgs", "update", "halo", "basis_single"]
 
 
@@ -101,11 +106,21 @@ def load(path: str = LIB_PATH):
     L.sscg_query.argtypes = [vp, i32, C.POINTER(i64)]
     L.sscg_destroy.argtypes = [vp]
     L.sscg_destroy.restype = None
+    L.sscg_coarse_create.argtypes = [C.POINTER(_Operator), i32, i32, i32, i32, C.POINTER(vp)]
+    L.sscg_coarse_restrict.argtypes = [vp, vp, vp, vp]
+    L.sscg_coarse_prolong_add.argtypes = [vp, vp, vp, vp]
+    L.sscg_coarse_fgs.argtypes = [vp, vp, vp, i32, vp]
+    L.sscg_coarse_entries.argtypes = [vp, vp, vp]
+    L.sscg_coarse_query.argtypes = [vp, i32, C.POINTER(i64)]
+    L.sscg_coarse_destroy.argtypes = [vp]
+    L.sscg_coarse_destroy.restype = None
     L.sscg_last_error.restype = C.c_char_p
     L.sscg_version.restype = C.c_char_p
     for name in ("sscg_partition", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host",
                  "sscg_iterate", "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect",
-                 "sscg_local_shape", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds", "sscg_query"):
+                 "sscg_local_shape", "sscg_set_bounds", "sscg_set_option", "sscg_estimate_bounds", "sscg_query",
+                 "sscg_coarse_create", "sscg_coarse_restrict", "sscg_coarse_prolong_add", "sscg_coarse_fgs",
+                 "sscg_coarse_entries", "sscg_coarse_query"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -348,3 +363,83 @@ class Solver:
         g = self.inspect(INSPECT_GRAM, k)
         s = self.s
         return g[: s * s].reshape(s, s), g[s * s:]
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class CoarseFGS:
+    """AMG coarse-grid Forward Gauss-Seidel (sscg_coarse_*; PAPER.md:225-246,
+    347-354; R25): one coarse level of b = (bx, by, bz) aggregates of
+    the fine operator ``op`` (Stencil '5pt', '7pt' or 'varcoef7'), A_c = P^T A_f P
+    never stored (mode 'streaming') or formed once ('assembled').  Vectors are
+    float64 CUDA tensors; calls run on torch's current stream."""
+
+    def __init__(self, op: Stencil, b=(2, 2, 2), mode: str = "streaming"):
+        L = load()
+        self.op = op   # keeps the face tensors alive
+        m = {"streaming": COARSE_STREAMING, "assembled": COARSE_ASSEMBLED}[mode]
+        h = C.c_void_p()
+        _check(L.sscg_coarse_create(C.byref(op._struct()), b[0], b[1], b[2], m, C.byref(h)))
+        self._h = h
+        self.b = tuple(b)
+        self.n_fine = op.nx * op.ny * op.nz
+        self.n = self.query(COARSE_QUERY_N)
+        self.dims = (self.query(COARSE_QUERY_NCX), self.query(COARSE_QUERY_NCY), self.query(COARSE_QUERY_NCZ))
+
+    def query(self, what: int) -> int:
+        v = C.c_int64()
+        _check(load().sscg_coarse_query(self._h, what, C.byref(v)))
+        return v.value
+
+    def restrict(self, rf, rc=None):
+        """r_c = P^T r_f"""
+        import torch
+        _check_dev("rf", rf, self.n_fine)
+        rc = torch.empty(self.n, dtype=torch.float64, device=rf.device) if rc is None else rc
+        _check_dev("rc", rc, self.n)
+        _check(load().sscg_coarse_restrict(self._h, _ptr(rf), _ptr(rc), _stream()))
+        return rc
+
+    def prolong_add(self, y, xf):
+        """x_f += P y (in place)"""
+        _check_dev("y", y, self.n)
+        _check_dev("xf", xf, self.n_fine)
+        _check(load().sscg_coarse_prolong_add(self._h, _ptr(y), _ptr(xf), _stream()))
+        return xf
+
+    def fgs(self, rc, nu: int, y=None):
+        """nu forward Gauss-Seidel sweeps on A_c y = r_c from y (zero if None);
+        y is updated in place and returned"""
+        import torch
+        _check_dev("rc", rc, self.n)
+        y = torch.zeros(self.n, dtype=torch.float64, device=rc.device) if y is None else y
+        _check_dev("y", y, self.n)
+        _check(load().sscg_coarse_fgs(self._h, _ptr(rc), _ptr(y), int(nu), _stream()))
+        return y
+
+    def entries(self):
+        """(7, n_c) row entries: neighbours z-1, y-1, x-1, itself, x+1, y+1, z+1"""
+        import torch
+        out = torch.empty(7 * self.n, dtype=torch.float64, device="cuda")
+        _check(load().sscg_coarse_entries(self._h, _ptr(out), _stream()))
+        return out.view(7, self.n)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().sscg_coarse_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

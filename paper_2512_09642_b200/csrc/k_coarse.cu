@@ -1,0 +1,394 @@
+// AMG coarse-grid Forward Gauss-Seidel (PAPER.md:225-246
+// §6 "AMG Coarse-Grid Extension", §8; R25).
+//
+// One coarse level of unsmoothed aggregation: P piecewise constant on
+// bx x by x bz blocks of fine cells, A_c = P^T A_f P.  For the 5-point,
+// 7-point and variable-coefficient 7-point operators A_c couples only
+// face-adjacent aggregates, so a coarse row has at most 7 entries.
+//
+//   streaming  (the paper's matrix-free variant): A_c is never stored; each
+//              visit of row I recomputes its entries from A_f -- entry (I, J)
+//              is the sum over the cells a of aggregate I of (A_f p_J)_a,
+//              p_J = P e_J: a face sum of -k_face for a neighbour, the sum of
+//              the cells' diagonals minus the couplings inside the aggregate
+//              for the diagonal.
+//   assembled  the same entries formed once at create (7 n_c doubles).
+//
+// Forward (lexicographic) Gauss-Seidel needs, for row c, the new values of
+// its lower neighbours (z-1, y-1, x-1) and the previous sweep's values of its
+// upper ones.  With the wavefront index t = I + J + K every lower neighbour
+// lies on t - 1 and every upper one on t + 1, so all rows of a wavefront are
+// independent, and sweep m can run wavefront t while sweep m-1 runs t + 2:
+// step tau processes the wavefronts t = tau - 2m of every sweep m at once, a
+// CTA barrier between steps -- T + 2(nu - 1) steps for nu sweeps instead of
+// nu T.  Rows read only wavefronts t +- 1, which no other sweep writes in the
+// same step, so the result is exactly the sequential sweep order.  r_c and y
+// live in shared memory of one CTA (the coarsest level is small: n_c ~ 5000
+// in the paper); arithmetic in the oracle's order without FMA contraction, so
+// results are bitwise equal to it.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <vector>
+
+#include "../../include/sscg.h"
+#include "sscg_internal.cuh"
+
+namespace sscg {
+sscg_status api_fail(sscg_status st, const char *fmt, ...);
+}
+using sscg::api_fail;
+
+namespace {
+
+struct CG {
+    int kind, nx, ny, nz, bx, by, bz, ncx, ncy, ncz;
+    const double *kx, *ky, *kz;   // VARCOEF7 faces (layout of sscg.h), else null
+};
+
+constexpr int NT = 1024;   // FGS threads (one CTA)
+
+// face coefficients around fine cell (i, j, k); 1 for the constant stencils
+__device__ __forceinline__ double kxm(const CG &g, int i, int j, int k)
+{
+    return g.kx ? g.kx[((int64_t)k * g.ny + j) * (g.nx + 1) + i] : 1.0;
+}
+__device__ __forceinline__ double kxp(const CG &g, int i, int j, int k) { return kxm(g, i + 1, j, k); }
+__device__ __forceinline__ double kym(const CG &g, int i, int j, int k)
+{
+    return g.ky ? g.ky[((int64_t)k * (g.ny + 1) + j) * g.nx + i] : 1.0;
+}
+__device__ __forceinline__ double kyp(const CG &g, int i, int j, int k) { return kym(g, i, j + 1, k); }
+__device__ __forceinline__ double kzm(const CG &g, int i, int j, int k)
+{
+    return g.kz ? g.kz[((int64_t)k * g.ny + j) * g.nx + i] : 1.0;
+}
+__device__ __forceinline__ double kzp(const CG &g, int i, int j, int k) { return kzm(g, i, j, k + 1); }
+
+// the fine diagonal: 4 / 6, or the six faces summed in the order z-, y-, x-, x+, y+, z+
+__device__ __forceinline__ double fine_diag(const CG &g, int i, int j, int k)
+{
+    if (g.kind == SSCG_OP_STENCIL5_2D) return 4.0;
+    if (g.kind == SSCG_OP_STENCIL7) return 6.0;
+    double d = __dadd_rn(kzm(g, i, j, k), kym(g, i, j, k));
+    d = __dadd_rn(d, kxm(g, i, j, k));
+    d = __dadd_rn(d, kxp(g, i, j, k));
+    d = __dadd_rn(d, kyp(g, i, j, k));
+    return __dadd_rn(d, kzp(g, i, j, k));
+}
+
+// the entries of coarse row (I, J, K): e[0..6] for the neighbours z-1, y-1,
+// x-1, itself, x+1, y+1, z+1 (0 where absent).  Each entry is the sum, over
+// the aggregate's cells in ascending fine index, of (A_f p_nbr)_a formed as
+// the fine operator's row is (diagonal first, then the couplings in the order
+// z-, y-, x-, x+, y+, z+; terms of cells outside the neighbour vanish exactly)
+__device__ void coarse_row(const CG &g, int I, int J, int K, double e[7])
+{
+    const int x0 = I * g.bx, x1 = min(x0 + g.bx, g.nx);
+    const int y0 = J * g.by, y1 = min(y0 + g.by, g.ny);
+    const int z0 = K * g.bz, z1 = min(z0 + g.bz, g.nz);
+    double d = 0.0;
+    for (int k = z0; k < z1; ++k)
+        for (int j = y0; j < y1; ++j)
+            for (int i = x0; i < x1; ++i) {
+                double t = fine_diag(g, i, j, k);
+                if (k - 1 >= z0) t = __dsub_rn(t, kzm(g, i, j, k));
+                if (j - 1 >= y0) t = __dsub_rn(t, kym(g, i, j, k));
+                if (i - 1 >= x0) t = __dsub_rn(t, kxm(g, i, j, k));
+                if (i + 1 < x1) t = __dsub_rn(t, kxp(g, i, j, k));
+                if (j + 1 < y1) t = __dsub_rn(t, kyp(g, i, j, k));
+                if (k + 1 < z1) t = __dsub_rn(t, kzp(g, i, j, k));
+                d = __dadd_rn(d, t);
+            }
+    e[3] = d;
+    double a = 0.0;
+    if (K > 0)
+        for (int j = y0; j < y1; ++j)
+            for (int i = x0; i < x1; ++i) a = __dsub_rn(a, kzm(g, i, j, z0));
+    e[0] = a;
+    a = 0.0;
+    if (J > 0)
+        for (int k = z0; k < z1; ++k)
+            for (int i = x0; i < x1; ++i) a = __dsub_rn(a, kym(g, i, y0, k));
+    e[1] = a;
+    a = 0.0;
+    if (I > 0)
+        for (int k = z0; k < z1; ++k)
+            for (int j = y0; j < y1; ++j) a = __dsub_rn(a, kxm(g, x0, j, k));
+    e[2] = a;
+    a = 0.0;
+    if (I + 1 < g.ncx)
+        for (int k = z0; k < z1; ++k)
+            for (int j = y0; j < y1; ++j) a = __dsub_rn(a, kxp(g, x1 - 1, j, k));
+    e[4] = a;
+    a = 0.0;
+    if (J + 1 < g.ncy)
+        for (int k = z0; k < z1; ++k)
+            for (int i = x0; i < x1; ++i) a = __dsub_rn(a, kyp(g, i, y1 - 1, k));
+    e[5] = a;
+    a = 0.0;
+    if (K + 1 < g.ncz)
+        for (int j = y0; j < y1; ++j)
+            for (int i = x0; i < x1; ++i) a = __dsub_rn(a, kzp(g, i, j, z1 - 1));
+    e[6] = a;
+}
+
+__global__ void k_coarse_entries(CG g, double *out)
+{
+    const int nc = g.ncx * g.ncy * g.ncz;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+        const int I = c % g.ncx, J = (c / g.ncx) % g.ncy, K = c / (g.ncx * g.ncy);
+        double e[7];
+        coarse_row(g, I, J, K, e);
+#pragma unroll
+        for (int d = 0; d < 7; ++d) out[(int64_t)d * nc + c] = e[d];
+    }
+}
+
+// r_c = P^T r_f: one coarse point per thread, its cells in ascending fine index
+__global__ void k_coarse_restrict(CG g, const double *rf, double *rc)
+{
+    const int nc = g.ncx * g.ncy * g.ncz;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+        const int I = c % g.ncx, J = (c / g.ncx) % g.ncy, K = c / (g.ncx * g.ncy);
+        const int x0 = I * g.bx, x1 = min(x0 + g.bx, g.nx);
+        const int y0 = J * g.by, y1 = min(y0 + g.by, g.ny);
+        const int z0 = K * g.bz, z1 = min(z0 + g.bz, g.nz);
+        double a = 0.0;
+        for (int k = z0; k < z1; ++k)
+            for (int j = y0; j < y1; ++j)
+                for (int i = x0; i < x1; ++i) a = __dadd_rn(a, rf[((int64_t)k * g.ny + j) * g.nx + i]);
+        rc[c] = a;
+    }
+}
+
+// x_f += P y: one fine cell per thread
+__global__ void k_coarse_prolong(CG g, const double *y, double *xf)
+{
+    const int64_t nf = (int64_t)g.nx * g.ny * g.nz;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nf; q += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(q % g.nx), j = (int)((q / g.nx) % g.ny), k = (int)(q / ((int64_t)g.nx * g.ny));
+        const int c = i / g.bx + g.ncx * (j / g.by + g.ncy * (k / g.bz));
+        xf[q] = __dadd_rn(xf[q], y[c]);
+    }
+}
+
+// nu pipelined Gauss-Seidel sweeps (see the file comment).  Shared memory:
+// y[nc], r[nc], the wavefront lists (points of wavefront t at
+// pts[off[t] .. off[t+1]), ascending index) and off[T+1].
+template <bool STREAM>
+__global__ void __launch_bounds__(NT, 1)
+    k_coarse_fgs(CG g, const double *__restrict__ A7, const double *rc, double *y, int nu, const int *wf_pts,
+                 const int *wf_off, int T)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int nc = g.ncx * g.ncy * g.ncz, sxy = g.ncx * g.ncy;
+    double *ys = sm, *rs = sm + nc;
+    int *pts = reinterpret_cast<int *>(rs + nc), *off = pts + nc;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < nc; i += NT) {
+        ys[i] = y[i];
+        rs[i] = rc[i];
+        pts[i] = wf_pts[i];
+    }
+    for (int i = tid; i <= T; i += NT) off[i] = wf_off[i];
+    __syncthreads();
+    const int steps = nu > 0 ? T + 2 * (nu - 1) : 0;
+    for (int tau = 0; tau < steps; ++tau) {
+        const int a = tau - (T - 1);
+        const int m_lo = a > 0 ? (a + 1) / 2 : 0, m_hi = min(nu - 1, tau / 2);
+        int base = 0;   // items of the step so far: thread tid takes items tid, tid + NT, ...
+        for (int m = m_lo; m <= m_hi; ++m) {
+            const int t = tau - 2 * m, o0 = off[t], cnt = off[t + 1] - o0;
+            int l = tid - base % NT;
+            if (l < 0) l += NT;
+            for (; l < cnt; l += NT) {
+                const int c = pts[o0 + l];
+                const int I = c % g.ncx, J = (c / g.ncx) % g.ncy, K = c / sxy;
+                double e[7];
+                if (STREAM) {
+                    coarse_row(g, I, J, K, e);
+                } else {
+#pragma unroll
+                    for (int d = 0; d < 7; ++d) e[d] = __ldg(A7 + (int64_t)d * nc + c);
+                }
+                // y_c = (r_c - sum_{j != c} a_cj y_j) / a_cc, j ascending
+                double s = rs[c];
+                if (K > 0) s = __dsub_rn(s, __dmul_rn(e[0], ys[c - sxy]));
+                if (J > 0) s = __dsub_rn(s, __dmul_rn(e[1], ys[c - g.ncx]));
+                if (I > 0) s = __dsub_rn(s, __dmul_rn(e[2], ys[c - 1]));
+                if (I + 1 < g.ncx) s = __dsub_rn(s, __dmul_rn(e[4], ys[c + 1]));
+                if (J + 1 < g.ncy) s = __dsub_rn(s, __dmul_rn(e[5], ys[c + g.ncx]));
+                if (K + 1 < g.ncz) s = __dsub_rn(s, __dmul_rn(e[6], ys[c + sxy]));
+                ys[c] = __ddiv_rn(s, e[3]);
+            }
+            base += cnt;
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < nc; i += NT) y[i] = ys[i];
+}
+
+size_t fgs_smem(int nc, int T) { return (size_t)nc * 16 + (size_t)nc * 4 + (size_t)(T + 1) * 4; }
+
+}  // namespace
+
+struct sscg_coarse {
+    CG g{};
+    int mode = 0, nc = 0, T = 0;
+    double *A7 = nullptr;
+    int *wf_pts = nullptr, *wf_off = nullptr;
+};
+
+#define CCU(call)                                                                                   \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return api_fail(e_ == cudaErrorMemoryAllocation ? SSCG_ERR_OOM : SSCG_ERR_CUDA, "%s: %s", #call, \
+                            cudaGetErrorString(e_));                                                \
+    } while (0)
+
+static unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8); }
+
+extern "C" void sscg_coarse_destroy(sscg_coarse *h)
+{
+    if (!h) return;
+    cudaFree(h->A7);
+    cudaFree(h->wf_pts);
+    cudaFree(h->wf_off);
+    delete h;
+}
+
+extern "C" sscg_status sscg_coarse_create(const sscg_operator *A, int32_t bx, int32_t by, int32_t bz, int32_t mode,
+                                          sscg_coarse **out)
+{
+    if (!A || !out) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_create: null argument");
+    *out = nullptr;
+    if (A->kind != SSCG_OP_STENCIL5_2D && A->kind != SSCG_OP_STENCIL7 && A->kind != SSCG_OP_VARCOEF7)
+        return api_fail(SSCG_ERR_UNSUPPORTED, "sscg_coarse_create: operator kind %d (5-point, 7-point and "
+                        "variable-coefficient 7-point only)", (int)A->kind);
+    if (bx < 1 || by < 1 || bz < 1 || A->nx < 1 || A->ny < 1 || A->nz < 1)
+        return api_fail(SSCG_ERR_INVALID, "sscg_coarse_create: bad grid or aggregate size");
+    if (A->kind == SSCG_OP_STENCIL5_2D && (A->nz != 1 || bz != 1))
+        return api_fail(SSCG_ERR_INVALID, "sscg_coarse_create: the 2D operator needs nz = bz = 1");
+    if (A->kind == SSCG_OP_VARCOEF7 && (!A->kx || !A->ky || !A->kz))
+        return api_fail(SSCG_ERR_INVALID, "sscg_coarse_create: face arrays missing");
+    if (mode != SSCG_COARSE_STREAMING && mode != SSCG_COARSE_ASSEMBLED)
+        return api_fail(SSCG_ERR_INVALID, "sscg_coarse_create: mode %d", (int)mode);
+    if (A->nx > (1 << 20) || A->ny > (1 << 20) || A->nz > (1 << 20))
+        return api_fail(SSCG_ERR_INVALID, "sscg_coarse_create: grid too large");
+    CG g{};
+    g.kind = A->kind;
+    g.nx = (int)A->nx; g.ny = (int)A->ny; g.nz = (int)A->nz;
+    g.bx = bx; g.by = by; g.bz = bz;
+    g.ncx = (g.nx + bx - 1) / bx; g.ncy = (g.ny + by - 1) / by; g.ncz = (g.nz + bz - 1) / bz;
+    if (A->kind == SSCG_OP_VARCOEF7) {
+        g.kx = A->kx; g.ky = A->ky; g.kz = A->kz;
+    }
+    const int64_t nc = (int64_t)g.ncx * g.ncy * g.ncz;
+    if (nc > SSCG_COARSE_MAX_N)
+        return api_fail(SSCG_ERR_UNSUPPORTED, "sscg_coarse_create: n_c = %lld > %d (one CTA's shared memory)",
+                        (long long)nc, SSCG_COARSE_MAX_N);
+    auto *h = new sscg_coarse;
+    h->g = g;
+    h->mode = mode;
+    h->nc = (int)nc;
+    h->T = g.ncx + g.ncy + g.ncz - 2;
+    // wavefront lists: points with I + J + K = t, ascending index
+    std::vector<int> off(h->T + 2, 0), pts(nc);
+    for (int64_t c = 0; c < nc; ++c) {
+        const int I = (int)(c % g.ncx), J = (int)((c / g.ncx) % g.ncy), K = (int)(c / ((int64_t)g.ncx * g.ncy));
+        off[I + J + K + 1] += 1;
+    }
+    for (int t = 0; t <= h->T; ++t) off[t + 1] += off[t];
+    std::vector<int> fill(off.begin(), off.end());
+    for (int64_t c = 0; c < nc; ++c) {
+        const int I = (int)(c % g.ncx), J = (int)((c / g.ncx) % g.ncy), K = (int)(c / ((int64_t)g.ncx * g.ncy));
+        pts[fill[I + J + K]++] = (int)c;
+    }
+    auto bail = [&](sscg_status st) {
+        sscg_coarse_destroy(h);
+        return st;
+    };
+    cudaError_t e = cudaMalloc(&h->wf_pts, nc * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&h->wf_off, (h->T + 2) * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemcpy(h->wf_pts, pts.data(), nc * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->wf_off, off.data(), (h->T + 2) * sizeof(int), cudaMemcpyHostToDevice);
+    const int smem = (int)fgs_smem(h->nc, h->T);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_coarse_fgs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_coarse_fgs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess && mode == SSCG_COARSE_ASSEMBLED) {
+        e = cudaMalloc(&h->A7, 7 * nc * sizeof(double));
+        if (e == cudaSuccess) {
+            k_coarse_entries<<<grid_for(nc), 256>>>(g, h->A7);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    if (e != cudaSuccess)
+        return bail(api_fail(e == cudaErrorMemoryAllocation ? SSCG_ERR_OOM : SSCG_ERR_CUDA, "sscg_coarse_create: %s",
+                             cudaGetErrorString(e)));
+    *out = h;
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_coarse_restrict(sscg_coarse *h, const double *rf, double *rc, void *stream)
+{
+    if (!h || !rf || !rc) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_restrict: null argument");
+    k_coarse_restrict<<<grid_for(h->nc), 256, 0, (cudaStream_t)stream>>>(h->g, rf, rc);
+    CCU(cudaGetLastError());
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_coarse_prolong_add(sscg_coarse *h, const double *y, double *xf, void *stream)
+{
+    if (!h || !y || !xf) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_prolong_add: null argument");
+    const int64_t nf = (int64_t)h->g.nx * h->g.ny * h->g.nz;
+    k_coarse_prolong<<<grid_for(nf), 256, 0, (cudaStream_t)stream>>>(h->g, y, xf);
+    CCU(cudaGetLastError());
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_coarse_fgs(sscg_coarse *h, const double *rc, double *y, int32_t nu, void *stream)
+{
+    if (!h || !rc || !y) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_fgs: null argument");
+    if (nu < 0) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_fgs: nu = %d", (int)nu);
+    if (nu == 0) return SSCG_OK;
+    const size_t smem = fgs_smem(h->nc, h->T);
+    if (h->mode == SSCG_COARSE_STREAMING)
+        k_coarse_fgs<true><<<1, NT, smem, (cudaStream_t)stream>>>(h->g, nullptr, rc, y, nu, h->wf_pts, h->wf_off, h->T);
+    else
+        k_coarse_fgs<false><<<1, NT, smem, (cudaStream_t)stream>>>(h->g, h->A7, rc, y, nu, h->wf_pts, h->wf_off, h->T);
+    CCU(cudaGetLastError());
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_coarse_entries(sscg_coarse *h, double *out, void *stream)
+{
+    if (!h || !out) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_entries: null argument");
+    if (h->mode == SSCG_COARSE_ASSEMBLED) {
+        CCU(cudaMemcpyAsync(out, h->A7, 7 * (size_t)h->nc * sizeof(double), cudaMemcpyDeviceToDevice,
+                            (cudaStream_t)stream));
+    } else {
+        k_coarse_entries<<<grid_for(h->nc), 256, 0, (cudaStream_t)stream>>>(h->g, out);
+        CCU(cudaGetLastError());
+    }
+    return SSCG_OK;
+}
+
+extern "C" sscg_status sscg_coarse_query(const sscg_coarse *h, int32_t what, int64_t *out)
+{
+    if (!h || !out) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_query: null argument");
+    switch (what) {
+    case SSCG_COARSE_QUERY_N: *out = h->nc; break;
+    case SSCG_COARSE_QUERY_NCX: *out = h->g.ncx; break;
+    case SSCG_COARSE_QUERY_NCY: *out = h->g.ncy; break;
+    case SSCG_COARSE_QUERY_NCZ: *out = h->g.ncz; break;
+    case SSCG_COARSE_QUERY_WAVEFRONTS: *out = h->T; break;
+    case SSCG_COARSE_QUERY_MATRIX_BYTES: *out = h->A7 ? 7 * (int64_t)h->nc * 8 : 0; break;
+    default: return api_fail(SSCG_ERR_INVALID, "sscg_coarse_query: unknown key %d", (int)what);
+    }
+    return SSCG_OK;
+}

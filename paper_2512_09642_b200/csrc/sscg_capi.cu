@@ -40,6 +40,20 @@ static sscg_status fail(sscg_status st, const char *fmt, ...)
     return st;
 }
 
+// for the other C-ABI translation units (k_coarse.cu)
+namespace sscg {
+sscg_status api_fail(sscg_status st, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+}  // namespace sscg
+
 #define CU(call)                                                                                   \
     do {                                                                                           \
         cudaError_t e_ = (call);                                                                   \

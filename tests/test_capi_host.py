@@ -112,3 +112,22 @@ def test_c_example_solves(tmp_path):
     r = subprocess.run([exe, "48", "16", "25"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "converged=1" in r.stdout
+
+
+def test_coarse_create_validates_before_touching_the_device(lib):
+    """sscg_coarse_create (R25) rejects unsupported operators, bad
+    aggregate sizes and coarse levels beyond one CTA's shared memory on the
+    host, before any CUDA call (so these paths run without a GPU)."""
+    def create(kind, dims, b, mode=0):
+        op = sscg._Operator(kind, *dims, None, None, None, 0, None, None, None)
+        h = C.c_void_p()
+        return lib.sscg_coarse_create(C.byref(op), *b, mode, C.byref(h))
+    assert create(sscg.OP_STENCIL27, (8, 8, 8), (2, 2, 2)) == sscg.ERR_UNSUPPORTED
+    assert create(sscg.OP_CSR, (0, 0, 0), (1, 1, 1)) == sscg.ERR_UNSUPPORTED
+    assert create(sscg.OP_STENCIL7, (64, 64, 64), (2, 2, 2)) == sscg.ERR_UNSUPPORTED   # n_c = 32768
+    assert b"n_c" in lib.sscg_last_error()
+    assert create(sscg.OP_STENCIL7, (8, 8, 8), (0, 2, 2)) == sscg.ERR_INVALID
+    assert create(sscg.OP_STENCIL5_2D, (16, 16, 1), (2, 2, 2)) == sscg.ERR_INVALID     # 2D needs bz = 1
+    assert create(sscg.OP_VARCOEF7, (8, 8, 8), (2, 2, 2)) == sscg.ERR_INVALID          # faces missing
+    assert create(sscg.OP_STENCIL7, (8, 8, 8), (2, 2, 2), mode=2) == sscg.ERR_INVALID
+    assert lib.sscg_coarse_fgs(None, None, None, 1, None) == sscg.ERR_INVALID
