@@ -321,6 +321,12 @@ struct K5Params {
     int64_t xoff;         //   this launch updates (*xpp)[xoff ...]; read per launch so one
                           //   captured graph serves every x (sscg_solve / sscg_iterate)
     int nx, pitch;
+    // w_{s-1} folded (DESIGN.md §6 "w_{s-1} fold"): not stored by the basis
+    // kernels; formed here as A p_{s-1} (7-point, constant centre) from
+    // p_{s-1} and its six neighbours (ghost planes current)
+    int ny;
+    int64_t plane;
+    double inv_nx, inv_ny, center;
 };
 
 // flat path: pitch == nx and x 16-B aligned; 2 points per thread per step.
@@ -334,7 +340,14 @@ struct K5Params {
 // 2 out) instead of P, W and x (2s+1 in): the per-point rounding is of the
 // same order as forming W alpha from the stored W (whose SpMV entries carry
 // the same m |p| cancellation), unlike the Gram dots, which keep W.
-template <int S, bool REC>
+//
+// FOLD (REC only): w_{s-1} = A p_{s-1} is not read but formed per point pair
+// from p_{s-1} (x+-1 from the neighbouring pairs, y+-1 and z+-1 from the rows /
+// planes around it, zero outside the grid in x and y; the ghost planes carry
+// the z neighbours), in the order of the single step it replaces: centre
+// term minus (z-1, y-1, x-1, x+1, y+1, z+1).  p_{s-1} is then loaded with
+// the default cache policy, since the neighbouring points re-read it from L2.
+template <int S, bool REC, bool FOLD>
 __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState *st)
 {
     PDL_ENTRY(st);
@@ -367,7 +380,7 @@ __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState 
         if (REC) {
 #pragma unroll
             for (int j = 0; j < s; ++j) {
-                const double2 pj = (j == 0) ? p0 : __ldcs(P2 + j * vs2 + e);
+                const double2 pj = (j == 0) ? p0 : (FOLD && j == s - 1) ? __ldg(P2 + j * vs2 + e) : __ldcs(P2 + j * vs2 + e);
                 ax.x = fma(al[j], pj.x, ax.x); ax.y = fma(al[j], pj.y, ax.y);
                 aw.x = fma(ga[j], pj.x, aw.x); aw.y = fma(ga[j], pj.y, aw.y);
             }
@@ -376,7 +389,32 @@ __global__ void __launch_bounds__(256) k5_update_vec(K5Params k, const DevState 
                 aw.x *= m.x;
                 aw.y *= m.y;
             }
-            const double2 wl = __ldcs(W2 + (s - 1) * vs2 + e);
+            double2 wl;
+            if (FOLD) {
+                const double2 *q2 = P2 + (s - 1) * vs2;
+                const double *q = reinterpret_cast<const double *>(q2);
+                const double2 c = __ldg(q2 + e);
+                // all neighbour loads are in bounds (the ghost planes bracket the
+                // launch range), issued before the coordinates mask them
+                const int64_t py = k.pitch >> 1, pz = k.plane >> 1;
+                double l = __ldg(q + 2 * e - 1), rr = __ldg(q + 2 * e + 2);
+                double2 ylo = __ldg(q2 + e - py), yhi = __ldg(q2 + e + py);
+                const double2 dn = __ldg(q2 + e - pz), up = __ldg(q2 + e + pz);
+                // grid coordinates of the pair's first point (rows of the
+                // launch range start on a plane boundary; exact in FP64)
+                const double fe = (double)(2 * e);
+                const double row = floor((fe + 0.5) * k.inv_nx);
+                const int x = (int)(fe - row * (double)k.nx);
+                const int y = (int)(row - floor((row + 0.5) * k.inv_ny) * (double)k.ny);
+                if (x == 0) l = 0.0;
+                if (x + 2 >= k.nx) rr = 0.0;
+                if (y == 0) ylo = make_double2(0.0, 0.0);
+                if (y + 1 >= k.ny) yhi = make_double2(0.0, 0.0);
+                wl.x = k.center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+                wl.y = k.center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+            } else {
+                wl = __ldcs(W2 + (s - 1) * vs2 + e);
+            }
             aw.x = fma(al[s - 1], wl.x, aw.x); aw.y = fma(al[s - 1], wl.y, aw.y);
         } else {
 #pragma unroll
@@ -556,7 +594,8 @@ void launch_kappa(const double *blk, int s, const DevState *st, double *h_kappa,
 }
 
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *const *xpp, int64_t xoff,
-               const DevState *st, cudaStream_t stream, int zb, int ze, double theta, double sigma, bool rec)
+               const DevState *st, cudaStream_t stream, int zb, int ze, double theta, double sigma, bool rec,
+               bool fold)
 {
     if (ze < 0) ze = sl.nzl + 1;
     if (ze <= zb) return;
@@ -576,6 +615,11 @@ void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double 
     k.alpha = alpha;
     k.nx = g.nx;
     k.pitch = g.pitch;
+    k.ny = g.ny;
+    k.plane = g.plane;
+    k.inv_nx = 1.0 / g.nx;
+    k.inv_ny = 1.0 / g.ny;
+    k.center = g.center;
     const bool vec = (g.pitch == g.nx) && (k.N % 2 == 0) && (k.xoff % 2 == 0);
     const int64_t work = vec ? k.N / 2 : k.N;
     int64_t blocks = (work + 255) / 256;
@@ -584,23 +628,31 @@ void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double 
 #endif
     const int64_t cap = (int64_t)k2_grid() * K5_BLOCKS_PER_SM;
     if (blocks > cap) blocks = cap;
-    if (vec && k.rec) {
+    // fold => rec and pitch == nx with nx even (uses_wlfold), so the flat path applies
+    if (vec && k.rec && fold) {
         switch (s) {
-        case 4: launch_pdl(g.kn.pdl, k5_update_vec<4, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        case 8: launch_pdl(g.kn.pdl, k5_update_vec<8, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        case 16: launch_pdl(g.kn.pdl, k5_update_vec<16, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        case 24: launch_pdl(g.kn.pdl, k5_update_vec<24, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        case 32: launch_pdl(g.kn.pdl, k5_update_vec<32, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        default: launch_pdl(g.kn.pdl, k5_update_vec<0, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 16: launch_pdl(g.kn.pdl, k5_update_vec<16, true, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 24: launch_pdl(g.kn.pdl, k5_update_vec<24, true, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 32: launch_pdl(g.kn.pdl, k5_update_vec<32, true, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        default: launch_pdl(g.kn.pdl, k5_update_vec<0, true, true>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        }
+    } else if (vec && k.rec) {
+        switch (s) {
+        case 4: launch_pdl(g.kn.pdl, k5_update_vec<4, true, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 8: launch_pdl(g.kn.pdl, k5_update_vec<8, true, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 16: launch_pdl(g.kn.pdl, k5_update_vec<16, true, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 24: launch_pdl(g.kn.pdl, k5_update_vec<24, true, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 32: launch_pdl(g.kn.pdl, k5_update_vec<32, true, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        default: launch_pdl(g.kn.pdl, k5_update_vec<0, true, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
         }
     } else if (vec) {
         switch (s) {
-        case 4: launch_pdl(g.kn.pdl, k5_update_vec<4, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        case 8: launch_pdl(g.kn.pdl, k5_update_vec<8, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        case 16: launch_pdl(g.kn.pdl, k5_update_vec<16, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        case 24: launch_pdl(g.kn.pdl, k5_update_vec<24, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        case 32: launch_pdl(g.kn.pdl, k5_update_vec<32, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
-        default: launch_pdl(g.kn.pdl, k5_update_vec<0, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 4: launch_pdl(g.kn.pdl, k5_update_vec<4, false, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 8: launch_pdl(g.kn.pdl, k5_update_vec<8, false, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 16: launch_pdl(g.kn.pdl, k5_update_vec<16, false, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 24: launch_pdl(g.kn.pdl, k5_update_vec<24, false, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        case 32: launch_pdl(g.kn.pdl, k5_update_vec<32, false, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
+        default: launch_pdl(g.kn.pdl, k5_update_vec<0, false, false>, dim3((unsigned)blocks), dim3(256), 0, stream, k, st); break;
         }
     }
     else launch_pdl(g.kn.pdl, k5_update_gen, dim3((unsigned)blocks), dim3(256), 0, stream, k, st);

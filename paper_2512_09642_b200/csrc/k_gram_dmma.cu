@@ -242,11 +242,20 @@ struct K2RParams {
     unsigned *ticket;
 };
 
-template <int NB, int EP, bool VARM>
+// PAP (the w_{s-1} fold; constant diagonal only): w_{s-1} is
+// not stored and not read.  Its fragment row is zero, and the pass forms the
+// LOWER block triangle instead, A being symmetric:
+//   Ghat_{ij} = p_i^T A p_j = (A p_i)^T p_j = w_i^T p_j,  i <= j,
+// from tile (J, I) -- p_j against the recovered w_i, i < j --, so no entry
+// needs w_{s-1} except the diagonal p_{s-1}^T A p_{s-1}, left 0 here and
+// written by k_pap (one stencil pass over p_{s-1}, a reduction).  Same tile
+// count and DMMA work as the upper triangle.
+template <int NB, int EP, bool VARM, bool PAP = false>
 __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     k2r(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmWl,
         const __grid_constant__ CUtensorMap tmDv, K2RParams k, const DevState *st)
 {
+    static_assert(!(PAP && VARM), "the fold needs a constant diagonal");
     PDL_ENTRY(st);
     constexpr int SP = 8 * NB;
     constexpr int NCW = ncw_for(NB, VARM), THREADS = threads_for(NB, VARM);
@@ -262,7 +271,7 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     __shared__ bool is_last;
     const int s = k.s, NS = k.nstage;
     const int stage_elems = SP * EP + k.wlp * (VARM ? 2 : 1);
-    const uint32_t stage_bytes = (uint32_t)(SP * EP + EP * (VARM ? 2 : 1)) * 8u;   // bytes the TMA delivers
+    const uint32_t stage_bytes = (uint32_t)(SP * EP + EP * (PAP ? 0 : VARM ? 2 : 1)) * 8u;   // bytes the TMA delivers
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nchunks = (k.N + EP - 1) / EP;
     const int nit = (int)((nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x);
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
         }
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
-        tma_prefetch_desc(&tmWl);
+        if (!PAP) tma_prefetch_desc(&tmWl);
         if (VARM) tma_prefetch_desc(&tmDv);
     }
     __syncthreads();
@@ -304,7 +313,7 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
                 const int x = (int)((blockIdx.x + (int64_t)it * gridDim.x) * EP);
                 mbar_expect_tx(&full[stg], stage_bytes);
                 tma_load_2d(dst, &tmP, x, 0, &full[stg]);
-                tma_load_2d(dst + SP * EP, &tmWl, x, s - 1, &full[stg]);
+                if (!PAP) tma_load_2d(dst + SP * EP, &tmWl, x, s - 1, &full[stg]);
                 if (VARM) tma_load_2d(dst + SP * EP + k.wlp, &tmDv, x, 0, &full[stg]);
             }
             __syncwarp();
@@ -333,10 +342,11 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
             use_wl[J] = (j == s - 1) ? 1.0 : 0.0;
             upd[J] = J * 8 * EP + EP;
             dnd[J] = J * 8 * EP - ((j == 0) ? 0 : EP);
-            if (!VARM && j == s - 1) {
+            if (!VARM && !PAP && j == s - 1) {
                 c1[J] = 1.0;
                 upd[J] = (SP - r) * EP;   // the w_{s-1} row: SP*EP + pt = o + (SP - r)*EP
             }
+            if (PAP && j == s - 1) upd[J] = 0;   // a zero row (c1 = c2 = cs = 0) read from its own, finite, values
         }
         for (int it = (grp < ngroups ? grp : nit); it < nit; it += ngroups) {
             const int stg = it % NS;
@@ -381,7 +391,7 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
 #pragma unroll
                 for (int i = 0; i < NB; ++i)
 #pragma unroll
-                    for (int J = i; J < NB; ++J, ++t) {
+                    for (int J = (PAP ? 0 : i); J < (PAP ? i + 1 : NB); ++J, ++t) {   // PAP: tile (i, J <= i)
                         dmma(acc[(2 * u + SX) % U][t][0], acc[(2 * u + SX) % U][t][1], a[i].x, b[J].x);
                         dmma(acc[(2 * u + SY) % U][t][0], acc[(2 * u + SY) % U][t][1], a[i].y, b[J].y);
                     }
@@ -417,7 +427,8 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
 #pragma unroll
                 for (int i = 0; i < NB; ++i)
 #pragma unroll
-                    for (int J = i; J < NB; ++J, ++t) dmma(acc[u][t][0], acc[u][t][1], a[i], b[J]);
+                    for (int J = (PAP ? 0 : i); J < (PAP ? i + 1 : NB); ++J, ++t)
+                        dmma(acc[u][t][0], acc[u][t][1], a[i], b[J]);
               }
             }
             }
@@ -434,38 +445,52 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     double *red = smem;
     if (warp > 0) {
         const int cw = warp - 1;
+        constexpr int NTT = NT;
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
+        for (int t = 0; t < NTT; ++t) {
 #pragma unroll
             for (int u = 1; u < U; ++u) {   // fold the accumulator sets in a fixed order
                 acc[0][t][0] += acc[u][t][0];
                 acc[0][t][1] += acc[u][t][1];
             }
-            red[((cw * NT + t) * 32 + lane) * 2 + 0] = acc[0][t][0];
-            red[((cw * NT + t) * 32 + lane) * 2 + 1] = acc[0][t][1];
+            red[((cw * NTT + t) * 32 + lane) * 2 + 0] = acc[0][t][0];
+            red[((cw * NTT + t) * 32 + lane) * 2 + 1] = acc[0][t][1];
         }
         if ((lane & 3) == 0)
 #pragma unroll
-            for (int i = 0; i < NB; ++i) red[NCW * NT * 64 + cw * SP + i * 8 + (lane >> 2)] = cac[i];
+            for (int i = 0; i < NB; ++i) red[NCW * NTT * 64 + cw * SP + i * 8 + (lane >> 2)] = cac[i];
     }
     __syncthreads();
     const int nent = s * s + s;
     double *mypart = k.part + (int64_t)blockIdx.x * nent;
-    for (int q = tid; q < NT * 64; q += THREADS) {
+    constexpr int NTT = NT;
+    for (int q = tid; q < NTT * 64; q += THREADS) {
         const int t = q >> 6, e = q & 63, ln = e >> 1, h = e & 1;
         double v = 0.0;
-        for (int w = 0; w < NCW; ++w) v += red[((w * NT + t) * 32 + ln) * 2 + h];
+        for (int w = 0; w < NCW; ++w) v += red[((w * NTT + t) * 32 + ln) * 2 + h];
         int I = 0, J = 0, tt = t;
-        for (int aa = 0; aa < NB; ++aa) {
-            if (tt < NB - aa) { I = aa; J = aa + tt; break; }
-            tt -= NB - aa;
+        if (!PAP) {   // upper tiles (I, J >= I), row-major
+            for (int aa = 0; aa < NB; ++aa) {
+                if (tt < NB - aa) { I = aa; J = aa + tt; break; }
+                tt -= NB - aa;
+            }
+        } else {      // lower tiles (I, J <= I), row-major
+            for (int aa = 0; aa < NB; ++aa) {
+                if (tt <= aa) { I = aa; J = tt; break; }
+                tt -= aa + 1;
+            }
         }
         const int i = I * 8 + (ln >> 2), j = J * 8 + 2 * (ln & 3) + h;
-        if (i < s && j < s && i <= j) mypart[i * s + j] = v;
+        if (i >= s || j >= s) continue;
+        if (!PAP) {
+            if (i <= j) mypart[i * s + j] = v;
+        } else if (j <= i) {                   // v = p_i^T w_j = Ghat_{j,i}
+            mypart[j * s + i] = (i == s - 1 && j == s - 1) ? 0.0 : v;   // the diagonal p_{s-1}^T A p_{s-1}: k_pap
+        }
     }
     for (int i = tid; i < s; i += THREADS) {
         double v = 0.0;
-        for (int w = 0; w < NCW; ++w) v += red[NCW * NT * 64 + w * SP + i];
+        for (int w = 0; w < NCW; ++w) v += red[NCW * NTT * 64 + w * SP + i];
         mypart[s * s + i] = v;
     }
     __threadfence();
@@ -685,6 +710,10 @@ bool k2r_prepare(const Geo &g, Slab &sl, int s)
         K2R_ATTR(5, 68, true) || K2R_ATTR(6, 68, true) || K2R_ATTR(7, 68, true) || K2R_ATTR(8, 68, true))
         return false;
 #undef K2R_ATTR
+#define K2R_ATTR_F(NB, EP) cudaFuncSetAttribute(k2r<NB, EP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
+    if (K2R_ATTR_F(1, K2R_EP_PAIRS) || K2R_ATTR_F(2, K2R_EP_PAIRS) || K2R_ATTR_F(3, K2R_EP_MID) || K2R_ATTR_F(4, K2R_EP_MID))
+        return false;
+#undef K2R_ATTR_F
     // P rows (own map: K2D's pitch differs), the single row w_{s-1} of W, and diag(M) (one row) when it varies
     if (!encode_rows_map(&sl.tmPr, sl.P + g.plane, N, s, g.vstride, ep, s_pad)) return false;
     if (!encode_rows_map(&sl.tmWl, sl.W + g.plane, N, s, g.vstride, ep, 1)) return false;
@@ -716,13 +745,14 @@ void launch_wrec(const Geo &g, const Slab &sl, int j, double theta, double sigma
 }
 
 void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma, const DevState *st, double *out_blk,
-                cudaStream_t stream)
+                cudaStream_t stream, bool fold)
 {
     const int s_pad = (s + 7) / 8 * 8, nb = s_pad / 8, ep = ep_for_k2r(s_pad);
     const bool varm = sl.dvec != nullptr;
+    fold = fold && !varm && nb <= 4;   // (the capi asks for it only then: uses_wlfold)
     K2RParams k;
     k.N = (int64_t)sl.nzl * g.plane;
-    if (g.kn.k2s && s >= 2 && s <= 8) {
+    if (g.kn.k2s && s >= 2 && s <= 8 && !fold) {
         k.s = s;
         k.inv_theta = 1.0 / theta;
         k.inv_2theta = 1.0 / (2.0 * theta);
@@ -781,6 +811,18 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     const size_t red = (size_t)(ncw_for(nb, varm) * nt * 64 + ncw_for(nb, varm) * s_pad) * sizeof(double);
     const size_t sm = std::max((size_t)k.nstage * stage, red);
     const CUtensorMap &dv = varm ? sl.tmDv : sl.tmWl;
+    if (fold) {
+#define K2R_LAUNCH_F(NB, EP)                                                                                 \
+        launch_pdl(g.kn.pdl, k2r<NB, EP, false, true>, dim3(gx), dim3(threads_for(NB, false)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st);
+        switch (nb) {
+        case 1: K2R_LAUNCH_F(1, K2R_EP_PAIRS) break;
+        case 2: K2R_LAUNCH_F(2, K2R_EP_PAIRS) break;
+        case 3: K2R_LAUNCH_F(3, K2R_EP_MID) break;
+        default: K2R_LAUNCH_F(4, K2R_EP_MID) break;
+        }
+#undef K2R_LAUNCH_F
+        return;
+    }
 #define K2R_LAUNCH(NB, EP)                                                                                   \
     if (varm) launch_pdl(g.kn.pdl, k2r<NB, EP, true>, dim3(gx), dim3(threads_for(NB, true)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st);          \
     else launch_pdl(g.kn.pdl, k2r<NB, EP, false>, dim3(gx), dim3(threads_for(NB, false)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st);
@@ -795,6 +837,98 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     default: K2R_LAUNCH(8, 68) break;
     }
 #undef K2R_LAUNCH
+}
+
+namespace {
+// k_pap (the w_{s-1} fold): Ghat_{s-1,s-1} = p_{s-1}^T A p_{s-1} over one slab,
+// A the 7-point stencil with a constant centre (zero outside the grid in x and
+// y; the ghost planes carry the z-neighbours), each A p formed in the order of
+// the single step it replaces: c p - (p_{z-1} + p_{y-1} + p_{x-1} + p_{x+1} +
+// p_{y+1} + p_{z+1}).  A block owns a 64 x 8 tile of columns and marches a
+// z-chunk: warp = row, lane = point pair; p(z-1), p(z) ride in registers, so
+// per plane only p(z+1) streams from HBM and the in-plane neighbours are L1
+// hits (a grid-stride pass with all six neighbour loads ran 0.27 ms at 448^3:
+// L2-bound).  Per-block partials in a fixed order, then the last block sums
+// them in index order (deterministic) into the slab's Gram block entry.
+constexpr int PAP_TX = 64;
+
+template <int PAP_TY>
+__global__ void __launch_bounds__(32 * PAP_TY) k_pap(const double *p, int nx, int ny, int nzl, int64_t plane, int zc,
+                                                     int tiles_x, double center, double *part, unsigned *ticket,
+                                                     double *entry, const DevState *st)
+{
+    constexpr int PAP_THREADS = 32 * PAP_TY;
+    PDL_ENTRY(st);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ntiles = tiles_x * ((ny + PAP_TY - 1) / PAP_TY);
+    const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+    const int x = (tile % tiles_x) * PAP_TX + 2 * lane, y = (tile / tiles_x) * PAP_TY + warp;
+    const int zb = 1 + chunk * zc, ze = min(nzl + 1, zb + zc);
+    double acc = 0.0;
+    if (x < nx && y < ny && zb < ze) {
+        // p points at plane 0 (the lower ghost plane) of p_{s-1}
+        const double *col = p + (int64_t)y * nx + x;
+        double2 dn = __ldg(reinterpret_cast<const double2 *>(col + (int64_t)(zb - 1) * plane));
+        double2 c = __ldg(reinterpret_cast<const double2 *>(col + (int64_t)zb * plane));
+        const bool hl = x > 0, hr = x + 2 < nx, hy0 = y > 0, hy1 = y + 1 < ny;
+#pragma unroll 4
+        for (int z = zb; z < ze; ++z) {
+            const double *pc = col + (int64_t)z * plane;
+            const double2 up = __ldg(reinterpret_cast<const double2 *>(pc + plane));
+            const double l = hl ? __ldg(pc - 1) : 0.0, rr = hr ? __ldg(pc + 2) : 0.0;
+            const double2 z0 = make_double2(0.0, 0.0);
+            const double2 ylo = hy0 ? __ldg(reinterpret_cast<const double2 *>(pc - nx)) : z0;
+            const double2 yhi = hy1 ? __ldg(reinterpret_cast<const double2 *>(pc + nx)) : z0;
+            const double ax = center * c.x - (dn.x + ylo.x + l + c.y + yhi.x + up.x);
+            const double ay = center * c.y - (dn.y + ylo.y + c.x + rr + yhi.y + up.y);
+            acc = fma(c.x, ax, acc);
+            acc = fma(c.y, ay, acc);
+            dn = c;
+            c = up;
+        }
+    }
+    __shared__ double red[PAP_THREADS / 32];
+    __shared__ bool is_last;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < PAP_THREADS / 32; ++w) v += red[w];
+        part[blockIdx.x] = v;
+        __threadfence();
+        is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    if (threadIdx.x < 32) {   // lane m sums partials m, m+32, ... in order, then a fixed xor tree
+        double v = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) v += __ldcg(part + b);
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) {
+            *entry = v;
+            *ticket = 0u;
+        }
+    }
+}
+}  // namespace
+
+// blocks: tiles x z-chunks, the chunk length chosen for about 8 blocks per SM
+// (one wave), bounded by the partial buffer (k2_grid() * 8 doubles at least)
+void launch_pap(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk, cudaStream_t stream)
+{
+    static const int ty = getenv("SSCG_PAP_TY") ? atoi(getenv("SSCG_PAP_TY")) : 8;
+    static const int per_sm = getenv("SSCG_PAP_BPS") ? atoi(getenv("SSCG_PAP_BPS")) : 8;
+    const int tiles_x = (g.nx + PAP_TX - 1) / PAP_TX, tiles = tiles_x * ((g.ny + ty - 1) / ty);
+    const int64_t want = (int64_t)k2_grid() * per_sm;
+    int nch = (int)std::max<int64_t>(1, std::min<int64_t>(sl.nzl, want / tiles));
+    const int zc = (sl.nzl + nch - 1) / nch;
+    nch = (sl.nzl + zc - 1) / zc;
+    auto kern = ty == 4 ? k_pap<4> : ty == 16 ? k_pap<16> : ty == 32 ? k_pap<32> : k_pap<8>;
+    launch_pdl(g.kn.pdl, kern, dim3((unsigned)(tiles * nch)), dim3(32 * ty), 0, stream,
+               (const double *)(sl.P + (int64_t)(s - 1) * g.vstride), g.nx, g.ny, sl.nzl, g.plane, zc, tiles_x,
+               g.center, sl.part, sl.ticket, out_blk + (int64_t)(s - 1) * s + (s - 1), st);
 }
 
 }  // namespace sscg

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(THREADS, KIND >= 3 ? 1 : 2)
 
     // ---------------- consumers ----------------
     const int cw = warp - 1;
+    double pacc = 0.0;   // dot mode (a.dot_entry): this thread's part of p^T A p
     const int ra = 2 * cw;                          // tile rows ra, ra + 1
     const int oa = (ra + 1) * BW + 2 + 2 * lane;    // pair of row ra in a p slot
     const int ob = oa + BW;
@@ -384,6 +385,16 @@ __global__ void __launch_bounds__(THREADS, KIND >= 3 ? 1 : 2)
                 if (lane == 0) mbar_arrive(&emptym[sl]);
                 ++mc;
             }
+            if (a.dot_entry) {   // p^T A p (the fold's Ghat_{s-1,s-1}): own cells only
+                if (sa) {
+                    pacc = fma(c0a.x, Apa.x, pacc);
+                    pacc = fma(c0a.y, Apa.y, pacc);
+                }
+                if (sb) {
+                    pacc = fma(c0b.x, Apb.x, pacc);
+                    pacc = fma(c0b.y, Apb.y, pacc);
+                }
+            }
             if (sa) {
                 if (!a.skip_w) __stcs(reinterpret_cast<double2 *>(a.w + ia), Apa);
                 if (a.mode >= 1) {
@@ -423,6 +434,34 @@ __global__ void __launch_bounds__(THREADS, KIND >= 3 ? 1 : 2)
             ++pc;
         }
         if (KIND != 2) relp(c0);   // the last plane (z_hi) was only read for its centres
+    }
+    if (a.dot_entry) {
+        // fixed-order block sum of the consumer warps (named barrier: the
+        // producer warp has returned), per-CTA partial, the last CTA sums the
+        // partials in index order (lane-strided, then a fixed xor tree)
+        __shared__ double dred[NCW];
+        __shared__ bool dlast;
+        for (int o = 16; o > 0; o >>= 1) pacc += __shfl_xor_sync(0xffffffffu, pacc, o);
+        if (lane == 0) dred[cw] = pacc;
+        asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+        if (cw == 0 && lane == 0) {
+            double v = 0.0;
+            for (int w = 0; w < NCW; ++w) v += dred[w];
+            a.dot_part[blockIdx.x] = v;
+            __threadfence();
+            dlast = atomicAdd(a.dot_ticket, 1u) == gridDim.x - 1;
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+        if (dlast && cw == 0) {
+            __threadfence();
+            double v = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(a.dot_part + b);
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) {
+                *a.dot_entry = v;
+                *a.dot_ticket = 0u;
+            }
+        }
     }
 }
 

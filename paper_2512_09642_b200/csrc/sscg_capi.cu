@@ -343,6 +343,7 @@ Knobs sscg::read_knobs()
     k.small = tri("SSCG_SMALL", -1);
     k.debug = getenv("SSCG_DEBUG") != nullptr;
     k.pdl = tri("SSCG_PDL", 1) != 0;
+    k.wl_fold = std::min(2, std::max(0, num("SSCG_WL_FOLD", 1)));
     return k;
 }
 
@@ -776,6 +777,7 @@ static bool uses_wfree(const sscg_ctx *c)
 
 static bool uses_mp3(const sscg_ctx *c);
 static bool uses_fused(const sscg_ctx *c);
+static bool uses_wlfold(const sscg_ctx *c);
 
 // KS (k_small.cu): the whole outer iteration in one launch of one 8-CTA
 // cluster, for a single slab of at most 8192 points (its P and W fit the
@@ -797,7 +799,7 @@ static bool uses_small(const sscg_ctx *c)
 //   0 = all planes, 1 = the two boundary planes (1 and nzl), 2 = the interior
 //   planes [2, nzl) that do not read a halo plane, 3 = the two planes next to
 //   each boundary (1, 2, nzl-1, nzl; the third step of a K1M triple)
-static sscg_status launch_basis(sscg_ctx *c, int j, int part)
+static sscg_status launch_basis(sscg_ctx *c, int j, int part, bool ignore_stop = false)
 {
     const Geo &g = c->g;
     const int s = c->s;
@@ -845,11 +847,41 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part)
         }
         const int cat = (uses_mp3(c) || uses_fused(c)) ? SSCG_PROF_BASIS_SINGLE : SSCG_PROF_BASIS;
         TRY(prof_mark(c, cat, true));
-        launch_k1(g, a, c->st, c->stream);
+        launch_k1(g, a, ignore_stop ? nullptr : c->st, c->stream);   // (no state: runs after the stop too)
         TRY(prof_mark(c, cat, false));
         ++c->launches;
     }
     return SSCG_OK;
+}
+
+// w_{s-1} fold: under the W-free schedule on the 7-point
+// constant-centre stencil, w_{s-1} = A p_{s-1} is never stored: the Gram pass
+// takes column s-1 from the transposed products w_i^T p_{s-1} (K2R PAP), one
+// reduction pass over p_{s-1} gives p_{s-1}^T A p_{s-1} (k_pap), and the
+// update forms w_{s-1} per point from p_{s-1} and its neighbours (K5 FOLD), so
+// the basis schedules stop at p_{s-1} and the single step j = s-1 disappears
+// (SSCG_WL_FOLD=0 keeps it)
+static bool uses_wlfold(const sscg_ctx *c)
+{
+    const Geo &g = c->g;
+    if (g.kn.wl_fold != 1 || g.kind != SSCG_OP_STENCIL7 || !uses_wfree(c)) return false;
+    if (c->s > 32 || (c->s <= 8 && g.kn.k2s)) return false;   // K2R with at most 4 row blocks; K2S reads the stored w_{s-1}
+    if ((g.nx & 1) || g.pitch != g.nx) return false;             // k_pap and K5 run on point pairs
+    for (const auto &sl : c->slabs)
+        if (sl.dvec || sl.dinv) return false;
+    return true;
+}
+
+// the update half of the fold alone (SSCG_WL_FOLD=2, or with the full fold):
+// K5 forms w_{s-1} from p_{s-1} and its neighbours instead of reading it
+static bool uses_k5fold(const sscg_ctx *c)
+{
+    const Geo &g = c->g;
+    if (g.kn.wl_fold == 1) return uses_wlfold(c);
+    if (g.kn.wl_fold != 2 || g.kind != SSCG_OP_STENCIL7 || !uses_rec_update(c) || (g.nx & 1)) return false;
+    for (const auto &sl : c->slabs)
+        if (sl.dvec || sl.dinv) return false;
+    return true;
 }
 
 // K1F pairs are used when every slab has the fused tensor maps (7-point,
@@ -1026,6 +1058,36 @@ static sscg_status launch_basis_pair(sscg_ctx *c, int j, int part)
 // One outer iteration.  Precondition: the halo planes of p_0 are current.
 //   for j: K1 boundary planes -> fork halo(p_{j+1}) -> K1 interior -> join
 //   K2 (+ slab sum) -> allreduce -> K4 -> K5 boundary -> fork halo(p_0) -> K5 interior -> join
+// the fold's diagonal entry p_{s-1}^T A p_{s-1} of one slab into its Gram block
+// (after K2R): the TMA single step (K1T) in its dot mode -- it streams p_{s-1}
+// as the single step it replaces did, stores nothing and reduces -- else k_pap
+static void launch_pap_dot(sscg_ctx *c, const Slab &sl, double *blk)
+{
+    const Geo &g = c->g;
+    const int s = c->s;
+    K1Args a{};
+    a.p = sl.P + (int64_t)(s - 1) * g.vstride;
+    a.w = sl.W + (int64_t)(s - 1) * g.vstride;   // (not written: skip_w)
+    a.dinv = sl.dinv;
+    a.dinv_c = g.dinv_c;
+    a.sigma = c->sigma;
+    a.mode = 0;
+    a.nzl = sl.nzl;
+    a.j = s - 1;
+    a.skip_w = 1;
+    a.zb = 1;
+    a.ze = sl.nzl + 1;
+    if (sl.has_k1t) {
+        a.tmP4 = &sl.tmP4;
+        a.tmM4 = &sl.tmM4;
+    }
+    a.dot_part = sl.part;
+    a.dot_ticket = sl.ticket;
+    a.dot_entry = blk + (int64_t)(s - 1) * s + (s - 1);
+    if (k1t_supported(g, a)) launch_k1(g, a, c->st, c->stream);
+    else launch_pap(g, sl, s, c->st, blk, c->stream);
+}
+
 static sscg_status enqueue_outer(sscg_ctx *c, double *x)
 {
     const Geo &g = c->g;
@@ -1050,9 +1112,13 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
         CU(cudaGetLastError());
         return SSCG_OK;
     }
+    // with the w_{s-1} fold the basis kernels stop at p_{s-1}: steps j < s_end
+    const bool fold = uses_wlfold(c);
+    const int s_end = fold ? s - 1 : s;
+    bool pend_last = false;   // p_{s-1} produced by a single step whose exchange is still due (fold)
     nvtxRangePushA("basis");
-    for (int j = 0; j < s; ++j) {
-        if (mp3 && j + 2 < s) {   // steps j, j+1, j+2 in one pass (K1M)
+    for (int j = 0; j < s_end; ++j) {
+        if (mp3 && j + 2 < s_end) {   // steps j, j+1, j+2 in one pass (K1M)
             if (!halo) {
                 TRY(launch_basis_triple(c, j));
             } else if (deep) {
@@ -1063,7 +1129,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
                 // SSCG_DEEP_OVERLAP=1: the planes the exchange sends go first and the
                 // exchange overlaps the rest of the triple (an extra launch per triple;
                 // measured slower on one GPU, tools/slab_overhead.py)
-                const bool next3 = j + 5 < s;
+                const bool next3 = j + 5 < s_end;
                 const int np3 = (j + 3 < s) ? (next3 ? 3 : 1) : 0, np2 = next3 ? 2 : 0;
                 if (ovl && np3 > 0 && g.kn.deep_overlap) {
                     TRY(launch_basis_triple_deep(c, j, 1));
@@ -1088,7 +1154,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
                 if (j + 3 < s) TRY(halo_fork(c, j + 3, false));
             }
             j += 2;
-        } else if (fuse && j + 1 < s) {   // steps j and j+1 in one pass (K1F)
+        } else if (fuse && j + 1 < s_end) {   // steps j and j+1 in one pass (K1F)
             if (!halo) {
                 TRY(launch_basis_pair(c, j, 0));
             } else {
@@ -1107,6 +1173,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
         } else if (!ovl) {
             if (j > 0) TRY(halo_fork(c, j, false));
             TRY(launch_basis(c, j, 0));
+            pend_last = j == s_end - 1;
         } else {
             TRY(launch_basis(c, j, 1));
             if (j < s - 1) TRY(halo_fork(c, j + 1, true));
@@ -1114,6 +1181,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
             if (j < s - 1) TRY(halo_join(c));
         }
     }
+    if (fold && halo && pend_last) TRY(halo_fork(c, s - 1, false));   // K2R / K5 read p_{s-1}'s ghost planes
     nvtxRangePop();
     nvtxRangePushA("gram+allreduce+fgs");
     const bool wfree = uses_wfree(c);
@@ -1130,10 +1198,14 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const int rows = c->blockcg ? 2 * s : s, nent = rows * rows + rows;
     for (auto &sl : c->slabs) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
-        if (wfree) launch_k2r(g, sl, s, c->theta, c->sigma, c->st, L == 1 ? c->blk : sl.blk, c->stream);
+        if (wfree) launch_k2r(g, sl, s, c->theta, c->sigma, c->st, L == 1 ? c->blk : sl.blk, c->stream, fold);
         else launch_k2(g, sl, rows, c->st, L == 1 ? c->blk : sl.blk, c->stream);
-        TRY(prof_mark(c, SSCG_PROF_GRAM, false));
         ++c->launches;
+        if (fold) {   // Ghat_{s-1,s-1} = p_{s-1}^T A p_{s-1}
+            launch_pap_dot(c, sl, L == 1 ? c->blk : sl.blk);
+            ++c->launches;
+        }
+        TRY(prof_mark(c, SSCG_PROF_GRAM, false));
     }
     if (L > 1) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
@@ -1186,7 +1258,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
                                 b, e);
             else
                 launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, b, e,
-                          c->theta, c->sigma, uses_rec_update(c));
+                          c->theta, c->sigma, uses_rec_update(c), uses_k5fold(c));
             TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
             ++c->launches;
         }
@@ -1209,7 +1281,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
                 if (zb >= ze) continue;
                 TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
                 launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, zb, ze,
-                          c->theta, c->sigma, uses_rec_update(c));
+                          c->theta, c->sigma, uses_rec_update(c), uses_k5fold(c));
                 TRY(prof_mark(c, SSCG_PROF_UPDATE, false));
                 ++c->launches;
             }
@@ -1496,6 +1568,8 @@ extern "C" sscg_status sscg_inspect(const sscg_ctx *cc, int32_t what, int32_t in
     if (what == SSCG_INSPECT_P || what == SSCG_INSPECT_W) {
         if (index < 0 || index >= s) return fail(SSCG_ERR_INVALID, "column %d out of range", index);
         if (!need(c->n_local * 8)) return fail(SSCG_ERR_INVALID, "buffer too small");
+        if (what == SSCG_INSPECT_W && index == s - 1 && uses_wlfold(c))   // not stored (fold): w_{s-1} = A p_{s-1}
+            TRY(launch_basis(c, s - 1, 0, true));
         for (auto &sl : c->slabs) {
             double *v = (what == SSCG_INSPECT_P ? sl.P : sl.W) + (int64_t)index * g.vstride;
             if (what == SSCG_INSPECT_W && uses_wfree(c) && index < s - 1)   // not stored: recover it (R23)
@@ -1788,21 +1862,22 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
     case SSCG_QUERY_BASIS_SINGLE_VECTORS: {
         // FP64 vectors of n_local read + written by the basis steps of one outer
         // (_SINGLE: by the single steps of a fused schedule, the SSCG_PROF_BASIS_SINGLE launches)
-        const bool wf = uses_wfree(c);
-        auto wst = [&](int j) { return (!wf || j == s - 1) ? 1 : 0; };   // w_j stored?
+        const bool wf = uses_wfree(c), fold = uses_wlfold(c);
+        const int se = fold ? s - 1 : s;   // steps run by basis kernels (fold: w_{s-1} formed in K2R / K5)
+        auto wst = [&](int j) { return (!wf || (j == s - 1 && !fold)) ? 1 : 0; };   // w_j stored?
         int64_t v = 0, v1 = 0;
         if (uses_mp3(c)) {
             int j = 0;
-            for (; j + 2 < s; j += 3)   // p_j, p_{j-1} in; p_{j+1..j+3} and stored w out
+            for (; j + 2 < se; j += 3)   // p_j, p_{j-1} in; p_{j+1..j+3} and stored w out
                 v += 1 + (j > 0) + (j + 1 < s) + (j + 2 < s) + (j + 3 < s) + wst(j) + wst(j + 1) + wst(j + 2);
-            if (j + 1 < s) { v += 1 + (j > 0) + 1 + (j + 2 < s) + wst(j) + wst(j + 1); j += 2; }   // a K1F pair
-            if (j < s) v1 += 1 + (j > 0 && j < s - 1) + wst(j) + (j < s - 1);                      // a single step
+            if (j + 1 < se) { v += 1 + (j > 0) + 1 + (j + 2 < s) + wst(j) + wst(j + 1); j += 2; }   // a K1F pair
+            if (j < se) v1 += 1 + (j > 0 && j < s - 1) + wst(j) + (j < s - 1);                      // a single step
         } else if (uses_fused(c)) {
             int j = 0;
-            for (; j + 1 < s; j += 2) v += 1 + (j > 0) + 1 + (j + 2 < s) + wst(j) + wst(j + 1);
-            if (j < s) v1 += 2;   // odd s: the last step alone (mode 0: reads p_{s-1}, writes w_{s-1})
+            for (; j + 1 < se; j += 2) v += 1 + (j > 0) + 1 + (j + 2 < s) + wst(j) + wst(j + 1);
+            if (j < se) v1 += 1 + (j > 0 && j < s - 1) + wst(j) + (j < s - 1);   // the last step alone
         } else {
-            for (int j = 0; j < s; ++j) {
+            for (int j = 0; j < se; ++j) {
                 const bool pn = j < s - 1, pm = !mono && j > 0 && pn;
                 v += 1 + pm + wst(j) + pn;
             }
@@ -1813,13 +1888,15 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
     case SSCG_QUERY_GRAM_VECTORS:
         // stored W: P and W (2s); recovered W: P, w_{s-1} and diag(M) when it varies;
         // block-conjugate: [P | Q'] and [W | Z'] (4s)
-        *out = c->blockcg ? 4 * (int64_t)s : uses_wfree(c) ? (int64_t)s + 1 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s;
+        // (fold: P, then p_{s-1} again for p_{s-1}^T A p_{s-1})
+        *out = c->blockcg ? 4 * (int64_t)s : uses_wlfold(c) ? (int64_t)s + 1 :
+               uses_wfree(c) ? (int64_t)s + 1 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s;
         return SSCG_OK;
     case SSCG_QUERY_UPDATE_VECTORS:
         // P (s) + x in, x + r out; the stored-W form also reads W (s), the
         // recurrence form only w_{s-1}
         // block-conjugate: P, W, Q', Z', x in; Q, Z, x, r out
-        *out = c->blockcg ? 6 * (int64_t)s + 3 :
+        *out = c->blockcg ? 6 * (int64_t)s + 3 : uses_k5fold(c) ? (int64_t)s + 3 :
                uses_rec_update(c) ? (int64_t)s + 4 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s + 3;
         return SSCG_OK;
     default:

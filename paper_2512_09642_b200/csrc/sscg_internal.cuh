@@ -125,6 +125,7 @@ struct Knobs {
     int small = -1;        // SSCG_SMALL        -1 auto (2D grids <= 8192 points), 0 forbid, 1 force the single-cluster outer iteration
     int debug = 0;         // SSCG_DEBUG
     int pdl = 1;           // SSCG_PDL          0: plain stream-ordered launches (no programmatic dependent launch)
+    int wl_fold = 1;       // SSCG_WL_FOLD      1: w_{s-1} never stored (K2R lower triangle + k_pap + K5 stencil); 2: only K5 forms it; 0: off
 };
 Knobs read_knobs();
 
@@ -171,6 +172,11 @@ struct K1Args {
     const CUtensorMap *tmP4, *tmM4;   // K1T tensor maps of this slab (host memory), or nullptr
     const CUtensorMap *tmKX, *tmKY, *tmKZ;   // K1T variable-coefficient face maps, or nullptr
     double *w2, *pn2;                 // K1F: w_{j+1}, p_{j+2} (nullptr at j+1 = s-1)
+    // K1T mode 0 with the w_{s-1} fold: accumulate p^T A p over the launch's own
+    // cells instead of storing w (skip_w): per-CTA partials, a ticket, and the
+    // entry the last CTA writes (the slab's Gram block entry (s-1, s-1)); else null
+    double *dot_part, *dot_entry;
+    unsigned *dot_ticket;
     int kx_shift;                     // K1FV: see Slab::kx_shift
     const CUtensorMap *tmF_P, *tmF_M; // K1F tensor maps
 };
@@ -238,7 +244,10 @@ bool k2d_enabled(const Geo &g, int s);
 // K2R: DMMA Gram pass recovering W = AP from the basis recurrence (W not stored, R23)
 bool k2r_prepare(const Geo &g, Slab &sl, int s);
 void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma, const DevState *st, double *out_blk,
-                cudaStream_t stream);
+                cudaStream_t stream, bool fold = false);
+// the w_{s-1} fold: Ghat_{s-1,s-1} = p_{s-1}^T A p_{s-1} of one slab
+// into its Gram block (after launch_k2r with fold = true)
+void launch_pap(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk, cudaStream_t stream);
 // w_j (j < s-1) from the recurrence into `out` (a vector in the padded layout) -- parity hooks
 void launch_wrec(const Geo &g, const Slab &sl, int j, double theta, double sigma, double *out, cudaStream_t stream);
 bool k2d_prepare(const Geo &g, Slab &sl, int s);
@@ -274,7 +283,8 @@ void launch_anorm(const Geo &g, const Slab &sl, double *bmax, int nblk, cudaStre
 // K5: x += P alpha;  p_0 -= W alpha over padded planes [zb, ze) (ze < 0: to nzl+1)
 //   rec: form W alpha from the Chebyshev recurrence (constant diagonal, vector path only)
 void launch_k5(const Geo &g, const Slab &sl, int s, const double *alpha, double *const *xpp, int64_t xoff,
-               const DevState *st, cudaStream_t stream, int zb, int ze, double theta, double sigma, bool rec);
+               const DevState *st, cudaStream_t stream, int zb, int ze, double theta, double sigma, bool rec,
+               bool fold = false);
 
 // KS: one whole outer iteration in one launch of one 8-CTA cluster for small problems (k_small.cu)
 bool ks_supported(const Geo &g, int s, int64_t npts);

@@ -18,7 +18,9 @@ vs the W-free K2R/K2S, the recurrence vs stored-W update).  Under the W-free
 schedule the product path never stores w_j (j < s-1): K2R recovers it per
 point inside the Gram pass and the Gram block checks that; the w_j read back
 here for j < s-1 come from the inspect hook's recovery kernel (k_wrec, the
-same per-point formula), w_{s-1} is the stored SpMV output."""
+same per-point formula); w_{s-1} is the stored SpMV output, or, under the
+w_{s-1} fold (7-point default: K2R and K5 form it from p_{s-1}), the inspect
+hook's single step over p_{s-1}."""
 import numpy as np
 import pytest
 
@@ -41,11 +43,12 @@ SHAPES = {
 
 # schedule switches forced per operator kind; {} = the default schedule
 SWITCHES = {
-    "7pt": [{}, {"SSCG_K1_MP3": "1"}, {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "1"}, {"SSCG_K1_FUSE": "0"},
+    "7pt": [{}, {"SSCG_WL_FOLD": "0"}, {"SSCG_K1_MP3": "1"}, {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "1"}, {"SSCG_K1_FUSE": "0"},
             {"SSCG_WFREE": "0"}, {"SSCG_WFREE": "0", "SSCG_K2_DMMA": "1"}, {"SSCG_K5_RECUR": "0"},
             {"SSCG_K1_TMA": "0", "SSCG_K1_FUSE": "0"}, {"SSCG_PDL": "0"}],
-    "7pt_mid": [{}, {"SSCG_K1_MP3": "1"}, {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "1"}, {"SSCG_WFREE": "0"}],
-    "cfg2": [{}, {"SSCG_K1_MP3": "1"}, {"SSCG_K5_RECUR": "0"}, {"SSCG_WFREE": "0"}],
+    "7pt_mid": [{}, {"SSCG_K1_MP3": "1"}, {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "1"}, {"SSCG_WFREE": "0"},
+                {"SSCG_WL_FOLD": "0"}],
+    "cfg2": [{}, {"SSCG_K1_MP3": "1"}, {"SSCG_K5_RECUR": "0"}, {"SSCG_WFREE": "0"}, {"SSCG_WL_FOLD": "0"}],
     "27pt": [{}, {"SSCG_K1_FUSE": "1"}, {"SSCG_WFREE": "0"}, {"SSCG_WFREE": "0", "SSCG_K2_DMMA": "1"},
              {"SSCG_K5_RECUR": "0"}],
     "varcoef7": [{}, {"SSCG_K1_FUSE_VC": "1"}, {"SSCG_K1_FUSE_VC": "0"}, {"SSCG_K2S": "0"}, {"SSCG_WFREE": "0"},

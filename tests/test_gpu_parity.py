@@ -472,6 +472,8 @@ def test_recurrence_update_matches_stored_w(cfg, monkeypatch):
         monkeypatch.setenv("SSCG_K5_RECUR", rec)
         with P.gpu_solver() as S:
             extra = 1 if kind == "varcoef7" else 0      # diag(M) varies: read per point
+            # the w_{s-1} fold (7-point, even nx, s > 8 -- K2S for smaller s): formed from p_{s-1}, not read
+            extra -= 1 if (kind == "7pt" and nx % 2 == 0 and s > 8) else 0
             assert S.query(sscg.QUERY_UPDATE_VECTORS) == (s + 4 + extra if rec == "1" else 2 * s + 3)
             x10 = S.solve(P.b_gpu(), rtol=0.0, max_outer=10).cpu().numpy()
             xf = S.solve(P.b_gpu(), rtol=1e-8, max_outer=20000).cpu().numpy()
@@ -571,3 +573,63 @@ def test_long_run_history_caps():
         assert np.all(np.isfinite(G))
         with pytest.raises(sscg.SSCGError):
             S.gram(2048)
+
+
+@pytest.mark.parametrize("cfg,slabs,env", [
+    (("7pt", 40, 36, 33, 16, 25), 1, {}),                                            # cfg 5 schedule: 5 triples, no single step
+    (("7pt", 64, 40, 30, 9, 20), 1, {}),                                             # triples then a pair stop at p_8
+    (("7pt", 60, 49, 23, 11, 20), 1, {}),                                            # triples then a single step
+    (("7pt", 40, 36, 33, 16, 25), 1, {"SSCG_K1_MP3": "0", "SSCG_K1_FUSE": "1"}),    # pairs, the last one a single step
+    (("7pt", 26, 24, 22, 8, 20), 1, {"SSCG_K2S": "0"}),                              # K2R with one row block
+    (("7pt", 30, 28, 26, 24, 20), 1, {}),                                            # K2R with three row blocks
+    (("7pt", 40, 36, 33, 16, 25), 3, {}),                                            # deep halos, peer stores
+    (("7pt", 58, 30, 37, 10, 20), 2, {"SSCG_PEER_HALO": "0"}),                       # deep halos, copies
+    (("7pt", 26, 24, 40, 7, 15), 4, {"SSCG_DEEP_HALO": "0", "SSCG_K2S": "0"}),      # 1-plane halos
+    (("7pt", 40, 36, 33, 16, 25), 3, {"SSCG_NCCL_SELF": "1"}),                       # the NCCL exchange code
+    (("7pt", 40, 36, 33, 10, 20), 3, {"SSCG_K1_MP3": "0", "SSCG_NO_OVERLAP": "1"}),  # pairs around exchanges
+    (("7pt", 40, 36, 33, 16, 25), 2, {"SSCG_K1_TMA": "0"}),                          # diagonal entry by k_pap
+], ids=lambda v: _ids(v) if isinstance(v, tuple) else (str(v) if not isinstance(v, dict) else "-".join(v) or "default"))
+def test_wl_fold_matches_stored(cfg, slabs, env, monkeypatch):
+    """The w_{s-1} fold (the default for the 7-point stencil):
+    w_{s-1} = A p_{s-1} is never stored -- the Gram pass takes column s-1 from
+    the transposed products w_i^T p_{s-1} (K2R PAP: the lower block triangle),
+    the TMA single step in its dot mode gives p_{s-1}^T A p_{s-1} (K1T, or
+    k_pap without TMA) and the update forms w_{s-1} per point (K5) --
+    so the last basis step disappears.  Against
+    the stored-w_{s-1} schedule (SSCG_WL_FOLD=0): the basis P and w_{s-1}
+    (read back through the inspect hook, a K1T step) to rounding -- bit for
+    bit where the same kernels produce them --, the Gram blocks and x to rounding (the stencil
+    sums in the order of the single step, the sums around it differ only in
+    where w_{s-1} comes from); the byte counts the schedule reports drop by
+    the single step and one vector each in K2R and K5.  Both agree with the
+    oracle, with several slabs too (ghost planes of p_{s-1} current)."""
+    import paper_2512_09642_b200 as sscg
+    kind, nx, ny, nz, s, nu = cfg
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    P = Problem(kind, nx, ny, nz, s, nu)
+    out = {}
+    for fold in ("1", "0"):
+        monkeypatch.setenv("SSCG_WL_FOLD", fold)
+        with P.gpu_solver(slabs=slabs) as S:
+            q = (S.query(sscg.QUERY_GRAM_VECTORS), S.query(sscg.QUERY_UPDATE_VECTORS),
+                 S.query(sscg.QUERY_BASIS_VECTORS), S.query(sscg.QUERY_BASIS_SINGLE_VECTORS))
+            x = S.solve(P.b_gpu(), rtol=0.0, max_outer=0).cpu().numpy()
+            basis0 = [S.basis(j) for j in range(s)]
+            x = S.solve(P.b_gpu(), rtol=0.0, max_outer=5).cpu().numpy()
+            out[fold] = (x, [S.gram(k)[0] for k in range(6)], basis0, q)
+    a, b = out["1"], out["0"]
+    assert a[3][0] == s + 1 and b[3][0] == s + 1        # Gram: P + p_{s-1} (k_pap) vs P + w_{s-1}
+    assert a[3][1] == s + 3 and b[3][1] == s + 4        # update: P, x in; x, r out (+ w_{s-1})
+    assert a[3][2] <= b[3][2] - 1                       # basis: no w_{s-1} store (no single step after triples)
+    for j in range(s):   # bit for bit, except where the fold moves p_{s-1} to another kernel (pairs: K1T, not K1F)
+        assert rel_inf(a[2][j][0], b[2][j][0]) <= 1e-14, j
+    assert rel_inf(a[2][s - 1][1], b[2][s - 1][1]) <= 1e-13
+    assert np.max(np.abs(a[1][0] - b[1][0])) <= 1e-13 * np.max(np.abs(b[1][0]))
+    for k in range(1, 6):   # rounding-level drift after the first update
+        assert np.max(np.abs(a[1][k] - b[1][k])) <= TOL_GRAM * np.max(np.abs(b[1][k])), k
+    assert np.linalg.norm(a[0] - b[0]) <= 1e-11 * np.linalg.norm(b[0])
+    x_or, tr = P.oracle(max_outer=5, dump_iter=0)
+    assert np.max(np.abs(a[1][0] - tr.ghat[0])) <= TOL_GRAM * np.max(np.abs(tr.ghat[0]))
+    assert rel_inf(a[2][s - 1][1], tr.W[s - 1]) <= 1e-12
+    assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)

@@ -31,6 +31,7 @@ def _cases(n=80, seed=2024):
                "SSCG_K1_MP3": str(rng.integers(0, 2)), "SSCG_K1_FUSE_VC": str(rng.integers(0, 2)),
                "SSCG_WFREE": str(rng.integers(0, 2)), "SSCG_K2S": str(rng.integers(0, 2))}
         env["SSCG_SMALL"] = str(rng.integers(0, 2))   # drawn last: the earlier draws keep their values
+        env["SSCG_WL_FOLD"] = "0" if (nx + ny + nz) % 3 == 0 else "1"   # derived, not drawn (same reason)
         out.append((kind, nx, ny, nz, s, nu, slabs, env))
     return out
 
