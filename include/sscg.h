@@ -350,7 +350,11 @@ SSCG_API void sscg_destroy(sscg_ctx *ctx);
  *                          operator -- entry (I, J) is the sum over the cells
  *                          a of aggregate I of (A_f p_J)_a, p_J = P e_J.
  *   SSCG_COARSE_ASSEMBLED  the entries are formed once at create (7 n_c
- *                          doubles, the same arithmetic) and read by FGS.
+ *                          doubles padded to 8 per row, the same arithmetic)
+ *                          and read by FGS.
+ * For the 5- and 7-point operators the streaming entries are integers (face
+ * areas, 4 / 6 x cells - 2 x internal couplings) formed in closed form --
+ * exact, hence the same doubles as any summation order.
  * Both give results bitwise equal to the definition written out in the
  * oracle (entry sums in ascending fine index, Gauss-Seidel row sums in
  * ascending coarse index, no fused multiply-add).
@@ -377,7 +381,8 @@ SSCG_API sscg_status sscg_coarse_fgs(sscg_coarse *h, const double *r_c, double *
 /* the (at most 7) entries of every coarse row, device out[7 * n_c]: out[d *
  * n_c + c] = A_c(c, neighbour d of c), d = 0..6 for the neighbours at
  * z-1, y-1, x-1, c itself, x+1, y+1, z+1 (0 where absent) -- computed by the
- * same routine FGS uses (streaming) or copied (assembled) */
+ * routine the assembly runs (the closed form of the constant stencils gives
+ * the same integers) */
 SSCG_API sscg_status sscg_coarse_entries(sscg_coarse *h, double *out, void *stream);
 /*   SSCG_COARSE_QUERY_N              n_c
  *   SSCG_COARSE_QUERY_NCX / _NCY / _NCZ  the coarse grid

@@ -173,71 +173,182 @@ __global__ void k_coarse_prolong(CG g, const double *y, double *xf)
     }
 }
 
-// nu pipelined Gauss-Seidel sweeps (see the file comment).  Shared memory:
-// y[nc], r[nc], the wavefront lists (points of wavefront t at
-// pts[off[t] .. off[t+1]), ascending index) and off[T+1].
-template <bool STREAM>
+// nu pipelined Gauss-Seidel sweeps (see the file comment).
+//
+// The items of a step are the wavefronts t = tau - 2m of the active sweeps m,
+// all of one parity; the host lists the coarse points parity-major (even t
+// ascending, then odd t ascending), so a step's items are ONE contiguous list
+// range [wlo[t_lo], whi[t_hi]), thread tid taking items tid, tid + NT, ...
+// Per item a packed word meta = c | flags << 24 (flags: the neighbour exists
+// at z-1, y-1, x-1, x+1, y+1, z+1) replaces the index arithmetic.  Entries:
+//   MODE 0 (assembled): A7L[q * 8 + d] in list order, the next step's entries
+//          loaded into registers before the barrier that ends this step, so
+//          no L2 latency sits on the step's critical path;
+//   MODE 1 (streaming, 5-/7-point): the entries in closed form from the
+//          aggregate's extents -- face areas and 6 / 4 x cells - 2 x internal
+//          couplings; every term is a small integer, so any summation order
+//          gives the oracle's doubles exactly;
+//   MODE 2 (streaming, variable coefficients): coarse_row from the faces at
+//          every visit (the oracle's per-cell order).
+// Within a step all reads (r, neighbour y) precede all writes of the thread's
+// items, and no item of a step reads another's output (neighbours lie on
+// t +- 1), so the result is the sequential sweep order, bitwise.
+// MODE 0: items per thread whose entries are prefetched (3 spilled at the
+// 64-register limit of 1024 threads: 0.31 ms per 20 sweeps at n_c = 4913 vs
+// 0.21 with 2)
+#ifndef COARSE_PF
+#define COARSE_PF 2
+#endif
+constexpr int PF = COARSE_PF;
+
+// Shared memory holds y and r_c in a row-padded layout, s(c) = I + px (J + ncy K)
+// with px = ncx rounded up to even: the items of a wavefront, consecutive in
+// ascending c, are (ncx - 1) apart in c -- with ncx = 17 every lane of a warp
+// hit the same bank (a 32-way conflict on every y load) -- and px - 1 odd
+// apart in s; meta carries s(c).
+template <int MODE>
 __global__ void __launch_bounds__(NT, 1)
-    k_coarse_fgs(CG g, const double *__restrict__ A7, const double *rc, double *y, int nu, const int *wf_pts,
-                 const int *wf_off, int T)
+    k_coarse_fgs(CG g, const double *__restrict__ A7L, const double *rc, double *y, int nu, const int *meta_g,
+                 const int *wlo_g, const int *whi_g, int T, int exl, int eyl, int ezl, double center)
 {
     extern __shared__ __align__(16) double sm[];
-    const int nc = g.ncx * g.ncy * g.ncz, sxy = g.ncx * g.ncy;
-    double *ys = sm, *rs = sm + nc;
-    int *pts = reinterpret_cast<int *>(rs + nc), *off = pts + nc;
+    const int nc = g.ncx * g.ncy * g.ncz, px = (g.ncx + 1) & ~1, ns = px * g.ncy * g.ncz, sxy = px * g.ncy;
+    double *ys = sm, *rs = sm + ns;
+    int *meta = reinterpret_cast<int *>(rs + ns), *wlo = meta + nc, *whi = wlo + T;
     const int tid = threadIdx.x;
+    auto sidx = [&](int c) { const int I = c % g.ncx, r = c / g.ncx; return I + px * r; };
     for (int i = tid; i < nc; i += NT) {
-        ys[i] = y[i];
-        rs[i] = rc[i];
-        pts[i] = wf_pts[i];
+        ys[sidx(i)] = y[i];
+        rs[sidx(i)] = rc[i];
+        meta[i] = meta_g[i];
     }
-    for (int i = tid; i <= T; i += NT) off[i] = wf_off[i];
+    for (int i = tid; i < T; i += NT) {
+        wlo[i] = wlo_g[i];
+        whi[i] = whi_g[i];
+    }
     __syncthreads();
     const int steps = nu > 0 ? T + 2 * (nu - 1) : 0;
-    for (int tau = 0; tau < steps; ++tau) {
+    auto range = [&](int tau, int &q0, int &q1) {
         const int a = tau - (T - 1);
         const int m_lo = a > 0 ? (a + 1) / 2 : 0, m_hi = min(nu - 1, tau / 2);
-        int base = 0;   // items of the step so far: thread tid takes items tid, tid + NT, ...
-        for (int m = m_lo; m <= m_hi; ++m) {
-            const int t = tau - 2 * m, o0 = off[t], cnt = off[t + 1] - o0;
-            int l = tid - base % NT;
-            if (l < 0) l += NT;
-            for (; l < cnt; l += NT) {
-                const int c = pts[o0 + l];
-                const int I = c % g.ncx, J = (c / g.ncx) % g.ncy, K = c / sxy;
-                double e[7];
-                if (STREAM) {
-                    coarse_row(g, I, J, K, e);
-                } else {
-#pragma unroll
-                    for (int d = 0; d < 7; ++d) e[d] = __ldg(A7 + (int64_t)d * nc + c);
-                }
-                // y_c = (r_c - sum_{j != c} a_cj y_j) / a_cc, j ascending
-                double s = rs[c];
-                if (K > 0) s = __dsub_rn(s, __dmul_rn(e[0], ys[c - sxy]));
-                if (J > 0) s = __dsub_rn(s, __dmul_rn(e[1], ys[c - g.ncx]));
-                if (I > 0) s = __dsub_rn(s, __dmul_rn(e[2], ys[c - 1]));
-                if (I + 1 < g.ncx) s = __dsub_rn(s, __dmul_rn(e[4], ys[c + 1]));
-                if (J + 1 < g.ncy) s = __dsub_rn(s, __dmul_rn(e[5], ys[c + g.ncx]));
-                if (K + 1 < g.ncz) s = __dsub_rn(s, __dmul_rn(e[6], ys[c + sxy]));
-                ys[c] = __ddiv_rn(s, e[3]);
-            }
-            base += cnt;
+        if (tau >= steps || m_lo > m_hi) {
+            q0 = q1 = 0;
+            return;
         }
+        q0 = wlo[tau - 2 * m_hi];
+        q1 = whi[tau - 2 * m_lo];
+    };
+    auto entries = [&](int q, int m, double e[7]) {
+        if (MODE == 0) {
+            const double2 *p = reinterpret_cast<const double2 *>(A7L + (int64_t)q * 8);
+            const double2 a0 = __ldg(p), a1 = __ldg(p + 1), a2 = __ldg(p + 2), a3 = __ldg(p + 3);
+            e[0] = a0.x; e[1] = a0.y; e[2] = a1.x; e[3] = a1.y; e[4] = a2.x; e[5] = a2.y; e[6] = a3.x;
+        } else if (MODE == 1) {
+            const int f = m >> 24;
+            const int ex = (f & 8) ? g.bx : exl, ey = (f & 16) ? g.by : eyl, ez = (f & 32) ? g.bz : ezl;
+            const double axy = (double)(ex * ey), axz = (double)(ex * ez), ayz = (double)(ey * ez);
+            e[0] = (f & 1) ? -axy : 0.0;
+            e[1] = (f & 2) ? -axz : 0.0;
+            e[2] = (f & 4) ? -ayz : 0.0;
+            e[4] = (f & 8) ? -ayz : 0.0;
+            e[5] = (f & 16) ? -axz : 0.0;
+            e[6] = (f & 32) ? -axy : 0.0;
+            e[3] = center * (double)(ex * ey * ez) -
+                   2.0 * (double)((ex - 1) * ey * ez + ex * (ey - 1) * ez + ex * ey * (ez - 1));
+        } else {
+            const int sc = m & 0xFFFFFF;   // s(c) = I + px (J + ncy K)
+            coarse_row(g, sc % px, (sc / px) % g.ncy, sc / sxy, e);
+        }
+    };
+    // y_c = (r_c - sum_{j != c} a_cj y_j) / a_cc, j ascending (the oracle's order, no FMA)
+    auto relax = [&](int m, const double e[7]) -> double {
+        const int c = m & 0xFFFFFF, f = m >> 24;
+        double s = rs[c];
+        if (f & 1) s = __dsub_rn(s, __dmul_rn(e[0], ys[c - sxy]));
+        if (f & 2) s = __dsub_rn(s, __dmul_rn(e[1], ys[c - px]));
+        if (f & 4) s = __dsub_rn(s, __dmul_rn(e[2], ys[c - 1]));
+        if (f & 8) s = __dsub_rn(s, __dmul_rn(e[4], ys[c + 1]));
+        if (f & 16) s = __dsub_rn(s, __dmul_rn(e[5], ys[c + px]));
+        if (f & 32) s = __dsub_rn(s, __dmul_rn(e[6], ys[c + sxy]));
+        return __ddiv_rn(s, e[3]);
+    };
+    // MODE 0: pe[k] = the entries of this thread's k-th item of the current step;
+    // as soon as item k is relaxed, pe[k] is refilled with the next step's k-th
+    // item (the loads depend on nothing), so the rest of the step and the
+    // barrier cover their L2 latency
+    double pe[PF][7];
+    int q0, q1, n0, n1;
+    range(0, q0, q1);
+    if (MODE == 0) {
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const int q = q0 + tid + k * NT;
+            if (q < q1) entries(q, 0, pe[k]);
+        }
+    }
+    for (int tau = 0; tau < steps; ++tau) {
+        range(tau + 1, n0, n1);
+        double v[PF];
+        int mk[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {   // reads of the first PF items
+            const int q = q0 + tid + k * NT;
+            mk[k] = (q < q1) ? meta[q] : -1;
+            if (mk[k] >= 0) {
+                double e[7];
+                if (MODE == 0) {
+#pragma unroll
+                    for (int d = 0; d < 7; ++d) e[d] = pe[k][d];
+                } else {
+                    entries(q, mk[k], e);
+                }
+                v[k] = relax(mk[k], e);
+            }
+            if (MODE == 0 && n0 + tid + k * NT < n1) entries(n0 + tid + k * NT, 0, pe[k]);
+        }
+        // items beyond PF per thread (n_c above ~2 PF NT): read and written in turn
+        // (no item of a step reads another's output, so the order is free)
+        for (int q = q0 + tid + PF * NT; q < q1; q += NT) {
+            double e[7];
+            const int m = meta[q];
+            entries(q, m, e);
+            ys[m & 0xFFFFFF] = relax(m, e);
+        }
+#pragma unroll
+        for (int k = 0; k < PF; ++k)
+            if (mk[k] >= 0) ys[mk[k] & 0xFFFFFF] = v[k];
+        q0 = n0;
+        q1 = n1;
         __syncthreads();
     }
-    for (int i = tid; i < nc; i += NT) y[i] = ys[i];
+    for (int i = tid; i < nc; i += NT) y[i] = ys[sidx(i)];
 }
 
-size_t fgs_smem(int nc, int T) { return (size_t)nc * 16 + (size_t)nc * 4 + (size_t)(T + 1) * 4; }
+// assembled entries in list order: A7L[q * 8 + d]
+__global__ void k_coarse_entries_list(CG g, const int *meta, int nc, double *out)
+{
+    const int px = (g.ncx + 1) & ~1;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nc; q += gridDim.x * blockDim.x) {
+        const int sc = meta[q] & 0xFFFFFF;
+        const int I = sc % px, J = (sc / px) % g.ncy, K = sc / (px * g.ncy);
+        double e[7];
+        coarse_row(g, I, J, K, e);
+#pragma unroll
+        for (int d = 0; d < 7; ++d) out[(int64_t)q * 8 + d] = e[d];
+        out[(int64_t)q * 8 + 7] = 0.0;
+    }
+}
+
+size_t fgs_smem(int nc, int ns, int T) { return (size_t)ns * 16 + (size_t)nc * 4 + (size_t)2 * T * 4; }
 
 }  // namespace
 
 struct sscg_coarse {
     CG g{};
     int mode = 0, nc = 0, T = 0;
-    double *A7 = nullptr;
-    int *wf_pts = nullptr, *wf_off = nullptr;
+    int exl = 0, eyl = 0, ezl = 0;   // extents of the last aggregate of each axis
+    double *A7L = nullptr;           // assembled: entries in list order, 8 doubles per point
+    int *meta = nullptr, *wlo = nullptr, *whi = nullptr;   // the parity-major point list (k_coarse_fgs)
 };
 
 #define CCU(call)                                                                                   \
@@ -253,9 +364,10 @@ static unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>((n + 25
 extern "C" void sscg_coarse_destroy(sscg_coarse *h)
 {
     if (!h) return;
-    cudaFree(h->A7);
-    cudaFree(h->wf_pts);
-    cudaFree(h->wf_off);
+    cudaFree(h->A7L);
+    cudaFree(h->meta);
+    cudaFree(h->wlo);
+    cudaFree(h->whi);
     delete h;
 }
 
@@ -293,36 +405,53 @@ extern "C" sscg_status sscg_coarse_create(const sscg_operator *A, int32_t bx, in
     h->g = g;
     h->mode = mode;
     h->nc = (int)nc;
-    h->T = g.ncx + g.ncy + g.ncz - 2;
-    // wavefront lists: points with I + J + K = t, ascending index
-    std::vector<int> off(h->T + 2, 0), pts(nc);
+    h->T = g.ncx + g.ncy + g.ncz - 2;   // wavefronts t = I + J + K in [0, T)
+    h->exl = g.nx - (g.ncx - 1) * bx;
+    h->eyl = g.ny - (g.ncy - 1) * by;
+    h->ezl = g.nz - (g.ncz - 1) * bz;
+    // the point list, parity-major: wavefronts t = 0, 2, 4, ... then 1, 3, ...,
+    // each in ascending index; meta = c | neighbour flags << 24
+    const int T = h->T;
+    std::vector<int> cnt(T, 0), wlo(T), whi(T), meta(nc);
     for (int64_t c = 0; c < nc; ++c) {
         const int I = (int)(c % g.ncx), J = (int)((c / g.ncx) % g.ncy), K = (int)(c / ((int64_t)g.ncx * g.ncy));
-        off[I + J + K + 1] += 1;
+        cnt[I + J + K] += 1;
     }
-    for (int t = 0; t <= h->T; ++t) off[t + 1] += off[t];
-    std::vector<int> fill(off.begin(), off.end());
+    int pos = 0;
+    for (int p = 0; p < 2; ++p)
+        for (int t = p; t < T; t += 2) {
+            wlo[t] = pos;
+            pos += cnt[t];
+            whi[t] = pos;
+        }
+    std::vector<int> fill(wlo);
     for (int64_t c = 0; c < nc; ++c) {
         const int I = (int)(c % g.ncx), J = (int)((c / g.ncx) % g.ncy), K = (int)(c / ((int64_t)g.ncx * g.ncy));
-        pts[fill[I + J + K]++] = (int)c;
+        const int flags = (K > 0) | (J > 0) << 1 | (I > 0) << 2 | (I + 1 < g.ncx) << 3 | (J + 1 < g.ncy) << 4 |
+                          (K + 1 < g.ncz) << 5;
+        meta[fill[I + J + K]++] = (I + ((g.ncx + 1) & ~1) * (J + g.ncy * K)) | flags << 24;   // s(c), see k_coarse_fgs
     }
     auto bail = [&](sscg_status st) {
         sscg_coarse_destroy(h);
         return st;
     };
-    cudaError_t e = cudaMalloc(&h->wf_pts, nc * sizeof(int));
-    if (e == cudaSuccess) e = cudaMalloc(&h->wf_off, (h->T + 2) * sizeof(int));
-    if (e == cudaSuccess) e = cudaMemcpy(h->wf_pts, pts.data(), nc * sizeof(int), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(h->wf_off, off.data(), (h->T + 2) * sizeof(int), cudaMemcpyHostToDevice);
-    const int smem = (int)fgs_smem(h->nc, h->T);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_coarse_fgs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_coarse_fgs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaMalloc(&h->meta, nc * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&h->wlo, T * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&h->whi, T * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemcpy(h->meta, meta.data(), nc * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->wlo, wlo.data(), T * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->whi, whi.data(), T * sizeof(int), cudaMemcpyHostToDevice);
+    const int smem = (int)fgs_smem(h->nc, ((h->g.ncx + 1) & ~1) * h->g.ncy * h->g.ncz, h->T);
+    if (smem > 226 * 1024)
+        return bail(api_fail(SSCG_ERR_UNSUPPORTED, "sscg_coarse_create: %d B of shared memory for n_c = %lld "
+                             "(row-padded y and r)", smem, (long long)nc));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_fgs<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_fgs<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_coarse_fgs<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess && mode == SSCG_COARSE_ASSEMBLED) {
-        e = cudaMalloc(&h->A7, 7 * nc * sizeof(double));
+        e = cudaMalloc(&h->A7L, 8 * nc * sizeof(double));
         if (e == cudaSuccess) {
-            k_coarse_entries<<<grid_for(nc), 256>>>(g, h->A7);
+            k_coarse_entries_list<<<grid_for(nc), 256>>>(g, h->meta, (int)nc, h->A7L);
             e = cudaGetLastError();
         }
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -356,11 +485,18 @@ extern "C" sscg_status sscg_coarse_fgs(sscg_coarse *h, const double *rc, double 
     if (!h || !rc || !y) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_fgs: null argument");
     if (nu < 0) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_fgs: nu = %d", (int)nu);
     if (nu == 0) return SSCG_OK;
-    const size_t smem = fgs_smem(h->nc, h->T);
-    if (h->mode == SSCG_COARSE_STREAMING)
-        k_coarse_fgs<true><<<1, NT, smem, (cudaStream_t)stream>>>(h->g, nullptr, rc, y, nu, h->wf_pts, h->wf_off, h->T);
+    const size_t smem = fgs_smem(h->nc, ((h->g.ncx + 1) & ~1) * h->g.ncy * h->g.ncz, h->T);
+    const double center = h->g.kind == SSCG_OP_STENCIL5_2D ? 4.0 : 6.0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (h->mode == SSCG_COARSE_ASSEMBLED)
+        k_coarse_fgs<0><<<1, NT, smem, st>>>(h->g, h->A7L, rc, y, nu, h->meta, h->wlo, h->whi, h->T, h->exl, h->eyl,
+                                             h->ezl, center);
+    else if (h->g.kind != SSCG_OP_VARCOEF7)   // streaming, constant stencils: closed-form entries
+        k_coarse_fgs<1><<<1, NT, smem, st>>>(h->g, nullptr, rc, y, nu, h->meta, h->wlo, h->whi, h->T, h->exl, h->eyl,
+                                             h->ezl, center);
     else
-        k_coarse_fgs<false><<<1, NT, smem, (cudaStream_t)stream>>>(h->g, h->A7, rc, y, nu, h->wf_pts, h->wf_off, h->T);
+        k_coarse_fgs<2><<<1, NT, smem, st>>>(h->g, nullptr, rc, y, nu, h->meta, h->wlo, h->whi, h->T, h->exl, h->eyl,
+                                             h->ezl, center);
     CCU(cudaGetLastError());
     return SSCG_OK;
 }
@@ -368,13 +504,8 @@ extern "C" sscg_status sscg_coarse_fgs(sscg_coarse *h, const double *rc, double 
 extern "C" sscg_status sscg_coarse_entries(sscg_coarse *h, double *out, void *stream)
 {
     if (!h || !out) return api_fail(SSCG_ERR_INVALID, "sscg_coarse_entries: null argument");
-    if (h->mode == SSCG_COARSE_ASSEMBLED) {
-        CCU(cudaMemcpyAsync(out, h->A7, 7 * (size_t)h->nc * sizeof(double), cudaMemcpyDeviceToDevice,
-                            (cudaStream_t)stream));
-    } else {
-        k_coarse_entries<<<grid_for(h->nc), 256, 0, (cudaStream_t)stream>>>(h->g, out);
-        CCU(cudaGetLastError());
-    }
+    k_coarse_entries<<<grid_for(h->nc), 256, 0, (cudaStream_t)stream>>>(h->g, out);   // (the routine the assembly ran)
+    CCU(cudaGetLastError());
     return SSCG_OK;
 }
 
@@ -387,7 +518,7 @@ extern "C" sscg_status sscg_coarse_query(const sscg_coarse *h, int32_t what, int
     case SSCG_COARSE_QUERY_NCY: *out = h->g.ncy; break;
     case SSCG_COARSE_QUERY_NCZ: *out = h->g.ncz; break;
     case SSCG_COARSE_QUERY_WAVEFRONTS: *out = h->T; break;
-    case SSCG_COARSE_QUERY_MATRIX_BYTES: *out = h->A7 ? 7 * (int64_t)h->nc * 8 : 0; break;
+    case SSCG_COARSE_QUERY_MATRIX_BYTES: *out = h->A7L ? 8 * (int64_t)h->nc * 8 : 0; break;
     default: return api_fail(SSCG_ERR_INVALID, "sscg_coarse_query: unknown key %d", (int)what);
     }
     return SSCG_OK;

@@ -67,7 +67,7 @@ def test_coarse_parity_bitwise(kind, dims, b, mode):
     A, faces, Ac = oracle_case(kind, dims, b)
     with gpu_coarse(kind, dims, b, mode, faces) as G:
         assert G.n == Ac.n and G.dims == orc.coarse_dims(A, b)
-        assert G.query(5) == (0 if mode == "streaming" else 7 * Ac.n * 8)   # COARSE_QUERY_MATRIX_BYTES
+        assert G.query(5) == (0 if mode == "streaming" else 8 * Ac.n * 8)   # COARSE_QUERY_MATRIX_BYTES (7 entries + pad)
         # entries of A_c
         assert np.array_equal(G.entries().cpu().numpy(), expected_entries(Ac, G.dims))
         # restriction of a fine residual, prolongation of a coarse vector
