@@ -46,7 +46,8 @@ struct CG {
     const double *kx, *ky, *kz;   // VARCOEF7 faces (layout of sscg.h), else null
 };
 
-constexpr int NT = 1024;   // FGS threads (one CTA)
+constexpr int NT = 1024;   // FGS threads (one CTA); 512 for the variable-coefficient streaming mode
+constexpr int nt_for(int mode) { return mode == 2 ? 512 : NT; }
 
 // face coefficients around fine cell (i, j, k); 1 for the constant stencils
 __device__ __forceinline__ double kxm(const CG &g, int i, int j, int k)
@@ -133,6 +134,88 @@ __device__ void coarse_row(const CG &g, int I, int J, int K, double e[7])
     e[6] = a;
 }
 
+// coarse_row for a full 2 x 2 x 2 aggregate of the variable-coefficient
+// operator, the streaming mode's common case: the 36 distinct faces it touches
+// are loaded first (independent L2 loads, one round trip instead of a chain of
+// ~96), then combined in exactly coarse_row's order -- the same doubles
+__device__ void coarse_row_vc222(const CG &g, int I, int J, int K, double e[7])
+{
+    const int x0 = 2 * I, y0 = 2 * J, z0 = 2 * K;
+    double fx[2][2][3], fy[2][3][2], fz[3][2][2];   // fx[k][j][i]: kx(x0+i, y0+j, z0+k), i = 0..2; etc.
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) fx[k][j][i] = __ldg(g.kx + ((int64_t)(z0 + k) * g.ny + y0 + j) * (g.nx + 1) + x0 + i);
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) fy[k][j][i] = __ldg(g.ky + ((int64_t)(z0 + k) * (g.ny + 1) + y0 + j) * g.nx + x0 + i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) fz[k][j][i] = __ldg(g.kz + ((int64_t)(z0 + k) * g.ny + y0 + j) * g.nx + x0 + i);
+    double d = 0.0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                // fine_diag: z-, y-, x-, x+, y+, z+
+                double t = __dadd_rn(fz[k][j][i], fy[k][j][i]);
+                t = __dadd_rn(t, fx[k][j][i]);
+                t = __dadd_rn(t, fx[k][j][i + 1]);
+                t = __dadd_rn(t, fy[k][j + 1][i]);
+                t = __dadd_rn(t, fz[k + 1][j][i]);
+                // couplings inside the aggregate, same order
+                if (k == 1) t = __dsub_rn(t, fz[k][j][i]);
+                if (j == 1) t = __dsub_rn(t, fy[k][j][i]);
+                if (i == 1) t = __dsub_rn(t, fx[k][j][i]);
+                if (i == 0) t = __dsub_rn(t, fx[k][j][i + 1]);
+                if (j == 0) t = __dsub_rn(t, fy[k][j + 1][i]);
+                if (k == 0) t = __dsub_rn(t, fz[k + 1][j][i]);
+                d = __dadd_rn(d, t);
+            }
+    e[3] = d;
+    double a;
+    a = 0.0;
+    if (K > 0)
+        for (int j = 0; j < 2; ++j)
+            for (int i = 0; i < 2; ++i) a = __dsub_rn(a, fz[0][j][i]);
+    e[0] = a;
+    a = 0.0;
+    if (J > 0)
+        for (int k = 0; k < 2; ++k)
+            for (int i = 0; i < 2; ++i) a = __dsub_rn(a, fy[k][0][i]);
+    e[1] = a;
+    a = 0.0;
+    if (I > 0)
+        for (int k = 0; k < 2; ++k)
+            for (int j = 0; j < 2; ++j) a = __dsub_rn(a, fx[k][j][0]);
+    e[2] = a;
+    a = 0.0;
+    if (I + 1 < g.ncx)
+        for (int k = 0; k < 2; ++k)
+            for (int j = 0; j < 2; ++j) a = __dsub_rn(a, fx[k][j][2]);
+    e[4] = a;
+    a = 0.0;
+    if (J + 1 < g.ncy)
+        for (int k = 0; k < 2; ++k)
+            for (int i = 0; i < 2; ++i) a = __dsub_rn(a, fy[k][2][i]);
+    e[5] = a;
+    a = 0.0;
+    if (K + 1 < g.ncz)
+        for (int j = 0; j < 2; ++j)
+            for (int i = 0; i < 2; ++i) a = __dsub_rn(a, fz[2][j][i]);
+    e[6] = a;
+}
+
 __global__ void k_coarse_entries(CG g, double *out)
 {
     const int nc = g.ncx * g.ncy * g.ncz;
@@ -206,7 +289,7 @@ constexpr int PF = COARSE_PF;
 // ascending c, are (ncx - 1) apart in c -- with ncx = 17 every lane of a warp
 // hit the same bank (a 32-way conflict on every y load) -- and px - 1 odd
 // apart in s; meta carries s(c).
-template <int MODE>
+template <int MODE, int NT = nt_for(MODE)>
 __global__ void __launch_bounds__(NT, 1)
     k_coarse_fgs(CG g, const double *__restrict__ A7L, const double *rc, double *y, int nu, const int *meta_g,
                  const int *wlo_g, const int *whi_g, int T, int exl, int eyl, int ezl, double center)
@@ -257,7 +340,11 @@ __global__ void __launch_bounds__(NT, 1)
                    2.0 * (double)((ex - 1) * ey * ez + ex * (ey - 1) * ez + ex * ey * (ez - 1));
         } else {
             const int sc = m & 0xFFFFFF;   // s(c) = I + px (J + ncy K)
-            coarse_row(g, sc % px, (sc / px) % g.ncy, sc / sxy, e);
+            const int I = sc % px, J = (sc / px) % g.ncy, K = sc / sxy;
+            if (g.bx == 2 && g.by == 2 && g.bz == 2 && 2 * I + 2 <= g.nx && 2 * J + 2 <= g.ny && 2 * K + 2 <= g.nz)
+                coarse_row_vc222(g, I, J, K, e);   // a full aggregate: all faces loaded at once
+            else
+                coarse_row(g, I, J, K, e);
         }
     };
     // y_c = (r_c - sum_{j != c} a_cj y_j) / a_cc, j ascending (the oracle's order, no FMA)
@@ -495,7 +582,7 @@ extern "C" sscg_status sscg_coarse_fgs(sscg_coarse *h, const double *rc, double 
         k_coarse_fgs<1><<<1, NT, smem, st>>>(h->g, nullptr, rc, y, nu, h->meta, h->wlo, h->whi, h->T, h->exl, h->eyl,
                                              h->ezl, center);
     else
-        k_coarse_fgs<2><<<1, NT, smem, st>>>(h->g, nullptr, rc, y, nu, h->meta, h->wlo, h->whi, h->T, h->exl, h->eyl,
+        k_coarse_fgs<2><<<1, nt_for(2), smem, st>>>(h->g, nullptr, rc, y, nu, h->meta, h->wlo, h->whi, h->T, h->exl, h->eyl,
                                              h->ezl, center);
     CCU(cudaGetLastError());
     return SSCG_OK;
