@@ -24,6 +24,12 @@
 // consumer thread arrives -- one elected lane per warp after __syncwarp measured
 // 0.69-0.70 vs 0.65 ms per launch); with 4 slots per ring a thread that waited for
 // U1(q-2) / U2(q-3) knows every read of the slot it overwrites is done.
+// Measured and not kept: waiting only for the two neighbour rows a warp reads
+// (per-row mbarriers per ring slot: 0.795 vs 0.743 ms per triple; spinning on
+// acquire loads of per-row plane counters: 1.18 ms) -- the CTA-wide plane
+// barrier keeps the rows in lockstep, which the shared stage ring relies on;
+// a 56 x 20 tile (24 row warps, 5 stages, 3 U slots; K1M_TY=20): 0.722 vs 0.743
+// ms per triple in the profiled pass, within box noise on the whole step.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
