@@ -29,7 +29,10 @@
 // acquire loads of per-row plane counters: 1.18 ms) -- the CTA-wide plane
 // barrier keeps the rows in lockstep, which the shared stage ring relies on;
 // a 56 x 20 tile (24 row warps, 5 stages, 3 U slots; K1M_TY=20): 0.722 vs 0.743
-// ms per triple in the profiled pass, within box noise on the whole step.
+// ms per triple in the profiled pass, within box noise on the whole step; two
+// box rows per warp (10 warps, the pair's inner y-neighbours from registers at
+// every level: ~20 % fewer consumer shared-memory wavefronts, parity green):
+// 0.764 vs 0.741 ms -- half the warps hide less latency than the wavefronts save.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
