@@ -5,7 +5,7 @@ for w in "--workload cfg1" "--workload cfg2" "--workload cfg3" "--workload cfg4 
 import json, sys
 d = json.loads(open('/tmp/w.json').read().strip().splitlines()[-1])
 k = d['kernels']
-k1s = k.get('basis_single', {}).get('frac')
-print("%-34s GDOF/s %7.3f ms/step %8.4f path %.3f | K1 %.3f | K1 single %s | K2 %.3f | K5 %.3f | K4 %.1f us" % (sys.argv[1], d['value'], d['ms_per_step'], d['roofline']['path_frac'], k['basis']['frac'], "%.3f" % k1s if k1s else "-", k['gram']['frac'], k['update']['frac'], k['fgs']['us_per_launch']))
+f = lambda n: "%.3f" % k[n]['frac'] if n in k and k[n].get('frac') else "-"   # KS (cfg 1): one launch
+print("%-34s GDOF/s %7.3f ms/step %8.4f path %.3f | K1 %s | K1 single %s | K2 %s | K5 %s | K4 %.1f us" % (sys.argv[1], d['value'], d['ms_per_step'], d['roofline']['path_frac'], f('basis'), f('basis_single'), f('gram'), f('update'), k['fgs']['us_per_launch']))
 PY
 done
