@@ -840,32 +840,33 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
 }
 
 namespace {
-// k_pap (the w_{s-1} fold): Ghat_{s-1,s-1} = p_{s-1}^T A p_{s-1} over one slab,
-// A the 7-point stencil with a constant centre (zero outside the grid in x and
-// y; the ghost planes carry the z-neighbours), each A p formed in the order of
+// k_pap (the w_{s-1} fold without TMA; the TMA path runs the K1T single step
+// in its dot mode): Ghat_{s-1,s-1} = p_{s-1}^T A p_{s-1} over one slab, A the
+// 7-point stencil with a constant centre (zero outside the grid in x and y;
+// the ghost planes carry the z-neighbours), each A p formed in the order of
 // the single step it replaces: c p - (p_{z-1} + p_{y-1} + p_{x-1} + p_{x+1} +
-// p_{y+1} + p_{z+1}).  A block owns a 64 x 8 tile of columns and marches a
+// p_{y+1} + p_{z+1}).  A block owns a 64 x 16 tile of columns and marches a
 // z-chunk: warp = row, lane = point pair; p(z-1), p(z) ride in registers, so
 // per plane only p(z+1) streams from HBM and the in-plane neighbours are L1
 // hits (a grid-stride pass with all six neighbour loads ran 0.27 ms at 448^3:
-// L2-bound).  Per-block partials in a fixed order, then the last block sums
-// them in index order (deterministic) into the slab's Gram block entry.
-constexpr int PAP_TX = 64;
+// L2-bound; this one 0.22 ms over tile heights 4..32 and 4..16 blocks per SM).
+// Per-block partials in a fixed order, then the last block sums them in index
+// order (deterministic) into the slab's Gram block entry.
+constexpr int PAP_TX = 64, PAP_TY = 16, PAP_THREADS = 32 * PAP_TY;
 
-template <int PAP_TY>
-__global__ void __launch_bounds__(32 * PAP_TY) k_pap(const double *p, int nx, int ny, int nzl, int64_t plane, int zc,
-                                                     int tiles_x, double center, double *part, unsigned *ticket,
-                                                     double *entry, const DevState *st)
+__global__ void __launch_bounds__(PAP_THREADS) k_pap(const double *p, int nx, int ny, int nzl, int64_t plane, int zc,
+                                                     int tiles_x, int nitems, double center, double *part,
+                                                     unsigned *ticket, double *entry, const DevState *st)
 {
-    constexpr int PAP_THREADS = 32 * PAP_TY;
     PDL_ENTRY(st);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ntiles = tiles_x * ((ny + PAP_TY - 1) / PAP_TY);
-    const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
-    const int x = (tile % tiles_x) * PAP_TX + 2 * lane, y = (tile / tiles_x) * PAP_TY + warp;
-    const int zb = 1 + chunk * zc, ze = min(nzl + 1, zb + zc);
     double acc = 0.0;
-    if (x < nx && y < ny && zb < ze) {
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {   // items: tile x z-chunk
+        const int tile = item % ntiles, chunk = item / ntiles;
+        const int x = (tile % tiles_x) * PAP_TX + 2 * lane, y = (tile / tiles_x) * PAP_TY + warp;
+        const int zb = 1 + chunk * zc, ze = min(nzl + 1, zb + zc);
+        if (x >= nx || y >= ny || zb >= ze) continue;
         // p points at plane 0 (the lower ghost plane) of p_{s-1}
         const double *col = p + (int64_t)y * nx + x;
         double2 dn = __ldg(reinterpret_cast<const double2 *>(col + (int64_t)(zb - 1) * plane));
@@ -914,21 +915,20 @@ __global__ void __launch_bounds__(32 * PAP_TY) k_pap(const double *p, int nx, in
 }
 }  // namespace
 
-// blocks: tiles x z-chunks, the chunk length chosen for about 8 blocks per SM
-// (one wave), bounded by the partial buffer (k2_grid() * 8 doubles at least)
+// items: tiles x z-chunks, the chunk length chosen for about 8 blocks per SM
+// (one wave); the grid (one partial per block) at most k2_grid() * 8 blocks,
+// which the partial buffer always holds
 void launch_pap(const Geo &g, const Slab &sl, int s, const DevState *st, double *out_blk, cudaStream_t stream)
 {
-    static const int ty = getenv("SSCG_PAP_TY") ? atoi(getenv("SSCG_PAP_TY")) : 8;
-    static const int per_sm = getenv("SSCG_PAP_BPS") ? atoi(getenv("SSCG_PAP_BPS")) : 8;
-    const int tiles_x = (g.nx + PAP_TX - 1) / PAP_TX, tiles = tiles_x * ((g.ny + ty - 1) / ty);
-    const int64_t want = (int64_t)k2_grid() * per_sm;
+    const int tiles_x = (g.nx + PAP_TX - 1) / PAP_TX, tiles = tiles_x * ((g.ny + PAP_TY - 1) / PAP_TY);
+    const int64_t want = (int64_t)k2_grid() * 8;
     int nch = (int)std::max<int64_t>(1, std::min<int64_t>(sl.nzl, want / tiles));
     const int zc = (sl.nzl + nch - 1) / nch;
     nch = (sl.nzl + zc - 1) / zc;
-    auto kern = ty == 4 ? k_pap<4> : ty == 16 ? k_pap<16> : ty == 32 ? k_pap<32> : k_pap<8>;
-    launch_pdl(g.kn.pdl, kern, dim3((unsigned)(tiles * nch)), dim3(32 * ty), 0, stream,
+    const int nitems = tiles * nch, grid = (int)std::min<int64_t>(nitems, want);
+    launch_pdl(g.kn.pdl, k_pap, dim3((unsigned)grid), dim3(PAP_THREADS), 0, stream,
                (const double *)(sl.P + (int64_t)(s - 1) * g.vstride), g.nx, g.ny, sl.nzl, g.plane, zc, tiles_x,
-               g.center, sl.part, sl.ticket, out_blk + (int64_t)(s - 1) * s + (s - 1), st);
+               nitems, g.center, sl.part, sl.ticket, out_blk + (int64_t)(s - 1) * s + (s - 1), st);
 }
 
 }  // namespace sscg
