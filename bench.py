@@ -47,6 +47,10 @@ WORKLOADS = {
                      "Jacobi, Lanczos-50 bounds widened 5% (GPU)"},
     "cfg5": {"kind": "7pt", "n": 448, "s": 16, "nu": 30, "bounds": "analytic",
              "desc": "cfg5: 3D 7-point Poisson {n}^3 per GPU (z-slab weak scaling), FP64, Jacobi, analytic bounds"},
+    # not a BASELINE config: the general sparse path (SSCG_OP_CSR) on cfg 2's operator, assembled
+    "csr": {"kind": "csr7", "n": 128, "s": 16, "nu": 25, "bounds": "analytic",
+            "desc": "csr: the 3D 7-point Poisson operator {n}^3 assembled as CSR (general sparse path, one slab "
+                    "per GPU; replicas for N > 1), FP64, Jacobi, analytic bounds"},
 }
 METRIC = "s-step CG time/outer-iter & GDOF/s at 1/2/4/8 B200; % of HBM peak"
 UNIT = "GDOF/s"
@@ -88,12 +92,18 @@ def workload(a, nranks):
                 "n_global": n * n * nranks, "parallelism": f"replicas x{nranks}" if nranks > 1 else "single GPU",
                 "l2": "working set (%.2f MB) resident in the 126 MB L2: a latency measurement, no roofline claim"
                       % ((2 * a.s + 2) * n * n * 8 / 1e6)}
-    nzg = n if a.strong else n * nranks
+    csr = a.kind == "csr7"
+    nzg = n if (a.strong or csr) else n * nranks
     desc = WORKLOADS[a.workload]["desc"].format(n=n)
     if a.strong:
         desc = desc.replace("per GPU", "global (strong scaling)")
     if a.block or a.gram_solver != "fgs":
         desc += "; variant: %s%s" % ("block-conjugate s-step CG, " if a.block else "", a.gram_solver + " Gram solve")
+    if csr:
+        return {"workload": f"{desc}, s={a.s}, nu={a.nu}, x0=0, b~U[-1,1] seed 42", "nx": n, "ny": n,
+                "nz_per_gpu": n, "nz_global": n, "s": a.s, "nu": a.nu, "n_global": n * n * n * nranks,
+                "parallelism": f"replicas x{nranks}" if nranks > 1 else "single GPU",
+                "l2": "no flush: the matrix and s+2 vectors (%.2f GB) >> 126 MB L2" % ((a.s + 2 + 12) * n ** 3 * 8 / 1e9)}
     return {"workload": f"{desc}, s={a.s}, nu={a.nu}, x0=0, b~U[-1,1] seed 42",
             "nx": n, "ny": n, "nz_per_gpu": nzg // nranks, "nz_global": nzg, "s": a.s, "nu": a.nu,
             "n_global": n * n * nzg, "parallelism": f"z-slab x{nranks}",
@@ -120,6 +130,9 @@ def oracle_sample(a, steps, warmup, planes=None):
     elif a.kind == "varcoef7":
         A = orc.stencil(orc.KIND_VARCOEF7, n, n, zs, *inputs.lognormal_faces(n, n, zs, seed=42))
         lmin, lmax, _ = orc.lanczos_bounds(A, 50, b, 0.05)     # untimed setup
+    elif a.kind == "csr7":   # the oracle's CSR operator on the sample
+        A = orc.csr(*inputs.stencil7_csr_fast(n, n, zs))
+        lmin, lmax = inputs.analytic_bounds("7pt", n, n, zs)
     else:
         A = orc.stencil({"7pt": orc.KIND_7PT, "27pt": orc.KIND_27PT}[a.kind], n, n, zs)
         lmin, lmax = inputs.analytic_bounds(a.kind, n, n, zs)
@@ -355,12 +368,14 @@ def run_ours(a):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, s, nu = a.n, a.s, a.nu
     twod = a.kind == "5pt"          # cfg 1: one 2D grid per GPU (replicas for N > 1)
-    nz = 1 if twod else (n if a.strong else n * world)
-    z0, nzl = (0, 1) if twod else sscg.partition(nz, world, 1, rank)
+    csr = a.kind == "csr7"          # the general sparse path: one slab per process (replicas for N > 1)
+    replica = twod or csr
+    nz = 1 if twod else (n if (a.strong or csr) else n * world)
+    z0, nzl = (0, 1) if twod else (0, nz) if csr else sscg.partition(nz, world, 1, rank)
     b_host = torch.from_numpy(inputs.rhs_uniform(n, n, nz, seed=42, z0=z0, nzl=nzl)).pin_memory()
     b = b_host.cuda()
     nid = None
-    if world > 1 and not twod:
+    if world > 1 and not replica:
         obj = [sscg.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
@@ -371,18 +386,23 @@ def run_ours(a):
                  for f in (kx[z0:z0 + nzl], ky[z0:z0 + nzl], kz[z0:z0 + nzl + 1])]
         del kx, ky, kz
         op = sscg.Stencil("varcoef7", n, n, nz, *faces)
+    elif csr:
+        csr_arrays = [torch.from_numpy(v).cuda() for v in inputs.stencil7_csr_fast(n, n, nz)]
+        op = sscg.CSR(*csr_arrays)
     else:
         op = sscg.Stencil(a.kind, n, n, nz)
     variant = {"gram_solver": a.gram_solver, "block": a.block}
     if twod:
         S = sscg.Solver(op, *inputs.analytic_bounds(a.kind, n, n), s, nu, **variant)
+    elif csr:
+        S = sscg.Solver(op, *inputs.analytic_bounds("7pt", n, n, nz), s, nu, **variant)
     elif WORKLOADS[a.workload]["bounds"] == "analytic":
         S = sscg.Solver(op, *inputs.analytic_bounds(a.kind, n, n, nz), s, nu, rank=rank, nranks=world, nccl_id=nid,
                         **variant)
     else:   # 50 Lanczos steps on the GPU, widened 5 % (R13), untimed setup
         S = sscg.Solver(op, 0.0, 0.0, s, nu, rank=rank, nranks=world, nccl_id=nid, **variant)
         S.set_bounds(*S.estimate_bounds(b, 50, 0.05))
-    n_local, n_global = S.n_local, n * n * nz * (world if twod else 1)
+    n_local, n_global = S.n_local, n * n * nz * (world if replica else 1)
 
     def barrier():
         torch.cuda.synchronize()
@@ -422,6 +442,8 @@ def run_ours(a):
     face_bytes = 0.0
     if a.kind == "varcoef7":   # kx, ky, kz of this slab, read by every basis step
         face_bytes = 8.0 * (n * (n + 1) * S.nz_local * 2 + n * n * (S.nz_local + 1))
+    if csr:                    # the matrix, streamed by every SpMV: rowptr (8 B/row), colind + val (12 B/nnz)
+        face_bytes = 8.0 * (n_local + 1) + 12.0 * float(csr_arrays[1].numel())
     basis_vecs = S.query(sscg.QUERY_BASIS_VECTORS)       # (4s-3) single steps, fewer with pairs / triples
     single_vecs = S.query(sscg.QUERY_BASIS_SINGLE_VECTORS)   # the single steps of a fused schedule (j = s-1)
     depth = S.query(sscg.QUERY_BASIS_FUSED)               # basis steps per launch: 1, 2 (K1F) or 3 (K1M)
@@ -451,7 +473,7 @@ def run_ours(a):
     k1 = kern["basis"]
     path_bytes = sum(bytes_per_outer.values())
     cfg = workload(a, world)
-    k1_name = {3: "k1m", 2: "k1f"}.get(depth, K1_NAME)
+    k1_name = {3: "k1m", 2: "k1f"}.get(depth, "k1_csr" if csr else K1_NAME)
     # read : write vectors of one interior basis launch (W recovered in the Gram pass: p only)
     wfree = gram_vecs < 2 * s
     mixrw = (2, depth) if wfree else (2, 2 * depth)

@@ -147,6 +147,24 @@ def poisson_csr_1d(n: int):
     return np.array(rowptr, np.int64), np.array(cols, np.int32), np.array(vals, np.float64)
 
 
+def stencil7_csr_fast(nx: int, ny: int, nz: int):
+    """The 7-point graph Laplacian (6 / -1, Dirichlet) of an nx x ny x nz grid as
+    CSR with ascending columns (z-1, y-1, x-1, itself, x+1, y+1, z+1), built
+    vectorised for large grids (bench.py's CSR workload); the same matrix as
+    stencil_csr("7pt", ...)."""
+    n = nx * ny * nz
+    g = np.arange(n, dtype=np.int64)
+    x, y, z = g % nx, (g // nx) % ny, g // (nx * ny)
+    offs = [(-nx * ny, z > 0), (-nx, y > 0), (-1, x > 0), (0, np.ones(n, bool)), (1, x < nx - 1),
+            (nx, y < ny - 1), (nx * ny, z < nz - 1)]
+    valid = np.stack([m for _, m in offs], axis=1)                    # [n, 7]
+    cols = g[:, None] + np.array([o for o, _ in offs], np.int64)[None, :]
+    vals = np.where(np.arange(7)[None, :] == 3, 6.0, -1.0) * np.ones((n, 1))
+    rowptr = np.zeros(n + 1, np.int64)
+    rowptr[1:] = np.cumsum(valid.sum(axis=1))
+    return rowptr, cols[valid].astype(np.int32), vals[valid]
+
+
 def stencil_csr(kind: str, nx: int, ny: int, nz: int = 1, faces=None):
     """Assemble a stencil operator as CSR (sorted columns) for CSR-path tests."""
     n = nx * ny * nz

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(256) k1_csr(Geo g, K1Args a, const DevState *s
         a.w[i] = ld(a.b + r) - Ap;
         return;
     }
-    a.w[i] = Ap;
+    if (!a.skip_w) a.w[i] = Ap;
     if (a.mode >= 1) {
         const double t = (a.dinv ? ld(a.dinv + i) : a.dinv_c) * Ap - a.sigma * ld(a.p + i);
         double v = a.coef * t;

@@ -279,7 +279,7 @@ static sscg_status build_basis_store(sscg_ctx *c, int nvec)
                 return fail(SSCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the fused variable-coefficient step");
             sl.has_k1f = true;
         }
-        if (kind == SSCG_OP_STENCIL7 || kind == SSCG_OP_STENCIL27 || kind == SSCG_OP_VARCOEF7) {
+        if (kind == SSCG_OP_STENCIL7 || kind == SSCG_OP_STENCIL27 || kind == SSCG_OP_VARCOEF7 || kind == SSCG_OP_CSR) {
             if (!k2r_prepare(g, sl, s)) return fail(SSCG_ERR_CUDA, "tensor maps for the recovered-W Gram pass");
             sl.has_k2r = true;
         }
@@ -481,8 +481,9 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
             CU(cudaGetLastError());
             sl.dinv = dv;
         }
-        if (A->kind != SSCG_OP_CSR && (diag_M || A->kind == SSCG_OP_VARCOEF7)) {
-            // diag(M) per point for the recurrence form of the update (R21)
+        if (diag_M || A->kind == SSCG_OP_VARCOEF7 || A->kind == SSCG_OP_CSR) {
+            // diag(M) per point for the recurrence form of the update (R21) and the
+            // W-free Gram pass (R23); for CSR 1 / the D^{-1} the basis uses
             double *dd = nullptr;
             TRY(dalloc(c, &dd, (size_t)g.vstride));
             CU(cudaMemsetAsync(dd, 0, (size_t)g.vstride * sizeof(double), c->stream));
@@ -757,7 +758,7 @@ static bool uses_rec_update(const sscg_ctx *c)
 {
     const Geo &g = c->g;
     if (!g.kn.k5_recur || c->blockcg) return false;
-    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2 || g.kind == SSCG_OP_CSR || g.pitch != g.nx) return false;
+    if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2 || g.pitch != g.nx) return false;
     for (const auto &sl : c->slabs)
         if (!sl.dvec && !(g.center > 0.0 && !sl.dinv)) return false;   // need m or diag(M) per point
     return true;
@@ -770,8 +771,8 @@ static bool uses_wfree(const sscg_ctx *c)
 {
     if (!c->g.kn.wfree || c->blockcg) return false;
     if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2) return false;
-    for (const auto &sl : c->slabs)
-        if (!sl.has_k2r || !sl.has_k1t) return false;
+    for (const auto &sl : c->slabs)   // (CSR: the row-per-thread K1, which skips w_j too)
+        if (!sl.has_k2r || (!sl.has_k1t && c->g.kind != SSCG_OP_CSR)) return false;
     return uses_rec_update(c);   // the update must not need the stored W either
 }
 
