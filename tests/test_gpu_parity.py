@@ -176,10 +176,15 @@ def test_nccl_self_path(cfg, slabs, env, monkeypatch):
         assert tuple(out["1"][3]) == tuple(out["0"][3])
 
 
-def test_csr_operator():
+@pytest.mark.parametrize("wfree", ["1", "0"])
+def test_csr_operator(wfree, monkeypatch):
+    """The CSR operator through the C ABI against the oracle's CSR, W-free (the
+    basis step stores p only; K2R and K5 recover w_j with diag(M) per row, R21 /
+    R23; the default) and with the stored W."""
     import torch
 
     import paper_2512_09642_b200 as sscg
+    monkeypatch.setenv("SSCG_WFREE", wfree)
     nx, ny, nz, s, nu = 14, 12, 10, 6, 15
     rp, ci, va = inputs.stencil_csr("7pt", nx, ny, nz)
     A = orc.csr(rp, ci, va)
@@ -189,6 +194,7 @@ def test_csr_operator():
     dev = torch.device("cuda")
     op = sscg.CSR(torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev), torch.from_numpy(va).to(dev))
     with sscg.Solver(op, lmin, lmax, s, nu) as S:
+        assert S.query(sscg.QUERY_GRAM_VECTORS) == (s + 2 if wfree == "1" else 2 * s)   # W-free: P, w_{s-1}, diag(M)
         x = S.solve(torch.from_numpy(b).to(dev), rtol=0.0, max_outer=8).cpu().numpy()
         assert_gram(S, tr, 0)
         assert_alpha(S, tr, 0)
