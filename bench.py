@@ -560,7 +560,9 @@ def run_ours(a):
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg, "roofline": roof,
             "kernels": kern, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "impl": "ours"}
+            "clocks": clk.summary(), "impl": "ours",
+            # the s-independent rate for constant-coefficient stencils
+            "gdof_step_per_s": value * s}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
