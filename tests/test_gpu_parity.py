@@ -643,3 +643,41 @@ def test_wl_fold_matches_stored(cfg, slabs, env, monkeypatch):
     assert np.max(np.abs(a[1][0] - tr.ghat[0])) <= TOL_GRAM * np.max(np.abs(tr.ghat[0]))
     assert rel_inf(a[2][s - 1][1], tr.W[s - 1]) <= 1e-12
     assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+def _fold_combos():
+    rng = np.random.default_rng(2026)
+    out = []
+    for _ in range(36):
+        s = int(rng.choice([9, 10, 11, 12, 13, 14, 15, 16, 17, 20, 24, 31, 32]))
+        slabs = int(rng.choice([1, 1, 2, 3]))
+        env = {"SSCG_K1_MP3": str(rng.integers(0, 2)), "SSCG_K1_FUSE": str(rng.integers(0, 2)),
+               "SSCG_DEEP_HALO": str(rng.integers(0, 2))}
+        nx = int(rng.choice([24, 38, 40, 58]))     # even: the fold needs pitch == nx
+        ny, nz = int(rng.integers(9, 40)), int(rng.integers(24, 48))
+        out.append((nx, ny, nz, s, slabs, env))
+    return out
+
+
+@pytest.mark.parametrize("case", _fold_combos(), ids=lambda c: "-".join(map(str, c[:5])) + "-" + "".join(c[5].values()))
+def test_wl_fold_random_schedules(case, monkeypatch):
+    """The w_{s-1} fold over random s (9..32: one to four K2R row blocks; the
+    triples ending in a pair, a single step or nothing), slab counts, basis
+    schedules (triples / pairs / single steps) and halo schedules: fold on vs
+    off to rounding, and on against the oracle."""
+    nx, ny, nz, s, slabs, env = case
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    P = Problem("7pt", nx, ny, nz, s, 20)
+    out = {}
+    for fold in ("1", "0"):
+        monkeypatch.setenv("SSCG_WL_FOLD", fold)
+        with P.gpu_solver(slabs=slabs) as S:
+            x = S.solve(P.b_gpu(), rtol=0.0, max_outer=4).cpu().numpy()
+            out[fold] = (x, S.gram(0)[0])
+    a, b = out["1"], out["0"]
+    assert np.max(np.abs(a[1] - b[1])) <= 1e-13 * np.max(np.abs(b[1]))
+    assert np.linalg.norm(a[0] - b[0]) <= 1e-11 * np.linalg.norm(b[0])
+    x_or, tr = P.oracle(max_outer=4)
+    assert np.max(np.abs(a[1] - tr.ghat[0])) <= TOL_GRAM * np.max(np.abs(tr.ghat[0]))
+    assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
