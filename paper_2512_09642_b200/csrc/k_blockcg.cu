@@ -102,6 +102,7 @@ struct K5BParams {
     const double *alpha, *B;
     double *const *xpp;   // device cell with the caller's x (process layout)
     int64_t xoff;
+    double inv_theta, inv_2theta, sigma, dm;   // REC: W_k recovered from P_k (constant diagonal m)
 };
 
 // one phase of the update at one point: y_j = v_j - sum_m o_m B_mj for the s
@@ -137,8 +138,11 @@ __device__ __forceinline__ double bcg_phase(const double *__restrict__ v, double
 }
 
 // one point per thread (grid-stride): Q' (Z') of the point is loaded before
-// Q_k (Z_k) overwrites it
-template <int S>
+// Q_k (Z_k) overwrites it.  REC (the W-free block mode): W_k is not stored but
+// recovered per point from the P_k values the first phase loads, in K2R's
+// arithmetic (w_0 = m(p_1/theta + sigma p_0), w_j = m((p_{j+1} + p_{j-1})/(2 theta)
+// + sigma p_j), w_{s-1} from its stored row) -- the W_k the Gram pass used.
+template <int S, bool REC>
 __global__ void __launch_bounds__(256) k5_block(K5BParams k, const DevState *st)
 {
     PDL_ENTRY(st);
@@ -161,11 +165,57 @@ __global__ void __launch_bounds__(256) k5_block(K5BParams k, const DevState *st)
 #pragma unroll
         for (int i = 0; i < S; ++i) o[i] = (i < s) ? k.P[(int64_t)(s + i) * vs + e] : 0.0;
         const double p0 = k.P[e];
-        const double ax = bcg_phase<S>(k.P + e, k.P + (int64_t)s * vs + e, vs, s, o, Bsh, al);
-        // r_{k+1} = p_0 - Z_k alpha with Z_k = W_k - Z' B
+        double ax, aw;
+        if constexpr (REC) {
+            // both phases in one pass over groups of four columns: Q' and Z' of the
+            // point in registers first (their slots are overwritten), each P_k row
+            // loaded once (one row of lookahead for w_j's p_{j+1})
+            double o2[S];
 #pragma unroll
-        for (int i = 0; i < S; ++i) o[i] = (i < s) ? k.W[(int64_t)(s + i) * vs + e] : 0.0;
-        const double aw = bcg_phase<S>(k.W + e, k.W + (int64_t)s * vs + e, vs, s, o, Bsh, al);
+            for (int i = 0; i < S; ++i) o2[i] = (i < s) ? k.W[(int64_t)(s + i) * vs + e] : 0.0;
+            const double wl = k.W[(int64_t)(s - 1) * vs + e];
+            const double c1a = k.inv_theta * k.dm, c1b = k.inv_2theta * k.dm, cs = k.sigma * k.dm;
+            const double *pp = k.P + e;
+            double *qy = k.P + (int64_t)s * vs + e, *zy = k.W + (int64_t)s * vs + e;
+            double pprev = 0.0, pnext = pp[0];   // p_{j0-1}, p_{j0}
+            ax = 0.0;
+            aw = 0.0;
+#pragma unroll 1
+            for (int j0 = 0; j0 < s; j0 += 4) {
+                double pv[5];
+                pv[0] = pnext;
+#pragma unroll
+                for (int u = 1; u < 5; ++u) pv[u] = (j0 + u < s) ? pp[(int64_t)(j0 + u) * vs] : 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + u;
+                    if (j >= s) break;
+                    const double pj = pv[u], dn = (u == 0) ? pprev : pv[u - 1];
+                    // w_j as K2R forms it (w_{s-1} stored)
+                    const double wj = (j == s - 1) ? wl
+                                                   : fma(pv[u + 1], j == 0 ? c1a : c1b, fma(j > 0 ? dn : pj, j > 0 ? c1b : 0.0, cs * pj));
+                    double sq = 0.0, sz = 0.0;
+#pragma unroll
+                    for (int m = 0; m < S; ++m) {
+                        sq = fma(o[m], Bsh[m * S + j], sq);
+                        sz = fma(o2[m], Bsh[m * S + j], sz);
+                    }
+                    const double qj = pj - sq, zj = wj - sz;
+                    qy[(int64_t)j * vs] = qj;
+                    zy[(int64_t)j * vs] = zj;
+                    ax = fma(al[j], qj, ax);
+                    aw = fma(al[j], zj, aw);
+                }
+                pprev = pv[3];
+                pnext = pv[4];
+            }
+        } else {
+            ax = bcg_phase<S>(k.P + e, k.P + (int64_t)s * vs + e, vs, s, o, Bsh, al);
+            // r_{k+1} = p_0 - Z_k alpha with Z_k = W_k - Z' B
+#pragma unroll
+            for (int i = 0; i < S; ++i) o[i] = (i < s) ? k.W[(int64_t)(s + i) * vs + e] : 0.0;
+            aw = bcg_phase<S>(k.W + e, k.W + (int64_t)s * vs + e, vs, s, o, Bsh, al);
+        }
         const int64_t xi = row * k.nx + xx;
         x[xi] = x[xi] + ax;
         k.P[e] = p0 - aw;
@@ -180,7 +230,8 @@ void launch_bcg_prep(const double *big, int s, double *blk2, double *Bm, DevStat
 }
 
 void launch_k5_block(const Geo &g, const Slab &sl, int s, const double *alpha, const double *B, double *const *xpp,
-                     int64_t xoff, const DevState *st, cudaStream_t stream, int zb, int ze)
+                     int64_t xoff, const DevState *st, cudaStream_t stream, int zb, int ze, bool rec, double theta,
+                     double sigma)
 {
     if (ze < 0) ze = sl.nzl + 1;
     if (ze <= zb) return;
@@ -196,10 +247,19 @@ void launch_k5_block(const Geo &g, const Slab &sl, int s, const double *alpha, c
     k.B = B;
     k.xpp = xpp;
     k.xoff = xoff + (int64_t)(zb - 1) * g.nx * g.ny;
+    k.inv_theta = 1.0 / theta;
+    k.inv_2theta = 1.0 / (2.0 * theta);
+    k.sigma = sigma;
+    k.dm = g.center;
     const unsigned blocks = (unsigned)std::min<int64_t>((k.N + 255) / 256, (int64_t)k2_grid() * 16);
-    if (s <= 8) launch_pdl(g.kn.pdl, k5_block<8>, dim3(blocks), dim3(256), 0, stream, k, st);
-    else if (s <= 16) launch_pdl(g.kn.pdl, k5_block<16>, dim3(blocks), dim3(256), 0, stream, k, st);
-    else launch_pdl(g.kn.pdl, k5_block<32>, dim3(blocks), dim3(256), 0, stream, k, st);
+    if (rec) {
+        if (s <= 8) launch_pdl(g.kn.pdl, k5_block<8, true>, dim3(blocks), dim3(256), 0, stream, k, st);
+        else launch_pdl(g.kn.pdl, k5_block<16, true>, dim3(blocks), dim3(256), 0, stream, k, st);
+        return;
+    }
+    if (s <= 8) launch_pdl(g.kn.pdl, k5_block<8, false>, dim3(blocks), dim3(256), 0, stream, k, st);
+    else if (s <= 16) launch_pdl(g.kn.pdl, k5_block<16, false>, dim3(blocks), dim3(256), 0, stream, k, st);
+    else launch_pdl(g.kn.pdl, k5_block<32, false>, dim3(blocks), dim3(256), 0, stream, k, st);
 }
 
 }  // namespace sscg

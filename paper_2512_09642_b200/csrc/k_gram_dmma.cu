@@ -240,6 +240,7 @@ struct K2RParams {
     double inv_theta, inv_2theta, sigma, dm;
     double *part, *out;
     unsigned *ticket;
+    int sb;                  // BLK: the basis size s (the pass runs over 2s rows, k.s = 2s)
 };
 
 // PAP (the w_{s-1} fold; constant diagonal only): w_{s-1} is
@@ -250,12 +251,18 @@ struct K2RParams {
 // needs w_{s-1} except the diagonal p_{s-1}^T A p_{s-1}, left 0 here and
 // written by k_pap (one stencil pass over p_{s-1}, a reduction).  Same tile
 // count and DMMA work as the upper triangle.
-template <int NB, int EP, bool VARM, bool PAP = false>
+// BLK (the block-conjugate mode without the stored W_k, R24): the
+// pass runs over the 2s rows A = [P_k | Q'] against B = [W_k | Z']: W_k's rows
+// recovered from P_k as above (w_{s-1} from its stored row), Z' = A Q' staged
+// from the stored rows s..2s-1 of W (tmDv carries that map); one more box per
+// stage, the same tiles, reduction and output block as the stored-W pass.
+template <int NB, int EP, bool VARM, bool PAP = false, bool BLK = false>
 __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     k2r(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmWl,
         const __grid_constant__ CUtensorMap tmDv, K2RParams k, const DevState *st)
 {
     static_assert(!(PAP && VARM), "the fold needs a constant diagonal");
+    static_assert(!(BLK && (VARM || PAP)), "the block mode's W-free pass: constant diagonal, w_{s-1} stored");
     PDL_ENTRY(st);
     constexpr int SP = 8 * NB;
     constexpr int NCW = ncw_for(NB, VARM), THREADS = threads_for(NB, VARM);
@@ -270,8 +277,9 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     __shared__ uint64_t full[MAXS], empty[MAXS];
     __shared__ bool is_last;
     const int s = k.s, NS = k.nstage;
-    const int stage_elems = SP * EP + k.wlp * (VARM ? 2 : 1);
-    const uint32_t stage_bytes = (uint32_t)(SP * EP + EP * (PAP ? 0 : VARM ? 2 : 1)) * 8u;   // bytes the TMA delivers
+    constexpr int SZ = BLK ? SP / 2 : 0;   // BLK: the Z' box (rows s..2s-1 of W)
+    const int stage_elems = SP * EP + SZ * EP + k.wlp * (VARM ? 2 : 1);
+    const uint32_t stage_bytes = (uint32_t)(SP * EP + SZ * EP + EP * (PAP ? 0 : VARM ? 2 : 1)) * 8u;   // bytes the TMA delivers
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nchunks = (k.N + EP - 1) / EP;
     const int nit = (int)((nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x);
@@ -284,7 +292,7 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
         mbar_fence_init();
         tma_prefetch_desc(&tmP);
         if (!PAP) tma_prefetch_desc(&tmWl);
-        if (VARM) tma_prefetch_desc(&tmDv);
+        if (VARM || BLK) tma_prefetch_desc(&tmDv);
     }
     __syncthreads();
 
@@ -313,7 +321,12 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
                 const int x = (int)((blockIdx.x + (int64_t)it * gridDim.x) * EP);
                 mbar_expect_tx(&full[stg], stage_bytes);
                 tma_load_2d(dst, &tmP, x, 0, &full[stg]);
-                if (!PAP) tma_load_2d(dst + SP * EP, &tmWl, x, s - 1, &full[stg]);
+                if (BLK) {
+                    tma_load_2d(dst + SP * EP, &tmDv, x, 0, &full[stg]);                 // Z' rows
+                    tma_load_2d(dst + SP * EP + SZ * EP, &tmWl, x, k.sb - 1, &full[stg]);   // w_{s-1}
+                } else if (!PAP) {
+                    tma_load_2d(dst + SP * EP, &tmWl, x, s - 1, &full[stg]);
+                }
                 if (VARM) tma_load_2d(dst + SP * EP + k.wlp, &tmDv, x, 0, &full[stg]);
             }
             __syncwarp();
@@ -347,6 +360,26 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
                 upd[J] = (SP - r) * EP;   // the w_{s-1} row: SP*EP + pt = o + (SP - r)*EP
             }
             if (PAP && j == s - 1) upd[J] = 0;   // a zero row (c1 = c2 = cs = 0) read from its own, finite, values
+            if (BLK) {   // rows of [W_k | Z']: recovered below s-1, w_{s-1} and Z' staged
+                const int sb = k.sb;
+                const bool recb = j < sb - 1;
+                c1[J] = !recb ? 0.0 : (j == 0 ? k.inv_theta : k.inv_2theta) * k.dm;
+                c2[J] = (recb && j > 0) ? k.inv_2theta * k.dm : 0.0;
+                cs[J] = recb ? k.sigma * k.dm : 0.0;
+                upd[J] = J * 8 * EP + EP;
+                dnd[J] = J * 8 * EP - ((j == 0) ? 0 : EP);
+                if (j == sb - 1) {
+                    c1[J] = 1.0;
+                    upd[J] = SP * EP + SZ * EP - r * EP;   // the w_{s-1} slot
+                } else if (j >= sb && j < 2 * sb) {
+                    c1[J] = 1.0;
+                    upd[J] = SP * EP + (j - sb - r) * EP;  // Z' row j - s
+                    dnd[J] = J * 8 * EP;                   // (times c2 = 0)
+                } else if (j >= 2 * sb) {
+                    upd[J] = J * 8 * EP;                   // padding rows: zero (own, finite, values x 0)
+                    dnd[J] = J * 8 * EP;
+                }
+            }
         }
         for (int it = (grp < ngroups ? grp : nit); it < nit; it += ngroups) {
             const int stg = it % NS;
@@ -698,7 +731,11 @@ void launch_k2d(const Geo &g, const Slab &sl, int s, const DevState *st, double 
 
 namespace sscg {
 
-bool k2r_prepare(const Geo &g, Slab &sl, int s)
+// BLK: the box pitch (k-step pairs for up to 16 rows: 72 = 64 mod 128 B; single
+// k-steps above: 68 = 32 mod 128 B)
+static int ep_for_k2rb(int sp) { return sp <= 16 ? 72 : 68; }
+
+bool k2r_prepare(const Geo &g, Slab &sl, int s, int nvec)
 {
     const int s_pad = (s + 7) / 8 * 8, ep = ep_for_k2r(s_pad);
     const int64_t N = (int64_t)sl.nzl * g.plane;
@@ -714,6 +751,19 @@ bool k2r_prepare(const Geo &g, Slab &sl, int s)
     if (K2R_ATTR_F(1, K2R_EP_PAIRS) || K2R_ATTR_F(2, K2R_EP_PAIRS) || K2R_ATTR_F(3, K2R_EP_MID) || K2R_ATTR_F(4, K2R_EP_MID))
         return false;
 #undef K2R_ATTR_F
+    // the block-conjugate mode's W-free pass over [P_k | Q'] x [W_k | Z'] (2s <= 32 rows)
+    sl.has_k2rb = false;
+    if (nvec >= 2 * s && 2 * s <= 32) {
+#define K2R_ATTR_B(NB, EP) cudaFuncSetAttribute(k2r<NB, EP, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
+        if (K2R_ATTR_B(1, 72) || K2R_ATTR_B(2, 72) || K2R_ATTR_B(3, 68) || K2R_ATTR_B(4, 68)) return false;
+#undef K2R_ATTR_B
+        const int spb = (2 * s + 7) / 8 * 8, epb = ep_for_k2rb(spb);
+        if (!encode_rows_map(&sl.tmPb, sl.P + g.plane, N, 2 * s, g.vstride, epb, spb) ||
+            !encode_rows_map(&sl.tmZb, sl.W + (int64_t)s * g.vstride + g.plane, N, s, g.vstride, epb, spb / 2) ||
+            !encode_rows_map(&sl.tmWlb, sl.W + g.plane, N, s, g.vstride, epb, 1))
+            return false;
+        sl.has_k2rb = true;
+    }
     // P rows (own map: K2D's pitch differs), the single row w_{s-1} of W, and diag(M) (one row) when it varies
     if (!encode_rows_map(&sl.tmPr, sl.P + g.plane, N, s, g.vstride, ep, s_pad)) return false;
     if (!encode_rows_map(&sl.tmWl, sl.W + g.plane, N, s, g.vstride, ep, 1)) return false;
@@ -837,6 +887,46 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     default: K2R_LAUNCH(8, 68) break;
     }
 #undef K2R_LAUNCH
+}
+
+// the block-conjugate mode's Gram pass without the stored W_k (BLK, above):
+// 2s rows [P_k | Q'] x [W_k | Z'] into the (2s) x (2s + 1) block
+void launch_k2r_block(const Geo &g, const Slab &sl, int s, double theta, double sigma, const DevState *st,
+                      double *out_blk, cudaStream_t stream)
+{
+    const int sp = (2 * s + 7) / 8 * 8, nb = sp / 8, ep = ep_for_k2rb(sp);
+    K2RParams k{};
+    k.N = (int64_t)sl.nzl * g.plane;
+    k.s = 2 * s;
+    k.sb = s;
+    k.s_pad = sp;
+    k.wlp = (ep * 8 + 127) / 128 * 128 / 8;
+    const size_t stage = (size_t)(sp * ep + (sp / 2) * ep + k.wlp) * sizeof(double);
+    {
+        const int nsmax = (int)std::max<size_t>(1, std::min<size_t>(MAXS, ((size_t)g.kn.k2_smem_kb * 1024) / stage));
+        const int gr = common_divisor_le(g.kn.k2_groups ? g.kn.k2_groups : 4, ncw_for(nb), ncw_for(nb));
+        k.ngroups = std::min(gr, nsmax);
+        while (ncw_for(nb) % k.ngroups) --k.ngroups;
+        k.nstage = std::max(k.ngroups, nsmax / k.ngroups * k.ngroups);
+    }
+    k.inv_theta = 1.0 / theta;
+    k.inv_2theta = 1.0 / (2.0 * theta);
+    k.sigma = sigma;
+    k.dm = g.center;
+    k.part = sl.part;
+    k.out = out_blk;
+    k.ticket = sl.ticket;
+    const int64_t nchunks = (k.N + ep - 1) / ep;
+    const int gx = (int)std::min<int64_t>(k2_grid(), nchunks);
+    const int nt = nb * (nb + 1) / 2;
+    const size_t red = (size_t)(ncw_for(nb) * nt * 64 + ncw_for(nb) * sp) * sizeof(double);
+    const size_t sm = std::max((size_t)k.nstage * stage, red);
+    switch (nb) {
+    case 1: launch_pdl(g.kn.pdl, k2r<1, 72, false, false, true>, dim3(gx), dim3(threads_for(1)), sm, stream, sl.tmPb, sl.tmWlb, sl.tmZb, k, st); break;
+    case 2: launch_pdl(g.kn.pdl, k2r<2, 72, false, false, true>, dim3(gx), dim3(threads_for(2)), sm, stream, sl.tmPb, sl.tmWlb, sl.tmZb, k, st); break;
+    case 3: launch_pdl(g.kn.pdl, k2r<3, 68, false, false, true>, dim3(gx), dim3(threads_for(3)), sm, stream, sl.tmPb, sl.tmWlb, sl.tmZb, k, st); break;
+    default: launch_pdl(g.kn.pdl, k2r<4, 68, false, false, true>, dim3(gx), dim3(threads_for(4)), sm, stream, sl.tmPb, sl.tmWlb, sl.tmZb, k, st); break;
+    }
 }
 
 namespace {

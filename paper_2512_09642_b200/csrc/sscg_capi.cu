@@ -280,7 +280,7 @@ static sscg_status build_basis_store(sscg_ctx *c, int nvec)
             sl.has_k1f = true;
         }
         if (kind == SSCG_OP_STENCIL7 || kind == SSCG_OP_STENCIL27 || kind == SSCG_OP_VARCOEF7 || kind == SSCG_OP_CSR) {
-            if (!k2r_prepare(g, sl, s)) return fail(SSCG_ERR_CUDA, "tensor maps for the recovered-W Gram pass");
+            if (!k2r_prepare(g, sl, s, nvec)) return fail(SSCG_ERR_CUDA, "tensor maps for the recovered-W Gram pass");
             sl.has_k2r = true;
         }
     }
@@ -769,8 +769,17 @@ static bool uses_rec_update(const sscg_ctx *c)
 // and the basis is Chebyshev (SSCG_WFREE=0 keeps the stored-W schedule)
 static bool uses_wfree(const sscg_ctx *c)
 {
-    if (!c->g.kn.wfree || c->blockcg) return false;
+    if (!c->g.kn.wfree) return false;
     if (c->basis != SSCG_BASIS_CHEBYSHEV || c->s < 2) return false;
+    if (c->blockcg) {
+        // the block mode (R24): W_k recovered in the 2s-row Gram pass (K2R BLK) and in
+        // K5B; Z' = A Q' stays stored.  Constant diagonal, 2s <= 32 rows.
+        const Geo &g = c->g;
+        if (g.kind == SSCG_OP_CSR || !(g.center > 0.0) || g.pitch != g.nx) return false;
+        for (const auto &sl : c->slabs)
+            if (!sl.has_k2rb || !sl.has_k1t || sl.dvec || sl.dinv) return false;
+        return true;
+    }
     for (const auto &sl : c->slabs)   // (CSR: the row-per-thread K1, which skips w_j too)
         if (!sl.has_k2r || (!sl.has_k1t && c->g.kind != SSCG_OP_CSR)) return false;
     return uses_rec_update(c);   // the update must not need the stored W either
@@ -865,7 +874,7 @@ static sscg_status launch_basis(sscg_ctx *c, int j, int part, bool ignore_stop =
 static bool uses_wlfold(const sscg_ctx *c)
 {
     const Geo &g = c->g;
-    if (g.kn.wl_fold != 1 || g.kind != SSCG_OP_STENCIL7 || !uses_wfree(c)) return false;
+    if (g.kn.wl_fold != 1 || g.kind != SSCG_OP_STENCIL7 || c->blockcg || !uses_wfree(c)) return false;
     if (c->s > 32 || (c->s <= 8 && g.kn.k2s)) return false;   // K2R with at most 4 row blocks; K2S reads the stored w_{s-1}
     if ((g.nx & 1) || g.pitch != g.nx) return false;             // k_pap and K5 run on point pairs
     for (const auto &sl : c->slabs)
@@ -1203,7 +1212,8 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
     const int rows = c->blockcg ? 2 * s : s, nent = rows * rows + rows;
     for (auto &sl : c->slabs) {
         TRY(prof_mark(c, SSCG_PROF_GRAM, true));
-        if (wfree) launch_k2r(g, sl, s, c->theta, c->sigma, c->st, L == 1 ? c->blk : sl.blk, c->stream, fold);
+        if (wfree && c->blockcg) launch_k2r_block(g, sl, s, c->theta, c->sigma, c->st, L == 1 ? c->blk : sl.blk, c->stream);
+        else if (wfree) launch_k2r(g, sl, s, c->theta, c->sigma, c->st, L == 1 ? c->blk : sl.blk, c->stream, fold);
         else launch_k2(g, sl, rows, c->st, L == 1 ? c->blk : sl.blk, c->stream);
         ++c->launches;
         if (fold) {   // Ghat_{s-1,s-1} = p_{s-1}^T A p_{s-1}
@@ -1260,7 +1270,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
             TRY(prof_mark(c, SSCG_PROF_UPDATE, true));
             if (c->blockcg)
                 launch_k5_block(g, sl, s, c->alpha, c->bmat, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream,
-                                b, e);
+                                b, e, wfree, c->theta, c->sigma);
             else
                 launch_k5(g, sl, s, c->alpha, c->xdev, sl.zoff * (int64_t)g.nx * g.ny, c->st, c->stream, b, e,
                           c->theta, c->sigma, uses_rec_update(c), uses_k5fold(c));
@@ -1894,14 +1904,16 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
         // stored W: P and W (2s); recovered W: P, w_{s-1} and diag(M) when it varies;
         // block-conjugate: [P | Q'] and [W | Z'] (4s)
         // (fold: P, then p_{s-1} again for p_{s-1}^T A p_{s-1})
-        *out = c->blockcg ? 4 * (int64_t)s : uses_wlfold(c) ? (int64_t)s + 1 :
+        // block-conjugate, W-free: [P | Q'], Z' and w_{s-1} (3s + 1)
+        *out = c->blockcg ? (uses_wfree(c) ? 3 * (int64_t)s + 1 : 4 * (int64_t)s) : uses_wlfold(c) ? (int64_t)s + 1 :
                uses_wfree(c) ? (int64_t)s + 1 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s;
         return SSCG_OK;
     case SSCG_QUERY_UPDATE_VECTORS:
         // P (s) + x in, x + r out; the stored-W form also reads W (s), the
         // recurrence form only w_{s-1}
         // block-conjugate: P, W, Q', Z', x in; Q, Z, x, r out
-        *out = c->blockcg ? 6 * (int64_t)s + 3 : uses_k5fold(c) ? (int64_t)s + 3 :
+        // (W-free: W_k recovered, so P, Q', Z', w_{s-1}, x in; Q, Z, x, r out: 5s + 4)
+        *out = c->blockcg ? (uses_wfree(c) ? 5 * (int64_t)s + 4 : 6 * (int64_t)s + 3) : uses_k5fold(c) ? (int64_t)s + 3 :
                uses_rec_update(c) ? (int64_t)s + 4 + (c->slabs[0].dvec ? 1 : 0) : 2 * (int64_t)s + 3;
         return SSCG_OK;
     default:

@@ -90,7 +90,8 @@ struct Slab {
     bool has_k2d;
     CUtensorMap tmWl, tmDv;       // K2R: the row w_{s-1} of W, diag(M) (one row)
     CUtensorMap tmPr;             // K2R: P rows, box pitch 136/72 (16-B point-pair loads)
-    bool has_k2r;
+    CUtensorMap tmPb, tmZb, tmWlb;   // K2R block mode: [P_k | Q'] rows, Z' rows, w_{s-1}
+    bool has_k2r, has_k2rb;
     CUtensorMap tmP4, tmM4;       // K1T: 4-D [x][y][plane][vector] views of P (halo box / tile box)
     bool has_k1t;
     CUtensorMap tmF_P, tmF_M;     // K1F: 2-cell / 1-cell halo boxes
@@ -242,7 +243,10 @@ int k2_num_entries(int s);
 // K2D: the Gram pass on FP64 tensor cores (k_gram_dmma.cu), s > 16 by default
 bool k2d_enabled(const Geo &g, int s);
 // K2R: DMMA Gram pass recovering W = AP from the basis recurrence (W not stored, R23)
-bool k2r_prepare(const Geo &g, Slab &sl, int s);
+bool k2r_prepare(const Geo &g, Slab &sl, int s, int nvec = 0);
+// the block-conjugate mode's Gram pass with W_k recovered (sl.has_k2rb)
+void launch_k2r_block(const Geo &g, const Slab &sl, int s, double theta, double sigma, const DevState *st,
+                      double *out_blk, cudaStream_t stream);
 void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma, const DevState *st, double *out_blk,
                 cudaStream_t stream, bool fold = false);
 // the w_{s-1} fold: Ghat_{s-1,s-1} = p_{s-1}^T A p_{s-1} of one slab
@@ -295,7 +299,8 @@ void launch_ks(const Geo &g, const Slab &sl, int s, double theta, double sigma, 
 // block-conjugate s-step CG (k_blockcg.cu, R24)
 void launch_bcg_prep(const double *big, int s, double *blk2, double *Bm, DevState *st, bool pdl, cudaStream_t strm);
 void launch_k5_block(const Geo &g, const Slab &sl, int s, const double *alpha, const double *B, double *const *xpp,
-                     int64_t xoff, const DevState *st, cudaStream_t stream, int zb, int ze);
+                     int64_t xoff, const DevState *st, cudaStream_t stream, int zb, int ze, bool rec = false,
+                     double theta = 0.0, double sigma = 0.0);
 
 // Lanczos spectral bounds (k_lanczos.cu)
 int lz_grid();

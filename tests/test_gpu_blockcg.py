@@ -27,13 +27,21 @@ def _oracle(P, gs, max_outer, rtol=0.0):
                         block=True)
 
 
+@pytest.mark.parametrize("wfree", ["1", "0"], ids=["wfree", "storedW"])
 @pytest.mark.parametrize("case", CASES, ids=_ids)
-def test_block_ten_outer(case):
+def test_block_ten_outer(case, wfree, monkeypatch):
+    """With W_k recovered (the default for constant diagonals: the 2s-row Gram
+    pass K2R BLK and K5B recover W_k from P_k, Z' stays stored) and with the
+    stored W."""
     import paper_2512_09642_b200 as sscg
+    monkeypatch.setenv("SSCG_WFREE", wfree)
     kind, nx, ny, nz, s, nu, gs = case
     P = Problem(kind, nx, ny, nz, s, nu, lanczos=(kind in ("27pt", "varcoef7")))
     x_or, tr = _oracle(P, gs, 10)
     with P.gpu_solver(gram_solver=gs, block=True) as S:
+        w_free = wfree == "1" and kind in ("7pt", "27pt") and s <= 16 and nx % 2 == 0   # (K1T stencils)
+        assert S.query(sscg.QUERY_GRAM_VECTORS) == (3 * s + 1 if w_free else 4 * s)
+        assert S.query(sscg.QUERY_UPDATE_VECTORS) == (5 * s + 4 if w_free else 6 * s + 3)
         x = S.solve(P.b_gpu(), rtol=0.0, max_outer=10).cpu().numpy()
         st = S.stats()
         assert st.outer_iterations == 10
