@@ -249,8 +249,9 @@ struct K2RParams {
 //   Ghat_{ij} = p_i^T A p_j = (A p_i)^T p_j = w_i^T p_j,  i <= j,
 // from tile (J, I) -- p_j against the recovered w_i, i < j --, so no entry
 // needs w_{s-1} except the diagonal p_{s-1}^T A p_{s-1}, left 0 here and
-// written by k_pap (one stencil pass over p_{s-1}, a reduction).  Same tile
-// count and DMMA work as the upper triangle.
+// written afterwards by one stencil pass over p_{s-1} with a reduction (the
+// TMA single step K1T in its dot mode; k_pap without TMA).  Same tile count
+// and DMMA work as the upper triangle.
 // BLK (the block-conjugate mode without the stored W_k, R24): the
 // pass runs over the 2s rows A = [P_k | Q'] against B = [W_k | Z']: W_k's rows
 // recovered from P_k as above (w_{s-1} from its stored row), Z' = A Q' staged
