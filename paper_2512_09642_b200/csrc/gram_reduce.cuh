@@ -32,8 +32,24 @@ __device__ __forceinline__ void last_cta_sum(const double *part, int nparts, int
             q = s * s + i;
         }
         double v = 0.0;
-        if (act)
-            for (int b = m; b < nparts; b += 8) v += __ldcg(part + (int64_t)b * nent + q);
+        if (act) {
+            // all of a lane's partials loaded before the first add (registers, up to
+            // 8 x LCS_R partials): one L2 round trip instead of one per partial; the
+            // adds keep the loop's order (b ascending; absent ones add +0.0)
+            constexpr int LCS_R = 24;
+            if (nparts <= 8 * LCS_R) {
+                double t[LCS_R];
+#pragma unroll
+                for (int i = 0; i < LCS_R; ++i) {
+                    const int b = m + 8 * i;
+                    t[i] = (b < nparts) ? __ldcg(part + (int64_t)b * nent + q) : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < LCS_R; ++i) v += t[i];
+            } else {
+                for (int b = m; b < nparts; b += 8) v += __ldcg(part + (int64_t)b * nent + q);
+            }
+        }
         v += __shfl_xor_sync(0xffffffffu, v, 4);
         v += __shfl_xor_sync(0xffffffffu, v, 2);
         v += __shfl_xor_sync(0xffffffffu, v, 1);
