@@ -291,9 +291,13 @@ SSCG_API sscg_status sscg_estimate_bounds(sscg_ctx *ctx, const double *v0, int32
  *                         Q_k^T r_k with the selected Gram solver (pair it
  *                         with SSCG_GRAM_CHOLESKY: inexact FGS solves break
  *                         the conjugacy), and the update is x += Q_k alpha,
- *                         r -= A Q_k alpha.  Needs s <= 32; uses the stored-W
- *                         schedule and twice the basis storage (reallocated
- *                         here; the next solve starts a new block sequence).
+ *                         r -= A Q_k alpha.  Needs s <= 32; twice the basis
+ *                         storage (reallocated here; the next solve starts a
+ *                         new block sequence); W_k = A P_k is recovered from
+ *                         the basis recurrence (not stored) for the 7- and
+ *                         27-point stencils with a constant diagonal and
+ *                         s <= 16, A Q_{k-1} is kept (stored-W schedule
+ *                         otherwise).
  *                         SSCG_INSPECT_GRAM then returns [G_k | c_k] of the
  *                         conjugated system.
  * Errors: SSCG_ERR_INVALID for an unknown key or value. */
