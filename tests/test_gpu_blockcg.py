@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 
 CASES = [("7pt", 40, 36, 33, 8, 20, "cholesky"), ("7pt", 40, 36, 33, 16, 25, "cholesky"),
          ("7pt", 33, 17, 19, 5, 10, "fgs"), ("27pt", 24, 22, 20, 8, 30, "cholesky"),
-         ("varcoef7", 24, 22, 20, 8, 20, "cholesky"), ("5pt", 64, 64, 1, 8, 20, "cholesky")]
+         ("varcoef7", 24, 22, 20, 8, 20, "cholesky"), ("5pt", 64, 64, 1, 8, 20, "cholesky"),
+         ("7pt", 26, 18, 21, 12, 20, "cholesky")]   # W-free with three 8-row blocks (2s = 24)
 
 
 def _ids(c):
