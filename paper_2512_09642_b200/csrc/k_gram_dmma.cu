@@ -252,17 +252,27 @@ struct K2RParams {
 // written afterwards by one stencil pass over p_{s-1} with a reduction (the
 // TMA single step K1T in its dot mode; k_pap without TMA).  Same tile count
 // and DMMA work as the upper triangle.
+// GS (with PAP; R27): no w_j is formed at all.  The tiles hold the
+// Euclidean Gram E = P^T P (lower block triangle, B fragment = A fragment),
+// and each CTA maps its partial E to its partial Ghat by the same recurrence
+// written in Gram space (A P_{:,0:s-1} = P_{:,0:s} T, T tridiagonal):
+//   Ghat_{ji} = p_i^T w_j = m ((E_{i,j+1} + E_{i,j-1})/(2 theta) + sigma E_{ij}),
+//   (j = 0: m (E_{i,1}/theta + sigma E_{i0})),  j <= i, (j, i) != (s-1, s-1),
+// every E entry it reads in the lower triangle (j + 1 <= i, or E_{i,i+1} =
+// E_{i+1,i}); c = P^T p_0 is E's column 0.  No recovery FMAs, no neighbour-row
+// loads, no c FMAs: the DMMA tiles are the whole per-point work.
 // BLK (the block-conjugate mode without the stored W_k, R24): the
 // pass runs over the 2s rows A = [P_k | Q'] against B = [W_k | Z']: W_k's rows
 // recovered from P_k as above (w_{s-1} from its stored row), Z' = A Q' staged
 // from the stored rows s..2s-1 of W (tmDv carries that map); one more box per
 // stage, the same tiles, reduction and output block as the stored-W pass.
-template <int NB, int EP, bool VARM, bool PAP = false, bool BLK = false>
+template <int NB, int EP, bool VARM, bool PAP = false, bool BLK = false, bool GS = false>
 __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     k2r(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmWl,
         const __grid_constant__ CUtensorMap tmDv, K2RParams k, const DevState *st)
 {
     static_assert(!(PAP && VARM), "the fold needs a constant diagonal");
+    static_assert(!GS || PAP, "the Gram-space map is the fold's");
     static_assert(!(BLK && (VARM || PAP)), "the block mode's W-free pass: constant diagonal, w_{s-1} stored");
     PDL_ENTRY(st);
     constexpr int SP = 8 * NB;
@@ -402,6 +412,18 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
                 double2 a[NB], b[NB];
 #pragma unroll
                 for (int i = 0; i < NB; ++i) a[i] = lds2(sP + o + i * 8 * EP);
+                constexpr int SX = 0, SY = (U > 1) ? 1 : 0;
+                if constexpr (GS) {   // E = P^T P: tile (i, J <= i) from the A fragments alone
+                    int t = 0;
+#pragma unroll
+                    for (int i = 0; i < NB; ++i)
+#pragma unroll
+                        for (int J = 0; J <= i; ++J, ++t) {
+                            dmma(acc[(2 * u + SX) % U][t][0], acc[(2 * u + SX) % U][t][1], a[i].x, a[J].x);
+                            dmma(acc[(2 * u + SY) % U][t][0], acc[(2 * u + SY) % U][t][1], a[i].y, a[J].y);
+                        }
+                    continue;
+                }
                 const double2 p0 = lds2(sP + pt);
 #pragma unroll
                 for (int J = 0; J < NB; ++J) {
@@ -420,7 +442,6 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
                 }
 #pragma unroll
                 for (int i = 0; i < NB; ++i) cac[i] = fma(a[i].y, p0.y, fma(a[i].x, p0.x, cac[i]));
-                constexpr int SX = 0, SY = (U > 1) ? 1 : 0;
                 int t = 0;
 #pragma unroll
                 for (int i = 0; i < NB; ++i)
@@ -442,6 +463,14 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
                 double a[NB], b[NB];
 #pragma unroll
                 for (int i = 0; i < NB; ++i) a[i] = sP[o + i * 8 * EP];
+                if constexpr (GS) {
+                    int t = 0;
+#pragma unroll
+                    for (int i = 0; i < NB; ++i)
+#pragma unroll
+                        for (int J = 0; J <= i; ++J, ++t) dmma(acc[u][t][0], acc[u][t][1], a[i], a[J]);
+                    continue;
+                }
                 const double p0 = sP[pt];
 #pragma unroll
                 for (int J = 0; J < NB; ++J) {
@@ -490,7 +519,7 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
             red[((cw * NTT + t) * 32 + lane) * 2 + 0] = acc[0][t][0];
             red[((cw * NTT + t) * 32 + lane) * 2 + 1] = acc[0][t][1];
         }
-        if ((lane & 3) == 0)
+        if (!GS && (lane & 3) == 0)
 #pragma unroll
             for (int i = 0; i < NB; ++i) red[NCW * NTT * 64 + cw * SP + i * 8 + (lane >> 2)] = cac[i];
     }
@@ -498,7 +527,39 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     const int nent = s * s + s;
     double *mypart = k.part + (int64_t)blockIdx.x * nent;
     constexpr int NTT = NT;
-    for (int q = tid; q < NTT * 64; q += THREADS) {
+    if constexpr (GS) {
+        // this CTA's E (lower triangle, row-major s x s after the reduction area),
+        // then its partial Ghat and c by the Gram-space recurrence
+        double *E = red + NCW * NTT * 64;
+        for (int q = tid; q < NTT * 64; q += THREADS) {
+            const int t = q >> 6, e = q & 63, ln = e >> 1, h = e & 1;
+            double v = 0.0;
+            for (int w = 0; w < NCW; ++w) v += red[((w * NTT + t) * 32 + ln) * 2 + h];
+            int I = 0, J = 0, tt = t;
+            for (int aa = 0; aa < NB; ++aa) {
+                if (tt <= aa) { I = aa; J = tt; break; }
+                tt -= aa + 1;
+            }
+            const int i = I * 8 + (ln >> 2), j = J * 8 + 2 * (ln & 3) + h;
+            if (i < s && j <= i) E[i * s + j] = v;
+        }
+        __syncthreads();
+        const double m2 = k.dm * k.inv_2theta, m1 = k.dm * k.inv_theta, ms = k.dm * k.sigma;
+        for (int q = tid; q < s * s; q += THREADS) {
+            const int j = q / s, i = q - j * s;   // entry (j, i), j <= i: p_i^T w_j
+            if (j > i) continue;
+            double v;
+            if (j == s - 1) v = 0.0;                                                   // p_{s-1}^T A p_{s-1}: the dot-mode single step
+            else if (j == 0) v = fma(i >= 1 ? E[i * s + 1] : E[s], m1, ms * E[i * s]);      // E_{i,1} (= E_{1,0} at i = 0)
+            else {
+                const double up = (j + 1 <= i) ? E[i * s + j + 1] : E[(j + 1) * s + i];   // E_{i,j+1}
+                v = fma(up + E[i * s + j - 1], m2, ms * E[i * s + j]);
+            }
+            mypart[q] = v;
+        }
+        for (int i = tid; i < s; i += THREADS) mypart[s * s + i] = E[i * s];   // c_i = p_i^T p_0
+    }
+    for (int q = tid; q < (GS ? 0 : NTT * 64); q += THREADS) {
         const int t = q >> 6, e = q & 63, ln = e >> 1, h = e & 1;
         double v = 0.0;
         for (int w = 0; w < NCW; ++w) v += red[((w * NTT + t) * 32 + ln) * 2 + h];
@@ -522,7 +583,7 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
             mypart[j * s + i] = (i == s - 1 && j == s - 1) ? 0.0 : v;   // the diagonal p_{s-1}^T A p_{s-1}: k_pap
         }
     }
-    for (int i = tid; i < s; i += THREADS) {
+    for (int i = tid; i < (GS ? 0 : s); i += THREADS) {
         double v = 0.0;
         for (int w = 0; w < NCW; ++w) v += red[NCW * NTT * 64 + w * SP + i];
         mypart[s * s + i] = v;
@@ -748,7 +809,8 @@ bool k2r_prepare(const Geo &g, Slab &sl, int s, int nvec)
         K2R_ATTR(5, 68, true) || K2R_ATTR(6, 68, true) || K2R_ATTR(7, 68, true) || K2R_ATTR(8, 68, true))
         return false;
 #undef K2R_ATTR
-#define K2R_ATTR_F(NB, EP) cudaFuncSetAttribute(k2r<NB, EP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
+#define K2R_ATTR_F(NB, EP) (cudaFuncSetAttribute(k2r<NB, EP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess || \
+                            cudaFuncSetAttribute(k2r<NB, EP, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess)
     if (K2R_ATTR_F(1, K2R_EP_PAIRS) || K2R_ATTR_F(2, K2R_EP_PAIRS) || K2R_ATTR_F(3, K2R_EP_MID) || K2R_ATTR_F(4, K2R_EP_MID))
         return false;
 #undef K2R_ATTR_F
@@ -859,12 +921,13 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     const int64_t nchunks = (k.N + ep - 1) / ep;
     const int gx = (int)std::min<int64_t>(k2_grid(), nchunks);
     const int nt = nb * (nb + 1) / 2;
-    const size_t red = (size_t)(ncw_for(nb, varm) * nt * 64 + ncw_for(nb, varm) * s_pad) * sizeof(double);
+    const size_t red = (size_t)(ncw_for(nb, varm) * nt * 64 + std::max(ncw_for(nb, varm) * s_pad, s * s)) * sizeof(double);
     const size_t sm = std::max((size_t)k.nstage * stage, red);
     const CUtensorMap &dv = varm ? sl.tmDv : sl.tmWl;
     if (fold) {
 #define K2R_LAUNCH_F(NB, EP)                                                                                 \
-        launch_pdl(g.kn.pdl, k2r<NB, EP, false, true>, dim3(gx), dim3(threads_for(NB, false)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st);
+        if (g.kn.gram_space) launch_pdl(g.kn.pdl, k2r<NB, EP, false, true, false, true>, dim3(gx), dim3(threads_for(NB, false)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st); \
+        else launch_pdl(g.kn.pdl, k2r<NB, EP, false, true>, dim3(gx), dim3(threads_for(NB, false)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st);
         switch (nb) {
         case 1: K2R_LAUNCH_F(1, K2R_EP_PAIRS) break;
         case 2: K2R_LAUNCH_F(2, K2R_EP_PAIRS) break;

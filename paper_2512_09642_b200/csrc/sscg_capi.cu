@@ -344,6 +344,7 @@ Knobs sscg::read_knobs()
     k.debug = getenv("SSCG_DEBUG") != nullptr;
     k.pdl = tri("SSCG_PDL", 1) != 0;
     k.wl_fold = std::min(2, std::max(0, num("SSCG_WL_FOLD", 1)));
+    k.gram_space = tri("SSCG_GRAM_SPACE", 1) != 0;
     return k;
 }
 

@@ -681,3 +681,37 @@ def test_wl_fold_random_schedules(case, monkeypatch):
     x_or, tr = P.oracle(max_outer=4)
     assert np.max(np.abs(a[1] - tr.ghat[0])) <= TOL_GRAM * np.max(np.abs(tr.ghat[0]))
     assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)
+
+
+@pytest.mark.parametrize("cfg,slabs,env", [
+    (("7pt", 40, 36, 33, 16, 25), 1, {}),
+    (("7pt", 64, 40, 30, 9, 20), 1, {}),
+    (("7pt", 30, 28, 26, 24, 20), 1, {}),
+    (("7pt", 34, 30, 28, 32, 20), 2, {}),
+    (("7pt", 26, 24, 22, 5, 20), 1, {"SSCG_K2S": "0"}),
+    (("7pt", 40, 36, 33, 16, 25), 3, {"SSCG_K1_TMA": "0"}),
+], ids=lambda v: _ids(v) if isinstance(v, tuple) else (str(v) if not isinstance(v, dict) else "-".join(v) or "default"))
+def test_gram_space_matches_point_space(cfg, slabs, env, monkeypatch):
+    """The folded Gram pass in Gram space (R27, the default: E = P^T P
+    on the tensor cores, Ghat = E T per CTA) against the same pass with w_j
+    recovered per point (SSCG_GRAM_SPACE=0): Gram blocks to rounding, x after
+    five outer iterations to rounding, and both against the oracle."""
+    kind, nx, ny, nz, s, nu = cfg
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    P = Problem(kind, nx, ny, nz, s, nu)
+    out = {}
+    for gs in ("1", "0"):
+        monkeypatch.setenv("SSCG_GRAM_SPACE", gs)
+        with P.gpu_solver(slabs=slabs) as S:
+            x = S.solve(P.b_gpu(), rtol=0.0, max_outer=5).cpu().numpy()
+            out[gs] = (x, [S.gram(k) for k in range(5)])
+    a, b = out["1"], out["0"]
+    for k in range(5):   # rounding at k = 0, rounding-level drift after the first update
+        (Ga, ca), (Gb, cb) = a[1][k], b[1][k]
+        assert np.max(np.abs(Ga - Gb)) <= (1e-12 if k == 0 else TOL_GRAM) * np.max(np.abs(Gb)), k
+        assert np.max(np.abs(ca - cb)) <= (1e-13 if k == 0 else TOL_GRAM) * np.max(np.abs(cb)), k
+    assert np.linalg.norm(a[0] - b[0]) <= 1e-11 * np.linalg.norm(b[0])
+    x_or, tr = P.oracle(max_outer=5, dump_iter=0)
+    assert np.max(np.abs(a[1][0][0] - tr.ghat[0])) <= TOL_GRAM * np.max(np.abs(tr.ghat[0]))
+    assert np.linalg.norm(a[0] - x_or) <= TOL_X10 * np.linalg.norm(x_or)

@@ -202,3 +202,33 @@ def test_w_recovered_from_recurrence(kind, n, s, nu, it):
     Gr, _ = orc.gram(P, Wr)
     assert np.max(np.abs(Gr - G)) <= 1e-14 * np.max(np.abs(G))
     assert np.max(np.abs(np.diag(Gr) - np.diag(G)) / np.diag(G)) <= 1e-13
+
+
+@pytest.mark.parametrize("s", [2, 9, 16, 24])
+def test_gram_space_recurrence_identity(s):
+    """The identity the folded Gram pass's Gram-space map rests on (DESIGN.md
+    R27): with a constant diagonal M = m I, PAPER.md:36-42 solved for A p_j
+    gives A P_{:,0:s} = P_{:,0:s+1} T (T (s+1) x s, m sigma on the diagonal,
+    m/theta at (1, 0), m/(2 theta) at (j +- 1, j) otherwise), so Ghat = P^T A P
+    = E T with E = P^T P_{:,0:s+1}: checked against the oracle's own Gram of
+    its stored W = A P on the s + 1 vectors of its basis."""
+    A = orc.stencil(orc.KIND_7PT, 14, 12, 11)
+    D = orc.diag(A)
+    lo, hi = inputs.analytic_bounds("7pt", 14, 12, 11)
+    r = inputs.rhs_uniform(14, 12, 11, seed=4)
+    P1, W1 = orc.chebyshev_basis(A, D, lo, hi, s + 1, r)
+    Ghat, c = orc.gram(P1[:s], W1[:s])
+    theta, sigma, m = 2 / (hi - lo), (hi + lo) / 2, D[0]
+    T = np.zeros((s + 1, s))
+    for j in range(s):
+        T[j, j] = m * sigma
+        T[j + 1, j] = m / theta if j == 0 else m / (2 * theta)
+        if j > 0:
+            T[j - 1, j] = m / (2 * theta)
+    E = P1[:s] @ P1.T                       # (s, s+1)
+    scale = np.max(np.abs(Ghat))
+    assert np.max(np.abs(E @ T - Ghat)) <= 1e-12 * scale
+    assert np.max(np.abs(E[:, 0] - c)) <= 1e-13 * np.max(np.abs(c))
+    # a wrong coefficient (1/theta at every j, say) is far outside that
+    T[2, 1] *= 2
+    assert np.max(np.abs(E @ T - Ghat)) > 1e-3 * scale
