@@ -266,13 +266,22 @@ struct K2RParams {
 // recovered from P_k as above (w_{s-1} from its stored row), Z' = A Q' staged
 // from the stored rows s..2s-1 of W (tmDv carries that map); one more box per
 // stage, the same tiles, reduction and output block as the stored-W pass.
-template <int NB, int EP, bool VARM, bool PAP = false, bool BLK = false, bool GS = false>
+// IL (with PAP, NB = 2, s even; DESIGN.md §6 K2R): interleaved fragment rows.
+// Fragment row r of block J is basis row 2r + J (not 8J + r), so a lane holds
+// p_{2r} and p_{2r+1}: w_{2r} takes its p_{2r+1} and w_{2r+1} its p_{2r} from
+// the lane's own A fragments, and only p_{2r-1} and p_{2r+2} are loaded -- two
+// shared loads per k-step pair fewer (five instead of seven).  The three
+// tiles are then even x even, odd x even and odd x odd rows: every unordered
+// pair once (the odd x even tile holds both orientations of the mixed pairs,
+// p_i^T w_j = p_j^T w_i, R26), and w_{s-1} (s-1 odd) is never a B column there.
+template <int NB, int EP, bool VARM, bool PAP = false, bool BLK = false, bool GS = false, bool IL = false>
 __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
     k2r(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmWl,
         const __grid_constant__ CUtensorMap tmDv, K2RParams k, const DevState *st)
 {
     static_assert(!(PAP && VARM), "the fold needs a constant diagonal");
     static_assert(!GS || PAP, "the Gram-space map is the fold's");
+    static_assert(!IL || (PAP && NB == 2 && !GS), "interleaved rows: the fold's two-block pass");
     static_assert(!(BLK && (VARM || PAP)), "the block mode's W-free pass: constant diagonal, w_{s-1} stored");
     PDL_ENTRY(st);
     constexpr int SP = 8 * NB;
@@ -355,9 +364,13 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
         // 0 itself with c2 = 0.  Both are per-lane smem offsets, no selects.
         double c1[NB], c2[NB], cs[NB], use_wl[NB];
         int upd[NB], dnd[NB];
+        // IL: lane rows 2r, 2r+1 at offsets (r + J) EP from o = r EP + pt; the
+        // loaded neighbours p_{2r-1} (row 0: its own row, c2 = 0) and p_{2r+2}
+        // (rows >= s-1 are zero rows: their own row)
+        const int ilo0 = (r > 0 ? 2 * r - 1 : 0) * EP, ilo1 = ((2 * r + 1 < s - 1) ? 2 * r + 2 : 2 * r + 1) * EP;
 #pragma unroll
         for (int J = 0; J < NB; ++J) {
-            const int j = J * 8 + r;
+            const int j = IL ? 2 * r + J : J * 8 + r;
             const bool rec = j < s - 1;
             const double mf = VARM ? 1.0 : k.dm;
             c1[J] = !rec ? 0.0 : (j == 0 ? k.inv_theta : k.inv_2theta) * mf;
@@ -411,8 +424,27 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
                 const int o = r * EP + pt;
                 double2 a[NB], b[NB];
 #pragma unroll
-                for (int i = 0; i < NB; ++i) a[i] = lds2(sP + o + i * 8 * EP);
+                for (int i = 0; i < NB; ++i) a[i] = lds2(sP + o + (IL ? (r + i) * EP : i * 8 * EP));   // IL: row 2r + i
                 constexpr int SX = 0, SY = (U > 1) ? 1 : 0;
+                if constexpr (IL) {
+                    const double2 p0 = lds2(sP + pt);
+                    const double2 dn0 = lds2(sP + pt + ilo0), up1 = lds2(sP + pt + ilo1);
+                    b[0].x = fma(a[1].x, c1[0], fma(dn0.x, c2[0], cs[0] * a[0].x));
+                    b[0].y = fma(a[1].y, c1[0], fma(dn0.y, c2[0], cs[0] * a[0].y));
+                    b[1].x = fma(up1.x, c1[1], fma(a[0].x, c2[1], cs[1] * a[1].x));
+                    b[1].y = fma(up1.y, c1[1], fma(a[0].y, c2[1], cs[1] * a[1].y));
+#pragma unroll
+                    for (int i = 0; i < NB; ++i) cac[i] = fma(a[i].y, p0.y, fma(a[i].x, p0.x, cac[i]));
+                    int t = 0;
+#pragma unroll
+                    for (int i = 0; i < NB; ++i)
+#pragma unroll
+                        for (int J = 0; J <= i; ++J, ++t) {
+                            dmma(acc[(2 * u + SX) % U][t][0], acc[(2 * u + SX) % U][t][1], a[i].x, b[J].x);
+                            dmma(acc[(2 * u + SY) % U][t][0], acc[(2 * u + SY) % U][t][1], a[i].y, b[J].y);
+                        }
+                    continue;
+                }
                 if constexpr (GS) {   // E = P^T P: tile (i, J <= i) from the A fragments alone
                     int t = 0;
 #pragma unroll
@@ -521,7 +553,7 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
         }
         if (!GS && (lane & 3) == 0)
 #pragma unroll
-            for (int i = 0; i < NB; ++i) red[NCW * NTT * 64 + cw * SP + i * 8 + (lane >> 2)] = cac[i];
+            for (int i = 0; i < NB; ++i) red[NCW * NTT * 64 + cw * SP + (IL ? 2 * (lane >> 2) + i : i * 8 + (lane >> 2))] = cac[i];
     }
     __syncthreads();
     const int nent = s * s + s;
@@ -574,6 +606,13 @@ __global__ void __launch_bounds__(threads_for(NB, VARM), 1)
                 if (tt <= aa) { I = aa; J = tt; break; }
                 tt -= aa + 1;
             }
+        }
+        if (IL) {   // rows 2r + I, columns 2c + J: even x even, odd x even, odd x odd
+            const int i = 2 * (ln >> 2) + I, j = 2 * (2 * (ln & 3) + h) + J;
+            if (i >= s || j >= s) continue;
+            if (j <= i) mypart[j * s + i] = (i == s - 1 && j == s - 1) ? 0.0 : v;   // v = p_i^T w_j = Ghat_{j,i}
+            else if (I != J) mypart[i * s + j] = v;                                  // mixed pair, j > i: Ghat_{i,j}
+            continue;
         }
         const int i = I * 8 + (ln >> 2), j = J * 8 + 2 * (ln & 3) + h;
         if (i >= s || j >= s) continue;
@@ -810,7 +849,8 @@ bool k2r_prepare(const Geo &g, Slab &sl, int s, int nvec)
         return false;
 #undef K2R_ATTR
 #define K2R_ATTR_F(NB, EP) (cudaFuncSetAttribute(k2r<NB, EP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess || \
-                            cudaFuncSetAttribute(k2r<NB, EP, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess)
+                            cudaFuncSetAttribute(k2r<NB, EP, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess || \
+                            cudaFuncSetAttribute(k2r<2, K2R_EP_PAIRS, false, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess)
     if (K2R_ATTR_F(1, K2R_EP_PAIRS) || K2R_ATTR_F(2, K2R_EP_PAIRS) || K2R_ATTR_F(3, K2R_EP_MID) || K2R_ATTR_F(4, K2R_EP_MID))
         return false;
 #undef K2R_ATTR_F
@@ -927,6 +967,7 @@ void launch_k2r(const Geo &g, const Slab &sl, int s, double theta, double sigma,
     if (fold) {
 #define K2R_LAUNCH_F(NB, EP)                                                                                 \
         if (g.kn.gram_space) launch_pdl(g.kn.pdl, k2r<NB, EP, false, true, false, true>, dim3(gx), dim3(threads_for(NB, false)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st); \
+        else if (NB == 2 && g.kn.k2_il && s % 2 == 0) launch_pdl(g.kn.pdl, k2r<2, EP, false, true, false, false, true>, dim3(gx), dim3(threads_for(2, false)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st); \
         else launch_pdl(g.kn.pdl, k2r<NB, EP, false, true>, dim3(gx), dim3(threads_for(NB, false)), sm, stream, sl.tmPr, sl.tmWl, dv, k, st);
         switch (nb) {
         case 1: K2R_LAUNCH_F(1, K2R_EP_PAIRS) break;

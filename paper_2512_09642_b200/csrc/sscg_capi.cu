@@ -344,7 +344,8 @@ Knobs sscg::read_knobs()
     k.debug = getenv("SSCG_DEBUG") != nullptr;
     k.pdl = tri("SSCG_PDL", 1) != 0;
     k.wl_fold = std::min(2, std::max(0, num("SSCG_WL_FOLD", 1)));
-    k.gram_space = tri("SSCG_GRAM_SPACE", 1) != 0;
+    k.gram_space = tri("SSCG_GRAM_SPACE", 0) == 1;
+    k.k2_il = tri("SSCG_K2_IL", 1) != 0;
     return k;
 }
 

@@ -127,7 +127,8 @@ struct Knobs {
     int debug = 0;         // SSCG_DEBUG
     int pdl = 1;           // SSCG_PDL          0: plain stream-ordered launches (no programmatic dependent launch)
     int wl_fold = 1;       // SSCG_WL_FOLD      1: w_{s-1} never stored (K2R lower triangle + k_pap + K5 stencil); 2: only K5 forms it; 0: off
-    int gram_space = 1;    // SSCG_GRAM_SPACE   1: the folded K2R forms E = P^T P and maps it to Ghat by the recurrence (R27); 0: w_j per point
+    int gram_space = 0;    // SSCG_GRAM_SPACE   1: the folded K2R forms E = P^T P and maps it to Ghat by the recurrence (R27: loses ~log10 kappa digits; opt-in)
+    int k2_il = 1;         // SSCG_K2_IL        0: the folded two-block K2R with blocked (8J + r) instead of interleaved (2r + J) fragment rows
 };
 Knobs read_knobs();
 

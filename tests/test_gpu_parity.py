@@ -690,19 +690,26 @@ def test_wl_fold_random_schedules(case, monkeypatch):
     (("7pt", 34, 30, 28, 32, 20), 2, {}),
     (("7pt", 26, 24, 22, 5, 20), 1, {"SSCG_K2S": "0"}),
     (("7pt", 40, 36, 33, 16, 25), 3, {"SSCG_K1_TMA": "0"}),
+    (("7pt", 44, 30, 28, 10, 20), 1, {}),
+    (("7pt", 38, 30, 28, 12, 20), 2, {}),
+    (("7pt", 36, 30, 31, 14, 20), 1, {"SSCG_K1_MP3": "0"}),
 ], ids=lambda v: _ids(v) if isinstance(v, tuple) else (str(v) if not isinstance(v, dict) else "-".join(v) or "default"))
-def test_gram_space_matches_point_space(cfg, slabs, env, monkeypatch):
-    """The folded Gram pass in Gram space (R27, the default: E = P^T P
-    on the tensor cores, Ghat = E T per CTA) against the same pass with w_j
-    recovered per point (SSCG_GRAM_SPACE=0): Gram blocks to rounding, x after
-    five outer iterations to rounding, and both against the oracle."""
+@pytest.mark.parametrize("knob", ["SSCG_GRAM_SPACE", "SSCG_K2_IL"])
+def test_folded_gram_variants(cfg, slabs, env, knob, monkeypatch):
+    """Two variants of the folded Gram pass against the plain one: (a) in Gram
+    space (R27, opt-in: E = P^T P on the tensor cores, Ghat = E T per
+    CTA) against w_j recovered per point; (b) interleaved fragment rows (the
+    default for s even, <= 16: a lane holds p_{2r}, p_{2r+1}) against blocked
+    ones.  Gram blocks to rounding, x after five outer iterations to rounding,
+    and the variant against the oracle.  (The model sizes here have small
+    kappa; R27's loss of ~log10 kappa digits shows at large grids.)"""
     kind, nx, ny, nz, s, nu = cfg
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     P = Problem(kind, nx, ny, nz, s, nu)
     out = {}
     for gs in ("1", "0"):
-        monkeypatch.setenv("SSCG_GRAM_SPACE", gs)
+        monkeypatch.setenv(knob, gs)
         with P.gpu_solver(slabs=slabs) as S:
             x = S.solve(P.b_gpu(), rtol=0.0, max_outer=5).cpu().numpy()
             out[gs] = (x, [S.gram(k) for k in range(5)])
