@@ -297,7 +297,9 @@ SSCG_API sscg_status sscg_estimate_bounds(sscg_ctx *ctx, const double *v0, int32
  *                         the basis recurrence (not stored) for the 7- and
  *                         27-point stencils with a constant diagonal and
  *                         s <= 16, A Q_{k-1} is kept (stored-W schedule
- *                         otherwise).
+ *                         otherwise).  With nranks > 1 every rank sets it
+ *                         (the reallocation re-maps the neighbours' basis
+ *                         for the peer-store halos: NCCL calls with them).
  *                         SSCG_INSPECT_GRAM then returns [G_k | c_k] of the
  *                         conjugated system.
  * Errors: SSCG_ERR_INVALID for an unknown key or value. */
@@ -326,9 +328,17 @@ SSCG_API sscg_status sscg_set_option(sscg_ctx *ctx, int32_t key, int32_t value);
  *                             4s in the block-conjugate mode
  *   SSCG_QUERY_BASIS_SINGLE_VECTORS  the part of BASIS_VECTORS moved by the
  *                             single steps of a fused schedule (0 without)
+ *   SSCG_QUERY_PEER_HALO      how the deep-halo triples reach their neighbours'
+ *                             ghost planes: 0 exchange (NCCL
+ *                             send/recv or device copies after each triple),
+ *                             1 peer stores into in-process slabs, 2 peer
+ *                             stores into basis vectors mapped at setup (other
+ *                             ranks' through CUDA IPC; SSCG_NCCL_SELF: the
+ *                             in-process slabs after the same NCCL round trip),
+ *                             ordered by a one-double token per triple
  * Errors: SSCG_ERR_INVALID. */
 enum { SSCG_QUERY_BASIS_FUSED = 0, SSCG_QUERY_BASIS_VECTORS = 1, SSCG_QUERY_UPDATE_VECTORS = 2,
-       SSCG_QUERY_GRAM_VECTORS = 3, SSCG_QUERY_BASIS_SINGLE_VECTORS = 4 };
+       SSCG_QUERY_GRAM_VECTORS = 3, SSCG_QUERY_BASIS_SINGLE_VECTORS = 4, SSCG_QUERY_PEER_HALO = 5 };
 SSCG_API sscg_status sscg_query(const sscg_ctx *ctx, int32_t what, int64_t *out);
 
 SSCG_API void sscg_destroy(sscg_ctx *ctx);

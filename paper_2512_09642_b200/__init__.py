@@ -33,7 +33,8 @@ SOLVE_X0_ZERO = 1
 OPT_GRAM_SOLVER, OPT_BASIS, OPT_DIAGNOSTICS, OPT_BLOCKCG = 0, 1, 2, 3
 GRAM_FGS, GRAM_CHOLESKY = 0, 1
 BASIS_CHEBYSHEV, BASIS_MONOMIAL = 0, 1
-QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS, QUERY_UPDATE_VECTORS, QUERY_GRAM_VECTORS, QUERY_BASIS_SINGLE_VECTORS = 0, 1, 2, 3, 4
+(QUERY_BASIS_FUSED, QUERY_BASIS_VECTORS, QUERY_UPDATE_VECTORS, QUERY_GRAM_VECTORS, QUERY_BASIS_SINGLE_VECTORS,
+ QUERY_PEER_HALO) = 0, 1, 2, 3, 4, 5
 
 EXPORTS = ["sscg_partition", "sscg_halo_plan", "sscg_nccl_unique_id", "sscg_setup", "sscg_solve", "sscg_solve_host", "sscg_iterate",
            "sscg_set_profiling", "sscg_profile", "sscg_stats", "sscg_inspect", "sscg_local_shape", "sscg_destroy",

@@ -102,6 +102,7 @@ struct Outs {
     // peer-store halos: p_{j+2}, p_{j+3} of the neighbour below / above, offset so
     // that own offset + pointer is the neighbour's ghost cell (null: none)
     double *lo[2], *hi[2];
+    int sys_fence;   // the peer stores go to another process's memory (CUDA IPC over NVLink)
 };
 
 __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int x, int y, int z, int v,
@@ -433,6 +434,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int z = max(it.q1 + 1, it.plo); z <= it.phi; ++z) release(z);
         sc = sbase + (it.phi - it.plo + 1);
     }
+    // stores into another rank's ghost planes are performed system-wide before
+    // this thread exits: the token the stream sends after the kernel (the
+    // ordering step of the cross-rank peer-store halo) then follows them
+    if (out.sys_fence) __threadfence_system();
 }
 
 }  // namespace
@@ -534,6 +539,7 @@ void launch_k1m(const Geo &g, const K1MArgs &a, double theta, const DevState *st
         out.lo[l] = (formed && a.peer_lo[l]) ? a.peer_lo[l] + (int64_t)a.peer_nzl_lo * g.plane : nullptr;
         out.hi[l] = (formed && a.peer_hi[l]) ? a.peer_hi[l] - (int64_t)a.nzl * g.plane : nullptr;
     }
+    out.sys_fence = a.peer_sys_fence;
     if (!out.lo[0]) out.lo[1] = nullptr;   // the kernel keys the steady range on level 2's pointer
     if (!out.hi[0]) out.hi[1] = nullptr;
     const int64_t tiles = (int64_t)wk.tiles_x * wk.tiles_y;

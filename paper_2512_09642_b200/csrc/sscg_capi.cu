@@ -126,6 +126,14 @@ struct sscg_ctx {
     double *lz_part = nullptr;        // dot partials [slab][grid]
     unsigned *lz_ticket = nullptr;    // [slab]
     ncclComm_t comm = nullptr;
+    // cross-rank peer-store halos: the neighbours' P mapped through
+    // CUDA IPC (or, SSCG_NCCL_SELF, the in-process slabs' descriptors after the
+    // same NCCL round trip); after each deep triple a one-double token to every
+    // such neighbour orders its next triple after this one's stores
+    bool peer_remote = false;
+    int peer_rank[2] = {-1, -1};      // rank below slab 0 / above the last slab (-1: none)
+    std::vector<void *> ipc_open;     // mappings to close at destroy
+    double *token = nullptr;          // [send, recv lo, recv hi]
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double *bbuf = nullptr, *xbuf = nullptr;   // device buffers of sscg_solve_host
     double *scratch = nullptr;                 // process-layout scratch for inspect
@@ -349,6 +357,8 @@ Knobs sscg::read_knobs()
     return k;
 }
 
+static sscg_status setup_peers(sscg_ctx *c);
+
 static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, double lmin, double lmax, int s,
                               int nu, const sscg_comm *cm, void *stream, sscg_ctx *c)
 {
@@ -538,6 +548,7 @@ static sscg_status setup_impl(const sscg_operator *A, const double *diag_M, doub
         NC(ncclCommInitRank(&c->comm, 1, id, 0));
         c->nccl_self = true;
     }
+    TRY(setup_peers(c));
     CU(cudaStreamSynchronize(c->stream));
     return SSCG_OK;
 }
@@ -572,6 +583,7 @@ extern "C" void sscg_destroy(sscg_ctx *c)
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     c->gexec = nullptr;
     if (c->comm) ncclCommDestroy(c->comm);
+    for (void *p : c->ipc_open) cudaIpcCloseMemHandle(p);
     for (void *p : c->allocs) cudaFree(p);
     if (c->st_host) cudaFreeHost(c->st_host);
     if (c->xhost) cudaFreeHost(c->xhost);
@@ -934,13 +946,188 @@ static bool uses_deep(const sscg_ctx *c)
     return halo && c->g.guard >= 2 && uses_mp3(c);
 }
 
-// peer-store halos: with in-process neighbours only, each deep
-// triple stores the planes its neighbours need straight into their ghost
-// planes (K1M), so no exchange follows it
+// peer-store halos: each deep triple stores the planes its
+// neighbours need straight into their ghost planes (K1M), so no exchange
+// follows it -- in-process neighbours by pointer; other ranks' basis mapped
+// through CUDA IPC at setup (peer_remote), then a token orders the triples
 static bool uses_peer(const sscg_ctx *c)
 {
-    return c->g.kn.peer_halo && c->nranks == 1 && c->slabs.size() > 1 && !c->nccl_self && uses_deep(c) &&
-           !c->g.kn.deep_overlap;
+    if (!c->g.kn.peer_halo || c->g.kn.deep_overlap || !uses_deep(c)) return false;
+    return (c->nranks == 1 && c->slabs.size() > 1 && !c->nccl_self) || c->peer_remote;
+}
+
+// the descriptor of one slab's P that a neighbour needs to store into it
+struct PeerInfo {
+    cudaIpcMemHandle_t h;
+    int64_t off, vstride;   // P - the allocation (bytes), vector stride (doubles)
+    int32_t nzl, pid;
+    uint64_t nonce, base;   // this process, and the allocation's address in it
+};
+
+static uint64_t proc_nonce()
+{
+    static int anchor;
+    return (uint64_t)(uintptr_t)&anchor ^ ((uint64_t)getpid() << 32);
+}
+
+// a neighbour's P: its own pointer in this process (the SSCG_NCCL_SELF test
+// mode), else the allocation opened through CUDA IPC (null if that fails)
+static double *peer_map(sscg_ctx *c, const PeerInfo &pi, bool *remote)
+{
+    void *base = nullptr;
+    *remote = !(pi.pid == (int32_t)getpid() && pi.nonce == proc_nonce());
+    if (!*remote) {
+        base = (void *)(uintptr_t)pi.base;
+    } else {
+        if (cudaIpcOpenMemHandle(&base, pi.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        c->ipc_open.push_back(base);
+    }
+    return reinterpret_cast<double *>(static_cast<char *>(base) + pi.off);
+}
+
+// neighbour descriptors of every slab: in-process neighbours by pointer; with a
+// communicator and the deep peer-store schedule, the other ranks' first / last
+// slab exchanged by NCCL and mapped (SSCG_NCCL_SELF: the in-process pairs make
+// the same round trip to self).  All ranks agree (min over the communicator)
+// or every rank keeps the NCCL exchange of the ghost planes.
+static sscg_status setup_peers(sscg_ctx *c)
+{
+    const Geo &g = c->g;
+    const int L = (int)c->slabs.size();
+    for (void *p : c->ipc_open) cudaIpcCloseMemHandle(p);   // a rebuilt store (SSCG_OPT_BLOCKCG): map again
+    c->ipc_open.clear();
+    for (int l = 0; l < L; ++l) {
+        Slab &sl = c->slabs[l];
+        for (int d = 0; d < 2; ++d) {
+            sl.nbP[d] = nullptr;
+            sl.nbvs[d] = 0;
+            sl.nbnzl[d] = 0;
+            sl.nb_remote[d] = 0;
+        }
+        if (l > 0) {
+            sl.nbP[0] = c->slabs[l - 1].P;
+            sl.nbvs[0] = g.vstride;
+            sl.nbnzl[0] = c->slabs[l - 1].nzl;
+        }
+        if (l + 1 < L) {
+            sl.nbP[1] = c->slabs[l + 1].P;
+            sl.nbvs[1] = g.vstride;
+            sl.nbnzl[1] = c->slabs[l + 1].nzl;
+        }
+    }
+    c->peer_remote = false;
+    if (!c->comm || !g.kn.peer_halo || g.kn.deep_overlap || !uses_deep(c)) return SSCG_OK;
+    // messages: (slab whose descriptor is sent, peer rank) and (slab, side, peer rank) received
+    struct Tx { int slab, peer; };
+    struct Rx { int slab, side, peer; };
+    std::vector<Tx> tx;
+    std::vector<Rx> rx;
+    if (c->nranks > 1) {
+        int64_t lo[6], hi[6];
+        TRY(sscg_halo_plan(c->nz_global, c->nranks, c->spr, c->rank, 0, lo));
+        TRY(sscg_halo_plan(c->nz_global, c->nranks, c->spr, c->rank, L - 1, hi));
+        c->peer_rank[0] = (lo[0] >= 0 && lo[0] != c->rank) ? (int)lo[0] : -1;
+        c->peer_rank[1] = (hi[3] >= 0 && hi[3] != c->rank) ? (int)hi[3] : -1;
+        if (c->peer_rank[0] >= 0) {
+            tx.push_back({0, c->peer_rank[0]});
+            rx.push_back({0, 0, c->peer_rank[0]});
+        }
+        if (c->peer_rank[1] >= 0) {
+            tx.push_back({L - 1, c->peer_rank[1]});
+            rx.push_back({L - 1, 1, c->peer_rank[1]});
+        }
+    } else if (c->nccl_self && L > 1) {
+        for (int l = 0; l + 1 < L; ++l) {   // in order: slab l+1's to slab l, slab l's to slab l+1
+            tx.push_back({l + 1, 0});
+            rx.push_back({l, 1, 0});
+            tx.push_back({l, 0});
+            rx.push_back({l + 1, 0, 0});
+        }
+    }
+    const size_t nb = sizeof(PeerInfo);
+    std::vector<PeerInfo> hin(tx.size()), hout(rx.size());
+    for (size_t i = 0; i < tx.size(); ++i) {
+        const Slab &sl = c->slabs[tx[i].slab];
+        PeerInfo &pi = hin[i];
+        memset(&pi, 0, nb);
+        CU(cudaIpcGetMemHandle(&pi.h, sl.Palloc));
+        pi.off = (int64_t)(reinterpret_cast<char *>(sl.P) - reinterpret_cast<char *>(sl.Palloc));
+        pi.vstride = g.vstride;
+        pi.nzl = sl.nzl;
+        pi.pid = (int32_t)getpid();
+        pi.nonce = proc_nonce();
+        pi.base = (uint64_t)(uintptr_t)sl.Palloc;
+    }
+    char *dbuf = nullptr;
+    int *dok = nullptr;
+    TRY(dalloc(c, &dbuf, (tx.size() + rx.size()) * nb + 1));
+    TRY(dalloc(c, &dok, 1));
+    if (!c->token) TRY(dalloc(c, &c->token, 3));
+    if (!tx.empty()) CU(cudaMemcpyAsync(dbuf, hin.data(), tx.size() * nb, cudaMemcpyHostToDevice, c->stream));
+    NC(ncclGroupStart());
+    for (size_t i = 0; i < tx.size(); ++i) {
+        NC(ncclSend(dbuf + i * nb, nb, ncclUint8, tx[i].peer, c->comm, c->stream));
+        NC(ncclRecv(dbuf + (tx.size() + i) * nb, nb, ncclUint8, rx[i].peer, c->comm, c->stream));
+    }
+    NC(ncclGroupEnd());
+    if (!rx.empty())
+        CU(cudaMemcpyAsync(hout.data(), dbuf + tx.size() * nb, rx.size() * nb, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    std::vector<double *> ptr(rx.size());
+    std::vector<int> remote(rx.size());
+    int ok = 1;
+    for (size_t i = 0; i < rx.size(); ++i) {
+        bool rem = false;
+        ptr[i] = peer_map(c, hout[i], &rem);
+        remote[i] = rem;
+        if (!ptr[i]) ok = 0;
+    }
+    CU(cudaMemcpyAsync(dok, &ok, sizeof ok, cudaMemcpyHostToDevice, c->stream));
+    NC(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->comm, c->stream));
+    CU(cudaMemcpyAsync(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    dfree(c, dbuf);
+    dfree(c, dok);
+    if (!ok) {   // every rank keeps the NCCL exchange
+        for (void *p : c->ipc_open) cudaIpcCloseMemHandle(p);
+        c->ipc_open.clear();
+        return SSCG_OK;
+    }
+    for (size_t i = 0; i < rx.size(); ++i) {
+        Slab &sl = c->slabs[rx[i].slab];
+        const int d = rx[i].side;
+        sl.nbP[d] = ptr[i];
+        sl.nbvs[d] = hout[i].vstride;
+        sl.nbnzl[d] = hout[i].nzl;
+        sl.nb_remote[d] = remote[i];
+    }
+    c->peer_remote = !rx.empty();
+    return SSCG_OK;
+}
+
+// the ordering step of the cross-rank peer-store halo: one double to and from
+// every neighbour that was stored into (graph-captured like the exchange)
+static sscg_status peer_token(sscg_ctx *c)
+{
+    if (!c->peer_remote) return SSCG_OK;
+    TRY(prof_mark(c, SSCG_PROF_HALO, true));
+    NC(ncclGroupStart());
+    if (c->nranks > 1) {
+        for (int d = 0; d < 2; ++d)
+            if (c->peer_rank[d] >= 0) {
+                NC(ncclSend(c->token, 1, ncclDouble, c->peer_rank[d], c->comm, c->stream));
+                NC(ncclRecv(c->token + 1 + d, 1, ncclDouble, c->peer_rank[d], c->comm, c->stream));
+            }
+    } else {
+        NC(ncclSend(c->token, 1, ncclDouble, 0, c->comm, c->stream));
+        NC(ncclRecv(c->token + 1, 1, ncclDouble, 0, c->comm, c->stream));
+    }
+    NC(ncclGroupEnd());
+    TRY(prof_mark(c, SSCG_PROF_HALO, false));
+    return SSCG_OK;
 }
 
 // deep-halo triple of steps j..j+2 on every slab.  part 0: all planes (levels 1
@@ -976,13 +1163,15 @@ static sscg_status launch_basis_triple_deep(sscg_ctx *c, int j, int part)
         if (part == 2) a.sm_cap = c->k1_sm_cap;
         if (part == 0 && uses_peer(c)) {
             const size_t l = &sl - c->slabs.data();
+            (void)l;
             for (int v = 0; v < 2; ++v) {
                 const int jv = j + 2 + v;   // p_{j+2}, p_{j+3}
                 if (jv > s - 1) continue;
-                if (l > 0) a.peer_lo[v] = c->slabs[l - 1].P + (int64_t)jv * g.vstride;
-                if (l + 1 < c->slabs.size()) a.peer_hi[v] = c->slabs[l + 1].P + (int64_t)jv * g.vstride;
+                if (sl.nbP[0]) a.peer_lo[v] = sl.nbP[0] + (int64_t)jv * sl.nbvs[0];
+                if (sl.nbP[1]) a.peer_hi[v] = sl.nbP[1] + (int64_t)jv * sl.nbvs[1];
             }
-            if (l > 0) a.peer_nzl_lo = c->slabs[l - 1].nzl;
+            a.peer_nzl_lo = sl.nbnzl[0];
+            a.peer_sys_fence = sl.nb_remote[0] || sl.nb_remote[1];
         }
         a.deep_lo = sl.has_lo;
         a.deep_hi = sl.has_hi;
@@ -1155,6 +1344,7 @@ static sscg_status enqueue_outer(sscg_ctx *c, double *x)
                 } else {
                     TRY(launch_basis_triple_deep(c, j, 0));
                     if (np3 > 0 && !uses_peer(c)) TRY(halo_fork(c, j + 3, false, np3, j + 2, np2));
+                    if (np3 > 0 && uses_peer(c)) TRY(peer_token(c));
                 }
             } else {
                 // boundary planes of step j, exchange of p_{j+1} (overlapped with the
@@ -1739,6 +1929,7 @@ extern "C" sscg_status sscg_set_option(sscg_ctx *c, int32_t key, int32_t value)
             // the store holds [P | Q'] and [W | Z'] (2s vectors) in the block mode
             drop_graph(c);
             TRY(build_basis_store(c, value ? 2 * c->s : c->s));
+            TRY(setup_peers(c));   // the neighbours' new stores (collective across ranks, like the option)
             TRY(alloc_gram_buffers(c, value ? 2 * c->s : c->s));
             if (value && !c->blk2) {
                 TRY(dalloc(c, &c->blk2, (size_t)c->s * c->s + c->s));
@@ -1874,6 +2065,9 @@ extern "C" sscg_status sscg_query(const sscg_ctx *c, int32_t what, int64_t *out)
     switch (what) {
     case SSCG_QUERY_BASIS_FUSED:   // basis steps per launch of the schedule's main kernel
         *out = uses_mp3(c) ? 3 : uses_fused(c) ? 2 : 1;
+        return SSCG_OK;
+    case SSCG_QUERY_PEER_HALO:
+        *out = !uses_peer(c) ? 0 : c->peer_remote ? 2 : 1;
         return SSCG_OK;
     case SSCG_QUERY_BASIS_VECTORS:
     case SSCG_QUERY_BASIS_SINGLE_VECTORS: {

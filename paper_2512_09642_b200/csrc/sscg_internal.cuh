@@ -78,6 +78,14 @@ struct Slab {
     double *P;         // s vectors, stride vstride (2s in the block-conjugate mode: [P_k | Q_{k-1}])
     double *W;         // s vectors, stride vstride (2s: [W_k | Z_{k-1} = A Q_{k-1}])
     double *Palloc, *Walloc;      // the allocations (P, W start Geo::guard planes in)
+    // peer-store halos: the basis P of the neighbour below [0] /
+    // above [1] that K1M stores ghost planes into -- an in-process slab, or
+    // another rank's P mapped through CUDA IPC -- with its vector stride and
+    // depth (null: exchange instead)
+    double *nbP[2];
+    int64_t nbvs[2];
+    int nbnzl[2];
+    int nb_remote[2];             // the neighbour is another process (K1M ends with a system-scope fence)
     bool want_k1f, want_k1m, want_k1fv;   // basis kernels whose tensor maps the store needs
     double *part;      // Gram partials [grid][nent]
     double *blk;       // this slab's reduced block (s*s + s)
@@ -221,6 +229,7 @@ struct K1MArgs {
     // exchange after the triple
     double *peer_lo[2], *peer_hi[2];
     int peer_nzl_lo;       // nzl of the slab below
+    int peer_sys_fence;    // a neighbour is another process: fence.sc.sys after the peer stores
     double sigma;
     const CUtensorMap *tmP, *tmM;
 };

@@ -147,7 +147,9 @@ def test_slab_decomposition(cfg, slabs):
                                            (("7pt", 58, 30, 37, 10, 20), 2, {"SSCG_K1_MP3": "1"}),
                                            (("varcoef7", 40, 26, 28, 8, 20), 3, {}),
                                            (("27pt", 24, 20, 30, 8, 20), 4, {}),
-                                           (("7pt", 34, 18, 20, 5, 10), 2, {"SSCG_NO_OVERLAP": "1"})],
+                                           (("7pt", 34, 18, 20, 5, 10), 2, {"SSCG_NO_OVERLAP": "1"}),
+                                           (("7pt", 58, 30, 37, 10, 20), 3, {"SSCG_K1_MP3": "1",
+                                                                             "SSCG_PEER_HALO": "0"})],
                          ids=lambda v: _ids(v) if isinstance(v, tuple) else (str(v) if not isinstance(v, dict) else
                                                                              "-".join(v) or "default"))
 def test_nccl_self_path(cfg, slabs, env, monkeypatch):
@@ -161,6 +163,7 @@ def test_nccl_self_path(cfg, slabs, env, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     P = Problem(kind, nx, ny, nz, s, nu, lanczos=(kind != "7pt"))
+    import paper_2512_09642_b200 as sscg
     out = {}
     for mode in ("0", "1"):
         monkeypatch.setenv("SSCG_NCCL_SELF", mode)
@@ -168,8 +171,18 @@ def test_nccl_self_path(cfg, slabs, env, monkeypatch):
             lb = S.estimate_bounds(P.b_gpu(), 20, 0.05) if kind != "7pt" else None
             x = S.solve(P.b_gpu(), rtol=0.0, max_outer=5).cpu().numpy()
             st = S.stats()
-            out[mode] = (x, S.gram(3)[0], st.allreduces, lb)
+            out[mode] = (x, S.gram(3)[0], st.allreduces, lb, S.query(sscg.QUERY_PEER_HALO),
+                         S.query(sscg.QUERY_BASIS_FUSED))
     assert out["1"][2] == 6 and out["0"][2] == 0      # one allreduce per outer (+ the final stopping test)
+    if env.get("SSCG_K1_MP3") == "1":
+        assert out["1"][5] == 3 and out["0"][5] == 3
+    if out["1"][5] == 3:
+        assert out["1"][4] == (0 if env.get("SSCG_PEER_HALO") == "0" else 2)
+    if out["1"][5] == 3 and env.get("SSCG_PEER_HALO") != "0":
+        # deep-halo triples: in-process peer stores (0), and in the NCCL mode the
+        # cross-rank peer-store path -- descriptors through an NCCL round trip,
+        # a token per triple
+        assert out["0"][4] == 1 and out["1"][4] == 2
     assert np.array_equal(out["1"][0], out["0"][0])
     assert np.array_equal(out["1"][1], out["0"][1])
     if out["0"][3] is not None:
