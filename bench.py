@@ -465,6 +465,29 @@ def run_ours(a):
         kern[k] = {"launches": cnt, "ms_per_launch": t_ms / max(cnt, 1), "bytes_per_launch": per_launch,
                    "achieved_gbs": gbs, "frac": (gbs / peak) if gbs else None,
                    "share_of_step": t_ms / st_prof.ms_total if st_prof.ms_total else None}
+    # the Gram pass also against the FP64 pipe (the limit at s >= 24): FP64 issue slots
+    # per grid point of the kernel as launched -- the tensor-core pass (K2R / K2D, s > 8 or the folded
+    # schedule) forms every 8 x 8 tile of a block triangle of ceil(s/8) blocks by DMMA m8n8k4 (64 FMA
+    # per tile and point) and c_i = p_i^T p_0 by s FMAs; the streaming pass K2S (s <= 8) forms
+    # s(s+1)/2 + s entries by DFMA; the W-free passes add 3 FP64 operations per recovered w_j(point).
+    # Peak: the DMMA rate measured by tools/dmma_probe.cu (profiles/r02a_dmma_probe.txt, 37.1 TFLOP/s
+    # = 18.55e12 FMA/s; DFMA alone measured 33.9).
+    if "gram" in kern and kern["gram"]["ms_per_launch"] > 0 and not csr:
+        wfree_g = gram_vecs < 2 * s
+        nb = (s + 7) // 8
+        if wfree_g:   # K2S for s <= 8 unless SSCG_K2S=0, else K2R
+            tensor = s > 8 or os.environ.get("SSCG_K2S", "1") == "0"
+        else:         # stored W: K2D for s > 16 unless forced, else the register-tiled K2
+            tensor = os.environ.get("SSCG_K2_DMMA", "1" if s > 16 else "0") == "1"
+        fma_pt = (64 * nb * (nb + 1) // 2 + s) if tensor else (s * (s + 1) // 2 + s)
+        if wfree_g:
+            fma_pt += 3 * s
+        gl = kern["gram"]
+        fma_s = fma_pt * (n_local * a.steps / max(gl["launches"], 1)) / (gl["ms_per_launch"] / 1e3)   # points per launch
+        gl["fp64_pipe"] = {"fma_slots_per_point": fma_pt, "achieved_tflops": 2 * fma_s / 1e12,
+                           "peak_tflops": 37.1, "frac": 2 * fma_s / 1e12 / 37.1,
+                           "peak_source": "profiles/r02a_dmma_probe.txt (FP64 DMMA, 8-16 warps per SM)",
+                           "kernel": ("K2R" if wfree_g else "K2D/K2") if tensor else "K2S"}
     for k in ("fgs", "allreduce", "halo"):
         t_ms, cnt = prof[k]
         kern[k] = {"launches": cnt, "us_per_launch": 1e3 * t_ms / max(cnt, 1),
