@@ -114,8 +114,10 @@ __device__ __forceinline__ ItemPlan plan_item(const K1FVWork &wk, int64_t item)
     p.phi = min(p.zhi + 1, wk.nzl + 1);
     p.mlo = max(p.zlo - 1, 1);
     p.mhi = min(p.zhi, wk.nzl);
-    p.flo = max(p.zlo - 1, 1);            // the fronts at [zlo-1, zhi] inside [1, nzl] read slots q, q+1
-    p.fhi = min(p.zhi + 1, wk.nzl + 1);
+    // the fronts at [zlo-1, zhi] inside [1, nzl] read slot q (kx, ky and the upper kz face of
+    // plane q); slot flo, one plane below the first front, carries only its lower kz face
+    p.flo = max(p.zlo - 1, 1) - 1;
+    p.fhi = min(p.zhi, wk.nzl);
     return p;
 }
 
@@ -227,11 +229,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                         ++mc;
                     }
                 }
-                // face slot z holds kx(z), ky(z) (1 <= z <= nzl) and kz(z-1) (1 <= z <= nzl+1)
+                // face slot z holds kx(z), ky(z) (flo < z <= fhi) and kz(z), the upper face of plane z
+                // (flo <= z <= fhi; kz index 0 is the bottom boundary face)
                 while (fnext <= min(q + 1, it.fhi)) {
                     const int sl = fc % NSF;
                     const int z = fnext, zl = z - 1;
-                    const bool xy = z <= wk.nzl;
+                    const bool xy = z != it.flo;
                     double *d = sf + sl * FS;
                     if (lane == 0) {
                         if (fc >= NSF) mbar_wait(&emptyf[sl], ((fc / NSF) - 1) & 1);
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                     if (lane == 0) {
                         if (xy) tma_load_3d(d + FKY, &fm.ky, x0 - 2, y0 - 1, zl, &fullf[sl]);
-                        tma_load_3d(d + FKZ, &fm.kz, x0 - 2, y0 - 1, zl, &fullf[sl]);
+                        tma_load_3d(d + FKZ, &fm.kz, x0 - 2, y0 - 1, z, &fullf[sl]);
                     }
                     __syncwarp();
                     ++fc;
@@ -308,7 +311,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         };
         auto releasef = [&](int z) { mbar_arrive_a(ef_a + 8 * ((fbase + (uint32_t)(z - it.flo)) % NSF)); };
         for (int z = it.plo; z <= min(it.zlo, it.phi); ++z) waitp(z);
-        for (int z = it.flo; z <= min(it.zlo, it.fhi); ++z) waitf(z);
         double2 pdn = make_double2(0.0, 0.0);
         if (it.zlo - 2 >= it.plo) {
             pdn = lds2(slotp(it.zlo - 2) + ok);
@@ -317,12 +319,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         double2 pc0 = lds2(slotp(it.zlo - 1) + ok);
         double2 um2 = make_double2(0.0, 0.0), um1 = make_double2(0.0, 0.0);
         double2 dinvb = make_double2(0.0, 0.0);   // D^{-1} of the back's cells (from the previous front)
+        // the own pair's kz faces roll through registers: at plane q, kza = kz(q-2), kzb = kz(q-1)
+        // (the back's lower / upper face, the front's lower face); the front loads kz(q)
+        waitf(it.flo);
+        double2 kza = make_double2(0.0, 0.0), kzb = lds2(slotf(it.flo) + ofz);
+        releasef(it.flo);
         int64_t off = (int64_t)(it.zlo - 1) * pl + (int64_t)gy * g.pitch + gx;
         const int64_t rowfaces = (int64_t)g.ny * (g.nx + 1);
-        // the own pair's faces at plane z (slot z; the upper kz face from slot z+1)
-        auto faces_at = [&](int z, double2 &kzd) -> PairFaces {
+        // the own pair's kx, ky faces at plane z (slot z) with the given upper kz face
+        auto faces_at = [&](int z, double2 kzu) -> PairFaces {
             PairFaces F;
-            const double *Fz = slotf(z), *Fz1 = slotf(z + 1);
+            const double *Fz = slotf(z);
             const int px = ck + (int)((fa + (int64_t)(z - 1) * rowfaces + wk.kx_shift) & 1);
             const double *kxr = Fz + FKX + (rk - 1) * KXP + px;
             F.kxw0 = kxr[0];
@@ -330,10 +337,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             F.kxe1 = kxr[2];
             F.kys = lds2(Fz + ofy);
             F.kyn = lds2(Fz + ofy + BW);
-            kzd = lds2(Fz + ofz);
-            F.kzu = lds2(Fz1 + ofz);
-            if (!v0) { F.kxw0 = F.kxe0 = 0.0; F.kys.x = F.kyn.x = kzd.x = F.kzu.x = 0.0; }
-            if (!v1) { F.kxe1 = 0.0; F.kys.y = F.kyn.y = kzd.y = F.kzu.y = 0.0; }
+            F.kzu = kzu;
+            // a cell outside the grid keeps whatever its face slots hold: its D^{-1}, u and
+            // stores are selected away below (never multiplied away), and a valid cell reads
+            // only its own faces (26 fewer selects per plane than zeroing them here)
             return F;
         };
         auto plane = [&](int q, auto steady) {
@@ -346,15 +353,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (S || q >= it.zlo) waitp(q + 1);
                 pup = lds2(slotp(q + 1) + ok);
             }
-            if ((S || (q + 1 >= it.flo && q + 1 <= it.fhi)) && (S || q >= it.zlo)) waitf(q + 1);
+            if (inside) waitf(q);
             const bool mloaded = front_pm && (S || (q >= it.mlo && q <= it.mhi));
             const uint32_t ms = mc & (NSM - 1);
             if (mloaded) mbar_wait_a(fm_a + 8 * ms, (mc / NSM) & 1);
             // ---------------- front(q): step j on tile + halo ----------------
-            double2 u = make_double2(0.0, 0.0), dinv = make_double2(0.0, 0.0);
+            double2 u = make_double2(0.0, 0.0), dinv = make_double2(0.0, 0.0), kzc = kzb;
             if (inside) {
-                double2 kzd;
-                const PairFaces F = faces_at(q, kzd);
+                kzc = lds2(slotf(q) + ofz);
+                const double2 kzd = kzb;
+                const PairFaces F = faces_at(q, kzc);
                 const double2 c = pc0;
                 const double2 ylo = lds2(P0 + ok - BW), yhi = lds2(P0 + ok + BW);
                 const double l = lgk ? P0[ok - 1] : 0.0;
@@ -391,8 +399,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const double2 c = um1, dn = um2, up = u;
                 const double2 ylo = lds2(U0 + ok - BW), yhi = lds2(U0 + ok + BW);
                 const double l = U0[ok - 1], rr = U0[ok + 2];
-                double2 D, kzdb;
-                const PairFaces Fb = faces_at(q - 1, kzdb);   // face slot q-1 is released after this
+                double2 D;
+                const double2 kzdb = kza;
+                const PairFaces Fb = faces_at(q - 1, kzb);   // face slot q-1 is released after this
                 double2 Ap = vc_apply(Fb, kzdb, c, dn, up, ylo, yhi, l, rr, D);
                 if (!v1) Ap.y = 0.0;
                 if (!skip_w2) __stcs(reinterpret_cast<double2 *>(gw2 + off - pl), Ap);
@@ -404,7 +413,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                     *reinterpret_cast<double2 *>(gpn2 + off - pl) = make_double2(v0b, v1b);
                 }
             }
-            if (S || (q - 1 >= it.flo && q - 1 <= it.fhi)) releasef(q - 1);   // faces of plane q-1 done
+            if (S || (q - 1 > it.flo && q - 1 <= it.fhi)) releasef(q - 1);   // faces of plane q-1 done
+            if (inside) {
+                kza = kzb;
+                kzb = kzc;
+            }
             ++uc;
             um2 = um1;
             um1 = u;
@@ -422,7 +435,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (; q < it.zhi; ++q) plane(q, Steady());
         for (; q <= it.zhi; ++q) plane(q, Gen());
         for (int z = max(it.zhi + 1, it.plo); z <= it.phi; ++z) release(z);
-        for (int z = max(it.zhi, it.flo); z <= it.fhi; ++z) releasef(z);
+        for (int z = max(it.zhi, it.flo + 1); z <= it.fhi; ++z) releasef(z);
         pc = pbase + (it.phi - it.plo + 1);
         fc = fbase + (it.fhi - it.flo + 1);
     }
