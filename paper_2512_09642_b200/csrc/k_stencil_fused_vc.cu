@@ -16,9 +16,19 @@
 // on the tile) coincide, so the z-columns of p_j and p_{j+1} roll through
 // registers.  The faces of the front region (kx rows as 1-D boxes from the
 // even element at or below x0-2, ky and kz as 3-D boxes) are staged per plane
-// by TMA into a 5-slot ring; a thread reads its own cells' faces of plane q
-// (front) and again of plane q-1 (back) from it, and keeps only D^{-1} of its
-// cells from the front for the back.  Tile 64 x 12, 16 warps, 115 registers.
+// by TMA into a 5-slot ring; slot z carries kx(z), ky(z) and the upper kz
+// face of plane z.  A thread reads its own cells' kx, ky of plane q (front)
+// and again of plane q-1 (back) from it; its kz faces roll through registers
+// (the lower face of plane q is the upper one of q-1, and the back reuses the
+// pair the front had one plane earlier), so two slots are live and three
+// planes of faces are in flight; it keeps D^{-1} of its cells from the front
+// for the back.  Faces of cells outside the grid are not zeroed: those cells'
+// D^{-1}, u and stores are selected away.  Tile 64 x 12, 16 warps, 114
+// registers.  ncu (384^3, profiles/r02o_*k1fv*): ~20 % of the warp samples
+// sit on the p_j / face mbarrier waits with the producer never blocked and
+// DRAM at 54 % -- the loads are in flight but late (TMA completion latency
+// ~3.5 us at this depth), which is what bounds the kernel, not issue slots
+// (29 fewer instructions per plane changed nothing measurable).
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
