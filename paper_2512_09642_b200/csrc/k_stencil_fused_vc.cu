@@ -23,12 +23,16 @@
 // pair the front had one plane earlier), so two slots are live and three
 // planes of faces are in flight; it keeps D^{-1} of its cells from the front
 // for the back.  Faces of cells outside the grid are not zeroed: those cells'
-// D^{-1}, u and stores are selected away.  Tile 64 x 12, 16 warps, 114
-// registers.  ncu (384^3, profiles/r02o_*k1fv*): ~20 % of the warp samples
-// sit on the p_j / face mbarrier waits with the producer never blocked and
-// DRAM at 54 % -- the loads are in flight but late (TMA completion latency
-// ~3.5 us at this depth), which is what bounds the kernel, not issue slots
-// (29 fewer instructions per plane changed nothing measurable).
+// D^{-1}, u and stores are selected away.  Tile 64 x 12, 15 consumer warps
+// and three producer warps (p_j / p_{j-1}; ky + kz boxes; the kx rows), 96
+// registers (18 warps: five on one scheduler).  With ONE producer warp, ncu
+// (384^3, profiles/r02o_*k1fv*) showed ~20 % of the consumers' samples on the
+// p_j / face mbarrier waits while the producer was never blocked on an empty
+// slot and busy ~94 % of its time: its ~19 TMA issues per plane (14 of them
+// the kx rows, serialised over lanes) were the critical path, not issue slots
+// of the consumers (29 fewer instructions per plane changed nothing) nor
+// DRAM (54 %).  Split producers: 0.718 -> 0.623 ms per pair at 384^3
+// (0.78 of copy), 0.0938 -> 0.086 ms at 192^3 (0.70).
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -61,7 +65,8 @@ constexpr int NSP = K1FV_NSP, NSM = 4, NU = 4;   // powers of two
 constexpr int NROW = TY + 2;               // row warps 1..TY+2
 constexpr int NCW = NROW + 1;              // + one warp for the 2*(TY+2) halo pairs
 constexpr int NCT = NCW * 32;
-constexpr int THREADS = NCT + 32;
+constexpr int NPW = 3;                    // producer warps: p_j / p_{j-1}, ky + kz faces, kx face rows
+constexpr int THREADS = NCT + 32 * NPW;
 constexpr uint32_t PBYTES = BW * BHP * 8, MBYTES = BW * BHM * 8;
 // face slots (per plane z of the march, the front cells' rows y0-1 .. y0+TY):
 //   KX: TY+2 rows of 70 faces from the even element at or below x0-2 (pitch 80)
@@ -215,54 +220,64 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
 
-    if (warp == 0) {   // producer warp: lane 0 issues, lanes 0..TY+1 the kx face rows
-        uint32_t pc = 0, mc = 0, fc = 0;
+    // two producer warps -- one warp issuing all ~19 loads of a plane was the
+    // critical path (ncu r02o: never blocked on an empty slot, busy ~94 % of the time)
+    if (warp == 0) {   // p_j and p_{j-1} planes: lane 0 issues
+        if (lane != 0) return;
+        uint32_t pc = 0, mc = 0;
         for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
             const ItemPlan it = plan_item(wk, item);
             const int x0 = it.tx * TX, y0 = it.ty * TY;
-            int pnext = it.plo, fnext = it.flo;
+            int pnext = it.plo;
             for (int q = it.zlo - 1; q <= it.zhi; ++q) {
+                while (pnext <= min(q + 1, it.phi)) {
+                    const int sl = pc & (NSP - 1);
+                    if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
+                    mbar_expect_tx(&fullp[sl], PBYTES);
+                    tma_load_4d(sp + sl * PS, &tmP, x0 - 2, y0 - 2, pnext, wk.j, &fullp[sl]);
+                    ++pc;
+                    ++pnext;
+                }
+                if (wk.front_pm && q >= it.mlo && q <= it.mhi) {
+                    const int sl = mc & (NSM - 1);
+                    if (mc >= NSM) mbar_wait(&emptym[sl], ((mc / NSM) - 1) & 1);
+                    mbar_expect_tx(&fullm[sl], MBYTES);
+                    tma_load_4d(sm + sl * MS, &tmM, x0 - 2, y0 - 1, q, wk.j - 1, &fullm[sl]);
+                    ++mc;
+                }
+            }
+        }
+        return;
+    }
+    if (warp < NPW) {   // face slots, as far ahead as the ring allows: warp 1 lane 0 the ky / kz boxes (and the
+                        // slot's byte count), warp 2 lanes 0..TY+1 the kx face rows (both wait for the empty slot)
+        const bool wkx = warp == 2;
+        uint32_t fc = 0;
+        for (int64_t item = blockIdx.x; item < wk.nitems; item += gridDim.x) {
+            const ItemPlan it = plan_item(wk, item);
+            const int x0 = it.tx * TX, y0 = it.ty * TY;
+            // face slot z holds kx(z), ky(z) (flo < z <= fhi) and kz(z), the upper face of plane z
+            // (flo <= z <= fhi; kz index 0 is the bottom boundary face)
+            for (int z = it.flo; z <= it.fhi; ++z) {
+                const int sl = fc % NSF;
+                const int zl = z - 1;
+                const bool xy = z != it.flo;
+                double *d = sf + sl * FS;
                 if (lane == 0) {
-                    while (pnext <= min(q + 1, it.phi)) {
-                        const int sl = pc & (NSP - 1);
-                        if (pc >= NSP) mbar_wait(&emptyp[sl], ((pc / NSP) - 1) & 1);
-                        mbar_expect_tx(&fullp[sl], PBYTES);
-                        tma_load_4d(sp + sl * PS, &tmP, x0 - 2, y0 - 2, pnext, wk.j, &fullp[sl]);
-                        ++pc;
-                        ++pnext;
-                    }
-                    if (wk.front_pm && q >= it.mlo && q <= it.mhi) {
-                        const int sl = mc & (NSM - 1);
-                        if (mc >= NSM) mbar_wait(&emptym[sl], ((mc / NSM) - 1) & 1);
-                        mbar_expect_tx(&fullm[sl], MBYTES);
-                        tma_load_4d(sm + sl * MS, &tmM, x0 - 2, y0 - 1, q, wk.j - 1, &fullm[sl]);
-                        ++mc;
-                    }
+                    if (fc >= NSF) mbar_wait(&emptyf[sl], ((fc / NSF) - 1) & 1);
+                    if (!wkx) mbar_expect_tx(&fullf[sl], (xy ? KXBYTES + KYBYTES : 0u) + KZBYTES);
                 }
-                // face slot z holds kx(z), ky(z) (flo < z <= fhi) and kz(z), the upper face of plane z
-                // (flo <= z <= fhi; kz index 0 is the bottom boundary face)
-                while (fnext <= min(q + 1, it.fhi)) {
-                    const int sl = fc % NSF;
-                    const int z = fnext, zl = z - 1;
-                    const bool xy = z != it.flo;
-                    double *d = sf + sl * FS;
-                    if (lane == 0) {
-                        if (fc >= NSF) mbar_wait(&emptyf[sl], ((fc / NSF) - 1) & 1);
-                        mbar_expect_tx(&fullf[sl], (xy ? KXBYTES + KYBYTES : 0u) + KZBYTES);
-                    }
-                    __syncwarp();
-                    if (xy && lane < TY + 2) {   // kx row (zl, y0-1+lane) from the even element at or below x0-2
-                        const int64_t e0 = ((int64_t)zl * g.ny + (y0 - 1 + lane)) * (g.nx + 1) + x0 - 2 + wk.kx_shift;
-                        tma_load_1d(d + FKX + lane * KXP, &fm.kx, (int)(e0 & ~(int64_t)1), &fullf[sl]);
-                    }
-                    if (lane == 0) {
-                        if (xy) tma_load_3d(d + FKY, &fm.ky, x0 - 2, y0 - 1, zl, &fullf[sl]);
-                        tma_load_3d(d + FKZ, &fm.kz, x0 - 2, y0 - 1, z, &fullf[sl]);
-                    }
-                    __syncwarp();
-                    ++fc;
-                    ++fnext;
+                __syncwarp();
+                if (wkx && xy && lane < TY + 2) {   // kx row (zl, y0-1+lane) from the even element at or below x0-2
+                    const int64_t e0 = ((int64_t)zl * g.ny + (y0 - 1 + lane)) * (g.nx + 1) + x0 - 2 + wk.kx_shift;
+                    tma_load_1d(d + FKX + lane * KXP, &fm.kx, (int)(e0 & ~(int64_t)1), &fullf[sl]);
                 }
+                if (!wkx && lane == 0) {
+                    if (xy) tma_load_3d(d + FKY, &fm.ky, x0 - 2, y0 - 1, zl, &fullf[sl]);
+                    tma_load_3d(d + FKZ, &fm.kz, x0 - 2, y0 - 1, z, &fullf[sl]);
+                }
+                __syncwarp();
+                ++fc;
             }
         }
         return;
@@ -270,8 +285,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     int rk, ck;
     bool task;
-    if (warp <= NROW) {
-        rk = warp;
+    if (warp - (NPW - 1) <= NROW) {   // consumer warps NPW .. NPW+NCW-1
+        rk = warp - (NPW - 1);
         ck = 2 + 2 * lane;
         task = true;
     } else {
